@@ -1,0 +1,187 @@
+"""Unpartitioned reference execution (oracle side).  TEST INFRASTRUCTURE ONLY.
+
+* ``tdl_eval`` evaluates a TDL lambda literally ("the output
+  tensor value at each index" is the lambda body; a reducer "aggregate[s]
+  elements ... along one or more dimensions") over an iteration
+  box, vectorised with numpy broadcasting, in fp64.
+* ``fast_eval`` is the same for the matmul defs via a library matmul
+  (allowed as a single step); pinned equal to ``tdl_eval``.
+* ``run_graph`` executes a training graph op by op in list order and, when
+  ``emulate_storage`` is set, rounds every stored tensor to its storage dtype
+  (bf16 by round-to-nearest-even from fp64, fp32 by cast) — the points where
+  the GPU path stores.  Reading §R5 in DESIGN.md.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .tdl import Affine
+
+
+def round_bf16(x):
+    """Round fp64 values to the nearest bf16 (8 significant bits), ties to
+    even.  Normal range only (finite, |x| < 3.4e38)."""
+    x = np.asarray(x, dtype=np.float64)
+    m, e = np.frexp(x)                   # x = m * 2**e, 0.5 <= |m| < 1
+    r = np.rint(m * 256.0)               # 8 significant bits, half-to-even
+    return np.ldexp(r, e - 8)
+
+
+def store_round(x, dtype):
+    if dtype == "bf16":
+        return round_bf16(x)
+    if dtype == "f32":
+        return np.asarray(x, dtype=np.float32).astype(np.float64)
+    return np.asarray(x, dtype=np.float64)
+
+
+def _grid(vars_, box):
+    n = len(vars_)
+    out = {}
+    for i, v in enumerate(vars_):
+        lo, hi = box[v]
+        shape = [1] * n
+        shape[i] = hi - lo + 1
+        out[v] = np.arange(lo, hi + 1).reshape(shape)
+    return out
+
+
+def _idx(aff: Affine, grid):
+    acc = aff.const
+    for v, c in aff.coef:
+        acc = acc + c * grid[v]
+    return acc
+
+
+def _ev(e, grid, inputs, shape):
+    k = e.kind
+    if k == "num":
+        return np.float64(e.val)
+    if k == "var":
+        return grid[e.val].astype(np.float64)
+    if k == "access":
+        arr, origin = inputs[e.val.tensor]
+        idx = []
+        for d, ix in enumerate(e.val.index):
+            idx.append(np.broadcast_to(_idx(ix, grid) - origin[d], shape))
+        return arr[tuple(idx)]
+    if k == "neg":
+        return -_ev(e.args[0], grid, inputs, shape)
+    if k == "bin":
+        a = _ev(e.args[0], grid, inputs, shape)
+        b = _ev(e.args[1], grid, inputs, shape)
+        op = e.val
+        if op == "+":
+            return a + b
+        if op == "-":
+            return a - b
+        if op == "*":
+            return a * b
+        if op == "/":
+            return a / b
+        if op == ">":
+            return (a > b).astype(np.float64)
+        if op == "<":
+            return (a < b).astype(np.float64)
+        if op == ">=":
+            return (a >= b).astype(np.float64)
+        if op == "<=":
+            return (a <= b).astype(np.float64)
+        if op == "==":
+            return (a == b).astype(np.float64)
+    if k == "call":
+        a = [_ev(x, grid, inputs, shape) for x in e.args]
+        f = e.val
+        if f == "max":
+            return np.maximum(a[0], a[1])
+        if f == "min":
+            return np.minimum(a[0], a[1])
+        if f == "exp":
+            return np.exp(a[0])
+        if f == "tanh":
+            return np.tanh(a[0])
+        if f == "sigmoid":
+            return 1.0 / (1.0 + np.exp(-a[0]))
+        if f == "sqrt":
+            return np.sqrt(a[0])
+        if f == "select":
+            return np.where(np.broadcast_to(a[0], shape) != 0, a[1], a[2])
+    raise ValueError(f"cannot evaluate {k}")
+
+
+def tdl_eval(opdef, inputs: dict, box: dict):
+    """inputs: param -> (array, origin) where origin is the global index of
+    array[0,...,0].  box: var -> (lo, hi) closed, for all out and reduce vars.
+    Returns the output over the out-var box (a partial if the reduce box is
+    not the full range)."""
+    if opdef.opaque:
+        raise ValueError("opaque functions are not executable (P:L411-423)")
+    vars_ = list(opdef.out_vars) + list(opdef.red_vars)
+    grid = _grid(vars_, box)
+    shape = tuple(box[v][1] - box[v][0] + 1 for v in vars_)
+    val = np.broadcast_to(_ev(opdef.body, grid, inputs, shape), shape).astype(np.float64)
+    nout = len(opdef.out_vars)
+    if opdef.reducer:
+        axes = tuple(range(nout, len(vars_)))
+        r = opdef.reducer
+        if r == "Sum":
+            val = val.sum(axis=axes)
+        elif r == "Max":
+            val = val.max(axis=axes)
+        elif r == "Min":
+            val = val.min(axis=axes)
+        elif r == "Prod":
+            val = val.prod(axis=axes)
+    return np.asarray(val, dtype=np.float64)
+
+
+_MM = {
+    # def name -> (A index fn, B index fn) as (rows-var-of-A...) realised with numpy
+    "mm_nn": lambda A, B: A @ B,
+    "mm_nt": lambda A, B: A @ B.T,
+    "mm_tn": lambda A, B: A.T @ B,
+}
+
+
+def fast_eval(opdef, inputs: dict, box: dict):
+    """Library-matmul evaluation for the three matmul defs over a box; falls
+    back to tdl_eval otherwise."""
+    name = opdef.name
+    if name in _MM and len(opdef.out_vars) == 2 and len(opdef.red_vars) == 1:
+        i, j = opdef.out_vars
+        k = opdef.red_vars[0]
+        (A, oa), (B, ob) = inputs[opdef.params[0][0]], inputs[opdef.params[1][0]]
+        (i0, i1), (j0, j1), (k0, k1) = box[i], box[j], box[k]
+        if name == "mm_nn":
+            a = A[i0 - oa[0]:i1 - oa[0] + 1, k0 - oa[1]:k1 - oa[1] + 1]
+            b = B[k0 - ob[0]:k1 - ob[0] + 1, j0 - ob[1]:j1 - ob[1] + 1]
+        elif name == "mm_nt":
+            a = A[i0 - oa[0]:i1 - oa[0] + 1, k0 - oa[1]:k1 - oa[1] + 1]
+            b = B[j0 - ob[0]:j1 - ob[0] + 1, k0 - ob[1]:k1 - ob[1] + 1]
+        else:
+            a = A[k0 - oa[0]:k1 - oa[0] + 1, i0 - oa[1]:i1 - oa[1] + 1]
+            b = B[k0 - ob[0]:k1 - ob[0] + 1, j0 - ob[1]:j1 - ob[1] + 1]
+        return _MM[name](np.asarray(a, np.float64), np.asarray(b, np.float64))
+    return tdl_eval(opdef, inputs, box)
+
+
+def full_box(g, op):
+    R = g.ranges[op["name"]]
+    return {v: (0, n - 1) for v, n in R.items()}
+
+
+def run_graph(g, values: dict, emulate_storage=True, fast=True):
+    """Execute every op of g in order on full tensors.  values: initial
+    tensors (inputs / weights / state) as fp64 arrays.  Returns dict of all
+    tensors (fp64 arrays holding storage-rounded values when emulating)."""
+    env = {t: np.asarray(v, dtype=np.float64) for t, v in values.items()}
+    for op in g.ops:
+        d = g.opdef(op)
+        ins = {p: (env[t], (0,) * env[t].ndim) for (p, _), t in zip(d.params, op["inputs"])}
+        box = full_box(g, op)
+        out = (fast_eval if fast else tdl_eval)(d, ins, box)
+        out = np.asarray(out, dtype=np.float64).reshape(g.shape(op["output"]))
+        if emulate_storage:
+            out = store_round(out, g.tensors[op["output"]]["dtype"])
+        env[op["output"]] = out
+    return env

@@ -1,0 +1,45 @@
+"""Seeded synthetic tensors for a graph's inputs, weights and state.
+
+Every value drawn here is exactly representable in bf16 (a signed 8-bit
+integer times a power of two), so both sides start from bit-identical
+operands without any rounding code.  Recipes:
+
+  input  X : q * 2^-7                    q ~ U{-128..128}
+  input  T : q * 2^-8
+  weight W : q * 2^-7 * 2^-round(log2(sqrt(fan_in)))   (He-like scale)
+  state  M : q * 2^-17                    (non-zero so momentum is exercised)
+  mode="int": all of the above replaced by q ~ U{-3..3} (exact fp64 sums,
+              used for partitioned-vs-unpartitioned equality tests)
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+def _q(rng, shape, lo=-128, hi=128):
+    return rng.integers(lo, hi + 1, size=shape).astype(np.float64)
+
+
+def make_values(graph: dict, seed: int = 0, mode: str = "float") -> dict:
+    rng = np.random.default_rng(seed)
+    out = {}
+    for name in sorted(graph["tensors"]):
+        t = graph["tensors"][name]
+        role = t["role"]
+        shape = tuple(t["shape"])
+        if role not in ("input", "weight", "state") or name in graph.get("alias", {}):
+            continue
+        if mode == "int":
+            out[name] = _q(rng, shape, -3, 3)
+            continue
+        if role == "input":
+            out[name] = _q(rng, shape) * (2.0 ** -7 if name != "T" else 2.0 ** -8)
+        elif role == "weight":
+            fan_in = shape[0]
+            s = round(math.log2(math.sqrt(fan_in)))
+            out[name] = _q(rng, shape) * 2.0 ** (-7 - s)
+        else:
+            out[name] = _q(rng, shape) * 2.0 ** -17
+    return out
