@@ -1,0 +1,208 @@
+"""Thin ctypes binding of libtofu (include/tofu.h).  Argument marshalling only:
+every step of the hot path runs in libtofu's kernels / host code.  Raises
+loudly when the library is missing — there is no fallback path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libtofu.so")
+
+TOFU_BF16, TOFU_F32 = 0, 1
+EW = {"relu": 0, "relu_grad": 1, "mse_grad": 2, "mom": 3, "sgd": 4, "sgd_mom": 5, "sumsq": 6}
+MAX_SRC = 8
+
+
+class TofuError(RuntimeError):
+    pass
+
+
+class GemmArgs(C.Structure):
+    _fields_ = [("M", C.c_int), ("N", C.c_int), ("K", C.c_int),
+                ("A", C.c_void_p), ("lda", C.c_int), ("a_mn_major", C.c_int),
+                ("B", C.c_void_p), ("ldb", C.c_int), ("b_mn_major", C.c_int),
+                ("C", C.c_void_p), ("ldc", C.c_int), ("c_mode", C.c_int),
+                ("bn", C.c_int), ("max_ctas", C.c_int)]
+
+
+class Piece(C.Structure):
+    _fields_ = [("extent", C.c_int64 * 4), ("dst", C.c_void_p), ("dst_stride", C.c_int64 * 4),
+                ("dst_dtype", C.c_int), ("nsrc", C.c_int), ("src", C.c_void_p * MAX_SRC),
+                ("src_stride", C.c_int64 * 4), ("src_dtype", C.c_int), ("pad_", C.c_int)]
+
+
+class PlanOptions(C.Structure):
+    _fields_ = [("frontier_cap", C.c_int), ("solution_cap", C.c_int), ("search", C.c_int)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise TofuError(f"libtofu.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        L.tofu_last_error.restype = C.c_char_p
+        L.tofu_version.restype = C.c_char_p
+        vp, i64p = C.c_void_p, C.POINTER(C.c_int64)
+        sig = {
+            "tofu_gemm_bf16": [C.POINTER(GemmArgs), vp],
+            "tofu_gemm_plan_tmaps": [C.POINTER(GemmArgs), vp, vp, C.POINTER(C.c_int)],
+            "tofu_gemm_launch_planned": [C.POINTER(GemmArgs), vp, vp, C.c_int, vp],
+            "tofu_pieces_run": [vp, C.c_int, C.c_int64, vp],
+            "tofu_elementwise": [C.c_int, C.c_int64, vp, vp, vp, vp, C.c_float, C.c_float, vp],
+            "tofu_describe_op": [C.c_char_p, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
+            "tofu_graph_create": [C.c_char_p, C.POINTER(vp)],
+            "tofu_graph_destroy": [vp],
+            "tofu_plan_create": [vp, C.c_int, C.POINTER(PlanOptions), C.POINTER(vp)],
+            "tofu_plan_destroy": [vp],
+            "tofu_plan_json": [vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
+            "tofu_plan_cost": [vp, i64p, i64p],
+            "tofu_exec_arena_bytes": [vp, vp, C.c_int, i64p],
+            "tofu_exec_shard": [vp, vp, C.c_int, C.c_char_p, i64p, i64p, C.POINTER(C.c_int)],
+            "tofu_exec_create": [vp, vp, C.c_int, C.POINTER(C.c_int), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)],
+            "tofu_exec_destroy": [vp],
+            "tofu_execute": [vp, vp],
+            "tofu_exec_ledger": [vp, i64p, i64p],
+            "tofu_exec_launch_count": [vp, i64p],
+            "tofu_exec_set_skip_comm": [vp, C.c_int],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name, None)
+            if f is None:
+                continue
+            f.argtypes = args
+            f.restype = None if name.endswith("_destroy") else C.c_int
+        _lib = L
+    return _lib
+
+
+def check(rc, what=""):
+    if rc != 0:
+        raise TofuError(f"{what} failed ({rc}): {lib().tofu_last_error().decode()}")
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+# ----------------------------------------------------------------------------- kernels
+def gemm(A, B, Cout, M, N, K, lda, a_mn, ldb, b_mn, ldc, c_mode, bn=0, max_ctas=0, stream=None):
+    a = GemmArgs(M, N, K, A.data_ptr(), lda, a_mn, B.data_ptr(), ldb, b_mn, Cout.data_ptr(), ldc, c_mode, bn, max_ctas)
+    check(lib().tofu_gemm_bf16(C.byref(a), _stream(stream)), "tofu_gemm_bf16")
+
+
+def elementwise(kind, n, y=None, x0=None, x1=None, x2=None, s0=0.0, s1=0.0, stream=None):
+    p = lambda t: None if t is None else C.c_void_p(t.data_ptr())
+    check(lib().tofu_elementwise(EW[kind] if isinstance(kind, str) else kind, n, p(y), p(x0), p(x1), p(x2),
+                                 s0, s1, _stream(stream)), "tofu_elementwise")
+
+
+def pieces_run(pieces_dev_ptr, n, max_elems, stream=None):
+    check(lib().tofu_pieces_run(C.c_void_p(pieces_dev_ptr), n, max_elems, _stream(stream)), "tofu_pieces_run")
+
+
+# ----------------------------------------------------------------------------- host API
+def describe_op(tdl: str, ways: int = 2) -> dict:
+    n = C.c_size_t(0)
+    check(lib().tofu_describe_op(tdl.encode(), ways, None, 0, C.byref(n)), "tofu_describe_op")
+    buf = C.create_string_buffer(n.value + 1)
+    check(lib().tofu_describe_op(tdl.encode(), ways, buf, n.value + 1, C.byref(n)), "tofu_describe_op")
+    return json.loads(buf.value.decode())
+
+
+class Graph:
+    def __init__(self, spec: dict):
+        self.spec = spec
+        h = C.c_void_p()
+        check(lib().tofu_graph_create(json.dumps(spec).encode(), C.byref(h)), "tofu_graph_create")
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.tofu_graph_destroy(self.h)
+            self.h = None
+
+
+class Plan:
+    def __init__(self, graph: Graph, k: int, frontier_cap=64, solution_cap=256, search=0):
+        self.graph = graph
+        self.k = k
+        h = C.c_void_p()
+        opts = PlanOptions(frontier_cap, solution_cap, search)
+        check(lib().tofu_plan_create(graph.h, k, C.byref(opts), C.byref(h)), "tofu_plan_create")
+        self.h = h
+
+    def json(self) -> dict:
+        n = C.c_size_t(0)
+        check(lib().tofu_plan_json(self.h, None, 0, C.byref(n)), "tofu_plan_json")
+        buf = C.create_string_buffer(n.value + 1)
+        check(lib().tofu_plan_json(self.h, buf, n.value + 1, C.byref(n)), "tofu_plan_json")
+        return json.loads(buf.value.decode())
+
+    def cost(self):
+        e, b = C.c_int64(), C.c_int64()
+        check(lib().tofu_plan_cost(self.h, C.byref(e), C.byref(b)), "tofu_plan_cost")
+        return e.value, b.value
+
+    def arena_bytes(self, rank: int) -> int:
+        n = C.c_int64()
+        check(lib().tofu_exec_arena_bytes(self.graph.h, self.h, rank, C.byref(n)), "tofu_exec_arena_bytes")
+        return n.value
+
+    def shard(self, rank: int, tensor: str):
+        off = C.c_int64()
+        box = (C.c_int64 * 8)()
+        r = C.c_int()
+        check(lib().tofu_exec_shard(self.graph.h, self.h, rank, tensor.encode(), C.byref(off), box, C.byref(r)),
+              "tofu_exec_shard")
+        return off.value, [(box[2 * d], box[2 * d + 1]) for d in range(r.value)]
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.tofu_plan_destroy(self.h)
+            self.h = None
+
+
+class Exec:
+    """Executor over local ranks.  arenas: list of k device pointers (ints)."""
+
+    def __init__(self, graph: Graph, plan: Plan, local_ranks, arenas, flags=None):
+        self.graph, self.plan = graph, plan
+        n = len(local_ranks)
+        lr = (C.c_int * n)(*local_ranks)
+        ar = (C.c_void_p * len(arenas))(*arenas)
+        fl = (C.c_void_p * len(arenas))(*(flags or [0] * len(arenas)))
+        h = C.c_void_p()
+        check(lib().tofu_exec_create(graph.h, plan.h, n, lr, ar, fl if flags else None, C.byref(h)),
+              "tofu_exec_create")
+        self.h = h
+
+    def run(self, stream=None):
+        check(lib().tofu_execute(self.h, _stream(stream)), "tofu_execute")
+
+    def ledger(self):
+        e, b = C.c_int64(), C.c_int64()
+        check(lib().tofu_exec_ledger(self.h, C.byref(e), C.byref(b)), "tofu_exec_ledger")
+        return e.value, b.value
+
+    def launches(self):
+        n = C.c_int64()
+        check(lib().tofu_exec_launch_count(self.h, C.byref(n)), "tofu_exec_launch_count")
+        return n.value
+
+    def skip_comm(self, on: bool):
+        check(lib().tofu_exec_set_skip_comm(self.h, 1 if on else 0), "tofu_exec_set_skip_comm")
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.tofu_exec_destroy(self.h)
+            self.h = None

@@ -1,0 +1,131 @@
+"""GPU parity: kernels of libtofu vs the oracle (fp64) on the same seeded
+bf16-exact inputs.  Tolerances (north star): normwise relative error <= 5e-3
+for bf16 outputs, <= 1e-5 for fp32 outputs."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.exec_ref import fast_eval, round_bf16  # noqa: E402
+from oracle.tdl import parse_def  # noqa: E402
+from tofu_inputs.graphs import MM_DEFS  # noqa: E402
+
+
+def _tofu():
+    from paper_1807_08887_b200 import tofu
+    tofu.lib()
+    return tofu
+
+
+def nrm(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def q(rng, shape, scale):
+    return rng.integers(-128, 129, size=shape).astype(np.float64) * scale
+
+
+def cuda_bf16(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16).cuda()
+
+
+DEF_MAJOR = {"mm_nn": (0, 1), "mm_nt": (0, 0), "mm_tn": (1, 1)}
+
+
+@pytest.mark.parametrize("defname", ["mm_nn", "mm_nt", "mm_tn"])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (200, 300, 104), (64, 520, 1000), (512, 1024, 2048),
+                                   (1, 8, 8), (384, 128, 4096)])
+@pytest.mark.parametrize("c_mode", [0, 1, 2])
+def test_gemm_parity(defname, M, N, K, c_mode):
+    t = _tofu()
+    am, bm = DEF_MAJOR[defname]
+    if (am and M % 8) or (bm and N % 8) or (not am and K % 8) or (not bm and K % 8):
+        pytest.skip("pitch must be a multiple of 8 elements")
+    rng = np.random.default_rng(M * 7 + N * 13 + K)
+    a_shape = (K, M) if am else (M, K)
+    b_shape = (K, N) if bm else (N, K)
+    A = q(rng, a_shape, 2 ** -7)
+    B = q(rng, b_shape, 2 ** -9)
+    d = parse_def(MM_DEFS[defname])
+    ref = fast_eval(d, {"A": (A, (0, 0)), "B": (B, (0, 0))},
+                    {"i": (0, M - 1), "j": (0, N - 1), "k": (0, K - 1)})
+    Ad, Bd = cuda_bf16(A), cuda_bf16(B)
+    if c_mode == 0:
+        Cd = torch.full((M, N), 7.0, dtype=torch.bfloat16, device="cuda")
+    else:
+        C0 = q(rng, (M, N), 2 ** -5) if c_mode == 2 else np.zeros((M, N))
+        Cd = torch.from_numpy(C0).float().cuda()
+        if c_mode == 2:
+            ref = ref + C0
+    t.gemm(Ad, Bd, Cd, M, N, K, lda=a_shape[1], a_mn=am, ldb=b_shape[1], b_mn=bm, ldc=N, c_mode=c_mode)
+    torch.cuda.synchronize()
+    got = Cd.double().cpu().numpy()
+    if c_mode == 0:
+        assert nrm(got, ref) <= 5e-3
+        # most elements equal the correctly rounded fp64 result
+        assert np.mean(got == round_bf16(ref)) > 0.97
+    else:
+        assert nrm(got, ref) <= 1e-5
+
+
+def test_gemm_strided_output_and_bn():
+    t = _tofu()
+    rng = np.random.default_rng(9)
+    M, N, K = 256, 512, 256
+    A, B = q(rng, (M, K), 2 ** -7), q(rng, (K, N), 2 ** -7)
+    for bn in (128, 256):
+        Cd = torch.zeros((M, N + 64), dtype=torch.float32, device="cuda")
+        t.gemm(cuda_bf16(A), cuda_bf16(B), Cd, M, N, K, K, 0, N, 1, N + 64, 1, bn=bn, max_ctas=3)
+        torch.cuda.synchronize()
+        got = Cd.double().cpu().numpy()
+        assert nrm(got[:, :N], A @ B) <= 1e-5
+        assert np.all(got[:, N:] == 0)
+
+
+@pytest.mark.parametrize("kind", ["relu", "relu_grad", "mse_grad", "mom", "sgd", "sgd_mom", "sumsq"])
+@pytest.mark.parametrize("n", [8, 1000, 1 << 20, 3 * 1024 + 5])
+def test_elementwise(kind, n):
+    t = _tofu()
+    rng = np.random.default_rng(n)
+    a = q(rng, n, 2 ** -7)
+    b = q(rng, n, 2 ** -7)
+    s0, s1 = 0.875, 0.0078125
+    if kind in ("relu", "relu_grad", "mse_grad", "sumsq"):
+        x0, x1 = cuda_bf16(a), cuda_bf16(b)
+        y = torch.zeros(n, dtype=torch.float32 if kind == "sumsq" else torch.bfloat16, device="cuda")
+        if kind == "sumsq":
+            y = torch.zeros(4, dtype=torch.float32, device="cuda")
+        t.elementwise(kind, n, y, x0, x1 if kind != "relu" else None, None, s0, s1)
+        torch.cuda.synchronize()
+        got = y.double().cpu().numpy()
+        if kind == "relu":
+            ref = round_bf16(np.maximum(a, 0))
+        elif kind == "relu_grad":
+            ref = round_bf16(np.where(a > 0, b, 0))
+        elif kind == "mse_grad":
+            ref = round_bf16((a - b) * s0)
+        else:
+            assert abs(got[0] - np.sum((a - b) ** 2) * s0) <= 1e-5 * np.sum((a - b) ** 2) * s0
+            return
+        assert np.array_equal(got, ref)
+    elif kind == "mom":
+        x0 = torch.from_numpy(a).float().cuda(); x1 = torch.from_numpy(b).float().cuda()
+        y = torch.empty(n, dtype=torch.float32, device="cuda")
+        t.elementwise(kind, n, y, x0, x1, None, s0, s1)
+        torch.cuda.synchronize()
+        assert nrm(y.double().cpu().numpy(), a * s0 + b) <= 1e-6
+    elif kind == "sgd":
+        x0 = cuda_bf16(a); x1 = torch.from_numpy(b).float().cuda()
+        y = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+        t.elementwise(kind, n, y, x0, x1, None, s0, s1)
+        torch.cuda.synchronize()
+        assert nrm(y.double().cpu().numpy(), round_bf16(a - b * s0)) <= 5e-3
+    else:
+        m = torch.from_numpy(a * 2 ** -6).float().cuda(); g = torch.from_numpy(b).float().cuda()
+        w = cuda_bf16(q(rng, n, 2 ** -7)); w0 = w.double().cpu().numpy()
+        t.elementwise(kind, n, None, m, g, w, s0, s1)
+        torch.cuda.synchronize()
+        mref = a * 2 ** -6 * s0 + b
+        assert nrm(m.double().cpu().numpy(), mref) <= 1e-6
+        assert nrm(w.double().cpu().numpy(), round_bf16(w0 - mref * s1)) <= 5e-3
