@@ -1,0 +1,314 @@
+"""Benchmark: Tofu-partitioned training step on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1] [--impl reference]
+
+One JSON line on rank 0.  N = 1 runs the workload unpartitioned on one GPU; N > 1 (torchrun, one
+process per GPU) partitions every tensor k = N ways with tofu_plan and runs the partitioned step
+through tofu_execute (MultiFetch / partition-n-reduce kernels reading peer HBM over NVLink).
+The global batch is fixed as N grows (strong scaling, as in the paper: one model split over GPUs).
+``--impl reference`` times the oracle (the CPU reference implementation) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from tofu_inputs.graphs import CONFIG_NAME, config  # noqa: E402
+from tofu_inputs.tensors import make_values  # noqa: E402
+
+METRIC = "samples/sec per training step"
+CLOCK_Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+           "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+           "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={CLOCK_Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) > 8:
+                for n, v in zip(names, r[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "src": "fallback"}
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+def oracle_step_time(spec, vals):
+    from oracle.exec_ref import run_graph
+    from oracle.graph import Graph
+    g = Graph(spec)
+    t = time.perf_counter()
+    run_graph(g, vals, emulate_storage=True)
+    return time.perf_counter() - t
+
+
+def reference_arm(args, world, rank):
+    """--impl reference: the oracle (fp64 CPU) on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    from tofu_inputs.graphs import mlp
+    full = config(args.config)
+    batch = full["tensors"]["X"]["shape"][0]
+    dims = [full["tensors"]["X"]["shape"][1], full["tensors"]["Y"]["shape"][1]]
+    sb = 32 if batch > 32 else batch
+    spec = mlp(sb, dims)   # bounded sample: same layer shapes, batch 32 per step
+    vals = make_values(spec, seed=0)
+    for _ in range(args.warmup):
+        oracle_step_time(spec, vals)
+    ts = [oracle_step_time(spec, vals) for _ in range(args.steps)]
+    t = sum(ts) / len(ts)
+    v = sb / t
+    sample = f"{CONFIG_NAME[args.config]} layer shapes at batch {sb} per step (full batch {batch}); fp64 numpy"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CONFIG_NAME[args.config], "global_batch": sb, "parallelism": "cpu"},
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cpu_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--impl", default="tofu", choices=["tofu", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        return reference_arm(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1807_08887_b200.runner import TofuRunner
+
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        group = dist.group.WORLD
+
+    spec = config(args.config)
+    k = world
+    vals = make_values(spec, seed=0)
+    if world > 1:
+        R = TofuRunner(spec, k, rank=rank, group=group)
+    else:
+        R = TofuRunner(spec, 1)
+    R.load(vals)
+    ex = R.exec
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # --- instrumented pass: per-launch device time (events between launches) -> dominant kernel
+    nl = ex.num_launches()
+    descs = [ex.launch_desc(i) for i in range(nl)]
+    for _ in range(2):
+        ex.run()
+    per = [0.0] * nl
+    reps = 3
+    for _ in range(reps):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(nl + 1)]
+        evs[0].record()
+        for i in range(nl):
+            ex.run_range(i, i + 1)
+            evs[i + 1].record()
+        torch.cuda.synchronize()
+        for i in range(nl):
+            per[i] += evs[i].elapsed_time(evs[i + 1]) / reps
+    cand = [i for i in range(nl) if descs[i]["kind"] in ("compute", "fetch", "reduce")]
+    dom = max(cand, key=lambda i: per[i])
+
+    # --- warmup + timed region (inputs > L2: W 128 MiB + M 256 MiB + dW 256 MiB per step)
+    for _ in range(args.warmup):
+        ex.run()
+    torch.cuda.synchronize()
+    dom_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for s in range(args.steps):
+            ex.time_launch(dom, *dom_ev[s])
+            ex.run()
+        t1.record()
+        torch.cuda.synchronize()
+        barrier()
+    ex.time_launch(-1)
+    ms = t0.elapsed_time(t1) / args.steps
+    dom_ms = sum(a.elapsed_time(b) for a, b in dom_ev) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+
+    batch = spec["tensors"]["X"]["shape"][0]
+    value = batch / (ms / 1e3)
+
+    # --- end to end through the public API: H2D inputs (pinned) + step + D2H loss every step
+    xs = {t: torch.from_numpy(np.asarray(vals[t], np.float32)).to(torch.bfloat16).pin_memory() for t in ("X", "T")}
+    h2d = 0
+    for t in ("X", "T"):
+        for r in R.local:
+            v = R.view(r, t)
+            if v is not None:
+                h2d += v.numel() * v.element_size()
+    loss_owner = R.view(R.local[0], "loss")
+    loss_host = torch.empty((), dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        R.load(xs); ex.run()
+    torch.cuda.synchronize()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        R.load(xs)
+        ex.run()
+        if loss_owner is not None:
+            loss_host.copy_(loss_owner, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        tt = torch.tensor([e2e_ms, h2d], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt[:1], op=dist.ReduceOp.MAX)
+        hh = tt[1:].clone()
+        dist.all_reduce(hh, op=dist.ReduceOp.SUM)
+        e2e_ms, h2d = float(tt[0]), int(hh[0])
+
+    pk = peaks()
+    d = descs[dom]
+    if d["flops"] > 0:
+        roof = {"bound": "tensor", "achieved": d["flops"] / (dom_ms / 1e3) / 1e12, "peak": pk["bf16_tflops_sustained"],
+                "unit": "TFLOP/s"}
+    else:
+        roof = {"bound": "hbm", "achieved": d["bytes"] / (dom_ms / 1e3) / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["kernel"] = f"{d['kind']}:{d['op']}({d['def']})"
+    roof["peak_src"] = pk["src"] + (" sustained bf16" if roof["bound"] == "tensor" else " hbm copy")
+    roof["kernel_ms"] = dom_ms
+    roof["traffic"] = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            pt = json.load(open(prof))
+            key = f"{CONFIG_NAME[args.config]}|k{k}|{d['op']}"
+            if key in pt:
+                roof["traffic"] = pt[key]
+        except Exception:
+            pass
+
+    ledger_el, ledger_b = R.ledger()
+    plan_el, plan_b = R.plan.cost()
+    # step roofline (north star): slower of compute at tensor peak and plan bytes at NVLink per GPU
+    flops_rank = sum(x["flops"] for x in descs if x["kind"] == "compute")
+    t_comp = flops_rank / (pk["bf16_tflops_sustained"] * 1e12)
+    t_comm = (plan_b / max(k, 1)) / 770e9 if k > 1 else 0.0
+    step_roof = max(t_comp, t_comm)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, bf16-exact values)",
+        "config": {"workload": CONFIG_NAME[args.config], "global_batch": batch, "parallelism": f"tofu-k{k}",
+                   "plan_factors": R.plan_json["factors"], "l2": "inputs larger than L2 (W+M+dW 640 MiB)"},
+        "roofline": roof,
+        "step_roofline": {"compute_ms": t_comp * 1e3, "comm_ms": t_comm * 1e3, "frac": step_roof / (ms / 1e3)},
+        "bytes_vs_plan": {"plan_bytes": plan_b, "ledger_bytes": ledger_b, "plan_elements": plan_el,
+                          "ledger_elements": ledger_el, "equal": plan_b == ledger_b},
+        "e2e": {"value": batch / (e2e_ms / 1e3), "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": 4},
+        "gpu_launches": ex.launches() * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        t = oracle_step_time(spec, vals)
+        line["cpu_baseline"] = {"value": batch / t, "unit": "samples/s", "cores": cpu_threads(), "kind": "oracle",
+                                "sample": f"1 full training step of {CONFIG_NAME[args.config]} (batch {batch}), fp64"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -110,6 +110,16 @@ int tofu_exec_ledger(const tofu_exec* e, int64_t* elements, int64_t* bytes);
 int tofu_exec_launch_count(const tofu_exec* e, int64_t* launches);
 /* 1 = skip fetch/reduce kernels (compute-only time), 0 = normal. */
 int tofu_exec_set_skip_comm(tofu_exec* e, int skip);
+/* Launch list introspection (kernels, barriers and memsets of one step, in issue order). */
+int tofu_exec_num_launches(const tofu_exec* e, int* n);
+/* JSON {"index","kind":"fetch"|"compute"|"reduce"|"barrier"|"memset","op","def","rank","flops",
+ *       "bytes"}: flops = 2·M·N·K for GEMM sub-ops; bytes = algorithmic bytes read + written. */
+int tofu_exec_launch_desc(const tofu_exec* e, int index, char* out, size_t cap, size_t* len);
+/* Issue launches [first, last) only (instrumented timing). */
+int tofu_execute_range(tofu_exec* e, int first, int last, void* stream);
+/* Record cudaEvent_t ev_start / ev_stop (on the execute stream) around launch `index` during every
+ * subsequent tofu_execute; index < 0 disables. */
+int tofu_exec_time_launch(tofu_exec* e, int index, void* ev_start, void* ev_stop);
 
 /* ======================================================================================= kernels
  * Device entry points used by tofu_execute, exported for parity tests.

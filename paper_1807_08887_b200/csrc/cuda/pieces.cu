@@ -103,3 +103,31 @@ extern "C" int tofu_pieces_run(const tofu_piece* pieces_dev, int n, int64_t max_
       pieces_dev);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }
+
+// Cross-process device barrier over NVLink (multi-process mode only).  Each rank bumps its own epoch
+// word (system-scope release) and waits until every peer's word reaches the same epoch (system-scope
+// acquire on the peer mapping).  flags: device array of n pointers (peer-mapped epoch words).
+namespace tofu {
+__global__ void barrier_kernel(unsigned long long* const* flags, int rank, int n) {
+  __shared__ unsigned long long epoch;
+  if (threadIdx.x == 0) {
+    unsigned long long old;
+    asm volatile("atom.add.release.sys.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(flags[rank]) : "memory");
+    epoch = old + 1;
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags[p]) : "memory");
+    } while (v < epoch);
+  }
+  __syncthreads();
+}
+}  // namespace tofu
+
+extern "C" int tofu_barrier_run(void* flags_ptrs_dev, int rank, int n, void* stream) {
+  tofu::barrier_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<unsigned long long* const*>(flags_ptrs_dev), rank, n);
+  return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
+}

@@ -1,0 +1,740 @@
+// Lowering of a plan to per-rank programs and their execution (a3, a8).
+//
+// "For each operator in the original graph, Tofu generates a copy for each GPU worker in the partitioned
+// graph" (§6).  Per (op, rank) the lowering computes the sub-op's iteration box, the required
+// region of every input (MultiFetch pieces from each owner into a staging buffer unless the region is
+// already local), and the produced output box: written straight into the owner's shard when
+// it is exactly the rank's own shard, otherwise staged and pulled by the owners (fp32 partials summed in
+// rank order when a reduction variable is split — partition-n-reduce P:L255-256, spread over all GPUs
+// P:L879-881).  The ledger counts every element moved between distinct ranks; it equals the plan cost.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <set>
+
+#include "common.h"
+#include "graph.h"
+#include "json.h"
+#include "plan.h"
+
+extern "C" int tofu_barrier_run(void* flags_ptrs_dev, int rank, int n, void* stream);
+
+namespace tofu {
+
+namespace {
+
+constexpr int64_t kAlign = 256;
+int64_t align_up(int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+int64_t vol(const std::vector<Rng>& b) {
+  int64_t p = 1;
+  for (auto& r : b) p *= r.len();
+  return p;
+}
+bool inter(const std::vector<Rng>& a, const std::vector<Rng>& b, std::vector<Rng>& out) {
+  out.resize(a.size());
+  for (size_t i = 0; i < a.size(); ++i) {
+    out[i] = {std::max(a[i].lo, b[i].lo), std::min(a[i].hi, b[i].hi)};
+    if (out[i].len() <= 0) return false;
+  }
+  return true;
+}
+bool same(const std::vector<Rng>& a, const std::vector<Rng>& b) {
+  for (size_t i = 0; i < a.size(); ++i)
+    if (a[i].lo != b[i].lo || a[i].hi != b[i].hi) return false;
+  return true;
+}
+bool contains(const std::vector<Rng>& outer, const std::vector<Rng>& in) {
+  for (size_t i = 0; i < outer.size(); ++i)
+    if (in[i].lo < outer[i].lo || in[i].hi > outer[i].hi) return false;
+  return true;
+}
+// row-major strides (elements) of a dense box
+std::vector<int64_t> strides_of(const std::vector<Rng>& box) {
+  std::vector<int64_t> s(box.size());
+  int64_t acc = 1;
+  for (int i = (int)box.size() - 1; i >= 0; --i) {
+    s[i] = acc;
+    acc *= box[i].len();
+  }
+  return s;
+}
+int64_t offset_in(const std::vector<Rng>& buf, const std::vector<Rng>& at) {
+  auto s = strides_of(buf);
+  int64_t o = 0;
+  for (size_t i = 0; i < buf.size(); ++i) o += (at[i].lo - buf[i].lo) * s[i];
+  return o;
+}
+
+struct Layout {  // one rank's arena
+  std::vector<int64_t> shard_off;             // per tensor (bytes), -1 = not owned
+  std::vector<std::vector<Rng>> shard_box;    // per tensor
+  int64_t staging_off = 0, staging_bytes = 0, total = 0;
+};
+
+struct Buf {  // an operand buffer of one (op, rank)
+  bool direct = false;
+  int64_t off = 0;            // bytes into the rank's arena
+  std::vector<Rng> buf_box;   // the box the buffer holds (dense row-major)
+  std::vector<Rng> box;       // the box the op uses (subset of buf_box)
+  int dtype = TOFU_F32;
+};
+
+struct LOp {
+  std::vector<Buf> in;
+  Buf out;
+  bool partial = false;
+  bool skip = false;          // fused into the previous op
+  bool fused_sgd = false;
+  std::vector<tofu_piece> fetch, reduce;
+  std::vector<int> fetch_src, reduce_nremote;  // for the ledger
+};
+
+Layout layout_rank(const Graph& g, const PlanSeq& p, int rank, std::vector<std::vector<LOp>>* lops_all = nullptr) {
+  Layout L;
+  const int nt = (int)g.tensors.size();
+  auto dig = worker_digits(rank, p.factors);
+  L.shard_off.assign(nt, -1);
+  L.shard_box.assign(nt, {});
+  std::map<int, int> alias_old;
+  for (auto& pr : g.alias) alias_old[pr.first] = pr.second;
+  int64_t off = 0;
+  for (int t = 0; t < nt; ++t) {
+    std::vector<Rng> box;
+    bool own = owned_box(g, t, p.tdims[t], p.factors, dig, box);
+    L.shard_box[t] = box;
+    if (!own) continue;
+    if (alias_old.count(t)) continue;  // stored in the old tensor's shard
+    L.shard_off[t] = off;
+    off = align_up(off + vol(box) * g.itemsize(t));
+  }
+  for (auto& kv : alias_old) {
+    // chains resolve to the root storage
+    int root = kv.second;
+    while (alias_old.count(root)) root = alias_old[root];
+    L.shard_off[kv.first] = L.shard_off[root];
+  }
+  L.staging_off = off;
+  return L;
+}
+
+}  // namespace
+
+struct Exec {
+  const Graph* g = nullptr;
+  Graph gcopy;
+  PlanSeq plan;
+  int k = 1;
+  std::vector<int> local;           // local ranks
+  std::vector<char*> arena;         // all k ranks (as addressable here)
+  std::vector<void*> flags;         // all k ranks' epoch words (multi-process) or empty
+  void* flags_dev = nullptr;        // device array of flag pointers
+  std::vector<Layout> lay;          // all ranks
+  std::vector<std::vector<LOp>> lops;  // [local index][op]
+  struct Launch {
+    int kind;  // 0 fetch pieces, 1 compute, 2 reduce pieces, 3 barrier, 4 memset
+    int op, li;
+    int64_t piece_off, npieces, max_elems;
+  };
+  std::vector<Launch> launches;
+  tofu_piece* pieces_dev = nullptr;
+  std::vector<tofu_piece> host_pieces;
+  bool finalized = false;
+  struct GemmLaunch {
+    tofu_gemm_args a;
+    alignas(64) CUtensorMap ta, tb;
+    int bn;
+  };
+  std::map<std::pair<int, int>, GemmLaunch> gemms;  // (op, li)
+  int64_t ledger_el = 0, ledger_bytes = 0;
+  int64_t n_kernels = 0;
+  bool skip_comm = false;
+  bool multi_process = false;
+  int timed_launch = -1;
+  cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+};
+
+namespace {
+
+const char* kernel_kind(const std::string& def) {
+  if (def == "mm_nn" || def == "matmul" || def == "mm_nt" || def == "mm_tn") return "gemm";
+  if (def == "relu" || def == "relu_grad" || def == "mse_grad" || def == "mom" || def == "sgd" || def == "sumsq")
+    return "ew";
+  return nullptr;
+}
+
+void lower(Exec& E) {
+  const Graph& g = *E.g;
+  const PlanSeq& p = E.plan;
+  const int k = E.k;
+  E.lay.resize(k);
+  // staging sizes per rank: computed while lowering each rank
+  std::vector<std::vector<LOp>> all(k, std::vector<LOp>(g.ops.size()));
+  for (int r = 0; r < k; ++r) E.lay[r] = layout_rank(g, p, r);
+  std::vector<int64_t> stage_need(k, 0);
+  for (int r = 0; r < k; ++r) {
+    auto dig = worker_digits(r, p.factors);
+    for (size_t o = 0; o < g.ops.size(); ++o) {
+      const OpDef& d = g.def_of((int)o);
+      const OpInfo& oi = g.ops[o];
+      if (!kernel_kind(g.defs[oi.def].name))
+        throw Error(TOFU_ERR_ARG, "no sub-operator kernel for def '" + g.defs[oi.def].name + "'");
+      LOp& L = all[r][o];
+      std::vector<Rng> ib;
+      iter_box(g, (int)o, p.osplit[o], p.factors, dig, ib);
+      for (int v : p.osplit[o])
+        if (d.is_red(v)) L.partial = true;
+      const bool is_ew = std::string(kernel_kind(d.name)) == "ew";
+      int64_t soff = 0;
+      for (size_t pi = 0; pi < d.params.size(); ++pi) {
+        int t = oi.inputs[pi];
+        Buf b;
+        b.box = required_box(g, (int)o, (int)pi, ib);
+        b.dtype = g.tensors[t].dtype;
+        const auto& own = E.lay[r].shard_box[t];
+        const bool owns = E.lay[r].shard_off[t] >= 0;
+        if (owns && (is_ew ? same(own, b.box) : contains(own, b.box))) {
+          b.direct = true;
+          b.off = E.lay[r].shard_off[t];
+          b.buf_box = own;
+        } else {
+          b.direct = false;
+          b.off = soff;  // relative to staging, fixed up below
+          b.buf_box = b.box;
+          soff = align_up(soff + vol(b.box) * g.itemsize(t));
+        }
+        L.in.push_back(b);
+      }
+      Buf ob;
+      ob.box.assign(ib.begin(), ib.begin() + d.n_out);
+      const int t = oi.output;
+      const bool owns = E.lay[r].shard_off[t] >= 0;
+      if (!L.partial && owns && same(E.lay[r].shard_box[t], ob.box)) {
+        ob.direct = true;
+        ob.off = E.lay[r].shard_off[t];
+        ob.buf_box = ob.box;
+        ob.dtype = g.tensors[t].dtype;
+      } else {
+        ob.direct = false;
+        ob.dtype = L.partial ? TOFU_F32 : g.tensors[t].dtype;
+        ob.off = soff;
+        ob.buf_box = ob.box;
+        soff = align_up(soff + vol(ob.box) * (ob.dtype == TOFU_BF16 ? 2 : 4));
+      }
+      L.out = ob;
+      stage_need[r] = std::max(stage_need[r], soff);
+    }
+  }
+  for (int r = 0; r < k; ++r) {
+    E.lay[r].staging_bytes = stage_need[r];
+    E.lay[r].total = E.lay[r].staging_off + stage_need[r];
+    for (auto& L : all[r]) {
+      for (auto& b : L.in)
+        if (!b.direct) b.off += E.lay[r].staging_off;
+      if (!L.out.direct) L.out.off += E.lay[r].staging_off;
+    }
+  }
+  // ------------------------------------------------------------------ pieces
+  auto ptr = [&](int r, int64_t off) -> char* { return E.arena.empty() ? nullptr : E.arena[r] + off; };
+  auto fill_geom = [](tofu_piece& pc, const std::vector<Rng>& ext_box) {
+    const int n = (int)ext_box.size();
+    for (int d = 0; d < 4; ++d) pc.extent[d] = 1;
+    for (int d = 0; d < n; ++d) pc.extent[4 - n + d] = ext_box[d].len();
+  };
+  auto set_strides = [](int64_t* dst, const std::vector<Rng>& buf) {
+    auto s = strides_of(buf);
+    const int n = (int)buf.size();
+    for (int d = 0; d < 4; ++d) dst[d] = 0;
+    for (int d = 0; d < n; ++d) dst[4 - n + d] = s[d];
+  };
+  E.ledger_el = E.ledger_bytes = 0;
+  for (int r = 0; r < k; ++r)
+    for (size_t o = 0; o < g.ops.size(); ++o) {
+      LOp& L = all[r][o];
+      const OpInfo& oi = g.ops[o];
+      for (size_t pi = 0; pi < L.in.size(); ++pi) {
+        Buf& b = L.in[pi];
+        if (b.direct) continue;
+        const int t = oi.inputs[pi];
+        for (int s = 0; s < k; ++s) {
+          if (E.lay[s].shard_off[t] < 0) continue;
+          std::vector<Rng> x;
+          const auto& own = E.lay[s].shard_box[t];
+          if (!b.box.empty() && !inter(b.box, own, x)) continue;
+          tofu_piece pc;
+          std::memset(&pc, 0, sizeof pc);
+          fill_geom(pc, b.box.empty() ? b.box : x);
+          pc.dst = ptr(r, b.off) ? ptr(r, b.off) + offset_in(b.buf_box, x) * g.itemsize(t) : nullptr;
+          set_strides(pc.dst_stride, b.buf_box);
+          pc.dst_dtype = pc.src_dtype = g.tensors[t].dtype;
+          pc.nsrc = 1;
+          pc.src[0] = ptr(s, E.lay[s].shard_off[t]) ? ptr(s, E.lay[s].shard_off[t]) + offset_in(own, x) * g.itemsize(t)
+                                                    : nullptr;
+          set_strides(pc.src_stride, own);
+          L.fetch.push_back(pc);
+          L.fetch_src.push_back(s);
+          if (s != r) {
+            E.ledger_el += vol(x);
+            E.ledger_bytes += vol(x) * g.itemsize(t);
+          }
+        }
+      }
+    }
+  // reduce / scatter: owner r pulls from every non-direct producer c
+  for (size_t o = 0; o < g.ops.size(); ++o) {
+    const int t = g.ops[o].output;
+    for (int r = 0; r < k; ++r) {
+      if (E.lay[r].shard_off[t] < 0) continue;
+      const auto& own = E.lay[r].shard_box[t];
+      std::vector<int> contrib;
+      for (int c = 0; c < k; ++c) {
+        const Buf& ob = all[c][o].out;
+        if (ob.direct) continue;
+        std::vector<Rng> x;
+        if (!ob.box.empty() && !inter(ob.box, own, x)) continue;
+        contrib.push_back(c);
+      }
+      if (contrib.empty()) continue;
+      // grid of breakpoints within own
+      const int n = (int)own.size();
+      std::vector<std::vector<int64_t>> cuts(n);
+      for (int d = 0; d < n; ++d) {
+        std::set<int64_t> cs = {own[d].lo, own[d].hi + 1};
+        for (int c : contrib) {
+          const auto& b = all[c][o].out.box;
+          if (b[d].lo > own[d].lo && b[d].lo <= own[d].hi) cs.insert(b[d].lo);
+          if (b[d].hi + 1 > own[d].lo && b[d].hi + 1 <= own[d].hi) cs.insert(b[d].hi + 1);
+        }
+        cuts[d].assign(cs.begin(), cs.end());
+      }
+      std::vector<int> ci(n, 0);
+      while (true) {
+        std::vector<Rng> cell(n);
+        for (int d = 0; d < n; ++d) cell[d] = {cuts[d][ci[d]], cuts[d][ci[d] + 1] - 1};
+        std::vector<int> srcs;
+        for (int c : contrib)
+          if (n == 0 || contains(all[c][o].out.box, cell)) srcs.push_back(c);
+        if (!srcs.empty()) {
+          if ((int)srcs.size() > TOFU_MAX_SRC) throw Error(TOFU_ERR_ARG, "more than 8 contributors to one element");
+          tofu_piece pc;
+          std::memset(&pc, 0, sizeof pc);
+          fill_geom(pc, cell);
+          const int64_t es = g.itemsize(t);
+          pc.dst = ptr(r, E.lay[r].shard_off[t]) ? ptr(r, E.lay[r].shard_off[t]) + offset_in(own, cell) * es : nullptr;
+          set_strides(pc.dst_stride, own);
+          pc.dst_dtype = g.tensors[t].dtype;
+          pc.nsrc = (int)srcs.size();
+          const Buf& ob0 = all[srcs[0]][o].out;
+          pc.src_dtype = ob0.dtype;
+          set_strides(pc.src_stride, ob0.buf_box);
+          int nrem = 0;
+          for (size_t s = 0; s < srcs.size(); ++s) {
+            const Buf& ob = all[srcs[s]][o].out;
+            const int64_t ses = ob.dtype == TOFU_BF16 ? 2 : 4;
+            pc.src[s] = ptr(srcs[s], ob.off) ? ptr(srcs[s], ob.off) + offset_in(ob.buf_box, cell) * ses : nullptr;
+            if (srcs[s] != r) {
+              ++nrem;
+              E.ledger_el += vol(cell);
+              E.ledger_bytes += vol(cell) * ses;
+            }
+          }
+          all[r][o].reduce.push_back(pc);
+          all[r][o].reduce_nremote.push_back(nrem);
+        }
+        int d = n - 1;
+        while (d >= 0 && ++ci[d] + 1 >= (int)cuts[d].size()) ci[d--] = 0;
+        if (d < 0) break;
+      }
+    }
+  }
+  // fused momentum + SGD (consecutive element-wise optimizer ops share one partition)
+  for (int r = 0; r < k; ++r)
+    for (size_t o = 0; o + 1 < g.ops.size(); ++o) {
+      const OpInfo &a = g.ops[o], &b = g.ops[o + 1];
+      if (g.defs[a.def].name != "mom" || g.defs[b.def].name != "sgd" || b.inputs[1] != a.output) continue;
+      LOp &La = all[r][o], &Lb = all[r][o + 1];
+      bool ok = La.out.direct && Lb.out.direct && La.fetch.empty() && Lb.fetch.empty();
+      for (auto& x : La.in) ok &= x.direct;
+      for (auto& x : Lb.in) ok &= x.direct;
+      ok &= La.in[0].off == La.out.off && Lb.in[0].off == Lb.out.off;  // in place (aliased state)
+      if (ok) {
+        La.fused_sgd = true;
+        Lb.skip = true;
+      }
+    }
+  E.lops.clear();
+  for (int r : E.local) E.lops.push_back(all[r]);
+}
+
+void build_launches(Exec& E) {
+  const Graph& g = *E.g;
+  std::vector<tofu_piece> host;
+  E.launches.clear();
+  const int nl = (int)E.local.size();
+  // multi-process: a device barrier before every phase that reads peer memory (its producers on other
+  // ranks must be done), and one at the end of the step (WAR on shards read by peers).
+  auto need_barrier = [&](int, bool) { return E.multi_process; };
+  for (size_t o = 0; o < g.ops.size(); ++o) {
+    // fetch phase
+    bool any_fetch = false;
+    for (int li = 0; li < nl; ++li) any_fetch |= !E.lops[li][o].fetch.empty();
+    if (any_fetch) {
+      if (need_barrier((int)o, true)) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
+      Exec::Launch L{0, (int)o, -1, (int64_t)host.size(), 0, 0};
+      for (int li = 0; li < nl; ++li)
+        for (auto& pc : E.lops[li][o].fetch) {
+          host.push_back(pc);
+          L.max_elems = std::max(L.max_elems, pc.extent[0] * pc.extent[1] * pc.extent[2] * pc.extent[3]);
+        }
+      L.npieces = (int64_t)host.size() - L.piece_off;
+      E.launches.push_back(L);
+    }
+    for (int li = 0; li < nl; ++li) {
+      if (E.lops[li][o].skip) continue;
+      if (g.defs[g.ops[o].def].name == "sumsq") E.launches.push_back({4, (int)o, li, 0, 0, 0});
+      E.launches.push_back({1, (int)o, li, 0, 0, 0});
+    }
+    bool any_red = false;
+    for (int li = 0; li < nl; ++li) any_red |= !E.lops[li][o].reduce.empty();
+    if (any_red) {
+      if (need_barrier((int)o, false)) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
+      Exec::Launch L{2, (int)o, -1, (int64_t)host.size(), 0, 0};
+      for (int li = 0; li < nl; ++li)
+        for (auto& pc : E.lops[li][o].reduce) {
+          host.push_back(pc);
+          L.max_elems = std::max(L.max_elems, pc.extent[0] * pc.extent[1] * pc.extent[2] * pc.extent[3]);
+        }
+      L.npieces = (int64_t)host.size() - L.piece_off;
+      E.launches.push_back(L);
+    }
+  }
+  if (E.multi_process) E.launches.push_back({3, -1, -1, 0, 0, 0});
+  E.host_pieces = std::move(host);
+  int64_t n = 0;
+  for (auto& L : E.launches)
+    if (L.kind != 4) ++n;
+  E.n_kernels = n;
+}
+
+void finalize(Exec& E) {
+  if (E.finalized) return;
+  const Graph& g = *E.g;
+  if (E.multi_process && !E.flags_dev) {
+    if (cudaMalloc(&E.flags_dev, sizeof(void*) * E.k) != cudaSuccess) throw Error(TOFU_ERR_CUDA, "cudaMalloc flags");
+    cudaMemcpy(E.flags_dev, E.flags.data(), sizeof(void*) * E.k, cudaMemcpyHostToDevice);
+  }
+  const auto& host = E.host_pieces;
+  const int nl = (int)E.local.size();
+  if (!host.empty()) {
+    if (cudaMalloc(&E.pieces_dev, host.size() * sizeof(tofu_piece)) != cudaSuccess)
+      throw Error(TOFU_ERR_CUDA, "cudaMalloc pieces");
+    if (cudaMemcpy(E.pieces_dev, host.data(), host.size() * sizeof(tofu_piece), cudaMemcpyHostToDevice) != cudaSuccess)
+      throw Error(TOFU_ERR_CUDA, "cudaMemcpy pieces");
+  }
+  // GEMM descriptors
+  for (int li = 0; li < nl; ++li) {
+    const int r = E.local[li];
+    for (size_t o = 0; o < g.ops.size(); ++o) {
+      const std::string& dn = g.defs[g.ops[o].def].name;
+      if (std::string(kernel_kind(dn)) != "gemm") continue;
+      LOp& L = E.lops[li][o];
+      const OpDef& d = g.def_of((int)o);
+      // vars: i, j (out), k (red) for all three defs
+      const int64_t M = L.out.box[0].len(), N = L.out.box[1].len();
+      const Buf &A = L.in[0], &B = L.in[1];
+      const int64_t K = (dn == "mm_tn") ? A.box[0].len() : A.box[1].len();
+      Exec::GemmLaunch G;
+      std::memset(&G.a, 0, sizeof G.a);
+      G.a.M = (int)M;
+      G.a.N = (int)N;
+      G.a.K = (int)K;
+      const int64_t ea = 2;
+      G.a.A = E.arena[r] + A.off + offset_in(A.buf_box, A.box) * ea;
+      G.a.lda = (int)A.buf_box[1].len();
+      G.a.a_mn_major = dn == "mm_tn" ? 1 : 0;
+      G.a.B = E.arena[r] + B.off + offset_in(B.buf_box, B.box) * ea;
+      G.a.ldb = (int)B.buf_box[1].len();
+      G.a.b_mn_major = (dn == "mm_nt") ? 0 : 1;
+      const int64_t ec = L.out.dtype == TOFU_BF16 ? 2 : 4;
+      G.a.C = E.arena[r] + L.out.off + offset_in(L.out.buf_box, L.out.box) * ec;
+      G.a.ldc = (int)L.out.buf_box[1].len();
+      G.a.c_mode = L.out.dtype == TOFU_BF16 ? 0 : 1;
+      (void)d;
+      int rc = tofu_gemm_plan_tmaps(&G.a, &G.ta, &G.tb, &G.bn);
+      if (rc) throw Error(rc, "gemm tensor map for op " + g.ops[o].name + " (pitch/alignment)");
+      E.gemms[{(int)o, li}] = G;
+    }
+  }
+  E.finalized = true;
+}
+
+bool lo_fused(const Exec& E, const Exec::Launch& L) { return E.lops[L.li][L.op].fused_sgd; }
+
+int run_compute(Exec& E, int o, int li, cudaStream_t st) {
+  const Graph& g = *E.g;
+  const int r = E.local[li];
+  LOp& L = E.lops[li][o];
+  const OpInfo& oi = g.ops[o];
+  const std::string& dn = g.defs[oi.def].name;
+  char* base = E.arena[r];
+  if (std::string(kernel_kind(dn)) == "gemm") {
+    auto& G = E.gemms.at({o, li});
+    return tofu_gemm_launch_planned(&G.a, &G.ta, &G.tb, G.bn, st);
+  }
+  const int64_t n = vol(L.out.box);
+  void* y = base + L.out.off;
+  const void* x0 = L.in.size() > 0 ? base + L.in[0].off : nullptr;
+  const void* x1 = L.in.size() > 1 ? base + L.in[1].off : nullptr;
+  auto attr = [&](const char* key, double dflt) {
+    auto it = oi.attrs.find(key);
+    return (float)(it == oi.attrs.end() ? dflt : it->second);
+  };
+  if (dn == "relu") return tofu_elementwise(TOFU_EW_RELU, n, y, x0, nullptr, nullptr, 0, 0, st);
+  if (dn == "relu_grad") return tofu_elementwise(TOFU_EW_RELU_GRAD, n, y, x0, x1, nullptr, 0, 0, st);
+  if (dn == "mse_grad") return tofu_elementwise(TOFU_EW_MSE_GRAD, n, y, x0, x1, nullptr, attr("scale", 1), 0, st);
+  if (dn == "sumsq") {
+    const int64_t m = vol(L.in[0].box);
+    return tofu_elementwise(TOFU_EW_SUMSQ, m, y, x0, x1, nullptr, attr("scale", 1), 0, st);
+  }
+  if (dn == "mom") {
+    if (L.fused_sgd) {
+      const OpInfo& nx = g.ops[o + 1];
+      LOp& Ln = E.lops[li][o + 1];
+      auto it = nx.attrs.find("lr");
+      const float lr = (float)(it == nx.attrs.end() ? 0.0 : it->second);
+      return tofu_elementwise(TOFU_EW_SGD_MOM, n, nullptr, base + L.in[0].off, x1, base + Ln.in[0].off, attr("mu", 0),
+                              lr, st);
+    }
+    return tofu_elementwise(TOFU_EW_MOM, n, y, x0, x1, nullptr, attr("mu", 0), 0, st);
+  }
+  if (dn == "sgd") return tofu_elementwise(TOFU_EW_SGD, n, y, x0, x1, nullptr, attr("lr", 0), 0, st);
+  return TOFU_ERR_ARG;
+}
+
+}  // namespace
+}  // namespace tofu
+
+struct tofu_exec {
+  tofu::Exec e;
+};
+
+extern "C" int tofu_exec_arena_bytes(const tofu_graph* g, const tofu_plan* p, int rank, int64_t* bytes) {
+  return tofu::guard([&]() {
+    if (!g || !p || !bytes) throw tofu::Error(TOFU_ERR_ARG, "null argument");
+    tofu::Exec E;
+    E.g = &tofu::graph_of(g);
+    E.plan = tofu::plan_of(p).seq;
+    E.k = tofu::plan_of(p).k;
+    if (rank < 0 || rank >= E.k) throw tofu::Error(TOFU_ERR_ARG, "rank out of range");
+    E.local = {rank};
+    tofu::lower(E);
+    *bytes = E.lay[rank].total;
+    return TOFU_OK;
+  });
+}
+
+extern "C" int tofu_exec_shard(const tofu_graph* g, const tofu_plan* p, int rank, const char* tensor, int64_t* offset,
+                               int64_t* box, int* rank_out) {
+  return tofu::guard([&]() {
+    const tofu::Graph& G = tofu::graph_of(g);
+    auto it = G.tensor_ix.find(tensor ? tensor : "");
+    if (it == G.tensor_ix.end()) throw tofu::Error(TOFU_ERR_ARG, "unknown tensor");
+    const auto& plan = tofu::plan_of(p);
+    if (rank < 0 || rank >= plan.k) throw tofu::Error(TOFU_ERR_ARG, "rank out of range");
+    tofu::Layout L = tofu::layout_rank(G, plan.seq, rank);
+    const int t = it->second;
+    *offset = L.shard_off[t];
+    *rank_out = (int)G.tensors[t].shape.size();
+    for (size_t d = 0; d < L.shard_box[t].size() && d < 4; ++d) {
+      box[2 * d] = L.shard_box[t][d].lo;
+      box[2 * d + 1] = L.shard_box[t][d].hi;
+    }
+    return TOFU_OK;
+  });
+}
+
+extern "C" int tofu_exec_create(const tofu_graph* g, const tofu_plan* p, int n_local, const int* local_ranks,
+                                void* const* arena_dev, void* const* flags_dev, tofu_exec** out) {
+  return tofu::guard([&]() {
+    if (!g || !p || !out || n_local < 1 || !local_ranks || !arena_dev) throw tofu::Error(TOFU_ERR_ARG, "null argument");
+    auto* h = new tofu_exec;
+    tofu::Exec& E = h->e;
+    try {
+      E.gcopy = tofu::graph_of(g);
+      E.g = &E.gcopy;
+      E.plan = tofu::plan_of(p).seq;
+      E.k = tofu::plan_of(p).k;
+      for (int i = 0; i < n_local; ++i) {
+        if (local_ranks[i] < 0 || local_ranks[i] >= E.k) throw tofu::Error(TOFU_ERR_ARG, "rank out of range");
+        E.local.push_back(local_ranks[i]);
+      }
+      for (int r = 0; r < E.k; ++r) {
+        if (!arena_dev[r] || (reinterpret_cast<uintptr_t>(arena_dev[r]) & 255))
+          throw tofu::Error(TOFU_ERR_ALIGN, "arena pointers must be non-null and 256-byte aligned");
+        E.arena.push_back(static_cast<char*>(arena_dev[r]));
+      }
+      E.multi_process = n_local < E.k;
+      if (E.multi_process) {
+        if (!flags_dev) throw tofu::Error(TOFU_ERR_ARG, "flags_dev required when not all ranks are local");
+        for (int r = 0; r < E.k; ++r) E.flags.push_back(flags_dev[r]);
+      }
+      tofu::lower(E);
+      tofu::build_launches(E);
+    } catch (...) {
+      if (E.pieces_dev) cudaFree(E.pieces_dev);
+      if (E.flags_dev) cudaFree(E.flags_dev);
+      delete h;
+      throw;
+    }
+    *out = h;
+    return TOFU_OK;
+  });
+}
+
+extern "C" void tofu_exec_destroy(tofu_exec* h) {
+  if (!h) return;
+  if (h->e.pieces_dev) cudaFree(h->e.pieces_dev);
+  if (h->e.flags_dev) cudaFree(h->e.flags_dev);
+  delete h;
+}
+
+namespace tofu {
+namespace {
+int run_launch(Exec& E, const Exec::Launch& L, cudaStream_t st) {
+  int rc = TOFU_OK;
+  switch (L.kind) {
+    case 0:
+    case 2:
+      if (!E.skip_comm) rc = tofu_pieces_run(E.pieces_dev + L.piece_off, (int)L.npieces, L.max_elems, st);
+      break;
+    case 1:
+      rc = run_compute(E, L.op, L.li, st);
+      break;
+    case 3:
+      if (!E.skip_comm) rc = tofu_barrier_run(E.flags_dev, E.local[0], E.k, st);
+      break;
+    case 4: {
+      const auto& out = E.lops[L.li][L.op].out;
+      rc = cudaMemsetAsync(E.arena[E.local[L.li]] + out.off, 0, 4, st) == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
+      break;
+    }
+  }
+  if (rc)
+    throw Error(rc, "launch failed at op " + (L.op >= 0 ? E.g->ops[L.op].name : std::string("end")) + ": " +
+                        cudaGetErrorString(cudaGetLastError()));
+  return rc;
+}
+
+void run_range(Exec& E, int first, int last, cudaStream_t st) {
+  finalize(E);
+  for (int i = first; i < last; ++i) {
+    const bool timed = i == E.timed_launch && E.ev_start;
+    if (timed) cudaEventRecord(E.ev_start, st);
+    run_launch(E, E.launches[i], st);
+    if (timed) cudaEventRecord(E.ev_stop, st);
+  }
+}
+
+std::string launch_desc(const Exec& E, int i) {
+  const Graph& g = *E.g;
+  const auto& L = E.launches[i];
+  static const char* kinds[] = {"fetch", "compute", "reduce", "barrier", "memset"};
+  std::string o = "{\"index\":" + std::to_string(i) + ",\"kind\":\"" + kinds[L.kind] + "\"";
+  o += ",\"op\":" + (L.op >= 0 ? json_quote(g.ops[L.op].name) : std::string("null"));
+  o += ",\"def\":" + (L.op >= 0 ? json_quote(g.defs[g.ops[L.op].def].name) : std::string("null"));
+  o += ",\"rank\":" + std::to_string(L.li >= 0 ? E.local[L.li] : -1);
+  double flops = 0, bytes = 0;
+  if (L.kind == 0 || L.kind == 2) {
+    for (int64_t p = L.piece_off; p < L.piece_off + L.npieces; ++p) {
+      const auto& pc = E.host_pieces[p];
+      const double n = (double)pc.extent[0] * pc.extent[1] * pc.extent[2] * pc.extent[3];
+      bytes += n * ((pc.src_dtype == TOFU_BF16 ? 2 : 4) * pc.nsrc + (pc.dst_dtype == TOFU_BF16 ? 2 : 4));
+    }
+  } else if (L.kind == 1) {
+    const LOp& lo = E.lops[L.li][L.op];
+    const std::string& dn = g.defs[g.ops[L.op].def].name;
+    if (std::string(kernel_kind(dn)) == "gemm") {
+      const double M = (double)lo.out.box[0].len(), N = (double)lo.out.box[1].len();
+      const double K = (double)(dn == "mm_tn" ? lo.in[0].box[0].len() : lo.in[0].box[1].len());
+      flops = 2 * M * N * K;
+      bytes = 2 * (M * K + K * N) + M * N * (lo.out.dtype == TOFU_BF16 ? 2 : 4);
+    } else {
+      const double n = (double)vol(lo.in[0].box);
+      for (size_t k = 0; k < lo.in.size(); ++k) bytes += n * (lo.in[k].dtype == TOFU_BF16 ? 2 : 4);
+      if (lo.fused_sgd) bytes += n * (4 + 2);  // m and w written back
+      else if (dn != "sumsq") bytes += n * (lo.out.dtype == TOFU_BF16 ? 2 : 4);
+      if (lo.fused_sgd) bytes += n * 2;       // w read
+    }
+  }
+  o += ",\"flops\":" + json_num(flops) + ",\"bytes\":" + json_num(bytes);
+  if (L.kind == 1 && lo_fused(E, L)) o += ",\"fused\":\"mom+sgd\"";
+  return o + "}";
+}
+}  // namespace
+}  // namespace tofu
+
+extern "C" int tofu_execute(tofu_exec* h, void* stream) {
+  return tofu::guard([&]() {
+    if (!h) throw tofu::Error(TOFU_ERR_ARG, "null exec");
+    tofu::run_range(h->e, 0, (int)h->e.launches.size(), reinterpret_cast<cudaStream_t>(stream));
+    return TOFU_OK;
+  });
+}
+
+extern "C" int tofu_execute_range(tofu_exec* h, int first, int last, void* stream) {
+  return tofu::guard([&]() {
+    if (!h || first < 0 || last > (int)h->e.launches.size() || first > last)
+      throw tofu::Error(TOFU_ERR_ARG, "bad launch range");
+    tofu::run_range(h->e, first, last, reinterpret_cast<cudaStream_t>(stream));
+    return TOFU_OK;
+  });
+}
+
+extern "C" int tofu_exec_num_launches(const tofu_exec* h, int* n) {
+  if (!h || !n) return tofu::fail(TOFU_ERR_ARG, "null argument");
+  *n = (int)h->e.launches.size();
+  return TOFU_OK;
+}
+
+extern "C" int tofu_exec_launch_desc(const tofu_exec* h, int index, char* out, size_t cap, size_t* len) {
+  return tofu::guard([&]() {
+    if (!h || index < 0 || index >= (int)h->e.launches.size()) throw tofu::Error(TOFU_ERR_ARG, "bad launch index");
+    return tofu::write_out(tofu::launch_desc(h->e, index), out, cap, len);
+  });
+}
+
+extern "C" int tofu_exec_time_launch(tofu_exec* h, int index, void* ev_start, void* ev_stop) {
+  if (!h) return tofu::fail(TOFU_ERR_ARG, "null exec");
+  h->e.timed_launch = index;
+  h->e.ev_start = reinterpret_cast<cudaEvent_t>(ev_start);
+  h->e.ev_stop = reinterpret_cast<cudaEvent_t>(ev_stop);
+  return TOFU_OK;
+}
+
+extern "C" int tofu_exec_ledger(const tofu_exec* h, int64_t* elements, int64_t* bytes) {
+  if (!h) return tofu::fail(TOFU_ERR_ARG, "null exec");
+  if (elements) *elements = h->e.skip_comm ? 0 : h->e.ledger_el;
+  if (bytes) *bytes = h->e.skip_comm ? 0 : h->e.ledger_bytes;
+  return TOFU_OK;
+}
+
+extern "C" int tofu_exec_launch_count(const tofu_exec* h, int64_t* launches) {
+  if (!h || !launches) return tofu::fail(TOFU_ERR_ARG, "null argument");
+  int64_t n = 0;
+  for (auto& L : h->e.launches) {
+    if (L.kind == 4) continue;
+    if (h->e.skip_comm && (L.kind == 0 || L.kind == 2 || L.kind == 3)) continue;
+    ++n;
+  }
+  *launches = n;
+  return TOFU_OK;
+}
+
+extern "C" int tofu_exec_set_skip_comm(tofu_exec* h, int skip) {
+  if (!h) return tofu::fail(TOFU_ERR_ARG, "null exec");
+  h->e.skip_comm = skip != 0;
+  return TOFU_OK;
+}

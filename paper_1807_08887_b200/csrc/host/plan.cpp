@@ -1,0 +1,480 @@
+// tofu_plan: recursive partitioning (§5.2) with the per-step DP over the coarsened graph
+// (P:L340-349).  One step = exact min-sum variable elimination over tensor-class and op-class
+// variables (on a chain this is the chain DP; the per-group brute force of P:L655-658 is the factor table
+// of each op class).  All co-optimal step plans are enumerated and carried forward as a frontier
+// (DESIGN.md §R4), k = k1·…·km with ki non-increasing primes.  search = 1 runs the same
+// elimination over sequence-valued variables (all steps jointly: exact, small graphs only).
+#include <algorithm>
+#include <chrono>
+#include <functional>
+#include <map>
+#include <numeric>
+#include <set>
+
+#include "common.h"
+#include "graph.h"
+#include "json.h"
+#include "plan.h"
+
+namespace tofu {
+namespace {
+
+std::vector<int> factorize(int k) {
+  std::vector<int> f;
+  for (int p = 2; (int64_t)p * p <= k; ++p)
+    while (k % p == 0) {
+      f.push_back(p);
+      k /= p;
+    }
+  if (k > 1) f.push_back(k);
+  std::sort(f.rbegin(), f.rend());
+  return f;
+}
+
+// ------------------------------------------------------------------------------ variable elimination
+struct Factor {
+  std::vector<int> scope;       // sorted var ids
+  std::vector<int64_t> table;   // row-major over scope domain sizes
+};
+
+struct VE {
+  std::vector<int> dsize;
+  std::vector<Factor> factors;
+  struct Trace {
+    int x;
+    std::vector<int> scope;
+    std::vector<int64_t> comb;
+  };
+  std::vector<Trace> trace;
+
+  static std::vector<int64_t> strides(const std::vector<int>& scope, const std::vector<int>& dsize) {
+    std::vector<int64_t> s(scope.size());
+    int64_t acc = 1;
+    for (int i = (int)scope.size() - 1; i >= 0; --i) {
+      s[i] = acc;
+      acc *= dsize[scope[i]];
+    }
+    return s;
+  }
+
+  int64_t run(int cap, std::vector<std::vector<int>>& sols) {
+    std::vector<Factor> active = factors;
+    std::set<int> remaining;
+    for (int v = 0; v < (int)dsize.size(); ++v) remaining.insert(v);
+    while (!remaining.empty()) {
+      int bx = -1;
+      double bw = 0;
+      for (int x : remaining) {
+        std::set<int> nb;
+        for (auto& f : active)
+          if (std::find(f.scope.begin(), f.scope.end(), x) != f.scope.end()) nb.insert(f.scope.begin(), f.scope.end());
+        double w = 1;
+        for (int y : nb) w *= dsize[y];
+        if (bx < 0 || w < bw) {
+          bx = x;
+          bw = w;
+        }
+      }
+      int x = bx;
+      std::vector<Factor> touching, rest;
+      for (auto& f : active)
+        (std::find(f.scope.begin(), f.scope.end(), x) != f.scope.end() ? touching : rest).push_back(f);
+      std::set<int> sc;
+      for (auto& f : touching) sc.insert(f.scope.begin(), f.scope.end());
+      sc.insert(x);
+      std::vector<int> scope(sc.begin(), sc.end());
+      auto st = strides(scope, dsize);
+      int64_t n = 1;
+      for (int y : scope) n *= dsize[y];
+      std::vector<int64_t> comb(n, 0);
+      std::vector<int> idx(scope.size());
+      for (auto& f : touching) {
+        auto fst = strides(f.scope, dsize);
+        std::vector<int> pos(f.scope.size());
+        for (size_t a = 0; a < f.scope.size(); ++a)
+          pos[a] = (int)(std::find(scope.begin(), scope.end(), f.scope[a]) - scope.begin());
+        for (int64_t e = 0; e < n; ++e) {
+          int64_t r = e, off = 0;
+          for (int a = (int)scope.size() - 1; a >= 0; --a) {
+            idx[a] = (int)(r % dsize[scope[a]]);
+            r /= dsize[scope[a]];
+          }
+          for (size_t a = 0; a < f.scope.size(); ++a) off += idx[pos[a]] * fst[a];
+          comb[e] += f.table[off];
+        }
+      }
+      // message: min over x
+      std::vector<int> mscope;
+      for (int y : scope)
+        if (y != x) mscope.push_back(y);
+      auto mst = strides(mscope, dsize);
+      int64_t mn = 1;
+      for (int y : mscope) mn *= dsize[y];
+      std::vector<int64_t> msg(mn, INT64_MAX);
+      int xpos = (int)(std::find(scope.begin(), scope.end(), x) - scope.begin());
+      for (int64_t e = 0; e < n; ++e) {
+        int64_t r = e, off = 0;
+        for (int a = (int)scope.size() - 1; a >= 0; --a) {
+          idx[a] = (int)(r % dsize[scope[a]]);
+          r /= dsize[scope[a]];
+        }
+        int b = 0;
+        for (int a = 0; a < (int)scope.size(); ++a)
+          if (a != xpos) off += idx[a] * mst[b++];
+        msg[off] = std::min(msg[off], comb[e]);
+      }
+      trace.push_back({x, scope, std::move(comb)});
+      rest.push_back({mscope, std::move(msg)});
+      active.swap(rest);
+      remaining.erase(x);
+    }
+    int64_t total = 0;
+    for (auto& f : active) total += f.table.at(0);
+    // enumerate co-optimal assignments (DFS in reverse elimination order)
+    std::vector<int> assign(dsize.size(), -1);
+    std::function<void(int)> dfs = [&](int i) {
+      if ((int)sols.size() >= cap) return;
+      if (i < 0) {
+        sols.push_back(assign);
+        return;
+      }
+      auto& tr = trace[i];
+      auto st = strides(tr.scope, dsize);
+      int64_t base = 0;
+      int64_t xs = 0;
+      for (size_t a = 0; a < tr.scope.size(); ++a) {
+        if (tr.scope[a] == tr.x) xs = st[a];
+        else base += assign[tr.scope[a]] * st[a];
+      }
+      int64_t m = INT64_MAX;
+      for (int v = 0; v < dsize[tr.x]; ++v) m = std::min(m, tr.comb[base + v * xs]);
+      for (int v = 0; v < dsize[tr.x]; ++v)
+        if (tr.comb[base + v * xs] == m) {
+          assign[tr.x] = v;
+          dfs(i - 1);
+          assign[tr.x] = -1;
+        }
+    };
+    dfs((int)trace.size() - 1);
+    return total;
+  }
+};
+
+int64_t extent_after(int64_t n, const std::vector<int>& seq, int axis, const std::vector<int>& factors) {
+  for (size_t i = 0; i < seq.size(); ++i)
+    if (seq[i] == axis) n /= factors[i];
+  return n;
+}
+
+std::vector<int> tensor_domain(const Graph& g, int cls, const PlanSeq& pre, int k) {
+  const auto& ms = g.classes[cls];
+  size_t rank = g.tensors[ms[0]].shape.size();
+  if (rank == 0) return {-1};
+  std::vector<int> dom;
+  for (size_t d = 0; d < rank; ++d) {
+    bool ok = true;
+    for (int t : ms)
+      if (extent_after(g.tensors[t].shape[d], pre.tdims[t], (int)d, pre.factors) % k) ok = false;
+    if (ok) dom.push_back((int)d);
+  }
+  return dom;
+}
+
+std::vector<int> op_domain(const Graph& g, int ocls, const PlanSeq& pre, int k) {
+  const auto& ms = g.op_classes[ocls];
+  std::vector<int> dom;
+  for (int v : g.def_of(ms[0]).split_vars()) {
+    bool ok = true;
+    for (int o : ms)
+      if (extent_after(g.ops[o].R[v], pre.osplit[o], v, pre.factors) % k) ok = false;
+    if (ok) dom.push_back(v);
+  }
+  return dom;
+}
+
+// canonical key (matches oracle.search.canon_key): per tensor class the dim sequence of its first member
+// (None = -1), then per op class the index of each step's var in split_vars().
+std::vector<int> canon_key(const Graph& g, const PlanSeq& p) {
+  std::vector<int> key;
+  for (auto& ms : g.classes)
+    for (int d : p.tdims[ms[0]]) key.push_back(d);
+  for (auto& ms : g.op_classes) {
+    auto sv = g.def_of(ms[0]).split_vars();
+    for (int v : p.osplit[ms[0]]) key.push_back((int)(std::find(sv.begin(), sv.end(), v) - sv.begin()));
+  }
+  return key;
+}
+
+struct StepResult {
+  int64_t cost;
+  std::vector<PlanSeq> plans;
+  bool truncated;
+};
+
+StepResult step_search(const Graph& g, const PlanSeq& pre, int k, int cap) {
+  const int nT = (int)g.classes.size(), nO = (int)g.op_classes.size();
+  std::vector<std::vector<int>> dom(nT + nO);
+  for (int c = 0; c < nT; ++c) {
+    dom[c] = tensor_domain(g, c, pre, k);
+    if (dom[c].empty()) throw Error(TOFU_ERR_PLAN, "no divisible dim for tensor class of " + g.tensors[g.classes[c][0]].name);
+  }
+  for (int c = 0; c < nO; ++c) {
+    dom[nT + c] = op_domain(g, c, pre, k);
+    if (dom[nT + c].empty()) throw Error(TOFU_ERR_PLAN, "no divisible var for op " + g.ops[g.op_classes[c][0]].name);
+  }
+  VE ve;
+  for (auto& d : dom) ve.dsize.push_back((int)d.size());
+  PlanSeq cur = pre;
+  cur.factors.push_back(k);
+  for (auto& s : cur.tdims) s.push_back(-1);
+  for (auto& s : cur.osplit) s.push_back(-1);
+  for (int oc = 0; oc < nO; ++oc) {
+    std::set<int> tcs;
+    for (int o : g.op_classes[oc]) {
+      for (int t : g.ops[o].inputs) tcs.insert(g.tclass[t]);
+      tcs.insert(g.tclass[g.ops[o].output]);
+    }
+    Factor f;
+    f.scope.assign(tcs.begin(), tcs.end());
+    f.scope.push_back(nT + oc);
+    int64_t n = 1;
+    for (int x : f.scope) n *= ve.dsize[x];
+    f.table.assign(n, 0);
+    std::vector<int> idx(f.scope.size());
+    for (int64_t e = 0; e < n; ++e) {
+      int64_t r = e;
+      for (int a = (int)f.scope.size() - 1; a >= 0; --a) {
+        idx[a] = (int)(r % ve.dsize[f.scope[a]]);
+        r /= ve.dsize[f.scope[a]];
+      }
+      const int v = dom[nT + oc][idx.back()];
+      int64_t val = 0;
+      for (int o : g.op_classes[oc]) {
+        for (size_t a = 0; a + 1 < f.scope.size(); ++a) {
+          const int d = dom[f.scope[a]][idx[a]];
+          for (int t : g.classes[f.scope[a]]) cur.tdims[t].back() = d;
+        }
+        cur.osplit[o].back() = v;
+        val += op_cost(g, o, cur).elements;
+      }
+      f.table[e] = val;
+    }
+    ve.factors.push_back(std::move(f));
+  }
+  std::vector<std::vector<int>> sols;
+  StepResult res;
+  res.cost = ve.run(cap, sols);
+  res.truncated = (int)sols.size() >= cap;
+  for (auto& s : sols) {
+    PlanSeq p = cur;
+    for (size_t t = 0; t < g.tensors.size(); ++t) p.tdims[t].back() = dom[g.tclass[t]][s[g.tclass[t]]];
+    for (size_t o = 0; o < g.ops.size(); ++o) p.osplit[o].back() = dom[nT + g.oclass[o]][s[nT + g.oclass[o]]];
+    res.plans.push_back(std::move(p));
+  }
+  std::sort(res.plans.begin(), res.plans.end(),
+            [&](const PlanSeq& a, const PlanSeq& b) { return canon_key(g, a) < canon_key(g, b); });
+  return res;
+}
+
+}  // namespace
+
+PlanResult make_plan(const Graph& g, int k, int frontier_cap, int solution_cap, int search) {
+  auto t0 = std::chrono::steady_clock::now();
+  PlanResult r;
+  r.k = k;
+  PlanSeq empty;
+  empty.tdims.assign(g.tensors.size(), {});
+  empty.osplit.assign(g.ops.size(), {});
+  std::vector<int> factors = factorize(k);
+  if (k == 1) {
+    r.seq = empty;
+  } else if (search == 0) {
+    std::vector<PlanSeq> frontier = {empty};
+    for (int ki : factors) {
+      int64_t best = INT64_MAX;
+      std::vector<PlanSeq> cands;
+      for (auto& pre : frontier) {
+        StepResult s = step_search(g, pre, ki, solution_cap);
+        r.truncated |= s.truncated;
+        if (s.cost < best) {
+          best = s.cost;
+          cands = std::move(s.plans);
+        } else if (s.cost == best) {
+          for (auto& p : s.plans) cands.push_back(std::move(p));
+        }
+      }
+      std::map<std::vector<int>, PlanSeq> uniq;
+      for (auto& p : cands) uniq.emplace(canon_key(g, p), std::move(p));
+      frontier.clear();
+      for (auto& kv : uniq) {
+        if ((int)frontier.size() >= frontier_cap) {
+          r.truncated = true;
+          break;
+        }
+        frontier.push_back(std::move(kv.second));
+      }
+    }
+    r.seq = frontier.front();
+  } else {
+    // flat exact search: VE over sequences of all steps
+    const int nT = (int)g.classes.size(), nO = (int)g.op_classes.size();
+    const int m = (int)factors.size();
+    std::vector<std::vector<std::vector<int>>> dom(nT + nO);
+    for (int c = 0; c < nT + nO; ++c) {
+      bool is_t = c < nT;
+      int rank = is_t ? (int)g.tensors[g.classes[c][0]].shape.size() : 0;
+      std::vector<int> axes = is_t ? std::vector<int>() : g.def_of(g.op_classes[c - nT][0]).split_vars();
+      if (is_t)
+        for (int d = 0; d < rank; ++d) axes.push_back(d);
+      if (is_t && rank == 0) {
+        dom[c].push_back(std::vector<int>(m, -1));
+        continue;
+      }
+      std::vector<int> seq(m, 0);
+      std::function<void(int)> rec = [&](int i) {
+        if (i == m) {
+          bool ok = true;
+          const auto& members = is_t ? g.classes[c] : g.op_classes[c - nT];
+          for (int x : members)
+            for (int a : axes) {
+              int64_t n = is_t ? g.tensors[x].shape[a] : g.ops[x].R[a];
+              for (int s = 0; s < m && ok; ++s)
+                if (seq[s] == a) {
+                  if (n % factors[s]) ok = false;
+                  n /= factors[s];
+                }
+            }
+          if (ok) dom[c].push_back(seq);
+          return;
+        }
+        for (int a : axes) {
+          seq[i] = a;
+          rec(i + 1);
+        }
+      };
+      rec(0);
+      if (dom[c].empty()) throw Error(TOFU_ERR_PLAN, "flat search: no divisible sequence");
+    }
+    VE ve;
+    for (auto& d : dom) ve.dsize.push_back((int)d.size());
+    PlanSeq cur = empty;
+    cur.factors = factors;
+    for (auto& s : cur.tdims) s.assign(m, -1);
+    for (auto& s : cur.osplit) s.assign(m, -1);
+    for (int oc = 0; oc < nO; ++oc) {
+      std::set<int> tcs;
+      for (int o : g.op_classes[oc]) {
+        for (int t : g.ops[o].inputs) tcs.insert(g.tclass[t]);
+        tcs.insert(g.tclass[g.ops[o].output]);
+      }
+      Factor f;
+      f.scope.assign(tcs.begin(), tcs.end());
+      f.scope.push_back(nT + oc);
+      int64_t n = 1;
+      for (int x : f.scope) n *= ve.dsize[x];
+      f.table.assign(n, 0);
+      std::vector<int> idx(f.scope.size());
+      for (int64_t e = 0; e < n; ++e) {
+        int64_t rr = e;
+        for (int a = (int)f.scope.size() - 1; a >= 0; --a) {
+          idx[a] = (int)(rr % ve.dsize[f.scope[a]]);
+          rr /= ve.dsize[f.scope[a]];
+        }
+        int64_t val = 0;
+        for (int o : g.op_classes[oc]) {
+          for (size_t a = 0; a + 1 < f.scope.size(); ++a)
+            for (int t : g.classes[f.scope[a]]) cur.tdims[t] = dom[f.scope[a]][idx[a]];
+          cur.osplit[o] = dom[nT + oc][idx.back()];
+          val += op_cost(g, o, cur).elements;
+        }
+        f.table[e] = val;
+      }
+      ve.factors.push_back(std::move(f));
+    }
+    std::vector<std::vector<int>> sols;
+    ve.run(1, sols);
+    PlanSeq p = cur;
+    for (size_t t = 0; t < g.tensors.size(); ++t) p.tdims[t] = dom[g.tclass[t]][sols[0][g.tclass[t]]];
+    for (size_t o = 0; o < g.ops.size(); ++o) p.osplit[o] = dom[nT + g.oclass[o]][sols[0][nT + g.oclass[o]]];
+    r.seq = p;
+  }
+  OpCost c = plan_cost(g, r.seq);
+  r.cost = c.elements;
+  r.bytes = c.bytes;
+  int64_t prev = 0;
+  for (size_t i = 1; i <= r.seq.factors.size(); ++i) {
+    PlanSeq pre;
+    pre.factors.assign(r.seq.factors.begin(), r.seq.factors.begin() + i);
+    for (auto& s : r.seq.tdims) pre.tdims.emplace_back(s.begin(), s.begin() + i);
+    for (auto& s : r.seq.osplit) pre.osplit.emplace_back(s.begin(), s.begin() + i);
+    int64_t ci = plan_cost(g, pre).elements;
+    r.deltas.push_back(ci - prev);
+    prev = ci;
+  }
+  r.search_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return r;
+}
+
+std::string plan_json(const Graph& g, const PlanResult& r) {
+  std::string o = "{\"k\":" + std::to_string(r.k) + ",\"factors\":[";
+  for (size_t i = 0; i < r.seq.factors.size(); ++i) o += (i ? "," : "") + std::to_string(r.seq.factors[i]);
+  o += "],\"tdims\":{";
+  for (size_t t = 0; t < g.tensors.size(); ++t) {
+    o += (t ? "," : "") + json_quote(g.tensors[t].name) + ":[";
+    for (size_t i = 0; i < r.seq.tdims[t].size(); ++i)
+      o += (i ? "," : "") + (r.seq.tdims[t][i] < 0 ? std::string("null") : std::to_string(r.seq.tdims[t][i]));
+    o += "]";
+  }
+  o += "},\"osplit\":{";
+  for (size_t op = 0; op < g.ops.size(); ++op) {
+    o += (op ? "," : "") + json_quote(g.ops[op].name) + ":[";
+    for (size_t i = 0; i < r.seq.osplit[op].size(); ++i)
+      o += (i ? "," : "") + json_quote(g.def_of((int)op).vars[r.seq.osplit[op][i]]);
+    o += "]";
+  }
+  o += "},\"cost\":" + std::to_string(r.cost) + ",\"bytes\":" + std::to_string(r.bytes) + ",\"deltas\":[";
+  for (size_t i = 0; i < r.deltas.size(); ++i) o += (i ? "," : "") + std::to_string(r.deltas[i]);
+  o += "],\"frontier_truncated\":" + std::string(r.truncated ? "true" : "false") +
+       ",\"search_ms\":" + json_num(r.search_ms) + "}";
+  return o;
+}
+
+}  // namespace tofu
+
+struct tofu_plan {
+  tofu::Graph g;
+  tofu::PlanResult r;
+};
+
+namespace tofu {
+const PlanResult& plan_of(const tofu_plan* p) { return p->r; }
+}
+
+extern "C" int tofu_plan_create(const tofu_graph* g, int k, const tofu_plan_options* opts, tofu_plan** out) {
+  return tofu::guard([&]() {
+    if (!g || !out || k < 1) throw tofu::Error(TOFU_ERR_ARG, "bad argument");
+    int fc = 64, sc = 256, search = 0;
+    if (opts) {
+      if (opts->frontier_cap > 0) fc = opts->frontier_cap;
+      if (opts->solution_cap > 0) sc = opts->solution_cap;
+      search = opts->search;
+    }
+    auto* h = new tofu_plan{tofu::graph_of(g), tofu::make_plan(tofu::graph_of(g), k, fc, sc, search)};
+    *out = h;
+    return TOFU_OK;
+  });
+}
+extern "C" void tofu_plan_destroy(tofu_plan* p) { delete p; }
+extern "C" int tofu_plan_cost(const tofu_plan* p, int64_t* elements, int64_t* bytes) {
+  if (!p) return tofu::fail(TOFU_ERR_ARG, "null plan");
+  if (elements) *elements = p->r.cost;
+  if (bytes) *bytes = p->r.bytes;
+  return TOFU_OK;
+}
+
+extern "C" int tofu_plan_json(const tofu_plan* p, char* out, size_t cap, size_t* len) {
+  return tofu::guard([&]() {
+    if (!p) throw tofu::Error(TOFU_ERR_ARG, "null plan");
+    return tofu::write_out(tofu::plan_json(p->g, p->r), out, cap, len);
+  });
+}

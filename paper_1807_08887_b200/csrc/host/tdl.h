@@ -1,0 +1,50 @@
+// TDL operator descriptions (§4.1) — host parser and access analysis.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace tofu {
+
+// Σ coef[v]·var_v + c, integer coefficients (Eq. 1 admits affine intervals only).
+struct Affine {
+  std::vector<std::pair<int, int64_t>> coef;  // (var index, coefficient), sorted by var index, non-zero
+  int64_t c = 0;
+  bool identity_of(int v) const { return coef.size() == 1 && coef[0].first == v && coef[0].second == 1 && c == 0; }
+};
+
+struct Access {
+  int param = 0;                 // index into OpDef::params
+  std::vector<Affine> idx;       // one per dim
+  std::vector<char> slice;       // ':' inside an opaque call (whole dim)
+};
+
+struct OpDef {
+  std::string name;
+  std::vector<std::string> params;
+  std::vector<int> ranks;
+  std::vector<std::string> vars;  // output vars, then reduce vars
+  int n_out = 0;
+  std::string reducer;            // "" if none
+  bool opaque = false;
+  std::vector<int> opaque_free;   // pass-through batch vars of an opaque op
+  std::vector<Access> accesses;
+  std::string cls;                // ElementWise | Reduction | OpaqueBatched | General
+
+  int n_red() const { return (int)vars.size() - n_out; }
+  bool is_red(int v) const { return v >= n_out; }
+  std::vector<int> split_vars() const;  // Case-1 output vars + Case-2 reduce vars
+};
+
+// Throws Error(TOFU_ERR_PARSE, "<Kind>: message").
+OpDef parse_tdl(const std::string& src);
+
+// Extent of every var given input and output shapes (reduce vars from the first dim they index alone).
+std::vector<int64_t> var_extents(const OpDef& d, const std::vector<std::vector<int64_t>>& in_shapes,
+                                 const std::vector<int64_t>& out_shape);
+
+// JSON analysis for tofu_describe_op.
+std::string describe_json(const OpDef& d, int ways);
+
+}  // namespace tofu

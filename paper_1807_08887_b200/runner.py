@@ -1,0 +1,110 @@
+"""Partitioned training-step runner over libtofu (device memory plumbing only).
+
+``TofuRunner(spec, k)`` plans the graph for k workers (tofu_plan), allocates
+one arena per local rank (torch device memory), loads tensors into the ranks'
+shards at the offsets libtofu reports, and runs steps through tofu_execute.
+
+* virtual mode (default): all k ranks live on one GPU; peer pointers are
+  local pointers and the same MultiFetch / reduce kernels run.
+* multi-process mode (``rank``/``group`` given): one process per GPU; arenas
+  and barrier words are allocated in torch symmetric memory and the peers'
+  mapped addresses are passed to libtofu, whose kernels then read peer HBM
+  over NVLink directly.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import tofu
+
+_TD = {"bf16": torch.bfloat16, "f32": torch.float32}
+
+
+class TofuRunner:
+    def __init__(self, spec: dict, k: int, device="cuda", rank: int | None = None, group=None, plan_opts=None):
+        self.spec = spec
+        self.k = k
+        self.device = torch.device(device)
+        self.graph = tofu.Graph(spec)
+        self.plan = tofu.Plan(self.graph, k, **(plan_opts or {}))
+        self.plan_json = self.plan.json()
+        self.multi = rank is not None
+        self.local = [rank] if self.multi else list(range(k))
+        self.arenas = {}
+        self._symm = None
+        if not self.multi:
+            for r in self.local:
+                n = max(256, self.plan.arena_bytes(r))
+                self.arenas[r] = torch.empty(n + 256, dtype=torch.uint8, device=self.device)
+            ptrs = [self._aligned(self.arenas[r]) for r in range(k)]
+            self.exec = tofu.Exec(self.graph, self.plan, self.local, ptrs)
+        else:
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm
+            nbytes = max(self.plan.arena_bytes(r) for r in range(k)) + 4096
+            buf = symm.empty(nbytes, dtype=torch.uint8, device=self.device)
+            hdl = symm.rendezvous(buf, group if group is not None else dist.group.WORLD)
+            self._symm = (buf, hdl)
+            self.arenas[rank] = buf
+            # arena at offset 0, barrier word in the last 4 KiB (zeroed before the first step)
+            ptrs = [int(p) for p in hdl.buffer_ptrs]
+            flags = [p + nbytes - 4096 for p in ptrs]
+            buf[nbytes - 4096:].zero_()
+            torch.cuda.synchronize()
+            dist.barrier(group)
+            self.exec = tofu.Exec(self.graph, self.plan, self.local, ptrs, flags)
+        self.shards = {r: {t: self.plan.shard(r, t) for t in spec["tensors"]} for r in range(k)}
+
+    @staticmethod
+    def _aligned(t):
+        p = t.data_ptr()
+        return (p + 255) // 256 * 256
+
+    def _base(self, r):
+        return self._aligned(self.arenas[r]) if not self.multi else self.arenas[r].data_ptr()
+
+    def view(self, r: int, name: str) -> torch.Tensor | None:
+        """The shard of tensor `name` held by rank r, as a torch view into the arena."""
+        off, box = self.shards[r][name]
+        if off < 0 or r not in self.arenas:
+            return None
+        info = self.spec["tensors"][name]
+        dt = _TD[info["dtype"]]
+        shape = [hi - lo + 1 for lo, hi in box]
+        n = int(np.prod(shape)) if shape else 1
+        arena = self.arenas[r]
+        start = self._base(r) - arena.data_ptr() + off
+        es = 2 if dt == torch.bfloat16 else 4
+        return arena[start:start + n * es].view(dt).view(shape if shape else [])
+
+    def load(self, values: dict):
+        """Copy full tensors (numpy or torch, host or device) into every local rank's shards."""
+        for name, v in values.items():
+            src = torch.as_tensor(np.asarray(v)) if not torch.is_tensor(v) else v
+            for r in self.local:
+                dst = self.view(r, name)
+                if dst is None:
+                    continue
+                _, box = self.shards[r][name]
+                sl = tuple(slice(lo, hi + 1) for lo, hi in box)
+                dst.copy_(src[sl].to(dst.dtype), non_blocking=True)
+
+    def gather(self, name: str) -> torch.Tensor:
+        """Assemble a full tensor from the local ranks' shards (virtual mode: all ranks)."""
+        info = self.spec["tensors"][name]
+        full = torch.empty(info["shape"], dtype=_TD[info["dtype"]], device=self.device)
+        for r in self.local:
+            v = self.view(r, name)
+            if v is None:
+                continue
+            _, box = self.shards[r][name]
+            sl = tuple(slice(lo, hi + 1) for lo, hi in box)
+            full[sl] = v
+        return full
+
+    def step(self, stream=None):
+        self.exec.run(stream)
+
+    def ledger(self):
+        return self.exec.ledger()

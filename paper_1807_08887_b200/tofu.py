@@ -71,6 +71,10 @@ def lib():
             "tofu_exec_ledger": [vp, i64p, i64p],
             "tofu_exec_launch_count": [vp, i64p],
             "tofu_exec_set_skip_comm": [vp, C.c_int],
+            "tofu_exec_num_launches": [vp, C.POINTER(C.c_int)],
+            "tofu_exec_launch_desc": [vp, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
+            "tofu_execute_range": [vp, C.c_int, C.c_int, vp],
+            "tofu_exec_time_launch": [vp, C.c_int, vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name, None)
@@ -198,6 +202,25 @@ class Exec:
         n = C.c_int64()
         check(lib().tofu_exec_launch_count(self.h, C.byref(n)), "tofu_exec_launch_count")
         return n.value
+
+    def num_launches(self) -> int:
+        n = C.c_int()
+        check(lib().tofu_exec_num_launches(self.h, C.byref(n)), "tofu_exec_num_launches")
+        return n.value
+
+    def launch_desc(self, i: int) -> dict:
+        buf = C.create_string_buffer(1024)
+        n = C.c_size_t()
+        check(lib().tofu_exec_launch_desc(self.h, i, buf, 1024, C.byref(n)), "tofu_exec_launch_desc")
+        return json.loads(buf.value.decode())
+
+    def run_range(self, first: int, last: int, stream=None):
+        check(lib().tofu_execute_range(self.h, first, last, _stream(stream)), "tofu_execute_range")
+
+    def time_launch(self, index: int, ev_start=None, ev_stop=None):
+        a = C.c_void_p(ev_start.cuda_event) if ev_start is not None else None
+        b = C.c_void_p(ev_stop.cuda_event) if ev_stop is not None else None
+        check(lib().tofu_exec_time_launch(self.h, index, a, b), "tofu_exec_time_launch")
 
     def skip_comm(self, on: bool):
         check(lib().tofu_exec_set_skip_comm(self.h, 1 if on else 0), "tofu_exec_set_skip_comm")

@@ -1,0 +1,165 @@
+"""CPU tests of libtofu's host side (C ABI): the library loads and exports
+every symbol include/tofu.h declares; describe_op and tofu_plan equal the
+oracle bit-exactly; the executor's lowered byte ledger equals the plan cost
+(no GPU needed: device allocations are deferred to the first tofu_execute)."""
+import ctypes as C
+import json
+import os
+import re
+from fractions import Fraction
+
+import pytest
+
+from fixtures import random_chain
+from oracle.cost import owned_box, digits, plan_cost
+from oracle.graph import Graph as OGraph
+from oracle.search import SearchError, flat_search, recursive_search
+from oracle.strategy import discover_strategies
+from oracle.tdl import parse_def, parse_program
+from tofu_inputs.graphs import config, mlp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def tofu():
+    from paper_1807_08887_b200 import build, tofu as t
+    build.build(verbose=False)
+    t.lib()
+    return t
+
+
+def test_library_exports_every_declared_symbol(tofu):
+    hdr = open(os.path.join(ROOT, "include", "tofu.h")).read()
+    names = set(re.findall(r"\b(tofu_[a-z0-9_]+)\s*\(", hdr))
+    assert len(names) >= 20
+    L = tofu.lib()
+    missing = [n for n in sorted(names) if not hasattr(L, n)]
+    assert not missing, missing
+
+
+def test_describe_op_matches_oracle(tofu):
+    corpus = parse_program(open(os.path.join(ROOT, "tests", "golden", "corpus.tdl")).read())
+    for name, d in corpus.items():
+        src = [l for l in open(os.path.join(ROOT, "tests", "golden", "corpus.tdl")).read().splitlines()
+               if l.startswith(f"def {name}(")][0]
+        for ways in (2, 3):
+            got = tofu.describe_op(src, ways)
+            assert got["out_vars"] == d.out_vars and got["red_vars"] == d.red_vars
+            assert got["class"] == {"ElementWise": "ElementWise"}.get(got["class"], got["class"])
+            from oracle.tdl import classify
+            assert got["class"] == classify(d)[0]
+            ost = discover_strategies(d, ways)
+            assert [s["var"] for s in got["strategies"]] == [s["var"] for s in ost]
+            for gs, os_ in zip(got["strategies"], ost):
+                assert gs["kind"] == os_["kind"]
+                for j in range(ways):
+                    for greg, (t, dims) in zip(gs["regions"][j], os_["regions"][j]):
+                        assert greg["tensor"] == t
+                        for gd, od in zip(greg["dims"], dims):
+                            if od is None:
+                                assert gd is None
+                                continue
+                            lo = {k: Fraction(*v) for k, v in gd["lo"].items()}
+                            hi = {k: Fraction(*v) for k, v in gd["hi"].items()}
+                            assert lo == dict(od.lo) and hi == dict(od.hi)
+                            assert gd["c_lo"] == od.c_lo and gd["c_hi"] == od.c_hi
+
+
+@pytest.mark.parametrize("src", ["def bad(A(2)) -> lambda i: A[i, i]", "def bad(A(1)) -> lambda i, j: A[i * j]",
+                                 "def bad(A(1)) -> lambda i: B[i]", "def bad(A(1)) -> lambda i: A[i"])
+def test_describe_op_errors(tofu, src):
+    with pytest.raises(tofu.TofuError):
+        tofu.describe_op(src)
+
+
+def _canon(plan):
+    return {"tdims": {t: [None if d is None else d for d in s] for t, s in plan["tdims"].items()},
+            "osplit": plan["osplit"]}
+
+
+@pytest.mark.parametrize("cfg,k", [(0, 2), (0, 4), (0, 8), (1, 2), (1, 4), (1, 8)])
+def test_plan_bit_exact_vs_oracle_configs(tofu, cfg, k):
+    spec = config(cfg)
+    g = tofu.Graph(spec)
+    p = tofu.Plan(g, k).json()
+    o = recursive_search(OGraph(spec), k)
+    assert p["cost"] == o["cost"] and p["bytes"] == o["bytes"] and p["deltas"] == o["deltas"]
+    assert p["tdims"] == o["tdims"] and p["osplit"] == o["osplit"]
+    assert p["factors"] == o["factors"]
+
+
+def test_plan_bit_exact_vs_oracle_random(tofu):
+    n = 0
+    for s in range(40):
+        spec = random_chain(s)
+        og = OGraph(spec)
+        for k in (2, 4, 8):
+            try:
+                o = recursive_search(og, k)
+            except SearchError:
+                with pytest.raises(tofu.TofuError):
+                    tofu.Plan(tofu.Graph(spec), k)
+                continue
+            p = tofu.Plan(tofu.Graph(spec), k).json()
+            assert (p["cost"], p["bytes"], p["deltas"]) == (o["cost"], o["bytes"], o["deltas"]), (s, k)
+            if not o["frontier_truncated"]:
+                assert p["tdims"] == o["tdims"] and p["osplit"] == o["osplit"], (s, k)
+            n += 1
+    assert n > 60
+
+
+def test_flat_search_equals_oracle(tofu):
+    for s in range(15):
+        spec = random_chain(s)
+        try:
+            c, _ = flat_search(OGraph(spec), 4)
+        except SearchError:
+            continue
+        p = tofu.Plan(tofu.Graph(spec), 4, search=1).json()
+        assert p["cost"] == c
+
+
+def test_shards_match_oracle_owned_boxes(tofu):
+    spec = config(0)
+    g = tofu.Graph(spec)
+    plan = tofu.Plan(g, 8)
+    pj = plan.json()
+    og = OGraph(spec)
+    for r in range(8):
+        dig = digits(r, pj["factors"])
+        offs = set()
+        for t in spec["tensors"]:
+            off, box = plan.shard(r, t)
+            ob = owned_box(og.shape(t), pj["tdims"][t], pj["factors"], dig)
+            if ob is None:
+                assert off == -1
+            else:
+                assert [tuple(b) for b in box] == [tuple(b) for b in ob]
+                assert off % 256 == 0
+        assert plan.arena_bytes(r) > 0
+
+
+@pytest.mark.parametrize("cfg,k", [(0, 2), (0, 4), (0, 8), (1, 8)])
+def test_lowered_ledger_equals_plan(tofu, cfg, k):
+    """Bytes the executor will move (counted from its lowered MultiFetch and
+    reduce pieces) == planned cost (north star: bytes moved equal the plan)."""
+    spec = config(cfg)
+    g = tofu.Graph(spec)
+    plan = tofu.Plan(g, k)
+    fake = [0x100000000 * (r + 1) for r in range(k)]  # never dereferenced before tofu_execute
+    ex = tofu.Exec(g, plan, list(range(k)), fake)
+    assert ex.ledger() == plan.cost()
+    assert ex.launches() > 0
+
+
+def test_plan_time_table2_scale(tofu):
+    """Search time (Table 2 reports 8.3 s for WResNet-152 on 8
+    workers): a 1500-op-scale chain plans for 8 workers in seconds."""
+    import time
+    spec = mlp(64, [256] * 41)   # 40 layers: 40 fwd + 80 bwd + 80 optimizer + 40 relu pairs ~ 280 ops
+    g = tofu.Graph(spec)
+    t = time.time()
+    p = tofu.Plan(g, 8).json()
+    assert time.time() - t < 60
+    assert p["cost"] >= 0
