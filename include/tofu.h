@@ -127,9 +127,11 @@ int tofu_exec_time_launch(tofu_exec* e, int index, void* ev_start, void* ev_stop
 
 /* a4 — C[m,n] (+)= Σ_k A[m,k]·B[k,n], bf16 operands, fp32 accumulation in TMEM (tcgen05).
  *   A K-major: A[m*lda+k]; MN-major: A[k*lda+m].  B K-major: B[n*ldb+k]; MN-major: B[k*ldb+n].
- *   c_mode 0: C bf16 = round(acc); 1: C f32 = acc; 2: C f32 += acc.  ldc in elements.
- *   Requirements: lda, ldb multiples of 8; A, B 16-byte aligned.  bn: 0 = auto, 128 or 256.
- *   max_ctas: 0 = #SMs (persistent grid), else cap.
+ *   c_mode 0: C bf16 = round(acc); 1: C f32 = acc; 2: C f32 += acc;
+ *          3: fused momentum-SGD on a weight gradient (P:L674-678 optimizer chain folded into its
+ *             producer): C f32 (momentum, in/out) = C*s0 + acc; D bf16 (weight, in/out) = D - C*s1.
+ *   ldc/ldd in elements.  Requirements: lda, ldb, ldd multiples of 8, ldc*elem a multiple of 16 B;
+ *   A, B, C, D 16-byte aligned.  bn: 0 = auto, 128 or 256.  max_ctas: 0 = #SMs (persistent grid).
  */
 typedef struct {
   int M, N, K;
@@ -140,12 +142,15 @@ typedef struct {
   void* C;
   int ldc, c_mode;
   int bn, max_ctas;
+  void* D;
+  int ldd;
+  float s0, s1;
 } tofu_gemm_args;
 int tofu_gemm_bf16(const tofu_gemm_args* args, void* stream);
-/* Split form used by the executor: encode the two TMA descriptors once (128 bytes each, 64-aligned). */
-int tofu_gemm_plan_tmaps(const tofu_gemm_args* args, void* tmap_a, void* tmap_b, int* bn_out);
-int tofu_gemm_launch_planned(const tofu_gemm_args* args, const void* tmap_a, const void* tmap_b, int bn,
-                             void* stream);
+/* Split form used by the executor: encode the four TMA descriptors (A, B, C, D) once into `tmaps`
+ * (4 x 128 bytes, 64-byte aligned), then launch with them. */
+int tofu_gemm_plan_tmaps(const tofu_gemm_args* args, void* tmaps, int* bn_out);
+int tofu_gemm_launch_planned(const tofu_gemm_args* args, const void* tmaps, int bn, void* stream);
 
 /* a5/a6 — box copy / reduction pieces (rank <= 4, innermost dim last, strides in elements).
  * A piece copies (nsrc == 1) or sums in order (nsrc > 1, fp32 arithmetic) nsrc source boxes of the same

@@ -1,19 +1,23 @@
 // Sub-operator GEMM on sm_100a: TMA -> smem (SWIZZLE_128B) -> tcgen05.mma (bf16 x bf16 -> fp32 in TMEM)
-// -> tcgen05.ld epilogue.  This is the dense-contraction sub-op every worker runs on its tile under
-// partition-n-reduce (§3.1: "executing the same operator on each worker using smaller inputs").
+// -> tcgen05.ld epilogue -> smem -> TMA store.  This is the dense-contraction sub-op every worker runs on its
+// tile under partition-n-reduce (§3.1: "executing the same operator on each worker using smaller
+// inputs").
 //
 // C[m, n] (+)= sum_k A[m, k] * B[k, n]
 //   A K-major : A[m*lda + k]      A MN-major : A[k*lda + m]
 //   B K-major : B[n*ldb + k]      B MN-major : B[k*ldb + n]
 // The three TDL matmul defs map to (A,B) majorness: mm_nn (K, MN), mm_nt (K, K), mm_tn (MN, MN).
 //
-// Epilogues: 0 = bf16 store, 1 = fp32 store (partial outputs of Case-2 strategies, weight grads),
-//            2 = fp32 accumulate (C += acc).
+// Epilogues (c_mode): 0 = bf16 store, 1 = fp32 store (Case-2 partials, weight grads), 2 = fp32 accumulate,
+// 3 = fused momentum-SGD on the weight gradient: M = M*s0 + acc (fp32, in place), W = W - M*s1 (bf16, in
+// place).  Mode 3 is the coalesced optimizer chain of P:L674-678 folded into the gradient's producer so the
+// gradient never touches HBM.
 //
-// Warp roles (192 threads): warp 0 = TMA producer (1 elected lane), warp 1 = TMEM allocator + MMA issuer
-// (1 lane), warps 2..5 = epilogue (warp w reads TMEM lanes 32*(w%4)..+31).  Persistent: each CTA walks
-// output tiles (grid = min(#tiles, #SMs)); the accumulator is double-buffered in TMEM so the epilogue of
-// tile t overlaps the mainloop of tile t+1.
+// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer (1 lane),
+// warps 2..5 = epilogue (warp w owns TMEM lanes 32*(w%4)..+31 = tile rows).  Persistent grid over output
+// tiles; the accumulator is double-buffered in TMEM so the epilogue of tile t overlaps the mainloop of t+1.
+// The epilogue moves 32x32 chunks through swizzled smem with TMA (loads of M/W prefetched NBUF-1 chunks ahead,
+// bulk-async stores), so every HBM access is a full-line TMA transfer.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cstdio>
@@ -27,33 +31,47 @@ namespace tofu {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int NTHREADS = 192;
+constexpr int SMEM_MAX = 232448;  // 227 KB opt-in per CTA on sm_100
 
-template <int BN>
+template <int BN, int MODE>
 struct GemmCfg {
-  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr bool LOADS = MODE >= 2;
+  static constexpr int NBUF = LOADS ? 3 : 2;
+  static constexpr int C_BYTES = 32 * 32 * (MODE == 0 ? 2 : 4);
+  static constexpr int D_OFF = 4096;
+  static constexpr int BUF_BYTES = MODE == 3 ? 6144 : (C_BYTES < 1024 ? 1024 : C_BYTES);
+  static constexpr int EPI_BYTES = 4 * NBUF * BUF_BYTES;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES_FIT = (SMEM_MAX - 1024 - 512 - EPI_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
   static constexpr int ACC_BUFS = 2;
   static constexpr int TMEM_COLS = BN * ACC_BUFS;  // 256 or 512 fp32 columns
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+  static_assert(STAGES >= 2, "pipeline too shallow");
+  static_assert(SMEM <= SMEM_MAX, "smem");
 };
 
-template <int BN, bool A_MN, bool B_MN, int OUT>
+template <int BN, bool A_MN, bool B_MN, int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
-    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, void* Cp,
-                     int M, int N, int K, int ldc) {
-  using Cfg = GemmCfg<BN>;
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD, int M, int N,
+                     int K, float s0, float s1) {
+  using Cfg = GemmCfg<BN, MODE>;
   constexpr int STAGES = Cfg::STAGES;
+  constexpr int NBUF = Cfg::NBUF;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint8_t* sE = smem + STAGES * Cfg::STAGE_BYTES;  // epilogue chunk buffers [4 warps][NBUF]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sE + Cfg::EPI_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* acc_full = empty + STAGES;          // [ACC_BUFS]
+  uint64_t* acc_full = empty + STAGES;             // [ACC_BUFS]
   uint64_t* acc_empty = acc_full + Cfg::ACC_BUFS;  // [ACC_BUFS]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + Cfg::ACC_BUFS);
+  uint64_t* ebar = acc_empty + Cfg::ACC_BUFS;      // [4][NBUF] epilogue load barriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 4 * NBUF);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -71,9 +89,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], 4);  // one arrive per epilogue warp
     }
+    for (int b = 0; b < 4 * NBUF; ++b) mbar_init(&ebar[b], 1);
     fence_mbar_init();
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmC);
+    if (MODE == 3) tma_prefetch_desc(&tmD);
   }
   if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
   tc_fence_before();
@@ -144,66 +165,104 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue (warps 2..5)
-    const int lane_base = 32 * (warp & 3);
+    const int q = warp & 3;  // TMEM lane quarter = tile rows 32q..32q+31
+    constexpr int NCH = BN / 32;
+    const int my_tiles = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const int S = my_tiles * NCH;
+    uint8_t* wbuf = sE + q * NBUF * Cfg::BUF_BYTES;
+    uint64_t* wbar = ebar + q * NBUF;
+    auto chunk_coords = [&](int s, int& col, int& row) {
+      const int tile = blockIdx.x + (s / NCH) * gridDim.x;
+      col = (tile % tiles_n) * BN + (s % NCH) * 32;
+      row = (tile / tiles_n) * BM + q * 32;
+    };
+    auto issue_load = [&](int s) {  // lane 0 only
+      int col, row;
+      chunk_coords(s, col, row);
+      uint8_t* b = wbuf + (s % NBUF) * Cfg::BUF_BYTES;
+      mbar_arrive_expect_tx(&wbar[s % NBUF], MODE == 3 ? 6144 : 4096);
+      tma_load_2d(b, &tmC, &wbar[s % NBUF], col, row);
+      if (MODE == 3) tma_load_2d(b + Cfg::D_OFF, &tmD, &wbar[s % NBUF], col, row);
+    };
+    if (Cfg::LOADS && lane == 0)
+      for (int s = 0; s < NBUF - 1 && s < S; ++s) issue_load(s);
     int local = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++local) {
-      const int m0 = (tile / tiles_n) * BM;
-      const int n0 = (tile % tiles_n) * BN;
-      const int buf = local & 1;
-      const uint32_t aph = (local >> 1) & 1;
-      mbar_wait(&acc_full[buf], aph);
-      tc_fence_after();
-      const int row = m0 + lane_base + lane;
-      const bool row_ok = row < M && nk > 0;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + buf * BN + ((uint32_t)lane_base << 16) + c, r);
-        tmem_ld_wait();
-        const int col = n0 + c;
-        if (!row_ok || col >= N) continue;
-        const bool full_chunk = (col + 32 <= N);
-        if (OUT == 0) {
-          __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(Cp) + (size_t)row * ldc + col;
-          if (full_chunk && ((reinterpret_cast<uintptr_t>(C) & 15) == 0)) {
-            uint32_t p[16];
+    for (int s = 0; s < S; ++s) {
+      const int c = s % NCH;
+      const int acc = local & 1;
+      if (c == 0) {
+        mbar_wait(&acc_full[acc], (local >> 1) & 1);
+        tc_fence_after();
+      }
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, r);
+      tmem_ld_wait();
+      if (c == NCH - 1) {  // accumulator fully read: hand TMEM back to the MMA warp
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[acc]);
+        ++local;
+      }
+      uint8_t* b = wbuf + (s % NBUF) * Cfg::BUF_BYTES;
+      if (Cfg::LOADS) {
+        if (lane == 0 && s + NBUF - 1 < S) {
+          bulk_wait_read<0>();  // the store that last used that buffer has read its smem
+          issue_load(s + NBUF - 1);
+        }
+        __syncwarp();
+        mbar_wait(&wbar[s % NBUF], (s / NBUF) & 1);
+      } else {
+        if (lane == 0) bulk_wait_read<NBUF - 1>();
+        __syncwarp();
+      }
+      if (MODE == 0) {
+        uint32_t p[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-              p[j] = *reinterpret_cast<uint32_t*>(&h);
-            }
-            uint4* dst = reinterpret_cast<uint4*>(C);
+        for (int j = 0; j < 16; ++j) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+          p[j] = *reinterpret_cast<uint32_t*>(&h);
+        }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dst[j] = make_uint4(p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
-          } else {
-            for (int j = 0; j < 32 && col + j < N; ++j) C[j] = __float2bfloat16_rn(__uint_as_float(r[j]));
+        for (int j = 0; j < 4; ++j)
+          *reinterpret_cast<uint4*>(b + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+              make_uint4(p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4* slot = reinterpret_cast<float4*>(b + lane * 128 + ((j ^ (lane & 7)) << 4));
+          float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                 __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+          if (MODE == 2) {
+            const float4 o = *slot;
+            v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+          } else if (MODE == 3) {
+            const float4 o = *slot;
+            v = make_float4(o.x * s0 + v.x, o.y * s0 + v.y, o.z * s0 + v.z, o.w * s0 + v.w);
           }
-        } else {
-          float* C = reinterpret_cast<float*>(Cp) + (size_t)row * ldc + col;
-          if (full_chunk && ((reinterpret_cast<uintptr_t>(C) & 15) == 0)) {
-            float4* dst = reinterpret_cast<float4*>(C);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                     __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-              if (OUT == 2) {
-                const float4 o = dst[j];
-                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
-              }
-              dst[j] = v;
-            }
-          } else {
-            for (int j = 0; j < 32 && col + j < N; ++j) {
-              const float v = __uint_as_float(r[j]);
-              C[j] = (OUT == 2) ? C[j] + v : v;
-            }
+          *slot = v;
+          if (MODE == 3) {  // W chunk: 8 bf16 per 16B, row = 64 B, SWIZZLE_64B
+            const int wj = j >> 1, half = j & 1;
+            uint2* wslot = reinterpret_cast<uint2*>(b + Cfg::D_OFF + lane * 64 + ((wj ^ ((lane >> 1) & 3)) << 4)) + half;
+            const uint2 wv = *wslot;
+            float2 w0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv.x));
+            float2 w1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv.y));
+            __nv_bfloat162 n0 = __floats2bfloat162_rn(w0.x - v.x * s1, w0.y - v.y * s1);
+            __nv_bfloat162 n1 = __floats2bfloat162_rn(w1.x - v.z * s1, w1.y - v.w * s1);
+            *wslot = make_uint2(*reinterpret_cast<uint32_t*>(&n0), *reinterpret_cast<uint32_t*>(&n1));
           }
         }
       }
-      tc_fence_before();
+      fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      if (lane == 0) {
+        int col, row;
+        chunk_coords(s, col, row);
+        tma_store_2d(&tmC, b, col, row);
+        if (MODE == 3) tma_store_2d(&tmD, b + Cfg::D_OFF, col, row);
+        bulk_commit();
+      }
     }
+    if (lane == 0) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -232,23 +291,22 @@ static int encode_fn_init() {
   return g_encode ? 0 : -1;
 }
 
-// 2-D bf16 tensor map: inner extent `inner` (contiguous), outer extent `outer`, row pitch `ld` elements.
-static int make_tmap(CUtensorMap* tm, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
-                     uint32_t box_outer) {
+// 2-D tensor map: inner extent (contiguous), outer extent, row pitch `ld` elements.
+static int make_tmap(CUtensorMap* tm, const void* ptr, CUtensorMapDataType dt, int esize, uint64_t inner,
+                     uint64_t outer, uint64_t ld, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld * 2};
+  cuuint64_t strides[1] = {ld * esize};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  CUresult r = g_encode(tm, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -(int)r - 1000;
 }
 
-template <int BN, bool A_MN, bool B_MN, int OUT>
-static int launch_t(const tofu_gemm_args* g, const CUtensorMap& ta, const CUtensorMap& tb, cudaStream_t st) {
-  using Cfg = GemmCfg<BN>;
-  auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, OUT>;
+template <int BN, bool A_MN, bool B_MN, int MODE>
+static int launch_t(const tofu_gemm_args* g, const CUtensorMap* tm, cudaStream_t st) {
+  using Cfg = GemmCfg<BN, MODE>;
+  auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, MODE>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
@@ -258,20 +316,19 @@ static int launch_t(const tofu_gemm_args* g, const CUtensorMap& ta, const CUtens
   const int tiles = ((g->M + BM - 1) / BM) * ((g->N + BN - 1) / BN);
   int grid = tiles < g_num_sms ? tiles : g_num_sms;
   if (g->max_ctas > 0 && grid > g->max_ctas) grid = g->max_ctas;
-  kern<<<grid, NTHREADS, Cfg::SMEM, st>>>(ta, tb, g->C, g->M, g->N, g->K, g->ldc);
+  kern<<<grid, NTHREADS, Cfg::SMEM, st>>>(tm[0], tm[1], tm[2], tm[3], g->M, g->N, g->K, g->s0, g->s1);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }
 
 template <int BN>
-static int dispatch_bn(const tofu_gemm_args* g, const CUtensorMap& ta, const CUtensorMap& tb, cudaStream_t st) {
+static int dispatch_bn(const tofu_gemm_args* g, const CUtensorMap* tm, cudaStream_t st) {
   const int key = (g->a_mn_major ? 1 : 0) | (g->b_mn_major ? 2 : 0) | (g->c_mode << 2);
   switch (key) {
 #define TOFU_CASE(AM, BMJ, O) \
-  case ((AM) | ((BMJ) << 1) | ((O) << 2)): return launch_t<BN, (bool)(AM), (bool)(BMJ), O>(g, ta, tb, st);
-    TOFU_CASE(0, 0, 0) TOFU_CASE(0, 0, 1) TOFU_CASE(0, 0, 2)
-    TOFU_CASE(0, 1, 0) TOFU_CASE(0, 1, 1) TOFU_CASE(0, 1, 2)
-    TOFU_CASE(1, 0, 0) TOFU_CASE(1, 0, 1) TOFU_CASE(1, 0, 2)
-    TOFU_CASE(1, 1, 0) TOFU_CASE(1, 1, 1) TOFU_CASE(1, 1, 2)
+  case ((AM) | ((BMJ) << 1) | ((O) << 2)): return launch_t<BN, (bool)(AM), (bool)(BMJ), O>(g, tm, st);
+#define TOFU_CASES(O) TOFU_CASE(0, 0, O) TOFU_CASE(0, 1, O) TOFU_CASE(1, 0, O) TOFU_CASE(1, 1, O)
+    TOFU_CASES(0) TOFU_CASES(1) TOFU_CASES(2) TOFU_CASES(3)
+#undef TOFU_CASES
 #undef TOFU_CASE
     default: return TOFU_ERR_ARG;
   }
@@ -281,47 +338,57 @@ static int dispatch_bn(const tofu_gemm_args* g, const CUtensorMap& ta, const CUt
 
 using namespace tofu;
 
-extern "C" int tofu_gemm_plan_tmaps(const tofu_gemm_args* g, void* tmap_a, void* tmap_b, int* bn_out) {
+// tmaps: 4 x CUtensorMap (A, B, C, D), 64-byte aligned, 512 bytes total.
+extern "C" int tofu_gemm_plan_tmaps(const tofu_gemm_args* g, void* tmaps, int* bn_out) {
   if (encode_fn_init() != 0) return TOFU_ERR_CUDA;
-  if (!g || g->M < 0 || g->N < 0 || g->K < 0 || g->c_mode < 0 || g->c_mode > 2) return TOFU_ERR_ARG;
-  // TMA: row pitch must be a multiple of 16 bytes, base 16-byte aligned
-  if ((g->lda % 8) || (g->ldb % 8) || (reinterpret_cast<uintptr_t>(g->A) & 15) ||
-      (reinterpret_cast<uintptr_t>(g->B) & 15))
+  if (!g || g->M < 0 || g->N < 0 || g->K < 0 || g->c_mode < 0 || g->c_mode > 3) return TOFU_ERR_ARG;
+  if (g->c_mode == 3 && (!g->D || (g->ldd % 8))) return TOFU_ERR_ARG;
+  // TMA: row pitch must be a multiple of 16 bytes, bases 16-byte aligned
+  const int ce = g->c_mode == 0 ? 2 : 4;
+  if ((g->lda % 8) || (g->ldb % 8) || ((g->ldc * ce) % 16) || (reinterpret_cast<uintptr_t>(g->A) & 15) ||
+      (reinterpret_cast<uintptr_t>(g->B) & 15) || (reinterpret_cast<uintptr_t>(g->C) & 15) ||
+      (reinterpret_cast<uintptr_t>(g->D) & 15))
     return TOFU_ERR_ALIGN;
-  const int bn = (g->bn == 128 || g->bn == 256) ? g->bn : ((g->N <= 128 || (long)g->M * g->N <= 148L * 128 * 256) ? 128 : 256);
-  CUtensorMap* ta = reinterpret_cast<CUtensorMap*>(tmap_a);
-  CUtensorMap* tb = reinterpret_cast<CUtensorMap*>(tmap_b);
+  const int bn = (g->bn == 128 || g->bn == 256) ? g->bn : (g->N <= 128 ? 128 : 256);
+  CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(tmaps);
+  const CUtensorMapDataType BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const auto SW128 = CU_TENSOR_MAP_SWIZZLE_128B, SW64 = CU_TENSOR_MAP_SWIZZLE_64B;
   int r;
-  if (!g->a_mn_major) r = make_tmap(ta, g->A, g->K, g->M, g->lda, 64, BM);
-  else r = make_tmap(ta, g->A, g->M, g->K, g->lda, 64, 64);
+  if (!g->a_mn_major) r = make_tmap(&tm[0], g->A, BF, 2, g->K, g->M, g->lda, 64, BM, SW128);
+  else r = make_tmap(&tm[0], g->A, BF, 2, g->M, g->K, g->lda, 64, 64, SW128);
   if (r) return TOFU_ERR_CUDA;
-  if (!g->b_mn_major) r = make_tmap(tb, g->B, g->K, g->N, g->ldb, 64, bn);
-  else r = make_tmap(tb, g->B, g->N, g->K, g->ldb, 64, 64);
+  if (!g->b_mn_major) r = make_tmap(&tm[1], g->B, BF, 2, g->K, g->N, g->ldb, 64, bn, SW128);
+  else r = make_tmap(&tm[1], g->B, BF, 2, g->N, g->K, g->ldb, 64, 64, SW128);
+  if (r) return TOFU_ERR_CUDA;
+  if (g->c_mode == 0) r = make_tmap(&tm[2], g->C, BF, 2, g->N, g->M, g->ldc, 32, 32, SW64);
+  else r = make_tmap(&tm[2], g->C, F32, 4, g->N, g->M, g->ldc, 32, 32, SW128);
+  if (r) return TOFU_ERR_CUDA;
+  if (g->c_mode == 3) r = make_tmap(&tm[3], g->D, BF, 2, g->N, g->M, g->ldd, 32, 32, SW64);
+  else tm[3] = tm[2];
   if (r) return TOFU_ERR_CUDA;
   *bn_out = bn;
   return TOFU_OK;
 }
 
-extern "C" int tofu_gemm_launch_planned(const tofu_gemm_args* g, const void* tmap_a, const void* tmap_b, int bn,
-                                        void* stream) {
+extern "C" int tofu_gemm_launch_planned(const tofu_gemm_args* g, const void* tmaps, int bn, void* stream) {
   if (g->M == 0 || g->N == 0) return TOFU_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (g->K == 0) {
     if (g->c_mode == 2) return TOFU_OK;
+    if (g->c_mode == 3) return TOFU_ERR_ARG;
     const size_t es = g->c_mode == 0 ? 2 : 4;
     return cudaMemset2DAsync(g->C, (size_t)g->ldc * es, 0, (size_t)g->N * es, g->M, st) == cudaSuccess
                ? TOFU_OK
                : TOFU_ERR_CUDA;
   }
-  const CUtensorMap& ta = *reinterpret_cast<const CUtensorMap*>(tmap_a);
-  const CUtensorMap& tb = *reinterpret_cast<const CUtensorMap*>(tmap_b);
-  return bn == 256 ? dispatch_bn<256>(g, ta, tb, st) : dispatch_bn<128>(g, ta, tb, st);
+  const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(tmaps);
+  return bn == 256 ? dispatch_bn<256>(g, tm, st) : dispatch_bn<128>(g, tm, st);
 }
 
 extern "C" int tofu_gemm_bf16(const tofu_gemm_args* g, void* stream) {
-  alignas(64) CUtensorMap ta, tb;
+  alignas(64) CUtensorMap tm[4];
   int bn = 0;
-  int r = tofu_gemm_plan_tmaps(g, &ta, &tb, &bn);
+  int r = tofu_gemm_plan_tmaps(g, tm, &bn);
   if (r) return r;
-  return tofu_gemm_launch_planned(g, &ta, &tb, bn, stream);
+  return tofu_gemm_launch_planned(g, tm, bn, stream);
 }

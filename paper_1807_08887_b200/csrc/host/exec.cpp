@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <set>
@@ -89,6 +90,7 @@ struct LOp {
   bool partial = false;
   bool skip = false;          // fused into the previous op
   bool fused_sgd = false;
+  int fused_opt = -1;         // GEMM epilogue absorbs mom (this index) + sgd (index + 1)
   std::vector<tofu_piece> fetch, reduce;
   std::vector<int> fetch_src, reduce_nremote;  // for the ledger
 };
@@ -145,7 +147,7 @@ struct Exec {
   bool finalized = false;
   struct GemmLaunch {
     tofu_gemm_args a;
-    alignas(64) CUtensorMap ta, tb;
+    alignas(64) CUtensorMap tm[4];
     int bn;
   };
   std::map<std::pair<int, int>, GemmLaunch> gemms;  // (op, li)
@@ -153,6 +155,7 @@ struct Exec {
   int64_t n_kernels = 0;
   bool skip_comm = false;
   bool multi_process = false;
+  bool fuse = true;
   int timed_launch = -1;
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
 };
@@ -365,6 +368,41 @@ void lower(Exec& E) {
         Lb.skip = true;
       }
     }
+  // wgrad GEMM -> mom -> sgd: fold the optimizer into the GEMM epilogue (c_mode 3) when the gradient is
+  // complete and local and read by nothing else; the gradient then never reaches HBM.
+  if (E.fuse)
+    for (int r = 0; r < k; ++r)
+      for (size_t o = 0; o < g.ops.size(); ++o) {
+        const OpInfo& a = g.ops[o];
+        const char* kk = kernel_kind(g.defs[a.def].name);
+        if (!kk || std::string(kk) != "gemm") continue;
+        int reader = -1, readers = 0;
+        for (size_t x = 0; x < g.ops.size(); ++x)
+          for (int t : g.ops[x].inputs)
+            if (t == a.output) {
+              ++readers;
+              reader = (int)x;
+            }
+        if (readers != 1 || reader <= (int)o || reader + 1 >= (int)g.ops.size()) continue;
+        const OpInfo &b = g.ops[reader], &c = g.ops[reader + 1];
+        if (g.defs[b.def].name != "mom" || !all[r][reader].fused_sgd) continue;
+        // moving mom+sgd up to the GEMM must not reorder any access to M / W
+        std::set<int> state = {b.inputs[0], b.output, c.inputs[0], c.output};
+        for (auto& pr : g.alias)
+          if (state.count(pr.first) || state.count(pr.second)) {
+            state.insert(pr.first);
+            state.insert(pr.second);
+          }
+        bool clash = false;
+        for (int x = (int)o + 1; x < reader; ++x) {
+          for (int t : g.ops[x].inputs) clash |= state.count(t) > 0;
+          clash |= state.count(g.ops[x].output) > 0;
+        }
+        LOp& La = all[r][o];
+        if (clash || !La.out.direct || La.partial || La.out.dtype != TOFU_F32) continue;
+        La.fused_opt = reader;
+        all[r][reader].skip = true;
+      }
   E.lops.clear();
   for (int r : E.local) E.lops.push_back(all[r]);
 }
@@ -463,7 +501,22 @@ void finalize(Exec& E) {
       G.a.ldc = (int)L.out.buf_box[1].len();
       G.a.c_mode = L.out.dtype == TOFU_BF16 ? 0 : 1;
       (void)d;
-      int rc = tofu_gemm_plan_tmaps(&G.a, &G.ta, &G.tb, &G.bn);
+      if (L.fused_opt >= 0) {
+        const LOp& Lm = E.lops[li][L.fused_opt];      // mom(M, G) -> M_new (in place)
+        const LOp& Ls = E.lops[li][L.fused_opt + 1];  // sgd(W, M_new) -> W_new (in place)
+        auto at = [&](int op, const char* key) {
+          auto it = g.ops[op].attrs.find(key);
+          return (float)(it == g.ops[op].attrs.end() ? 0.0 : it->second);
+        };
+        G.a.c_mode = 3;
+        G.a.C = E.arena[r] + Lm.in[0].off;
+        G.a.ldc = (int)Lm.in[0].buf_box.back().len();
+        G.a.D = E.arena[r] + Ls.in[0].off;
+        G.a.ldd = (int)Ls.in[0].buf_box.back().len();
+        G.a.s0 = at(L.fused_opt, "mu");
+        G.a.s1 = at(L.fused_opt + 1, "lr");
+      }
+      int rc = tofu_gemm_plan_tmaps(&G.a, G.tm, &G.bn);
       if (rc) throw Error(rc, "gemm tensor map for op " + g.ops[o].name + " (pitch/alignment)");
       E.gemms[{(int)o, li}] = G;
     }
@@ -482,7 +535,7 @@ int run_compute(Exec& E, int o, int li, cudaStream_t st) {
   char* base = E.arena[r];
   if (std::string(kernel_kind(dn)) == "gemm") {
     auto& G = E.gemms.at({o, li});
-    return tofu_gemm_launch_planned(&G.a, &G.ta, &G.tb, G.bn, st);
+    return tofu_gemm_launch_planned(&G.a, G.tm, G.bn, st);
   }
   const int64_t n = vol(L.out.box);
   void* y = base + L.out.off;
@@ -577,6 +630,7 @@ extern "C" int tofu_exec_create(const tofu_graph* g, const tofu_plan* p, int n_l
         E.arena.push_back(static_cast<char*>(arena_dev[r]));
       }
       E.multi_process = n_local < E.k;
+      if (const char* f = std::getenv("TOFU_FUSE")) E.fuse = std::string(f) != "0";
       if (E.multi_process) {
         if (!flags_dev) throw tofu::Error(TOFU_ERR_ARG, "flags_dev required when not all ranks are local");
         for (int r = 0; r < E.k; ++r) E.flags.push_back(flags_dev[r]);
@@ -660,7 +714,7 @@ std::string launch_desc(const Exec& E, int i) {
       const double M = (double)lo.out.box[0].len(), N = (double)lo.out.box[1].len();
       const double K = (double)(dn == "mm_tn" ? lo.in[0].box[0].len() : lo.in[0].box[1].len());
       flops = 2 * M * N * K;
-      bytes = 2 * (M * K + K * N) + M * N * (lo.out.dtype == TOFU_BF16 ? 2 : 4);
+      bytes = 2 * (M * K + K * N) + M * N * (lo.fused_opt >= 0 ? (8 + 4) : (lo.out.dtype == TOFU_BF16 ? 2 : 4));
     } else {
       const double n = (double)vol(lo.in[0].box);
       for (size_t k = 0; k < lo.in.size(); ++k) bytes += n * (lo.in[k].dtype == TOFU_BF16 ? 2 : 4);
@@ -671,6 +725,7 @@ std::string launch_desc(const Exec& E, int i) {
   }
   o += ",\"flops\":" + json_num(flops) + ",\"bytes\":" + json_num(bytes);
   if (L.kind == 1 && lo_fused(E, L)) o += ",\"fused\":\"mom+sgd\"";
+  if (L.kind == 1 && E.lops[L.li][L.op].fused_opt >= 0) o += ",\"fused\":\"gemm+mom+sgd\"";
   return o + "}";
 }
 }  // namespace

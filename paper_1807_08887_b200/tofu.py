@@ -25,7 +25,8 @@ class GemmArgs(C.Structure):
                 ("A", C.c_void_p), ("lda", C.c_int), ("a_mn_major", C.c_int),
                 ("B", C.c_void_p), ("ldb", C.c_int), ("b_mn_major", C.c_int),
                 ("C", C.c_void_p), ("ldc", C.c_int), ("c_mode", C.c_int),
-                ("bn", C.c_int), ("max_ctas", C.c_int)]
+                ("bn", C.c_int), ("max_ctas", C.c_int), ("D", C.c_void_p), ("ldd", C.c_int),
+                ("s0", C.c_float), ("s1", C.c_float)]
 
 
 class Piece(C.Structure):
@@ -52,8 +53,8 @@ def lib():
         vp, i64p = C.c_void_p, C.POINTER(C.c_int64)
         sig = {
             "tofu_gemm_bf16": [C.POINTER(GemmArgs), vp],
-            "tofu_gemm_plan_tmaps": [C.POINTER(GemmArgs), vp, vp, C.POINTER(C.c_int)],
-            "tofu_gemm_launch_planned": [C.POINTER(GemmArgs), vp, vp, C.c_int, vp],
+            "tofu_gemm_plan_tmaps": [C.POINTER(GemmArgs), vp, C.POINTER(C.c_int)],
+            "tofu_gemm_launch_planned": [C.POINTER(GemmArgs), vp, C.c_int, vp],
             "tofu_pieces_run": [vp, C.c_int, C.c_int64, vp],
             "tofu_elementwise": [C.c_int, C.c_int64, vp, vp, vp, vp, C.c_float, C.c_float, vp],
             "tofu_describe_op": [C.c_char_p, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
@@ -99,8 +100,10 @@ def _stream(stream):
 
 
 # ----------------------------------------------------------------------------- kernels
-def gemm(A, B, Cout, M, N, K, lda, a_mn, ldb, b_mn, ldc, c_mode, bn=0, max_ctas=0, stream=None):
-    a = GemmArgs(M, N, K, A.data_ptr(), lda, a_mn, B.data_ptr(), ldb, b_mn, Cout.data_ptr(), ldc, c_mode, bn, max_ctas)
+def gemm(A, B, Cout, M, N, K, lda, a_mn, ldb, b_mn, ldc, c_mode, bn=0, max_ctas=0, stream=None, D=None, ldd=0,
+         s0=0.0, s1=0.0):
+    a = GemmArgs(M, N, K, A.data_ptr(), lda, a_mn, B.data_ptr(), ldb, b_mn, Cout.data_ptr(), ldc, c_mode, bn, max_ctas,
+                 D.data_ptr() if D is not None else None, ldd, s0, s1)
     check(lib().tofu_gemm_bf16(C.byref(a), _stream(stream)), "tofu_gemm_bf16")
 
 

@@ -57,7 +57,8 @@ def per_op_check(spec, vals, out):
 
 
 @pytest.mark.parametrize("k", [1, 2, 4, 8])
-def test_mlp_step_per_op_parity(k):
+def test_mlp_step_per_op_parity(k, monkeypatch):
+    monkeypatch.setenv("TOFU_FUSE", "0")   # every op materialised, each checked on its own inputs
     spec = config(0)
     vals = make_values(spec, seed=11)
     R, out = run_gpu(spec, k, vals)
@@ -66,7 +67,8 @@ def test_mlp_step_per_op_parity(k):
 
 
 @pytest.mark.parametrize("k", [1, 8])
-def test_mlp_step_end_to_end(k):
+def test_mlp_step_end_to_end(k, monkeypatch):
+    monkeypatch.setenv("TOFU_FUSE", "0")
     spec = config(0)
     vals = make_values(spec, seed=12)
     _, out = run_gpu(spec, k, vals)
@@ -123,3 +125,26 @@ def test_fc_config_full_size_sampled(k):
     lref = float(np.sum((Y - T) ** 2) / Y.size)
     assert abs(loss - lref) <= 1e-5 * lref
     assert R.ledger() == R.plan.cost()
+
+
+@pytest.mark.parametrize("cfg,k", [(0, 1), (0, 2), (1, 1)])
+def test_fused_optimizer_epilogue(cfg, k):
+    """Fused wgrad -> momentum -> SGD (GEMM epilogue c_mode 3) vs the oracle on
+    the GPU's own X / dY / H: M_new fp32 (1e-5), W_new bf16 (5e-3)."""
+    spec = config(cfg)
+    if cfg == 1:
+        spec = mlp(512, [1024, 2048])
+    vals = make_values(spec, seed=17)
+    R, out = run_gpu(spec, k, vals)
+    descs = [R.exec.launch_desc(i) for i in range(R.exec.num_launches())]
+    assert any(d.get("fused") == "gemm+mom+sgd" for d in descs)
+    L = sum(1 for t in spec["tensors"] if t.startswith("W") and not t.endswith("_new"))
+    for l in range(1, L + 1):
+        hin = "X" if l == 1 else f"H{l-1}"
+        g = "dY" if l == L else f"dZ{l}"
+        hv = vals["X"] if l == 1 else out[hin]
+        grad = hv.T @ out[g]
+        mref = vals[f"M{l}"] * 0.875 + grad
+        e_m = nrm(out[f"M{l}"], mref)
+        e_w = nrm(out[f"W{l}"], store_round(vals[f"W{l}"] - out[f"M{l}"] * 0.0078125, "bf16"))
+        assert e_m <= 1e-5 and e_w <= 5e-3, (l, e_m, e_w)

@@ -42,6 +42,8 @@ def test_gemm_parity(defname, M, N, K, c_mode):
     am, bm = DEF_MAJOR[defname]
     if (am and M % 8) or (bm and N % 8) or (not am and K % 8) or (not bm and K % 8):
         pytest.skip("pitch must be a multiple of 8 elements")
+    if (N * (2 if c_mode == 0 else 4)) % 16:
+        pytest.skip("output pitch must be a multiple of 16 bytes (TMA store)")
     rng = np.random.default_rng(M * 7 + N * 13 + K)
     a_shape = (K, M) if am else (M, K)
     b_shape = (K, N) if bm else (N, K)
@@ -67,6 +69,32 @@ def test_gemm_parity(defname, M, N, K, c_mode):
         assert np.mean(got == round_bf16(ref)) > 0.97
     else:
         assert nrm(got, ref) <= 1e-5
+
+
+@pytest.mark.parametrize("defname", ["mm_tn", "mm_nn"])
+@pytest.mark.parametrize("M,N,K", [(256, 512, 128), (200, 328, 72), (1024, 2048, 512)])
+def test_gemm_fused_momentum_sgd(defname, M, N, K):
+    """c_mode 3: M = M*mu + A.B (fp32, 1e-5), W = bf16(W - lr*M) (5e-3)."""
+    t = _tofu()
+    am, bm = DEF_MAJOR[defname]
+    rng = np.random.default_rng(M + N + K)
+    a_shape = (K, M) if am else (M, K)
+    b_shape = (K, N) if bm else (N, K)
+    A, B = q(rng, a_shape, 2 ** -7), q(rng, b_shape, 2 ** -9)
+    d = parse_def(MM_DEFS[defname])
+    acc = fast_eval(d, {"A": (A, (0, 0)), "B": (B, (0, 0))}, {"i": (0, M - 1), "j": (0, N - 1), "k": (0, K - 1)})
+    M0 = q(rng, (M, N), 2 ** -12)
+    W0 = q(rng, (M, N), 2 ** -7)
+    Md = torch.from_numpy(M0).float().cuda()
+    Wd = cuda_bf16(W0)
+    mu, lr = 0.875, 0.0078125
+    t.gemm(cuda_bf16(A), cuda_bf16(B), Md, M, N, K, a_shape[1], am, b_shape[1], bm, N, 3, D=Wd, ldd=N, s0=mu, s1=lr)
+    torch.cuda.synchronize()
+    mref = M0 * mu + acc
+    got_m = Md.double().cpu().numpy()
+    assert nrm(got_m, mref) <= 1e-5
+    wref = round_bf16(W0 - got_m * lr)
+    assert nrm(Wd.double().cpu().numpy(), wref) <= 5e-3
 
 
 def test_gemm_strided_output_and_bn():
