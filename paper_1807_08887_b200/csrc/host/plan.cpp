@@ -58,16 +58,21 @@ struct VE {
   }
 
   int64_t run(int cap, std::vector<std::vector<int>>& sols) {
+    // min-degree greedy order (ties -> smallest var id), with var -> factor adjacency kept incrementally
     std::vector<Factor> active = factors;
+    std::vector<char> alive(active.size(), 1);
+    const int nv = (int)dsize.size();
+    std::vector<std::set<int>> adj(nv);  // var -> ids of alive factors containing it
+    for (size_t f = 0; f < active.size(); ++f)
+      for (int y : active[f].scope) adj[y].insert((int)f);
     std::set<int> remaining;
-    for (int v = 0; v < (int)dsize.size(); ++v) remaining.insert(v);
+    for (int v = 0; v < nv; ++v) remaining.insert(v);
     while (!remaining.empty()) {
       int bx = -1;
       double bw = 0;
       for (int x : remaining) {
         std::set<int> nb;
-        for (auto& f : active)
-          if (std::find(f.scope.begin(), f.scope.end(), x) != f.scope.end()) nb.insert(f.scope.begin(), f.scope.end());
+        for (int f : adj[x]) nb.insert(active[f].scope.begin(), active[f].scope.end());
         double w = 1;
         for (int y : nb) w *= dsize[y];
         if (bx < 0 || w < bw) {
@@ -76,19 +81,17 @@ struct VE {
         }
       }
       int x = bx;
-      std::vector<Factor> touching, rest;
-      for (auto& f : active)
-        (std::find(f.scope.begin(), f.scope.end(), x) != f.scope.end() ? touching : rest).push_back(f);
+      std::vector<int> tids(adj[x].begin(), adj[x].end());
       std::set<int> sc;
-      for (auto& f : touching) sc.insert(f.scope.begin(), f.scope.end());
+      for (int f : tids) sc.insert(active[f].scope.begin(), active[f].scope.end());
       sc.insert(x);
       std::vector<int> scope(sc.begin(), sc.end());
-      auto st = strides(scope, dsize);
       int64_t n = 1;
       for (int y : scope) n *= dsize[y];
       std::vector<int64_t> comb(n, 0);
       std::vector<int> idx(scope.size());
-      for (auto& f : touching) {
+      for (int fi : tids) {
+        const Factor& f = active[fi];
         auto fst = strides(f.scope, dsize);
         std::vector<int> pos(f.scope.size());
         for (size_t a = 0; a < f.scope.size(); ++a)
@@ -103,7 +106,6 @@ struct VE {
           comb[e] += f.table[off];
         }
       }
-      // message: min over x
       std::vector<int> mscope;
       for (int y : scope)
         if (y != x) mscope.push_back(y);
@@ -124,10 +126,20 @@ struct VE {
         msg[off] = std::min(msg[off], comb[e]);
       }
       trace.push_back({x, scope, std::move(comb)});
-      rest.push_back({mscope, std::move(msg)});
-      active.swap(rest);
+      for (int fi : tids) {
+        alive[fi] = 0;
+        for (int y : active[fi].scope) adj[y].erase(fi);
+      }
+      const int nid = (int)active.size();
+      active.push_back({mscope, std::move(msg)});
+      alive.push_back(1);
+      for (int y : mscope) adj[y].insert(nid);
       remaining.erase(x);
     }
+    std::vector<Factor> rest;
+    for (size_t f = 0; f < active.size(); ++f)
+      if (alive[f]) rest.push_back(std::move(active[f]));
+    active.swap(rest);
     int64_t total = 0;
     for (auto& f : active) total += f.table.at(0);
     // enumerate co-optimal assignments (DFS in reverse elimination order)
@@ -211,7 +223,27 @@ struct StepResult {
   bool truncated;
 };
 
-StepResult step_search(const Graph& g, const PlanSeq& pre, int k, int cap) {
+// Memo of per-op costs: an op's cost depends only on its own split sequence and the dim sequences of its
+// tensors, which repeat across frontier prefixes and across factor-table entries.
+struct CostMemo {
+  std::map<std::vector<int>, int64_t> m;
+  int64_t get(const Graph& g, int o, const PlanSeq& p) {
+    std::vector<int> key;
+    key.push_back(o);
+    for (int f : p.factors) key.push_back(f);
+    for (int v : p.osplit[o]) key.push_back(v);
+    for (int t : g.ops[o].inputs)
+      for (int d : p.tdims[t]) key.push_back(d);
+    for (int d : p.tdims[g.ops[o].output]) key.push_back(d);
+    auto it = m.find(key);
+    if (it != m.end()) return it->second;
+    int64_t c = op_cost(g, o, p).elements;
+    m.emplace(std::move(key), c);
+    return c;
+  }
+};
+
+StepResult step_search(const Graph& g, const PlanSeq& pre, int k, int cap, CostMemo& memo) {
   const int nT = (int)g.classes.size(), nO = (int)g.op_classes.size();
   std::vector<std::vector<int>> dom(nT + nO);
   for (int c = 0; c < nT; ++c) {
@@ -255,7 +287,7 @@ StepResult step_search(const Graph& g, const PlanSeq& pre, int k, int cap) {
           for (int t : g.classes[f.scope[a]]) cur.tdims[t].back() = d;
         }
         cur.osplit[o].back() = v;
-        val += op_cost(g, o, cur).elements;
+        val += memo.get(g, o, cur);
       }
       f.table[e] = val;
     }
@@ -271,8 +303,13 @@ StepResult step_search(const Graph& g, const PlanSeq& pre, int k, int cap) {
     for (size_t o = 0; o < g.ops.size(); ++o) p.osplit[o].back() = dom[nT + g.oclass[o]][s[nT + g.oclass[o]]];
     res.plans.push_back(std::move(p));
   }
-  std::sort(res.plans.begin(), res.plans.end(),
-            [&](const PlanSeq& a, const PlanSeq& b) { return canon_key(g, a) < canon_key(g, b); });
+  std::vector<std::pair<std::vector<int>, size_t>> keyed;
+  for (size_t i = 0; i < res.plans.size(); ++i) keyed.emplace_back(canon_key(g, res.plans[i]), i);
+  std::sort(keyed.begin(), keyed.end());
+  std::vector<PlanSeq> sorted;
+  sorted.reserve(keyed.size());
+  for (auto& kv : keyed) sorted.push_back(std::move(res.plans[kv.second]));
+  res.plans.swap(sorted);
   return res;
 }
 
@@ -290,11 +327,12 @@ PlanResult make_plan(const Graph& g, int k, int frontier_cap, int solution_cap, 
     r.seq = empty;
   } else if (search == 0) {
     std::vector<PlanSeq> frontier = {empty};
+    CostMemo memo;
     for (int ki : factors) {
       int64_t best = INT64_MAX;
       std::vector<PlanSeq> cands;
       for (auto& pre : frontier) {
-        StepResult s = step_search(g, pre, ki, solution_cap);
+        StepResult s = step_search(g, pre, ki, solution_cap, memo);
         r.truncated |= s.truncated;
         if (s.cost < best) {
           best = s.cost;
