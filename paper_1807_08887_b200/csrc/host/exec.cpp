@@ -156,6 +156,7 @@ struct Exec {
   bool skip_comm = false;
   bool multi_process = false;
   bool fuse = true;
+  std::vector<char> remote_fetch, remote_reduce;  // per op, over all ranks
   int timed_launch = -1;
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
 };
@@ -403,6 +404,13 @@ void lower(Exec& E) {
         La.fused_opt = reader;
         all[r][reader].skip = true;
       }
+  E.remote_fetch.assign(g.ops.size(), 0);
+  E.remote_reduce.assign(g.ops.size(), 0);
+  for (int r = 0; r < k; ++r)
+    for (size_t o = 0; o < g.ops.size(); ++o) {
+      for (int s : all[r][o].fetch_src) E.remote_fetch[o] |= s != r;
+      for (int n : all[r][o].reduce_nremote) E.remote_reduce[o] |= n > 0;
+    }
   E.lops.clear();
   for (int r : E.local) E.lops.push_back(all[r]);
 }
@@ -412,15 +420,17 @@ void build_launches(Exec& E) {
   std::vector<tofu_piece> host;
   E.launches.clear();
   const int nl = (int)E.local.size();
-  // multi-process: a device barrier before every phase that reads peer memory (its producers on other
-  // ranks must be done), and one at the end of the step (WAR on shards read by peers).
-  auto need_barrier = [&](int, bool) { return E.multi_process; };
+  // Multi-process synchronisation.  Barrier placement is decided from ALL ranks' lowered pieces (every
+  // process must issue the same barrier sequence).  A phase that reads peer memory (fetch or reduce with a
+  // source on another rank, anywhere) is bracketed by device barriers: the one before makes the peers'
+  // producers visible (RAW); the one after guarantees no rank overwrites a shard or staging buffer a peer
+  // is still reading (WAR; staging is reused op to op).  A final barrier closes the step.
   for (size_t o = 0; o < g.ops.size(); ++o) {
-    // fetch phase
     bool any_fetch = false;
     for (int li = 0; li < nl; ++li) any_fetch |= !E.lops[li][o].fetch.empty();
+    const bool bar_f = E.multi_process && E.remote_fetch[o];
+    if (bar_f) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
     if (any_fetch) {
-      if (need_barrier((int)o, true)) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
       Exec::Launch L{0, (int)o, -1, (int64_t)host.size(), 0, 0};
       for (int li = 0; li < nl; ++li)
         for (auto& pc : E.lops[li][o].fetch) {
@@ -430,6 +440,7 @@ void build_launches(Exec& E) {
       L.npieces = (int64_t)host.size() - L.piece_off;
       E.launches.push_back(L);
     }
+    if (bar_f) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
     for (int li = 0; li < nl; ++li) {
       if (E.lops[li][o].skip) continue;
       if (g.defs[g.ops[o].def].name == "sumsq") E.launches.push_back({4, (int)o, li, 0, 0, 0});
@@ -437,8 +448,9 @@ void build_launches(Exec& E) {
     }
     bool any_red = false;
     for (int li = 0; li < nl; ++li) any_red |= !E.lops[li][o].reduce.empty();
+    const bool bar_r = E.multi_process && E.remote_reduce[o];
+    if (bar_r) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
     if (any_red) {
-      if (need_barrier((int)o, false)) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
       Exec::Launch L{2, (int)o, -1, (int64_t)host.size(), 0, 0};
       for (int li = 0; li < nl; ++li)
         for (auto& pc : E.lops[li][o].reduce) {
@@ -448,6 +460,7 @@ void build_launches(Exec& E) {
       L.npieces = (int64_t)host.size() - L.piece_off;
       E.launches.push_back(L);
     }
+    if (bar_r) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
   }
   if (E.multi_process) E.launches.push_back({3, -1, -1, 0, 0, 0});
   E.host_pieces = std::move(host);

@@ -6,10 +6,10 @@ shards at the offsets libtofu reports, and runs steps through tofu_execute.
 
 * virtual mode (default): all k ranks live on one GPU; peer pointers are
   local pointers and the same MultiFetch / reduce kernels run.
-* multi-process mode (``rank``/``group`` given): one process per GPU; arenas
-  and barrier words are allocated in torch symmetric memory and the peers'
-  mapped addresses are passed to libtofu, whose kernels then read peer HBM
-  over NVLink directly.
+* multi-process mode (``rank``/``group`` given): one process per GPU; each
+  rank's arena (+ barrier words) is exported with CUDA IPC and mapped by its
+  peers; the mapped addresses are passed to libtofu, whose kernels then read
+  peer HBM over NVLink directly.
 """
 from __future__ import annotations
 
@@ -40,19 +40,28 @@ class TofuRunner:
             ptrs = [self._aligned(self.arenas[r]) for r in range(k)]
             self.exec = tofu.Exec(self.graph, self.plan, self.local, ptrs)
         else:
+            # one process per GPU: every rank allocates its own arena (+ 4 KiB of barrier words) and
+            # exports it with CUDA IPC; peers map it (cudaIpcOpenMemHandle, lazy peer access over
+            # NVLink) so libtofu's MultiFetch / reduce kernels load peer HBM directly.
             import torch.distributed as dist
-            import torch.distributed._symmetric_memory as symm
-            nbytes = max(self.plan.arena_bytes(r) for r in range(k)) + 4096
-            buf = symm.empty(nbytes, dtype=torch.uint8, device=self.device)
-            hdl = symm.rendezvous(buf, group if group is not None else dist.group.WORLD)
-            self._symm = (buf, hdl)
+            nbytes = (max(self.plan.arena_bytes(r) for r in range(k)) + 4095) // 4096 * 4096
+            buf = torch.zeros(nbytes + 4096, dtype=torch.uint8, device=self.device)
             self.arenas[rank] = buf
-            # arena at offset 0, barrier word in the last 4 KiB (zeroed before the first step)
-            ptrs = [int(p) for p in hdl.buffer_ptrs]
-            flags = [p + nbytes - 4096 for p in ptrs]
-            buf[nbytes - 4096:].zero_()
             torch.cuda.synchronize()
-            dist.barrier(group)
+            handle = buf.untyped_storage()._share_cuda_()
+            handles = [None] * k
+            dist.all_gather_object(handles, (rank, handle), group=group)
+            self._peer = {}
+            ptrs = [0] * k
+            for r, h in handles:
+                if r == rank:
+                    ptrs[r] = buf.data_ptr()
+                else:
+                    st = torch.UntypedStorage._new_shared_cuda(*h)
+                    self._peer[r] = st
+                    ptrs[r] = st.data_ptr()
+            flags = [p + nbytes for p in ptrs]
+            dist.barrier(group=group)
             self.exec = tofu.Exec(self.graph, self.plan, self.local, ptrs, flags)
         self.shards = {r: {t: self.plan.shard(r, t) for t in spec["tensors"]} for r in range(k)}
 

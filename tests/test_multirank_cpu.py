@@ -1,0 +1,67 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2 and 4): every process
+plans the same graph independently and must get the same plan; each process
+lowers only its own rank, and the device-barrier sequence of every rank must
+be identical (a mismatch deadlocks the NVLink barriers); the byte ledger is
+the same on every rank and equals the plan."""
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cfg, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    from paper_1807_08887_b200 import tofu
+    from tofu_inputs.graphs import config
+    spec = config(cfg)
+    g = tofu.Graph(spec)
+    plan = tofu.Plan(g, world)
+    pj = plan.json()
+    fake = [0x100000000 * (r + 1) for r in range(world)]
+    flags = [0x7f0000000000 + 64 * r for r in range(world)]
+    ex = tofu.Exec(g, plan, [rank], fake, flags)
+    kinds = [ex.launch_desc(i) for i in range(ex.num_launches())]
+    barriers = [(i, d["op"]) for i, d in enumerate(kinds) if d["kind"] == "barrier"]
+    # barrier order relative to ops (indices differ per rank; the op sequence must not)
+    bseq = [d["op"] for d in kinds if d["kind"] == "barrier"]
+    out = [None] * world
+    dist.all_gather_object(out, {"plan": {k: pj[k] for k in ("factors", "tdims", "osplit", "cost", "bytes")},
+                                 "bseq": bseq, "ledger": ex.ledger(), "cost": plan.cost(),
+                                 "arena": plan.arena_bytes(rank)})
+    if rank == 0:
+        q.put(out)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,cfg", [(2, 0), (4, 0), (2, 1)])
+def test_ranks_agree(world, cfg):
+    from paper_1807_08887_b200 import build
+    build.build(verbose=False)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, cfg, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = q.get(timeout=180)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for o in out[1:]:
+        assert o["plan"] == out[0]["plan"]
+        assert o["bseq"] == out[0]["bseq"]
+        assert o["ledger"] == out[0]["ledger"]
+    assert out[0]["ledger"] == out[0]["cost"]
+    assert len(out[0]["bseq"]) >= 1 and out[0]["bseq"][-1] is None   # closing barrier
