@@ -283,21 +283,14 @@ def main():
             v = R.view(r, t)
             if v is not None:
                 h2d += v.numel() * v.element_size()
-    loss_owner = R.view(R.local[0], "loss")
-    loss_host = torch.empty((), dtype=torch.float32).pin_memory()
-    for _ in range(2):
-        R.load(xs); ex.run()
+    batches = lambda s: xs
+    R.train(batches, 2)
     torch.cuda.synchronize()
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(args.steps):
-        R.load(xs)
-        ex.run()
-        if loss_owner is not None:
-            loss_host.copy_(loss_owner, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+    losses = R.train(batches, args.steps, start_event=e0)
     e1.record()
     torch.cuda.synchronize()
     barrier()
@@ -342,6 +335,9 @@ def main():
     t_comp = flops_rank / (pk["bf16_tflops_sustained"] * 1e12)
     t_comm = (plan_b / max(k, 1)) / 770e9 if k > 1 else 0.0
     step_roof = max(t_comp, t_comm)
+    # the optimizer state (weight, gradient, momentum: the paper's 3W) makes the step HBM-bound
+    hbm_rank = sum(x["bytes"] for x in descs if x["kind"] == "compute")
+    t_hbm = hbm_rank / (pk["hbm_gbs"] * 1e9)
 
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
@@ -350,11 +346,16 @@ def main():
         "config": {"workload": CONFIG_NAME[args.config], "global_batch": batch, "parallelism": f"tofu-k{k}",
                    "plan_factors": R.plan_json["factors"], "l2": "inputs larger than L2 (W+M+dW 640 MiB)"},
         "roofline": roof,
-        "step_roofline": {"compute_ms": t_comp * 1e3, "comm_ms": t_comm * 1e3, "frac": step_roof / (ms / 1e3)},
+        "step_roofline": {"compute_ms": t_comp * 1e3, "comm_ms": t_comm * 1e3, "hbm_ms": t_hbm * 1e3,
+                          "frac_compute_vs_nvlink": step_roof / (ms / 1e3),
+                          "frac": max(step_roof, t_hbm) / (ms / 1e3),
+                          "note": "roofline = slower of tensor-peak compute, plan bytes at 770 GB/s NVLink, and "
+                                  "algorithmic HBM bytes of the sub-ops at measured copy bandwidth"},
         "bytes_vs_plan": {"plan_bytes": plan_b, "ledger_bytes": ledger_b, "plan_elements": plan_el,
                           "ledger_elements": ledger_el, "equal": plan_b == ledger_b},
         "e2e": {"value": batch / (e2e_ms / 1e3), "unit": "samples/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": 4},
+                "d2h_bytes_per_step": 4, "api": "TofuRunner.train (H2D of step s+1 overlapped with step s)",
+                "last_loss": float(losses[-1]) if losses.numel() else None},
         "gpu_launches": ex.launches() * args.steps,
         "clocks": clk.summary(),
     }

@@ -117,3 +117,56 @@ class TofuRunner:
 
     def ledger(self):
         return self.exec.ledger()
+
+    def train(self, host_batches, steps: int, result: str = "loss", start_event=None):
+        """End-to-end training loop through the public API: every step copies that step's inputs from
+        pinned host memory into the ranks' shards and reads the step's `result` back to the host.
+        The host->device copy of step s+1 runs on a copy stream while step s computes (double-buffered
+        device staging); the result is read back asynchronously into pinned memory.
+
+        host_batches: callable s -> {name: pinned host tensor (full shape)}.  Returns the pinned host
+        tensor of per-step results (valid after the caller synchronises)."""
+        comp = torch.cuda.current_stream()
+        copy = torch.cuda.Stream()
+        names = list(host_batches(0).keys())
+        slots = [(r, n) for r in self.local for n in names if self.view(r, n) is not None]
+        bufs = [{s: torch.empty_like(self.view(*s)) for s in slots} for _ in range(2)]
+        ready = [torch.cuda.Event() for _ in range(2)]
+        free = [torch.cuda.Event() for _ in range(2)]
+        used = [False, False]
+        res_view = None
+        for r in self.local:
+            res_view = self.view(r, result) if res_view is None else res_view
+        out = torch.empty([steps] + (list(res_view.shape) if res_view is not None else []),
+                          dtype=res_view.dtype if res_view is not None else torch.float32).pin_memory()
+        if start_event is not None:
+            copy.wait_event(start_event)
+        else:
+            copy.wait_stream(comp)
+
+        def issue(s):
+            b = s % 2
+            hb = host_batches(s)
+            with torch.cuda.stream(copy):
+                if used[b]:
+                    copy.wait_event(free[b])
+                for (r, n) in slots:
+                    _, box = self.shards[r][n]
+                    sl = tuple(slice(lo, hi + 1) for lo, hi in box)
+                    bufs[b][(r, n)].copy_(hb[n][sl], non_blocking=True)
+                ready[b].record(copy)
+            used[b] = True
+
+        issue(0)
+        for s in range(steps):
+            b = s % 2
+            if s + 1 < steps:
+                issue(s + 1)
+            comp.wait_event(ready[b])
+            for sl in slots:
+                self.view(*sl).copy_(bufs[b][sl], non_blocking=True)
+            free[b].record(comp)
+            self.step()
+            if res_view is not None:
+                out[s].copy_(res_view, non_blocking=True)
+        return out
