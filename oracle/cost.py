@@ -83,8 +83,8 @@ def iter_box(ranges: dict, var_order, splits_seq, factors, dig):
     return dict(zip(var_order, _box(ext, splits_seq, factors, dig, names=var_order)))
 
 
-def access_hull(aff, ibox):
-    lo = hi = aff.const
+def access_hull(aff, ibox, off=0):
+    lo = hi = aff.const + off
     for v, c in aff.coef:
         a, b = ibox[v]
         lo += min(c * a, c * b)
@@ -117,24 +117,31 @@ def op_cost_box(g, op, tdims, osplit, factors):
     fetch = out = 0
     fetch_b = out_b = 0
     param_t = {p: t for (p, _), t in zip(d.params, op["inputs"])}
+    param_off = {p: off for (p, _), off in zip(d.params, op["offsets"])}
     o_t = op["output"]
     for w in range(nw):
         dig = digits(w, factors)
         ib = iter_box(R, var_order, seq, factors, dig)
-        for acc in d.accesses:
-            t = param_t[acc.tensor]
+        for p_, _ in d.params:
+            # one required region per param: the hull of all its accesses
+            req = None
+            t = param_t[p_]
             shape = g.shape(t)
-            req = []
-            for dim, ix in enumerate(acc.index):
-                req.append((0, shape[dim] - 1) if ix is None else access_hull(ix, ib))
+            for acc in d.accesses:
+                if acc.tensor != p_:
+                    continue
+                r = [(0, shape[dim] - 1) if ix is None else access_hull(ix, ib, param_off[p_][dim])
+                     for dim, ix in enumerate(acc.index)]
+                req = r if req is None else [(min(a[0], b[0]), max(a[1], b[1])) for a, b in zip(req, r)]
+            if req is None:
+                continue
             own = owned_box(shape, tdims[t], factors, dig)
             n_req = _vol(req)
             n_loc = 0 if own is None else _vol(_inter(req, own))
             fetch += n_req - n_loc
             fetch_b += (n_req - n_loc) * ITEMSIZE[g.tensors[t]["dtype"]]
-        oshape = g.shape(o_t)
-        prod = [ib[v] for v in d.out_vars]
-        own = owned_box(oshape, tdims[o_t], factors, dig)
+        prod = [(ib[v][0] + off, ib[v][1] + off) for v, off in zip(d.out_vars, op["out_offset"])]
+        own = owned_box(g.shape(o_t), tdims[o_t], factors, dig)
         n_p = _vol(prod)
         n_loc = 0 if own is None else _vol(_inter(prod, own))
         out += n_p - n_loc
@@ -175,6 +182,7 @@ def op_cost_enum(g, op, tdims, osplit, factors):
     for k in factors:
         nw *= k
     param_t = {p: t for (p, _), t in zip(d.params, op["inputs"])}
+    param_off = {p: off for (p, _), off in zip(d.params, op["offsets"])}
     pts = {w: [] for w in range(nw)}
     for point in itertools.product(*[range(R[v]) for v in vars_]):
         env = dict(zip(vars_, point))
@@ -194,25 +202,30 @@ def op_cost_enum(g, op, tdims, osplit, factors):
     for w in range(nw):
         if not pts[w]:
             continue
-        for acc in d.accesses:
-            t = param_t[acc.tensor]
+        for p_, _ in d.params:
+            t = param_t[p_]
             shape = g.shape(t)
             lo = [None] * len(shape)
             hi = [None] * len(shape)
-            for env in pts[w]:
-                for dim, ix in enumerate(acc.index):
-                    if ix is None:
-                        a, b = 0, shape[dim] - 1
-                    else:
-                        a = b = ix.const + sum(c * env[v] for v, c in ix.coef)
-                    lo[dim] = a if lo[dim] is None else min(lo[dim], a)
-                    hi[dim] = b if hi[dim] is None else max(hi[dim], b)
+            for acc in d.accesses:
+                if acc.tensor != p_:
+                    continue
+                for env in pts[w]:
+                    for dim, ix in enumerate(acc.index):
+                        if ix is None:
+                            a, b = 0, shape[dim] - 1
+                        else:
+                            a = b = ix.const + param_off[p_][dim] + sum(c * env[v] for v, c in ix.coef)
+                        lo[dim] = a if lo[dim] is None else min(lo[dim], a)
+                        hi[dim] = b if hi[dim] is None else max(hi[dim], b)
+            if lo and lo[0] is None:
+                continue
             for idx in itertools.product(*[range(a, b + 1) for a, b in zip(lo, hi)]):
                 if _owner_of(idx, shape, tdims[t], factors) != w:
                     total += 1
         o_t = op["output"]
         oshape = g.shape(o_t)
-        produced = {tuple(env[v] for v in d.out_vars) for env in pts[w]}
+        produced = {tuple(env[v] + off for v, off in zip(d.out_vars, op["out_offset"])) for env in pts[w]}
         for idx in produced:
             if _owner_of(idx, oshape, tdims[o_t], factors) != w:
                 total += 1

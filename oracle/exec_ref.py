@@ -177,11 +177,21 @@ def run_graph(g, values: dict, emulate_storage=True, fast=True):
     env = {t: np.asarray(v, dtype=np.float64) for t, v in values.items()}
     for op in g.ops:
         d = g.opdef(op)
-        ins = {p: (env[t], (0,) * env[t].ndim) for (p, _), t in zip(d.params, op["inputs"])}
+        # an input offset o means the def's index i reads tensor element i + o (output views, §R10)
+        ins = {p: (env[t], tuple(-x for x in off)) for (p, _), t, off in zip(d.params, op["inputs"], op["offsets"])}
         box = full_box(g, op)
         out = (fast_eval if fast else tdl_eval)(d, ins, box)
-        out = np.asarray(out, dtype=np.float64).reshape(g.shape(op["output"]))
+        R = g.ranges[op["name"]]
+        oshape = [R[v] for v in d.out_vars]
+        out = np.asarray(out, dtype=np.float64).reshape(oshape)
         if emulate_storage:
             out = store_round(out, g.tensors[op["output"]]["dtype"])
-        env[op["output"]] = out
+        t = op["output"]
+        if list(oshape) == list(g.shape(t)) and not any(op["out_offset"]):
+            env[t] = out
+        else:
+            full = env.get(t)
+            full = np.zeros(g.shape(t)) if full is None else full.copy()
+            full[tuple(slice(o, o + n) for o, n in zip(op["out_offset"], oshape))] = out
+            env[t] = full
     return env

@@ -50,6 +50,13 @@ class Graph:
         for o in self.ops:
             o.setdefault("merge", None)
             o.setdefault("backward_of", None)
+            # output views (reading §R10): constant per-dim offsets added to an input's access indices
+            # and to the output index, so one op reads / writes a slice (e.g. one timestep) of a tensor
+            offs = o.get("offsets") or [None] * len(o["inputs"])
+            o["offsets"] = [tuple(x) if x else (0,) * len(self.tensors[t]["shape"])
+                            for x, t in zip(offs, o["inputs"])]
+            oo = o.get("out_offset")
+            o["out_offset"] = tuple(oo) if oo else (0,) * len(self.tensors[o["output"]]["shape"])
         self.alias = dict(spec.get("alias", {}))
         self._validate()
         self.ranges = {o["name"]: self._ranges(o) for o in self.ops}
@@ -65,15 +72,22 @@ class Graph:
         return self.defs[op["def"]]
 
     def _ranges(self, op):
+        """Extent of every index var: inferred from the output / input shapes
+        (tdl.var_ranges), overridden by the op's explicit "ranges" (needed when
+        the op reads or writes a view, §R10)."""
         d = self.opdef(op)
         shapes = {p: self.shape(t) for (p, _), t in zip(d.params, op["inputs"])}
-        return var_ranges(d, shapes, self.shape(op["output"]))
+        over = op.get("ranges") or {}
+        oshape = [over.get(v, n) for v, n in zip(d.out_vars, self.shape(op["output"]))]
+        R = var_ranges(d, shapes, oshape)
+        R.update({v: int(n) for v, n in over.items()})
+        return R
 
     def bound(self, op, tensor_param):
         return tensor_param
 
     def _validate(self):
-        produced = set()
+        produced = {}
         for o in self.ops:
             if o["def"] not in self.defs:
                 raise GraphError(f"UnknownOperator {o['def']}")
@@ -87,19 +101,26 @@ class Graph:
                     raise GraphError(f"ShapeMismatch {o['name']}: {t} rank {len(self.shape(t))} != {r}")
             if len(self.shape(o["output"])) != len(d.out_vars):
                 raise GraphError(f"ShapeMismatch {o['name']}: output rank")
-            if o["output"] in produced:
-                raise GraphError(f"tensor {o['output']} produced twice")
-            produced.add(o["output"])
+            R = self._ranges(o)
+            obox = [(off, off + R[v] - 1) for v, off in zip(d.out_vars, o["out_offset"])]
+            for (lo, hi), n in zip(obox, self.shape(o["output"])):
+                if lo < 0 or hi >= n:
+                    raise GraphError(f"ShapeMismatch {o['name']}: output view out of range")
+            for other in produced.get(o["output"], []):
+                if all(a[0] <= b[1] and b[0] <= a[1] for a, b in zip(obox, other)):
+                    raise GraphError(f"tensor {o['output']} produced twice (overlapping views)")
+            produced.setdefault(o["output"], []).append(obox)
             # every access must stay inside its tensor for the full iteration space
-            shapes = {p: self.shape(t) for (p, _), t in zip(d.params, o["inputs"])}
-            R = var_ranges(d, shapes, self.shape(o["output"]))
+            pidx = {p: i for i, (p, _) in enumerate(d.params)}
             for acc in d.accesses:
+                t = o["inputs"][pidx[acc.tensor]]
+                offs = o["offsets"][pidx[acc.tensor]]
                 for dim, ix in enumerate(acc.index):
                     if ix is None:
                         continue
-                    lo = ix.const + sum(min(0, c * (R[v] - 1)) for v, c in ix.coef)
-                    hi = ix.const + sum(max(0, c * (R[v] - 1)) for v, c in ix.coef)
-                    if lo < 0 or hi >= shapes[acc.tensor][dim]:
+                    lo = ix.const + offs[dim] + sum(min(0, c * (R[v] - 1)) for v, c in ix.coef)
+                    hi = ix.const + offs[dim] + sum(max(0, c * (R[v] - 1)) for v, c in ix.coef)
+                    if lo < 0 or hi >= self.shape(t)[dim]:
                         raise GraphError(f"ShapeMismatch {o['name']}: {acc.tensor} dim {dim} accessed [{lo},{hi}]")
 
     # ------------------------------------------------------------------ coarsening
@@ -124,7 +145,8 @@ class Graph:
 
         for o in self.ops:
             d = self.opdef(o)
-            if classify(d)[0] == "ElementWise":
+            if classify(d)[0] == "ElementWise" and not any(any(x) for x in o["offsets"]) \
+                    and not any(o["out_offset"]):
                 for t in o["inputs"]:
                     union(t, o["output"])
         for new, old in self.alias.items():

@@ -150,6 +150,19 @@ class SearchError(Exception):
     pass
 
 
+def _op_cost_cached(g, op, td, osp, factors):
+    """op_cost_box memoised (per graph object) on exactly the arguments it reads: the op, its split
+    sequence, its tensors' dim sequences and the factors — no change to the value."""
+    memo = g.__dict__.setdefault("_cost_memo", {})
+    key = (op["name"], tuple(factors), tuple(osp[op["name"]]),
+           tuple(tuple(td[t]) for t in list(op["inputs"]) + [op["output"]]))
+    v = memo.get(key)
+    if v is None:
+        v = op_cost_box(g, op, td, osp, factors)[0]
+        memo[key] = v
+    return v
+
+
 def step_search(g, prefix, k, cap=256):
     """All co-optimal basic plans for the next step (size-k split) given a
     plan prefix.  Returns (cost_of_prefix_plus_step, [plans]) where plans are
@@ -184,7 +197,7 @@ def step_search(g, prefix, k, cap=256):
                 for t in list(op["inputs"]) + [op["output"]]:
                     td[t] = list(prefix["tdims"][t]) + [choice[tclass[t]]]
                 osp = {name: list(prefix["osplit"][name]) + [v]}
-                val += op_cost_box(g, op, td, osp, factors)[0]
+                val += _op_cost_cached(g, op, td, osp, factors)
             table[idx] = val
         factors_ve.append((scope, table))
     total, sols = _VE(domains, factors_ve).run(cap)

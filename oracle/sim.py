@@ -80,7 +80,7 @@ def simulate(g, plan, values, emulate_storage=False):
                 sp = [(factors[i], dig[i]) for i in range(len(factors)) if seq[i] == v]
                 box[v] = nested_range(R[v], sp)
             ins = {}
-            for (p, _), t in zip(d.params, op["inputs"]):
+            for (p, _), t, poff in zip(d.params, op["inputs"], op["offsets"]):
                 shape = g.shape(t)
                 # required hull of every access to this param
                 lo = [None] * len(shape)
@@ -92,7 +92,7 @@ def simulate(g, plan, values, emulate_storage=False):
                         if ix is None:
                             a, b = 0, shape[dim] - 1
                         else:
-                            corners = [ix.const + sum(c * (box[v][0] if s == 0 else box[v][1])
+                            corners = [ix.const + poff[dim] + sum(c * (box[v][0] if s == 0 else box[v][1])
                                                       for (v, c), s in zip(ix.coef, sel))
                                        for sel in itertools.product((0, 1), repeat=len(ix.coef))]
                             a, b = min(corners), max(corners)
@@ -114,12 +114,22 @@ def simulate(g, plan, values, emulate_storage=False):
                         ledger["sent"][src] += n
                         ledger["recv"][w] += n
                 assert not np.isnan(region).any(), (op["name"], t)
-                ins[p] = (region, tuple(lo))
+                ins[p] = (region, tuple(a - b for a, b in zip(lo, poff)))
             val = fast_eval(d, ins, box)
-            obox = [box[v] for v in d.out_vars]
+            obox = [(box[v][0] + off, box[v][1] + off) for v, off in zip(d.out_vars, op["out_offset"])]
             contrib.append((w, obox, np.asarray(val, dtype=np.float64).reshape(
                 tuple(b - a + 1 for a, b in obox))))
-        # route produced values to owners; owners sum in rank order
+        # route produced values to owners; owners sum in rank order.  Elements outside this op's output
+        # view keep their current value (another op, or the initial value, owns them).
+        cur = np.full(oshape, np.nan)
+        if o_t in local[0]:
+            for w in range(nw):
+                mask = owners[o_t] == w
+                cur[mask] = local[w][o_t][mask]
+        cur = np.where(np.isnan(cur), 0.0, cur)
+        lo_o = [min(c[1][dd][0] for c in contrib) for dd in range(len(oshape))]
+        hi_o = [max(c[1][dd][1] for c in contrib) for dd in range(len(oshape))]
+        view = tuple(slice(a, b + 1) for a, b in zip(lo_o, hi_o))
         acc = np.zeros(oshape)
         for w, obox, val in contrib:
             sl = tuple(slice(a, b + 1) for a, b in obox)
@@ -134,6 +144,11 @@ def simulate(g, plan, values, emulate_storage=False):
                 if c:
                     ledger["sent"][w] += c
                     ledger["recv"][dst] += c
+        if oshape:
+            cur[view] = acc[view]
+        else:
+            cur = acc
+        acc = cur
         if emulate_storage:
             acc = store_round(acc, g.tensors[o_t]["dtype"])
         for w in range(nw):

@@ -22,6 +22,9 @@
 #include "plan.h"
 
 extern "C" int tofu_barrier_run(void* flags_ptrs_dev, int rank, int n, void* stream);
+extern "C" int tofu_lstm_cell(int kind, int64_t nb, int64_t nh, int g0, int ng, const void* const* ptrs,
+                              const int64_t* lds, const int64_t* gss, const int* dts, void* out, int64_t out_ld,
+                              int64_t out_gs, int out_dt, void* stream);
 
 namespace tofu {
 
@@ -163,12 +166,92 @@ struct Exec {
 
 namespace {
 
-const char* kernel_kind(const std::string& def) {
-  if (def == "mm_nn" || def == "matmul" || def == "mm_nt" || def == "mm_tn") return "gemm";
-  if (def == "relu" || def == "relu_grad" || def == "mse_grad" || def == "mom" || def == "sgd" || def == "sumsq")
-    return "ew";
+// A contraction def `reduce(Sum; K..; A[..] * B[..])` whose indices are single variables maps onto the
+// tcgen05 GEMM: output dims = (M vars)(N vars), A = (M)(K) K-major or (K)(M) MN-major, B = (N)(K) K-major
+// or (K)(N) MN-major; multi-variable groups are flattened (e.g. the LSTM gate dims (g, h)).
+struct GemmForm {
+  bool ok = false;
+  int a_param = 0, b_param = 1;
+  int nm = 0, nn = 0, nk = 0;
+  bool a_mn = false, b_mn = false;  // MN-major operands
+  int a_split = 0, b_split = 0;     // number of leading dims in the operand's first group
+};
+
+GemmForm gemm_form(const OpDef& d) {
+  GemmForm f;
+  if (!d.prod2 || d.accesses.size() != 2) return f;
+  auto vars_of = [&](const Access& a, std::vector<int>& out) {
+    for (size_t k = 0; k < a.idx.size(); ++k) {
+      if (a.slice[k] || a.idx[k].coef.size() != 1 || a.idx[k].coef[0].second != 1 || a.idx[k].c != 0) return false;
+      out.push_back(a.idx[k].coef[0].first);
+    }
+    return true;
+  };
+  std::vector<int> av, bv;
+  if (!vars_of(d.accesses[0], av) || !vars_of(d.accesses[1], bv)) return f;
+  std::vector<int> mv, nv, kv;
+  for (int v = 0; v < d.n_out; ++v) {
+    const bool ina = std::find(av.begin(), av.end(), v) != av.end();
+    const bool inb = std::find(bv.begin(), bv.end(), v) != bv.end();
+    if (ina == inb) return f;
+    (ina ? mv : nv).push_back(v);
+  }
+  for (int v = d.n_out; v < (int)d.vars.size(); ++v) kv.push_back(v);
+  // output order must be (M)(N)
+  for (size_t k = 0; k < mv.size(); ++k)
+    if (mv[k] != (int)k) return f;
+  auto cat = [](std::vector<int> a, const std::vector<int>& b) {
+    a.insert(a.end(), b.begin(), b.end());
+    return a;
+  };
+  if (av == cat(mv, kv)) f.a_mn = false;
+  else if (av == cat(kv, mv)) f.a_mn = true;
+  else return f;
+  if (bv == cat(nv, kv)) f.b_mn = false;
+  else if (bv == cat(kv, nv)) f.b_mn = true;
+  else return f;
+  f.a_param = d.accesses[0].param;
+  f.b_param = d.accesses[1].param;
+  f.nm = (int)mv.size();
+  f.nn = (int)nv.size();
+  f.nk = (int)kv.size();
+  f.a_split = f.a_mn ? f.nk : f.nm;
+  f.b_split = f.b_mn ? f.nk : f.nn;
+  f.ok = f.nm > 0 && f.nn > 0 && f.nk > 0;
+  return f;
+}
+
+// View `box` inside the dense row-major buffer `buf` as a 2-D matrix [dims < split][dims >= split]:
+// every dim of a group except its first must be fully covered so rows have a uniform pitch and each row
+// is contiguous.  Outputs rows/cols, the row pitch and the element offset of the box origin.
+bool flat2(const std::vector<Rng>& buf, const std::vector<Rng>& box, int split, int64_t& rows, int64_t& cols,
+           int64_t& ld, int64_t& off) {
+  const int n = (int)buf.size();
+  if (split <= 0 || split >= n) return false;
+  for (int d = 0; d < n; ++d) {
+    if (d == 0 || d == split) continue;
+    if (box[d].lo != buf[d].lo || box[d].hi != buf[d].hi) return false;
+  }
+  rows = cols = ld = 1;
+  for (int d = 0; d < split; ++d) rows *= box[d].len();
+  for (int d = split; d < n; ++d) {
+    cols *= box[d].len();
+    ld *= buf[d].len();
+  }
+  off = offset_in(buf, box);
+  return true;
+}
+
+const char* kernel_kind(const OpDef& d) {
+  static const std::set<std::string> ew = {"relu", "relu_grad", "mse_grad", "mom", "sgd", "mom3", "sgd3", "sumsq"};
+  static const std::set<std::string> lstm = {"cell_c", "cell_h", "cell_bwd_a", "cell_bwd_c"};
+  if (gemm_form(d).ok) return "gemm";
+  if (ew.count(d.name)) return "ew";
+  if (lstm.count(d.name)) return "lstm";
   return nullptr;
 }
+bool is_mom(const std::string& n) { return n == "mom" || n == "mom3"; }
+bool is_sgd(const std::string& n) { return n == "sgd" || n == "sgd3"; }
 
 void lower(Exec& E) {
   const Graph& g = *E.g;
@@ -184,14 +267,15 @@ void lower(Exec& E) {
     for (size_t o = 0; o < g.ops.size(); ++o) {
       const OpDef& d = g.def_of((int)o);
       const OpInfo& oi = g.ops[o];
-      if (!kernel_kind(g.defs[oi.def].name))
-        throw Error(TOFU_ERR_ARG, "no sub-operator kernel for def '" + g.defs[oi.def].name + "'");
+      if (!kernel_kind(d))
+        throw Error(TOFU_ERR_ARG, "no sub-operator kernel for def '" + d.name + "'");
       LOp& L = all[r][o];
       std::vector<Rng> ib;
       iter_box(g, (int)o, p.osplit[o], p.factors, dig, ib);
       for (int v : p.osplit[o])
         if (d.is_red(v)) L.partial = true;
-      const bool is_ew = std::string(kernel_kind(d.name)) == "ew";
+      const std::string kind = kernel_kind(d);
+      const GemmForm gf = gemm_form(d);
       int64_t soff = 0;
       for (size_t pi = 0; pi < d.params.size(); ++pi) {
         int t = oi.inputs[pi];
@@ -200,7 +284,13 @@ void lower(Exec& E) {
         b.dtype = g.tensors[t].dtype;
         const auto& own = E.lay[r].shard_box[t];
         const bool owns = E.lay[r].shard_off[t] >= 0;
-        if (owns && (is_ew ? same(own, b.box) : contains(own, b.box))) {
+        bool usable = owns && (kind == "ew" ? same(own, b.box) : contains(own, b.box));
+        if (usable && kind == "gemm") {
+          int64_t r_, c_, ld_, off_;
+          const int split = (int)pi == gf.a_param ? gf.a_split : gf.b_split;
+          usable = flat2(own, b.box, split, r_, c_, ld_, off_);
+        }
+        if (usable) {
           b.direct = true;
           b.off = E.lay[r].shard_off[t];
           b.buf_box = own;
@@ -213,13 +303,19 @@ void lower(Exec& E) {
         L.in.push_back(b);
       }
       Buf ob;
-      ob.box.assign(ib.begin(), ib.begin() + d.n_out);
+      ob.box = produced_box(g, (int)o, ib);
       const int t = oi.output;
       const bool owns = E.lay[r].shard_off[t] >= 0;
-      if (!L.partial && owns && same(E.lay[r].shard_box[t], ob.box)) {
+      const auto& oown = E.lay[r].shard_box[t];
+      bool odirect = !L.partial && owns && (kind == "ew" ? same(oown, ob.box) : contains(oown, ob.box));
+      if (odirect && kind == "gemm") {
+        int64_t r_, c_, ld_, off_;
+        odirect = flat2(oown, ob.box, gf.nm, r_, c_, ld_, off_);
+      }
+      if (odirect) {
         ob.direct = true;
         ob.off = E.lay[r].shard_off[t];
-        ob.buf_box = ob.box;
+        ob.buf_box = oown;
         ob.dtype = g.tensors[t].dtype;
       } else {
         ob.direct = false;
@@ -358,7 +454,7 @@ void lower(Exec& E) {
   for (int r = 0; r < k; ++r)
     for (size_t o = 0; o + 1 < g.ops.size(); ++o) {
       const OpInfo &a = g.ops[o], &b = g.ops[o + 1];
-      if (g.defs[a.def].name != "mom" || g.defs[b.def].name != "sgd" || b.inputs[1] != a.output) continue;
+      if (!is_mom(g.defs[a.def].name) || !is_sgd(g.defs[b.def].name) || b.inputs[1] != a.output) continue;
       LOp &La = all[r][o], &Lb = all[r][o + 1];
       bool ok = La.out.direct && Lb.out.direct && La.fetch.empty() && Lb.fetch.empty();
       for (auto& x : La.in) ok &= x.direct;
@@ -375,7 +471,7 @@ void lower(Exec& E) {
     for (int r = 0; r < k; ++r)
       for (size_t o = 0; o < g.ops.size(); ++o) {
         const OpInfo& a = g.ops[o];
-        const char* kk = kernel_kind(g.defs[a.def].name);
+        const char* kk = kernel_kind(g.defs[a.def]);
         if (!kk || std::string(kk) != "gemm") continue;
         int reader = -1, readers = 0;
         for (size_t x = 0; x < g.ops.size(); ++x)
@@ -386,7 +482,7 @@ void lower(Exec& E) {
             }
         if (readers != 1 || reader <= (int)o || reader + 1 >= (int)g.ops.size()) continue;
         const OpInfo &b = g.ops[reader], &c = g.ops[reader + 1];
-        if (g.defs[b.def].name != "mom" || !all[r][reader].fused_sgd) continue;
+        if (!is_mom(g.defs[b.def].name) || !all[r][reader].fused_sgd) continue;
         // moving mom+sgd up to the GEMM must not reorder any access to M / W
         std::set<int> state = {b.inputs[0], b.output, c.inputs[0], c.output};
         for (auto& pr : g.alias)
@@ -489,31 +585,32 @@ void finalize(Exec& E) {
   for (int li = 0; li < nl; ++li) {
     const int r = E.local[li];
     for (size_t o = 0; o < g.ops.size(); ++o) {
-      const std::string& dn = g.defs[g.ops[o].def].name;
-      if (std::string(kernel_kind(dn)) != "gemm") continue;
-      LOp& L = E.lops[li][o];
       const OpDef& d = g.def_of((int)o);
-      // vars: i, j (out), k (red) for all three defs
-      const int64_t M = L.out.box[0].len(), N = L.out.box[1].len();
-      const Buf &A = L.in[0], &B = L.in[1];
-      const int64_t K = (dn == "mm_tn") ? A.box[0].len() : A.box[1].len();
+      if (std::string(kernel_kind(d)) != "gemm") continue;
+      LOp& L = E.lops[li][o];
+      if (L.skip) continue;
+      const GemmForm gf = gemm_form(d);
+      const Buf &A = L.in[gf.a_param], &B = L.in[gf.b_param];
+      int64_t ar, ac, lda, aoff, br, bc, ldb, boff, cr, cc, ldc, coff;
+      if (!flat2(A.buf_box, A.box, gf.a_split, ar, ac, lda, aoff) ||
+          !flat2(B.buf_box, B.box, gf.b_split, br, bc, ldb, boff) ||
+          !flat2(L.out.buf_box, L.out.box, gf.nm, cr, cc, ldc, coff))
+        throw Error(TOFU_ERR_ARG, "GEMM operand of op " + g.ops[o].name + " is not a 2-D view");
       Exec::GemmLaunch G;
       std::memset(&G.a, 0, sizeof G.a);
-      G.a.M = (int)M;
-      G.a.N = (int)N;
-      G.a.K = (int)K;
-      const int64_t ea = 2;
-      G.a.A = E.arena[r] + A.off + offset_in(A.buf_box, A.box) * ea;
-      G.a.lda = (int)A.buf_box[1].len();
-      G.a.a_mn_major = dn == "mm_tn" ? 1 : 0;
-      G.a.B = E.arena[r] + B.off + offset_in(B.buf_box, B.box) * ea;
-      G.a.ldb = (int)B.buf_box[1].len();
-      G.a.b_mn_major = (dn == "mm_nt") ? 0 : 1;
+      G.a.M = (int)cr;
+      G.a.N = (int)cc;
+      G.a.K = (int)(gf.a_mn ? ar : ac);
+      G.a.A = E.arena[r] + A.off + aoff * 2;
+      G.a.lda = (int)lda;
+      G.a.a_mn_major = gf.a_mn ? 1 : 0;
+      G.a.B = E.arena[r] + B.off + boff * 2;
+      G.a.ldb = (int)ldb;
+      G.a.b_mn_major = gf.b_mn ? 1 : 0;
       const int64_t ec = L.out.dtype == TOFU_BF16 ? 2 : 4;
-      G.a.C = E.arena[r] + L.out.off + offset_in(L.out.buf_box, L.out.box) * ec;
-      G.a.ldc = (int)L.out.buf_box[1].len();
+      G.a.C = E.arena[r] + L.out.off + coff * ec;
+      G.a.ldc = (int)ldc;
       G.a.c_mode = L.out.dtype == TOFU_BF16 ? 0 : 1;
-      (void)d;
       if (L.fused_opt >= 0) {
         const LOp& Lm = E.lops[li][L.fused_opt];      // mom(M, G) -> M_new (in place)
         const LOp& Ls = E.lops[li][L.fused_opt + 1];  // sgd(W, M_new) -> W_new (in place)
@@ -521,11 +618,15 @@ void finalize(Exec& E) {
           auto it = g.ops[op].attrs.find(key);
           return (float)(it == g.ops[op].attrs.end() ? 0.0 : it->second);
         };
+        int64_t mr, mc, ldm, moff, wr, wc, ldw, woff;
+        if (!flat2(Lm.in[0].buf_box, Lm.in[0].box, gf.nm, mr, mc, ldm, moff) ||
+            !flat2(Ls.in[0].buf_box, Ls.in[0].box, gf.nm, wr, wc, ldw, woff) || mr != cr || mc != cc)
+          throw Error(TOFU_ERR_ARG, "fused optimizer operands of op " + g.ops[o].name + " do not match the GEMM");
         G.a.c_mode = 3;
-        G.a.C = E.arena[r] + Lm.in[0].off;
-        G.a.ldc = (int)Lm.in[0].buf_box.back().len();
-        G.a.D = E.arena[r] + Ls.in[0].off;
-        G.a.ldd = (int)Ls.in[0].buf_box.back().len();
+        G.a.C = E.arena[r] + Lm.in[0].off + moff * 4;
+        G.a.ldc = (int)ldm;
+        G.a.D = E.arena[r] + Ls.in[0].off + woff * 2;
+        G.a.ldd = (int)ldw;
         G.a.s0 = at(L.fused_opt, "mu");
         G.a.s1 = at(L.fused_opt + 1, "lr");
       }
@@ -545,10 +646,40 @@ int run_compute(Exec& E, int o, int li, cudaStream_t st) {
   LOp& L = E.lops[li][o];
   const OpInfo& oi = g.ops[o];
   const std::string& dn = g.defs[oi.def].name;
+  const OpDef& d = g.defs[oi.def];
   char* base = E.arena[r];
-  if (std::string(kernel_kind(dn)) == "gemm") {
+  const std::string kind = kernel_kind(d);
+  if (kind == "gemm") {
     auto& G = E.gemms.at({o, li});
     return tofu_gemm_launch_planned(&G.a, G.tm, G.bn, st);
+  }
+  if (kind == "lstm") {
+    // operand slots of the cell kernel: gx, gh, cp, c, du, dr, dn
+    static const std::map<std::string, std::vector<int>> slots = {
+        {"cell_c", {0, 1, 2}}, {"cell_h", {0, 1, 3}}, {"cell_bwd_a", {0, 1, 2, 3, 4, 5, 6}},
+        {"cell_bwd_c", {0, 1, 3, 4, 5, 6}}};
+    const void* ptrs[7] = {};
+    int64_t lds[7] = {}, gss[7] = {};
+    int dts[7] = {};
+    const auto& sl = slots.at(dn);
+    for (size_t pi = 0; pi < sl.size(); ++pi) {
+      const Buf& b = L.in[pi];
+      auto st_ = strides_of(b.buf_box);
+      const int64_t es = b.dtype == TOFU_BF16 ? 2 : 4;
+      ptrs[sl[pi]] = base + b.off + offset_in(b.buf_box, b.box) * es;
+      lds[sl[pi]] = st_[0];
+      gss[sl[pi]] = b.buf_box.size() == 3 ? st_[1] : 0;
+      dts[sl[pi]] = b.dtype;
+    }
+    const Buf& ob = L.out;
+    auto ost = strides_of(ob.buf_box);
+    const int64_t oes = ob.dtype == TOFU_BF16 ? 2 : 4;
+    const int64_t nb = ob.box[0].len(), nh = ob.box.back().len();
+    const int g0 = ob.box.size() == 3 ? (int)ob.box[1].lo : 0, ng = ob.box.size() == 3 ? (int)ob.box[1].len() : 0;
+    static const std::map<std::string, int> kinds = {{"cell_c", 0}, {"cell_h", 1}, {"cell_bwd_a", 2}, {"cell_bwd_c", 3}};
+    return tofu_lstm_cell(kinds.at(dn), nb, nh, g0, ng, ptrs, lds, gss, dts,
+                          base + ob.off + offset_in(ob.buf_box, ob.box) * oes, ost[0],
+                          ob.box.size() == 3 ? ost[1] : 0, ob.dtype, st);
   }
   const int64_t n = vol(L.out.box);
   void* y = base + L.out.off;
@@ -565,7 +696,7 @@ int run_compute(Exec& E, int o, int li, cudaStream_t st) {
     const int64_t m = vol(L.in[0].box);
     return tofu_elementwise(TOFU_EW_SUMSQ, m, y, x0, x1, nullptr, attr("scale", 1), 0, st);
   }
-  if (dn == "mom") {
+  if (is_mom(dn)) {
     if (L.fused_sgd) {
       const OpInfo& nx = g.ops[o + 1];
       LOp& Ln = E.lops[li][o + 1];
@@ -576,7 +707,7 @@ int run_compute(Exec& E, int o, int li, cudaStream_t st) {
     }
     return tofu_elementwise(TOFU_EW_MOM, n, y, x0, x1, nullptr, attr("mu", 0), 0, st);
   }
-  if (dn == "sgd") return tofu_elementwise(TOFU_EW_SGD, n, y, x0, x1, nullptr, attr("lr", 0), 0, st);
+  if (is_sgd(dn)) return tofu_elementwise(TOFU_EW_SGD, n, y, x0, x1, nullptr, attr("lr", 0), 0, st);
   return TOFU_ERR_ARG;
 }
 
@@ -723,11 +854,16 @@ std::string launch_desc(const Exec& E, int i) {
   } else if (L.kind == 1) {
     const LOp& lo = E.lops[L.li][L.op];
     const std::string& dn = g.defs[g.ops[L.op].def].name;
-    if (std::string(kernel_kind(dn)) == "gemm") {
-      const double M = (double)lo.out.box[0].len(), N = (double)lo.out.box[1].len();
-      const double K = (double)(dn == "mm_tn" ? lo.in[0].box[0].len() : lo.in[0].box[1].len());
+    const OpDef& dd = g.defs[g.ops[L.op].def];
+    if (std::string(kernel_kind(dd)) == "gemm") {
+      const GemmForm gf = gemm_form(dd);
+      double M = 1, N = 1, K = 1;
+      for (int v = 0; v < dd.n_out; ++v) (v < gf.nm ? M : N) *= (double)lo.out.box[v].len();
+      const auto& ab = lo.in[gf.a_param].box;
+      for (int q = 0; q < gf.nk; ++q) K *= (double)ab[gf.a_mn ? q : gf.nm + q].len();
       flops = 2 * M * N * K;
       bytes = 2 * (M * K + K * N) + M * N * (lo.fused_opt >= 0 ? (8 + 4) : (lo.out.dtype == TOFU_BF16 ? 2 : 4));
+      (void)dn;
     } else {
       const double n = (double)vol(lo.in[0].box);
       for (size_t k = 0; k < lo.in.size(); ++k) bytes += n * (lo.in[k].dtype == TOFU_BF16 ? 2 : 4);

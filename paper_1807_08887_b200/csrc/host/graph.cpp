@@ -47,7 +47,7 @@ Graph graph_from_json(const std::string& text) {
     if (it == g.tensor_ix.end()) throw Error(TOFU_ERR_PARSE, "unknown tensor " + n);
     return it->second;
   };
-  std::set<int> produced;
+  std::map<int, std::vector<std::vector<Rng>>> produced;
   for (auto& o : j.at("ops").arr) {
     OpInfo oi;
     oi.name = o.at("name").as_str();
@@ -61,22 +61,55 @@ Graph graph_from_json(const std::string& text) {
     for (size_t p = 0; p < oi.inputs.size(); ++p)
       if ((int)g.tensors[oi.inputs[p]].shape.size() != d.ranks[p])
         throw Error(TOFU_ERR_PARSE, "ShapeMismatch " + oi.name + ": rank of " + g.tensors[oi.inputs[p]].name);
-    if ((int)g.tensors[oi.output].shape.size() != d.n_out)
-      throw Error(TOFU_ERR_PARSE, "ShapeMismatch " + oi.name + ": output rank");
-    if (!produced.insert(oi.output).second)
-      throw Error(TOFU_ERR_PARSE, "tensor " + g.tensors[oi.output].name + " produced twice");
+    const auto& oshape = g.tensors[oi.output].shape;
+    if ((int)oshape.size() != d.n_out) throw Error(TOFU_ERR_PARSE, "ShapeMismatch " + oi.name + ": output rank");
     if (auto* m = o.get("merge"); m && !m->is_null()) oi.merge = m->kind == Json::Str ? m->str : json_num(m->num);
     if (auto* a = o.get("attrs"); a && a->kind == Json::Obj)
       for (auto& kv : a->obj)
         if (kv.second.kind == Json::Num) oi.attrs[kv.first] = kv.second.num;
+    // offsets
+    oi.in_off.resize(oi.inputs.size());
+    const Json* offs = o.get("offsets");
+    for (size_t p = 0; p < oi.inputs.size(); ++p) {
+      oi.in_off[p].assign(g.tensors[oi.inputs[p]].shape.size(), 0);
+      if (offs && offs->kind == Json::Arr && p < offs->arr.size() && offs->arr[p].kind == Json::Arr)
+        for (size_t dd = 0; dd < offs->arr[p].arr.size() && dd < oi.in_off[p].size(); ++dd)
+          oi.in_off[p][dd] = offs->arr[p].arr[dd].as_int();
+    }
+    oi.out_off.assign(oshape.size(), 0);
+    if (auto* oo = o.get("out_offset"); oo && oo->kind == Json::Arr)
+      for (size_t dd = 0; dd < oo->arr.size() && dd < oi.out_off.size(); ++dd) oi.out_off[dd] = oo->arr[dd].as_int();
     std::vector<std::vector<int64_t>> ins;
     for (int t : oi.inputs) ins.push_back(g.tensors[t].shape);
-    oi.R = var_extents(d, ins, g.tensors[oi.output].shape);
+    // var extents: inferred from shapes, overridden by explicit "ranges" (views)
+    std::map<std::string, int64_t> over;
+    if (auto* rg = o.get("ranges"); rg && rg->kind == Json::Obj)
+      for (auto& kv : rg->obj) over[kv.first] = kv.second.as_int();
+    std::vector<int64_t> oshape_it(oshape);
+    for (int v = 0; v < d.n_out; ++v)
+      if (over.count(d.vars[v])) oshape_it[v] = over[d.vars[v]];
+    oi.R = var_extents(d, ins, oshape_it);
+    for (size_t v = 0; v < d.vars.size(); ++v)
+      if (over.count(d.vars[v])) oi.R[v] = over[d.vars[v]];
+    // output view inside the tensor and disjoint from other producers' views
+    std::vector<Rng> obox;
+    for (int v = 0; v < d.n_out; ++v) {
+      obox.push_back({oi.out_off[v], oi.out_off[v] + oi.R[v] - 1});
+      if (obox.back().lo < 0 || obox.back().hi >= oshape[v])
+        throw Error(TOFU_ERR_PARSE, "ShapeMismatch " + oi.name + ": output view out of range");
+    }
+    for (auto& other : produced[oi.output]) {
+      bool overlap = true;
+      for (size_t dd = 0; dd < obox.size(); ++dd)
+        overlap &= obox[dd].lo <= other[dd].hi && other[dd].lo <= obox[dd].hi;
+      if (overlap) throw Error(TOFU_ERR_PARSE, "tensor " + g.tensors[oi.output].name + " produced twice");
+    }
+    produced[oi.output].push_back(obox);
     // every access must stay inside its tensor over the full iteration space
     for (auto& a : d.accesses)
       for (size_t dim = 0; dim < a.idx.size(); ++dim) {
         if (a.slice[dim]) continue;
-        int64_t lo = a.idx[dim].c, hi = a.idx[dim].c;
+        int64_t lo = a.idx[dim].c + oi.in_off[a.param][dim], hi = lo;
         for (auto& kv : a.idx[dim].coef) {
           int64_t x = kv.second * (oi.R[kv.first] - 1);
           lo += std::min<int64_t>(0, x);
@@ -108,7 +141,7 @@ Graph graph_from_json(const std::string& text) {
     }
   };
   for (auto& o : g.ops)
-    if (g.defs[o.def].cls == "ElementWise")
+    if (g.defs[o.def].cls == "ElementWise" && !o.has_offsets())
       for (int t : o.inputs) unite(t, o.output);
   for (auto& pr : g.alias) unite(pr.first, pr.second);
   std::map<std::string, std::vector<int>> bykey;
@@ -222,7 +255,7 @@ std::vector<Rng> required_box(const Graph& g, int op, int param, const std::vect
         lo = 0;
         hi = shape[dim] - 1;
       } else {
-        lo = hi = a.idx[dim].c;
+        lo = hi = a.idx[dim].c + g.ops[op].in_off[param][dim];
         for (auto& kv : a.idx[dim].coef) {
           int64_t x = kv.second * ib[kv.first].lo, y = kv.second * ib[kv.first].hi;
           lo += std::min(x, y);
@@ -234,6 +267,13 @@ std::vector<Rng> required_box(const Graph& g, int op, int param, const std::vect
     }
   }
   return req;
+}
+
+std::vector<Rng> produced_box(const Graph& g, int op, const std::vector<Rng>& ib) {
+  const OpDef& d = g.def_of(op);
+  std::vector<Rng> b;
+  for (int v = 0; v < d.n_out; ++v) b.push_back({ib[v].lo + g.ops[op].out_off[v], ib[v].hi + g.ops[op].out_off[v]});
+  return b;
 }
 
 static int64_t vol(const std::vector<Rng>& b) {
@@ -273,7 +313,7 @@ OpCost op_cost(const Graph& g, int op, const PlanSeq& p) {
       c.fetch += n - loc;
       c.bytes += (n - loc) * g.itemsize(t);
     }
-    prod.assign(ib.begin(), ib.begin() + d.n_out);
+    prod = produced_box(g, op, ib);
     int64_t n = vol(prod);
     int64_t loc = owned_box(g, o.output, p.tdims[o.output], p.factors, dig, own) ? inter_vol(prod, own) : 0;
     c.out += n - loc;

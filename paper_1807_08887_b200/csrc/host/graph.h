@@ -26,6 +26,18 @@ struct OpInfo {
   std::string merge;
   std::map<std::string, double> attrs;
   std::vector<int64_t> R;  // extent of every def var
+  // output views: constant offsets added to each input's access indices and to the
+  // output index, so an op reads / writes a slice (e.g. one timestep) of a tensor
+  std::vector<std::vector<int64_t>> in_off;  // [param][dim]
+  std::vector<int64_t> out_off;              // [dim]
+  bool has_offsets() const {
+    for (auto& v : in_off)
+      for (auto x : v)
+        if (x) return true;
+    for (auto x : out_off)
+      if (x) return true;
+    return false;
+  }
 };
 
 struct Graph {
@@ -67,8 +79,10 @@ bool owned_box(const Graph& g, int t, const std::vector<int>& tdims, const std::
                const std::vector<int>& dig, std::vector<Rng>& box);
 void iter_box(const Graph& g, int op, const std::vector<int>& oseq, const std::vector<int>& factors,
               const std::vector<int>& dig, std::vector<Rng>& box);
-// Required hull of every access of input param p over an iteration box.
+// Required hull of every access of input param p over an iteration box (input offsets applied).
 std::vector<Rng> required_box(const Graph& g, int op, int param, const std::vector<Rng>& ibox);
+// Produced output box of an iteration box (output offset applied).
+std::vector<Rng> produced_box(const Graph& g, int op, const std::vector<Rng>& ibox);
 
 struct OpCost {
   int64_t elements = 0, bytes = 0, fetch = 0, out = 0;

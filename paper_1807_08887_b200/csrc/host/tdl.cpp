@@ -273,8 +273,24 @@ struct Parser {
         if (accept(";")) break;
         expect(",");
       }
+      const size_t body0 = i;
       expr();
+      const size_t body1 = i;
       expect(")");
+      // contraction form: ID [ ... ] * ID [ ... ] at bracket depth 0 with nothing else
+      if (d.reducer == "Sum" && d.accesses.size() == 2) {
+        int depth = 0, stars = 0, others = 0;
+        for (size_t q = body0; q < body1; ++q) {
+          const std::string& x = t[q].s;
+          if (x == "[") ++depth;
+          else if (x == "]") --depth;
+          else if (depth == 0 && t[q].kind == 2) {
+            if (x == "*") ++stars;
+            else ++others;
+          } else if (depth == 0 && t[q].kind == 0) ++others;
+        }
+        d.prod2 = stars == 1 && others == 0 && t[body0].kind == 1 && d.accesses[0].param != d.accesses[1].param;
+      }
     } else if (peek().s == "opaque") {
       ++i;
       expect("(");

@@ -31,6 +31,7 @@ struct OpDef {
   std::vector<int> opaque_free;   // pass-through batch vars of an opaque op
   std::vector<Access> accesses;
   std::string cls;                // ElementWise | Reduction | OpaqueBatched | General
+  bool prod2 = false;             // body is exactly `reduce(Sum; ..; A[..] * B[..])` (a contraction)
 
   int n_red() const { return (int)vars.size() - n_out; }
   bool is_red(int v) const { return v >= n_out; }

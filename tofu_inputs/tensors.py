@@ -10,6 +10,7 @@ operands without any rounding code.  Recipes:
   state  M : q * 2^-17                    (non-zero so momentum is exercised)
   mode="int": all of the above replaced by q ~ U{-3..3} (exact fp64 sums,
               used for partitioned-vs-unpartitioned equality tests)
+  tensors with "init": "zeros" (initial recurrent state, zero gradients) are zero
 """
 from __future__ import annotations
 
@@ -30,6 +31,9 @@ def make_values(graph: dict, seed: int = 0, mode: str = "float") -> dict:
         role = t["role"]
         shape = tuple(t["shape"])
         if role not in ("input", "weight", "state") or name in graph.get("alias", {}):
+            continue
+        if t.get("init") == "zeros":
+            out[name] = np.zeros(shape)
             continue
         if mode == "int":
             out[name] = _q(rng, shape, -3, 3)
