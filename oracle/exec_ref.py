@@ -4,8 +4,8 @@
   tensor value at each index" is the lambda body; a reducer "aggregate[s]
   elements ... along one or more dimensions") over an iteration
   box, vectorised with numpy broadcasting, in fp64.
-* ``fast_eval`` is the same for the matmul defs via a library matmul
-  (allowed as a single step); pinned equal to ``tdl_eval``.
+* ``fast_eval`` is the same for contraction defs (A[..] * B[..] summed) via
+  one library einsum (allowed as a single step); pinned equal to ``tdl_eval``.
 * ``run_graph`` executes a training graph op by op in list order and, when
   ``emulate_storage`` is set, rounds every stored tensor to its storage dtype
   (bf16 by round-to-nearest-even from fp64, fp32 by cast) — the points where
@@ -143,26 +143,40 @@ _MM = {
 }
 
 
+def _contraction(opdef):
+    """(A access, B access) when the body is exactly reduce(Sum; ..; A[..] * B[..]) with single-variable
+    indices, else None."""
+    b = opdef.body
+    if opdef.reducer != "Sum" or b.kind != "bin" or b.val != "*":
+        return None
+    x, y = b.args
+    if x.kind != "access" or y.kind != "access":
+        return None
+    for acc in (x.val, y.val):
+        for ix in acc.index:
+            if ix is None or len(ix.coef) != 1 or ix.coef[0][1] != 1 or ix.const != 0:
+                return None
+    return x.val, y.val
+
+
 def fast_eval(opdef, inputs: dict, box: dict):
-    """Library-matmul evaluation for the three matmul defs over a box; falls
-    back to tdl_eval otherwise."""
-    name = opdef.name
-    if name in _MM and len(opdef.out_vars) == 2 and len(opdef.red_vars) == 1:
-        i, j = opdef.out_vars
-        k = opdef.red_vars[0]
-        (A, oa), (B, ob) = inputs[opdef.params[0][0]], inputs[opdef.params[1][0]]
-        (i0, i1), (j0, j1), (k0, k1) = box[i], box[j], box[k]
-        if name == "mm_nn":
-            a = A[i0 - oa[0]:i1 - oa[0] + 1, k0 - oa[1]:k1 - oa[1] + 1]
-            b = B[k0 - ob[0]:k1 - ob[0] + 1, j0 - ob[1]:j1 - ob[1] + 1]
-        elif name == "mm_nt":
-            a = A[i0 - oa[0]:i1 - oa[0] + 1, k0 - oa[1]:k1 - oa[1] + 1]
-            b = B[j0 - ob[0]:j1 - ob[0] + 1, k0 - ob[1]:k1 - ob[1] + 1]
-        else:
-            a = A[k0 - oa[0]:k1 - oa[0] + 1, i0 - oa[1]:i1 - oa[1] + 1]
-            b = B[k0 - ob[0]:k1 - ob[0] + 1, j0 - ob[1]:j1 - ob[1] + 1]
-        return _MM[name](np.asarray(a, np.float64), np.asarray(b, np.float64))
-    return tdl_eval(opdef, inputs, box)
+    """Library evaluation (numpy einsum -> BLAS) of contraction defs over a box — one library primitive
+    for the whole sum, as the TDL text states it; anything else goes to tdl_eval."""
+    con = _contraction(opdef)
+    if con is None:
+        return tdl_eval(opdef, inputs, box)
+    letters = {v: chr(ord("a") + i) for i, v in enumerate(opdef.all_vars())}
+    ops, subs = [], []
+    for acc in con:
+        arr, origin = inputs[acc.tensor]
+        sl = []
+        for d, ix in enumerate(acc.index):
+            v = ix.coef[0][0]
+            sl.append(slice(box[v][0] - origin[d], box[v][1] - origin[d] + 1))
+        ops.append(np.asarray(arr[tuple(sl)], dtype=np.float64))
+        subs.append("".join(letters[ix.coef[0][0]] for ix in acc.index))
+    out = "".join(letters[v] for v in opdef.out_vars)
+    return np.einsum(f"{subs[0]},{subs[1]}->{out}", ops[0], ops[1], optimize=True)
 
 
 def full_box(g, op):

@@ -666,7 +666,10 @@ int run_compute(Exec& E, int o, int li, cudaStream_t st) {
       const Buf& b = L.in[pi];
       auto st_ = strides_of(b.buf_box);
       const int64_t es = b.dtype == TOFU_BF16 ? 2 : 4;
-      ptrs[sl[pi]] = base + b.off + offset_in(b.buf_box, b.box) * es;
+      // the kernel addresses gates by absolute index x (p[b*ld + x*gs + h]); the required box may start at
+      // a later gate (e.g. cell_h reads only gate 3), so point at gate 0 of the box row
+      const int64_t g_lo = b.buf_box.size() == 3 ? b.box[1].lo : 0;
+      ptrs[sl[pi]] = base + b.off + (offset_in(b.buf_box, b.box) - (b.buf_box.size() == 3 ? g_lo * st_[1] : 0)) * es;
       lds[sl[pi]] = st_[0];
       gss[sl[pi]] = b.buf_box.size() == 3 ? st_[1] : 0;
       dts[sl[pi]] = b.dtype;

@@ -81,7 +81,7 @@ def test_lstm_partitioned_matches_unpartitioned():
     e = abs(o1["loss"] - ref["loss"]) / abs(ref["loss"])
     for k in (2, 4, 8):
         _, ok = _run(spec, k, vals, steps=2)
-        for t in ("L1.Wx", "L1.Wh", "L2.Wx", "L2.MX", "loss"):
+        for t in ("L1.Wx", "L1.Wh", "L2.Wx", "L2.Mx", "loss"):
             err = nrm(ok[t], o1[t]) if np.ndim(o1[t]) else abs(ok[t] - o1[t]) / abs(o1[t])
             assert err <= 5e-3, (k, t, err)
 
@@ -91,7 +91,7 @@ def test_lstm_fused_optimizer_runs():
     vals = _scale_weights(make_values(spec, seed=9))
     R, out = _run(spec, 1, vals)
     descs = [R.exec.launch_desc(i) for i in range(R.exec.num_launches())]
-    assert sum(d.get("fused") == "gemm+mom+sgd" for d in descs) == 4
+    assert sum(d.get("fused") == "gemm+mom+sgd" for d in descs) == 4   # every weight gradient of both layers
     ref = run_graph(OGraph(spec), vals, emulate_storage=True)
-    for t in ("L1.Wx", "L2.Wh", "L1.MX", "L2.MH"):
+    for t in ("L1.Wx", "L2.Wh", "L1.Mx", "L2.Mh"):
         assert nrm(out[t], ref[t]) <= 2e-2, t

@@ -38,6 +38,56 @@ def test_fast_matmul_equals_tdl_interpreter(name):
     assert np.array_equal(fast_eval(d, ins, box), tdl_eval(d, ins, box))
 
 
+@pytest.mark.parametrize("name,shapes,box", [
+    ("gate", ([6, 5], [5, 4, 3]), {"b": (1, 4), "g": (0, 3), "h": (1, 2), "k": (0, 4)}),
+    ("mm_rec", ([6, 4, 3], [5, 4, 3]), {"b": (0, 5), "k": (2, 4), "g": (1, 3), "h": (0, 2)}),
+    ("gate_wgrad", ([6, 5], [6, 4, 3]), {"k": (0, 4), "g": (0, 3), "h": (0, 2), "b": (2, 5)}),
+])
+def test_fast_contractions_equal_tdl_interpreter(name, shapes, box):
+    from tofu_inputs.graphs import LSTM_DEFS
+    d = parse_def(LSTM_DEFS[name])
+    rng = np.random.default_rng(3)
+    A, B = (rng.integers(-4, 5, s).astype(float) for s in shapes)
+    ins = {d.params[0][0]: (A, (0,) * A.ndim), d.params[1][0]: (B, (0,) * B.ndim)}
+    assert np.array_equal(fast_eval(d, ins, box), tdl_eval(d, ins, box))
+
+
+def test_lstm_graph_backward_is_the_gradient():
+    """The LSTM cell backward defs (tofu_inputs.graphs.lstm) are the gradient
+    of the loss: central finite differences on every weight tensor, fp64."""
+    from tofu_inputs.graphs import lstm
+    spec = lstm(2, 4, 3, 2)
+    g = Graph(spec)
+    vals = make_values(spec, seed=3)
+    for n in vals:
+        if n.endswith("Wx") or n.endswith("Wh"):
+            vals[n] = vals[n] * 8
+    env = run_graph(g, vals, emulate_storage=False, fast=False)
+    h = 1e-6
+    rng = np.random.default_rng(0)
+    for w in ("L1.Wx", "L1.Wh", "L2.Wx", "L2.Wh"):
+        for _ in range(4):
+            idx = tuple(rng.integers(0, s) for s in vals[w].shape)
+            vp = dict(vals); vp[w] = vals[w].copy(); vp[w][idx] += h
+            vm = dict(vals); vm[w] = vals[w].copy(); vm[w][idx] -= h
+            fd = (run_graph(g, vp, emulate_storage=False)["loss"] - run_graph(g, vm, emulate_storage=False)["loss"]) / (2 * h)
+            gd = env[w.replace(".W", ".dW")][idx]
+            assert abs(fd - gd) <= 1e-4 * max(abs(fd), 1e-9), (w, idx, fd, gd)
+
+
+def test_lstm_partitioned_sim_equals_unpartitioned():
+    from tofu_inputs.graphs import lstm
+    spec = lstm(2, 8, 3, 4)
+    g = Graph(spec)
+    vals = make_values(spec, seed=4)
+    ref = run_graph(g, vals, emulate_storage=False)
+    plan = recursive_search(g, 2)
+    res, ledger = simulate(g, plan, vals)
+    for t in ref:
+        assert np.allclose(res[t], ref[t], rtol=1e-12, atol=1e-14), t
+    assert ledger["elements"] == plan["cost"]
+
+
 def test_mlp_graph_backward_is_the_gradient():
     """The backward ops of tofu_inputs.mlp are the gradient of the loss op:
     compared with central finite differences in fp64."""

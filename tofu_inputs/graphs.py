@@ -95,7 +95,7 @@ def mlp(batch: int, dims: list, lr: float = LR, mu: float = MU, relu_last: bool 
         alias[f"W{l}_new"] = f"W{l}"
     used = {d for o in ops for d in [o["def"]]}
     defs = {k: v for k, v in defs.items() if k in used}
-    return {"defs": defs, "tensors": T, "ops": ops, "alias": alias}
+    return {"defs": defs, "tensors": T, "ops": ops, "alias": alias, "meta": {"samples_per_step": batch}}
 
 
 def config(i: int) -> dict:
@@ -232,13 +232,13 @@ def lstm(layers: int, hidden: int, steps: int, batch: int, lr: float = LR, mu: f
                    merge=p + "dc", backward_of=p + f"c{t}")
                 op(p + f"rec{t}", "mm_rec", [p + "dA", p + "Wh"], p + f"R{t - 1}", offsets=[[t * B, 0, 0], None],
                    ranges={"b": B}, merge=p + "rec", backward_of=p + f"gh{t}")
+        if l > 1:   # input gradient first: it reads Wx before the optimizer (fused into wgx) updates it
+            op(p + "dx", "mm_rec", [p + "dA", p + "Wx"], f"L{l - 1}.dHs", backward_of=p + "gx")
         xin = "X" if l == 1 else f"L{l - 1}.Hs"
         xoff = None if l == 1 else [[B, 0], None]
         op(p + "wgx", "gate_wgrad", [xin, p + "dA"], p + "dWx", offsets=xoff, ranges={"b": T * B},
            backward_of=p + "gx")
         op(p + "wgh", "gate_wgrad", [p + "Hs", p + "dA"], p + "dWh", ranges={"b": T * B}, backward_of=p + "gh0")
-        if l > 1:
-            op(p + "dx", "mm_rec", [p + "dA", p + "Wx"], f"L{l - 1}.dHs", backward_of=p + "gx")
     # ---------------------------------------------------------------- optimizer (SGD with momentum)
     for l in range(1, L + 1):
         p = f"L{l}."
@@ -251,7 +251,8 @@ def lstm(layers: int, hidden: int, steps: int, batch: int, lr: float = LR, mu: f
             alias[m + "_new"] = m
             alias[p + w + "_new"] = p + w
     used = {o["def"] for o in ops}
-    return {"defs": {k: v for k, v in defs.items() if k in used}, "tensors": Tn, "ops": ops, "alias": alias}
+    return {"defs": {k: v for k, v in defs.items() if k in used}, "tensors": Tn, "ops": ops, "alias": alias,
+            "meta": {"samples_per_step": B, "tokens_per_step": T * B}}
 
 
 CONFIG_K[2] = 8
