@@ -145,12 +145,17 @@ typedef struct {
   void* D;
   int ldd;
   float s0, s1;
+  int splits;  /* split-K: 0 = auto (when the output tiles cannot fill the SMs), 1 = off, n = n splits;
+                  tofu_gemm_plan_tmaps writes the chosen value back */
+  void* ws;    /* split-K fp32 workspace (tofu_gemm_workspace_bytes); NULL = library-owned */
 } tofu_gemm_args;
 int tofu_gemm_bf16(const tofu_gemm_args* args, void* stream);
-/* Split form used by the executor: encode the four TMA descriptors (A, B, C, D) once into `tmaps`
- * (4 x 128 bytes, 64-byte aligned), then launch with them. */
-int tofu_gemm_plan_tmaps(const tofu_gemm_args* args, void* tmaps, int* bn_out);
+/* Split form used by the executor: encode the TMA descriptors (A, B, C, D, workspace) once into `tmaps`
+ * (5 x 128 bytes, 64-byte aligned; args->splits/ws are updated), then launch with them.  Split-K results
+ * are reduced in fixed split order (deterministic). */
+int tofu_gemm_plan_tmaps(tofu_gemm_args* args, void* tmaps, int* bn_out);
 int tofu_gemm_launch_planned(const tofu_gemm_args* args, const void* tmaps, int bn, void* stream);
+int64_t tofu_gemm_workspace_bytes(const tofu_gemm_args* args);
 
 /* a5/a6 — box copy / reduction pieces (rank <= 4, innermost dim last, strides in elements).
  * A piece copies (nsrc == 1) or sums in order (nsrc > 1, fp32 arithmetic) nsrc source boxes of the same

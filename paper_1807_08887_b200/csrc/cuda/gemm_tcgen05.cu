@@ -10,7 +10,8 @@
 //
 // Epilogues (c_mode): 0 = bf16 store, 1 = fp32 store (Case-2 partials, weight grads), 2 = fp32 accumulate,
 // 3 = fused momentum-SGD on the weight gradient: M = M*s0 + acc (fp32, in place), W = W - M*s1 (bf16, in
-// place).  Mode 3 is the coalesced optimizer chain of P:L674-678 folded into the gradient's producer so the
+// place); 4 (internal) = split-K fp32 partial into plane `split` of a 3-D workspace, reduced in split order
+// by splitk_reduce_kernel (used when the output has too few tiles to fill 148 SMs, e.g. M = 128 RNN steps).  Mode 3 is the coalesced optimizer chain of P:L674-678 folded into the gradient's producer so the
 // gradient never touches HBM.
 //
 // Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer (1 lane),
@@ -35,7 +36,7 @@ constexpr int SMEM_MAX = 232448;  // 227 KB opt-in per CTA on sm_100
 
 template <int BN, int MODE>
 struct GemmCfg {
-  static constexpr bool LOADS = MODE >= 2;
+  static constexpr bool LOADS = MODE == 2 || MODE == 3;
   static constexpr int NBUF = LOADS ? 3 : 2;
   static constexpr int C_BYTES = 32 * 32 * (MODE == 0 ? 2 : 4);
   static constexpr int D_OFF = 4096;
@@ -57,7 +58,7 @@ template <int BN, bool A_MN, bool B_MN, int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD, int M, int N,
-                     int K, float s0, float s1) {
+                     int K, float s0, float s1, int splits) {
   using Cfg = GemmCfg<BN, MODE>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int NBUF = Cfg::NBUF;
@@ -79,6 +80,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int tiles_n = (N + BN - 1) / BN;
   const int ntiles = tiles_m * tiles_n;
   const int nk = (K + BK - 1) / BK;
+  // work unit = (output tile, K split); split s covers k-blocks [s*nk/splits, (s+1)*nk/splits)
+  const int nunits = ntiles * splits;
+  auto kb_lo = [&](int sp) { return (int)((int64_t)sp * nk / splits); };
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -106,10 +110,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       int it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int tile = u / splits, sp = u % splits;
         const int m0 = (tile / tiles_n) * BM;
         const int n0 = (tile % tiles_n) * BN;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        for (int kb = kb_lo(sp); kb < kb_lo(sp + 1); ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
@@ -137,13 +142,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
       int it = 0, local = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++local) {
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++local) {
+        const int sp = u % splits;
+        const int kb0 = kb_lo(sp);
         const int buf = local & 1;
         const uint32_t aph = (local >> 1) & 1;
         mbar_wait(&acc_empty[buf], aph ^ 1);  // epilogue has drained this accumulator
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + buf * BN;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        for (int kb = kb0; kb < kb_lo(sp + 1); ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&full[s], ph);
@@ -156,7 +163,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                      : umma_sdesc_sw128(a0 + kk * 32, 16, 1024);
             const uint64_t bd = B_MN ? umma_sdesc_sw128(b0 + kk * 2048, 8192, 1024)
                                      : umma_sdesc_sw128(b0 + kk * 32, 16, 1024);
-            umma_bf16(tmem_d, ad, bd, idesc, (kb | kk) ? 1u : 0u);
+            umma_bf16(tmem_d, ad, bd, idesc, (kb > kb0 || kk) ? 1u : 0u);
           }
           umma_commit(&empty[s]);  // frees the smem stage when these MMAs complete
         }
@@ -167,12 +174,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // ------------------------------------------------------------ epilogue (warps 2..5)
     const int q = warp & 3;  // TMEM lane quarter = tile rows 32q..32q+31
     constexpr int NCH = BN / 32;
-    const int my_tiles = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    const int S = my_tiles * NCH;
+    const int my_units = blockIdx.x < nunits ? (nunits - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const int S = my_units * NCH;
     uint8_t* wbuf = sE + q * NBUF * Cfg::BUF_BYTES;
     uint64_t* wbar = ebar + q * NBUF;
+    int split_of_chunk = 0;
     auto chunk_coords = [&](int s, int& col, int& row) {
-      const int tile = blockIdx.x + (s / NCH) * gridDim.x;
+      const int u = blockIdx.x + (s / NCH) * gridDim.x;
+      const int tile = u / splits;
+      split_of_chunk = u % splits;
       col = (tile % tiles_n) * BN + (s % NCH) * 32;
       row = (tile / tiles_n) * BM + q * 32;
     };
@@ -257,7 +267,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (lane == 0) {
         int col, row;
         chunk_coords(s, col, row);
-        tma_store_2d(&tmC, b, col, row);
+        if (MODE == 4) tma_store_3d(&tmC, b, col, row, split_of_chunk);  // fp32 partial plane of this split
+        else tma_store_2d(&tmC, b, col, row);
         if (MODE == 3) tma_store_2d(&tmD, b + Cfg::D_OFF, col, row);
         bulk_commit();
       }
@@ -313,10 +324,11 @@ static int launch_t(const tofu_gemm_args* g, const CUtensorMap* tm, cudaStream_t
       return TOFU_ERR_CUDA;
     attr_set = true;
   }
-  const int tiles = ((g->M + BM - 1) / BM) * ((g->N + BN - 1) / BN);
-  int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  const int splits = MODE == 4 ? g->splits : 1;
+  const int units = ((g->M + BM - 1) / BM) * ((g->N + BN - 1) / BN) * splits;
+  int grid = units < g_num_sms ? units : g_num_sms;
   if (g->max_ctas > 0 && grid > g->max_ctas) grid = g->max_ctas;
-  kern<<<grid, NTHREADS, Cfg::SMEM, st>>>(tm[0], tm[1], tm[2], tm[3], g->M, g->N, g->K, g->s0, g->s1);
+  kern<<<grid, NTHREADS, Cfg::SMEM, st>>>(tm[0], tm[1], tm[2], tm[3], g->M, g->N, g->K, g->s0, g->s1, splits);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }
 
@@ -327,19 +339,81 @@ static int dispatch_bn(const tofu_gemm_args* g, const CUtensorMap* tm, cudaStrea
 #define TOFU_CASE(AM, BMJ, O) \
   case ((AM) | ((BMJ) << 1) | ((O) << 2)): return launch_t<BN, (bool)(AM), (bool)(BMJ), O>(g, tm, st);
 #define TOFU_CASES(O) TOFU_CASE(0, 0, O) TOFU_CASE(0, 1, O) TOFU_CASE(1, 0, O) TOFU_CASE(1, 1, O)
-    TOFU_CASES(0) TOFU_CASES(1) TOFU_CASES(2) TOFU_CASES(3)
+    TOFU_CASES(0) TOFU_CASES(1) TOFU_CASES(2) TOFU_CASES(3) TOFU_CASES(4)
 #undef TOFU_CASES
 #undef TOFU_CASE
     default: return TOFU_ERR_ARG;
   }
 }
 
+// Split-K reduction: C = epilogue(sum_s WS[s]) in fixed split order (deterministic).
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N,
+                                                            void* C, int ldc, int mode) {
+  const int64_t plane = (int64_t)M * N;
+  const bool vec = (N % 4 == 0) && (ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+  if (vec) {
+    const int64_t n4 = plane / 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+      float4 acc = reinterpret_cast<const float4*>(ws)[i];
+      for (int s = 1; s < splits; ++s) {
+        const float4 v = reinterpret_cast<const float4*>(ws + s * plane)[i];
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+      const int64_t m = (i * 4) / N, n = (i * 4) % N;
+      if (mode == 0) {
+        __nv_bfloat162 a = __floats2bfloat162_rn(acc.x, acc.y), b = __floats2bfloat162_rn(acc.z, acc.w);
+        uint2 u;
+        u.x = *reinterpret_cast<uint32_t*>(&a);
+        u.y = *reinterpret_cast<uint32_t*>(&b);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(C) + m * ldc + n) = u;
+      } else {
+        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + m * ldc + n);
+        if (mode == 2) {
+          const float4 o = *dst;
+          acc.x += o.x; acc.y += o.y; acc.z += o.z; acc.w += o.w;
+        }
+        *dst = acc;
+      }
+    }
+  } else {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < plane; i += (int64_t)gridDim.x * blockDim.x) {
+      float acc = ws[i];
+      for (int s = 1; s < splits; ++s) acc += ws[s * plane + i];
+      const int64_t m = i / N, n = i % N;
+      if (mode == 0) reinterpret_cast<__nv_bfloat16*>(C)[m * ldc + n] = __float2bfloat16_rn(acc);
+      else if (mode == 1) reinterpret_cast<float*>(C)[m * ldc + n] = acc;
+      else reinterpret_cast<float*>(C)[m * ldc + n] += acc;
+    }
+  }
+}
+
+static void* g_ws = nullptr;
+static size_t g_ws_bytes = 0;
+static std::mutex g_ws_mu;
+
+static int auto_splits(const tofu_gemm_args* g, int bn) {
+  if (g->c_mode == 3 || g->splits == 1) return 1;
+  const int nk = (g->K + BK - 1) / BK;
+  if (g->splits > 1) return g->splits < nk ? g->splits : nk;
+  const int tiles = ((g->M + BM - 1) / BM) * ((g->N + bn - 1) / bn);
+  if (tiles * 2 > g_num_sms || nk < 8) return 1;
+  int sp = g_num_sms / tiles;
+  if (sp > nk / 4) sp = nk / 4;
+  if (sp > 16) sp = 16;
+  return sp < 2 ? 1 : sp;
+}
+
 }  // namespace tofu
 
 using namespace tofu;
 
-// tmaps: 4 x CUtensorMap (A, B, C, D), 64-byte aligned, 512 bytes total.
-extern "C" int tofu_gemm_plan_tmaps(const tofu_gemm_args* g, void* tmaps, int* bn_out) {
+extern "C" int64_t tofu_gemm_workspace_bytes(const tofu_gemm_args* g) {
+  return g->splits > 1 ? (int64_t)g->splits * g->M * g->N * 4 : 0;
+}
+
+// tmaps: 5 x CUtensorMap (A, B, C, D, split-K workspace), 64-byte aligned, 640 bytes.  args->splits is
+// in/out: 0 = choose (split-K when the output has too few tiles to fill the SMs), 1 = off, n = n splits.
+extern "C" int tofu_gemm_plan_tmaps(tofu_gemm_args* g, void* tmaps, int* bn_out) {
   if (encode_fn_init() != 0) return TOFU_ERR_CUDA;
   if (!g || g->M < 0 || g->N < 0 || g->K < 0 || g->c_mode < 0 || g->c_mode > 3) return TOFU_ERR_ARG;
   if (g->c_mode == 3 && (!g->D || (g->ldd % 8))) return TOFU_ERR_ARG;
@@ -350,6 +424,7 @@ extern "C" int tofu_gemm_plan_tmaps(const tofu_gemm_args* g, void* tmaps, int* b
       (reinterpret_cast<uintptr_t>(g->D) & 15))
     return TOFU_ERR_ALIGN;
   const int bn = (g->bn == 128 || g->bn == 256) ? g->bn : (g->N <= 128 ? 128 : 256);
+  g->splits = auto_splits(g, bn);
   CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(tmaps);
   const CUtensorMapDataType BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   const auto SW128 = CU_TENSOR_MAP_SWIZZLE_128B, SW64 = CU_TENSOR_MAP_SWIZZLE_64B;
@@ -366,6 +441,28 @@ extern "C" int tofu_gemm_plan_tmaps(const tofu_gemm_args* g, void* tmaps, int* b
   if (g->c_mode == 3) r = make_tmap(&tm[3], g->D, BF, 2, g->N, g->M, g->ldd, 32, 32, SW64);
   else tm[3] = tm[2];
   if (r) return TOFU_ERR_CUDA;
+  if (g->splits > 1) {
+    void* ws = g->ws;
+    if (!ws) {  // library-owned workspace (not CUDA-graph safe; the executor passes its own)
+      std::lock_guard<std::mutex> lk(g_ws_mu);
+      const size_t need = (size_t)tofu_gemm_workspace_bytes(g);
+      if (need > g_ws_bytes) {
+        if (g_ws) cudaFree(g_ws);
+        if (cudaMalloc(&g_ws, need) != cudaSuccess) return TOFU_ERR_CUDA;
+        g_ws_bytes = need;
+      }
+      ws = g_ws;
+      g->ws = ws;
+    }
+    cuuint64_t dims[3] = {(cuuint64_t)g->N, (cuuint64_t)g->M, (cuuint64_t)g->splits};
+    cuuint64_t strides[2] = {(cuuint64_t)g->N * 4, (cuuint64_t)g->N * g->M * 4};
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if ((g->N * 4) % 16) return TOFU_ERR_ALIGN;
+    if (g_encode(&tm[4], F32, 3, ws, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, SW128,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return TOFU_ERR_CUDA;
+  }
   *bn_out = bn;
   return TOFU_OK;
 }
@@ -382,13 +479,28 @@ extern "C" int tofu_gemm_launch_planned(const tofu_gemm_args* g, const void* tma
                : TOFU_ERR_CUDA;
   }
   const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(tmaps);
+  if (g->splits > 1) {
+    // partial products into the workspace planes, then one ordered reduction into C
+    const CUtensorMap tw[4] = {tm[0], tm[1], tm[4], tm[4]};
+    tofu_gemm_args p = *g;
+    p.c_mode = 4;
+    int rc = bn == 256 ? dispatch_bn<256>(&p, tw, st) : dispatch_bn<128>(&p, tw, st);
+    if (rc) return rc;
+    const int64_t n = (int64_t)g->M * g->N / 4 + 1;
+    int blocks = (int)((n + 255) / 256);
+    if (blocks > g_num_sms * 8) blocks = g_num_sms * 8;
+    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float*>(g->ws), g->splits, g->M, g->N, g->C,
+                                                 g->ldc, g->c_mode);
+    return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
+  }
   return bn == 256 ? dispatch_bn<256>(g, tm, st) : dispatch_bn<128>(g, tm, st);
 }
 
 extern "C" int tofu_gemm_bf16(const tofu_gemm_args* g, void* stream) {
-  alignas(64) CUtensorMap tm[4];
+  alignas(64) CUtensorMap tm[5];
+  tofu_gemm_args a = *g;
   int bn = 0;
-  int r = tofu_gemm_plan_tmaps(g, tm, &bn);
+  int r = tofu_gemm_plan_tmaps(&a, tm, &bn);
   if (r) return r;
-  return tofu_gemm_launch_planned(g, tm, bn, stream);
+  return tofu_gemm_launch_planned(&a, tm, bn, stream);
 }

@@ -146,11 +146,12 @@ struct Exec {
   };
   std::vector<Launch> launches;
   tofu_piece* pieces_dev = nullptr;
+  void* ws_dev = nullptr;  // split-K workspace shared by this executor's GEMMs (one stream)
   std::vector<tofu_piece> host_pieces;
   bool finalized = false;
   struct GemmLaunch {
     tofu_gemm_args a;
-    alignas(64) CUtensorMap tm[4];
+    alignas(64) CUtensorMap tm[5];
     int bn;
   };
   std::map<std::pair<int, int>, GemmLaunch> gemms;  // (op, li)
@@ -581,7 +582,10 @@ void finalize(Exec& E) {
     if (cudaMemcpy(E.pieces_dev, host.data(), host.size() * sizeof(tofu_piece), cudaMemcpyHostToDevice) != cudaSuccess)
       throw Error(TOFU_ERR_CUDA, "cudaMemcpy pieces");
   }
-  // GEMM descriptors
+  // GEMM descriptors (pass 0 sizes the shared split-K workspace with a placeholder address, pass 1 encodes
+  // the real descriptors)
+  for (int pass = 0; pass < 2; ++pass) {
+  int64_t ws_need = 0;
   for (int li = 0; li < nl; ++li) {
     const int r = E.local[li];
     for (size_t o = 0; o < g.ops.size(); ++o) {
@@ -630,10 +634,16 @@ void finalize(Exec& E) {
         G.a.s0 = at(L.fused_opt, "mu");
         G.a.s1 = at(L.fused_opt + 1, "lr");
       }
+      G.a.splits = 0;
+      G.a.ws = pass == 0 ? reinterpret_cast<void*>(uintptr_t(1) << 20) : E.ws_dev;
       int rc = tofu_gemm_plan_tmaps(&G.a, G.tm, &G.bn);
       if (rc) throw Error(rc, "gemm tensor map for op " + g.ops[o].name + " (pitch/alignment)");
-      E.gemms[{(int)o, li}] = G;
+      ws_need = std::max<int64_t>(ws_need, tofu_gemm_workspace_bytes(&G.a));
+      if (pass == 1) E.gemms[{(int)o, li}] = G;
     }
+  }
+  if (pass == 0 && ws_need > 0 && cudaMalloc(&E.ws_dev, ws_need) != cudaSuccess)
+    throw Error(TOFU_ERR_CUDA, "cudaMalloc split-K workspace");
   }
   E.finalized = true;
 }
@@ -799,6 +809,7 @@ extern "C" void tofu_exec_destroy(tofu_exec* h) {
   if (!h) return;
   if (h->e.pieces_dev) cudaFree(h->e.pieces_dev);
   if (h->e.flags_dev) cudaFree(h->e.flags_dev);
+  if (h->e.ws_dev) cudaFree(h->e.ws_dev);
   delete h;
 }
 
@@ -833,9 +844,10 @@ void run_range(Exec& E, int first, int last, cudaStream_t st) {
   finalize(E);
   for (int i = first; i < last; ++i) {
     const bool timed = i == E.timed_launch && E.ev_start;
-    if (timed) cudaEventRecord(E.ev_start, st);
+    // external event nodes when captured into a CUDA graph, so every replay re-times the launch
+    if (timed) cudaEventRecordWithFlags(E.ev_start, st, cudaEventRecordExternal);
     run_launch(E, E.launches[i], st);
-    if (timed) cudaEventRecord(E.ev_stop, st);
+    if (timed) cudaEventRecordWithFlags(E.ev_stop, st, cudaEventRecordExternal);
   }
 }
 

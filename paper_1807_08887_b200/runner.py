@@ -113,7 +113,24 @@ class TofuRunner:
         return full
 
     def step(self, stream=None):
-        self.exec.run(stream)
+        if getattr(self, "_graph", None) is not None:
+            self._graph.replay()
+        else:
+            self.exec.run(stream)
+
+    def capture(self):
+        """Capture one step (all of its kernel launches) into a CUDA graph; later step() calls replay it.
+        Run at least one eager step first (one-time kernel attribute setup happens outside capture)."""
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.exec.run()
+        torch.cuda.synchronize()
+        self._graph = g
+        return g
+
+    def uncapture(self):
+        self._graph = None
 
     def ledger(self):
         return self.exec.ledger()

@@ -26,7 +26,7 @@ class GemmArgs(C.Structure):
                 ("B", C.c_void_p), ("ldb", C.c_int), ("b_mn_major", C.c_int),
                 ("C", C.c_void_p), ("ldc", C.c_int), ("c_mode", C.c_int),
                 ("bn", C.c_int), ("max_ctas", C.c_int), ("D", C.c_void_p), ("ldd", C.c_int),
-                ("s0", C.c_float), ("s1", C.c_float)]
+                ("s0", C.c_float), ("s1", C.c_float), ("splits", C.c_int), ("ws", C.c_void_p)]
 
 
 class Piece(C.Structure):
@@ -101,9 +101,9 @@ def _stream(stream):
 
 # ----------------------------------------------------------------------------- kernels
 def gemm(A, B, Cout, M, N, K, lda, a_mn, ldb, b_mn, ldc, c_mode, bn=0, max_ctas=0, stream=None, D=None, ldd=0,
-         s0=0.0, s1=0.0):
+         s0=0.0, s1=0.0, splits=0):
     a = GemmArgs(M, N, K, A.data_ptr(), lda, a_mn, B.data_ptr(), ldb, b_mn, Cout.data_ptr(), ldc, c_mode, bn, max_ctas,
-                 D.data_ptr() if D is not None else None, ldd, s0, s1)
+                 D.data_ptr() if D is not None else None, ldd, s0, s1, splits, None)
     check(lib().tofu_gemm_bf16(C.byref(a), _stream(stream)), "tofu_gemm_bf16")
 
 

@@ -171,6 +171,7 @@ def test_pipelined_train_loop_equals_manual_steps():
     B.load(vals)
     lb = B.train(lambda s: batches[s], 4)
     torch.cuda.synchronize()
-    assert la == [float(x) for x in lb]
+    # the loss reduction uses atomics inside a rank: equal to fp32 rounding, not bitwise
+    assert np.allclose(la, [float(x) for x in lb], rtol=1e-6, atol=0)
     for t in ("W1", "W2", "M1"):
         assert torch.equal(A.gather(t), B.gather(t))

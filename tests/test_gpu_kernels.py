@@ -97,6 +97,36 @@ def test_gemm_fused_momentum_sgd(defname, M, N, K):
     assert nrm(Wd.double().cpu().numpy(), wref) <= 5e-3
 
 
+@pytest.mark.parametrize("defname", ["mm_nn", "mm_nt", "mm_tn"])
+@pytest.mark.parametrize("M,N,K,splits", [(128, 4096, 16384, 0), (128, 512, 4096, 5), (200, 264, 3000, 3),
+                                          (64, 256, 1024, 16)])
+@pytest.mark.parametrize("c_mode", [0, 1, 2])
+def test_gemm_split_k(defname, M, N, K, splits, c_mode):
+    """Split-K (auto for few output tiles, or forced) reduces fp32 partials in
+    fixed split order: same tolerances as the unsplit GEMM, and deterministic."""
+    t = _tofu()
+    am, bm = DEF_MAJOR[defname]
+    if (am and M % 8) or (not am and K % 8) or (N * (2 if c_mode == 0 else 4)) % 16:
+        pytest.skip("pitch")
+    rng = np.random.default_rng(M + 3 * N + K)
+    a_shape = (K, M) if am else (M, K)
+    b_shape = (K, N) if bm else (N, K)
+    A, B = q(rng, a_shape, 2 ** -7), q(rng, b_shape, 2 ** -9)
+    d = parse_def(MM_DEFS[defname])
+    ref = fast_eval(d, {"A": (A, (0, 0)), "B": (B, (0, 0))}, {"i": (0, M - 1), "j": (0, N - 1), "k": (0, K - 1)})
+    C0 = q(rng, (M, N), 2 ** -5) if c_mode == 2 else np.zeros((M, N))
+    if c_mode == 2:
+        ref = ref + C0
+    outs = []
+    for rep in range(2):
+        Cd = (torch.from_numpy(C0).float().cuda() if c_mode else torch.zeros((M, N), dtype=torch.bfloat16, device="cuda"))
+        t.gemm(cuda_bf16(A), cuda_bf16(B), Cd, M, N, K, a_shape[1], am, b_shape[1], bm, N, c_mode, splits=splits)
+        torch.cuda.synchronize()
+        outs.append(Cd.double().cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+    assert nrm(outs[0], ref) <= (5e-3 if c_mode == 0 else 1e-5)
+
+
 def test_gemm_strided_output_and_bn():
     t = _tofu()
     rng = np.random.default_rng(9)

@@ -93,5 +93,5 @@ def test_lstm_fused_optimizer_runs():
     descs = [R.exec.launch_desc(i) for i in range(R.exec.num_launches())]
     assert sum(d.get("fused") == "gemm+mom+sgd" for d in descs) == 4   # every weight gradient of both layers
     ref = run_graph(OGraph(spec), vals, emulate_storage=True)
-    for t in ("L1.Wx", "L2.Wh", "L1.Mx", "L2.Mh"):
-        assert nrm(out[t], ref[t]) <= 2e-2, t
+    for t in ("L1.Wx", "L2.Wh", "L1.Mx", "L2.Mh"):     # storage of t holds t_new after the step (alias)
+        assert nrm(out[t], ref[t + "_new"]) <= 2e-2, t
