@@ -7,8 +7,11 @@
 //   cell_bwd_c : d loss / d c_{t-1}
 // with dh = DU + DR (from the layer above and from step t+1) and dc = DN + dh * o * (1 - tanh(c_t)^2).
 // The formulas are the TDL defs of tofu_inputs/graphs.py (oracle-checked against finite differences).
+// Kinds 4 (cell_c + cell_h) and 5 (cell_bwd_a + cell_bwd_c) are the executor's fusions of the two ops of
+// one timestep that read the same gate rows: one pass over GX / GH instead of two (HBM-bound kernels).
 // Operands are pitched views of the (b, [gate,] h) box: element (b, x, h) at p[b*ld + x*gs + h].
-// Each thread handles one (b, h) and reads the four gates it needs; threads of a warp walk h (coalesced).
+// Each thread handles V consecutive h of one b (V = 8: 16-byte bf16 / 2x16-byte fp32 accesses when every
+// operand allows it, else V = 1).
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -22,67 +25,166 @@ struct LOpnd {
   int dt;
 };
 
-__device__ __forceinline__ float ldv(const LOpnd& o, int64_t i) {
-  return o.dt == TOFU_BF16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(o.p)[i])
-                           : reinterpret_cast<const float*>(o.p)[i];
-}
-__device__ __forceinline__ void stv(void* p, int dt, int64_t i, float v) {
-  if (dt == TOFU_BF16) reinterpret_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(v);
-  else reinterpret_cast<float*>(p)[i] = v;
-}
-__device__ __forceinline__ float sig(float x) { return 1.f / (1.f + __expf(-x)); }
-
 struct LstmArgs {
-  int kind;  // 0 c, 1 h, 2 bwd_a, 3 bwd_c
+  int kind;  // 0 c, 1 h, 2 bwd_a, 3 bwd_c, 4 c+h, 5 bwd_a+bwd_c
   int64_t nb, nh;
-  int g0, ng;  // gate range of the output (bwd_a)
+  int g0, ng;  // gate range of the dA output
   LOpnd gx, gh, cp, c, du, dr, dn;
-  void* out;
+  void* out;  // c / h / dA / dC
   int64_t out_ld, out_gs;
   int out_dt;
+  void* out2;  // fused second output: h (kind 4) or dC (kind 5)
+  int64_t out2_ld;
+  int out2_dt;
 };
 
-__global__ void __launch_bounds__(256) lstm_kernel(const LstmArgs a) {
-  const int64_t n = a.nb * a.nh;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = e / a.nh, h = e % a.nh;
-    const int64_t go = b * a.gx.ld + h, ho = b * a.gh.ld + h;
-    const float ai = ldv(a.gx, go) + ldv(a.gh, ho);
-    const float af = ldv(a.gx, go + a.gx.gs) + ldv(a.gh, ho + a.gh.gs);
-    const float ag = ldv(a.gx, go + 2 * a.gx.gs) + ldv(a.gh, ho + 2 * a.gh.gs);
-    const float ao = ldv(a.gx, go + 3 * a.gx.gs) + ldv(a.gh, ho + 3 * a.gh.gs);
-    const float I = sig(ai), F = sig(af), G = tanhf(ag), O = sig(ao);
-    if (a.kind == 0) {
-      stv(a.out, a.out_dt, b * a.out_ld + h, F * ldv(a.cp, b * a.cp.ld + h) + I * G);
-    } else if (a.kind == 1) {
-      stv(a.out, a.out_dt, b * a.out_ld + h, O * tanhf(ldv(a.c, b * a.c.ld + h)));
+template <int V>
+__device__ __forceinline__ void ldv(const LOpnd& o, int64_t i, float (&v)[V]) {
+  if (V == 8) {
+    if (o.dt == TOFU_BF16) {
+      const uint4 u = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(o.p) + i);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        v[2 * j] = f.x;
+        v[2 * j + 1] = f.y;
+      }
     } else {
-      const float tc = tanhf(ldv(a.c, b * a.c.ld + h));
-      const float dh = ldv(a.du, b * a.du.ld + h) + ldv(a.dr, b * a.dr.ld + h);
-      const float dc = ldv(a.dn, b * a.dn.ld + h) + dh * O * (1.f - tc * tc);
-      if (a.kind == 3) {
-        stv(a.out, a.out_dt, b * a.out_ld + h, dc * F);
-      } else {
-        const float cprev = ldv(a.cp, b * a.cp.ld + h);
+      const float4 a = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(o.p) + i);
+      const float4 b = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(o.p) + i + 4);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    }
+  } else {
+    v[0] = o.dt == TOFU_BF16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(o.p)[i])
+                             : reinterpret_cast<const float*>(o.p)[i];
+  }
+}
+
+template <int V>
+__device__ __forceinline__ void stv(void* p, int dt, int64_t i, const float (&v)[V]) {
+  if (V == 8) {
+    if (dt == TOFU_BF16) {
+      uint4 u;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+      *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p) + i) = u;
+    } else {
+      float* f = reinterpret_cast<float*>(p) + i;
+      *reinterpret_cast<float4*>(f) = make_float4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<float4*>(f + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    }
+  } else {
+    if (dt == TOFU_BF16) reinterpret_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(v[0]);
+    else reinterpret_cast<float*>(p)[i] = v[0];
+  }
+}
+
+__device__ __forceinline__ float sig(float x) { return 1.f / (1.f + __expf(-x)); }
+
+template <int V>
+__global__ void __launch_bounds__(256) lstm_kernel(const LstmArgs a) {
+  const int64_t nhv = a.nh / V;
+  const int64_t n = a.nb * nhv;
+  const int kind = a.kind;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / nhv, h = (e % nhv) * V;
+    const int64_t go = b * a.gx.ld + h, ho = b * a.gh.ld + h;
+    float I[V], F[V], G[V], O[V], t0[V], t1[V];
+    ldv<V>(a.gx, go, t0);
+    ldv<V>(a.gh, ho, t1);
+#pragma unroll
+    for (int j = 0; j < V; ++j) I[j] = sig(t0[j] + t1[j]);
+    ldv<V>(a.gx, go + a.gx.gs, t0);
+    ldv<V>(a.gh, ho + a.gh.gs, t1);
+#pragma unroll
+    for (int j = 0; j < V; ++j) F[j] = sig(t0[j] + t1[j]);
+    ldv<V>(a.gx, go + 2 * a.gx.gs, t0);
+    ldv<V>(a.gh, ho + 2 * a.gh.gs, t1);
+#pragma unroll
+    for (int j = 0; j < V; ++j) G[j] = tanhf(t0[j] + t1[j]);
+    ldv<V>(a.gx, go + 3 * a.gx.gs, t0);
+    ldv<V>(a.gh, ho + 3 * a.gh.gs, t1);
+#pragma unroll
+    for (int j = 0; j < V; ++j) O[j] = sig(t0[j] + t1[j]);
+    if (kind == 0 || kind == 4) {
+      float cp[V], c[V];
+      ldv<V>(a.cp, b * a.cp.ld + h, cp);
+#pragma unroll
+      for (int j = 0; j < V; ++j) c[j] = F[j] * cp[j] + I[j] * G[j];
+      stv<V>(a.out, a.out_dt, b * a.out_ld + h, c);
+      if (kind == 4) {
+        // h_t from the c_t as stored (fp32 storage of the c tensor: identical to the unfused cell_h input)
+        float hh[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) hh[j] = O[j] * tanhf(c[j]);
+        stv<V>(a.out2, a.out2_dt, b * a.out2_ld + h, hh);
+      }
+    } else if (kind == 1) {
+      float c[V], hh[V];
+      ldv<V>(a.c, b * a.c.ld + h, c);
+#pragma unroll
+      for (int j = 0; j < V; ++j) hh[j] = O[j] * tanhf(c[j]);
+      stv<V>(a.out, a.out_dt, b * a.out_ld + h, hh);
+    } else {
+      float c[V], du[V], dr[V], dn[V], dh[V], dc[V], tc[V];
+      ldv<V>(a.c, b * a.c.ld + h, c);
+      ldv<V>(a.du, b * a.du.ld + h, du);
+      ldv<V>(a.dr, b * a.dr.ld + h, dr);
+      ldv<V>(a.dn, b * a.dn.ld + h, dn);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        tc[j] = tanhf(c[j]);
+        dh[j] = du[j] + dr[j];
+        dc[j] = dn[j] + dh[j] * O[j] * (1.f - tc[j] * tc[j]);
+      }
+      if (kind == 3 || kind == 5) {
+        float r[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) r[j] = dc[j] * F[j];
+        if (kind == 3) stv<V>(a.out, a.out_dt, b * a.out_ld + h, r);
+        else stv<V>(a.out2, a.out2_dt, b * a.out2_ld + h, r);
+      }
+      if (kind == 2 || kind == 5) {
+        float cprev[V];
+        ldv<V>(a.cp, b * a.cp.ld + h, cprev);
         for (int x = a.g0; x < a.g0 + a.ng; ++x) {
-          float v;
-          if (x == 0) v = dc * G * I * (1.f - I);
-          else if (x == 1) v = dc * cprev * F * (1.f - F);
-          else if (x == 2) v = dc * I * (1.f - G * G);
-          else v = dh * tc * O * (1.f - O);
-          stv(a.out, a.out_dt, b * a.out_ld + (x - a.g0) * a.out_gs + h, v);
+          float r[V];
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            if (x == 0) r[j] = dc[j] * G[j] * I[j] * (1.f - I[j]);
+            else if (x == 1) r[j] = dc[j] * cprev[j] * F[j] * (1.f - F[j]);
+            else if (x == 2) r[j] = dc[j] * I[j] * (1.f - G[j] * G[j]);
+            else r[j] = dh[j] * tc[j] * O[j] * (1.f - O[j]);
+          }
+          stv<V>(a.out, a.out_dt, b * a.out_ld + (x - a.g0) * a.out_gs + h, r);
         }
       }
     }
   }
 }
 
+__host__ inline bool vec8_ok(const LstmArgs& a) {
+  if (a.nh % 8) return false;
+  auto ok = [](const void* p, int64_t ld, int64_t gs, int dt) {
+    if (!p) return true;
+    const int64_t align = dt == TOFU_BF16 ? 8 : 4;  // elements per 16 bytes
+    return (reinterpret_cast<uintptr_t>(p) % 16) == 0 && ld % align == 0 && gs % align == 0;
+  };
+  const LOpnd* ops[7] = {&a.gx, &a.gh, &a.cp, &a.c, &a.du, &a.dr, &a.dn};
+  for (auto o : ops)
+    if (!ok(o->p, o->ld, o->gs, o->dt)) return false;
+  return ok(a.out, a.out_ld, a.out_gs, a.out_dt) && ok(a.out2, a.out2_ld, 0, a.out2_dt);
+}
+
 }  // namespace tofu
 
-// Internal entry (not in the public header): operands are (ptr, ld, gs, dtype) quadruples.
+// Internal entry (not in the public header): operands are (ptr, ld, gs, dtype) quadruples in the slot order
+// gx, gh, cp, c, du, dr, dn; out2 is the second output of the fused kinds 4 / 5 (else NULL).
 extern "C" int tofu_lstm_cell(int kind, int64_t nb, int64_t nh, int g0, int ng, const void* const* ptrs,
                               const int64_t* lds, const int64_t* gss, const int* dts, void* out, int64_t out_ld,
-                              int64_t out_gs, int out_dt, void* stream) {
+                              int64_t out_gs, int out_dt, void* out2, int64_t out2_ld, int out2_dt, void* stream) {
   tofu::LstmArgs a{};
   a.kind = kind;
   a.nb = nb;
@@ -95,10 +197,16 @@ extern "C" int tofu_lstm_cell(int kind, int64_t nb, int64_t nh, int g0, int ng, 
   a.out_ld = out_ld;
   a.out_gs = out_gs;
   a.out_dt = out_dt;
-  const int64_t n = nb * nh;
+  a.out2 = out2;
+  a.out2_ld = out2_ld;
+  a.out2_dt = out2_dt;
+  const bool v8 = tofu::vec8_ok(a);
+  const int64_t n = nb * (v8 ? nh / 8 : nh);
   if (n == 0) return TOFU_OK;
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  tofu::lstm_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (v8) tofu::lstm_kernel<8><<<(unsigned)blocks, 256, 0, st>>>(a);
+  else tofu::lstm_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(a);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }

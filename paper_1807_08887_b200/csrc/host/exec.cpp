@@ -24,7 +24,7 @@
 extern "C" int tofu_barrier_run(void* flags_ptrs_dev, int rank, int n, void* stream);
 extern "C" int tofu_lstm_cell(int kind, int64_t nb, int64_t nh, int g0, int ng, const void* const* ptrs,
                               const int64_t* lds, const int64_t* gss, const int* dts, void* out, int64_t out_ld,
-                              int64_t out_gs, int out_dt, void* stream);
+                              int64_t out_gs, int out_dt, void* out2, int64_t out2_ld, int out2_dt, void* stream);
 
 namespace tofu {
 
@@ -94,6 +94,7 @@ struct LOp {
   bool skip = false;          // fused into the previous op
   bool fused_sgd = false;
   int fused_opt = -1;         // GEMM epilogue absorbs mom (this index) + sgd (index + 1)
+  bool fused_next = false;    // LSTM cell: this launch also computes the next op (c+h, bwd_a+bwd_c)
   std::vector<tofu_piece> fetch, reduce;
   std::vector<int> fetch_src, reduce_nremote;  // for the ledger
 };
@@ -501,6 +502,32 @@ void lower(Exec& E) {
         La.fused_opt = reader;
         all[r][reader].skip = true;
       }
+  // LSTM: the two cell ops of one timestep read the same gate rows -> one kernel (one pass over GX / GH)
+  if (E.fuse)
+    for (int r = 0; r < k; ++r)
+      for (size_t o = 0; o + 1 < g.ops.size(); ++o) {
+        const std::string &na = g.defs[g.ops[o].def].name, &nb = g.defs[g.ops[o + 1].def].name;
+        const bool fwd = na == "cell_c" && nb == "cell_h";
+        const bool bwd = na == "cell_bwd_a" && nb == "cell_bwd_c";
+        if (!fwd && !bwd) continue;
+        LOp &La = all[r][o], &Lb = all[r][o + 1];
+        if (La.skip || !La.out.direct || !Lb.out.direct || !Lb.fetch.empty()) continue;
+        auto same_buf = [](const Buf& x, const Buf& y) { return x.off == y.off && same(x.box, y.box) && same(x.buf_box, y.buf_box); };
+        // gate operands: both direct views of the same shard rows (the ops read different gate subsets; the
+        // kernel addresses gates from the row base, so only rows and h must agree)
+        auto same_rows = [](const Buf& x, const Buf& y) {
+          return x.direct && y.direct && x.off == y.off && same(x.buf_box, y.buf_box) && x.box.size() == 3 &&
+                 x.box[0].lo == y.box[0].lo && x.box[0].hi == y.box[0].hi && x.box[2].lo == y.box[2].lo &&
+                 x.box[2].hi == y.box[2].hi;
+        };
+        bool ok = same_rows(La.in[0], Lb.in[0]) && same_rows(La.in[1], Lb.in[1]);
+        if (fwd) ok &= g.ops[o + 1].inputs[2] == g.ops[o].output && same_buf(Lb.in[2], La.out);  // h reads this c
+        if (bwd)
+          for (int q = 0; q < 4; ++q) ok &= same_buf(La.in[3 + q], Lb.in[2 + q]);  // C, DU, DR, DN
+        if (!ok) continue;
+        La.fused_next = true;
+        Lb.skip = true;
+      }
   E.remote_fetch.assign(g.ops.size(), 0);
   E.remote_reduce.assign(g.ops.size(), 0);
   for (int r = 0; r < k; ++r)
@@ -690,9 +717,21 @@ int run_compute(Exec& E, int o, int li, cudaStream_t st) {
     const int64_t nb = ob.box[0].len(), nh = ob.box.back().len();
     const int g0 = ob.box.size() == 3 ? (int)ob.box[1].lo : 0, ng = ob.box.size() == 3 ? (int)ob.box[1].len() : 0;
     static const std::map<std::string, int> kinds = {{"cell_c", 0}, {"cell_h", 1}, {"cell_bwd_a", 2}, {"cell_bwd_c", 3}};
-    return tofu_lstm_cell(kinds.at(dn), nb, nh, g0, ng, ptrs, lds, gss, dts,
+    int kind_id = kinds.at(dn);
+    void* out2 = nullptr;
+    int64_t out2_ld = 0;
+    int out2_dt = TOFU_F32;
+    if (L.fused_next) {
+      const Buf& nb2 = E.lops[li][o + 1].out;
+      auto st2 = strides_of(nb2.buf_box);
+      out2 = base + nb2.off + offset_in(nb2.buf_box, nb2.box) * (nb2.dtype == TOFU_BF16 ? 2 : 4);
+      out2_ld = st2[0];
+      out2_dt = nb2.dtype;
+      kind_id = kind_id == 0 ? 4 : 5;
+    }
+    return tofu_lstm_cell(kind_id, nb, nh, g0, ng, ptrs, lds, gss, dts,
                           base + ob.off + offset_in(ob.buf_box, ob.box) * oes, ost[0],
-                          ob.box.size() == 3 ? ost[1] : 0, ob.dtype, st);
+                          ob.box.size() == 3 ? ost[1] : 0, ob.dtype, out2, out2_ld, out2_dt, st);
   }
   const int64_t n = vol(L.out.box);
   void* y = base + L.out.off;
@@ -890,6 +929,7 @@ std::string launch_desc(const Exec& E, int i) {
   o += ",\"flops\":" + json_num(flops) + ",\"bytes\":" + json_num(bytes);
   if (L.kind == 1 && lo_fused(E, L)) o += ",\"fused\":\"mom+sgd\"";
   if (L.kind == 1 && E.lops[L.li][L.op].fused_opt >= 0) o += ",\"fused\":\"gemm+mom+sgd\"";
+  if (L.kind == 1 && E.lops[L.li][L.op].fused_next) o += ",\"fused\":\"lstm-cell-pair\"";
   return o + "}";
 }
 }  // namespace

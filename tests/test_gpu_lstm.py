@@ -95,3 +95,18 @@ def test_lstm_fused_optimizer_runs():
     ref = run_graph(OGraph(spec), vals, emulate_storage=True)
     for t in ("L1.Wx", "L2.Wh", "L1.Mx", "L2.Mh"):     # storage of t holds t_new after the step (alias)
         assert nrm(out[t], ref[t + "_new"]) <= 2e-2, t
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_lstm_fused_cells_equal_unfused(k, monkeypatch):
+    """Fused cell pairs (c+h, bwd_a+bwd_c; one pass over the gate rows) give exactly the unfused results."""
+    spec = lstm(2, 64, 4, 16)
+    vals = _scale_weights(make_values(spec, seed=10))
+    monkeypatch.setenv("TOFU_FUSE", "0")
+    _, a = _run(spec, k, vals)
+    monkeypatch.setenv("TOFU_FUSE", "1")
+    R, b = _run(spec, k, vals)
+    descs = [R.exec.launch_desc(i) for i in range(R.exec.num_launches())]
+    assert sum(d.get("fused") == "lstm-cell-pair" for d in descs) >= 8 * k
+    for t in ("L1.Cs", "L2.Hs", "L1.dA", "L2.D0", "L1.dHs"):
+        assert np.array_equal(a[t], b[t]), t
