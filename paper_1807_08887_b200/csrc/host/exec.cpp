@@ -884,9 +884,18 @@ void run_range(Exec& E, int first, int last, cudaStream_t st) {
   for (int i = first; i < last; ++i) {
     const bool timed = i == E.timed_launch && E.ev_start;
     // external event nodes when captured into a CUDA graph, so every replay re-times the launch
-    if (timed) cudaEventRecordWithFlags(E.ev_start, st, cudaEventRecordExternal);
+    // (the External flag is only valid while capturing; eager launches record plainly)
+    unsigned evflags = cudaEventRecordDefault;
+    if (timed) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(st, &cs);
+      if (cs == cudaStreamCaptureStatusActive) evflags = cudaEventRecordExternal;
+      if (cudaEventRecordWithFlags(E.ev_start, st, evflags) != cudaSuccess)
+        throw Error(TOFU_ERR_CUDA, std::string("timing event: ") + cudaGetErrorString(cudaGetLastError()));
+    }
     run_launch(E, E.launches[i], st);
-    if (timed) cudaEventRecordWithFlags(E.ev_stop, st, cudaEventRecordExternal);
+    if (timed && cudaEventRecordWithFlags(E.ev_stop, st, evflags) != cudaSuccess)
+      throw Error(TOFU_ERR_CUDA, std::string("timing event: ") + cudaGetErrorString(cudaGetLastError()));
   }
 }
 

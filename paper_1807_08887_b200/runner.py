@@ -36,7 +36,7 @@ class TofuRunner:
         if not self.multi:
             for r in self.local:
                 n = max(256, self.plan.arena_bytes(r))
-                self.arenas[r] = torch.empty(n + 256, dtype=torch.uint8, device=self.device)
+                self.arenas[r] = torch.zeros(n + 256, dtype=torch.uint8, device=self.device)
             ptrs = [self._aligned(self.arenas[r]) for r in range(k)]
             self.exec = tofu.Exec(self.graph, self.plan, self.local, ptrs)
         else:

@@ -66,6 +66,22 @@ def test_mlp_step_per_op_parity(k, monkeypatch):
     assert R.ledger() == R.plan.cost()
 
 
+@pytest.mark.parametrize("k", [1, 2, 8])
+def test_mlp_step_fused_product_path(k, monkeypatch):
+    """The product path (optimizer folded into the wgrad epilogue, DESIGN R8): the weight gradient is
+    never materialised, so check the momentum and weights it updates, and the loss."""
+    monkeypatch.setenv("TOFU_FUSE", "1")
+    spec = config(0)
+    vals = make_values(spec, seed=13)
+    R, out = run_gpu(spec, k, vals)
+    ref = run_graph(OGraph(spec), vals, emulate_storage=True)
+    for t in ["Y", "M1_new", "M2_new", "W1_new", "W2_new", "loss"]:
+        r = ref[t]
+        e = nrm(out[t], r) if np.ndim(r) else abs(out[t] - r) / abs(r)
+        assert e <= 2e-2, (t, e)
+    assert R.ledger() == R.plan.cost()
+
+
 @pytest.mark.parametrize("k", [1, 8])
 def test_mlp_step_end_to_end(k, monkeypatch):
     monkeypatch.setenv("TOFU_FUSE", "0")
