@@ -84,12 +84,13 @@ def iter_box(ranges: dict, var_order, splits_seq, factors, dig):
 
 
 def access_hull(aff, ibox, off=0):
-    lo = hi = aff.const + off
-    for v, c in aff.coef:
-        a, b = ibox[v]
-        lo += min(c * a, c * b)
-        hi += max(c * a, c * b)
-    return lo, hi
+    return aff.hull(ibox, off)
+
+
+def clip(box, shape):
+    """Required region ∩ the tensor: elements outside a tensor read as zero (reading R11) and are never
+    communicated."""
+    return [(max(lo, 0), min(hi, n - 1)) for (lo, hi), n in zip(box, shape)]
 
 
 def _vol(box):
@@ -135,6 +136,7 @@ def op_cost_box(g, op, tdims, osplit, factors):
                 req = r if req is None else [(min(a[0], b[0]), max(a[1], b[1])) for a, b in zip(req, r)]
             if req is None:
                 continue
+            req = clip(req, shape)
             own = owned_box(shape, tdims[t], factors, dig)
             n_req = _vol(req)
             n_loc = 0 if own is None else _vol(_inter(req, own))
@@ -211,13 +213,14 @@ def op_cost_enum(g, op, tdims, osplit, factors):
                 if acc.tensor != p_:
                     continue
                 for env in pts[w]:
-                    for dim, ix in enumerate(acc.index):
-                        if ix is None:
-                            a, b = 0, shape[dim] - 1
-                        else:
-                            a = b = ix.const + param_off[p_][dim] + sum(c * env[v] for v, c in ix.coef)
+                    pt = [(0, shape[dim] - 1) if ix is None else (ix.value(env) + param_off[p_][dim],) * 2
+                          for dim, ix in enumerate(acc.index)]
+                    for dim, (a, b) in enumerate(pt):
                         lo[dim] = a if lo[dim] is None else min(lo[dim], a)
                         hi[dim] = b if hi[dim] is None else max(hi[dim], b)
+            # the hull of the accessed indices ∩ the tensor (outside it: zeros, not data, R11)
+            lo = [None if a is None else max(a, 0) for a in lo]
+            hi = [None if b is None else min(b, n - 1) for b, n in zip(hi, shape)]
             if lo and lo[0] is None:
                 continue
             for idx in itertools.product(*[range(a, b + 1) for a, b in zip(lo, hi)]):

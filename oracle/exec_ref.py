@@ -47,10 +47,23 @@ def _grid(vars_, box):
 
 
 def _idx(aff: Affine, grid):
-    acc = aff.const
-    for v, c in aff.coef:
-        acc = acc + c * grid[v]
-    return acc
+    return aff.value(grid)
+
+
+def _gather(arr, origin, index_arrays, shape):
+    """arr[index] with zero for indices outside the array (reading R11: an access outside its tensor
+    reads 0, i.e. zero padding).  Inside the tensor every access lies in the array by construction
+    (the array is the tensor or a region covering the required hull)."""
+    if any(n == 0 for n in arr.shape):
+        return np.zeros(shape)
+    ok = True
+    idx = []
+    for d, i in enumerate(index_arrays):
+        i = np.broadcast_to(i - origin[d], shape)
+        inb = (i >= 0) & (i < arr.shape[d])
+        ok = ok & inb
+        idx.append(np.where(inb, i, 0))
+    return np.where(ok, arr[tuple(idx)], 0.0)
 
 
 def _ev(e, grid, inputs, shape):
@@ -61,10 +74,7 @@ def _ev(e, grid, inputs, shape):
         return grid[e.val].astype(np.float64)
     if k == "access":
         arr, origin = inputs[e.val.tensor]
-        idx = []
-        for d, ix in enumerate(e.val.index):
-            idx.append(np.broadcast_to(_idx(ix, grid) - origin[d], shape))
-        return arr[tuple(idx)]
+        return _gather(arr, origin, [_idx(ix, grid) for ix in e.val.index], shape)
     if k == "neg":
         return -_ev(e.args[0], grid, inputs, shape)
     if k == "bin":
@@ -154,9 +164,80 @@ def _contraction(opdef):
         return None
     for acc in (x.val, y.val):
         for ix in acc.index:
-            if ix is None or len(ix.coef) != 1 or ix.coef[0][1] != 1 or ix.const != 0:
+            if ix is None or not ix.is_var():
                 return None
     return x.val, y.val
+
+
+def _product(opdef):
+    """(A access, B access) when the body is reduce(Sum; ..; A[..] * B[..]) with any index forms."""
+    b = opdef.body
+    if opdef.reducer != "Sum" or b.kind != "bin" or b.val != "*":
+        return None
+    x, y = b.args
+    if x.kind != "access" or y.kind != "access" or any(ix is None for a in (x, y) for ix in a.val.index):
+        return None
+    return x.val, y.val
+
+
+def tap_eval(opdef, inputs: dict, box: dict):
+    """Sum-of-products defs whose indices mix variables (convolutions: ``X[b, y + ky - 1, ..]``) evaluated
+    as the sum over "tap" values of one library einsum each: every index dimension that mixes several
+    variables has all but one of them fixed (the smallest extents: the filter taps), the tap values are
+    looped over, and for each the operands are gathered (zero outside the tensor, R11) into arrays with
+    one axis per remaining variable and contracted by einsum.  The taps' partial sums are added in tap
+    order.  Returns None when the def does not have this form (e.g. a variable left in two dims)."""
+    con = _product(opdef)
+    if con is None:
+        return None
+    ext = {v: box[v][1] - box[v][0] + 1 for v in opdef.all_vars()}
+    fixed = []
+    while True:
+        cand = None
+        for acc in con:
+            for ix in acc.index:
+                free = [v for v in ix.vars() if v not in fixed]
+                if len(free) >= 2:
+                    cand = min(free, key=lambda v: (ext[v], v))
+                    break
+            if cand:
+                break
+        if cand is None:
+            break
+        fixed.append(cand)
+    plan = []   # per operand: [(dim, free var or None)]
+    for acc in con:
+        dims, seen = [], set()
+        for d, ix in enumerate(acc.index):
+            free = [v for v in ix.vars() if v not in fixed]
+            if len(free) > 1 or (free and free[0] in seen):
+                return None
+            dims.append(free[0] if free else None)
+            seen.update(free)
+        plan.append(dims)
+    letters = {v: chr(ord("a") + i) for i, v in enumerate(opdef.all_vars())}
+    out_free = [v for v in opdef.out_vars if v not in fixed]
+    out = np.zeros(tuple(ext[v] for v in opdef.out_vars))
+    import itertools
+    for tap in itertools.product(*[range(box[v][0], box[v][1] + 1) for v in fixed]):
+        env = dict(zip(fixed, tap))
+        ops, subs = [], []
+        for acc, dims in zip(con, plan):
+            arr, origin = inputs[acc.tensor]
+            axes = [v for v in dims if v is not None]
+            gshape = tuple(ext[v] for v in axes)
+            grid = dict(env)
+            for i, v in enumerate(axes):
+                sh = [1] * len(axes)
+                sh[i] = ext[v]
+                grid[v] = np.arange(box[v][0], box[v][1] + 1).reshape(sh)
+            idx = [np.asarray(ix.value(grid)) for ix in acc.index]
+            ops.append(_gather(arr, origin, idx, gshape))
+            subs.append("".join(letters[v] for v in axes))
+        part = np.einsum(f"{subs[0]},{subs[1]}->{''.join(letters[v] for v in out_free)}", ops[0], ops[1])
+        sl = tuple(env[v] - box[v][0] if v in env else slice(None) for v in opdef.out_vars)
+        out[sl] += part
+    return out
 
 
 def fast_eval(opdef, inputs: dict, box: dict):
@@ -164,7 +245,8 @@ def fast_eval(opdef, inputs: dict, box: dict):
     for the whole sum, as the TDL text states it; anything else goes to tdl_eval."""
     con = _contraction(opdef)
     if con is None:
-        return tdl_eval(opdef, inputs, box)
+        r = tap_eval(opdef, inputs, box)
+        return tdl_eval(opdef, inputs, box) if r is None else r
     letters = {v: chr(ord("a") + i) for i, v in enumerate(opdef.all_vars())}
     ops, subs = [], []
     for acc in con:

@@ -108,6 +108,11 @@ def eval_affine(aff, env: dict) -> SymInterval:
     acc = SymInterval.const(aff.const)
     for v, a in aff.coef:
         acc = acc.add(env[v].mul_const(a))
+    for kind, mult, inner, d in aff.terms:
+        if kind == "div":   # 𝓘 / k (Fig. int-arith)
+            acc = acc.add(eval_affine(inner, env).div_const(d).mul_const(mult))
+        else:               # remainder: [0, d-1] (reading R11)
+            acc = acc.add(SymInterval((), F(min(0, mult * (d - 1))), (), F(max(0, mult * (d - 1)))))
     return acc
 
 

@@ -92,10 +92,8 @@ def simulate(g, plan, values, emulate_storage=False):
                         if ix is None:
                             a, b = 0, shape[dim] - 1
                         else:
-                            corners = [ix.const + poff[dim] + sum(c * (box[v][0] if s == 0 else box[v][1])
-                                                      for (v, c), s in zip(ix.coef, sel))
-                                       for sel in itertools.product((0, 1), repeat=len(ix.coef))]
-                            a, b = min(corners), max(corners)
+                            a, b = ix.hull(box, poff[dim])
+                            a, b = max(a, 0), min(b, shape[dim] - 1)   # outside the tensor: zeros (R11)
                         lo[dim] = a if lo[dim] is None else min(lo[dim], a)
                         hi[dim] = b if hi[dim] is None else max(hi[dim], b)
                 sl = tuple(slice(a, b + 1) for a, b in zip(lo, hi))

@@ -38,12 +38,56 @@ class TdlError(Exception):
 # ----------------------------------------------------------------------------- AST
 @dataclass(frozen=True)
 class Affine:
-    """sum(coef[v] * v) + const; coefficients are ints."""
+    """sum(coef[v] * v) + const (+ quasi-affine terms); coefficients are ints.
+
+    ``terms`` (reading R11): mult * floor(inner / d) ('div') or mult * (inner mod d) ('mod')
+    with an affine ``inner`` — the ``I / k`` of Fig. int-arith taken as integer division
+    of an index, plus its remainder; needed to describe the gradient of a strided convolution."""
     coef: tuple  # tuple of (var, int) sorted by var
     const: int
+    terms: tuple = ()  # tuple of (kind 'div'|'mod', mult int, inner Affine, d int)
 
     def vars(self):
-        return [v for v, c in self.coef if c != 0]
+        vs = [v for v, c in self.coef if c != 0]
+        for _, _, inner, _ in self.terms:
+            vs += [v for v in inner.vars() if v not in vs]
+        return vs
+
+    def value(self, env):
+        """Index value at a point (env: var -> int or numpy int array); floor division, non-negative mod."""
+        acc = self.const
+        for v, c in self.coef:
+            acc = acc + c * env[v]
+        for kind, mult, inner, d in self.terms:
+            x = inner.value(env)
+            acc = acc + mult * (x // d if kind == "div" else x % d)
+        return acc
+
+    def hull(self, box, off=0):
+        """Closed integer range of the index over a var box (var -> (lo, hi)): linear part by interval
+        arithmetic (exact for it), each div / mod term bounded separately (an over-approximation only
+        when a term shares a variable with another part)."""
+        lo = hi = self.const + off
+        for v, c in self.coef:
+            a, b = box[v]
+            lo += min(c * a, c * b)
+            hi += max(c * a, c * b)
+        for kind, mult, inner, d in self.terms:
+            ilo, ihi = inner.hull(box)
+            if kind == "div":
+                tl, th = ilo // d, ihi // d
+            elif ihi - ilo + 1 >= d or ilo // d != ihi // d:
+                tl, th = 0, d - 1
+            else:
+                tl, th = ilo % d, ihi % d
+            lo += min(mult * tl, mult * th)
+            hi += max(mult * tl, mult * th)
+        return lo, hi
+
+    def is_var(self, v=None):
+        """Exactly one variable with coefficient 1 and nothing else."""
+        return (len(self.coef) == 1 and self.coef[0][1] == 1 and self.const == 0 and not self.terms
+                and (v is None or self.coef[0][0] == v))
 
 
 @dataclass(frozen=True)
@@ -82,7 +126,7 @@ class OpDef:
 
 
 # ----------------------------------------------------------------------------- lexer
-_TOK = re.compile(r"\s*(?:(\d+\.\d*|\d+)|([A-Za-z_][A-Za-z_0-9]*)|(->|>=|<=|==|[-+*/()\[\],:;<>]))")
+_TOK = re.compile(r"\s*(?:(\d+\.\d*|\d+)|([A-Za-z_][A-Za-z_0-9]*)|(->|>=|<=|==|[-+*/%()\[\],:;<>]))")
 
 
 def _lex(src):
@@ -140,10 +184,12 @@ class _P:
 
 
 # ----------------------------------------------------------------------------- parser
-def _parse_affine(p, known_vars):
-    """Parse an affine index: sum of [int *] var | int, with + / -."""
+def _parse_affine(p, known_vars, stop=(",", "]")):
+    """Parse an index: sum of [int *] var | int | [int *] '(' affine ')' ('/' | '%') int, with + / -
+    (the parenthesised floor-division / remainder terms are reading R11)."""
     coef = {}
     const = 0
+    terms = []
     sign = 1
     if p.accept("-"):
         sign = -1
@@ -151,7 +197,27 @@ def _parse_affine(p, known_vars):
         sign = 1
     while True:
         tok = p.next()
-        if tok[0] == "num":
+        mult = None
+        if tok[0] == "num" and p.peek()[1] == "*" and p.t[p.i + 1][1] == "(":
+            if "." in tok[1]:
+                raise TdlError("NonAffineIndex", "non-integer constant in index")
+            mult = int(tok[1])
+            p.next()
+            tok = p.next()
+        if tok[1] == "(":
+            inner = _parse_affine(p, known_vars, stop=(")",))
+            p.expect(")")
+            kind = p.next()
+            if kind[1] not in ("/", "%"):
+                raise TdlError("NonAffineIndex", f"parenthesised index term needs / or % at {kind[2]}")
+            dtok = p.next()
+            if dtok[0] != "num" or "." in dtok[1] or int(dtok[1]) <= 0:
+                raise TdlError("NonAffineIndex", "index division by a positive integer constant only")
+            terms.append(("div" if kind[1] == "/" else "mod", sign * (1 if mult is None else mult), inner,
+                          int(dtok[1])))
+        elif mult is not None:
+            raise TdlError("Syntax", f"bad index term at {tok[2]}")
+        elif tok[0] == "num":
             if "." in tok[1]:
                 raise TdlError("NonAffineIndex", "non-integer constant in index")
             n = int(tok[1])
@@ -182,13 +248,13 @@ def _parse_affine(p, known_vars):
         elif nxt == "-":
             p.next()
             sign = -1
-        elif nxt in (",", "]"):
+        elif nxt in stop:
             break
-        elif nxt in ("*", "/"):
+        elif nxt in ("*", "/", "%"):
             raise TdlError("NonAffineIndex", "non-affine index expression")
         else:
             raise TdlError("Syntax", f"unexpected {nxt!r} in index")
-    return Affine(tuple(sorted((v, c) for v, c in coef.items() if c != 0)), const)
+    return Affine(tuple(sorted((v, c) for v, c in coef.items() if c != 0)), const, tuple(terms))
 
 
 class _BodyParser:
@@ -353,7 +419,7 @@ def parse_def(src: str) -> OpDef:
         opaque = True
         # pass-through dims: output vars used directly as the index of a non-sliced dim
         for ix in acc.index:
-            if ix is not None and len(ix.coef) == 1 and ix.coef[0][1] == 1 and ix.const == 0:
+            if ix is not None and ix.is_var():
                 opaque_free.append(ix.coef[0][0])
         bp.accesses.append(acc)
         body = Expr("opaque", fn, [Expr("access", acc), res])
@@ -430,7 +496,7 @@ def split_vars(d: OpDef):
     return list(d.out_vars) + list(d.red_vars)
 
 
-def var_ranges(d: OpDef, in_shapes: dict, out_shape) -> dict:
+def var_ranges(d: OpDef, in_shapes: dict, out_shape, given: dict | None = None) -> dict:
     """Concrete extent of every index variable.  Output vars from the output
     shape; reduce vars from the first input dim they index alone (coef 1,
     no other var) or, failing that, bounded by dim size."""
@@ -438,16 +504,17 @@ def var_ranges(d: OpDef, in_shapes: dict, out_shape) -> dict:
     for v, n in zip(d.out_vars, out_shape):
         R[v] = int(n)
     for v in d.red_vars:
+        if given and v in given:
+            R[v] = int(given[v])
+            continue
         best = None
         for acc in d.accesses:
             for dim, ix in enumerate(acc.index):
                 if ix is None:
                     continue
-                if ix.vars() == [v]:
-                    c = dict(ix.coef)[v]
-                    if c == 1 and ix.const == 0:
-                        best = int(in_shapes[acc.tensor][dim])
-                        break
+                if ix.is_var(v):
+                    best = int(in_shapes[acc.tensor][dim])
+                    break
             if best is not None:
                 break
         if best is None:

@@ -261,3 +261,224 @@ CONFIG_NAME[2] = "lstm-6x4096-T20-b128"
 
 def _config_lstm():
     return lstm(6, 4096, 20, 128)
+
+
+# ------------------------------------------------------------------------------------------------ WResNet
+WRN_UNITS = {50: [3, 4, 6, 3], 101: [3, 4, 23, 3], 152: [3, 8, 36, 3]}
+
+
+def conv_defs(R: int, s: int, p: int) -> dict:
+    """TDL of a 2-D convolution (NHWC activations X[b, y, x, c], weights W[co, ky, kx, ci]) with an R x R
+    filter, stride s, zero padding p (reading R11: an access outside its tensor reads 0), and its two
+    gradients.  The data gradient of a stride-2 convolution is written with the floor-division /
+    remainder index terms of reading R11: output pixel y receives from the input-gradient pixel
+    (y + p - 2*ty) / 2 through filter tap (y + p) % 2 + 2*ty."""
+    n = f"k{R}s{s}p{p}"
+    sy = "y" if s == 1 else f"{s}*y"
+    sx = "x" if s == 1 else f"{s}*x"
+    d = {
+        "conv_" + n: (f"def conv_{n}(X(4), W(4)) -> lambda b, y, x, co: reduce(Sum; ky, kx, ci; "
+                      f"X[b, {sy} + ky - {p}, {sx} + kx - {p}, ci] * W[co, ky, kx, ci])"),
+        "wconv_" + n: (f"def wconv_{n}(D(4), X(4)) -> lambda co, ky, kx, ci: reduce(Sum; b, y, x; "
+                       f"D[b, y, x, co] * X[b, {sy} + ky - {p}, {sx} + kx - {p}, ci])"),
+    }
+    if s == 1:
+        d["dconv_" + n] = (f"def dconv_{n}(D(4), W(4)) -> lambda b, y, x, ci: reduce(Sum; ky, kx, co; "
+                           f"D[b, y - ky + {p}, x - kx + {p}, co] * W[co, ky, kx, ci])")
+    elif s == 2:
+        d["dconv_" + n] = (f"def dconv_{n}(D(4), W(4)) -> lambda b, y, x, ci: reduce(Sum; ty, tx, co; "
+                           f"D[b, (y - 2*ty + {p}) / 2, (x - 2*tx + {p}) / 2, co] * "
+                           f"W[co, (y + {p}) % 2 + 2*ty, (x + {p}) % 2 + 2*tx, ci])")
+    return d
+
+
+def wresnet(units: list, width: int, batch: int, image: int = 224, base: int = 64, classes: int = 1000,
+            lr: float = LR, mu: float = MU) -> dict:
+    """Wide ResNet training step (ResNet widened by a scalar on every convolution's channels,
+    ImageNet 224x224 images).  Reading R12: bottleneck units (1x1, 3x3, 1x1; the stride of a
+    stage's first unit on its 3x3 convolution and on its 1x1 projection shortcut), stem 7x7/2 convolution
+    + ReLU + 3x3/2 max pool, global average pool, one FC layer, MSE loss, SGD with momentum; no batch
+    normalisation; the RGB image is padded to 8 channels (3 live).  Channels: stem base*width, stage s
+    bottleneck base*width*2^s, output 4*base*width*2^s."""
+    defs = dict(MM_DEFS)
+    T, ops, alias = {}, [], {}
+
+    def tensor(name, shape, dtype, role, grad_of=None, **kw):
+        T[name] = {"shape": list(shape), "dtype": dtype, "role": role, "grad_of": grad_of, "merge": None}
+        T[name].update(kw)
+
+    def op(name, d, ins, out, backward_of=None, ranges=None, attrs=None):
+        o = {"name": name, "def": d, "inputs": list(ins), "output": out, "backward_of": backward_of,
+             "merge": None, "attrs": attrs or {}}
+        if ranges:
+            o["ranges"] = ranges
+        ops.append(o)
+
+    def need_conv(R, s, p):
+        defs.update(conv_defs(R, s, p))
+        return f"k{R}s{s}p{p}"
+
+    defs["relu4"] = "def relu4(X(4)) -> lambda b, y, x, c: max(X[b, y, x, c], 0)"
+    defs["relu_grad4"] = "def relu_grad4(Y(4), D(4)) -> lambda b, y, x, c: select(Y[b, y, x, c] > 0, D[b, y, x, c], 0)"
+    defs["addrelu"] = "def addrelu(A(4), B(4)) -> lambda b, y, x, c: max(A[b, y, x, c] + B[b, y, x, c], 0)"
+    defs["add4"] = "def add4(A(4), B(4)) -> lambda b, y, x, c: A[b, y, x, c] + B[b, y, x, c]"
+    # max pool 3x3 / 2, pad 1 (inputs are ReLU outputs >= 0, so zero padding equals -inf padding)
+    defs["maxpool"] = ("def maxpool(X(4)) -> lambda b, y, x, c: reduce(Max; ky, kx; "
+                       "X[b, 2*y + ky - 1, 2*x + kx - 1, c])")
+    # its gradient: every input equal to its window's maximum receives the window's gradient; K[3, 3, c] = 1
+    # masks the filter taps that exist (tap (y + 1) % 2 + 2*ty <= 2); it carries a channel dim so that it
+    # can be split like the other operands (every tensor is split, P:L1524-1525)
+    defs["maxpool_grad"] = ("def maxpool_grad(X(4), Y(4), D(4), K(3)) -> lambda b, y, x, c: reduce(Sum; ty, tx; "
+                            "select(X[b, y, x, c] == Y[b, (y - 2*ty + 1) / 2, (x - 2*tx + 1) / 2, c], "
+                            "D[b, (y - 2*ty + 1) / 2, (x - 2*tx + 1) / 2, c] * K[(y + 1) % 2 + 2*ty, (x + 1) % 2 + 2*tx, c], 0))")
+    cin = 8
+    H = image
+    X = "X"
+    tensor(X, (batch, H, H, cin), "bf16", "input", live_channels=3)
+    c0 = base * width
+    # ------------------------------------------------------------------ forward
+    fwd_units = []
+    k = need_conv(7, 2, 3)
+    H1 = (H + 2 * 3 - 7) // 2 + 1
+    tensor("stem.W", (c0, 7, 7, cin), "bf16", "weight", fan_in=7 * 7 * 3)
+    tensor("stem.Z", (batch, H1, H1, c0), "bf16", "act")
+    tensor("stem.H", (batch, H1, H1, c0), "bf16", "act")
+    op("stem.conv", "conv_" + k, [X, "stem.W"], "stem.Z")
+    op("stem.relu", "relu4", ["stem.Z"], "stem.H")
+    H2 = (H1 + 2 - 3) // 2 + 1
+    tensor("pool.Y", (batch, H2, H2, c0), "bf16", "act")
+    tensor("pool.K", (3, 3, c0), "bf16", "state", init="ones")
+    op("pool", "maxpool", ["stem.H"], "pool.Y", ranges={"ky": 3, "kx": 3})
+    x, c, Hc = "pool.Y", c0, H2
+    for s, n in enumerate(units):
+        mid, outc = base * width * 2 ** s, 4 * base * width * 2 ** s
+        for u in range(n):
+            p = f"s{s}u{u}."
+            stride = 2 if (u == 0 and s > 0) else 1
+            Ho = (Hc - 1) // stride + 1
+            k1, k2, k3 = need_conv(1, 1, 0), need_conv(3, stride, 1), need_conv(1, 1, 0)
+            tensor(p + "W1", (mid, 1, 1, c), "bf16", "weight", fan_in=c)
+            tensor(p + "W2", (mid, 3, 3, mid), "bf16", "weight", fan_in=9 * mid)
+            tensor(p + "W3", (outc, 1, 1, mid), "bf16", "weight", fan_in=mid)
+            tensor(p + "Z1", (batch, Hc, Hc, mid), "bf16", "act")
+            tensor(p + "H1", (batch, Hc, Hc, mid), "bf16", "act")
+            tensor(p + "Z2", (batch, Ho, Ho, mid), "bf16", "act")
+            tensor(p + "H2", (batch, Ho, Ho, mid), "bf16", "act")
+            tensor(p + "Z3", (batch, Ho, Ho, outc), "bf16", "act")
+            tensor(p + "O", (batch, Ho, Ho, outc), "bf16", "act")
+            op(p + "conv1", "conv_" + k1, [x, p + "W1"], p + "Z1")
+            op(p + "relu1", "relu4", [p + "Z1"], p + "H1")
+            op(p + "conv2", "conv_" + k2, [p + "H1", p + "W2"], p + "Z2")
+            op(p + "relu2", "relu4", [p + "Z2"], p + "H2")
+            op(p + "conv3", "conv_" + k3, [p + "H2", p + "W3"], p + "Z3")
+            proj = u == 0
+            if proj:
+                kp = need_conv(1, stride, 0)
+                tensor(p + "Wp", (outc, 1, 1, c), "bf16", "weight", fan_in=c)
+                tensor(p + "P", (batch, Ho, Ho, outc), "bf16", "act")
+                op(p + "proj", "conv_" + kp, [x, p + "Wp"], p + "P")
+                sc = p + "P"
+            else:
+                sc = x
+            op(p + "add", "addrelu", [p + "Z3", sc], p + "O")
+            fwd_units.append((p, x, c, Hc, mid, outc, stride, Ho, proj))
+            x, c, Hc = p + "O", outc, Ho
+    defs["gap"] = (f"def gap(X(4)) -> lambda b, c: reduce(Sum; y, x; X[b, y, x, c] * {_num(1.0 / (Hc * Hc))})")
+    defs["gap_grad"] = f"def gap_grad(D(2)) -> lambda b, y, x, c: D[b, c] * {_num(1.0 / (Hc * Hc))}"
+    tensor("gap.Y", (batch, c), "bf16", "act")
+    op("gap", "gap", [x], "gap.Y")
+    tensor("fc.W", (c, classes), "bf16", "weight")
+    tensor("Y", (batch, classes), "bf16", "act")
+    op("fc", "mm_nn", ["gap.Y", "fc.W"], "Y")
+    n_out = batch * classes
+    defs["mse_grad"] = f"def mse_grad(Y(2), T(2)) -> lambda i, j: (Y[i, j] - T[i, j]) * {_num(2.0 / n_out)}"
+    defs["sumsq"] = (f"def sumsq(Y(2), T(2)) -> lambda : reduce(Sum; i, j; "
+                     f"(Y[i, j] - T[i, j]) * (Y[i, j] - T[i, j]) * {_num(1.0 / n_out)})")
+    tensor("T", (batch, classes), "bf16", "input")
+    tensor("loss", (), "f32", "loss")
+    tensor("dY", (batch, classes), "bf16", "grad", grad_of="Y")
+    op("loss", "sumsq", ["Y", "T"], "loss", attrs={"scale": 1.0 / n_out})
+    op("loss_grad", "mse_grad", ["Y", "T"], "dY", attrs={"scale": 2.0 / n_out})
+    # ------------------------------------------------------------------ backward
+    wgrads = []   # (weight, grad)
+    tensor("gap.dY", (batch, c), "bf16", "grad", grad_of="gap.Y")
+    op("fc_dgrad", "mm_nt", ["dY", "fc.W"], "gap.dY", backward_of="fc")
+    tensor("fc.dW", (c, classes), "f32", "grad", grad_of="fc.W")
+    op("fc_wgrad", "mm_tn", ["gap.Y", "dY"], "fc.dW", backward_of="fc")
+    wgrads.append(("fc.W", "fc.dW"))
+    dx = x + ".d"
+    tensor(dx, (batch, Hc, Hc, c), "bf16", "grad", grad_of=x)
+    op("gap_bwd", "gap_grad", ["gap.dY"], dx, backward_of="gap")
+    for (p, xin, cin_u, Hin, mid, outc, stride, Ho, proj) in reversed(fwd_units):
+        k1, k2, k3 = f"k1s1p0", f"k3s{stride}p1", "k1s1p0"
+        dO = p + "O.d"
+        tensor(p + "dS", (batch, Ho, Ho, outc), "bf16", "grad", grad_of=p + "Z3")
+        op(p + "add_bwd", "relu_grad4", [p + "O", dO], p + "dS", backward_of=p + "add")
+        tensor(p + "dH2", (batch, Ho, Ho, mid), "bf16", "grad", grad_of=p + "H2")
+        op(p + "conv3_dgrad", "dconv_" + k3, [p + "dS", p + "W3"], p + "dH2", backward_of=p + "conv3")
+        tensor(p + "dW3", (outc, 1, 1, mid), "f32", "grad", grad_of=p + "W3")
+        op(p + "conv3_wgrad", "wconv_" + k3, [p + "dS", p + "H2"], p + "dW3", backward_of=p + "conv3")
+        tensor(p + "dZ2", (batch, Ho, Ho, mid), "bf16", "grad", grad_of=p + "Z2")
+        op(p + "relu2_bwd", "relu_grad4", [p + "H2", p + "dH2"], p + "dZ2", backward_of=p + "relu2")
+        tensor(p + "dH1", (batch, Hin, Hin, mid), "bf16", "grad", grad_of=p + "H1")
+        rng2 = {"ty": 2, "tx": 2} if stride == 2 else None
+        op(p + "conv2_dgrad", "dconv_" + k2, [p + "dZ2", p + "W2"], p + "dH1", backward_of=p + "conv2",
+           ranges=rng2)
+        tensor(p + "dW2", (mid, 3, 3, mid), "f32", "grad", grad_of=p + "W2")
+        op(p + "conv2_wgrad", "wconv_" + k2, [p + "dZ2", p + "H1"], p + "dW2", backward_of=p + "conv2")
+        tensor(p + "dZ1", (batch, Hin, Hin, mid), "bf16", "grad", grad_of=p + "Z1")
+        op(p + "relu1_bwd", "relu_grad4", [p + "H1", p + "dH1"], p + "dZ1", backward_of=p + "relu1")
+        tensor(p + "dXm", (batch, Hin, Hin, cin_u), "bf16", "grad")
+        op(p + "conv1_dgrad", "dconv_" + k1, [p + "dZ1", p + "W1"], p + "dXm", backward_of=p + "conv1")
+        tensor(p + "dW1", (mid, 1, 1, cin_u), "f32", "grad", grad_of=p + "W1")
+        op(p + "conv1_wgrad", "wconv_" + k1, [p + "dZ1", xin], p + "dW1", backward_of=p + "conv1")
+        dxin = xin + ".d"
+        tensor(dxin, (batch, Hin, Hin, cin_u), "bf16", "grad", grad_of=xin)
+        if proj:
+            kp = f"k1s{stride}p0"
+            tensor(p + "dXp", (batch, Hin, Hin, cin_u), "bf16", "grad")
+            op(p + "proj_dgrad", "dconv_" + kp, [p + "dS", p + "Wp"], p + "dXp", backward_of=p + "proj",
+               ranges={"ty": 1, "tx": 1} if stride == 2 else None)
+            tensor(p + "dWp", (outc, 1, 1, cin_u), "f32", "grad", grad_of=p + "Wp")
+            op(p + "proj_wgrad", "wconv_" + kp, [p + "dS", xin], p + "dWp", backward_of=p + "proj")
+            op(p + "dx_sum", "add4", [p + "dXm", p + "dXp"], dxin, backward_of=p + "add")
+            wgrads.append((p + "Wp", p + "dWp"))
+        else:
+            op(p + "dx_sum", "add4", [p + "dXm", p + "dS"], dxin, backward_of=p + "add")
+        wgrads += [(p + "W3", p + "dW3"), (p + "W2", p + "dW2"), (p + "W1", p + "dW1")]
+    tensor("stem.dH", (batch, H1, H1, c0), "bf16", "grad", grad_of="stem.H")
+    op("pool_bwd", "maxpool_grad", ["stem.H", "pool.Y", "pool.Y.d", "pool.K"], "stem.dH", backward_of="pool",
+       ranges={"ty": 2, "tx": 2})
+    tensor("stem.dZ", (batch, H1, H1, c0), "bf16", "grad", grad_of="stem.Z")
+    op("stem.relu_bwd", "relu_grad4", ["stem.H", "stem.dH"], "stem.dZ", backward_of="stem.relu")
+    tensor("stem.dW", (c0, 7, 7, cin), "f32", "grad", grad_of="stem.W")
+    op("stem.wgrad", "wconv_k7s2p3", ["stem.dZ", X], "stem.dW", backward_of="stem.conv")
+    wgrads.append(("stem.W", "stem.dW"))
+    # ------------------------------------------------------------------ optimizer (SGD with momentum)
+    defs["mom"] = f"def mom(M(2), G(2)) -> lambda i, j: M[i, j] * {_num(mu)} + G[i, j]"
+    defs["sgd"] = f"def sgd(W(2), M(2)) -> lambda i, j: W[i, j] - M[i, j] * {_num(lr)}"
+    defs["mom4"] = f"def mom4(M(4), G(4)) -> lambda a, b, c, d: M[a, b, c, d] * {_num(mu)} + G[a, b, c, d]"
+    defs["sgd4"] = f"def sgd4(W(4), M(4)) -> lambda a, b, c, d: W[a, b, c, d] - M[a, b, c, d] * {_num(lr)}"
+    for w, g in wgrads:
+        shp = T[w]["shape"]
+        r = "4" if len(shp) == 4 else ""
+        m = w[:-1] + "M" + w[-1] if w.endswith(("1", "2", "3", "p")) else w + ".M"
+        m = w + ".M"
+        tensor(m, shp, "f32", "state")
+        tensor(m + "_new", shp, "f32", "state")
+        tensor(w + "_new", shp, "bf16", "weight")
+        op(w + ".mom", "mom" + r, [m, g], m + "_new", attrs={"mu": mu})
+        op(w + ".sgd", "sgd" + r, [w, m + "_new"], w + "_new", attrs={"lr": lr})
+        alias[m + "_new"] = m
+        alias[w + "_new"] = w
+    used = {o["def"] for o in ops}
+    return {"defs": {k_: v for k_, v in defs.items() if k_ in used}, "tensors": T, "ops": ops, "alias": alias,
+            "meta": {"samples_per_step": batch}}
+
+
+def wresnet_depth(L: int, width: int, batch: int, image: int = 224) -> dict:
+    return wresnet(WRN_UNITS[L], width, batch, image)
+
+
+CONFIG_K[3] = 8
+CONFIG_NAME[3] = "wresnet-152-4-b32"

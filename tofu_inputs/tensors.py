@@ -10,7 +10,9 @@ operands without any rounding code.  Recipes:
   state  M : q * 2^-17                    (non-zero so momentum is exercised)
   mode="int": all of the above replaced by q ~ U{-3..3} (exact fp64 sums,
               used for partitioned-vs-unpartitioned equality tests)
-  tensors with "init": "zeros" (initial recurrent state, zero gradients) are zero
+  tensors with "init": "zeros" (initial recurrent state, zero gradients) are zero, "ones" are one
+  a tensor's "fan_in" overrides shape[0] (convolution weights [co, ky, kx, ci]: ky*kx*ci)
+  an input's "live_channels" n zeroes its last dim from n on (an RGB image padded to 8 channels)
 """
 from __future__ import annotations
 
@@ -35,13 +37,18 @@ def make_values(graph: dict, seed: int = 0, mode: str = "float") -> dict:
         if t.get("init") == "zeros":
             out[name] = np.zeros(shape)
             continue
+        if t.get("init") == "ones":
+            out[name] = np.ones(shape)
+            continue
         if mode == "int":
             out[name] = _q(rng, shape, -3, 3)
             continue
         if role == "input":
             out[name] = _q(rng, shape) * (2.0 ** -7 if name != "T" else 2.0 ** -8)
+            if t.get("live_channels") is not None:   # channel padding of an image (last dim) is zero
+                out[name][..., int(t["live_channels"]):] = 0.0
         elif role == "weight":
-            fan_in = shape[0]
+            fan_in = int(t.get("fan_in") or shape[0])
             s = round(math.log2(math.sqrt(fan_in)))
             out[name] = _q(rng, shape) * 2.0 ** (-7 - s)
         else:
