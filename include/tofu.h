@@ -157,6 +157,99 @@ int tofu_gemm_plan_tmaps(tofu_gemm_args* args, void* tmaps, int* bn_out);
 int tofu_gemm_launch_planned(const tofu_gemm_args* args, const void* tmaps, int bn, void* stream);
 int64_t tofu_gemm_workspace_bytes(const tofu_gemm_args* args);
 
+/* a4' — implicit-GEMM convolution sub-op (NHWC bf16 activations, weights [co][ky][kx][ci], fp32
+ * accumulation in TMEM via tcgen05).  The convolution TDL defs (tofu_inputs.graphs.conv_defs; reading R11)
+ * are executed as a GEMM one of whose operands is gathered pixel by pixel from an activation buffer S
+ * (zero outside the buffer: zero padding) while the other is dense and loaded by TMA.
+ *
+ * Pixel grid: rows g = (gb, gy, gx) in [0,nb) x [0,ngy) x [0,ngx), flattened gb-major.  Tap t (< ntaps <=
+ * TOFU_CONV_MAX_TAPS) reads S pixel (gb + sb0, ay*gy + cy + tap_dy[t], ax*gx + cx + tap_dx[t]) (buffer
+ * coordinates; outside [0,sH) x [0,sW) the value is 0) at channels sc0 + [0, nch).
+ *
+ * kind 0 — forward / data gradient (P:L248-259 sub-op):  M = grid pixels, K = ntaps*nch (k = t*nch + c),
+ *   N = n_out.  A[m,k] = S[...] gathered.  B dense in Bp (row pitch ldb, a box of rows x cols):
+ *     b_mn_major 0 (forward, W[co][taps][ci]):   B[k,n] = Bp[n*ldb + tap_w[t]*b_tap + c]
+ *     b_mn_major 1 (data grad, W[co][taps][ci]): B[k,n] = Bp[c*ldb + tap_w[t]*b_tap + n]
+ *   (nch must be a multiple of 64, or — forward only — taps in natural order with b_tap == nch so the K
+ *   columns are contiguous).  Output pixel of row (gb, gy, gx): C[gb*c_sb + (c_ys*gy + c_y0)*c_sy +
+ *   (c_xs*gx + c_x0)*c_sx + n], c_mode 0 = bf16 store, 1 = f32 store (a Case-2 partial).
+ * kind 1 — weight gradient:  M = m_out (output channels), N = ntaps*nch (n = t*nch + c), K = grid pixels.
+ *   A[k,m] = Ap[k*lda + m] (the output gradient, pixel rows contiguous, MN-major), B[k,n] = S[...] gathered.
+ *   C[m,n] f32 at Cp[m*ldc + n]: c_mode 1 store, 2 accumulate, 3 fused momentum-SGD (as tofu_gemm_args:
+ *   C = momentum (in/out) = C*s0 + acc, D bf16 weight (in/out) = D - C*s1, row pitch ldd).  splits: split-K
+ *   over pixels (0 = auto, 1 = off) with fp32 workspace ws (tofu_conv_workspace_bytes), reduced in fixed
+ *   order (deterministic); the optimizer is applied by the reduction.
+ * Requirements: nch % 8 == 0, S channel stride 1 and sc0 % 8 == 0, 16-byte aligned pointers, pitches
+ * multiples of 8 elements.  Returns TOFU_ERR_ARG / TOFU_ERR_ALIGN on violations.
+ */
+#define TOFU_CONV_MAX_TAPS 64
+typedef struct {
+  int kind;
+  int nb, ngy, ngx;
+  int ay, ax, cy, cx, sb0;
+  int ntaps, nch;
+  short tap_dy[TOFU_CONV_MAX_TAPS], tap_dx[TOFU_CONV_MAX_TAPS], tap_w[TOFU_CONV_MAX_TAPS];
+  const void* S;
+  int64_t s_sb, s_sy, s_sx;
+  int sH, sW, sc0;
+  int n_out, m_out;         /* kind 0: N; kind 1: M */
+  const void* Bp;           /* kind 0 dense operand */
+  int64_t ldb;
+  int b_mn_major, b_tap, b_rows, b_cols;   /* dense box extents (rows x cols of the Bp view) */
+  const void* Ap;           /* kind 1 dense operand */
+  int64_t lda;
+  void* C;
+  int64_t c_sb, c_sy, c_sx;
+  int c_ys, c_y0, c_xs, c_x0;
+  int64_t ldc;
+  int c_mode;
+  void* D;
+  int64_t ldd;
+  float s0, s1;
+  int splits;
+  void* ws;
+} tofu_conv_args;
+/* Encode TMA descriptors once (tmaps: 4 x 128 B, 64-byte aligned; args->splits updated), then launch. */
+int tofu_conv_plan(tofu_conv_args* args, void* tmaps);
+int tofu_conv_launch_planned(const tofu_conv_args* args, const void* tmaps, void* stream);
+int tofu_conv_bf16(const tofu_conv_args* args, void* stream);
+int64_t tofu_conv_workspace_bytes(const tofu_conv_args* args);
+
+/* Window ops of the WResNet stem and head (NHWC bf16, channel stride 1, C % 8 == 0; every pointer is the
+ * element (first b, buffer row 0, buffer col 0, first channel) of its buffer, 16-byte aligned):
+ *   tofu_maxpool:      out[b,oy,ox,c] = max_{ky,kx<3} X[b, 2oy+ky-1, 2ox+kx-1, c]   (0 outside X: R11; X >= 0)
+ *                      iterates the Y-side box (nb, Ho, Wo) at global origin (oy0, ox0); X buffer (H, W) at
+ *                      global origin (y0, x0).
+ *   tofu_maxpool_grad: out[b,y,x,c] = Σ_{ty in [ty0,ty1], tx in [tx0,tx1]} select(X[b,y,x,c] == Y[b,oy,ox,c],
+ *                      dY[b,oy,ox,c] * K[(y+1)%2 + 2ty, (x+1)%2 + 2tx, c], 0) with oy = (y+1-2ty)/2 (floor),
+ *                      ox likewise, K = 0 past tap 2 and Y/dY = 0 outside their buffers (the maxpool_grad TDL
+ *                      def); iterates the X-side box (nb, H, W) at (y0, x0); Y / dY buffers (Ho, Wo) at (oy0, ox0).
+ *   tofu_gap:          out[b,c] (+partial) = Σ_{y<H, x<W} X[b,y,x,c] * s   (o_sb = row pitch of out)
+ *   tofu_gap_grad:     out[b,y,x,c] = dY[b,c] * s over the (nb, H, W) box   (y_sb = row pitch of dY)
+ * out_f32: 1 = f32 output (a Case-2 partial), 0 = bf16. */
+typedef struct {
+  int nb, C;
+  int H, W, y0, x0;
+  int Ho, Wo, oy0, ox0;
+  int64_t x_sb, x_sy, x_sx;
+  int64_t y_sb, y_sy, y_sx;
+  int64_t d_sb, d_sy, d_sx;
+  int64_t o_sb, o_sy, o_sx;
+  int64_t k_sy, k_sx;
+  const void* X;
+  const void* Y;
+  const void* dY;
+  const void* K;
+  void* out;
+  int out_f32;
+  int ty0, ty1, tx0, tx1;
+  float s;
+} tofu_window_args;
+int tofu_maxpool(const tofu_window_args* a, void* stream);
+int tofu_maxpool_grad(const tofu_window_args* a, void* stream);
+int tofu_gap(const tofu_window_args* a, void* stream);
+int tofu_gap_grad(const tofu_window_args* a, void* stream);
+
 /* a5/a6 — box copy / reduction pieces (rank <= 4, innermost dim last, strides in elements).
  * A piece copies (nsrc == 1) or sums in order (nsrc > 1, fp32 arithmetic) nsrc source boxes of the same
  * extent into one destination box, converting dtype.  Sources may be peer pointers. */
@@ -182,6 +275,8 @@ int tofu_pieces_run(const tofu_piece* pieces_dev, int n, int64_t max_elems, void
  *   TOFU_EW_SGD_MOM   fused: m' = m*s0 + g; w' = w - m'*s1; x0 = m (f32, in/out), x1 = g (f32),
  *                     x2 = w (bf16, in/out); y unused
  *   TOFU_EW_SUMSQ     y[0] (f32, accumulated with atomicAdd) += Σ (x0 - x1)^2 * s0  (bf16, bf16)
+ *   TOFU_EW_ADD       y = x0 + x1                         (bf16, bf16 -> bf16; gradient sums)
+ *   TOFU_EW_ADDRELU   y = max(x0 + x1, 0)                 (bf16, bf16 -> bf16; residual join)
  */
 #define TOFU_EW_RELU 0
 #define TOFU_EW_RELU_GRAD 1
@@ -190,6 +285,8 @@ int tofu_pieces_run(const tofu_piece* pieces_dev, int n, int64_t max_elems, void
 #define TOFU_EW_SGD 4
 #define TOFU_EW_SGD_MOM 5
 #define TOFU_EW_SUMSQ 6
+#define TOFU_EW_ADD 7
+#define TOFU_EW_ADDRELU 8
 int tofu_elementwise(int kind, int64_t n, void* y_dev, const void* x0_dev, const void* x1_dev, void* x2_dev,
                      float s0, float s1, void* stream);
 

@@ -1,0 +1,724 @@
+// Implicit-GEMM convolution sub-op on sm_100a (WResNet, configs[3]): the convolution TDL defs (forward,
+// data gradient, weight gradient; tofu_inputs.graphs.conv_defs, DESIGN reading R11) executed on the
+// worker's tile as one tcgen05 GEMM whose activation operand is GATHERED pixel by pixel (cp.async, zero-fill
+// outside the buffer = zero padding) straight into the 128B-swizzled shared-memory layout the UMMA
+// descriptors expect, while the dense operand (weights, or the output gradient for the weight gradient)
+// arrives by TMA.  This is the same partition-n-reduce sub-op the paper runs with cuDNN; the
+// im2col matrix is never materialised.
+//
+//   kind 0 (forward / data gradient): rows = output pixels, K = taps x channels, A gathered (K-major),
+//          B = weights via TMA (K-major for the forward, MN-major for the data gradient), output rows
+//          stored directly (a row = one pixel's channels; strided pixel grids serve the stride-2 data
+//          gradient's sub-pixel phases).
+//   kind 1 (weight gradient): M = output channels, N = taps x input channels, K = pixels; A = output
+//          gradient via TMA (MN-major), B gathered (MN-major rows of 64 channels); fp32 output through the
+//          TMA-store epilogue of the GEMM (store / accumulate / fused momentum-SGD), split-K over pixels.
+//
+// Warp roles (256 threads): warp 0 lane 0 = TMA producer of the dense operand, warp 1 = TMEM allocator +
+// MMA issuer, warps 2..5 = epilogue (TMEM lane quarter w%4), warps 6..7 = gather producers (64 threads,
+// LAG cp.async groups in flight each; a stage is published with fence.proxy.async + mbarrier arrive once
+// its copies land).  Persistent grid, TMEM accumulator double-buffered as in gemm_tcgen05.cu.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cstdio>
+#include <mutex>
+
+#include "common.cuh"
+#include "../tofu_kernels.h"
+
+namespace tofu {
+namespace conv {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int NTHREADS = 256;
+constexpr int SMEM_MAX = 232448;
+constexpr int LAG = 2;
+constexpr int NGATHER = 64;
+
+struct Params {
+  tofu_conv_args a;
+  int M, N, K, splits;
+};
+
+struct RowInfo {
+  long long off;  // element offset of the pixel's image (b) in S
+  int y, x;       // buffer coordinates before the tap offset
+};
+
+template <int KIND, int BN, int MODE>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr bool LOADS = MODE == 2 || MODE == 3;
+  static constexpr int NBUF = KIND == 1 ? (LOADS ? 3 : 2) : 0;
+  static constexpr int D_OFF = 4096;
+  static constexpr int BUF_BYTES = MODE == 3 ? 6144 : 4096;
+  static constexpr int EPI_BYTES = 4 * NBUF * BUF_BYTES;
+  static constexpr int ROWS = KIND == 0 ? BM : BK;
+  static constexpr int ROW_BYTES = 2 * ROWS * (int)sizeof(RowInfo);
+  static constexpr int FIT = (SMEM_MAX - 1024 - 512 - EPI_BYTES - ROW_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = FIT > 6 ? 6 : FIT;
+  static constexpr int TMEM_COLS = BN * 2;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + ROW_BYTES + 1024 + 512;
+  static_assert(STAGES > LAG, "pipeline too shallow for the gather lag");
+  static_assert(SMEM <= SMEM_MAX, "smem");
+};
+
+__device__ __forceinline__ RowInfo pixel_info(const tofu_conv_args& a, int g, int ngyx) {
+  RowInfo ri;
+  const int gb = g / ngyx, rem = g - gb * ngyx;
+  const int gy = rem / a.ngx, gx = rem - gy * a.ngx;
+  ri.off = (long long)(gb + a.sb0) * a.s_sb;
+  ri.y = a.ay * gy + a.cy;
+  ri.x = a.ax * gx + a.cx;
+  return ri;
+}
+
+template <int KIND, int BN, bool B_MN, int MODE>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    conv_kernel(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap tmDense,
+                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD) {
+  using C_ = Cfg<KIND, BN, MODE>;
+  constexpr int STAGES = C_::STAGES;
+  constexpr int NBUF = C_::NBUF;
+  const tofu_conv_args& a = P.a;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C_::A_BYTES;
+  uint8_t* sE = smem + STAGES * C_::STAGE_BYTES;
+  RowInfo* rows = reinterpret_cast<RowInfo*>(sE + C_::EPI_BYTES);  // [2][ROWS]
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(rows) + C_::ROW_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* ebar = acc_empty + 2;  // [4][NBUF]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 4 * (NBUF > 0 ? NBUF : 1));
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int M = P.M, N = P.N, K = P.K, splits = P.splits;
+  const int tiles_m = (M + BM - 1) / BM;
+  const int tiles_n = (N + BN - 1) / BN;
+  const int nk = (K + BK - 1) / BK;
+  const int nunits = tiles_m * tiles_n * splits;
+  auto kb_lo = [&](int sp) { return (int)((int64_t)sp * nk / splits); };
+  const int ngyx = a.ngy * a.ngx;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1 + NGATHER);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);
+    }
+    for (int b = 0; b < 4 * NBUF; ++b) mbar_init(&ebar[b], 1);
+    fence_mbar_init();
+    tma_prefetch_desc(&tmDense);
+    if (KIND == 1) tma_prefetch_desc(&tmC);
+    if (MODE == 3) tma_prefetch_desc(&tmD);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C_::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (dense operand)
+    if (lane == 0) {
+      int it = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int tile = u / splits, sp = u % splits;
+        const int m0 = (tile / tiles_n) * BM;
+        const int n0 = (tile % tiles_n) * BN;
+        for (int kb = kb_lo(sp); kb < kb_lo(sp + 1); ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          const int k0 = kb * BK;
+          if constexpr (KIND == 0) {
+            mbar_arrive_expect_tx(&full[s], C_::B_BYTES);
+            uint8_t* b = sB + s * C_::B_BYTES;
+            if (!B_MN) {  // W[n][taps][c]: columns tap_w[t]*b_tap + c
+              const int col = (a.nch % BK == 0) ? a.tap_w[k0 / a.nch] * a.b_tap + k0 % a.nch : k0;
+              tma_load_2d(b, &tmDense, &full[s], col, n0);
+            } else {      // W[c][taps][n]: rows = the K channels of one tap, columns tap_w[t]*b_tap + n
+              // nch >= 64: one tap per k-block; nch in {8,16,32}: 64/nch taps, one box of nch rows each
+              const int bk = a.nch < BK ? a.nch : BK;
+              for (int h = 0; h < BK / bk; ++h) {
+                const int k = k0 + h * bk;
+                int t = k / a.nch;
+                if (t >= a.ntaps) t = a.ntaps - 1;  // K tail: the gathered rows there are zero
+                const int c = k % a.nch;
+#pragma unroll
+                for (int q = 0; q < BN / 64; ++q)
+                  tma_load_2d(b + q * 8192 + h * bk * 128, &tmDense, &full[s], a.tap_w[t] * a.b_tap + n0 + 64 * q, c);
+              }
+            }
+          } else {
+            mbar_arrive_expect_tx(&full[s], C_::A_BYTES);
+            uint8_t* aa = sA + s * C_::A_BYTES;
+#pragma unroll
+            for (int q = 0; q < BM / 64; ++q) tma_load_2d(aa + q * 8192, &tmDense, &full[s], m0 + 64 * q, k0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr bool A_MN = KIND == 1;
+      constexpr bool BMN = KIND == 1 ? true : B_MN;
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN ? 1 : 0, BMN ? 1 : 0);
+      int it = 0, local = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++local) {
+        const int sp = u % splits;
+        const int kb0 = kb_lo(sp);
+        const int buf = local & 1;
+        mbar_wait(&acc_empty[buf], ((local >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + buf * BN;
+        for (int kb = kb0; kb < kb_lo(sp + 1); ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&full[s], (it / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + s * C_::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + s * C_::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = A_MN ? umma_sdesc_sw128(a0 + kk * 2048, 8192, 1024)
+                                     : umma_sdesc_sw128(a0 + kk * 32, 16, 1024);
+            const uint64_t bd = BMN ? umma_sdesc_sw128(b0 + kk * 2048, 8192, 1024)
+                                    : umma_sdesc_sw128(b0 + kk * 32, 16, 1024);
+            umma_bf16(tmem_d, ad, bd, idesc, (kb > kb0 || kk) ? 1u : 0u);
+          }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&acc_full[buf]);
+      }
+    }
+  } else if (warp >= 6) {
+    // ------------------------------------------------------------ gather producers (64 threads)
+    const int gt = threadIdx.x - 192;
+    int it = 0, local = 0;
+    auto publish = [&](int upto) {  // stages < upto whose copies have landed: publish to the MMA
+      fence_proxy_async_smem();
+      mbar_arrive(&full[upto % STAGES]);
+    };
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++local) {
+      const int tile = u / splits, sp = u % splits;
+      const int m0 = (tile / tiles_n) * BM;
+      const int n0 = (tile % tiles_n) * BN;
+      if constexpr (KIND == 0) {
+        RowInfo* ri = rows + (local & 1) * BM;
+        for (int r = gt; r < BM; r += NGATHER) {
+          const int m = m0 + r;
+          if (m < M) {
+            ri[r] = pixel_info(a, m, ngyx);
+          } else {
+            ri[r].off = 0;
+            ri[r].y = ri[r].x = -(1 << 29);
+          }
+        }
+        named_bar_sync(1, NGATHER);
+        const int j = gt & 7;
+        for (int kb = kb_lo(sp); kb < kb_lo(sp + 1); ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          const int k = kb * BK + j * 8;
+          const int t = k / a.nch, c = k - t * a.nch;
+          const bool tv = t < a.ntaps;
+          const int dy = tv ? a.tap_dy[t] : 0, dx = tv ? a.tap_dx[t] : 0;
+          const __nv_bfloat16* S = reinterpret_cast<const __nv_bfloat16*>(a.S) + a.sc0 + c;
+          uint8_t* dst = sA + s * C_::A_BYTES;
+#pragma unroll 4
+          for (int i = 0; i < BM / 8; ++i) {
+            const int r = (gt >> 3) + 8 * i;
+            const RowInfo q = ri[r];
+            const int iy = q.y + dy, ix = q.x + dx;
+            const bool ok = tv && (unsigned)iy < (unsigned)a.sH && (unsigned)ix < (unsigned)a.sW;
+            const __nv_bfloat16* src = ok ? S + q.off + iy * a.s_sy + ix * a.s_sx : S;
+            cp_async_16(dst + r * 128 + ((j ^ (r & 7)) << 4), src, ok ? 16u : 0u);
+          }
+          cp_async_commit();
+          if (it >= LAG) {
+            cp_async_wait<LAG>();
+            publish(it - LAG);
+          }
+        }
+      } else {
+        constexpr int CPR = BN / 8;           // 16-byte chunks per k row
+        constexpr int RSTEP = NGATHER / CPR;  // rows covered per pass
+        const int jj = gt % CPR;
+        const int n = n0 + jj * 8;
+        const int t = n / a.nch, c = n - t * a.nch;
+        const bool tv = n < N && t < a.ntaps;
+        const int dy = tv ? a.tap_dy[t] : 0, dx = tv ? a.tap_dx[t] : 0;
+        const __nv_bfloat16* S = reinterpret_cast<const __nv_bfloat16*>(a.S) + a.sc0 + c;
+        const int sub = jj >> 3, j = jj & 7;
+        for (int kb = kb_lo(sp); kb < kb_lo(sp + 1); ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          RowInfo* ri = rows + (it & 1) * BK;
+          {
+            const int g = kb * BK + gt;
+            if (g < K) {
+              ri[gt] = pixel_info(a, g, ngyx);
+            } else {
+              ri[gt].off = 0;
+              ri[gt].y = ri[gt].x = -(1 << 29);
+            }
+          }
+          named_bar_sync(1, NGATHER);
+          uint8_t* dst = sB + s * C_::B_BYTES + sub * 8192;
+#pragma unroll 4
+          for (int i = 0; i < BK / RSTEP; ++i) {
+            const int r = gt / CPR + RSTEP * i;
+            const RowInfo q = ri[r];
+            const int iy = q.y + dy, ix = q.x + dx;
+            const bool ok = tv && (unsigned)iy < (unsigned)a.sH && (unsigned)ix < (unsigned)a.sW;
+            const __nv_bfloat16* src = ok ? S + q.off + iy * a.s_sy + ix * a.s_sx : S;
+            cp_async_16(dst + r * 128 + ((j ^ (r & 7)) << 4), src, ok ? 16u : 0u);
+          }
+          cp_async_commit();
+          if (it >= LAG) {
+            cp_async_wait<LAG>();
+            publish(it - LAG);
+          }
+        }
+      }
+    }
+    cp_async_wait<0>();
+    for (int q = it - LAG < 0 ? 0 : it - LAG; q < it; ++q) publish(q);
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 2..5)
+    const int q = warp & 3;
+    constexpr int NCH = BN / 32;
+    if constexpr (KIND == 0) {
+      int local = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++local) {
+        const int tile = u / splits;
+        const int m0 = (tile / tiles_n) * BM;
+        const int n0 = (tile % tiles_n) * BN;
+        const int acc = local & 1;
+        mbar_wait(&acc_full[acc], (local >> 1) & 1);
+        tc_fence_after();
+        const int m = m0 + q * 32 + lane;
+        char* rowp = nullptr;
+        if (m < M) {
+          const int gb = m / ngyx, rem = m - gb * ngyx;
+          const int gy = rem / a.ngx, gx = rem - gy * a.ngx;
+          const int64_t e = (int64_t)gb * a.c_sb + (int64_t)(a.c_ys * gy + a.c_y0) * a.c_sy +
+                            (int64_t)(a.c_xs * gx + a.c_x0) * a.c_sx;
+          rowp = reinterpret_cast<char*>(a.C) + e * (MODE == 0 ? 2 : 4);
+        }
+        for (int c = 0; c < NCH; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, r);
+          tmem_ld_wait();
+          if (c == NCH - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[acc]);
+          }
+          const int n = n0 + c * 32;
+          if (!rowp || n >= N) continue;
+          if (MODE == 0) {
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(rowp) + n;
+            if (n + 32 <= N) {
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                uint4 w;
+                uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                  __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(r[8 * v + 2 * h]),
+                                                            __uint_as_float(r[8 * v + 2 * h + 1]));
+                  wp[h] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+                reinterpret_cast<uint4*>(o)[v] = w;
+              }
+            } else {
+              for (int e = 0; e < N - n; ++e) o[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
+            }
+          } else {
+            float* o = reinterpret_cast<float*>(rowp) + n;
+            if (n + 32 <= N) {
+#pragma unroll
+              for (int v = 0; v < 8; ++v)
+                reinterpret_cast<float4*>(o)[v] = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                                              __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+            } else {
+              for (int e = 0; e < N - n; ++e) o[e] = __uint_as_float(r[e]);
+            }
+          }
+        }
+      }
+    } else {
+      // TMA-store epilogue (fp32 chunks of 32 x 32 through swizzled smem), as gemm_tcgen05.cu
+      const int my_units = blockIdx.x < nunits ? (nunits - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+      const int S = my_units * NCH;
+      uint8_t* wbuf = sE + q * NBUF * C_::BUF_BYTES;
+      uint64_t* wbar = ebar + q * NBUF;
+      int split_of_chunk = 0;
+      auto chunk_coords = [&](int s, int& col, int& row) {
+        const int u = blockIdx.x + (s / NCH) * gridDim.x;
+        const int tile = u / splits;
+        split_of_chunk = u % splits;
+        col = (tile % tiles_n) * BN + (s % NCH) * 32;
+        row = (tile / tiles_n) * BM + q * 32;
+      };
+      auto issue_load = [&](int s) {
+        int col, row;
+        chunk_coords(s, col, row);
+        uint8_t* b = wbuf + (s % NBUF) * C_::BUF_BYTES;
+        mbar_arrive_expect_tx(&wbar[s % NBUF], MODE == 3 ? 6144 : 4096);
+        tma_load_2d(b, &tmC, &wbar[s % NBUF], col, row);
+        if (MODE == 3) tma_load_2d(b + C_::D_OFF, &tmD, &wbar[s % NBUF], col, row);
+      };
+      if (C_::LOADS && lane == 0)
+        for (int s = 0; s < NBUF - 1 && s < S; ++s) issue_load(s);
+      int local = 0;
+      for (int s = 0; s < S; ++s) {
+        const int c = s % NCH;
+        const int acc = local & 1;
+        if (c == 0) {
+          mbar_wait(&acc_full[acc], (local >> 1) & 1);
+          tc_fence_after();
+        }
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, r);
+        tmem_ld_wait();
+        if (c == NCH - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[acc]);
+          ++local;
+        }
+        uint8_t* b = wbuf + (s % NBUF) * C_::BUF_BYTES;
+        if (C_::LOADS) {
+          if (lane == 0 && s + NBUF - 1 < S) {
+            bulk_wait_read<0>();
+            issue_load(s + NBUF - 1);
+          }
+          __syncwarp();
+          mbar_wait(&wbar[s % NBUF], (s / NBUF) & 1);
+        } else {
+          if (lane == 0) bulk_wait_read<(NBUF > 0 ? NBUF - 1 : 0)>();
+          __syncwarp();
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4* slot = reinterpret_cast<float4*>(b + lane * 128 + ((j ^ (lane & 7)) << 4));
+          float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                                 __uint_as_float(r[4 * j + 3]));
+          if (MODE == 2) {
+            const float4 o = *slot;
+            v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+          } else if (MODE == 3) {
+            const float4 o = *slot;
+            v = make_float4(o.x * a.s0 + v.x, o.y * a.s0 + v.y, o.z * a.s0 + v.z, o.w * a.s0 + v.w);
+          }
+          *slot = v;
+          if (MODE == 3) {
+            const int wj = j >> 1, half = j & 1;
+            uint2* wslot = reinterpret_cast<uint2*>(b + C_::D_OFF + lane * 64 + ((wj ^ ((lane >> 1) & 3)) << 4)) + half;
+            const uint2 wv = *wslot;
+            float2 w0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv.x));
+            float2 w1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv.y));
+            __nv_bfloat162 o0 = __floats2bfloat162_rn(w0.x - v.x * a.s1, w0.y - v.y * a.s1);
+            __nv_bfloat162 o1 = __floats2bfloat162_rn(w1.x - v.z * a.s1, w1.y - v.w * a.s1);
+            *wslot = make_uint2(*reinterpret_cast<uint32_t*>(&o0), *reinterpret_cast<uint32_t*>(&o1));
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          int col, row;
+          chunk_coords(s, col, row);
+          if (MODE == 4) tma_store_3d(&tmC, b, col, row, split_of_chunk);
+          else tma_store_2d(&tmC, b, col, row);
+          if (MODE == 3) tma_store_2d(&tmD, b + C_::D_OFF, col, row);
+          bulk_commit();
+        }
+      }
+      if (lane == 0) bulk_wait<0>();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C_::TMEM_COLS);
+  }
+}
+
+// Split-K reduction of the weight gradient: C = epilogue(Σ_s WS[s]) in split order; mode 1 store,
+// 2 accumulate, 3 fused momentum-SGD (C momentum in/out, D bf16 weight in/out).
+__global__ void __launch_bounds__(256) splitk_reduce(const float* __restrict__ ws, int splits, int M, int N, float* C,
+                                                     int64_t ldc, int mode, __nv_bfloat16* D, int64_t ldd, float s0,
+                                                     float s1) {
+  const int64_t plane = (int64_t)M * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < plane; i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = ws[i];
+    for (int s = 1; s < splits; ++s) acc += ws[s * plane + i];
+    const int64_t m = i / N, n = i % N;
+    float* c = C + m * ldc + n;
+    if (mode == 1) *c = acc;
+    else if (mode == 2) *c += acc;
+    else {
+      const float mm = *c * s0 + acc;
+      *c = mm;
+      __nv_bfloat16* w = D + m * ldd + n;
+      *w = __float2bfloat16_rn(__bfloat162float(*w) - mm * s1);
+    }
+  }
+}
+
+// zero output rows of a kind-0 sub-op with no taps (e.g. the odd phases of a 1x1 stride-2 data gradient)
+__global__ void __launch_bounds__(256) zero_rows(Params P) {
+  const tofu_conv_args& a = P.a;
+  const int ngyx = a.ngy * a.ngx;
+  const int64_t total = (int64_t)P.M * P.N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i / P.N), n = (int)(i % P.N);
+    const int gb = m / ngyx, rem = m - gb * ngyx;
+    const int gy = rem / a.ngx, gx = rem - gy * a.ngx;
+    const int64_t e = (int64_t)gb * a.c_sb + (int64_t)(a.c_ys * gy + a.c_y0) * a.c_sy +
+                      (int64_t)(a.c_xs * gx + a.c_x0) * a.c_sx + n;
+    if (a.c_mode == 0) reinterpret_cast<__nv_bfloat16*>(a.C)[e] = __float2bfloat16_rn(0.f);
+    else reinterpret_cast<float*>(a.C)[e] = 0.f;
+  }
+}
+
+// ------------------------------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::once_flag g_once;
+static int g_sms = 148;
+
+static int init() {
+  std::call_once(g_once, []() {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+  });
+  return g_encode ? 0 : -1;
+}
+
+static int tmap2(CUtensorMap* tm, const void* ptr, CUtensorMapDataType dt, int es, uint64_t inner, uint64_t outer,
+                 uint64_t ld, uint32_t bi, uint32_t bo, CUtensorMapSwizzle sw) {
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * es};
+  cuuint32_t box[2] = {bi, bo};
+  cuuint32_t estr[2] = {1, 1};
+  return g_encode(tm, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
+             ? 0
+             : 1;
+}
+
+static int bn_of(const tofu_conv_args* a, int N) {
+  if (a->kind == 1) return 128;
+  return N <= 128 ? 128 : 256;
+}
+
+static void dims_of(const tofu_conv_args* a, int& M, int& N, int& K) {
+  const int pix = a->nb * a->ngy * a->ngx;
+  if (a->kind == 0) {
+    M = pix;
+    N = a->n_out;
+    K = a->ntaps * a->nch;
+  } else {
+    M = a->m_out;
+    N = a->ntaps * a->nch;
+    K = pix;
+  }
+}
+
+static int auto_splits(const tofu_conv_args* a, int M, int N, int K, int bn) {
+  if (a->kind != 1 || a->splits == 1) return 1;
+  const int nk = (K + BK - 1) / BK;
+  if (a->splits > 1) return a->splits < nk ? a->splits : nk;
+  const int tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+  if (tiles * 2 > g_sms || nk < 8) return 1;
+  int sp = g_sms / tiles;
+  if (sp > nk / 4) sp = nk / 4;
+  if (sp > 32) sp = 32;
+  return sp < 2 ? 1 : sp;
+}
+
+template <int KIND, int BN, bool B_MN, int MODE>
+static int launch_t(const Params& P, const CUtensorMap* tm, cudaStream_t st) {
+  using C_ = Cfg<KIND, BN, MODE>;
+  auto kern = conv_kernel<KIND, BN, B_MN, MODE>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM) != cudaSuccess)
+      return TOFU_ERR_CUDA;
+    attr = true;
+  }
+  const int units = ((P.M + BM - 1) / BM) * ((P.N + BN - 1) / BN) * P.splits;
+  const int grid = units < g_sms ? units : g_sms;
+  kern<<<grid, NTHREADS, C_::SMEM, st>>>(P, tm[0], tm[1], tm[2]);
+  return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
+}
+
+static int dispatch(const Params& P, const CUtensorMap* tm, int mode, cudaStream_t st) {
+  const tofu_conv_args& a = P.a;
+  const int bn = bn_of(&a, P.N);
+  if (a.kind == 0) {
+    const int key = (bn == 256 ? 1 : 0) | (a.b_mn_major ? 2 : 0) | (mode << 2);
+    switch (key) {
+      case 0: return launch_t<0, 128, false, 0>(P, tm, st);
+      case 1: return launch_t<0, 256, false, 0>(P, tm, st);
+      case 2: return launch_t<0, 128, true, 0>(P, tm, st);
+      case 3: return launch_t<0, 256, true, 0>(P, tm, st);
+      case 4: return launch_t<0, 128, false, 1>(P, tm, st);
+      case 5: return launch_t<0, 256, false, 1>(P, tm, st);
+      case 6: return launch_t<0, 128, true, 1>(P, tm, st);
+      case 7: return launch_t<0, 256, true, 1>(P, tm, st);
+      default: return TOFU_ERR_ARG;
+    }
+  }
+  switch (mode) {
+    case 1: return launch_t<1, 128, true, 1>(P, tm, st);
+    case 2: return launch_t<1, 128, true, 2>(P, tm, st);
+    case 3: return launch_t<1, 128, true, 3>(P, tm, st);
+    case 4: return launch_t<1, 128, true, 4>(P, tm, st);
+    default: return TOFU_ERR_ARG;
+  }
+}
+
+}  // namespace conv
+}  // namespace tofu
+
+using namespace tofu::conv;
+
+extern "C" int64_t tofu_conv_workspace_bytes(const tofu_conv_args* a) {
+  int M, N, K;
+  dims_of(a, M, N, K);
+  return a->kind == 1 && a->splits > 1 ? (int64_t)a->splits * M * N * 4 : 0;
+}
+
+// tmaps: 4 x CUtensorMap (dense operand, C, D, split-K workspace)
+extern "C" int tofu_conv_plan(tofu_conv_args* a, void* tmaps) {
+  if (init() != 0) return TOFU_ERR_CUDA;
+  if (!a || a->kind < 0 || a->kind > 1 || a->ntaps < 0 || a->ntaps > TOFU_CONV_MAX_TAPS || a->nch <= 0 ||
+      a->nb < 0 || a->ngy < 0 || a->ngx < 0)
+    return TOFU_ERR_ARG;
+  if (a->nch % 8 || a->sc0 % 8 || a->s_sx % 8 || a->s_sy % 8 || a->s_sb % 8) return TOFU_ERR_ALIGN;
+  auto mis = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) != 0; };
+  if (mis(a->S) || mis(a->C) || mis(a->Bp) || mis(a->Ap) || mis(a->D)) return TOFU_ERR_ALIGN;
+  int M, N, K;
+  dims_of(a, M, N, K);
+  CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(tmaps);
+  const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const auto SW128 = CU_TENSOR_MAP_SWIZZLE_128B;
+  const int bn = bn_of(a, N);
+  if (a->kind == 0) {
+    if (a->c_mode != 0 && a->c_mode != 1) return TOFU_ERR_ARG;
+    if (a->nch % BK != 0 && !a->b_mn_major) {  // K columns contiguous: taps in natural order, b_tap == nch
+      if (a->b_tap != a->nch) return TOFU_ERR_ARG;
+      for (int t = 0; t < a->ntaps; ++t)
+        if (a->tap_w[t] != t) return TOFU_ERR_ARG;
+    }
+    if (a->ldb % 8) return TOFU_ERR_ALIGN;
+    if (a->ntaps > 0) {
+      if (a->b_mn_major && a->nch < BK && BK % a->nch) return TOFU_ERR_ARG;
+      const uint32_t bk = a->nch < BK ? a->nch : BK;
+      const int r = !a->b_mn_major ? tmap2(&tm[0], a->Bp, BF, 2, a->b_cols, a->b_rows, a->ldb, 64, bn, SW128)
+                                   : tmap2(&tm[0], a->Bp, BF, 2, a->b_cols, a->b_rows, a->ldb, 64, bk, SW128);
+      if (r) return TOFU_ERR_CUDA;
+    }
+    tm[1] = tm[2] = tm[0];
+    a->splits = 1;
+    return TOFU_OK;
+  }
+  // kind 1: A = output gradient [K pixels][M channels] MN-major; C f32 [M][N]
+  if (a->c_mode < 1 || a->c_mode > 3 || (a->lda % 8) || (a->ldc % 4)) return TOFU_ERR_ALIGN;
+  if (a->c_mode == 3 && (!a->D || a->ldd % 8)) return TOFU_ERR_ARG;
+  a->splits = auto_splits(a, M, N, K, bn);
+  if (tmap2(&tm[0], a->Ap, BF, 2, M, K, a->lda, 64, 64, SW128)) return TOFU_ERR_CUDA;
+  if (tmap2(&tm[1], a->C, F32, 4, N, M, a->ldc, 32, 32, SW128)) return TOFU_ERR_CUDA;
+  if (a->c_mode == 3) {
+    if (tmap2(&tm[2], a->D, BF, 2, N, M, a->ldd, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return TOFU_ERR_CUDA;
+  } else {
+    tm[2] = tm[1];
+  }
+  if (a->splits > 1) {
+    if (!a->ws || (N * 4) % 16) return TOFU_ERR_ARG;
+    cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)M, (cuuint64_t)a->splits};
+    cuuint64_t strides[2] = {(cuuint64_t)N * 4, (cuuint64_t)N * M * 4};
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (g_encode(&tm[3], F32, 3, a->ws, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, SW128,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return TOFU_ERR_CUDA;
+  }
+  return TOFU_OK;
+}
+
+extern "C" int tofu_conv_launch_planned(const tofu_conv_args* a, const void* tmaps, void* stream) {
+  int M, N, K;
+  dims_of(a, M, N, K);
+  if (M == 0 || N == 0) return TOFU_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Params P;
+  P.a = *a;
+  P.M = M;
+  P.N = N;
+  P.K = K;
+  P.splits = a->splits > 1 ? a->splits : 1;
+  const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(tmaps);
+  if (K == 0) {
+    if (a->kind == 1) {
+      if (a->c_mode == 1) return cudaMemset2DAsync(a->C, a->ldc * 4, 0, (size_t)N * 4, M, st) == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
+      return a->c_mode == 2 ? TOFU_OK : TOFU_ERR_ARG;
+    }
+    int blocks = (int)(((int64_t)M * N + 255) / 256);
+    if (blocks > g_sms * 8) blocks = g_sms * 8;
+    zero_rows<<<blocks, 256, 0, st>>>(P);
+    return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
+  }
+  if (a->kind == 0) return dispatch(P, tm, a->c_mode, st);
+  if (P.splits > 1) {
+    const CUtensorMap tw[3] = {tm[0], tm[3], tm[3]};
+    int rc = dispatch(P, tw, 4, st);
+    if (rc) return rc;
+    int blocks = (int)(((int64_t)M * N + 255) / 256);
+    if (blocks > g_sms * 8) blocks = g_sms * 8;
+    splitk_reduce<<<blocks, 256, 0, st>>>(reinterpret_cast<const float*>(a->ws), P.splits, M, N,
+                                          reinterpret_cast<float*>(a->C), a->ldc, a->c_mode,
+                                          reinterpret_cast<__nv_bfloat16*>(a->D), a->ldd, a->s0, a->s1);
+    return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
+  }
+  return dispatch(P, tm, a->c_mode, st);
+}
+
+extern "C" int tofu_conv_bf16(const tofu_conv_args* args, void* stream) {
+  alignas(64) CUtensorMap tm[4];
+  tofu_conv_args a = *args;
+  void* own_ws = nullptr;
+  int r = tofu_conv_plan(&a, tm);
+  if (r == TOFU_ERR_ARG && a.kind == 1 && a.splits > 1 && !a.ws) {
+    // library-owned workspace for the one-shot entry point (not CUDA-graph safe)
+    if (cudaMalloc(&own_ws, tofu_conv_workspace_bytes(&a)) != cudaSuccess) return TOFU_ERR_CUDA;
+    a.ws = own_ws;
+    r = tofu_conv_plan(&a, tm);
+  }
+  if (!r) r = tofu_conv_launch_planned(&a, tm, stream);
+  if (own_ws) {
+    cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream));
+    cudaFree(own_ws);
+  }
+  return r;
+}

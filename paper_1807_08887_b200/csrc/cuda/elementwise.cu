@@ -37,7 +37,8 @@ __global__ void __launch_bounds__(256) ew_kernel(int64_t n, void* __restrict__ y
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += stride) {
     const int64_t i = v * 8;
     float a[8], b[8], o[8];
-    if (KIND == TOFU_EW_RELU || KIND == TOFU_EW_RELU_GRAD || KIND == TOFU_EW_MSE_GRAD || KIND == TOFU_EW_SUMSQ) {
+    if (KIND == TOFU_EW_RELU || KIND == TOFU_EW_RELU_GRAD || KIND == TOFU_EW_MSE_GRAD || KIND == TOFU_EW_SUMSQ ||
+        KIND == TOFU_EW_ADD || KIND == TOFU_EW_ADDRELU) {
       unpack8(reinterpret_cast<const uint4*>(x0)[v], a);
       if (KIND != TOFU_EW_RELU) unpack8(reinterpret_cast<const uint4*>(x1)[v], b);
 #pragma unroll
@@ -46,6 +47,8 @@ __global__ void __launch_bounds__(256) ew_kernel(int64_t n, void* __restrict__ y
         if (KIND == TOFU_EW_RELU_GRAD) o[j] = a[j] > 0.f ? b[j] : 0.f;
         if (KIND == TOFU_EW_MSE_GRAD) o[j] = (a[j] - b[j]) * s0;
         if (KIND == TOFU_EW_SUMSQ) { const float d = a[j] - b[j]; local += d * d * s0; }
+        if (KIND == TOFU_EW_ADD) o[j] = a[j] + b[j];
+        if (KIND == TOFU_EW_ADDRELU) o[j] = fmaxf(a[j] + b[j], 0.f);
       }
       if (KIND != TOFU_EW_SUMSQ) reinterpret_cast<uint4*>(y)[v] = pack8(o);
     } else if (KIND == TOFU_EW_MOM) {
@@ -93,6 +96,11 @@ __global__ void __launch_bounds__(256) ew_kernel(int64_t n, void* __restrict__ y
       if (KIND == TOFU_EW_MSE_GRAD)
         reinterpret_cast<__nv_bfloat16*>(y)[i] = __float2bfloat16_rn((__bfloat162float(xb0[i]) - __bfloat162float(xb1[i])) * s0);
       if (KIND == TOFU_EW_SUMSQ) { const float d = __bfloat162float(xb0[i]) - __bfloat162float(xb1[i]); local += d * d * s0; }
+      if (KIND == TOFU_EW_ADD)
+        reinterpret_cast<__nv_bfloat16*>(y)[i] = __float2bfloat16_rn(__bfloat162float(xb0[i]) + __bfloat162float(xb1[i]));
+      if (KIND == TOFU_EW_ADDRELU)
+        reinterpret_cast<__nv_bfloat16*>(y)[i] =
+            __float2bfloat16_rn(fmaxf(__bfloat162float(xb0[i]) + __bfloat162float(xb1[i]), 0.f));
       if (KIND == TOFU_EW_MOM)
         reinterpret_cast<float*>(y)[i] = reinterpret_cast<const float*>(x0)[i] * s0 + reinterpret_cast<const float*>(x1)[i];
       if (KIND == TOFU_EW_SGD)
@@ -140,7 +148,7 @@ extern "C" int tofu_elementwise(int kind, int64_t n, void* y, const void* x0, co
   switch (kind) {
 #define K(X) case X: tofu::ew_kernel<X><<<(unsigned)grid, 256, 0, st>>>(n, y, x0, x1, x2, s0, s1); break;
     K(TOFU_EW_RELU) K(TOFU_EW_RELU_GRAD) K(TOFU_EW_MSE_GRAD) K(TOFU_EW_MOM) K(TOFU_EW_SGD) K(TOFU_EW_SGD_MOM)
-    K(TOFU_EW_SUMSQ)
+    K(TOFU_EW_SUMSQ) K(TOFU_EW_ADD) K(TOFU_EW_ADDRELU)
 #undef K
     default: return TOFU_ERR_ARG;
   }

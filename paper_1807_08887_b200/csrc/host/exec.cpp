@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -156,6 +157,11 @@ struct Exec {
     int bn;
   };
   std::map<std::pair<int, int>, GemmLaunch> gemms;  // (op, li)
+  struct ConvLaunch {
+    tofu_conv_args a;
+    alignas(64) CUtensorMap tm[4];
+  };
+  std::map<std::pair<int, int>, std::vector<ConvLaunch>> convs;  // (op, li) -> launches (4 phases: stride-2 dgrad)
   int64_t ledger_el = 0, ledger_bytes = 0;
   int64_t n_kernels = 0;
   bool skip_comm = false;
@@ -184,7 +190,7 @@ GemmForm gemm_form(const OpDef& d) {
   if (!d.prod2 || d.accesses.size() != 2) return f;
   auto vars_of = [&](const Access& a, std::vector<int>& out) {
     for (size_t k = 0; k < a.idx.size(); ++k) {
-      if (a.slice[k] || a.idx[k].coef.size() != 1 || a.idx[k].coef[0].second != 1 || a.idx[k].c != 0) return false;
+      if (a.slice[k] || !a.idx[k].plain() || a.idx[k].coef.size() != 1 || a.idx[k].coef[0].second != 1 || a.idx[k].c != 0) return false;
       out.push_back(a.idx[k].coef[0].first);
     }
     return true;
@@ -244,16 +250,100 @@ bool flat2(const std::vector<Rng>& buf, const std::vector<Rng>& box, int split, 
   return true;
 }
 
+// Convolution defs (tofu_inputs.graphs.conv_defs, reading R11): recognised by name AND checked to be the
+// canonical convolution by re-deriving its TDL from (kind, R, s, p) and comparing every access index.
+struct ConvGeom {
+  int kind = -1;  // 0 forward, 1 data gradient, 2 weight gradient
+  int R = 0, s = 0, p = 0;
+};
+
+std::string conv_tdl(int kind, int R, int s, int p) {
+  const std::string n = "k" + std::to_string(R) + "s" + std::to_string(s) + "p" + std::to_string(p);
+  const std::string P = std::to_string(p);
+  const std::string sy = s == 1 ? "y" : std::to_string(s) + "*y", sx = s == 1 ? "x" : std::to_string(s) + "*x";
+  if (kind == 0)
+    return "def conv_" + n + "(X(4), W(4)) -> lambda b, y, x, co: reduce(Sum; ky, kx, ci; X[b, " + sy + " + ky - " + P +
+           ", " + sx + " + kx - " + P + ", ci] * W[co, ky, kx, ci])";
+  if (kind == 2)
+    return "def wconv_" + n + "(D(4), X(4)) -> lambda co, ky, kx, ci: reduce(Sum; b, y, x; D[b, y, x, co] * X[b, " + sy +
+           " + ky - " + P + ", " + sx + " + kx - " + P + ", ci])";
+  if (s == 1)
+    return "def dconv_" + n + "(D(4), W(4)) -> lambda b, y, x, ci: reduce(Sum; ky, kx, co; D[b, y - ky + " + P +
+           ", x - kx + " + P + ", co] * W[co, ky, kx, ci])";
+  return "def dconv_" + n + "(D(4), W(4)) -> lambda b, y, x, ci: reduce(Sum; ty, tx, co; D[b, (y - 2*ty + " + P +
+         ") / 2, (x - 2*tx + " + P + ") / 2, co] * W[co, (y + " + P + ") % 2 + 2*ty, (x + " + P + ") % 2 + 2*tx, ci])";
+}
+
+bool same_access(const Access& a, const Access& b) {
+  if (a.param != b.param || a.idx.size() != b.idx.size()) return false;
+  for (size_t k = 0; k < a.idx.size(); ++k) {
+    const Affine &x = a.idx[k], &y = b.idx[k];
+    if (x.coef != y.coef || x.c != y.c || x.terms.size() != y.terms.size()) return false;
+    for (size_t q = 0; q < x.terms.size(); ++q) {
+      const auto &u = x.terms[q], &v = y.terms[q];
+      if (u.mod != v.mod || u.mult != v.mult || u.d != v.d || u.inner.coef != v.inner.coef || u.inner.c != v.inner.c)
+        return false;
+    }
+  }
+  return true;
+}
+
+ConvGeom conv_geom(const OpDef& d) {
+  ConvGeom g;
+  int kind = -1, R = 0, s = 0, p = 0;
+  const char* nm = d.name.c_str();
+  if (std::sscanf(nm, "conv_k%ds%dp%d", &R, &s, &p) == 3 && d.name.rfind("conv_", 0) == 0) kind = 0;
+  else if (std::sscanf(nm, "dconv_k%ds%dp%d", &R, &s, &p) == 3) kind = 1;
+  else if (std::sscanf(nm, "wconv_k%ds%dp%d", &R, &s, &p) == 3) kind = 2;
+  if (kind < 0 || R < 1 || s < 1 || s > 2 || p < 0) return g;
+  const OpDef ref = parse_tdl(conv_tdl(kind, R, s, p));
+  if (ref.vars != d.vars || ref.n_out != d.n_out || ref.reducer != d.reducer ||
+      ref.accesses.size() != d.accesses.size())
+    return g;
+  for (size_t q = 0; q < ref.accesses.size(); ++q)
+    if (!same_access(ref.accesses[q], d.accesses[q])) return g;
+  g.kind = kind;
+  g.R = R;
+  g.s = s;
+  g.p = p;
+  return g;
+}
+
 const char* kernel_kind(const OpDef& d) {
-  static const std::set<std::string> ew = {"relu", "relu_grad", "mse_grad", "mom", "sgd", "mom3", "sgd3", "sumsq"};
+  static const std::set<std::string> ew = {"relu",  "relu_grad",  "mse_grad", "mom",  "sgd",     "mom3", "sgd3",
+                                           "sumsq", "relu4",      "relu_grad4", "mom4", "sgd4", "add4", "addrelu"};
   static const std::set<std::string> lstm = {"cell_c", "cell_h", "cell_bwd_a", "cell_bwd_c"};
+  static const std::set<std::string> win = {"maxpool", "maxpool_grad", "gap", "gap_grad"};
   if (gemm_form(d).ok) return "gemm";
   if (ew.count(d.name)) return "ew";
   if (lstm.count(d.name)) return "lstm";
+  if (win.count(d.name)) return "window";
+  if (conv_geom(d).kind >= 0) return "conv";
   return nullptr;
 }
-bool is_mom(const std::string& n) { return n == "mom" || n == "mom3"; }
-bool is_sgd(const std::string& n) { return n == "sgd" || n == "sgd3"; }
+bool is_mom(const std::string& n) { return n == "mom" || n == "mom3" || n == "mom4"; }
+bool is_sgd(const std::string& n) { return n == "sgd" || n == "sgd3" || n == "sgd4"; }
+
+// box == buffer in dims [from, n)
+bool full_from(const std::vector<Rng>& buf, const std::vector<Rng>& box, int from) {
+  for (int d = from; d < (int)buf.size(); ++d)
+    if (box[d].lo != buf[d].lo || box[d].hi != buf[d].hi) return false;
+  return true;
+}
+
+// Can the conv kernel read operand `pi` (box inside buffer buf) in place?  (Staged operands are dense boxes.)
+bool conv_operand_ok(const ConvGeom& cg, int pi, const std::vector<Rng>& buf, const std::vector<Rng>& box) {
+  if (box.size() != 4) return false;
+  const bool gather = (cg.kind == 2) ? pi == 1 : pi == 0;
+  if (gather) return (box[3].lo - buf[3].lo) % 8 == 0 && buf[3].len() % 8 == 0 && box[3].len() % 8 == 0;
+  if (cg.kind == 2) return full_from(buf, box, 1) || (box[1].lo == buf[1].lo && box[1].hi == buf[1].hi &&
+                                                     box[2].lo == buf[2].lo && box[2].hi == buf[2].hi);
+  // weights [co][ky][kx][ci]: all taps present; the forward's K columns (taps x ci) either come in whole
+  // 64-channel blocks per tap or are contiguous (ci not a sub-range)
+  if (box[1].lo != buf[1].lo || box[1].hi != buf[1].hi || box[2].lo != buf[2].lo || box[2].hi != buf[2].hi) return false;
+  if (cg.kind == 0) return box[3].len() % 64 == 0 || (box[3].lo == buf[3].lo && box[3].hi == buf[3].hi);
+  return true;
+}
 
 void lower(Exec& E) {
   const Graph& g = *E.g;
@@ -287,6 +377,8 @@ void lower(Exec& E) {
         const auto& own = E.lay[r].shard_box[t];
         const bool owns = E.lay[r].shard_off[t] >= 0;
         bool usable = owns && (kind == "ew" ? same(own, b.box) : contains(own, b.box));
+        if (usable && kind == "conv") usable = conv_operand_ok(conv_geom(d), (int)pi, own, b.box);
+        if (usable && kind == "window") usable = b.box.size() < 4 || (b.box[3].lo - own[3].lo) % 8 == 0;
         if (usable && kind == "gemm") {
           int64_t r_, c_, ld_, off_;
           const int split = (int)pi == gf.a_param ? gf.a_split : gf.b_split;
@@ -314,6 +406,11 @@ void lower(Exec& E) {
         int64_t r_, c_, ld_, off_;
         odirect = flat2(oown, ob.box, gf.nm, r_, c_, ld_, off_);
       }
+      if (odirect && kind == "conv") {
+        const ConvGeom cg = conv_geom(d);
+        odirect = cg.kind == 2 ? full_from(oown, ob.box, 1) : (ob.box[3].lo - oown[3].lo) % 8 == 0;
+      }
+      if (odirect && kind == "window") odirect = (ob.box.back().lo - oown.back().lo) % 8 == 0;
       if (odirect) {
         ob.direct = true;
         ob.off = E.lay[r].shard_off[t];
@@ -474,7 +571,8 @@ void lower(Exec& E) {
       for (size_t o = 0; o < g.ops.size(); ++o) {
         const OpInfo& a = g.ops[o];
         const char* kk = kernel_kind(g.defs[a.def]);
-        if (!kk || std::string(kk) != "gemm") continue;
+        if (!kk || !(std::string(kk) == "gemm" || (std::string(kk) == "conv" && conv_geom(g.defs[a.def]).kind == 2)))
+          continue;
         int reader = -1, readers = 0;
         for (size_t x = 0; x < g.ops.size(); ++x)
           for (int t : g.ops[x].inputs)
@@ -594,6 +692,8 @@ void build_launches(Exec& E) {
   E.n_kernels = n;
 }
 
+std::vector<tofu_conv_args> conv_args(Exec& E, int o, int li);
+
 void finalize(Exec& E) {
   if (E.finalized) return;
   const Graph& g = *E.g;
@@ -669,6 +769,42 @@ void finalize(Exec& E) {
       if (pass == 1) E.gemms[{(int)o, li}] = G;
     }
   }
+  for (int li = 0; li < nl; ++li)
+    for (size_t o = 0; o < g.ops.size(); ++o) {
+      const OpDef& d = g.def_of((int)o);
+      if (std::string(kernel_kind(d)) != "conv" || E.lops[li][o].skip) continue;
+      LOp& L = E.lops[li][o];
+      std::vector<Exec::ConvLaunch> cls;
+      for (auto& a : conv_args(E, (int)o, li)) {
+        Exec::ConvLaunch C;
+        C.a = a;
+        if (a.kind == 1 && L.fused_opt >= 0) {
+          const int r = E.local[li];
+          const LOp& Lm = E.lops[li][L.fused_opt];      // mom(M, G) -> M_new (in place)
+          const LOp& Ls = E.lops[li][L.fused_opt + 1];  // sgd(W, M_new) -> W_new (in place)
+          if (!full_from(Lm.in[0].buf_box, Lm.in[0].box, 1) || !full_from(Ls.in[0].buf_box, Ls.in[0].box, 1))
+            throw Error(TOFU_ERR_ARG, "fused optimizer operands of op " + g.ops[o].name + " are not row blocks");
+          C.a.c_mode = 3;
+          C.a.C = E.arena[r] + Lm.in[0].off + offset_in(Lm.in[0].buf_box, Lm.in[0].box) * 4;
+          C.a.ldc = strides_of(Lm.in[0].buf_box)[0];
+          C.a.D = E.arena[r] + Ls.in[0].off + offset_in(Ls.in[0].buf_box, Ls.in[0].box) * 2;
+          C.a.ldd = strides_of(Ls.in[0].buf_box)[0];
+          auto at = [&](int op, const char* key) {
+            auto it = g.ops[op].attrs.find(key);
+            return (float)(it == g.ops[op].attrs.end() ? 0.0 : it->second);
+          };
+          C.a.s0 = at(L.fused_opt, "mu");
+          C.a.s1 = at(L.fused_opt + 1, "lr");
+        }
+        C.a.splits = 0;
+        C.a.ws = pass == 0 ? reinterpret_cast<void*>(uintptr_t(1) << 20) : E.ws_dev;
+        const int rc = tofu_conv_plan(&C.a, C.tm);
+        if (rc) throw Error(rc, "conv descriptors for op " + g.ops[o].name + " (geometry/alignment)");
+        ws_need = std::max<int64_t>(ws_need, tofu_conv_workspace_bytes(&C.a));
+        cls.push_back(C);
+      }
+      if (pass == 1) E.convs[{(int)o, li}] = std::move(cls);
+    }
   if (pass == 0 && ws_need > 0 && cudaMalloc(&E.ws_dev, ws_need) != cudaSuccess)
     throw Error(TOFU_ERR_CUDA, "cudaMalloc split-K workspace");
   }
@@ -676,6 +812,241 @@ void finalize(Exec& E) {
 }
 
 bool lo_fused(const Exec& E, const Exec::Launch& L) { return E.lops[L.li][L.op].fused_sgd; }
+
+// tofu_conv_args of one convolution sub-op (op o, local rank li) on its iteration box: the pixel grid, tap
+// table and buffer geometry (DESIGN reading R11; include/tofu.h documents the fields).
+std::vector<tofu_conv_args> conv_args(Exec& E, int o, int li) {
+  const Graph& g = *E.g;
+  const int r = E.local[li];
+  const OpDef& d = g.def_of(o);
+  const ConvGeom cg = conv_geom(d);
+  const LOp& L = E.lops[li][o];
+  std::vector<Rng> ib;
+  iter_box(g, o, E.plan.osplit[o], E.plan.factors, worker_digits(r, E.plan.factors), ib);
+  char* base = E.arena[r];
+  auto es = [](int dt) { return (int64_t)(dt == TOFU_BF16 ? 2 : 4); };
+  auto box_ptr = [&](const Buf& b) { return base + b.off + offset_in(b.buf_box, b.box) * es(b.dtype); };
+  tofu_conv_args a;
+  std::memset(&a, 0, sizeof a);
+  const int R = cg.R, s = cg.s, p = cg.p;
+  // gathered source
+  const Buf& S = L.in[cg.kind == 2 ? 1 : 0];
+  auto st = strides_of(S.buf_box);
+  a.S = base + S.off;
+  a.s_sb = st[0];
+  a.s_sy = st[1];
+  a.s_sx = st[2];
+  a.sH = (int)S.buf_box[1].len();
+  a.sW = (int)S.buf_box[2].len();
+  std::vector<tofu_conv_args> out;
+  if (cg.kind == 0 || cg.kind == 2) {
+    // pixels = output (forward) or reduce (weight gradient) box over (b, y, x); vars b,y,x at 0..2 (fwd) or 4..6
+    const int vb = cg.kind == 0 ? 0 : 4, vky = cg.kind == 0 ? 4 : 1, vci = cg.kind == 0 ? 6 : 3;
+    a.nb = (int)ib[vb].len();
+    a.ngy = (int)ib[vb + 1].len();
+    a.ngx = (int)ib[vb + 2].len();
+    a.sb0 = (int)(ib[vb].lo - S.buf_box[0].lo);
+    a.ay = a.ax = s;
+    a.cy = (int)(s * ib[vb + 1].lo - p - S.buf_box[1].lo);
+    a.cx = (int)(s * ib[vb + 2].lo - p - S.buf_box[2].lo);
+    a.ntaps = 0;
+    for (int64_t ky = ib[vky].lo; ky <= ib[vky].hi; ++ky)
+      for (int64_t kx = ib[vky + 1].lo; kx <= ib[vky + 1].hi; ++kx) {
+        a.tap_dy[a.ntaps] = (short)ky;
+        a.tap_dx[a.ntaps] = (short)kx;
+        a.tap_w[a.ntaps] = (short)(ky * R + kx);
+        ++a.ntaps;
+      }
+    a.nch = (int)ib[vci].len();
+    a.sc0 = (int)(ib[vci].lo - S.buf_box[3].lo);
+    if (cg.kind == 0) {
+      const Buf& W = L.in[1];
+      a.kind = 0;
+      a.n_out = (int)ib[3].len();
+      a.Bp = box_ptr(W);
+      a.ldb = strides_of(W.buf_box)[0];
+      a.b_tap = (int)W.buf_box[3].len();
+      a.b_rows = (int)W.box[0].len();
+      a.b_cols = (int)(a.ldb - (W.box[3].lo - W.buf_box[3].lo));
+      a.b_mn_major = 0;
+      const Buf& O = L.out;
+      auto os = strides_of(O.buf_box);
+      a.C = box_ptr(O);
+      a.c_sb = os[0];
+      a.c_sy = os[1];
+      a.c_sx = os[2];
+      a.c_ys = a.c_xs = 1;
+      a.c_mode = O.dtype == TOFU_F32 ? 1 : 0;
+      out.push_back(a);
+    } else {
+      const Buf& D = L.in[0];
+      a.kind = 1;
+      a.m_out = (int)ib[0].len();
+      a.Ap = box_ptr(D);
+      a.lda = D.buf_box[3].len();
+      const Buf& O = L.out;
+      a.C = box_ptr(O);
+      a.ldc = strides_of(O.buf_box)[0];
+      a.c_mode = 1;  // weight gradients are f32 (partials included)
+      out.push_back(a);
+    }
+    return out;
+  }
+  // data gradient: rows = dX pixels (b, y, x); vars b,y,x,ci = 0..3, (ky|ty),(kx|tx) = 4,5, co = 6
+  const Buf& W = L.in[1];
+  const Buf& O = L.out;
+  auto os = strides_of(O.buf_box);
+  a.kind = 0;
+  a.nb = (int)ib[0].len();
+  a.sb0 = (int)(ib[0].lo - S.buf_box[0].lo);
+  a.nch = (int)ib[6].len();
+  a.sc0 = (int)(ib[6].lo - S.buf_box[3].lo);
+  a.n_out = (int)ib[3].len();
+  a.Bp = box_ptr(W);
+  a.ldb = strides_of(W.buf_box)[0];
+  a.b_tap = (int)W.buf_box[3].len();
+  a.b_rows = (int)W.box[0].len();
+  a.b_cols = (int)(a.ldb - (W.box[3].lo - W.buf_box[3].lo));
+  a.b_mn_major = 1;
+  a.C = box_ptr(O);
+  a.c_sb = os[0];
+  a.c_sy = os[1];
+  a.c_sx = os[2];
+  a.c_mode = O.dtype == TOFU_F32 ? 1 : 0;
+  a.ay = a.ax = 1;
+  if (s == 1) {  // dX[y] = Σ D[y - ky + p] W[ky]
+    a.ngy = (int)ib[1].len();
+    a.ngx = (int)ib[2].len();
+    a.cy = (int)(ib[1].lo + p - S.buf_box[1].lo);
+    a.cx = (int)(ib[2].lo + p - S.buf_box[2].lo);
+    a.c_ys = a.c_xs = 1;
+    a.ntaps = 0;
+    for (int64_t ky = ib[4].lo; ky <= ib[4].hi; ++ky)
+      for (int64_t kx = ib[5].lo; kx <= ib[5].hi; ++kx) {
+        a.tap_dy[a.ntaps] = (short)-ky;
+        a.tap_dx[a.ntaps] = (short)-kx;
+        a.tap_w[a.ntaps] = (short)(ky * R + kx);
+        ++a.ntaps;
+      }
+    out.push_back(a);
+    return out;
+  }
+  // stride 2: one launch per sub-pixel phase (ry, rx); y = 2u + ry reads D[u + (ry+p)/2 - ty] through tap
+  // ky = (ry+p)%2 + 2ty (< R), the dconv_k*s2 def's floor-division / remainder indices
+  auto fdiv = [](int64_t v, int64_t q) { return v >= 0 ? v / q : -((-v + q - 1) / q); };
+  for (int ry = 0; ry < 2; ++ry)
+    for (int rx = 0; rx < 2; ++rx) {
+      tofu_conv_args b = a;
+      const int64_t ulo = fdiv(ib[1].lo - ry + 1, 2), uhi = fdiv(ib[1].hi - ry, 2);
+      const int64_t vlo = fdiv(ib[2].lo - rx + 1, 2), vhi = fdiv(ib[2].hi - rx, 2);
+      if (uhi < ulo || vhi < vlo) continue;
+      b.ngy = (int)(uhi - ulo + 1);
+      b.ngx = (int)(vhi - vlo + 1);
+      b.cy = (int)(ulo + (ry + p) / 2 - S.buf_box[1].lo);
+      b.cx = (int)(vlo + (rx + p) / 2 - S.buf_box[2].lo);
+      b.c_ys = b.c_xs = 2;
+      b.c_y0 = (int)(2 * ulo + ry - ib[1].lo);
+      b.c_x0 = (int)(2 * vlo + rx - ib[2].lo);
+      b.ntaps = 0;
+      for (int64_t ty = ib[4].lo; ty <= ib[4].hi; ++ty)
+        for (int64_t tx = ib[5].lo; tx <= ib[5].hi; ++tx) {
+          const int64_t ky = (ry + p) % 2 + 2 * ty, kx = (rx + p) % 2 + 2 * tx;
+          if (ky >= R || kx >= R) continue;
+          b.tap_dy[b.ntaps] = (short)-ty;
+          b.tap_dx[b.ntaps] = (short)-tx;
+          b.tap_w[b.ntaps] = (short)(ky * R + kx);
+          ++b.ntaps;
+        }
+      out.push_back(b);
+    }
+  return out;
+}
+
+// maxpool / maxpool_grad / gap / gap_grad on the op's iteration box (tofu_window_args in include/tofu.h)
+int run_window(Exec& E, int o, int li, cudaStream_t st) {
+  const Graph& g = *E.g;
+  const int r = E.local[li];
+  const LOp& L = E.lops[li][o];
+  const std::string& dn = g.def_of(o).name;
+  std::vector<Rng> ib;
+  iter_box(g, o, E.plan.osplit[o], E.plan.factors, worker_digits(r, E.plan.factors), ib);
+  char* base = E.arena[r];
+  auto es = [](int dt) { return (int64_t)(dt == TOFU_BF16 ? 2 : 4); };
+  // pointer to (box b lo, buffer row 0, buffer col 0, box c lo) of a 4-D buffer
+  auto p4 = [&](const Buf& b) {
+    auto s = strides_of(b.buf_box);
+    return base + b.off + ((b.box[0].lo - b.buf_box[0].lo) * s[0] + (b.box[3].lo - b.buf_box[3].lo)) * es(b.dtype);
+  };
+  tofu_window_args a;
+  std::memset(&a, 0, sizeof a);
+  a.out_f32 = L.out.dtype == TOFU_F32;
+  auto os = strides_of(L.out.buf_box);
+  const int64_t oe = es(L.out.dtype);
+  if (dn == "maxpool") {  // vars b, y, x, c | ky, kx
+    const Buf& X = L.in[0];
+    auto xs = strides_of(X.buf_box);
+    a.nb = (int)ib[0].len(); a.C = (int)ib[3].len();
+    a.H = (int)X.buf_box[1].len(); a.W = (int)X.buf_box[2].len();
+    a.y0 = (int)X.buf_box[1].lo; a.x0 = (int)X.buf_box[2].lo;
+    a.Ho = (int)ib[1].len(); a.Wo = (int)ib[2].len(); a.oy0 = (int)ib[1].lo; a.ox0 = (int)ib[2].lo;
+    a.x_sb = xs[0]; a.x_sy = xs[1]; a.x_sx = xs[2];
+    a.X = p4(X);
+    a.o_sb = os[0]; a.o_sy = os[1]; a.o_sx = os[2];
+    a.out = base + L.out.off + offset_in(L.out.buf_box, L.out.box) * oe;
+    return tofu_maxpool(&a, st);
+  }
+  if (dn == "maxpool_grad") {  // vars b, y, x, c | ty, tx ; inputs X, Y, D, K
+    const Buf &X = L.in[0], &Y = L.in[1], &D = L.in[2], &K = L.in[3];
+    auto xs = strides_of(X.buf_box), ys = strides_of(Y.buf_box), ds = strides_of(D.buf_box), ks = strides_of(K.buf_box);
+    if (Y.buf_box[1].lo != D.buf_box[1].lo || Y.buf_box[2].lo != D.buf_box[2].lo ||
+        Y.buf_box[1].len() != D.buf_box[1].len() || Y.buf_box[2].len() != D.buf_box[2].len())
+      throw Error(TOFU_ERR_ARG, "maxpool_grad: Y and dY regions differ");
+    a.nb = (int)ib[0].len(); a.C = (int)ib[3].len();
+    a.H = (int)ib[1].len(); a.W = (int)ib[2].len(); a.y0 = (int)ib[1].lo; a.x0 = (int)ib[2].lo;
+    a.Ho = (int)Y.buf_box[1].len(); a.Wo = (int)Y.buf_box[2].len();
+    a.oy0 = (int)Y.buf_box[1].lo; a.ox0 = (int)Y.buf_box[2].lo;
+    a.x_sb = xs[0]; a.x_sy = xs[1]; a.x_sx = xs[2];
+    a.y_sb = ys[0]; a.y_sy = ys[1]; a.y_sx = ys[2];
+    a.d_sb = ds[0]; a.d_sy = ds[1]; a.d_sx = ds[2];
+    a.k_sy = ks[0]; a.k_sx = ks[1];
+    a.X = base + X.off + offset_in(X.buf_box, X.box) * 2;
+    a.Y = p4(Y);
+    a.dY = p4(D);
+    // K[ky][kx][c]: pointer at (ky 0, kx 0, box c lo)
+    a.K = base + K.off + ((0 - K.buf_box[0].lo) * ks[0] + (0 - K.buf_box[1].lo) * ks[1] + (K.box[2].lo - K.buf_box[2].lo)) * 2;
+    if (K.buf_box[0].lo != 0 || K.buf_box[1].lo != 0 || K.buf_box[0].len() < 3 || K.buf_box[1].len() < 3)
+      throw Error(TOFU_ERR_ARG, "maxpool_grad: mask region must hold all taps");
+    a.ty0 = (int)ib[4].lo; a.ty1 = (int)ib[4].hi; a.tx0 = (int)ib[5].lo; a.tx1 = (int)ib[5].hi;
+    a.o_sb = os[0]; a.o_sy = os[1]; a.o_sx = os[2];
+    a.out = base + L.out.off + offset_in(L.out.buf_box, L.out.box) * oe;
+    return tofu_maxpool_grad(&a, st);
+  }
+  if (dn == "gap") {  // vars b, c | y, x
+    const Buf& X = L.in[0];
+    auto xs = strides_of(X.buf_box);
+    a.nb = (int)ib[0].len(); a.C = (int)ib[1].len();
+    a.H = (int)ib[2].len(); a.W = (int)ib[3].len();
+    a.x_sb = xs[0]; a.x_sy = xs[1]; a.x_sx = xs[2];
+    a.X = base + X.off + offset_in(X.buf_box, X.box) * 2;
+    a.o_sb = os[0];
+    a.out = base + L.out.off + offset_in(L.out.buf_box, L.out.box) * oe;
+    auto it = g.ops[o].attrs.find("scale");
+    a.s = it != g.ops[o].attrs.end() ? (float)it->second : 0.f;
+    return tofu_gap(&a, st);
+  }
+  // gap_grad: vars b, y, x, c ; input D[b, c]
+  const Buf& D = L.in[0];
+  auto ds = strides_of(D.buf_box);
+  a.nb = (int)ib[0].len(); a.C = (int)ib[3].len();
+  a.H = (int)ib[1].len(); a.W = (int)ib[2].len();
+  a.y_sb = ds[0];
+  a.dY = base + D.off + offset_in(D.buf_box, D.box) * 2;
+  a.o_sb = os[0]; a.o_sy = os[1]; a.o_sx = os[2];
+  a.out = base + L.out.off + offset_in(L.out.buf_box, L.out.box) * oe;
+  auto it = g.ops[o].attrs.find("scale");
+  a.s = it != g.ops[o].attrs.end() ? (float)it->second : 0.f;
+  return tofu_gap_grad(&a, st);
+}
 
 int run_compute(Exec& E, int o, int li, cudaStream_t st) {
   const Graph& g = *E.g;
@@ -690,6 +1061,14 @@ int run_compute(Exec& E, int o, int li, cudaStream_t st) {
     auto& G = E.gemms.at({o, li});
     return tofu_gemm_launch_planned(&G.a, G.tm, G.bn, st);
   }
+  if (kind == "conv") {
+    for (auto& C : E.convs.at({o, li})) {
+      const int rc = tofu_conv_launch_planned(&C.a, C.tm, st);
+      if (rc) return rc;
+    }
+    return TOFU_OK;
+  }
+  if (kind == "window") return run_window(E, o, li, st);
   if (kind == "lstm") {
     // operand slots of the cell kernel: gx, gh, cp, c, du, dr, dn
     static const std::map<std::string, std::vector<int>> slots = {
@@ -741,8 +1120,10 @@ int run_compute(Exec& E, int o, int li, cudaStream_t st) {
     auto it = oi.attrs.find(key);
     return (float)(it == oi.attrs.end() ? dflt : it->second);
   };
-  if (dn == "relu") return tofu_elementwise(TOFU_EW_RELU, n, y, x0, nullptr, nullptr, 0, 0, st);
-  if (dn == "relu_grad") return tofu_elementwise(TOFU_EW_RELU_GRAD, n, y, x0, x1, nullptr, 0, 0, st);
+  if (dn == "relu" || dn == "relu4") return tofu_elementwise(TOFU_EW_RELU, n, y, x0, nullptr, nullptr, 0, 0, st);
+  if (dn == "relu_grad" || dn == "relu_grad4") return tofu_elementwise(TOFU_EW_RELU_GRAD, n, y, x0, x1, nullptr, 0, 0, st);
+  if (dn == "add4") return tofu_elementwise(TOFU_EW_ADD, n, y, x0, x1, nullptr, 0, 0, st);
+  if (dn == "addrelu") return tofu_elementwise(TOFU_EW_ADDRELU, n, y, x0, x1, nullptr, 0, 0, st);
   if (dn == "mse_grad") return tofu_elementwise(TOFU_EW_MSE_GRAD, n, y, x0, x1, nullptr, attr("scale", 1), 0, st);
   if (dn == "sumsq") {
     const int64_t m = vol(L.in[0].box);
@@ -927,6 +1308,15 @@ std::string launch_desc(const Exec& E, int i) {
       flops = 2 * M * N * K;
       bytes = 2 * (M * K + K * N) + M * N * (lo.fused_opt >= 0 ? (8 + 4) : (lo.out.dtype == TOFU_BF16 ? 2 : 4));
       (void)dn;
+    } else if (std::string(kernel_kind(dd)) == "conv") {
+      // implicit GEMM: 2·M·N·K over the launches (the stride-2 data gradient's phases skip absent taps);
+      // bytes: each operand region once + the output (fused optimizer: momentum and weight read + written)
+      for (auto& a : conv_args(const_cast<Exec&>(E), L.op, L.li)) {
+        const double pix = (double)a.nb * a.ngy * a.ngx, kn = (double)a.ntaps * a.nch;
+        flops += a.kind == 0 ? 2 * pix * a.n_out * kn : 2 * (double)a.m_out * kn * pix;
+      }
+      for (auto& b : lo.in) bytes += (double)vol(b.box) * (b.dtype == TOFU_BF16 ? 2 : 4);
+      bytes += (double)vol(lo.out.box) * (lo.fused_opt >= 0 ? 12 : (lo.out.dtype == TOFU_BF16 ? 2 : 4));
     } else {
       const double n = (double)vol(lo.in[0].box);
       for (size_t k = 0; k < lo.in.size(); ++k) bytes += n * (lo.in[k].dtype == TOFU_BF16 ? 2 : 4);

@@ -88,7 +88,10 @@ Graph graph_from_json(const std::string& text) {
     std::vector<int64_t> oshape_it(oshape);
     for (int v = 0; v < d.n_out; ++v)
       if (over.count(d.vars[v])) oshape_it[v] = over[d.vars[v]];
-    oi.R = var_extents(d, ins, oshape_it);
+    std::vector<int64_t> given(d.vars.size(), -1);
+    for (size_t v = 0; v < d.vars.size(); ++v)
+      if (over.count(d.vars[v])) given[v] = over[d.vars[v]];
+    oi.R = var_extents(d, ins, oshape_it, given);
     for (size_t v = 0; v < d.vars.size(); ++v)
       if (over.count(d.vars[v])) oi.R[v] = over[d.vars[v]];
     // output view inside the tensor and disjoint from other producers' views
@@ -105,19 +108,7 @@ Graph graph_from_json(const std::string& text) {
       if (overlap) throw Error(TOFU_ERR_PARSE, "tensor " + g.tensors[oi.output].name + " produced twice");
     }
     produced[oi.output].push_back(obox);
-    // every access must stay inside its tensor over the full iteration space
-    for (auto& a : d.accesses)
-      for (size_t dim = 0; dim < a.idx.size(); ++dim) {
-        if (a.slice[dim]) continue;
-        int64_t lo = a.idx[dim].c + oi.in_off[a.param][dim], hi = lo;
-        for (auto& kv : a.idx[dim].coef) {
-          int64_t x = kv.second * (oi.R[kv.first] - 1);
-          lo += std::min<int64_t>(0, x);
-          hi += std::max<int64_t>(0, x);
-        }
-        if (lo < 0 || hi >= ins[a.param][dim])
-          throw Error(TOFU_ERR_PARSE, "ShapeMismatch " + oi.name + ": access out of range");
-      }
+    // accesses may leave their tensor: zero padding (reading R11), nothing to check
     g.ops.push_back(oi);
   }
   if (auto* al = j.get("alias"); al && al->kind == Json::Obj)
@@ -255,16 +246,16 @@ std::vector<Rng> required_box(const Graph& g, int op, int param, const std::vect
         lo = 0;
         hi = shape[dim] - 1;
       } else {
-        lo = hi = a.idx[dim].c + g.ops[op].in_off[param][dim];
-        for (auto& kv : a.idx[dim].coef) {
-          int64_t x = kv.second * ib[kv.first].lo, y = kv.second * ib[kv.first].hi;
-          lo += std::min(x, y);
-          hi += std::max(x, y);
-        }
+        a.idx[dim].hull(ib, g.ops[op].in_off[param][dim], lo, hi);
       }
       req[dim].lo = std::min(req[dim].lo, lo);
       req[dim].hi = std::max(req[dim].hi, hi);
     }
+  }
+  // the hull ∩ the tensor: elements outside it read as zero and are never moved (reading R11)
+  for (size_t dim = 0; dim < req.size(); ++dim) {
+    req[dim].lo = std::max<int64_t>(req[dim].lo, 0);
+    req[dim].hi = std::min<int64_t>(req[dim].hi, shape[dim] - 1);
   }
   return req;
 }

@@ -67,10 +67,6 @@ struct PlanSeq {
 };
 
 // Closed range of the part selected by (k_i, digit_i) nested splits of an extent-n axis.
-struct Rng {
-  int64_t lo, hi;
-  int64_t len() const { return hi >= lo ? hi - lo + 1 : 0; }
-};
 Rng nested_range(int64_t n, const std::vector<std::pair<int, int>>& splits);
 std::vector<int> worker_digits(int w, const std::vector<int>& factors);
 

@@ -57,7 +57,7 @@ std::vector<Tok> lex(const std::string& src) {
           break;
         }
       if (done) continue;
-      if (std::string("-+*/()[],:;<>").find(c) == std::string::npos)
+      if (std::string("-+*/%()[],:;<>").find(c) == std::string::npos)
         perr("Syntax", "bad character at " + std::to_string(i));
       t.push_back({2, std::string(1, c), st});
       ++i;
@@ -97,15 +97,42 @@ struct Parser {
     return k.s;
   }
 
-  Affine affine() {
+  // index := term (('+'|'-') term)* ; term := int ['*' var] | var ['*' int] | [int '*'] '(' lin ')' ('/'|'%') int
+  Affine affine(bool inner = false) {
     std::map<int, int64_t> co;
     int64_t c = 0;
     int64_t sign = 1;
+    Affine a;
     if (accept("-")) sign = -1;
     else accept("+");
     while (true) {
       Tok k = next();
-      if (k.kind == 0) {
+      int64_t mult = 0;
+      if (k.kind == 0 && peek().s == "*" && i + 1 < t.size() && t[i + 1].s == "(") {
+        if (k.s.find('.') != std::string::npos) perr("NonAffineIndex", "non-integer constant in index");
+        mult = std::stoll(k.s);
+        ++i;
+        k = next();
+      }
+      if (k.kind == 2 && k.s == "(") {
+        if (inner) perr("NonAffineIndex", "nested index division");
+        Affine in = affine(true);
+        expect(")");
+        Tok op = next();
+        if (op.s != "/" && op.s != "%") perr("NonAffineIndex", "parenthesised index term needs / or %");
+        Tok dv = next();
+        if (dv.kind != 0 || dv.s.find('.') != std::string::npos || std::stoll(dv.s) <= 0)
+          perr("NonAffineIndex", "index division by a positive integer constant only");
+        Affine::Term term;
+        term.mod = op.s == "%";
+        term.mult = sign * (mult ? mult : 1);
+        term.d = std::stoll(dv.s);
+        term.inner.coef = in.coef;
+        term.inner.c = in.c;
+        a.terms.push_back(term);
+      } else if (mult) {
+        perr("Syntax", "bad index term at " + std::to_string(k.pos));
+      } else if (k.kind == 0) {
         if (k.s.find('.') != std::string::npos) perr("NonAffineIndex", "non-integer constant in index");
         int64_t n = std::stoll(k.s);
         if (accept("*")) {
@@ -132,11 +159,10 @@ struct Parser {
       const std::string& nx = peek().s;
       if (nx == "+") { ++i; sign = 1; }
       else if (nx == "-") { ++i; sign = -1; }
-      else if (nx == "," || nx == "]") break;
-      else if (nx == "*" || nx == "/") perr("NonAffineIndex", "non-affine index expression");
+      else if (inner ? nx == ")" : (nx == "," || nx == "]")) break;
+      else if (nx == "*" || nx == "/" || nx == "%") perr("NonAffineIndex", "non-affine index expression");
       else perr("Syntax", "unexpected '" + nx + "' in index");
     }
-    Affine a;
     for (auto& kv : co)
       if (kv.second) a.coef.push_back(kv);
     a.c = c;
@@ -307,7 +333,8 @@ struct Parser {
       }
       d.opaque = true;
       for (size_t k = 0; k < a.idx.size(); ++k)
-        if (!a.slice[k] && a.idx[k].coef.size() == 1 && a.idx[k].coef[0].second == 1 && a.idx[k].c == 0)
+        if (!a.slice[k] && a.idx[k].plain() && a.idx[k].coef.size() == 1 && a.idx[k].coef[0].second == 1 &&
+            a.idx[k].c == 0)
           d.opaque_free.push_back(a.idx[k].coef[0].first);
       d.accesses.push_back(a);
     } else {
@@ -320,12 +347,12 @@ struct Parser {
       std::map<int, size_t> seen;
       for (size_t dim = 0; dim < a.idx.size(); ++dim) {
         if (a.slice[dim]) continue;
-        for (auto& kv : a.idx[dim].coef) {
-          used.insert(kv.first);
-          auto it = seen.find(kv.first);
+        for (int v : a.idx[dim].vars()) {
+          used.insert(v);
+          auto it = seen.find(v);
           if (it != seen.end() && it->second != dim)
-            perr("AssumptionViolation", d.vars[kv.first] + " indexes two dims of " + d.params[a.param]);
-          seen[kv.first] = dim;
+            perr("AssumptionViolation", d.vars[v] + " indexes two dims of " + d.params[a.param]);
+          seen[v] = dim;
         }
       }
     }
@@ -377,11 +404,70 @@ OpDef parse_tdl(const std::string& src) {
   return p.run();
 }
 
+int64_t Lin::eval(const int64_t* env) const {
+  int64_t x = c;
+  for (auto& kv : coef) x += kv.second * env[kv.first];
+  return x;
+}
+
+int64_t Affine::eval(const int64_t* env) const {
+  int64_t x = Lin::eval(env);
+  for (auto& t : terms) {
+    const int64_t in = t.inner.eval(env);
+    x += t.mult * (t.mod ? floormod(in, t.d) : floordiv(in, t.d));
+  }
+  return x;
+}
+
+static void lin_hull(const Lin& l, const std::vector<Rng>& box, int64_t& lo, int64_t& hi) {
+  lo = hi = l.c;
+  for (auto& kv : l.coef) {
+    const int64_t x = kv.second * box[kv.first].lo, y = kv.second * box[kv.first].hi;
+    lo += std::min(x, y);
+    hi += std::max(x, y);
+  }
+}
+
+void Affine::hull(const std::vector<Rng>& box, int64_t off, int64_t& lo, int64_t& hi) const {
+  lin_hull(*this, box, lo, hi);
+  lo += off;
+  hi += off;
+  for (auto& t : terms) {
+    int64_t il, ih, tl, th;
+    lin_hull(t.inner, box, il, ih);
+    if (!t.mod) {
+      tl = floordiv(il, t.d);
+      th = floordiv(ih, t.d);
+    } else if (ih - il + 1 >= t.d || floordiv(il, t.d) != floordiv(ih, t.d)) {
+      tl = 0;
+      th = t.d - 1;
+    } else {
+      tl = floormod(il, t.d);
+      th = floormod(ih, t.d);
+    }
+    lo += std::min(t.mult * tl, t.mult * th);
+    hi += std::max(t.mult * tl, t.mult * th);
+  }
+}
+
+std::vector<int> Affine::vars() const {
+  std::vector<int> v;
+  for (auto& kv : coef) v.push_back(kv.first);
+  for (auto& t : terms)
+    for (auto& kv : t.inner.coef)
+      if (std::find(v.begin(), v.end(), kv.first) == v.end()) v.push_back(kv.first);
+  return v;
+}
+
 std::vector<int64_t> var_extents(const OpDef& d, const std::vector<std::vector<int64_t>>& in_shapes,
-                                 const std::vector<int64_t>& out_shape) {
+                                 const std::vector<int64_t>& out_shape, const std::vector<int64_t>& given) {
   std::vector<int64_t> R(d.vars.size(), -1);
   for (int v = 0; v < d.n_out; ++v) R[v] = out_shape.at(v);
   for (int v = d.n_out; v < (int)d.vars.size(); ++v) {
+    if (v < (int)given.size() && given[v] >= 0) {
+      R[v] = given[v];
+      continue;
+    }
     for (auto& a : d.accesses) {
       for (size_t dim = 0; dim < a.idx.size() && R[v] < 0; ++dim)
         if (!a.slice[dim] && a.idx[dim].identity_of(v)) R[v] = in_shapes.at(a.param).at(dim);
@@ -415,7 +501,21 @@ std::string describe_json(const OpDef& d, int ways) {
       for (size_t k = 0; k < a.idx[dim].coef.size(); ++k)
         o += (k ? "," : "") + json_quote(d.vars[a.idx[dim].coef[k].first]) + ":" +
              std::to_string(a.idx[dim].coef[k].second);
-      o += "},\"const\":" + std::to_string(a.idx[dim].c) + "}";
+      o += "},\"const\":" + std::to_string(a.idx[dim].c);
+      if (!a.idx[dim].terms.empty()) {
+        o += ",\"terms\":[";
+        for (size_t q = 0; q < a.idx[dim].terms.size(); ++q) {
+          const auto& tm = a.idx[dim].terms[q];
+          o += (q ? "," : "") + std::string("{\"kind\":") + (tm.mod ? "\"mod\"" : "\"div\"") +
+               ",\"mult\":" + std::to_string(tm.mult) + ",\"d\":" + std::to_string(tm.d) + ",\"coef\":{";
+          for (size_t r = 0; r < tm.inner.coef.size(); ++r)
+            o += (r ? "," : "") + json_quote(d.vars[tm.inner.coef[r].first]) + ":" +
+                 std::to_string(tm.inner.coef[r].second);
+          o += "},\"const\":" + std::to_string(tm.inner.c) + "}";
+        }
+        o += "]";
+      }
+      o += "}";
     }
     o += "]}";
   }
@@ -433,12 +533,30 @@ std::string describe_json(const OpDef& d, int ways) {
         for (size_t dim = 0; dim < a.idx.size(); ++dim) {
           o += dim ? "," : "";
           if (a.slice[dim]) { o += "null"; continue; }
+          // Fig. int-arith: each var's ZV interval times its (rational) coefficient, summed; a remainder
+          // term contributes the constant interval [min(0, mult(d-1)), max(0, mult(d-1))] (reading R11)
           std::map<int, Q> lo, hi;
-          for (auto& kv : a.idx[dim].coef) {
-            Q l = kv.first == v ? Q(j, ways) : Q(0), u = kv.first == v ? Q(j + 1, ways) : Q(1);
-            Q a1 = Q(kv.second) * l, a2 = Q(kv.second) * u;
-            if (kv.second >= 0) { lo[kv.first] = a1; hi[kv.first] = a2; }
-            else { lo[kv.first] = a2; hi[kv.first] = a1; }
+          Q clo(a.idx[dim].c), chi(a.idx[dim].c);
+          auto add_lin = [&](const Lin& l, Q q) {
+            for (auto& kv : l.coef) {
+              Q co = Q(kv.second) * q;
+              Q lv = kv.first == v ? Q(j, ways) : Q(0), uv = kv.first == v ? Q(j + 1, ways) : Q(1);
+              const bool neg = co.n < 0;
+              lo[kv.first] = lo[kv.first] + co * (neg ? uv : lv);
+              hi[kv.first] = hi[kv.first] + co * (neg ? lv : uv);
+            }
+          };
+          add_lin(a.idx[dim], Q(1));
+          for (auto& tm : a.idx[dim].terms) {
+            if (!tm.mod) {
+              add_lin(tm.inner, Q(tm.mult, tm.d));
+              clo = clo + Q(tm.inner.c) * Q(tm.mult, tm.d);
+              chi = chi + Q(tm.inner.c) * Q(tm.mult, tm.d);
+            } else {
+              const int64_t e = tm.mult * (tm.d - 1);
+              clo = clo + Q(std::min<int64_t>(0, e));
+              chi = chi + Q(std::max<int64_t>(0, e));
+            }
           }
           auto dump = [&](std::map<int, Q>& m) {
             std::string s = "{";
@@ -450,8 +568,8 @@ std::string describe_json(const OpDef& d, int ways) {
             }
             return s + "}";
           };
-          o += "{\"lo\":" + dump(lo) + ",\"c_lo\":" + std::to_string(a.idx[dim].c) + ",\"hi\":" + dump(hi) +
-               ",\"c_hi\":" + std::to_string(a.idx[dim].c) + "}";
+          auto qs = [](const Q& q) { return q.d == 1 ? std::to_string(q.n) : qj(q); };
+          o += "{\"lo\":" + dump(lo) + ",\"c_lo\":" + qs(clo) + ",\"hi\":" + dump(hi) + ",\"c_hi\":" + qs(chi) + "}";
         }
         o += "]}";
       }

@@ -7,12 +7,41 @@
 
 namespace tofu {
 
-// Σ coef[v]·var_v + c, integer coefficients (Eq. 1 admits affine intervals only).
-struct Affine {
+// Closed integer range [lo, hi] (empty when hi < lo).
+struct Rng {
+  int64_t lo, hi;
+  int64_t len() const { return hi >= lo ? hi - lo + 1 : 0; }
+};
+
+// Σ coef[v]·var_v + c, integer coefficients.
+struct Lin {
   std::vector<std::pair<int, int64_t>> coef;  // (var index, coefficient), sorted by var index, non-zero
   int64_t c = 0;
-  bool identity_of(int v) const { return coef.size() == 1 && coef[0].first == v && coef[0].second == 1 && c == 0; }
+  int64_t eval(const int64_t* env) const;
 };
+
+// Index expression: Σ coef[v]·var_v + c (Eq. 1 admits affine intervals), plus quasi-affine
+// terms mult·⌊inner / d⌋ and mult·(inner mod d) (reading R11: the I / k of Fig. int-arith, P:L510-522,
+// taken as integer division of an index, and its remainder) used by strided-convolution gradients.
+struct Affine : Lin {
+  struct Term {
+    bool mod = false;
+    int64_t mult = 1, d = 1;
+    Lin inner;
+  };
+  std::vector<Term> terms;
+  bool identity_of(int v) const {
+    return coef.size() == 1 && coef[0].first == v && coef[0].second == 1 && c == 0 && terms.empty();
+  }
+  bool plain() const { return terms.empty(); }
+  int64_t eval(const int64_t* env) const;
+  // closed range over a var box: the linear part exactly, each term bounded on its own
+  void hull(const std::vector<Rng>& box, int64_t off, int64_t& lo, int64_t& hi) const;
+  std::vector<int> vars() const;  // every var the index mentions
+};
+
+inline int64_t floordiv(int64_t a, int64_t d) { return a >= 0 ? a / d : -((-a + d - 1) / d); }
+inline int64_t floormod(int64_t a, int64_t d) { return a - d * floordiv(a, d); }
 
 struct Access {
   int param = 0;                 // index into OpDef::params
@@ -42,8 +71,9 @@ struct OpDef {
 OpDef parse_tdl(const std::string& src);
 
 // Extent of every var given input and output shapes (reduce vars from the first dim they index alone).
+// `given` (may be empty) holds explicit extents (-1 = infer) for vars no dim determines.
 std::vector<int64_t> var_extents(const OpDef& d, const std::vector<std::vector<int64_t>>& in_shapes,
-                                 const std::vector<int64_t>& out_shape);
+                                 const std::vector<int64_t>& out_shape, const std::vector<int64_t>& given = {});
 
 // JSON analysis for tofu_describe_op.
 std::string describe_json(const OpDef& d, int ways);

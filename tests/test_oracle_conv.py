@@ -246,9 +246,9 @@ def test_conv_box_cost_equals_element_enumeration():
     assert checked > 100
 
 
-@pytest.mark.parametrize("k", [2, 4])
-def test_wresnet_partitioned_sim_equals_unpartitioned(k):
-    spec = wresnet([1, 1], 1, 4, 16, base=4, classes=4)
+@pytest.mark.parametrize("k,units", [(2, [1, 1]), (4, [1])])
+def test_wresnet_partitioned_sim_equals_unpartitioned(k, units):
+    spec = wresnet(units, 1, 4, 16 if k == 2 else 8, base=4, classes=4)
     g = Graph(spec)
     vals = make_values(spec, seed=4, mode="int")
     ref = run_graph(g, vals, emulate_storage=False)

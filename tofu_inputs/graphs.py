@@ -386,7 +386,7 @@ def wresnet(units: list, width: int, batch: int, image: int = 224, base: int = 6
     defs["gap"] = (f"def gap(X(4)) -> lambda b, c: reduce(Sum; y, x; X[b, y, x, c] * {_num(1.0 / (Hc * Hc))})")
     defs["gap_grad"] = f"def gap_grad(D(2)) -> lambda b, y, x, c: D[b, c] * {_num(1.0 / (Hc * Hc))}"
     tensor("gap.Y", (batch, c), "bf16", "act")
-    op("gap", "gap", [x], "gap.Y")
+    op("gap", "gap", [x], "gap.Y", attrs={"scale": 1.0 / (Hc * Hc)})
     tensor("fc.W", (c, classes), "bf16", "weight")
     tensor("Y", (batch, classes), "bf16", "act")
     op("fc", "mm_nn", ["gap.Y", "fc.W"], "Y")
@@ -408,7 +408,7 @@ def wresnet(units: list, width: int, batch: int, image: int = 224, base: int = 6
     wgrads.append(("fc.W", "fc.dW"))
     dx = x + ".d"
     tensor(dx, (batch, Hc, Hc, c), "bf16", "grad", grad_of=x)
-    op("gap_bwd", "gap_grad", ["gap.dY"], dx, backward_of="gap")
+    op("gap_bwd", "gap_grad", ["gap.dY"], dx, backward_of="gap", attrs={"scale": 1.0 / (Hc * Hc)})
     for (p, xin, cin_u, Hin, mid, outc, stride, Ho, proj) in reversed(fwd_units):
         k1, k2, k3 = f"k1s1p0", f"k3s{stride}p1", "k1s1p0"
         dO = p + "O.d"
