@@ -14,10 +14,11 @@
 //          gradient via TMA (MN-major), B gathered (MN-major rows of 64 channels); fp32 output through the
 //          TMA-store epilogue of the GEMM (store / accumulate / fused momentum-SGD), split-K over pixels.
 //
-// Warp roles (256 threads): warp 0 lane 0 = TMA producer of the dense operand, warp 1 = TMEM allocator +
-// MMA issuer, warps 2..5 = epilogue (TMEM lane quarter w%4), warps 6..7 = gather producers (64 threads,
-// LAG cp.async groups in flight each; a stage is published with fence.proxy.async + mbarrier arrive once
-// its copies land).  Persistent grid, TMEM accumulator double-buffered as in gemm_tcgen05.cu.
+// Warp roles (320 threads): warp 0 lane 0 = TMA producer of the dense operand, warp 1 = TMEM allocator +
+// MMA issuer, warps 2..5 = epilogue (TMEM lane quarter w%4), warps 6..9 = gather producers (128 threads;
+// each thread's copies of a stage arrive on the stage's mbarrier when they land (cp.async.mbarrier.arrive),
+// so a producer runs up to STAGES ahead without blocking; the MMA thread fences generic -> async proxy
+// after the wait).  Persistent grid, TMEM accumulator double-buffered as in gemm_tcgen05.cu.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cstdio>
@@ -31,10 +32,9 @@ namespace conv {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int NTHREADS = 256;
+constexpr int NTHREADS = 320;
 constexpr int SMEM_MAX = 232448;
-constexpr int LAG = 2;
-constexpr int NGATHER = 64;
+constexpr int NGATHER = 128;  // warps 6..9
 
 struct Params {
   tofu_conv_args a;
@@ -42,7 +42,7 @@ struct Params {
 };
 
 struct RowInfo {
-  long long off;  // element offset of the pixel's image (b) in S
+  long long off;  // element offset in S of the pixel's (b, y, x) before the tap offset (y, x may be outside)
   int y, x;       // buffer coordinates before the tap offset
 };
 
@@ -62,7 +62,7 @@ struct Cfg {
   static constexpr int STAGES = FIT > 6 ? 6 : FIT;
   static constexpr int TMEM_COLS = BN * 2;
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + ROW_BYTES + 1024 + 512;
-  static_assert(STAGES > LAG, "pipeline too shallow for the gather lag");
+  static_assert(STAGES >= 3, "pipeline too shallow");
   static_assert(SMEM <= SMEM_MAX, "smem");
 };
 
@@ -70,9 +70,15 @@ __device__ __forceinline__ RowInfo pixel_info(const tofu_conv_args& a, int g, in
   RowInfo ri;
   const int gb = g / ngyx, rem = g - gb * ngyx;
   const int gy = rem / a.ngx, gx = rem - gy * a.ngx;
-  ri.off = (long long)(gb + a.sb0) * a.s_sb;
   ri.y = a.ay * gy + a.cy;
   ri.x = a.ax * gx + a.cx;
+  ri.off = (long long)(gb + a.sb0) * a.s_sb + (long long)ri.y * a.s_sy + (long long)ri.x * a.s_sx;
+  return ri;
+}
+__device__ __forceinline__ RowInfo no_pixel() {
+  RowInfo ri;
+  ri.off = 0;
+  ri.y = ri.x = -(1 << 29);
   return ri;
 }
 
@@ -185,6 +191,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int kb = kb0; kb < kb_lo(sp + 1); ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&full[s], (it / STAGES) & 1);
+          fence_proxy_async_smem();  // the gathered operand was written by cp.async (generic proxy)
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + s * C_::A_BYTES);
           const uint32_t b0 = smem_u32(sB + s * C_::B_BYTES);
@@ -202,98 +209,69 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp >= 6) {
-    // ------------------------------------------------------------ gather producers (64 threads)
+    // ------------------------------------------------------------ gather producers (warps 6..9)
+    // Per stage a thread issues a fixed set of 16-byte copies whose shared-memory slots are compile-time
+    // offsets (the 128B swizzle phase of its rows is constant); per copy: one row-info load, two bounds
+    // tests, one 64-bit add.
     const int gt = threadIdx.x - 192;
     int it = 0, local = 0;
-    auto publish = [&](int upto) {  // stages < upto whose copies have landed: publish to the MMA
-      fence_proxy_async_smem();
-      mbar_arrive(&full[upto % STAGES]);
-    };
+    const __nv_bfloat16* S0 = reinterpret_cast<const __nv_bfloat16*>(a.S);
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++local) {
       const int tile = u / splits, sp = u % splits;
       const int m0 = (tile / tiles_n) * BM;
       const int n0 = (tile % tiles_n) * BN;
       if constexpr (KIND == 0) {
         RowInfo* ri = rows + (local & 1) * BM;
-        for (int r = gt; r < BM; r += NGATHER) {
-          const int m = m0 + r;
-          if (m < M) {
-            ri[r] = pixel_info(a, m, ngyx);
-          } else {
-            ri[r].off = 0;
-            ri[r].y = ri[r].x = -(1 << 29);
-          }
-        }
+        ri[gt] = m0 + gt < M ? pixel_info(a, m0 + gt, ngyx) : no_pixel();
         named_bar_sync(1, NGATHER);
-        const int j = gt & 7;
+        const int j = gt & 7, r0 = gt >> 3;              // rows r0 + 16 i
+        const int slot = r0 * 128 + ((j ^ (r0 & 7)) << 4);
         for (int kb = kb_lo(sp); kb < kb_lo(sp + 1); ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           const int k = kb * BK + j * 8;
           const int t = k / a.nch, c = k - t * a.nch;
           const bool tv = t < a.ntaps;
-          const int dy = tv ? a.tap_dy[t] : 0, dx = tv ? a.tap_dx[t] : 0;
-          const __nv_bfloat16* S = reinterpret_cast<const __nv_bfloat16*>(a.S) + a.sc0 + c;
-          uint8_t* dst = sA + s * C_::A_BYTES;
-#pragma unroll 4
-          for (int i = 0; i < BM / 8; ++i) {
-            const int r = (gt >> 3) + 8 * i;
-            const RowInfo q = ri[r];
-            const int iy = q.y + dy, ix = q.x + dx;
-            const bool ok = tv && (unsigned)iy < (unsigned)a.sH && (unsigned)ix < (unsigned)a.sW;
-            const __nv_bfloat16* src = ok ? S + q.off + iy * a.s_sy + ix * a.s_sx : S;
-            cp_async_16(dst + r * 128 + ((j ^ (r & 7)) << 4), src, ok ? 16u : 0u);
+          const int dy = tv ? a.tap_dy[t] : -(1 << 29), dx = tv ? a.tap_dx[t] : 0;
+          const __nv_bfloat16* S = S0 + a.sc0 + c + ((long long)dy * a.s_sy + (long long)dx * a.s_sx);
+          uint8_t* dst = sA + s * C_::A_BYTES + slot;
+#pragma unroll
+          for (int i = 0; i < BM / 16; ++i) {
+            const RowInfo q = ri[r0 + 16 * i];
+            const bool ok = (unsigned)(q.y + dy) < (unsigned)a.sH && (unsigned)(q.x + dx) < (unsigned)a.sW;
+            cp_async_16(dst + i * 2048, ok ? S + q.off : S0, ok ? 16u : 0u);
           }
-          cp_async_commit();
-          if (it >= LAG) {
-            cp_async_wait<LAG>();
-            publish(it - LAG);
-          }
+          cp_async_mbar_arrive(&full[s]);  // lands asynchronously; the MMA thread fences the proxies
         }
       } else {
         constexpr int CPR = BN / 8;           // 16-byte chunks per k row
         constexpr int RSTEP = NGATHER / CPR;  // rows covered per pass
-        const int jj = gt % CPR;
+        static_assert(RSTEP % 8 == 0 && BK % RSTEP == 0, "gather rows must keep one swizzle phase per thread");
+        const int jj = gt % CPR, r0 = gt / CPR;
         const int n = n0 + jj * 8;
         const int t = n / a.nch, c = n - t * a.nch;
         const bool tv = n < N && t < a.ntaps;
-        const int dy = tv ? a.tap_dy[t] : 0, dx = tv ? a.tap_dx[t] : 0;
-        const __nv_bfloat16* S = reinterpret_cast<const __nv_bfloat16*>(a.S) + a.sc0 + c;
+        const int dy = tv ? a.tap_dy[t] : -(1 << 29), dx = tv ? a.tap_dx[t] : 0;
+        const __nv_bfloat16* S = S0 + a.sc0 + c + ((long long)dy * a.s_sy + (long long)dx * a.s_sx);
         const int sub = jj >> 3, j = jj & 7;
+        const int slot = sub * 8192 + r0 * 128 + ((j ^ (r0 & 7)) << 4);  // RSTEP is a multiple of 8
         for (int kb = kb_lo(sp); kb < kb_lo(sp + 1); ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           RowInfo* ri = rows + (it & 1) * BK;
-          {
-            const int g = kb * BK + gt;
-            if (g < K) {
-              ri[gt] = pixel_info(a, g, ngyx);
-            } else {
-              ri[gt].off = 0;
-              ri[gt].y = ri[gt].x = -(1 << 29);
-            }
-          }
+          if (gt < BK) ri[gt] = kb * BK + gt < K ? pixel_info(a, kb * BK + gt, ngyx) : no_pixel();
           named_bar_sync(1, NGATHER);
-          uint8_t* dst = sB + s * C_::B_BYTES + sub * 8192;
-#pragma unroll 4
+          uint8_t* dst = sB + s * C_::B_BYTES + slot;
+#pragma unroll
           for (int i = 0; i < BK / RSTEP; ++i) {
-            const int r = gt / CPR + RSTEP * i;
-            const RowInfo q = ri[r];
-            const int iy = q.y + dy, ix = q.x + dx;
-            const bool ok = tv && (unsigned)iy < (unsigned)a.sH && (unsigned)ix < (unsigned)a.sW;
-            const __nv_bfloat16* src = ok ? S + q.off + iy * a.s_sy + ix * a.s_sx : S;
-            cp_async_16(dst + r * 128 + ((j ^ (r & 7)) << 4), src, ok ? 16u : 0u);
+            const RowInfo q = ri[r0 + RSTEP * i];
+            const bool ok = (unsigned)(q.y + dy) < (unsigned)a.sH && (unsigned)(q.x + dx) < (unsigned)a.sW;
+            cp_async_16(dst + i * RSTEP * 128, ok ? S + q.off : S0, ok ? 16u : 0u);
           }
-          cp_async_commit();
-          if (it >= LAG) {
-            cp_async_wait<LAG>();
-            publish(it - LAG);
-          }
+          cp_async_mbar_arrive(&full[s]);  // lands asynchronously; the MMA thread fences the proxies
         }
       }
     }
-    cp_async_wait<0>();
-    for (int q = it - LAG < 0 ? 0 : it - LAG; q < it; ++q) publish(q);
   } else {
     // ------------------------------------------------------------ epilogue (warps 2..5)
     const int q = warp & 3;

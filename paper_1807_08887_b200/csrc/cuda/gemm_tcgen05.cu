@@ -11,7 +11,8 @@
 // Epilogues (c_mode): 0 = bf16 store, 1 = fp32 store (Case-2 partials, weight grads), 2 = fp32 accumulate,
 // 3 = fused momentum-SGD on the weight gradient: M = M*s0 + acc (fp32, in place), W = W - M*s1 (bf16, in
 // place); 4 (internal) = split-K fp32 partial into plane `split` of a 3-D workspace, reduced in split order
-// by splitk_reduce_kernel (used when the output has too few tiles to fill 148 SMs, e.g. M = 128 RNN steps).  Mode 3 is the coalesced optimizer chain of P:L674-678 folded into the gradient's producer so the
+// by splitk_reduce_kernel (used when the output has too few tiles to fill 148 SMs, e.g. M = 128 RNN steps; the
+// reduction applies the fused optimizer when c_mode is 3).  Mode 3 is the coalesced optimizer chain of P:L674-678 folded into the gradient's producer so the
 // gradient never touches HBM.
 //
 // Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer (1 lane),
@@ -348,8 +349,22 @@ static int dispatch_bn(const tofu_gemm_args* g, const CUtensorMap* tm, cudaStrea
 
 // Split-K reduction: C = epilogue(sum_s WS[s]) in fixed split order (deterministic).
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N,
-                                                            void* C, int ldc, int mode) {
+                                                            void* C, int ldc, int mode, __nv_bfloat16* D, int ldd,
+                                                            float s0, float s1) {
   const int64_t plane = (int64_t)M * N;
+  if (mode == 3) {  // fused momentum-SGD on the reduced weight gradient (c_mode 3 with split-K)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < plane; i += (int64_t)gridDim.x * blockDim.x) {
+      float acc = ws[i];
+      for (int s = 1; s < splits; ++s) acc += ws[s * plane + i];
+      const int64_t m = i / N, n = i % N;
+      float* c = reinterpret_cast<float*>(C) + m * ldc + n;
+      const float mm = *c * s0 + acc;
+      *c = mm;
+      __nv_bfloat16* w = D + m * ldd + n;
+      *w = __float2bfloat16_rn(__bfloat162float(*w) - mm * s1);
+    }
+    return;
+  }
   const bool vec = (N % 4 == 0) && (ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
   if (vec) {
     const int64_t n4 = plane / 4;
@@ -392,7 +407,7 @@ static size_t g_ws_bytes = 0;
 static std::mutex g_ws_mu;
 
 static int auto_splits(const tofu_gemm_args* g, int bn) {
-  if (g->c_mode == 3 || g->splits == 1) return 1;
+  if (g->splits == 1) return 1;
   const int nk = (g->K + BK - 1) / BK;
   if (g->splits > 1) return g->splits < nk ? g->splits : nk;
   const int tiles = ((g->M + BM - 1) / BM) * ((g->N + bn - 1) / bn);
@@ -490,7 +505,8 @@ extern "C" int tofu_gemm_launch_planned(const tofu_gemm_args* g, const void* tma
     int blocks = (int)((n + 255) / 256);
     if (blocks > g_num_sms * 8) blocks = g_num_sms * 8;
     splitk_reduce_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float*>(g->ws), g->splits, g->M, g->N, g->C,
-                                                 g->ldc, g->c_mode);
+                                                 g->ldc, g->c_mode, reinterpret_cast<__nv_bfloat16*>(g->D), g->ldd,
+                                                 g->s0, g->s1);
     return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
   }
   return bn == 256 ? dispatch_bn<256>(g, tm, st) : dispatch_bn<128>(g, tm, st);

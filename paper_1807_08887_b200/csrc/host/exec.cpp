@@ -694,6 +694,65 @@ void build_launches(Exec& E) {
 
 std::vector<tofu_conv_args> conv_args(Exec& E, int o, int li);
 
+// 1x1 stride-1 convolution as tofu_gemm_args (forward: pixels x ci . (co x ci)^T; data gradient:
+// pixels x co . (co x ci); weight gradient: (pixels x co)^T . (pixels x ci)), optimizer fused as for GEMMs.
+bool conv1x1_gemm(Exec& E, int o, int li, Exec::GemmLaunch& G) {
+  const Graph& g = *E.g;
+  const ConvGeom cg = conv_geom(g.def_of(o));
+  if (cg.R != 1 || cg.s != 1 || cg.p != 0) return false;
+  const int r = E.local[li];
+  const LOp& L = E.lops[li][o];
+  const Buf &P0 = L.in[0], &P1 = L.in[1], &O = L.out;
+  int64_t r0, c0, ld0, off0, r1, c1, ld1, off1, ro, co, ldo, offo;
+  const bool w_out = cg.kind == 2;
+  // activations / gradients over pixels: [b, y, x][c] row blocks; weights [co][1][1][ci]: [co][ci]
+  if (!flat2(P0.buf_box, P0.box, 3, r0, c0, ld0, off0)) return false;
+  if (!flat2(P1.buf_box, P1.box, cg.kind == 2 ? 3 : 1, r1, c1, ld1, off1)) return false;
+  if (!flat2(O.buf_box, O.box, w_out ? 1 : 3, ro, co, ldo, offo)) return false;
+  std::memset(&G.a, 0, sizeof G.a);
+  char* base = E.arena[r];
+  G.a.A = base + P0.off + off0 * 2;
+  G.a.lda = (int)ld0;
+  G.a.B = base + P1.off + off1 * 2;
+  G.a.ldb = (int)ld1;
+  G.a.M = (int)ro;
+  G.a.N = (int)co;
+  if (cg.kind == 0) {        // A = X [pixels][ci] K-major, B = W [co][ci] K-major
+    G.a.K = (int)c0;
+  } else if (cg.kind == 1) { // A = dY [pixels][co] K-major, B = W [co][ci] MN-major
+    G.a.K = (int)c0;
+    G.a.b_mn_major = 1;
+  } else {                   // A = dY [pixels][co] MN-major, B = X [pixels][ci] MN-major
+    G.a.K = (int)r0;
+    G.a.a_mn_major = 1;
+    G.a.b_mn_major = 1;
+  }
+  const int64_t ec = O.dtype == TOFU_BF16 ? 2 : 4;
+  G.a.C = base + O.off + offo * ec;
+  G.a.ldc = (int)ldo;
+  G.a.c_mode = O.dtype == TOFU_BF16 ? 0 : 1;
+  if (L.fused_opt >= 0) {
+    const LOp& Lm = E.lops[li][L.fused_opt];
+    const LOp& Ls = E.lops[li][L.fused_opt + 1];
+    int64_t mr, mc, ldm, moff, wr, wc, ldw, woff;
+    if (!flat2(Lm.in[0].buf_box, Lm.in[0].box, 1, mr, mc, ldm, moff) ||
+        !flat2(Ls.in[0].buf_box, Ls.in[0].box, 1, wr, wc, ldw, woff) || mr != ro || mc != co)
+      return false;
+    auto at = [&](int op, const char* key) {
+      auto it = g.ops[op].attrs.find(key);
+      return (float)(it == g.ops[op].attrs.end() ? 0.0 : it->second);
+    };
+    G.a.c_mode = 3;
+    G.a.C = base + Lm.in[0].off + moff * 4;
+    G.a.ldc = (int)ldm;
+    G.a.D = base + Ls.in[0].off + woff * 2;
+    G.a.ldd = (int)ldw;
+    G.a.s0 = at(L.fused_opt, "mu");
+    G.a.s1 = at(L.fused_opt + 1, "lr");
+  }
+  return true;
+}
+
 void finalize(Exec& E) {
   if (E.finalized) return;
   const Graph& g = *E.g;
@@ -774,6 +833,19 @@ void finalize(Exec& E) {
       const OpDef& d = g.def_of((int)o);
       if (std::string(kernel_kind(d)) != "conv" || E.lops[li][o].skip) continue;
       LOp& L = E.lops[li][o];
+      {  // a 1x1 stride-1 convolution is a plain GEMM over pixel rows: the TMA-fed tcgen05 GEMM when every
+         // operand is a row block of its buffer (else the gather kernel)
+        Exec::GemmLaunch G;
+        if (conv1x1_gemm(E, (int)o, li, G)) {
+          G.a.splits = 0;
+          G.a.ws = pass == 0 ? reinterpret_cast<void*>(uintptr_t(1) << 20) : E.ws_dev;
+          int rc = tofu_gemm_plan_tmaps(&G.a, G.tm, &G.bn);
+          if (rc) throw Error(rc, "gemm tensor map for 1x1 conv op " + g.ops[o].name);
+          ws_need = std::max<int64_t>(ws_need, tofu_gemm_workspace_bytes(&G.a));
+          if (pass == 1) E.gemms[{(int)o, li}] = G;
+          continue;
+        }
+      }
       std::vector<Exec::ConvLaunch> cls;
       for (auto& a : conv_args(E, (int)o, li)) {
         Exec::ConvLaunch C;
@@ -1062,6 +1134,8 @@ int run_compute(Exec& E, int o, int li, cudaStream_t st) {
     return tofu_gemm_launch_planned(&G.a, G.tm, G.bn, st);
   }
   if (kind == "conv") {
+    auto git = E.gemms.find({o, li});
+    if (git != E.gemms.end()) return tofu_gemm_launch_planned(&git->second.a, git->second.tm, git->second.bn, st);
     for (auto& C : E.convs.at({o, li})) {
       const int rc = tofu_conv_launch_planned(&C.a, C.tm, st);
       if (rc) return rc;

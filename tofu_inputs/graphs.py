@@ -10,6 +10,7 @@ Workloads follow BASELINE.json configs:
   configs[0]  mlp(64, [256, 512, 512])          2-layer MLP, k = 2
   configs[1]  mlp(512, [8192, 8192])            single large FC layer, k = 8
   configs[2]  lstm(6, 4096, 20, 128)             6-layer LSTM, hidden 4K, 20 steps, batch 128
+  configs[3]  wresnet_depth(152, 4, 32)          WResNet-152-4, batch 32, 224x224 images
 """
 from __future__ import annotations
 
@@ -105,6 +106,8 @@ def config(i: int) -> dict:
         return mlp(512, [8192, 8192])
     if i == 2:
         return lstm(6, 4096, 20, 128)
+    if i == 3:
+        return wresnet_depth(152, 4, 32)
     raise ValueError(f"config {i} not built yet")
 
 
