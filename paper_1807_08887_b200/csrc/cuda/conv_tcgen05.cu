@@ -75,6 +75,15 @@ __device__ __forceinline__ RowInfo pixel_info(const tofu_conv_args& a, int g, in
   ri.off = (long long)(gb + a.sb0) * a.s_sb + (long long)ri.y * a.s_sy + (long long)ri.x * a.s_sx;
   return ri;
 }
+__device__ __forceinline__ RowInfo lds_rowinfo(const RowInfo* p) {  // explicit shared-space load
+  uint32_t w0, w1, w2, w3;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(smem_u32(p)));
+  RowInfo r;
+  r.off = (long long)(((uint64_t)w1 << 32) | w0);
+  r.y = (int)w2;
+  r.x = (int)w3;
+  return r;
+}
 __device__ __forceinline__ RowInfo no_pixel() {
   RowInfo ri;
   ri.off = 0;
@@ -221,11 +230,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int m0 = (tile / tiles_n) * BM;
       const int n0 = (tile % tiles_n) * BN;
       if constexpr (KIND == 0) {
-        RowInfo* ri = rows + (local & 1) * BM;
-        ri[gt] = m0 + gt < M ? pixel_info(a, m0 + gt, ngyx) : no_pixel();
-        named_bar_sync(1, NGATHER);
-        const int j = gt & 7, r0 = gt >> 3;              // rows r0 + 16 i
+        // this thread's 8 rows (r0 + 16 i) of the tile, decoded once per tile into registers
+        const int j = gt & 7, r0 = gt >> 3;
         const int slot = r0 * 128 + ((j ^ (r0 & 7)) << 4);
+        RowInfo q[BM / 16];
+#pragma unroll
+        for (int i = 0; i < BM / 16; ++i) {
+          const int m = m0 + r0 + 16 * i;
+          q[i] = m < M ? pixel_info(a, m, ngyx) : no_pixel();
+        }
         for (int kb = kb_lo(sp); kb < kb_lo(sp + 1); ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
@@ -237,9 +250,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           uint8_t* dst = sA + s * C_::A_BYTES + slot;
 #pragma unroll
           for (int i = 0; i < BM / 16; ++i) {
-            const RowInfo q = ri[r0 + 16 * i];
-            const bool ok = (unsigned)(q.y + dy) < (unsigned)a.sH && (unsigned)(q.x + dx) < (unsigned)a.sW;
-            cp_async_16(dst + i * 2048, ok ? S + q.off : S0, ok ? 16u : 0u);
+            const bool ok = (unsigned)(q[i].y + dy) < (unsigned)a.sH && (unsigned)(q[i].x + dx) < (unsigned)a.sW;
+            cp_async_16(dst + i * 2048, ok ? S + q[i].off : S0, ok ? 16u : 0u);
           }
           cp_async_mbar_arrive(&full[s]);  // lands asynchronously; the MMA thread fences the proxies
         }
@@ -259,14 +271,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const int s = it % STAGES;
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           RowInfo* ri = rows + (it & 1) * BK;
-          if (gt < BK) ri[gt] = kb * BK + gt < K ? pixel_info(a, kb * BK + gt, ngyx) : no_pixel();
+          if (gt < BK) {
+            const RowInfo v = kb * BK + gt < K ? pixel_info(a, kb * BK + gt, ngyx) : no_pixel();
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(ri + gt)),
+                         "r"((uint32_t)((uint64_t)v.off & 0xffffffffu)), "r"((uint32_t)((uint64_t)v.off >> 32)),
+                         "r"((uint32_t)v.y), "r"((uint32_t)v.x)
+                         : "memory");
+          }
           named_bar_sync(1, NGATHER);
           uint8_t* dst = sB + s * C_::B_BYTES + slot;
+          RowInfo q[BK / RSTEP];
+#pragma unroll
+          for (int i = 0; i < BK / RSTEP; ++i) q[i] = lds_rowinfo(ri + r0 + RSTEP * i);  // all loads first
 #pragma unroll
           for (int i = 0; i < BK / RSTEP; ++i) {
-            const RowInfo q = ri[r0 + RSTEP * i];
-            const bool ok = (unsigned)(q.y + dy) < (unsigned)a.sH && (unsigned)(q.x + dx) < (unsigned)a.sW;
-            cp_async_16(dst + i * RSTEP * 128, ok ? S + q.off : S0, ok ? 16u : 0u);
+            const bool ok = (unsigned)(q[i].y + dy) < (unsigned)a.sH && (unsigned)(q[i].x + dx) < (unsigned)a.sW;
+            cp_async_16(dst + i * RSTEP * 128, ok ? S + q[i].off : S0, ok ? 16u : 0u);
           }
           cp_async_mbar_arrive(&full[s]);  // lands asynchronously; the MMA thread fences the proxies
         }
@@ -321,7 +341,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 reinterpret_cast<uint4*>(o)[v] = w;
               }
             } else {
-              for (int e = 0; e < N - n; ++e) o[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
+#pragma unroll
+              for (int e = 0; e < 32; ++e)
+                if (e < N - n) o[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
             }
           } else {
             float* o = reinterpret_cast<float*>(rowp) + n;
@@ -331,7 +353,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 reinterpret_cast<float4*>(o)[v] = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
                                                               __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
             } else {
-              for (int e = 0; e < N - n; ++e) o[e] = __uint_as_float(r[e]);
+#pragma unroll
+              for (int e = 0; e < 32; ++e)
+                if (e < N - n) o[e] = __uint_as_float(r[e]);
             }
           }
         }
