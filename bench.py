@@ -105,32 +105,60 @@ def oracle_step_time(spec, vals):
     return time.perf_counter() - t
 
 
+def graph_work(spec):
+    """Σ over ops of the iteration-space volume (multiply-adds of a contraction, elements otherwise): the
+    oracle's work, used to extrapolate a bounded oracle sample to the full workload."""
+    from oracle.graph import Graph
+    g = Graph(spec)
+    tot = 0
+    for op in g.ops:
+        v = 1
+        for n in g.ranges[op["name"]].values():
+            v *= n
+        tot += v
+    return tot
+
+
+def oracle_sample(cfg):
+    """(sample spec, full-workload samples represented per sample step, description) of the bounded CPU
+    oracle run for workload cfg: about 10-30 s of fp64 work on the host cores."""
+    full = config(cfg)
+    batch = full.get("meta", {}).get("samples_per_step", full["tensors"]["X"]["shape"][0])
+    if cfg == 2:
+        from tofu_inputs.graphs import lstm
+        spec = lstm(1, 4096, 20, 1)   # 1 of 6 layers, 1 sequence: 1/6 of a sequence's work
+        return spec, 1.0 / 6.0, "1 LSTM layer (of 6), batch 1 sequence of 20 steps, fp64; samples/s = 1/(6 t)"
+    if cfg == 3:
+        from tofu_inputs.graphs import wresnet
+        spec = wresnet([1], 4, 1, 224)   # stem + first bottleneck unit at full width, 1 image
+        frac = graph_work(spec) / (graph_work(full) / batch)
+        return spec, frac, ("WResNet-152-4 stem + first bottleneck unit, 1 image, fp64; extrapolated to the full "
+                            f"network by iteration-space work (this sample = {frac:.4f} of an image)")
+    from tofu_inputs.graphs import mlp
+    dims = [full["tensors"]["X"]["shape"][1], full["tensors"]["Y"]["shape"][1]]
+    sb = 32 if batch > 32 else batch
+    return mlp(sb, dims), float(sb), f"{CONFIG_NAME[cfg]} layer shapes at batch {sb} per step (full batch {batch}); fp64"
+
+
 def reference_arm(args, world, rank):
     """--impl reference: the oracle (fp64 CPU) on the host cores, rank 0 only."""
     if rank != 0:
         return
-    from tofu_inputs.graphs import mlp
+    spec, per_step, sample = oracle_sample(args.config)
     full = config(args.config)
-    batch = full.get("meta", {}).get("samples_per_step", full["tensors"]["X"]["shape"][0])
-    if args.config == 2:
-        from tofu_inputs.graphs import lstm
-        sb = 1
-        spec = lstm(6, 4096, 20, sb)   # bounded sample: same model, 1 sequence per step
-    else:
-        dims = [full["tensors"]["X"]["shape"][1], full["tensors"]["Y"]["shape"][1]]
-        sb = 32 if batch > 32 else batch
-        spec = mlp(sb, dims)   # bounded sample: same layer shapes, batch 32 per step
+    full_batch = full.get("meta", {}).get("samples_per_step", full["tensors"]["X"]["shape"][0])
     vals = make_values(spec, seed=0)
     for _ in range(args.warmup):
         oracle_step_time(spec, vals)
     ts = [oracle_step_time(spec, vals) for _ in range(args.steps)]
     t = sum(ts) / len(ts)
-    v = sb / t
-    sample = f"{CONFIG_NAME[args.config]} layer shapes at batch {sb} per step (full batch {batch}); fp64 numpy"
+    v = per_step / t
+    sb = per_step
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": CONFIG_NAME[args.config], "global_batch": sb, "parallelism": "cpu"},
+            "config": {"workload": CONFIG_NAME[args.config], "global_batch": full_batch, "parallelism": "cpu",
+                       "oracle_samples_per_step": sb},
             "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cpu_threads(), "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -385,17 +413,9 @@ def main():
     if world == 1 and args.virtual_k > 1:
         line["virtual_partitioned"] = virtual_partitioned(spec, vals, args.virtual_k, max(args.steps, 5))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        if args.config == 2:
-            from tofu_inputs.graphs import lstm
-            sspec = lstm(1, 4096, 20, 1)
-            t = oracle_step_time(sspec, make_values(sspec, seed=0)) * 6
-            sample = "1 LSTM layer (of 6) at batch 1 sequence, 20 steps, fp64; time x6 for the 6-layer step"
-            v = 1.0 / t
-        else:
-            t = oracle_step_time(spec, vals)
-            sample = f"1 full training step of {CONFIG_NAME[args.config]} (batch {batch}), fp64"
-            v = batch / t
-        line["cpu_baseline"] = {"value": v, "unit": "samples/s", "cores": cpu_threads(), "kind": "oracle",
+        sspec, per_step, sample = oracle_sample(args.config)
+        t = oracle_step_time(sspec, make_values(sspec, seed=0))
+        line["cpu_baseline"] = {"value": per_step / t, "unit": "samples/s", "cores": cpu_threads(), "kind": "oracle",
                                 "sample": sample}
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -234,7 +234,7 @@ def tap_eval(opdef, inputs: dict, box: dict):
             idx = [np.asarray(ix.value(grid)) for ix in acc.index]
             ops.append(_gather(arr, origin, idx, gshape))
             subs.append("".join(letters[v] for v in axes))
-        part = np.einsum(f"{subs[0]},{subs[1]}->{''.join(letters[v] for v in out_free)}", ops[0], ops[1])
+        part = np.einsum(f"{subs[0]},{subs[1]}->{''.join(letters[v] for v in out_free)}", ops[0], ops[1], optimize=True)
         sl = tuple(env[v] - box[v][0] if v in env else slice(None) for v in opdef.out_vars)
         out[sl] += part
     return out
