@@ -52,7 +52,7 @@ struct Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr bool LOADS = MODE == 2 || MODE == 3;
-  static constexpr int NBUF = KIND == 1 ? (LOADS ? 3 : 2) : 0;
+  static constexpr int NBUF = KIND == 1 ? 2 : 0;
   static constexpr int D_OFF = 4096;
   static constexpr int BUF_BYTES = MODE == 3 ? 6144 : 4096;
   static constexpr int EPI_BYTES = 4 * NBUF * BUF_BYTES;
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       } else {
         constexpr int CPR = BN / 8;           // 16-byte chunks per k row
         constexpr int RSTEP = NGATHER / CPR;  // rows covered per pass
-        static_assert(RSTEP % 8 == 0 && BK % RSTEP == 0, "gather rows must keep one swizzle phase per thread");
+        static_assert(BK % RSTEP == 0, "gather rows");
         const int jj = gt % CPR, r0 = gt / CPR;
         const int n = n0 + jj * 8;
         const int t = n / a.nch, c = n - t * a.nch;
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int dy = tv ? a.tap_dy[t] : -(1 << 29), dx = tv ? a.tap_dx[t] : 0;
         const __nv_bfloat16* S = S0 + a.sc0 + c + ((long long)dy * a.s_sy + (long long)dx * a.s_sx);
         const int sub = jj >> 3, j = jj & 7;
-        const int slot = sub * 8192 + r0 * 128 + ((j ^ (r0 & 7)) << 4);  // RSTEP is a multiple of 8
+        const int slot = sub * 8192 + r0 * 128;
         for (int kb = kb_lo(sp); kb < kb_lo(sp + 1); ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
@@ -286,7 +286,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
           for (int i = 0; i < BK / RSTEP; ++i) {
             const bool ok = (unsigned)(q[i].y + dy) < (unsigned)a.sH && (unsigned)(q[i].x + dx) < (unsigned)a.sW;
-            cp_async_16(dst + i * RSTEP * 128, ok ? S + q[i].off : S0, ok ? 16u : 0u);
+            const int sw = (j ^ ((r0 + RSTEP * i) & 7)) << 4;  // 128B swizzle phase of the row
+            cp_async_16(dst + i * RSTEP * 128 + sw, ok ? S + q[i].off : S0, ok ? 16u : 0u);
           }
           cp_async_mbar_arrive(&full[s]);  // lands asynchronously; the MMA thread fences the proxies
         }
@@ -481,19 +482,23 @@ __global__ void __launch_bounds__(256) splitk_reduce(const float* __restrict__ w
   }
 }
 
-// zero output rows of a kind-0 sub-op with no taps (e.g. the odd phases of a 1x1 stride-2 data gradient)
+// zero output rows of a kind-0 sub-op with no taps (e.g. the odd phases of a 1x1 stride-2 data gradient):
+// one thread per (row, 8 channels), 16-byte stores (N % 8 == 0 and 16-byte aligned rows, checked by the host)
 __global__ void __launch_bounds__(256) zero_rows(Params P) {
   const tofu_conv_args& a = P.a;
   const int ngyx = a.ngy * a.ngx;
-  const int64_t total = (int64_t)P.M * P.N;
+  const int n8 = P.N / 8;
+  const int64_t total = (int64_t)P.M * n8;
+  const int es = a.c_mode == 0 ? 2 : 4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int m = (int)(i / P.N), n = (int)(i % P.N);
+    const int m = (int)(i / n8), n = (int)(i - (int64_t)m * n8) * 8;
     const int gb = m / ngyx, rem = m - gb * ngyx;
     const int gy = rem / a.ngx, gx = rem - gy * a.ngx;
     const int64_t e = (int64_t)gb * a.c_sb + (int64_t)(a.c_ys * gy + a.c_y0) * a.c_sy +
                       (int64_t)(a.c_xs * gx + a.c_x0) * a.c_sx + n;
-    if (a.c_mode == 0) reinterpret_cast<__nv_bfloat16*>(a.C)[e] = __float2bfloat16_rn(0.f);
-    else reinterpret_cast<float*>(a.C)[e] = 0.f;
+    uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<char*>(a.C) + e * es);
+    o[0] = make_uint4(0, 0, 0, 0);
+    if (es == 4) o[1] = make_uint4(0, 0, 0, 0);
   }
 }
 
@@ -528,10 +533,7 @@ static int tmap2(CUtensorMap* tm, const void* ptr, CUtensorMapDataType dt, int e
              : 1;
 }
 
-static int bn_of(const tofu_conv_args* a, int N) {
-  if (a->kind == 1) return 128;
-  return N <= 128 ? 128 : 256;
-}
+static int bn_of(const tofu_conv_args* a, int N) { return N <= 128 ? 128 : 256; }
 
 static void dims_of(const tofu_conv_args* a, int& M, int& N, int& K) {
   const int pix = a->nb * a->ngy * a->ngx;
@@ -591,6 +593,13 @@ static int dispatch(const Params& P, const CUtensorMap* tm, int mode, cudaStream
       default: return TOFU_ERR_ARG;
     }
   }
+  if (bn == 256) switch (mode) {
+      case 1: return launch_t<1, 256, true, 1>(P, tm, st);
+      case 2: return launch_t<1, 256, true, 2>(P, tm, st);
+      case 3: return launch_t<1, 256, true, 3>(P, tm, st);
+      case 4: return launch_t<1, 256, true, 4>(P, tm, st);
+      default: return TOFU_ERR_ARG;
+    }
   switch (mode) {
     case 1: return launch_t<1, 128, true, 1>(P, tm, st);
     case 2: return launch_t<1, 128, true, 2>(P, tm, st);
@@ -686,7 +695,8 @@ extern "C" int tofu_conv_launch_planned(const tofu_conv_args* a, const void* tma
       if (a->c_mode == 1) return cudaMemset2DAsync(a->C, a->ldc * 4, 0, (size_t)N * 4, M, st) == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
       return a->c_mode == 2 ? TOFU_OK : TOFU_ERR_ARG;
     }
-    int blocks = (int)(((int64_t)M * N + 255) / 256);
+    if (N % 8) return TOFU_ERR_ALIGN;
+    int blocks = (int)(((int64_t)M * (N / 8) + 255) / 256);
     if (blocks > g_sms * 8) blocks = g_sms * 8;
     zero_rows<<<blocks, 256, 0, st>>>(P);
     return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;

@@ -56,3 +56,11 @@ for i in sorted(range(nl), key=lambda i: -ms[i])[:25]:
     d = descs[i]
     print(f"{ms[i]:7.3f} ms {d['kind']:8s} {d['op']:22s} {d['def']:14s} TF/s={d['flops'] / (ms[i] / 1e3) / 1e12:7.1f} "
           f"GB/s={d['bytes'] / (ms[i] / 1e3) / 1e9:7.1f} {d.get('fused', '')}")
+
+if os.environ.get("UNIT"):
+    print("--- launches of", os.environ["UNIT"])
+    for i, d in enumerate(descs):
+        if d["op"] and d["op"].startswith(os.environ["UNIT"] + "."):
+            print(f"{ms[i]:7.3f} ms {d['kind']:8s} {d['op']:22s} {d['def']:14s} "
+                  f"TF/s={d['flops'] / (ms[i] / 1e3) / 1e12:7.1f} GB/s={d['bytes'] / (ms[i] / 1e3) / 1e9:7.1f} "
+                  f"{d.get('fused', '')}")
