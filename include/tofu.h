@@ -148,10 +148,16 @@ typedef struct {
   int splits;  /* split-K: 0 = auto (when the output tiles cannot fill the SMs), 1 = off, n = n splits;
                   tofu_gemm_plan_tmaps writes the chosen value back */
   void* ws;    /* split-K fp32 workspace (tofu_gemm_workspace_bytes); NULL = library-owned */
+  /* element-wise epilogue of a bf16 output (c_mode 0; the consumers' ops fused into their producer, DESIGN
+   * R8/R13): ep bit 1 = add aux_add, bit 0 = relu, bit 2 = zero where aux_mask <= 0, applied in that order;
+   * aux tensors bf16 with C's layout (pitch ldc).  ep != 0 disables split-K. */
+  const void* aux_add;
+  const void* aux_mask;
+  int ep;
 } tofu_gemm_args;
 int tofu_gemm_bf16(const tofu_gemm_args* args, void* stream);
-/* Split form used by the executor: encode the TMA descriptors (A, B, C, D, workspace) once into `tmaps`
- * (5 x 128 bytes, 64-byte aligned; args->splits/ws are updated), then launch with them.  Split-K results
+/* Split form used by the executor: encode the TMA descriptors (A, B, C, D, workspace, mask) once into `tmaps`
+ * (6 x 128 bytes, 64-byte aligned; args->splits/ws are updated), then launch with them.  Split-K results
  * are reduced in fixed split order (deterministic). */
 int tofu_gemm_plan_tmaps(tofu_gemm_args* args, void* tmaps, int* bn_out);
 int tofu_gemm_launch_planned(const tofu_gemm_args* args, const void* tmaps, int bn, void* stream);
@@ -208,6 +214,11 @@ typedef struct {
   float s0, s1;
   int splits;
   void* ws;
+  /* kind 0, c_mode 0: element-wise epilogue as tofu_gemm_args.ep (bit 1 add aux_add, bit 0 relu, bit 2 zero
+   * where aux_mask <= 0); aux tensors bf16 with C's layout. */
+  const void* aux_add;
+  const void* aux_mask;
+  int ep;
 } tofu_conv_args;
 /* Encode TMA descriptors once (tmaps: 4 x 128 B, 64-byte aligned; args->splits updated), then launch. */
 int tofu_conv_plan(tofu_conv_args* args, void* tmaps);

@@ -308,14 +308,32 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc_fence_after();
         const int m = m0 + q * 32 + lane;
         char* rowp = nullptr;
+        int64_t erow = 0;
         if (m < M) {
           const int gb = m / ngyx, rem = m - gb * ngyx;
           const int gy = rem / a.ngx, gx = rem - gy * a.ngx;
-          const int64_t e = (int64_t)gb * a.c_sb + (int64_t)(a.c_ys * gy + a.c_y0) * a.c_sy +
-                            (int64_t)(a.c_xs * gx + a.c_x0) * a.c_sx;
-          rowp = reinterpret_cast<char*>(a.C) + e * (MODE == 0 ? 2 : 4);
+          erow = (int64_t)gb * a.c_sb + (int64_t)(a.c_ys * gy + a.c_y0) * a.c_sy + (int64_t)(a.c_xs * gx + a.c_x0) * a.c_sx;
+          rowp = reinterpret_cast<char*>(a.C) + erow * (MODE == 0 ? 2 : 4);
         }
+        // fused element-wise operands of this row's chunk, prefetched one chunk ahead (64 B each)
+        uint4 xa[4], xm[4];
+        auto load_aux = [&](int c, uint4 (&A)[4], uint4 (&Mk)[4]) {
+          const int n = n0 + c * 32;
+          const bool ok = MODE == 0 && a.ep && rowp && n + 32 <= N;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            A[v] = ok && (a.ep & 2)
+                       ? __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.aux_add) + erow + n) + v)
+                       : make_uint4(0, 0, 0, 0);
+            Mk[v] = ok && (a.ep & 4)
+                        ? __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.aux_mask) + erow + n) + v)
+                        : make_uint4(0, 0, 0, 0);
+          }
+        };
+        if (a.ep) load_aux(0, xa, xm);
         for (int c = 0; c < NCH; ++c) {
+          uint4 na[4], nm[4];
+          if (a.ep && c + 1 < NCH) load_aux(c + 1, na, nm);
           uint32_t r[32];
           tmem_ld_32x32b_x32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, r);
           tmem_ld_wait();
@@ -326,7 +344,48 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
           const int n = n0 + c * 32;
           if (!rowp || n >= N) continue;
-          if (MODE == 0) {
+          if (MODE == 0 && a.ep && n + 32 <= N) {
+            // fused element-wise consumers (DESIGN R8/R13): v = acc (+ add), relu, zero where mask <= 0
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              float f[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(r[8 * v + e]);
+              if (a.ep & 2) {
+                const uint4 u = xa[v];
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 x = __bfloat1622float2(h[e]);
+                  f[2 * e] += x.x;
+                  f[2 * e + 1] += x.y;
+                }
+              }
+              if (a.ep & 1)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) f[e] = fmaxf(f[e], 0.f);
+              if (a.ep & 4) {
+                const uint4 u = xm[v];
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 x = __bfloat1622float2(h[e]);
+                  if (!(x.x > 0.f)) f[2 * e] = 0.f;
+                  if (!(x.y > 0.f)) f[2 * e + 1] = 0.f;
+                }
+              }
+              uint4 w;
+              __nv_bfloat162* wh = reinterpret_cast<__nv_bfloat162*>(&w);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) wh[e] = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+              reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(rowp) + n)[v] = w;
+            }
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              xa[v] = na[v];
+              xm[v] = nm[v];
+            }
+          } else if (MODE == 0) {
             __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(rowp) + n;
             if (n + 32 <= N) {
 #pragma unroll
@@ -637,6 +696,9 @@ extern "C" int tofu_conv_plan(tofu_conv_args* a, void* tmaps) {
   const int bn = bn_of(a, N);
   if (a->kind == 0) {
     if (a->c_mode != 0 && a->c_mode != 1) return TOFU_ERR_ARG;
+    if (a->ep && (a->c_mode != 0 || a->n_out % 32 || ((a->ep & 2) && !a->aux_add) || ((a->ep & 4) && !a->aux_mask) ||
+                  mis(a->aux_add) || mis(a->aux_mask)))
+      return TOFU_ERR_ARG;
     if (a->nch % BK != 0 && !a->b_mn_major) {  // K columns contiguous: taps in natural order, b_tap == nch
       if (a->b_tap != a->nch) return TOFU_ERR_ARG;
       for (int t = 0; t < a->ntaps; ++t)

@@ -39,7 +39,7 @@ template <int BN, int MODE>
 struct GemmCfg {
   static constexpr bool LOADS = MODE == 2 || MODE == 3;
   static constexpr int NBUF = LOADS ? 3 : 2;
-  static constexpr int C_BYTES = 32 * 32 * (MODE == 0 ? 2 : 4);
+  static constexpr int C_BYTES = 32 * 32 * (MODE == 0 || MODE == 5 ? 2 : 4);
   static constexpr int D_OFF = 4096;
   static constexpr int BUF_BYTES = MODE == 3 ? 6144 : (C_BYTES < 1024 ? 1024 : C_BYTES);
   static constexpr int EPI_BYTES = 4 * NBUF * BUF_BYTES;
@@ -58,8 +58,10 @@ struct GemmCfg {
 template <int BN, bool A_MN, bool B_MN, int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD, int M, int N,
-                     int K, float s0, float s1, int splits) {
+                     const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD,
+                     const __grid_constant__ CUtensorMap tmE, int M, int N, int K, float s0, float s1, int splits,
+                     int ep, const __nv_bfloat16* __restrict__ aux_add, const __nv_bfloat16* __restrict__ aux_mask,
+                     int ldx) {
   using Cfg = GemmCfg<BN, MODE>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int NBUF = Cfg::NBUF;
@@ -197,10 +199,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     };
     if (Cfg::LOADS && lane == 0)
       for (int s = 0; s < NBUF - 1 && s < S; ++s) issue_load(s);
+    // MODE 5: the element-wise operands of this thread's row segment (64 B each), prefetched one chunk ahead
+    uint4 xa[4], xm[4];
+    auto load_aux = [&](int s, uint4 (&A)[4], uint4 (&Mk)[4]) {
+      int col, row;
+      chunk_coords(s, col, row);
+      row += lane;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const bool ok = row < M && col + 8 * v < N;
+        const int64_t e = (int64_t)row * ldx + col + 8 * v;
+        A[v] = (ok && (ep & 2)) ? __ldg(reinterpret_cast<const uint4*>(aux_add + e)) : make_uint4(0, 0, 0, 0);
+        Mk[v] = (ok && (ep & 4)) ? __ldg(reinterpret_cast<const uint4*>(aux_mask + e)) : make_uint4(0, 0, 0, 0);
+      }
+    };
+    if (MODE == 5 && S > 0) load_aux(0, xa, xm);
     int local = 0;
     for (int s = 0; s < S; ++s) {
       const int c = s % NCH;
       const int acc = local & 1;
+      uint4 na[4], nm[4];
+      if (MODE == 5 && s + 1 < S) load_aux(s + 1, na, nm);
       if (c == 0) {
         mbar_wait(&acc_full[acc], (local >> 1) & 1);
         tc_fence_after();
@@ -226,7 +245,49 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (lane == 0) bulk_wait_read<NBUF - 1>();
         __syncwarp();
       }
-      if (MODE == 0) {
+      if (MODE == 5) {
+        // fused element-wise ops of the output's consumers (DESIGN R8/R13): v = acc (+ add), relu, mask
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int off = lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
+          float v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[8 * j + e]);
+          if (ep & 2) {
+            const uint4 u = xa[j];
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(h[e]);
+              v[2 * e] += f.x;
+              v[2 * e + 1] += f.y;
+            }
+          }
+          if (ep & 1)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
+          if (ep & 4) {
+            const uint4 u = xm[j];
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(h[e]);
+              if (!(f.x > 0.f)) v[2 * e] = 0.f;
+              if (!(f.y > 0.f)) v[2 * e + 1] = 0.f;
+            }
+          }
+          uint4 w;
+          __nv_bfloat162* wh = reinterpret_cast<__nv_bfloat162*>(&w);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) wh[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+          *reinterpret_cast<uint4*>(b + off) = w;
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          xa[v] = na[v];
+          xm[v] = nm[v];
+        }
+      } else if (MODE == 0) {
         uint32_t p[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -329,18 +390,21 @@ static int launch_t(const tofu_gemm_args* g, const CUtensorMap* tm, cudaStream_t
   const int units = ((g->M + BM - 1) / BM) * ((g->N + BN - 1) / BN) * splits;
   int grid = units < g_num_sms ? units : g_num_sms;
   if (g->max_ctas > 0 && grid > g->max_ctas) grid = g->max_ctas;
-  kern<<<grid, NTHREADS, Cfg::SMEM, st>>>(tm[0], tm[1], tm[2], tm[3], g->M, g->N, g->K, g->s0, g->s1, splits);
+  kern<<<grid, NTHREADS, Cfg::SMEM, st>>>(tm[0], tm[1], tm[2], tm[3], tm[5], g->M, g->N, g->K, g->s0, g->s1, splits,
+                                         g->ep, reinterpret_cast<const __nv_bfloat16*>(g->aux_add),
+                                         reinterpret_cast<const __nv_bfloat16*>(g->aux_mask), g->ldc);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }
 
 template <int BN>
 static int dispatch_bn(const tofu_gemm_args* g, const CUtensorMap* tm, cudaStream_t st) {
-  const int key = (g->a_mn_major ? 1 : 0) | (g->b_mn_major ? 2 : 0) | (g->c_mode << 2);
+  const int mode = g->c_mode == 0 && g->ep ? 5 : g->c_mode;
+  const int key = (g->a_mn_major ? 1 : 0) | (g->b_mn_major ? 2 : 0) | (mode << 2);
   switch (key) {
 #define TOFU_CASE(AM, BMJ, O) \
   case ((AM) | ((BMJ) << 1) | ((O) << 2)): return launch_t<BN, (bool)(AM), (bool)(BMJ), O>(g, tm, st);
 #define TOFU_CASES(O) TOFU_CASE(0, 0, O) TOFU_CASE(0, 1, O) TOFU_CASE(1, 0, O) TOFU_CASE(1, 1, O)
-    TOFU_CASES(0) TOFU_CASES(1) TOFU_CASES(2) TOFU_CASES(3) TOFU_CASES(4)
+    TOFU_CASES(0) TOFU_CASES(1) TOFU_CASES(2) TOFU_CASES(3) TOFU_CASES(4) TOFU_CASES(5)
 #undef TOFU_CASES
 #undef TOFU_CASE
     default: return TOFU_ERR_ARG;
@@ -407,7 +471,7 @@ static size_t g_ws_bytes = 0;
 static std::mutex g_ws_mu;
 
 static int auto_splits(const tofu_gemm_args* g, int bn) {
-  if (g->splits == 1) return 1;
+  if (g->splits == 1 || g->ep) return 1;
   const int nk = (g->K + BK - 1) / BK;
   if (g->splits > 1) return g->splits < nk ? g->splits : nk;
   const int tiles = ((g->M + BM - 1) / BM) * ((g->N + bn - 1) / bn);
@@ -426,11 +490,14 @@ extern "C" int64_t tofu_gemm_workspace_bytes(const tofu_gemm_args* g) {
   return g->splits > 1 ? (int64_t)g->splits * g->M * g->N * 4 : 0;
 }
 
-// tmaps: 5 x CUtensorMap (A, B, C, D, split-K workspace), 64-byte aligned, 640 bytes.  args->splits is
+// tmaps: 6 x CUtensorMap (A, B, C, D, split-K workspace, mask operand), 64-byte aligned, 768 bytes.  args->splits is
 // in/out: 0 = choose (split-K when the output has too few tiles to fill the SMs), 1 = off, n = n splits.
 extern "C" int tofu_gemm_plan_tmaps(tofu_gemm_args* g, void* tmaps, int* bn_out) {
   if (encode_fn_init() != 0) return TOFU_ERR_CUDA;
   if (!g || g->M < 0 || g->N < 0 || g->K < 0 || g->c_mode < 0 || g->c_mode > 3) return TOFU_ERR_ARG;
+  if (g->ep && (g->c_mode != 0 || ((g->ep & 2) && !g->aux_add) || ((g->ep & 4) && !g->aux_mask) ||
+                (reinterpret_cast<uintptr_t>(g->aux_add) & 15) || (reinterpret_cast<uintptr_t>(g->aux_mask) & 15)))
+    return TOFU_ERR_ARG;
   if (g->c_mode == 3 && (!g->D || (g->ldd % 8))) return TOFU_ERR_ARG;
   // TMA: row pitch must be a multiple of 16 bytes, bases 16-byte aligned
   const int ce = g->c_mode == 0 ? 2 : 4;
@@ -454,7 +521,11 @@ extern "C" int tofu_gemm_plan_tmaps(tofu_gemm_args* g, void* tmaps, int* bn_out)
   else r = make_tmap(&tm[2], g->C, F32, 4, g->N, g->M, g->ldc, 32, 32, SW128);
   if (r) return TOFU_ERR_CUDA;
   if (g->c_mode == 3) r = make_tmap(&tm[3], g->D, BF, 2, g->N, g->M, g->ldd, 32, 32, SW64);
+  else if (g->ep & 2) r = make_tmap(&tm[3], g->aux_add, BF, 2, g->N, g->M, g->ldc, 32, 32, SW64);
   else tm[3] = tm[2];
+  if (r) return TOFU_ERR_CUDA;
+  if (g->ep & 4) r = make_tmap(&tm[5], g->aux_mask, BF, 2, g->N, g->M, g->ldc, 32, 32, SW64);
+  else tm[5] = tm[2];
   if (r) return TOFU_ERR_CUDA;
   if (g->splits > 1) {
     void* ws = g->ws;
@@ -496,7 +567,7 @@ extern "C" int tofu_gemm_launch_planned(const tofu_gemm_args* g, const void* tma
   const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(tmaps);
   if (g->splits > 1) {
     // partial products into the workspace planes, then one ordered reduction into C
-    const CUtensorMap tw[4] = {tm[0], tm[1], tm[4], tm[4]};
+    const CUtensorMap tw[6] = {tm[0], tm[1], tm[4], tm[4], tm[4], tm[4]};
     tofu_gemm_args p = *g;
     p.c_mode = 4;
     int rc = bn == 256 ? dispatch_bn<256>(&p, tw, st) : dispatch_bn<128>(&p, tw, st);
@@ -513,7 +584,7 @@ extern "C" int tofu_gemm_launch_planned(const tofu_gemm_args* g, const void* tma
 }
 
 extern "C" int tofu_gemm_bf16(const tofu_gemm_args* g, void* stream) {
-  alignas(64) CUtensorMap tm[5];
+  alignas(64) CUtensorMap tm[6];
   tofu_gemm_args a = *g;
   int bn = 0;
   int r = tofu_gemm_plan_tmaps(&a, tm, &bn);

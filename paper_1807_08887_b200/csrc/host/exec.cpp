@@ -96,6 +96,8 @@ struct LOp {
   bool fused_sgd = false;
   int fused_opt = -1;         // GEMM epilogue absorbs mom (this index) + sgd (index + 1)
   bool fused_next = false;    // LSTM cell: this launch also computes the next op (c+h, bwd_a+bwd_c)
+  int ep = 0;                 // element-wise epilogue of the output's consumers: 1 relu, 2 add, 4 mask
+  Buf epi_add, epi_mask;      // its bf16 operands (the output's layout)
   std::vector<tofu_piece> fetch, reduce;
   std::vector<int> fetch_src, reduce_nremote;  // for the ledger
 };
@@ -153,7 +155,7 @@ struct Exec {
   bool finalized = false;
   struct GemmLaunch {
     tofu_gemm_args a;
-    alignas(64) CUtensorMap tm[5];
+    alignas(64) CUtensorMap tm[6];
     int bn;
   };
   std::map<std::pair<int, int>, GemmLaunch> gemms;  // (op, li)
@@ -626,6 +628,97 @@ void lower(Exec& E) {
         La.fused_next = true;
         Lb.skip = true;
       }
+  // Element-wise consumers folded into their producer's epilogue (R8/R13): a GEMM / convolution whose bf16
+  // output T is read only by one relu / addrelu / add / relu_grad(·, T) op (and an add's result only by one
+  // relu_grad) writes that op's output directly; the other operands (produced earlier) are read by the
+  // epilogue.  Every operand must be the rank's own shard of the same box (no communication moves).
+  if (E.fuse) {
+    std::vector<int> producer(g.tensors.size(), -1), nprod(g.tensors.size(), 0), nread(g.tensors.size(), 0);
+    for (size_t o = 0; o < g.ops.size(); ++o) {
+      producer[g.ops[o].output] = (int)o;
+      ++nprod[g.ops[o].output];
+      for (int t : g.ops[o].inputs) ++nread[t];
+    }
+    std::set<int> aliased;
+    for (auto& pr : g.alias) {
+      aliased.insert(pr.first);
+      aliased.insert(pr.second);
+    }
+    auto consumer = [&](int t) {  // the single op reading t (after its producer), else -1
+      if (nread[t] != 1 || nprod[t] != 1 || aliased.count(t)) return -1;
+      for (size_t x = producer[t] + 1; x < g.ops.size(); ++x)
+        for (int u : g.ops[x].inputs)
+          if (u == t) return (int)x;
+      return -1;
+    };
+    auto earlier = [&](int t, int o) { return nprod[t] == 0 || (nprod[t] == 1 && producer[t] < o); };
+    for (int r = 0; r < k; ++r)
+      for (size_t o = 0; o < g.ops.size(); ++o) {
+        LOp& Lo = all[r][o];
+        const OpDef& d = g.def_of((int)o);
+        const char* kk = kernel_kind(d);
+        if (!kk || Lo.skip || Lo.partial || Lo.fused_opt >= 0 || !Lo.reduce.empty() || Lo.out.dtype != TOFU_BF16)
+          continue;
+        const std::string kind = kk;
+        if (kind == "conv") {
+          const ConvGeom cg = conv_geom(d);
+          if (!(cg.kind == 0 || (cg.kind == 1 && cg.s == 1))) continue;
+          if (!(cg.R == 1 && cg.s == 1) && Lo.out.box.back().len() % 32) continue;  // gather-kernel epilogue chunks
+        } else if (kind != "gemm") {
+          continue;
+        }
+        const int t = g.ops[o].output;
+        const int e = consumer(t);
+        if (e < 0) continue;
+        LOp& Le = all[r][e];
+        const std::string& en = g.def_of(e).name;
+        auto same_direct = [&](const Buf& b) { return b.direct && same(b.box, Lo.out.box) && same(b.buf_box, b.box); };
+        bool ok = Le.fetch.empty() && Le.reduce.empty() && !Le.skip && same_direct(Le.out) && Le.out.dtype == TOFU_BF16;
+        for (auto& b : Le.in) ok &= same_direct(b) && b.dtype == TOFU_BF16;
+        if (!ok) continue;
+        const auto& ins = g.ops[e].inputs;
+        int ep = 0, add_i = -1, mask_i = -1;
+        if ((en == "relu" || en == "relu4") && ins[0] == t) ep = 1;
+        else if ((en == "addrelu" || en == "add4") && ins.size() == 2 && (ins[0] == t) != (ins[1] == t)) {
+          add_i = ins[0] == t ? 1 : 0;
+          ep = 2 | (en == "addrelu" ? 1 : 0);
+        } else if ((en == "relu_grad" || en == "relu_grad4") && ins[1] == t && ins[0] != t) {
+          mask_i = 0;
+          ep = 4;
+        }
+        if (!ep || (add_i >= 0 && !earlier(ins[add_i], (int)o)) || (mask_i >= 0 && !earlier(ins[mask_i], (int)o)))
+          continue;
+        Buf out = Le.out;
+        Buf mask;
+        int e2 = -1;
+        if (en == "add4") {  // gradient sum followed by its single relu_grad: fold the mask too
+          const int t2 = g.ops[e].output, c2 = consumer(t2);
+          if (c2 >= 0) {
+            LOp& L2 = all[r][c2];
+            const std::string& n2 = g.def_of(c2).name;
+            bool ok2 = (n2 == "relu_grad" || n2 == "relu_grad4") && g.ops[c2].inputs[1] == t2 &&
+                       g.ops[c2].inputs[0] != t2 && earlier(g.ops[c2].inputs[0], (int)o) && L2.fetch.empty() &&
+                       L2.reduce.empty() && !L2.skip && same_direct(L2.out) && L2.out.dtype == TOFU_BF16;
+            for (auto& b : L2.in) ok2 &= same_direct(b);
+            if (ok2) {
+              e2 = c2;
+              ep |= 4;
+              mask = L2.in[0];
+              out = L2.out;
+            }
+          }
+        }
+        Lo.ep = ep;
+        if (add_i >= 0) Lo.epi_add = Le.in[add_i];
+        if (mask_i >= 0) Lo.epi_mask = Le.in[mask_i];
+        if (e2 >= 0) {
+          Lo.epi_mask = mask;
+          all[r][e2].skip = true;
+        }
+        Lo.out = out;
+        Le.skip = true;
+      }
+  }
   E.remote_fetch.assign(g.ops.size(), 0);
   E.remote_reduce.assign(g.ops.size(), 0);
   for (int r = 0; r < k; ++r)
@@ -731,6 +824,11 @@ bool conv1x1_gemm(Exec& E, int o, int li, Exec::GemmLaunch& G) {
   G.a.C = base + O.off + offo * ec;
   G.a.ldc = (int)ldo;
   G.a.c_mode = O.dtype == TOFU_BF16 ? 0 : 1;
+  if (L.ep) {
+    G.a.ep = L.ep;
+    if (L.ep & 2) G.a.aux_add = base + L.epi_add.off + offset_in(L.epi_add.buf_box, L.epi_add.box) * 2;
+    if (L.ep & 4) G.a.aux_mask = base + L.epi_mask.off + offset_in(L.epi_mask.buf_box, L.epi_mask.box) * 2;
+  }
   if (L.fused_opt >= 0) {
     const LOp& Lm = E.lops[li][L.fused_opt];
     const LOp& Ls = E.lops[li][L.fused_opt + 1];
@@ -801,6 +899,11 @@ void finalize(Exec& E) {
       G.a.C = E.arena[r] + L.out.off + coff * ec;
       G.a.ldc = (int)ldc;
       G.a.c_mode = L.out.dtype == TOFU_BF16 ? 0 : 1;
+      if (L.ep) {
+        G.a.ep = L.ep;
+        if (L.ep & 2) G.a.aux_add = E.arena[r] + L.epi_add.off + offset_in(L.epi_add.buf_box, L.epi_add.box) * 2;
+        if (L.ep & 4) G.a.aux_mask = E.arena[r] + L.epi_mask.off + offset_in(L.epi_mask.buf_box, L.epi_mask.box) * 2;
+      }
       if (L.fused_opt >= 0) {
         const LOp& Lm = E.lops[li][L.fused_opt];      // mom(M, G) -> M_new (in place)
         const LOp& Ls = E.lops[li][L.fused_opt + 1];  // sgd(W, M_new) -> W_new (in place)
@@ -901,6 +1004,12 @@ std::vector<tofu_conv_args> conv_args(Exec& E, int o, int li) {
   tofu_conv_args a;
   std::memset(&a, 0, sizeof a);
   const int R = cg.R, s = cg.s, p = cg.p;
+  auto set_epilogue = [&](tofu_conv_args& x) {
+    if (!L.ep) return;
+    x.ep = L.ep;
+    if (L.ep & 2) x.aux_add = box_ptr(L.epi_add);
+    if (L.ep & 4) x.aux_mask = box_ptr(L.epi_mask);
+  };
   // gathered source
   const Buf& S = L.in[cg.kind == 2 ? 1 : 0];
   auto st = strides_of(S.buf_box);
@@ -949,6 +1058,7 @@ std::vector<tofu_conv_args> conv_args(Exec& E, int o, int li) {
       a.c_sx = os[2];
       a.c_ys = a.c_xs = 1;
       a.c_mode = O.dtype == TOFU_F32 ? 1 : 0;
+      set_epilogue(a);
       out.push_back(a);
     } else {
       const Buf& D = L.in[0];
@@ -1000,6 +1110,7 @@ std::vector<tofu_conv_args> conv_args(Exec& E, int o, int li) {
         a.tap_w[a.ntaps] = (short)(ky * R + kx);
         ++a.ntaps;
       }
+    set_epilogue(a);
     out.push_back(a);
     return out;
   }
@@ -1398,11 +1509,16 @@ std::string launch_desc(const Exec& E, int i) {
       else if (dn != "sumsq") bytes += n * (lo.out.dtype == TOFU_BF16 ? 2 : 4);
       if (lo.fused_sgd) bytes += n * 2;       // w read
     }
+    bytes += (double)vol(lo.out.box) * 2 * (((lo.ep >> 1) & 1) + ((lo.ep >> 2) & 1));  // epilogue operands
   }
   o += ",\"flops\":" + json_num(flops) + ",\"bytes\":" + json_num(bytes);
   if (L.kind == 1 && lo_fused(E, L)) o += ",\"fused\":\"mom+sgd\"";
   if (L.kind == 1 && E.lops[L.li][L.op].fused_opt >= 0) o += ",\"fused\":\"gemm+mom+sgd\"";
   if (L.kind == 1 && E.lops[L.li][L.op].fused_next) o += ",\"fused\":\"lstm-cell-pair\"";
+  if (L.kind == 1 && E.lops[L.li][L.op].ep) {
+    const int ep = E.lops[L.li][L.op].ep;
+    o += std::string(",\"fused\":\"epilogue") + (ep & 2 ? "+add" : "") + (ep & 1 ? "+relu" : "") + (ep & 4 ? "+mask" : "") + "\"";
+  }
   return o + "}";
 }
 }  // namespace

@@ -26,7 +26,8 @@ class GemmArgs(C.Structure):
                 ("B", C.c_void_p), ("ldb", C.c_int), ("b_mn_major", C.c_int),
                 ("C", C.c_void_p), ("ldc", C.c_int), ("c_mode", C.c_int),
                 ("bn", C.c_int), ("max_ctas", C.c_int), ("D", C.c_void_p), ("ldd", C.c_int),
-                ("s0", C.c_float), ("s1", C.c_float), ("splits", C.c_int), ("ws", C.c_void_p)]
+                ("s0", C.c_float), ("s1", C.c_float), ("splits", C.c_int), ("ws", C.c_void_p),
+                ("aux_add", C.c_void_p), ("aux_mask", C.c_void_p), ("ep", C.c_int)]
 
 
 class Piece(C.Structure):

@@ -69,3 +69,27 @@ def test_wresnet_partitioned_equals_unpartitioned():
         for t in ("Y", "loss", "stem.W_new", "s3u0.W2_new", "fc.W_new"):
             e = nrm(ok[t], o1[t]) if np.ndim(o1[t]) else abs(ok[t] - o1[t]) / abs(o1[t])
             assert e <= 1e-2, (k, t, e)
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_wresnet_epilogue_fusion(k, monkeypatch):
+    """Channel counts that enable the element-wise epilogue fusions (relu / residual add / relu-gradient mask
+    folded into the convolution and GEMM producers): fused run vs the oracle end to end, and vs the unfused
+    GPU run (identical up to the one skipped bf16 rounding of each fused intermediate, R13)."""
+    spec = wresnet([2, 1], 1, 2, 64, base=32, classes=32)
+    vals = make_values(spec, seed=25)
+    monkeypatch.setenv("TOFU_FUSE", "1")
+    R, fused = run_gpu(spec, k, vals)
+    descs = [R.exec.launch_desc(i) for i in range(R.exec.num_launches())]
+    assert sum("epilogue" in d.get("fused", "") for d in descs) >= 10
+    ref = run_graph(OGraph(spec), vals, emulate_storage=True)
+    for t in ("Y", "loss", "stem.W_new", "s0u1.W2_new", "s1u0.W3_new", "fc.W_new", "s0u0.W1.M_new"):
+        r = ref[t]
+        e = nrm(fused[t], r) if np.ndim(r) else abs(fused[t] - r) / abs(r)
+        assert e <= 3e-2, (t, e)
+    monkeypatch.setenv("TOFU_FUSE", "0")
+    _, plain = run_gpu(spec, k, vals)
+    for t in ("Y", "s0u1.W2_new", "s0u0.W1.M_new", "stem.W.M_new"):
+        e = nrm(fused[t], plain[t])
+        assert e <= 2e-2, (t, e)
+    assert R.ledger() == R.plan.cost()
