@@ -22,6 +22,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -592,7 +593,23 @@ static int tmap2(CUtensorMap* tm, const void* ptr, CUtensorMapDataType dt, int e
              : 1;
 }
 
-static int bn_of(const tofu_conv_args* a, int N) { return N <= 128 ? 128 : 256; }
+static int bn_of(const tofu_conv_args* a, int N) {
+  if (N <= 128) return 128;
+  if (a->kind == 0) {  // wave quantisation (see gemm_tcgen05.cu); 128-wide tiles re-gather A twice as often
+    static const double pen = [] {
+      const char* e = getenv("TOFU_CONV_BN128_EFF");
+      return e ? atof(e) : 0.0;  // measured: the gather-bound kernel loses ~30% at 128-wide tiles
+    }();
+    const int64_t tm = ((int64_t)a->nb * a->ngy * a->ngx + BM - 1) / BM;
+    const int64_t t256 = tm * ((N + 255) / 256), t128 = tm * ((N + 127) / 128);
+    if (t256 * 2 > g_sms) {
+      const double e256 = (double)t256 / (((t256 + g_sms - 1) / g_sms) * g_sms);
+      const double e128 = pen * (double)t128 / (((t128 + g_sms - 1) / g_sms) * g_sms);
+      if (e128 > e256 * 1.02) return 128;
+    }
+  }
+  return 256;
+}
 
 static void dims_of(const tofu_conv_args* a, int& M, int& N, int& K) {
   const int pix = a->nb * a->ngy * a->ngx;

@@ -35,10 +35,16 @@ constexpr int BK = 64;
 constexpr int NTHREADS = 192;
 constexpr int SMEM_MAX = 232448;  // 227 KB opt-in per CTA on sm_100
 
+#ifndef TOFU_NBUF3
+#define TOFU_NBUF3 3
+#endif
+constexpr int NBUF3 = TOFU_NBUF3;
+
 template <int BN, int MODE>
 struct GemmCfg {
   static constexpr bool LOADS = MODE == 2 || MODE == 3;
-  static constexpr int NBUF = LOADS ? 3 : 2;
+  // the fused optimizer (MODE 3) streams momentum + weight through the epilogue (HBM-bound): deeper prefetch
+  static constexpr int NBUF = LOADS ? (MODE == 3 ? NBUF3 : 3) : 2;
   static constexpr int C_BYTES = 32 * 32 * (MODE == 0 || MODE == 5 ? 2 : 4);
   static constexpr int D_OFF = 4096;
   static constexpr int BUF_BYTES = MODE == 3 ? 6144 : (C_BYTES < 1024 ? 1024 : C_BYTES);
@@ -505,7 +511,8 @@ extern "C" int tofu_gemm_plan_tmaps(tofu_gemm_args* g, void* tmaps, int* bn_out)
       (reinterpret_cast<uintptr_t>(g->B) & 15) || (reinterpret_cast<uintptr_t>(g->C) & 15) ||
       (reinterpret_cast<uintptr_t>(g->D) & 15))
     return TOFU_ERR_ALIGN;
-  const int bn = (g->bn == 128 || g->bn == 256) ? g->bn : (g->N <= 128 ? 128 : 256);
+  int bn = (g->bn == 128 || g->bn == 256) ? g->bn : (g->N <= 128 ? 128 : 256);
+  // (measured: 128-wide tiles do not recover the last-wave loss of 196-tile shapes, they run ~25% slower)
   g->splits = auto_splits(g, bn);
   CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(tmaps);
   const CUtensorMapDataType BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;

@@ -9,7 +9,7 @@ import json
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libtofu.so")
+LIB_PATH = os.environ.get("TOFU_LIB") or os.path.join(_PKG, "libtofu.so")  # TOFU_LIB: an experimental build
 
 TOFU_BF16, TOFU_F32 = 0, 1
 EW = {"relu": 0, "relu_grad": 1, "mse_grad": 2, "mom": 3, "sgd": 4, "sgd_mom": 5, "sumsq": 6}
@@ -26,6 +26,27 @@ class GemmArgs(C.Structure):
                 ("B", C.c_void_p), ("ldb", C.c_int), ("b_mn_major", C.c_int),
                 ("C", C.c_void_p), ("ldc", C.c_int), ("c_mode", C.c_int),
                 ("bn", C.c_int), ("max_ctas", C.c_int), ("D", C.c_void_p), ("ldd", C.c_int),
+                ("s0", C.c_float), ("s1", C.c_float), ("splits", C.c_int), ("ws", C.c_void_p),
+                ("aux_add", C.c_void_p), ("aux_mask", C.c_void_p), ("ep", C.c_int)]
+
+
+MAX_TAPS = 64
+
+
+class ConvArgs(C.Structure):
+    _fields_ = [("kind", C.c_int), ("nb", C.c_int), ("ngy", C.c_int), ("ngx", C.c_int),
+                ("ay", C.c_int), ("ax", C.c_int), ("cy", C.c_int), ("cx", C.c_int), ("sb0", C.c_int),
+                ("ntaps", C.c_int), ("nch", C.c_int),
+                ("tap_dy", C.c_short * MAX_TAPS), ("tap_dx", C.c_short * MAX_TAPS), ("tap_w", C.c_short * MAX_TAPS),
+                ("S", C.c_void_p), ("s_sb", C.c_int64), ("s_sy", C.c_int64), ("s_sx", C.c_int64),
+                ("sH", C.c_int), ("sW", C.c_int), ("sc0", C.c_int),
+                ("n_out", C.c_int), ("m_out", C.c_int),
+                ("Bp", C.c_void_p), ("ldb", C.c_int64), ("b_mn_major", C.c_int), ("b_tap", C.c_int),
+                ("b_rows", C.c_int), ("b_cols", C.c_int),
+                ("Ap", C.c_void_p), ("lda", C.c_int64),
+                ("C", C.c_void_p), ("c_sb", C.c_int64), ("c_sy", C.c_int64), ("c_sx", C.c_int64),
+                ("c_ys", C.c_int), ("c_y0", C.c_int), ("c_xs", C.c_int), ("c_x0", C.c_int),
+                ("ldc", C.c_int64), ("c_mode", C.c_int), ("D", C.c_void_p), ("ldd", C.c_int64),
                 ("s0", C.c_float), ("s1", C.c_float), ("splits", C.c_int), ("ws", C.c_void_p),
                 ("aux_add", C.c_void_p), ("aux_mask", C.c_void_p), ("ep", C.c_int)]
 
@@ -57,6 +78,7 @@ def lib():
             "tofu_gemm_plan_tmaps": [C.POINTER(GemmArgs), vp, C.POINTER(C.c_int)],
             "tofu_gemm_launch_planned": [C.POINTER(GemmArgs), vp, C.c_int, vp],
             "tofu_pieces_run": [vp, C.c_int, C.c_int64, vp],
+            "tofu_conv_bf16": [C.POINTER(ConvArgs), vp],
             "tofu_elementwise": [C.c_int, C.c_int64, vp, vp, vp, vp, C.c_float, C.c_float, vp],
             "tofu_describe_op": [C.c_char_p, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
             "tofu_graph_create": [C.c_char_p, C.POINTER(vp)],
@@ -102,10 +124,17 @@ def _stream(stream):
 
 # ----------------------------------------------------------------------------- kernels
 def gemm(A, B, Cout, M, N, K, lda, a_mn, ldb, b_mn, ldc, c_mode, bn=0, max_ctas=0, stream=None, D=None, ldd=0,
-         s0=0.0, s1=0.0, splits=0):
+         s0=0.0, s1=0.0, splits=0, aux_add=None, aux_mask=None, ep=0):
     a = GemmArgs(M, N, K, A.data_ptr(), lda, a_mn, B.data_ptr(), ldb, b_mn, Cout.data_ptr(), ldc, c_mode, bn, max_ctas,
-                 D.data_ptr() if D is not None else None, ldd, s0, s1, splits, None)
+                 D.data_ptr() if D is not None else None, ldd, s0, s1, splits, None,
+                 aux_add.data_ptr() if aux_add is not None else None,
+                 aux_mask.data_ptr() if aux_mask is not None else None, ep)
     check(lib().tofu_gemm_bf16(C.byref(a), _stream(stream)), "tofu_gemm_bf16")
+
+
+def conv(args: ConvArgs, stream=None):
+    """tofu_conv_bf16 (include/tofu.h): one implicit-GEMM convolution sub-op."""
+    check(lib().tofu_conv_bf16(C.byref(args), _stream(stream)), "tofu_conv_bf16")
 
 
 def elementwise(kind, n, y=None, x0=None, x1=None, x2=None, s0=0.0, s1=0.0, stream=None):
