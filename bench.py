@@ -128,12 +128,17 @@ def oracle_sample(cfg):
         from tofu_inputs.graphs import lstm
         spec = lstm(1, 4096, 20, 1)   # 1 of 6 layers, 1 sequence: 1/6 of a sequence's work
         return spec, 1.0 / 6.0, "1 LSTM layer (of 6), batch 1 sequence of 20 steps, fp64; samples/s = 1/(6 t)"
-    if cfg == 3:
-        from tofu_inputs.graphs import wresnet
-        spec = wresnet([1], 4, 1, 224)   # stem + first bottleneck unit at full width, 1 image
+    if cfg in (3, 4, 5):
+        from tofu_inputs.graphs import lstm, wresnet
+        # cfg 3/5: stem + first bottleneck unit at full width, 1 image; cfg 4: one LSTM layer, 1 sequence
+        spec = {3: lambda: wresnet([1], 4, 1, 224), 4: lambda: lstm(1, 8192, 2, 1),
+                5: lambda: wresnet([1], 10, 1, 112)}[cfg]()
         frac = graph_work(spec) / (graph_work(full) / batch)
-        return spec, frac, ("WResNet-152-4 stem + first bottleneck unit, 1 image, fp64; extrapolated to the full "
-                            f"network by iteration-space work (this sample = {frac:.4f} of an image)")
+        what = {3: "WResNet-152-4 stem + first bottleneck unit, 1 image",
+                4: "1 LSTM layer (of 10), 1 sequence of 2 steps (of 20)",
+                5: "WResNet-152-10 stem + first bottleneck unit, 1 image at 112x112"}[cfg]
+        return spec, frac, (f"{what}, fp64; extrapolated to the full network by iteration-space work (this sample "
+                            f"= {frac:.4f} of a sample)")
     from tofu_inputs.graphs import mlp
     dims = [full["tensors"]["X"]["shape"][1], full["tensors"]["Y"]["shape"][1]]
     sb = 32 if batch > 32 else batch
@@ -238,12 +243,20 @@ def main():
 
     spec = config(args.config)
     k = world
-    vals = make_values(spec, seed=0)
+    big = args.config >= 4   # parameters drawn on the device (float64 host copies would not fit in RAM)
+    vals = None if big else make_values(spec, seed=0)
     if world > 1:
         R = TofuRunner(spec, k, rank=rank, group=group)
     else:
         R = TofuRunner(spec, 1)
-    R.load(vals)
+    if big:
+        from tofu_inputs.tensors import make_values_device
+        for name, v in make_values_device(spec, seed=0):
+            R.load({name: v})
+            del v
+        vals = {n: v.cpu().numpy() for n, v in make_values_device(spec, seed=0, names=("X", "T"))}
+    else:
+        R.load(vals)
     ex = R.exec
     stream = torch.cuda.current_stream()
 
@@ -410,7 +423,7 @@ def main():
         "cuda_graph": use_graph,
         "clocks": clk.summary(),
     }
-    if world == 1 and args.virtual_k > 1:
+    if world == 1 and args.virtual_k > 1 and not big:
         line["virtual_partitioned"] = virtual_partitioned(spec, vals, args.virtual_k, max(args.steps, 5))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sspec, per_step, sample = oracle_sample(args.config)

@@ -11,6 +11,9 @@ Workloads follow BASELINE.json configs:
   configs[1]  mlp(512, [8192, 8192])            single large FC layer, k = 8
   configs[2]  lstm(6, 4096, 20, 128)             6-layer LSTM, hidden 4K, 20 steps, batch 128
   configs[3]  wresnet_depth(152, 4, 32)          WResNet-152-4, batch 32, 224x224 images
+  configs[4]  lstm(10, 8192, 20, 128) (bench config 4) and wresnet_depth(152, 10, 32) (bench config 5):
+              the "models exceeding a single GPU's HBM" of the north star (both fit one B200's 180 GB at
+              these batch sizes; reading R12 / SURVEY bite 4)
 """
 from __future__ import annotations
 
@@ -108,6 +111,10 @@ def config(i: int) -> dict:
         return lstm(6, 4096, 20, 128)
     if i == 3:
         return wresnet_depth(152, 4, 32)
+    if i == 4:   # configs[4], first model: RNN-10-8K (batch 128 as the paper ran it)
+        return lstm(10, 8192, 20, 128)
+    if i == 5:   # configs[4], second model: WResNet-152-10, batch 32
+        return wresnet_depth(152, 10, 32)
     raise ValueError(f"config {i} not built yet")
 
 
@@ -485,3 +492,8 @@ def wresnet_depth(L: int, width: int, batch: int, image: int = 224) -> dict:
 
 CONFIG_K[3] = 8
 CONFIG_NAME[3] = "wresnet-152-4-b32"
+
+CONFIG_K[4] = 8
+CONFIG_NAME[4] = "lstm-10x8192-T20-b128"
+CONFIG_K[5] = 8
+CONFIG_NAME[5] = "wresnet-152-10-b32"

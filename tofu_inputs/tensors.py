@@ -54,3 +54,36 @@ def make_values(graph: dict, seed: int = 0, mode: str = "float") -> dict:
         else:
             out[name] = _q(rng, shape) * 2.0 ** -17
     return out
+
+
+def make_values_device(graph: dict, seed: int = 0, device="cuda", names=None):
+    """The same recipes drawn with torch's generator on the device (for models whose parameters would not
+    fit in host memory as float64; used by bench.py for the largest configs).  Yields (name, tensor)."""
+    import torch
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    for name in sorted(graph["tensors"]):
+        t = graph["tensors"][name]
+        role = t["role"]
+        shape = tuple(t["shape"])
+        if role not in ("input", "weight", "state") or name in graph.get("alias", {}):
+            continue
+        if names is not None and name not in names:
+            continue
+        if t.get("init") == "zeros":
+            yield name, torch.zeros(shape, device=device)
+            continue
+        if t.get("init") == "ones":
+            yield name, torch.ones(shape, device=device)
+            continue
+        q = torch.randint(-128, 129, shape, generator=gen, device=device).float()
+        if role == "input":
+            q *= 2.0 ** -7 if name != "T" else 2.0 ** -8
+            if t.get("live_channels") is not None:
+                q[..., int(t["live_channels"]):] = 0.0
+        elif role == "weight":
+            fan_in = int(t.get("fan_in") or shape[0])
+            q *= 2.0 ** (-7 - round(math.log2(math.sqrt(fan_in))))
+        else:
+            q *= 2.0 ** -17
+        yield name, q
