@@ -10,6 +10,8 @@
 #include <map>
 #include <numeric>
 #include <set>
+#include <string>
+#include <unordered_map>
 
 #include "common.h"
 #include "graph.h"
@@ -44,6 +46,7 @@ struct VE {
     int x;
     std::vector<int> scope;
     std::vector<int64_t> comb;
+    std::vector<int64_t> st;  // strides of scope
   };
   std::vector<Trace> trace;
 
@@ -57,7 +60,9 @@ struct VE {
     return s;
   }
 
-  int64_t run(int cap, std::vector<std::vector<int>>& sols) {
+  // order: elimination order to follow (computed by the min-degree rule when empty and written back; it
+  // depends only on the factor scopes and domain sizes, so frontier prefixes with equal domains share it)
+  int64_t run(int cap, std::vector<std::vector<int>>& sols, std::vector<int>& order) {
     // min-degree greedy order (ties -> smallest var id), with var -> factor adjacency kept incrementally
     std::vector<Factor> active = factors;
     std::vector<char> alive(active.size(), 1);
@@ -67,18 +72,25 @@ struct VE {
       for (int y : active[f].scope) adj[y].insert((int)f);
     std::set<int> remaining;
     for (int v = 0; v < nv; ++v) remaining.insert(v);
+    const bool given = (int)order.size() == nv;
+    if (!given) order.clear();
     while (!remaining.empty()) {
       int bx = -1;
-      double bw = 0;
-      for (int x : remaining) {
-        std::set<int> nb;
-        for (int f : adj[x]) nb.insert(active[f].scope.begin(), active[f].scope.end());
-        double w = 1;
-        for (int y : nb) w *= dsize[y];
-        if (bx < 0 || w < bw) {
-          bx = x;
-          bw = w;
+      if (given) {
+        bx = order[nv - (int)remaining.size()];
+      } else {
+        double bw = 0;
+        for (int x : remaining) {
+          std::set<int> nb;
+          for (int f : adj[x]) nb.insert(active[f].scope.begin(), active[f].scope.end());
+          double w = 1;
+          for (int y : nb) w *= dsize[y];
+          if (bx < 0 || w < bw) {
+            bx = x;
+            bw = w;
+          }
         }
+        order.push_back(bx);
       }
       int x = bx;
       std::vector<int> tids(adj[x].begin(), adj[x].end());
@@ -125,7 +137,7 @@ struct VE {
           if (a != xpos) off += idx[a] * mst[b++];
         msg[off] = std::min(msg[off], comb[e]);
       }
-      trace.push_back({x, scope, std::move(comb)});
+      trace.push_back({x, scope, std::move(comb), strides(scope, dsize)});
       for (int fi : tids) {
         alive[fi] = 0;
         for (int y : active[fi].scope) adj[y].erase(fi);
@@ -151,7 +163,7 @@ struct VE {
         return;
       }
       auto& tr = trace[i];
-      auto st = strides(tr.scope, dsize);
+      const auto& st = tr.st;
       int64_t base = 0;
       int64_t xs = 0;
       for (size_t a = 0; a < tr.scope.size(); ++a) {
@@ -211,8 +223,15 @@ std::vector<int> canon_key(const Graph& g, const PlanSeq& p) {
   for (auto& ms : g.classes)
     for (int d : p.tdims[ms[0]]) key.push_back(d);
   for (auto& ms : g.op_classes) {
-    auto sv = g.def_of(ms[0]).split_vars();
-    for (int v : p.osplit[ms[0]]) key.push_back((int)(std::find(sv.begin(), sv.end(), v) - sv.begin()));
+    const OpDef& d = g.def_of(ms[0]);
+    for (int v : p.osplit[ms[0]]) {
+      if (!d.opaque) {  // split_vars() is 0..n-1: the index is the var itself
+        key.push_back(v);
+      } else {
+        const auto& sv = d.opaque_free;
+        key.push_back((int)(std::find(sv.begin(), sv.end(), v) - sv.begin()));
+      }
+    }
   }
   return key;
 }
@@ -226,24 +245,30 @@ struct StepResult {
 // Memo of per-op costs: an op's cost depends only on its own split sequence and the dim sequences of its
 // tensors, which repeat across frontier prefixes and across factor-table entries.
 struct CostMemo {
-  std::map<std::vector<int>, int64_t> m;
+  std::unordered_map<std::string, int64_t> m;
+  std::string key;  // reused buffer: op id (4 bytes), then one byte per factor / var / dim (all < 128)
   int64_t get(const Graph& g, int o, const PlanSeq& p) {
-    std::vector<int> key;
-    key.push_back(o);
-    for (int f : p.factors) key.push_back(f);
-    for (int v : p.osplit[o]) key.push_back(v);
+    key.assign(reinterpret_cast<const char*>(&o), sizeof o);
+    for (int f : p.factors) key.push_back((char)f);
+    for (int v : p.osplit[o]) key.push_back((char)v);
     for (int t : g.ops[o].inputs)
-      for (int d : p.tdims[t]) key.push_back(d);
-    for (int d : p.tdims[g.ops[o].output]) key.push_back(d);
+      for (int d : p.tdims[t]) key.push_back((char)d);
+    for (int d : p.tdims[g.ops[o].output]) key.push_back((char)d);
     auto it = m.find(key);
     if (it != m.end()) return it->second;
     int64_t c = op_cost(g, o, p).elements;
-    m.emplace(std::move(key), c);
+    m.emplace(key, c);
     return c;
   }
 };
 
-StepResult step_search(const Graph& g, const PlanSeq& pre, int k, int cap, CostMemo& memo) {
+using OrderCache = std::map<std::vector<int>, std::vector<int>>;  // domain sizes -> elimination order
+// An op class's factor table depends on the prefix only through its members' own split sequences and their
+// tensors' dim sequences (and the step's domains): frontier prefixes share most tables.
+using TableCache = std::unordered_map<std::string, std::vector<int64_t>>;
+
+StepResult step_search(const Graph& g, const PlanSeq& pre, int k, int cap, CostMemo& memo, OrderCache& oc,
+                       TableCache& tc) {
   const int nT = (int)g.classes.size(), nO = (int)g.op_classes.size();
   std::vector<std::vector<int>> dom(nT + nO);
   for (int c = 0; c < nT; ++c) {
@@ -271,6 +296,27 @@ StepResult step_search(const Graph& g, const PlanSeq& pre, int k, int cap, CostM
     f.scope.push_back(nT + oc);
     int64_t n = 1;
     for (int x : f.scope) n *= ve.dsize[x];
+    std::string tkey;
+    tkey.append(reinterpret_cast<const char*>(&oc), sizeof oc);
+    tkey.push_back((char)k);
+    for (int fct : pre.factors) tkey.push_back((char)fct);
+    for (int x : f.scope) {
+      tkey.push_back((char)0x7f);
+      for (int dv : dom[x]) tkey.push_back((char)dv);
+    }
+    for (int o : g.op_classes[oc]) {
+      tkey.push_back((char)0x7e);
+      for (int v : pre.osplit[o]) tkey.push_back((char)v);
+      for (int t : g.ops[o].inputs)
+        for (int d : pre.tdims[t]) tkey.push_back((char)d);
+      for (int d : pre.tdims[g.ops[o].output]) tkey.push_back((char)d);
+    }
+    auto hit = tc.find(tkey);
+    if (hit != tc.end()) {
+      f.table = hit->second;
+      ve.factors.push_back(std::move(f));
+      continue;
+    }
     f.table.assign(n, 0);
     std::vector<int> idx(f.scope.size());
     for (int64_t e = 0; e < n; ++e) {
@@ -291,11 +337,13 @@ StepResult step_search(const Graph& g, const PlanSeq& pre, int k, int cap, CostM
       }
       f.table[e] = val;
     }
+    tc.emplace(std::move(tkey), f.table);
     ve.factors.push_back(std::move(f));
   }
   std::vector<std::vector<int>> sols;
   StepResult res;
-  res.cost = ve.run(cap, sols);
+  std::vector<int>& order = oc[ve.dsize];
+  res.cost = ve.run(cap, sols, order);
   res.truncated = (int)sols.size() >= cap;
   for (auto& s : sols) {
     PlanSeq p = cur;
@@ -328,11 +376,13 @@ PlanResult make_plan(const Graph& g, int k, int frontier_cap, int solution_cap, 
   } else if (search == 0) {
     std::vector<PlanSeq> frontier = {empty};
     CostMemo memo;
+    OrderCache ocache;
+    TableCache tcache;
     for (int ki : factors) {
       int64_t best = INT64_MAX;
       std::vector<PlanSeq> cands;
       for (auto& pre : frontier) {
-        StepResult s = step_search(g, pre, ki, solution_cap, memo);
+        StepResult s = step_search(g, pre, ki, solution_cap, memo, ocache, tcache);
         r.truncated |= s.truncated;
         if (s.cost < best) {
           best = s.cost;
@@ -430,7 +480,8 @@ PlanResult make_plan(const Graph& g, int k, int frontier_cap, int solution_cap, 
       ve.factors.push_back(std::move(f));
     }
     std::vector<std::vector<int>> sols;
-    ve.run(1, sols);
+    std::vector<int> order;
+    ve.run(1, sols, order);
     PlanSeq p = cur;
     for (size_t t = 0; t < g.tensors.size(); ++t) p.tdims[t] = dom[g.tclass[t]][sols[0][g.tclass[t]]];
     for (size_t o = 0; o < g.ops.size(); ++o) p.osplit[o] = dom[nT + g.oclass[o]][sols[0][nT + g.oclass[o]]];
