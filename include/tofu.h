@@ -185,8 +185,8 @@ int64_t tofu_gemm_workspace_bytes(const tofu_gemm_args* args);
  *   C = momentum (in/out) = C*s0 + acc, D bf16 weight (in/out) = D - C*s1, row pitch ldd).  splits: split-K
  *   over pixels (0 = auto, 1 = off) with fp32 workspace ws (tofu_conv_workspace_bytes), reduced in fixed
  *   order (deterministic); the optimizer is applied by the reduction.
- * Requirements: nch % 8 == 0, S channel stride 1 and sc0 % 8 == 0, 16-byte aligned pointers, pitches
- * multiples of 8 elements.  Returns TOFU_ERR_ARG / TOFU_ERR_ALIGN on violations.
+ * Tensor-core requirements: nch % 8 == 0, sc0 % 8 == 0, 16-byte aligned pointers, pitches multiples of 8
+ * elements; shapes that miss them run on the direct path (field `direct`).
  */
 #define TOFU_CONV_MAX_TAPS 64
 typedef struct {
@@ -219,6 +219,10 @@ typedef struct {
   const void* aux_add;
   const void* aux_mask;
   int ep;
+  /* set by tofu_conv_plan: 1 = the geometry misses the tensor-core kernel's 16-byte granules (a channel range
+   * of fewer than 8 channels, unaligned pitches, e.g. an 8-way split of the 8-channel image); the same math
+   * then runs on CUDA cores (fp32 accumulation, same epilogues).  Never chosen for aligned shapes. */
+  int direct;
 } tofu_conv_args;
 /* Encode TMA descriptors once (tmaps: 4 x 128 B, 64-byte aligned; args->splits updated), then launch. */
 int tofu_conv_plan(tofu_conv_args* args, void* tmaps);

@@ -562,6 +562,68 @@ __global__ void __launch_bounds__(256) zero_rows(Params P) {
   }
 }
 
+// Direct path (CUDA cores) for geometries the tensor-core kernel cannot take (channel ranges < 8, unaligned
+// pitches): one thread per output element, fp32 accumulation over K in the same order (taps, channels /
+// pixels), the same epilogues.  Only degenerate partitions use it (e.g. an 8-way split of the stem's 8 image
+// channels), never an aligned shape.
+__device__ __forceinline__ float bf(const __nv_bfloat16* p, int64_t i) { return __bfloat162float(p[i]); }
+
+__global__ void __launch_bounds__(256) conv_direct(Params P) {
+  const tofu_conv_args& a = P.a;
+  const int ngyx = a.ngy * a.ngx;
+  const int64_t total = (int64_t)P.M * P.N;
+  const __nv_bfloat16* S = reinterpret_cast<const __nv_bfloat16*>(a.S);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i / P.N), n = (int)(i % P.N);
+    float acc = 0.f;
+    if (a.kind == 0) {
+      const RowInfo q = pixel_info(a, m, ngyx);
+      const __nv_bfloat16* B = reinterpret_cast<const __nv_bfloat16*>(a.Bp);
+      for (int t = 0; t < a.ntaps; ++t) {
+        const int iy = q.y + a.tap_dy[t], ix = q.x + a.tap_dx[t];
+        if ((unsigned)iy >= (unsigned)a.sH || (unsigned)ix >= (unsigned)a.sW) continue;
+        const int64_t so = q.off + (int64_t)a.tap_dy[t] * a.s_sy + (int64_t)a.tap_dx[t] * a.s_sx + a.sc0;
+        for (int c = 0; c < a.nch; ++c) {
+          const int64_t bo = a.b_mn_major ? (int64_t)c * a.ldb + (int64_t)a.tap_w[t] * a.b_tap + n
+                                          : (int64_t)n * a.ldb + (int64_t)a.tap_w[t] * a.b_tap + c;
+          acc += bf(S, so + c) * bf(B, bo);
+        }
+      }
+      const int gb = m / ngyx, rem = m - gb * ngyx;
+      const int gy = rem / a.ngx, gx = rem - gy * a.ngx;
+      const int64_t e = (int64_t)gb * a.c_sb + (int64_t)(a.c_ys * gy + a.c_y0) * a.c_sy +
+                        (int64_t)(a.c_xs * gx + a.c_x0) * a.c_sx + n;
+      if (a.c_mode == 1) {
+        reinterpret_cast<float*>(a.C)[e] = acc;
+      } else {
+        if (a.ep & 2) acc += bf(reinterpret_cast<const __nv_bfloat16*>(a.aux_add), e);
+        if (a.ep & 1) acc = fmaxf(acc, 0.f);
+        if ((a.ep & 4) && !(bf(reinterpret_cast<const __nv_bfloat16*>(a.aux_mask), e) > 0.f)) acc = 0.f;
+        reinterpret_cast<__nv_bfloat16*>(a.C)[e] = __float2bfloat16_rn(acc);
+      }
+    } else {
+      const int t = n / a.nch, c = n - t * a.nch;
+      const __nv_bfloat16* A = reinterpret_cast<const __nv_bfloat16*>(a.Ap);
+      for (int p = 0; p < P.K; ++p) {
+        const RowInfo q = pixel_info(a, p, ngyx);
+        const int iy = q.y + a.tap_dy[t], ix = q.x + a.tap_dx[t];
+        if ((unsigned)iy >= (unsigned)a.sH || (unsigned)ix >= (unsigned)a.sW) continue;
+        acc += bf(A, (int64_t)p * a.lda + m) *
+               bf(S, q.off + (int64_t)a.tap_dy[t] * a.s_sy + (int64_t)a.tap_dx[t] * a.s_sx + a.sc0 + c);
+      }
+      float* C = reinterpret_cast<float*>(a.C) + (int64_t)m * a.ldc + n;
+      if (a.c_mode == 1) *C = acc;
+      else if (a.c_mode == 2) *C += acc;
+      else {
+        const float mm = *C * a.s0 + acc;
+        *C = mm;
+        __nv_bfloat16* w = reinterpret_cast<__nv_bfloat16*>(a.D) + (int64_t)m * a.ldd + n;
+        *w = __float2bfloat16_rn(__bfloat162float(*w) - mm * a.s1);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static std::once_flag g_once;
@@ -702,11 +764,21 @@ extern "C" int tofu_conv_plan(tofu_conv_args* a, void* tmaps) {
   if (!a || a->kind < 0 || a->kind > 1 || a->ntaps < 0 || a->ntaps > TOFU_CONV_MAX_TAPS || a->nch <= 0 ||
       a->nb < 0 || a->ngy < 0 || a->ngx < 0)
     return TOFU_ERR_ARG;
-  if (a->nch % 8 || a->sc0 % 8 || a->s_sx % 8 || a->s_sy % 8 || a->s_sb % 8) return TOFU_ERR_ALIGN;
   auto mis = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) != 0; };
-  if (mis(a->S) || mis(a->C) || mis(a->Bp) || mis(a->Ap) || mis(a->D)) return TOFU_ERR_ALIGN;
   int M, N, K;
   dims_of(a, M, N, K);
+  a->direct = 0;
+  if (a->nch % 8 || a->sc0 % 8 || a->s_sx % 8 || a->s_sy % 8 || a->s_sb % 8 || mis(a->S) || mis(a->C) ||
+      mis(a->Bp) || mis(a->Ap) || mis(a->D) || mis(a->aux_add) || mis(a->aux_mask) || a->ldb % 8 || a->lda % 8 ||
+      (a->kind == 0 && a->b_mn_major && a->nch < BK && BK % a->nch) ||
+      (a->kind == 0 && !a->b_mn_major && a->nch % BK && a->b_tap != a->nch) ||
+      (a->kind == 0 && a->ep && a->n_out % 32) || (a->kind == 1 && (a->ldc % 4 || (N * 4) % 16 || a->ldd % 8))) {
+    a->direct = 1;  // CUDA-core path; splits off, same epilogues
+    a->splits = 1;
+    if ((a->kind == 0 && a->c_mode != 0 && a->c_mode != 1) || (a->kind == 1 && (a->c_mode < 1 || a->c_mode > 3)))
+      return TOFU_ERR_ARG;
+    return TOFU_OK;
+  }
   CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(tmaps);
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   const auto SW128 = CU_TENSOR_MAP_SWIZZLE_128B;
@@ -769,6 +841,12 @@ extern "C" int tofu_conv_launch_planned(const tofu_conv_args* a, const void* tma
   P.K = K;
   P.splits = a->splits > 1 ? a->splits : 1;
   const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(tmaps);
+  if (a->direct) {
+    int blocks = (int)(((int64_t)M * N + 255) / 256);
+    if (blocks > g_sms * 16) blocks = g_sms * 16;
+    conv_direct<<<blocks, 256, 0, st>>>(P);
+    return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
+  }
   if (K == 0) {
     if (a->kind == 1) {
       if (a->c_mode == 1) return cudaMemset2DAsync(a->C, a->ldc * 4, 0, (size_t)N * 4, M, st) == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;

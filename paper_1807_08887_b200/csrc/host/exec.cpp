@@ -942,11 +942,11 @@ void finalize(Exec& E) {
         if (conv1x1_gemm(E, (int)o, li, G)) {
           G.a.splits = 0;
           G.a.ws = pass == 0 ? reinterpret_cast<void*>(uintptr_t(1) << 20) : E.ws_dev;
-          int rc = tofu_gemm_plan_tmaps(&G.a, G.tm, &G.bn);
-          if (rc) throw Error(rc, "gemm tensor map for 1x1 conv op " + g.ops[o].name);
-          ws_need = std::max<int64_t>(ws_need, tofu_gemm_workspace_bytes(&G.a));
-          if (pass == 1) E.gemms[{(int)o, li}] = G;
-          continue;
+          if (tofu_gemm_plan_tmaps(&G.a, G.tm, &G.bn) == TOFU_OK) {  // else: the convolution kernel below
+            ws_need = std::max<int64_t>(ws_need, tofu_gemm_workspace_bytes(&G.a));
+            if (pass == 1) E.gemms[{(int)o, li}] = G;
+            continue;
+          }
         }
       }
       std::vector<Exec::ConvLaunch> cls;

@@ -48,7 +48,7 @@ class ConvArgs(C.Structure):
                 ("c_ys", C.c_int), ("c_y0", C.c_int), ("c_xs", C.c_int), ("c_x0", C.c_int),
                 ("ldc", C.c_int64), ("c_mode", C.c_int), ("D", C.c_void_p), ("ldd", C.c_int64),
                 ("s0", C.c_float), ("s1", C.c_float), ("splits", C.c_int), ("ws", C.c_void_p),
-                ("aux_add", C.c_void_p), ("aux_mask", C.c_void_p), ("ep", C.c_int)]
+                ("aux_add", C.c_void_p), ("aux_mask", C.c_void_p), ("ep", C.c_int), ("direct", C.c_int)]
 
 
 class Piece(C.Structure):

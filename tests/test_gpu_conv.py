@@ -21,8 +21,9 @@ def small(batch=2, image=64, base=8, units=(1, 1, 1, 1), classes=16):
     return wresnet(list(units), 1, batch, image, base=base, classes=classes)
 
 
-@pytest.mark.parametrize("k", [1, 2, 4])
+@pytest.mark.parametrize("k", [1, 2, 4, 8])
 def test_wresnet_step_per_op_parity(k, monkeypatch):
+    """k = 4, 8 plans split activations spatially (halo regions fetched from the neighbours)."""
     monkeypatch.setenv("TOFU_FUSE", "0")
     spec = small()
     vals = make_values(spec, seed=21)
@@ -71,7 +72,7 @@ def test_wresnet_partitioned_equals_unpartitioned():
             assert e <= 1e-2, (k, t, e)
 
 
-@pytest.mark.parametrize("k", [1, 2])
+@pytest.mark.parametrize("k", [1, 2, 8])
 def test_wresnet_epilogue_fusion(k, monkeypatch):
     """Channel counts that enable the element-wise epilogue fusions (relu / residual add / relu-gradient mask
     folded into the convolution and GEMM producers): fused run vs the oracle end to end, and vs the unfused
