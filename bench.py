@@ -280,8 +280,16 @@ def main():
         torch.cuda.synchronize()
         for i in range(nl):
             per[i] += evs[i].elapsed_time(evs[i + 1]) / reps
+    # dominant kernel: the kernel (def, or fetch / reduce) taking the largest share of the step; its longest
+    # launch is the one timed live below
     cand = [i for i in range(nl) if descs[i]["kind"] in ("compute", "fetch", "reduce")]
-    dom = max(cand, key=lambda i: per[i])
+    kkey = lambda i: descs[i]["def"] if descs[i]["kind"] == "compute" else descs[i]["kind"]
+    share = {}
+    for i in cand:
+        share[kkey(i)] = share.get(kkey(i), 0.0) + per[i]
+    top = max(share, key=share.get)
+    dom = max((i for i in cand if kkey(i) == top), key=lambda i: per[i])
+    dom_share = share[top] / max(sum(per), 1e-9)
 
     # --- warmup + timed region (inputs > L2: W 128 MiB + M 256 MiB + dW 256 MiB per step)
     for _ in range(args.warmup):
@@ -379,6 +387,7 @@ def main():
     roof["kernel"] = f"{d['kind']}:{d['op']}({d['def']})"
     roof["peak_src"] = pk["src"] + (" sustained bf16" if roof["bound"] == "tensor" else " hbm copy")
     roof["kernel_ms"] = dom_ms
+    roof["kernel_step_share"] = dom_share   # share of the step taken by all launches of this kernel
     roof["algorithmic"] = {"flops": d["flops"], "bytes": d["bytes"], "fused": d.get("fused")}
     roof["traffic"] = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
