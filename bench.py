@@ -139,10 +139,8 @@ def oracle_sample(cfg):
                 5: "WResNet-152-10 stem + first bottleneck unit, 1 image at 112x112"}[cfg]
         return spec, frac, (f"{what}, fp64; extrapolated to the full network by iteration-space work (this sample "
                             f"= {frac:.4f} of a sample)")
-    from tofu_inputs.graphs import mlp
-    dims = [full["tensors"]["X"]["shape"][1], full["tensors"]["Y"]["shape"][1]]
-    sb = 32 if batch > 32 else batch
-    return mlp(sb, dims), float(sb), f"{CONFIG_NAME[cfg]} layer shapes at batch {sb} per step (full batch {batch}); fp64"
+    # MLP / FC: the whole training step of the workload itself (a few seconds of fp64 work)
+    return full, float(batch), f"1 full training step of {CONFIG_NAME[cfg]} (batch {batch}), fp64"
 
 
 def reference_arm(args, world, rank):

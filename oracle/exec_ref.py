@@ -50,16 +50,46 @@ def _idx(aff: Affine, grid):
     return aff.value(grid)
 
 
+def _slice_access(acc, arr, origin, grid, rank):
+    """An access whose every index is a distinct plain variable, inside the array, is a slice of it: return
+    that view laid out on the grid's axes (the same values _gather would produce, without index arrays)."""
+    axes = []
+    for ix in acc.index:
+        if ix is None or not ix.is_var():
+            return None
+        axes.append(ix.coef[0][0])
+    if len(set(axes)) != len(axes):
+        return None
+    order = list(grid)
+    sl = []
+    for d, v in enumerate(axes):
+        g = grid[v]
+        lo, hi = int(g.flat[0]) - origin[d], int(g.flat[-1]) - origin[d]
+        if lo < 0 or hi >= arr.shape[d]:
+            return None
+        sl.append(slice(lo, hi + 1))
+    sub = arr[tuple(sl)]
+    pos = [order.index(v) for v in axes]
+    sub = np.transpose(sub, np.argsort(pos))          # dims in grid-axis order
+    shp = [1] * rank
+    for p_, n in zip(sorted(pos), sub.shape):
+        shp[p_] = n
+    return sub.reshape(shp)
+
+
 def _gather(arr, origin, index_arrays, shape):
     """arr[index] with zero for indices outside the array (reading R11: an access outside its tensor
     reads 0, i.e. zero padding).  Inside the tensor every access lies in the array by construction
     (the array is the tensor or a region covering the required hull)."""
     if any(n == 0 for n in arr.shape):
         return np.zeros(shape)
+    local = [np.asarray(i - origin[d]) for d, i in enumerate(index_arrays)]
+    if all(i.min() >= 0 and i.max() < arr.shape[d] for d, i in enumerate(local)):   # nothing outside
+        return arr[tuple(np.broadcast_to(i, shape) for i in local)]
     ok = True
     idx = []
-    for d, i in enumerate(index_arrays):
-        i = np.broadcast_to(i - origin[d], shape)
+    for d, i in enumerate(local):
+        i = np.broadcast_to(i, shape)
         inb = (i >= 0) & (i < arr.shape[d])
         ok = ok & inb
         idx.append(np.where(inb, i, 0))
@@ -74,6 +104,9 @@ def _ev(e, grid, inputs, shape):
         return grid[e.val].astype(np.float64)
     if k == "access":
         arr, origin = inputs[e.val.tensor]
+        view = _slice_access(e.val, arr, origin, grid, len(shape))
+        if view is not None:
+            return view
         return _gather(arr, origin, [_idx(ix, grid) for ix in e.val.index], shape)
     if k == "neg":
         return -_ev(e.args[0], grid, inputs, shape)
