@@ -265,6 +265,11 @@ int tofu_maxpool_grad(const tofu_window_args* a, void* stream);
 int tofu_gap(const tofu_window_args* a, void* stream);
 int tofu_gap_grad(const tofu_window_args* a, void* stream);
 
+/* Weight re-layout for the convolution data gradient: WT[i][t][o] = W[o][t][i] (bf16, dense, co x taps x ci
+ * -> ci x taps x co), so the data gradient reads its weight operand K-major (executor-owned copy, refreshed
+ * before each data-gradient launch; DESIGN a10). */
+int tofu_transpose_taps(const void* W, void* WT, int co, int taps, int ci, void* stream);
+
 /* a5/a6 — box copy / reduction pieces (rank <= 4, innermost dim last, strides in elements).
  * A piece copies (nsrc == 1) or sums in order (nsrc > 1, fp32 arithmetic) nsrc source boxes of the same
  * extent into one destination box, converting dtype.  Sources may be peer pointers. */

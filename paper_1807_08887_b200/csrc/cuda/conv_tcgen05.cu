@@ -759,6 +759,12 @@ extern "C" int64_t tofu_conv_workspace_bytes(const tofu_conv_args* a) {
 }
 
 // tmaps: 4 x CUtensorMap (dense operand, C, D, split-K workspace)
+static bool natural_taps(const tofu_conv_args* a) {
+  for (int t = 0; t < a->ntaps; ++t)
+    if (a->tap_w[t] != t) return false;
+  return true;
+}
+
 extern "C" int tofu_conv_plan(tofu_conv_args* a, void* tmaps) {
   if (init() != 0) return TOFU_ERR_CUDA;
   if (!a || a->kind < 0 || a->kind > 1 || a->ntaps < 0 || a->ntaps > TOFU_CONV_MAX_TAPS || a->nch <= 0 ||
@@ -771,7 +777,7 @@ extern "C" int tofu_conv_plan(tofu_conv_args* a, void* tmaps) {
   if (a->nch % 8 || a->sc0 % 8 || a->s_sx % 8 || a->s_sy % 8 || a->s_sb % 8 || mis(a->S) || mis(a->C) ||
       mis(a->Bp) || mis(a->Ap) || mis(a->D) || mis(a->aux_add) || mis(a->aux_mask) || a->ldb % 8 || a->lda % 8 ||
       (a->kind == 0 && a->b_mn_major && a->nch < BK && BK % a->nch) ||
-      (a->kind == 0 && !a->b_mn_major && a->nch % BK && a->b_tap != a->nch) ||
+      (a->kind == 0 && !a->b_mn_major && a->nch % BK && (a->b_tap != a->nch || !natural_taps(a))) ||
       (a->kind == 0 && a->ep && a->n_out % 32) || (a->kind == 1 && (a->ldc % 4 || (N * 4) % 16 || a->ldd % 8))) {
     a->direct = 1;  // CUDA-core path; splits off, same epilogues
     a->splits = 1;

@@ -154,6 +154,24 @@ __global__ void __launch_bounds__(256) gap_grad_kernel(tofu_window_args a) {
   }
 }
 
+// WT[i][t][o] = W[o][t][i]: 32x32 tiles through shared memory (coalesced reads and writes)
+__global__ void __launch_bounds__(256) transpose_taps_kernel(const __nv_bfloat16* __restrict__ W,
+                                                             __nv_bfloat16* __restrict__ WT, int co, int taps, int ci) {
+  __shared__ __nv_bfloat16 tile[32][34];
+  const int t = blockIdx.z;
+  const int o0 = blockIdx.y * 32, i0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    const int o = o0 + r, i = i0 + tx;
+    if (o < co && i < ci) tile[r][tx] = W[((int64_t)o * taps + t) * ci + i];
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int i = i0 + r, o = o0 + tx;
+    if (o < co && i < ci) WT[((int64_t)i * taps + t) * co + o] = tile[tx][r];
+  }
+}
+
 static int grid_for(int64_t work) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -200,5 +218,14 @@ extern "C" int tofu_gap_grad(const tofu_window_args* a, void* stream) {
   const int64_t n = (int64_t)a->nb * a->H * a->W * (a->C / 8);
   if (n == 0) return TOFU_OK;
   gap_grad_kernel<<<grid_for(n), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(*a);
+  return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
+}
+
+extern "C" int tofu_transpose_taps(const void* W, void* WT, int co, int taps, int ci, void* stream) {
+  if (!W || !WT || co < 0 || taps < 0 || ci < 0) return TOFU_ERR_ARG;
+  if (co == 0 || taps == 0 || ci == 0) return TOFU_OK;
+  dim3 grid((ci + 31) / 32, (co + 31) / 32, taps);
+  tofu::win::transpose_taps_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(W), reinterpret_cast<__nv_bfloat16*>(WT), co, taps, ci);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }

@@ -95,6 +95,7 @@ struct LOp {
   bool skip = false;          // fused into the previous op
   bool fused_sgd = false;
   int fused_opt = -1;         // GEMM epilogue absorbs mom (this index) + sgd (index + 1)
+  int64_t wt_off = -1;        // conv data gradient: arena offset of the transposed weight shard (K-major B)
   bool fused_next = false;    // LSTM cell: this launch also computes the next op (c+h, bwd_a+bwd_c)
   int ep = 0;                 // element-wise epilogue of the output's consumers: 1 relu, 2 add, 4 mask
   Buf epi_add, epi_mask;      // its bf16 operands (the output's layout)
@@ -719,6 +720,31 @@ void lower(Exec& E) {
         Le.skip = true;
       }
   }
+  // Conv data gradients read their weights K-major from an executor-owned transposed copy of the weight
+  // shard (W[co][ky][kx][ci] -> WT[ci][ky][kx][co], refreshed right before the launch): the MN-major weight
+  // operand runs ~30% slower on the tensor cores (profiles/r01b_summary.md).  Appended after the staging
+  // region (persistent, one per op).  TOFU_WT=0 disables.
+  {
+    const char* ev = std::getenv("TOFU_WT");
+    const bool use_wt = !(ev && ev[0] == '0');
+    for (int r = 0; r < k && use_wt; ++r)
+      for (size_t o = 0; o < g.ops.size(); ++o) {
+        const OpDef& d = g.def_of((int)o);
+        const char* kk = kernel_kind(d);
+        if (!kk || std::string(kk) != "conv") continue;
+        const ConvGeom cg = conv_geom(d);
+        LOp& L = all[r][o];
+        if (cg.kind != 1 || L.skip || (cg.R == 1 && cg.s == 1)) continue;  // 1x1 stride-1: the GEMM path
+        const Buf& W = L.in[1];
+        if (!W.direct || W.buf_box.size() != 4 || W.box[1].lo != W.buf_box[1].lo || W.box[1].hi != W.buf_box[1].hi ||
+            W.box[2].lo != W.buf_box[2].lo || W.box[2].hi != W.buf_box[2].hi)
+          continue;
+        const int64_t nch = W.box[0].len(), co_sh = W.buf_box[0].len();
+        if (nch % 64 || co_sh % 8 || W.buf_box[3].len() % 8) continue;  // whole 64-channel K blocks per tap
+        L.wt_off = E.lay[r].total;
+        E.lay[r].total = align_up(E.lay[r].total + vol(W.buf_box) * 2);
+      }
+  }
   E.remote_fetch.assign(g.ops.size(), 0);
   E.remote_reduce.assign(g.ops.size(), 0);
   for (int r = 0; r < k; ++r)
@@ -1084,12 +1110,23 @@ std::vector<tofu_conv_args> conv_args(Exec& E, int o, int li) {
   a.nch = (int)ib[6].len();
   a.sc0 = (int)(ib[6].lo - S.buf_box[3].lo);
   a.n_out = (int)ib[3].len();
-  a.Bp = box_ptr(W);
-  a.ldb = strides_of(W.buf_box)[0];
-  a.b_tap = (int)W.buf_box[3].len();
-  a.b_rows = (int)W.box[0].len();
-  a.b_cols = (int)(a.ldb - (W.box[3].lo - W.buf_box[3].lo));
-  a.b_mn_major = 1;
+  if (L.wt_off >= 0) {  // K-major from the transposed shard WT[ci][ky][kx][co]
+    const int64_t co_sh = W.buf_box[0].len(), ci_sh = W.buf_box[3].len(), taps_sh = W.buf_box[1].len() * W.buf_box[2].len();
+    a.ldb = taps_sh * co_sh;
+    a.Bp = base + L.wt_off + ((W.box[3].lo - W.buf_box[3].lo) * a.ldb + (W.box[0].lo - W.buf_box[0].lo)) * 2;
+    a.b_tap = (int)co_sh;
+    a.b_rows = (int)W.box[3].len();
+    a.b_cols = (int)(a.ldb - (W.box[0].lo - W.buf_box[0].lo));
+    a.b_mn_major = 0;
+    (void)ci_sh;
+  } else {
+    a.Bp = box_ptr(W);
+    a.ldb = strides_of(W.buf_box)[0];
+    a.b_tap = (int)W.buf_box[3].len();
+    a.b_rows = (int)W.box[0].len();
+    a.b_cols = (int)(a.ldb - (W.box[3].lo - W.buf_box[3].lo));
+    a.b_mn_major = 1;
+  }
   a.C = box_ptr(O);
   a.c_sb = os[0];
   a.c_sy = os[1];
@@ -1247,6 +1284,12 @@ int run_compute(Exec& E, int o, int li, cudaStream_t st) {
   if (kind == "conv") {
     auto git = E.gemms.find({o, li});
     if (git != E.gemms.end()) return tofu_gemm_launch_planned(&git->second.a, git->second.tm, git->second.bn, st);
+    if (L.wt_off >= 0) {  // refresh the transposed weight shard (the weights may have been updated since)
+      const Buf& W = L.in[1];
+      const int rc = tofu_transpose_taps(base + W.off, base + L.wt_off, (int)W.buf_box[0].len(),
+                                         (int)(W.buf_box[1].len() * W.buf_box[2].len()), (int)W.buf_box[3].len(), st);
+      if (rc) return rc;
+    }
     for (auto& C : E.convs.at({o, li})) {
       const int rc = tofu_conv_launch_planned(&C.a, C.tm, st);
       if (rc) return rc;
@@ -1515,6 +1558,7 @@ std::string launch_desc(const Exec& E, int i) {
   if (L.kind == 1 && lo_fused(E, L)) o += ",\"fused\":\"mom+sgd\"";
   if (L.kind == 1 && E.lops[L.li][L.op].fused_opt >= 0) o += ",\"fused\":\"gemm+mom+sgd\"";
   if (L.kind == 1 && E.lops[L.li][L.op].fused_next) o += ",\"fused\":\"lstm-cell-pair\"";
+  if (L.kind == 1 && E.lops[L.li][L.op].wt_off >= 0) o += ",\"weights\":\"transposed\"";
   if (L.kind == 1 && E.lops[L.li][L.op].ep) {
     const int ep = E.lops[L.li][L.op].ep;
     o += std::string(",\"fused\":\"epilogue") + (ep & 2 ? "+add" : "") + (ep & 1 ? "+relu" : "") + (ep & 4 ? "+mask" : "") + "\"";

@@ -67,9 +67,16 @@ def timeit(a, n=20):
 
 
 flops = 2 * B * H * H * C * C * 9
+mask = (torch.randn(B, H, H, C, device=dev)).bfloat16()
+dm = args(0, X, Y, WT, 0, flip=True)
+dm.ep, dm.aux_mask = 4, mask.data_ptr()
+fr = args(0, X, Y, W, 0)
+fr.ep = 1
 for name, a in [("fwd  (B K-major)", args(0, X, Y, W, 0)),
+                ("fwd + relu epilogue", fr),
                 ("dgrad(B MN-major)", args(0, X, Y, W, 1, flip=True)),
                 ("dgrad(B K-major, W^T)", args(0, X, Y, WT, 0, flip=True)),
+                ("dgrad(W^T) + mask epilogue", dm),
                 ("wgrad", args(1, X, dW))]:
     ms = timeit(a)
     print(f"{name:24s} {ms * 1e3:8.1f} us  {flops / ms / 1e9:7.1f} TF/s")
