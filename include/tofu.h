@@ -145,7 +145,8 @@ typedef struct {
   void* D;
   int ldd;
   float s0, s1;
-  int splits;  /* split-K: 0 = auto (when the output tiles cannot fill the SMs), 1 = off, n = n splits;
+  int splits;  /* split-K: 0 = auto (when the output tiles cannot fill the SMs), 1 = off, n = n splits,
+                  -1 = stream-K (needs sk_ws; not chosen automatically for the GEMM, see gemm_tcgen05.cu);
                   tofu_gemm_plan_tmaps writes the chosen value back */
   void* ws;    /* split-K fp32 workspace (tofu_gemm_workspace_bytes); NULL = library-owned */
   /* element-wise epilogue of a bf16 output (c_mode 0; the consumers' ops fused into their producer, DESIGN
@@ -154,6 +155,12 @@ typedef struct {
   const void* aux_add;
   const void* aux_mask;
   int ep;
+  /* stream-K workspace (tofu_sk_workspace_bytes, zero-filled once by its owner, left zeroed by every launch;
+   * one launch at a time may use it): NULL = data-parallel tiles only.  With it (and splits = -1 for the
+   * GEMM; automatic for compute-bound convolutions), shapes whose tile count leaves SMs idle in the last
+   * wave split the k-loop of some tiles across CTAs and sum the fp32 partials in fixed CTA order before the
+   * epilogue (common.cuh WorkList). */
+  void* sk_ws;
 } tofu_gemm_args;
 int tofu_gemm_bf16(const tofu_gemm_args* args, void* stream);
 /* Split form used by the executor: encode the TMA descriptors (A, B, C, D, workspace, mask) once into `tmaps`
@@ -162,6 +169,8 @@ int tofu_gemm_bf16(const tofu_gemm_args* args, void* stream);
 int tofu_gemm_plan_tmaps(tofu_gemm_args* args, void* tmaps, int* bn_out);
 int tofu_gemm_launch_planned(const tofu_gemm_args* args, const void* tmaps, int bn, void* stream);
 int64_t tofu_gemm_workspace_bytes(const tofu_gemm_args* args);
+/* Bytes of a stream-K workspace for the current device (one fp32 128x256 partial + 8 flags per SM). */
+int64_t tofu_sk_workspace_bytes(void);
 
 /* a4' — implicit-GEMM convolution sub-op (NHWC bf16 activations, weights [co][ky][kx][ci], fp32
  * accumulation in TMEM via tcgen05).  The convolution TDL defs (tofu_inputs.graphs.conv_defs; reading R11)
@@ -219,6 +228,7 @@ typedef struct {
   const void* aux_add;
   const void* aux_mask;
   int ep;
+  void* sk_ws;  /* stream-K workspace, as tofu_gemm_args.sk_ws */
   /* set by tofu_conv_plan: 1 = the geometry misses the tensor-core kernel's 16-byte granules (a channel range
    * of fewer than 8 channels, unaligned pitches, e.g. an 8-way split of the 8-channel image); the same math
    * then runs on CUDA cores (fp32 accumulation, same epilogues).  Never chosen for aligned shapes. */

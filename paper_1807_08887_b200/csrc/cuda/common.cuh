@@ -162,4 +162,113 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N, int a_mn_ma
          | ((uint32_t)(M >> 4) << 24);   // M >> 4
 }
 
+// ---------------------------------------------------------------- persistent work list (data-parallel + stream-K)
+// The tcgen05 kernels (gemm_tcgen05.cu, conv_tcgen05.cu) run one CTA per SM over a list of segments, each an
+// output tile and a k-block range.  The first dp_units = (ntiles - sk_tiles) * splits units are data-parallel:
+// unit u goes to CTA u % grid (tile u / splits, split plane u % splits).  The remaining sk_tiles tiles are
+// stream-K: their sk_tiles * nk k-block iterations, tile-major, are divided evenly over the grid, CTA b taking
+// [bound(b), bound(b+1)).  A tile cut between CTAs is finished by the CTA holding its k-block 0, which
+// processes that piece LAST in its list; the CTAs holding the rest of the tile process it FIRST, write their
+// fp32 partial to their slot of the stream-K workspace and raise a flag.  The finisher adds the partials in
+// CTA order (deterministic for a given shape) before its epilogue, then lowers the flags again (the workspace
+// flags are zero between launches).  This removes the wave-quantisation tail of shapes whose tile count is
+// not a multiple of the SM count (e.g. the 196 tiles of a WResNet stage-2 3x3 convolution on 148 SMs).
+// The host guarantees sk_tiles * nk >= grid (every CTA has a non-empty range) and co-residency (grid <= #SMs,
+// one CTA per SM).
+struct WorkList {
+  int nk, splits, grid, cta, sk_tile0, n_dp, n_sk, t0;
+  int64_t sk_iters, lo, hi;
+  __device__ __forceinline__ void init(int ntiles, int nk_, int splits_, int sk_tiles) {
+    nk = nk_;
+    splits = splits_;
+    grid = gridDim.x;
+    cta = blockIdx.x;
+    sk_tile0 = ntiles - sk_tiles;
+    const int dp_units = sk_tile0 * splits;
+    n_dp = cta < dp_units ? (dp_units - cta + grid - 1) / grid : 0;
+    sk_iters = (int64_t)sk_tiles * nk;
+    lo = bound(cta);
+    hi = bound(cta + 1);
+    t0 = (int)(lo / (nk > 0 ? nk : 1));
+    n_sk = hi > lo ? (int)((hi - 1) / nk) - t0 + 1 : 0;
+  }
+  __device__ __forceinline__ int64_t bound(int c) const { return sk_iters * c / grid; }
+  __device__ __forceinline__ int count() const { return n_dp + n_sk; }
+  // segment i: tile, k-blocks [kb0, kb1), split plane; partial = a leading piece of a cut tile (writes its
+  // fp32 partial to the workspace instead of the epilogue's store)
+  __device__ __forceinline__ void seg(int i, int& tile, int& kb0, int& kb1, int& split, bool& partial) const {
+    if (i < n_dp) {
+      const int u = cta + i * grid;
+      partial = false;
+      if (splits == 1) {  // the common case: no divisions
+        tile = u;
+        split = kb0 = 0;
+        kb1 = nk;
+        return;
+      }
+      tile = u / splits;
+      split = u - tile * splits;
+      kb0 = (int)((int64_t)split * nk / splits);
+      kb1 = (int)((int64_t)(split + 1) * nk / splits);
+      partial = false;
+      return;
+    }
+    const int ts = t0 + (i - n_dp);
+    const int64_t ts0 = (int64_t)ts * nk;
+    tile = sk_tile0 + ts;
+    split = 0;
+    kb0 = (int)((lo > ts0 ? lo : ts0) - ts0);
+    kb1 = (int)((hi < ts0 + nk ? hi : ts0 + nk) - ts0);
+    partial = kb0 > 0;
+  }
+  // finisher of stream-K tile `tile` (the segment holding k-block 0): contributors are CTAs cta+1 .. last-1
+  __device__ __forceinline__ int contrib_end(int tile) const {
+    if (tile < sk_tile0) return cta + 1;
+    const int64_t te = (int64_t)(tile - sk_tile0 + 1) * nk;
+    int c = cta + 1;
+    while (c < grid && bound(c) < te) ++c;
+    return c;
+  }
+};
+
+// stream-K workspace: [grid slots][BM x 256 fp32 partial] then int flags [grid][SK_FLAGS] (one per epilogue warp)
+constexpr int SK_SLOT_FLOATS = 128 * 256;
+constexpr int SK_FLAGS = 8;
+__device__ __forceinline__ float4* sk_slot(void* ws, int c) {
+  return reinterpret_cast<float4*>(ws) + (int64_t)c * (SK_SLOT_FLOATS / 4);
+}
+__device__ __forceinline__ int* sk_flag(void* ws, int grid, int c, int q) {
+  return reinterpret_cast<int*>(reinterpret_cast<float*>(ws) + (int64_t)grid * SK_SLOT_FLOATS) + c * SK_FLAGS + q;
+}
+// epilogue warp q, chunk ch (32 columns) of a partial: coalesced float4 layout [q][ch][8][32 lanes]
+__device__ __forceinline__ void sk_write_chunk(float4* slot, int q, int nch, int ch, int lane, const uint32_t (&r)[32]) {
+  float4* p = slot + ((int64_t)(q * nch + ch) * 8) * 32 + lane;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    __stcg(p + j * 32, make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                   __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
+}
+__device__ __forceinline__ void sk_add_chunk(const float4* slot, int q, int nch, int ch, int lane, uint32_t (&r)[32]) {
+  const float4* p = slot + ((int64_t)(q * nch + ch) * 8) * 32 + lane;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float4 v = __ldcg(p + j * 32);
+    r[4 * j] = __float_as_uint(__uint_as_float(r[4 * j]) + v.x);
+    r[4 * j + 1] = __float_as_uint(__uint_as_float(r[4 * j + 1]) + v.y);
+    r[4 * j + 2] = __float_as_uint(__uint_as_float(r[4 * j + 2]) + v.z);
+    r[4 * j + 3] = __float_as_uint(__uint_as_float(r[4 * j + 3]) + v.w);
+  }
+}
+__device__ __forceinline__ void sk_signal(int* flag) {  // after this warp's partial stores (all lanes fenced)
+  __threadfence();
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(1) : "memory");
+}
+__device__ __forceinline__ void sk_wait(int* flag) {
+  int v = 0;
+  do {
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+  } while (v == 0);
+}
+
 }  // namespace tofu

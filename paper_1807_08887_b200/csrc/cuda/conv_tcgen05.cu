@@ -40,6 +40,7 @@ constexpr int NGATHER = 128;  // warps 6..9
 struct Params {
   tofu_conv_args a;
   int M, N, K, splits;
+  int sk_tiles;  // stream-K tiles (common.cuh WorkList); 0 = data-parallel only
 };
 
 struct RowInfo {
@@ -119,8 +120,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int tiles_m = (M + BM - 1) / BM;
   const int tiles_n = (N + BN - 1) / BN;
   const int nk = (K + BK - 1) / BK;
-  const int nunits = tiles_m * tiles_n * splits;
-  auto kb_lo = [&](int sp) { return (int)((int64_t)sp * nk / splits); };
+  WorkList wl;
+  wl.init(tiles_m * tiles_n, nk, splits, P.sk_tiles);
+  const int nseg = wl.count();
+  void* const sk_ws = a.sk_ws;
   const int ngyx = a.ngy * a.ngx;
 
   if (warp == 0 && lane == 0) {
@@ -148,11 +151,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // ------------------------------------------------------------ TMA producer (dense operand)
     if (lane == 0) {
       int it = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const int tile = u / splits, sp = u % splits;
+      for (int i = 0; i < nseg; ++i) {
+        int tile, kb0, kb1, sp;
+        bool part;
+        wl.seg(i, tile, kb0, kb1, sp, part);
         const int m0 = (tile / tiles_n) * BM;
         const int n0 = (tile % tiles_n) * BN;
-        for (int kb = kb_lo(sp); kb < kb_lo(sp + 1); ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           const int k0 = kb * BK;
@@ -190,15 +195,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       constexpr bool A_MN = KIND == 1;
       constexpr bool BMN = KIND == 1 ? true : B_MN;
       constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN ? 1 : 0, BMN ? 1 : 0);
-      int it = 0, local = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++local) {
-        const int sp = u % splits;
-        const int kb0 = kb_lo(sp);
+      int it = 0;
+      for (int local = 0; local < nseg; ++local) {
+        int tile, kb0, kb1, sp;
+        bool part;
+        wl.seg(local, tile, kb0, kb1, sp, part);
         const int buf = local & 1;
         mbar_wait(&acc_empty[buf], ((local >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + buf * BN;
-        for (int kb = kb0; kb < kb_lo(sp + 1); ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&full[s], (it / STAGES) & 1);
           fence_proxy_async_smem();  // the gathered operand was written by cp.async (generic proxy)
@@ -224,10 +230,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // offsets (the 128B swizzle phase of its rows is constant); per copy: one row-info load, two bounds
     // tests, one 64-bit add.
     const int gt = threadIdx.x - 192;
-    int it = 0, local = 0;
+    int it = 0;
     const __nv_bfloat16* S0 = reinterpret_cast<const __nv_bfloat16*>(a.S);
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++local) {
-      const int tile = u / splits, sp = u % splits;
+    for (int i = 0; i < nseg; ++i) {
+      int tile, kb0, kb1, sp;
+      bool part;
+      wl.seg(i, tile, kb0, kb1, sp, part);
       const int m0 = (tile / tiles_n) * BM;
       const int n0 = (tile % tiles_n) * BN;
       if constexpr (KIND == 0) {
@@ -240,7 +248,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const int m = m0 + r0 + 16 * i;
           q[i] = m < M ? pixel_info(a, m, ngyx) : no_pixel();
         }
-        for (int kb = kb_lo(sp); kb < kb_lo(sp + 1); ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           const int k = kb * BK + j * 8;
@@ -268,7 +276,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const __nv_bfloat16* S = S0 + a.sc0 + c + ((long long)dy * a.s_sy + (long long)dx * a.s_sx);
         const int sub = jj >> 3, j = jj & 7;
         const int slot = sub * 8192 + r0 * 128;
-        for (int kb = kb_lo(sp); kb < kb_lo(sp + 1); ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           RowInfo* ri = rows + (it & 1) * BK;
@@ -299,9 +307,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int q = warp & 3;
     constexpr int NCH = BN / 32;
     if constexpr (KIND == 0) {
-      int local = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++local) {
-        const int tile = u / splits;
+      for (int local = 0; local < nseg; ++local) {
+        int tile, kb0, kb1, sp;
+        bool part;
+        wl.seg(local, tile, kb0, kb1, sp, part);
+        const int cend = part ? blockIdx.x + 1 : wl.contrib_end(tile);
+        for (int cc = blockIdx.x + 1; cc < cend; ++cc) sk_wait(sk_flag(sk_ws, gridDim.x, cc, q));
         const int m0 = (tile / tiles_n) * BM;
         const int n0 = (tile % tiles_n) * BN;
         const int acc = local & 1;
@@ -320,7 +331,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         uint4 xa[4], xm[4];
         auto load_aux = [&](int c, uint4 (&A)[4], uint4 (&Mk)[4]) {
           const int n = n0 + c * 32;
-          const bool ok = MODE == 0 && a.ep && rowp && n + 32 <= N;
+          const bool ok = MODE == 0 && a.ep && !part && rowp && n + 32 <= N;
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
             A[v] = ok && (a.ep & 2)
@@ -343,6 +354,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[acc]);
           }
+          if (part) {  // stream-K leading piece: fp32 partial to this CTA's workspace slot
+            sk_write_chunk(sk_slot(sk_ws, blockIdx.x), q, NCH, c, lane, r);
+            if (c == NCH - 1) sk_signal(sk_flag(sk_ws, gridDim.x, blockIdx.x, q));
+            continue;
+          }
+          for (int cc = blockIdx.x + 1; cc < cend; ++cc) sk_add_chunk(sk_slot(sk_ws, cc), q, NCH, c, lane, r);
+          if (c == NCH - 1 && lane == 0)
+            for (int cc = blockIdx.x + 1; cc < cend; ++cc) *sk_flag(sk_ws, gridDim.x, cc, q) = 0;
           const int n = n0 + c * 32;
           if (!rowp || n >= N) continue;
           if (MODE == 0 && a.ep && n + 32 <= N) {
@@ -423,15 +442,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     } else {
       // TMA-store epilogue (fp32 chunks of 32 x 32 through swizzled smem), as gemm_tcgen05.cu
-      const int my_units = blockIdx.x < nunits ? (nunits - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-      const int S = my_units * NCH;
+      const int S = nseg * NCH;
       uint8_t* wbuf = sE + q * NBUF * C_::BUF_BYTES;
       uint64_t* wbar = ebar + q * NBUF;
       int split_of_chunk = 0;
+      bool part_of_chunk = false;
       auto chunk_coords = [&](int s, int& col, int& row) {
-        const int u = blockIdx.x + (s / NCH) * gridDim.x;
-        const int tile = u / splits;
-        split_of_chunk = u % splits;
+        int tile, kb0, kb1;
+        wl.seg(s / NCH, tile, kb0, kb1, split_of_chunk, part_of_chunk);
         col = (tile % tiles_n) * BN + (s % NCH) * 32;
         row = (tile / tiles_n) * BM + q * 32;
       };
@@ -439,6 +457,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         int col, row;
         chunk_coords(s, col, row);
         uint8_t* b = wbuf + (s % NBUF) * C_::BUF_BYTES;
+        if (part_of_chunk) {  // a stream-K partial: no epilogue operands needed
+          mbar_arrive_expect_tx(&wbar[s % NBUF], 0);
+          return;
+        }
         mbar_arrive_expect_tx(&wbar[s % NBUF], MODE == 3 ? 6144 : 4096);
         tma_load_2d(b, &tmC, &wbar[s % NBUF], col, row);
         if (MODE == 3) tma_load_2d(b + C_::D_OFF, &tmD, &wbar[s % NBUF], col, row);
@@ -446,10 +468,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (C_::LOADS && lane == 0)
         for (int s = 0; s < NBUF - 1 && s < S; ++s) issue_load(s);
       int local = 0;
+      bool part = false;
+      int cend = blockIdx.x + 1;
       for (int s = 0; s < S; ++s) {
         const int c = s % NCH;
         const int acc = local & 1;
         if (c == 0) {
+          int tile, kb0, kb1, sp;
+          wl.seg(s / NCH, tile, kb0, kb1, sp, part);
+          cend = part ? blockIdx.x + 1 : wl.contrib_end(tile);
+          for (int cc = blockIdx.x + 1; cc < cend; ++cc) sk_wait(sk_flag(sk_ws, gridDim.x, cc, q));
           mbar_wait(&acc_full[acc], (local >> 1) & 1);
           tc_fence_after();
         }
@@ -461,6 +489,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&acc_empty[acc]);
           ++local;
+        }
+        if (part) {
+          sk_write_chunk(sk_slot(sk_ws, blockIdx.x), q, NCH, c, lane, r);
+          if (c == NCH - 1) sk_signal(sk_flag(sk_ws, gridDim.x, blockIdx.x, q));
+        } else {
+          for (int cc = blockIdx.x + 1; cc < cend; ++cc) sk_add_chunk(sk_slot(sk_ws, cc), q, NCH, c, lane, r);
+          if (c == NCH - 1 && lane == 0)
+            for (int cc = blockIdx.x + 1; cc < cend; ++cc) *sk_flag(sk_ws, gridDim.x, cc, q) = 0;
         }
         uint8_t* b = wbuf + (s % NBUF) * C_::BUF_BYTES;
         if (C_::LOADS) {
@@ -474,6 +510,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (lane == 0) bulk_wait_read<(NBUF > 0 ? NBUF - 1 : 0)>();
           __syncwarp();
         }
+        if (part) continue;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           float4* slot = reinterpret_cast<float4*>(b + lane * 128 + ((j ^ (lane & 7)) << 4));
@@ -686,6 +723,14 @@ static void dims_of(const tofu_conv_args* a, int& M, int& N, int& K) {
   }
 }
 
+static bool sk_enabled() {  // TOFU_SK=0 turns stream-K off (A/B measurements)
+  static const bool on = [] {
+    const char* e = getenv("TOFU_SK");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static int auto_splits(const tofu_conv_args* a, int M, int N, int K, int bn) {
   if (a->kind != 1 || a->splits == 1) return 1;
   const int nk = (K + BK - 1) / BK;
@@ -708,9 +753,19 @@ static int launch_t(const Params& P, const CUtensorMap* tm, cudaStream_t st) {
       return TOFU_ERR_CUDA;
     attr = true;
   }
-  const int units = ((P.M + BM - 1) / BM) * ((P.N + BN - 1) / BN) * P.splits;
-  const int grid = units < g_sms ? units : g_sms;
-  kern<<<grid, NTHREADS, C_::SMEM, st>>>(P, tm[0], tm[1], tm[2]);
+  const int tiles = ((P.M + BM - 1) / BM) * ((P.N + BN - 1) / BN);
+  const int units = tiles * P.splits;
+  int grid = units < g_sms ? units : g_sms;
+  Params Q = P;
+  // HBM bytes: the gathered activations once (taps re-read them from L2), the dense operand, the output side
+  const double M = P.M, N = P.N, K = P.K, ch = P.a.nch;
+  const double e = MODE == 3 ? 12 : MODE == 2 ? 8 : MODE == 1 ? 4 : 2 + 2 * (((P.a.ep >> 1) & 1) + ((P.a.ep >> 2) & 1));
+  const double bytes = KIND == 0 ? 2 * M * ch + 2 * N * K + e * M * N : 2 * K * M + 2 * K * ch + e * M * N;
+  Q.sk_tiles = P.splits == 1 && sk_enabled()
+                   ? sk_tiles_for(tiles, (P.K + BK - 1) / BK, g_sms, P.a.sk_ws, KIND == 1, 2 * M * N * K / bytes)
+                   : 0;
+  if (Q.sk_tiles) grid = g_sms;
+  kern<<<grid, NTHREADS, C_::SMEM, st>>>(Q, tm[0], tm[1], tm[2]);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }
 
@@ -846,6 +901,7 @@ extern "C" int tofu_conv_launch_planned(const tofu_conv_args* a, const void* tma
   P.N = N;
   P.K = K;
   P.splits = a->splits > 1 ? a->splits : 1;
+  P.sk_tiles = 0;
   const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(tmaps);
   if (a->direct) {
     int blocks = (int)(((int64_t)M * N + 255) / 256);

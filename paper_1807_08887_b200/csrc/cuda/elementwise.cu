@@ -27,6 +27,11 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
   return u;
 }
 
+// sum-of-squares reduction scratch (one launch at a time per device: executors run on one stream each)
+constexpr int SUMSQ_MAX_BLOCKS = 4096;
+__device__ float g_sumsq_part[SUMSQ_MAX_BLOCKS];
+__device__ unsigned g_sumsq_ticket = 0;
+
 template <int KIND>
 __global__ void __launch_bounds__(256) ew_kernel(int64_t n, void* __restrict__ y, const void* __restrict__ x0,
                                                  const void* __restrict__ x1, void* __restrict__ x2, float s0,
@@ -115,7 +120,10 @@ __global__ void __launch_bounds__(256) ew_kernel(int64_t n, void* __restrict__ y
     }
   }
   if (KIND == TOFU_EW_SUMSQ) {
+    // deterministic: per-block partials, summed in block order by the last block to finish (no float atomics,
+    // so a loss is bitwise reproducible run to run and across executors)
     __shared__ float red[8];
+    __shared__ bool last;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = local;
@@ -123,7 +131,25 @@ __global__ void __launch_bounds__(256) ew_kernel(int64_t n, void* __restrict__ y
     if (threadIdx.x == 0) {
       float s = 0.f;
       for (int w = 0; w < 8; ++w) s += red[w];
-      atomicAdd(reinterpret_cast<float*>(y), s);
+      g_sumsq_part[blockIdx.x] = s;
+      __threadfence();
+      last = atomicAdd(&g_sumsq_ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      float t = 0.f;
+      for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) t += __ldcg(&g_sumsq_part[b]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        float s = 0.f;
+        for (int w = 0; w < 8; ++w) s += red[w];
+        *reinterpret_cast<float*>(y) += s;
+        g_sumsq_ticket = 0;  // ready for the next launch (launches of one stream are ordered)
+      }
     }
   }
 }
@@ -144,6 +170,7 @@ extern "C" int tofu_elementwise(int kind, int64_t n, void* y, const void* x0, co
   int64_t want = (n / 8 + 255) / 256;
   int64_t grid = sms * 8;
   if (want < grid) grid = want < 1 ? 1 : want;
+  if (grid > tofu::SUMSQ_MAX_BLOCKS) grid = tofu::SUMSQ_MAX_BLOCKS;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   switch (kind) {
 #define K(X) case X: tofu::ew_kernel<X><<<(unsigned)grid, 256, 0, st>>>(n, y, x0, x1, x2, s0, s1); break;

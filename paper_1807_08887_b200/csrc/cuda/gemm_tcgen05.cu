@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -32,23 +33,30 @@ namespace tofu {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int NTHREADS = 192;
 constexpr int SMEM_MAX = 232448;  // 227 KB opt-in per CTA on sm_100
-
-#ifndef TOFU_NBUF3
-#define TOFU_NBUF3 3
-#endif
-constexpr int NBUF3 = TOFU_NBUF3;
-
-template <int BN, int MODE>
+// Epilogue width: 4 warps (one per TMEM lane quarter) or 8 (two per quarter, each half of the tile's columns),
+// chosen per launch (bit 3 of the MODE_ template value): 8 for memory-leaning launches, whose epilogue streams the output
+// and its fused operands through HBM (measured, tools/sk_bench.py: the residual-add / relu-gradient-mask
+// epilogues of 1x1 convolutions with K <= 1024 run 1.3-1.7x faster, the configs[1] fused momentum-SGD weight
+// gradient 0.200 -> 0.167 ms); 4 for compute-bound launches, which keep one more smem pipeline stage.
+template <int BN, int MODE_>
 struct GemmCfg {
-  static constexpr bool LOADS = MODE == 2 || MODE == 3;
-  // the fused optimizer (MODE 3) streams momentum + weight through the epilogue (HBM-bound): deeper prefetch
-  static constexpr int NBUF = LOADS ? (MODE == 3 ? NBUF3 : 3) : 2;
+  static constexpr int MODE = MODE_ & 7;
+  static constexpr bool W8 = (MODE_ & 8) != 0;
+  // MODE 5 may load (residual add / relu mask operands, when its runtime `ep` asks for them)
+  static constexpr bool LOADS = MODE == 2 || MODE == 3 || MODE == 5;
+  // the fused optimizer (MODE 3) and the fused element-wise epilogue (MODE 5) stream extra operands through
+  // the epilogue (HBM-bound): deeper prefetch
+  static constexpr int NBUF = LOADS ? (MODE == 3 ? (W8 ? 2 : 3) : MODE == 5 ? 2 : 3) : 2;
   static constexpr int C_BYTES = 32 * 32 * (MODE == 0 || MODE == 5 ? 2 : 4);
-  static constexpr int D_OFF = 4096;
-  static constexpr int BUF_BYTES = MODE == 3 ? 6144 : (C_BYTES < 1024 ? 1024 : C_BYTES);
-  static constexpr int EPI_BYTES = 4 * NBUF * BUF_BYTES;
+  // MODE 3: W chunk at D_OFF.  MODE 5: add chunk at 0 (the bf16 result overwrites it in place, each thread
+  // its own 16-byte slots), mask chunk at D_OFF = 2048.
+  static constexpr int D_OFF = MODE == 5 ? 2048 : 4096;
+  static constexpr int BUF_BYTES = MODE == 3 ? 6144 : MODE == 5 ? 4096 : (C_BYTES < 1024 ? 1024 : C_BYTES);
+  // epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter, each half of the tile's columns)
+  static constexpr int EW = W8 ? 8 : 4;
+  static constexpr int THREADS = 64 + 32 * EW;
+  static constexpr int EPI_BYTES = EW * NBUF * BUF_BYTES;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -61,14 +69,14 @@ struct GemmCfg {
   static_assert(SMEM <= SMEM_MAX, "smem");
 };
 
-template <int BN, bool A_MN, bool B_MN, int MODE>
-__global__ void __launch_bounds__(NTHREADS, 1)
+template <int BN, bool A_MN, bool B_MN, int MODE_>
+__global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD,
                      const __grid_constant__ CUtensorMap tmE, int M, int N, int K, float s0, float s1, int splits,
-                     int ep, const __nv_bfloat16* __restrict__ aux_add, const __nv_bfloat16* __restrict__ aux_mask,
-                     int ldx) {
-  using Cfg = GemmCfg<BN, MODE>;
+                     int ep, int sk_tiles, void* sk_ws) {
+  using Cfg = GemmCfg<BN, MODE_>;
+  constexpr int MODE = Cfg::MODE;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int NBUF = Cfg::NBUF;
   extern __shared__ uint8_t smem_raw[];
@@ -81,7 +89,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* acc_full = empty + STAGES;             // [ACC_BUFS]
   uint64_t* acc_empty = acc_full + Cfg::ACC_BUFS;  // [ACC_BUFS]
   uint64_t* ebar = acc_empty + Cfg::ACC_BUFS;      // [4][NBUF] epilogue load barriers
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 4 * NBUF);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + Cfg::EW * NBUF);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -89,9 +97,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int tiles_n = (N + BN - 1) / BN;
   const int ntiles = tiles_m * tiles_n;
   const int nk = (K + BK - 1) / BK;
-  // work unit = (output tile, K split); split s covers k-blocks [s*nk/splits, (s+1)*nk/splits)
-  const int nunits = ntiles * splits;
-  auto kb_lo = [&](int sp) { return (int)((int64_t)sp * nk / splits); };
+  // segments = (output tile, k-block range): data-parallel units (tile, K split) then stream-K pieces
+  WorkList wl;
+  wl.init(ntiles, nk, splits, sk_tiles);
+  const int nseg = wl.count();
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -100,14 +109,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     for (int b = 0; b < Cfg::ACC_BUFS; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 4);  // one arrive per epilogue warp
+      mbar_init(&acc_empty[b], Cfg::EW);  // one arrive per epilogue warp
     }
-    for (int b = 0; b < 4 * NBUF; ++b) mbar_init(&ebar[b], 1);
+    for (int b = 0; b < Cfg::EW * NBUF; ++b) mbar_init(&ebar[b], 1);
     fence_mbar_init();
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmC);
-    if (MODE == 3) tma_prefetch_desc(&tmD);
+    if (MODE == 3 || MODE == 5) tma_prefetch_desc(&tmD);
+    if (MODE == 5) tma_prefetch_desc(&tmE);
   }
   if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
   tc_fence_before();
@@ -119,11 +129,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       int it = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const int tile = u / splits, sp = u % splits;
+      for (int i = 0; i < nseg; ++i) {
+        int tile, kb0, kb1, sp;
+        bool part;
+        wl.seg(i, tile, kb0, kb1, sp, part);
         const int m0 = (tile / tiles_n) * BM;
         const int n0 = (tile % tiles_n) * BN;
-        for (int kb = kb_lo(sp); kb < kb_lo(sp + 1); ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
@@ -150,16 +162,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
-      int it = 0, local = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++local) {
-        const int sp = u % splits;
-        const int kb0 = kb_lo(sp);
+      int it = 0;
+      for (int local = 0; local < nseg; ++local) {
+        int tile, kb0, kb1, sp;
+        bool part;
+        wl.seg(local, tile, kb0, kb1, sp, part);
         const int buf = local & 1;
         const uint32_t aph = (local >> 1) & 1;
         mbar_wait(&acc_empty[buf], aph ^ 1);  // epilogue has drained this accumulator
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + buf * BN;
-        for (int kb = kb0; kb < kb_lo(sp + 1); ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&full[s], ph);
@@ -182,65 +195,75 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else {
     // ------------------------------------------------------------ epilogue (warps 2..5)
     const int q = warp & 3;  // TMEM lane quarter = tile rows 32q..32q+31
-    constexpr int NCH = BN / 32;
-    const int my_units = blockIdx.x < nunits ? (nunits - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    const int S = my_units * NCH;
-    uint8_t* wbuf = sE + q * NBUF * Cfg::BUF_BYTES;
-    uint64_t* wbar = ebar + q * NBUF;
+    constexpr int NCH = BN / 32;              // 32-column chunks of a tile row quarter
+    constexpr int NCW = NCH / (Cfg::EW / 4);  // of which this warp handles [h*NCW, (h+1)*NCW)
+    const int e = warp - 2, h = e / 4;
+    const int S = nseg * NCW;
+    uint8_t* wbuf = sE + e * NBUF * Cfg::BUF_BYTES;
+    uint64_t* wbar = ebar + e * NBUF;
     int split_of_chunk = 0;
+    bool part_of_chunk = false;
     auto chunk_coords = [&](int s, int& col, int& row) {
-      const int u = blockIdx.x + (s / NCH) * gridDim.x;
-      const int tile = u / splits;
-      split_of_chunk = u % splits;
-      col = (tile % tiles_n) * BN + (s % NCH) * 32;
+      int tile, kb0, kb1;
+      wl.seg(s / NCW, tile, kb0, kb1, split_of_chunk, part_of_chunk);
+      col = (tile % tiles_n) * BN + (h * NCW + s % NCW) * 32;
       row = (tile / tiles_n) * BM + q * 32;
     };
+    // MODE 5 loads only the operands its runtime `ep` names (2 KB each: a 32x32 bf16 chunk, SWIZZLE_64B)
+    const bool loads = MODE == 5 ? (ep & 6) != 0 : Cfg::LOADS;
+    const uint32_t load_bytes = MODE == 3 ? 6144 : MODE == 5 ? 2048u * (((ep >> 1) & 1) + ((ep >> 2) & 1)) : 4096;
     auto issue_load = [&](int s) {  // lane 0 only
       int col, row;
       chunk_coords(s, col, row);
       uint8_t* b = wbuf + (s % NBUF) * Cfg::BUF_BYTES;
-      mbar_arrive_expect_tx(&wbar[s % NBUF], MODE == 3 ? 6144 : 4096);
-      tma_load_2d(b, &tmC, &wbar[s % NBUF], col, row);
-      if (MODE == 3) tma_load_2d(b + Cfg::D_OFF, &tmD, &wbar[s % NBUF], col, row);
-    };
-    if (Cfg::LOADS && lane == 0)
-      for (int s = 0; s < NBUF - 1 && s < S; ++s) issue_load(s);
-    // MODE 5: the element-wise operands of this thread's row segment (64 B each), prefetched one chunk ahead
-    uint4 xa[4], xm[4];
-    auto load_aux = [&](int s, uint4 (&A)[4], uint4 (&Mk)[4]) {
-      int col, row;
-      chunk_coords(s, col, row);
-      row += lane;
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const bool ok = row < M && col + 8 * v < N;
-        const int64_t e = (int64_t)row * ldx + col + 8 * v;
-        A[v] = (ok && (ep & 2)) ? __ldg(reinterpret_cast<const uint4*>(aux_add + e)) : make_uint4(0, 0, 0, 0);
-        Mk[v] = (ok && (ep & 4)) ? __ldg(reinterpret_cast<const uint4*>(aux_mask + e)) : make_uint4(0, 0, 0, 0);
+      if (part_of_chunk) {  // a stream-K partial: no epilogue operands needed
+        mbar_arrive_expect_tx(&wbar[s % NBUF], 0);
+        return;
+      }
+      mbar_arrive_expect_tx(&wbar[s % NBUF], load_bytes);
+      if (MODE == 5) {
+        if (ep & 2) tma_load_2d(b, &tmD, &wbar[s % NBUF], col, row);
+        if (ep & 4) tma_load_2d(b + Cfg::D_OFF, &tmE, &wbar[s % NBUF], col, row);
+      } else {
+        tma_load_2d(b, &tmC, &wbar[s % NBUF], col, row);
+        if (MODE == 3) tma_load_2d(b + Cfg::D_OFF, &tmD, &wbar[s % NBUF], col, row);
       }
     };
-    if (MODE == 5 && S > 0) load_aux(0, xa, xm);
+    if (loads && lane == 0)
+      for (int s = 0; s < NBUF - 1 && s < S; ++s) issue_load(s);
     int local = 0;
+    bool part = false;         // current segment is a stream-K partial (written to the workspace)
+    int cend = blockIdx.x + 1; // finisher: partials of CTAs blockIdx.x+1 .. cend-1 are added
     for (int s = 0; s < S; ++s) {
-      const int c = s % NCH;
+      const int cw = s % NCW, c = h * NCW + cw;
       const int acc = local & 1;
-      uint4 na[4], nm[4];
-      if (MODE == 5 && s + 1 < S) load_aux(s + 1, na, nm);
-      if (c == 0) {
+      if (cw == 0) {
+        int tile, kb0, kb1, sp;
+        wl.seg(s / NCW, tile, kb0, kb1, sp, part);
+        cend = part ? blockIdx.x + 1 : wl.contrib_end(tile);
+        for (int cc = blockIdx.x + 1; cc < cend; ++cc) sk_wait(sk_flag(sk_ws, gridDim.x, cc, e));
         mbar_wait(&acc_full[acc], (local >> 1) & 1);
         tc_fence_after();
       }
       uint32_t r[32];
       tmem_ld_32x32b_x32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, r);
       tmem_ld_wait();
-      if (c == NCH - 1) {  // accumulator fully read: hand TMEM back to the MMA warp
+      if (cw == NCW - 1) {  // accumulator fully read: hand TMEM back to the MMA warp
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[acc]);
         ++local;
       }
+      if (part) {
+        sk_write_chunk(sk_slot(sk_ws, blockIdx.x), q, NCH, c, lane, r);
+        if (cw == NCW - 1) sk_signal(sk_flag(sk_ws, gridDim.x, blockIdx.x, e));
+      } else {
+        for (int cc = blockIdx.x + 1; cc < cend; ++cc) sk_add_chunk(sk_slot(sk_ws, cc), q, NCH, c, lane, r);
+        if (cw == NCW - 1 && lane == 0)
+          for (int cc = blockIdx.x + 1; cc < cend; ++cc) *sk_flag(sk_ws, gridDim.x, cc, e) = 0;
+      }
       uint8_t* b = wbuf + (s % NBUF) * Cfg::BUF_BYTES;
-      if (Cfg::LOADS) {
+      if (loads) {
         if (lane == 0 && s + NBUF - 1 < S) {
           bulk_wait_read<0>();  // the store that last used that buffer has read its smem
           issue_load(s + NBUF - 1);
@@ -251,6 +274,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (lane == 0) bulk_wait_read<NBUF - 1>();
         __syncwarp();
       }
+      if (part) continue;
       if (MODE == 5) {
         // fused element-wise ops of the output's consumers (DESIGN R8/R13): v = acc (+ add), relu, mask
 #pragma unroll
@@ -260,7 +284,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
           for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[8 * j + e]);
           if (ep & 2) {
-            const uint4 u = xa[j];
+            const uint4 u = *reinterpret_cast<const uint4*>(b + off);
             const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -273,7 +297,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
             for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
           if (ep & 4) {
-            const uint4 u = xm[j];
+            const uint4 u = *reinterpret_cast<const uint4*>(b + Cfg::D_OFF + off);
             const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -287,11 +311,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
           for (int e = 0; e < 4; ++e) wh[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
           *reinterpret_cast<uint4*>(b + off) = w;
-        }
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          xa[v] = na[v];
-          xm[v] = nm[v];
         }
       } else if (MODE == 0) {
         uint32_t p[16];
@@ -382,10 +401,33 @@ static int make_tmap(CUtensorMap* tm, const void* ptr, CUtensorMapDataType dt, i
   return r == CUDA_SUCCESS ? 0 : -(int)r - 1000;
 }
 
-template <int BN, bool A_MN, bool B_MN, int MODE>
-static int launch_t(const tofu_gemm_args* g, const CUtensorMap* tm, cudaStream_t st) {
-  using Cfg = GemmCfg<BN, MODE>;
-  auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, MODE>;
+static bool sk_enabled() {  // TOFU_SK=0 turns stream-K off (A/B measurements)
+  static const bool on = [] {
+    const char* e = getenv("TOFU_SK");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// algorithmic flops / HBM bytes of a launch (operands once, output side e bytes per element)
+static double gemm_intensity(const tofu_gemm_args* g, int mode) {
+  const double M = g->M, N = g->N, K = g->K;
+  const double e = mode == 3 ? 12 : mode == 2 ? 8 : mode == 1 ? 4 : 2 + 2 * (((g->ep >> 1) & 1) + ((g->ep >> 2) & 1));
+  return 2 * M * N * K / (2 * M * K + 2 * N * K + e * M * N);
+}
+static int ew8_override() {  // TOFU_EW8=0 / 1 forces the 4- / 8-warp epilogue (A/B measurements); else auto
+  static const int v = [] {
+    const char* e = getenv("TOFU_EW8");
+    return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
+  }();
+  return v;
+}
+
+template <int BN, bool A_MN, bool B_MN, int MODE_>
+static int launch_t(const tofu_gemm_args* g, const CUtensorMap* tm, cudaStream_t st, double ai) {
+  using Cfg = GemmCfg<BN, MODE_>;
+  constexpr int MODE = Cfg::MODE;
+  auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, MODE_>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
@@ -393,24 +435,44 @@ static int launch_t(const tofu_gemm_args* g, const CUtensorMap* tm, cudaStream_t
     attr_set = true;
   }
   const int splits = MODE == 4 ? g->splits : 1;
-  const int units = ((g->M + BM - 1) / BM) * ((g->N + BN - 1) / BN) * splits;
+  const int tiles = ((g->M + BM - 1) / BM) * ((g->N + BN - 1) / BN);
+  const int units = tiles * splits;
   int grid = units < g_num_sms ? units : g_num_sms;
   if (g->max_ctas > 0 && grid > g->max_ctas) grid = g->max_ctas;
-  kern<<<grid, NTHREADS, Cfg::SMEM, st>>>(tm[0], tm[1], tm[2], tm[3], tm[5], g->M, g->N, g->K, g->s0, g->s1, splits,
-                                         g->ep, reinterpret_cast<const __nv_bfloat16*>(g->aux_add),
-                                         reinterpret_cast<const __nv_bfloat16*>(g->aux_mask), g->ldc);
+  int sk = 0;
+  // stream-K only on request (splits = -1): measured on one B200 it does not pay for TMA-fed GEMMs, whose
+  // power-capped clock rises when the last partial wave leaves SMs idle (tools/sk_bench.py, e.g. 196 tiles
+  // K = 9216: 111 us data-parallel vs 118 us stream-K); the gathered convolutions use it by default
+  if (g->splits == -1 && g->max_ctas == 0 && sk_enabled()) {
+    (void)ai;
+    sk = sk_tiles_for(tiles, (g->K + BK - 1) / BK, g_num_sms, g->sk_ws, false, 1e30);
+    if (sk) grid = g_num_sms;
+  }
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(tm[0], tm[1], tm[2], tm[3], tm[5], g->M, g->N, g->K, g->s0, g->s1, splits,
+                                         g->ep, sk, g->sk_ws);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }
 
 template <int BN>
 static int dispatch_bn(const tofu_gemm_args* g, const CUtensorMap* tm, cudaStream_t st) {
   const int mode = g->c_mode == 0 && g->ep ? 5 : g->c_mode;
-  const int key = (g->a_mn_major ? 1 : 0) | (g->b_mn_major ? 2 : 0) | (mode << 2);
+  const double ai = gemm_intensity(g, mode);
+  const int ov = ew8_override();
+  // 8 epilogue warps when a tile's epilogue traffic rivals its mainloop: per output element 2K flops against
+  // e bytes of output-side HBM traffic (bf16 / fused element-wise / fused optimizer outputs).  Measured: the
+  // configs[1] weight gradient (2K/e = 85) and the WResNet 1x1 add / mask epilogues (2K/e = 128..512) gain;
+  // with the optimizer the wide epilogue leaves 2 smem stages (vs 3) and loses from 2K/e ~ 430 (LSTM gate
+  // weight gradients), bf16 outputs keep 3 (vs 4) and lose at 2K/e >= 1000.
+  const double e = mode == 3 ? 12 : 2 + 2 * (((g->ep >> 1) & 1) + ((g->ep >> 2) & 1));
+  const double lim = mode == 3 ? 200.0 : 600.0;
+  const bool w8 = (mode == 0 || mode == 3 || mode == 5) && (ov >= 0 ? ov == 1 : 2.0 * g->K / e < lim);
+  const int key = (g->a_mn_major ? 1 : 0) | (g->b_mn_major ? 2 : 0) | ((mode | (w8 ? 8 : 0)) << 2);
   switch (key) {
 #define TOFU_CASE(AM, BMJ, O) \
-  case ((AM) | ((BMJ) << 1) | ((O) << 2)): return launch_t<BN, (bool)(AM), (bool)(BMJ), O>(g, tm, st);
+  case ((AM) | ((BMJ) << 1) | ((O) << 2)): return launch_t<BN, (bool)(AM), (bool)(BMJ), O>(g, tm, st, ai);
 #define TOFU_CASES(O) TOFU_CASE(0, 0, O) TOFU_CASE(0, 1, O) TOFU_CASE(1, 0, O) TOFU_CASE(1, 1, O)
     TOFU_CASES(0) TOFU_CASES(1) TOFU_CASES(2) TOFU_CASES(3) TOFU_CASES(4) TOFU_CASES(5)
+    TOFU_CASES(8) TOFU_CASES(11) TOFU_CASES(13)
 #undef TOFU_CASES
 #undef TOFU_CASE
     default: return TOFU_ERR_ARG;
@@ -492,6 +554,11 @@ static int auto_splits(const tofu_gemm_args* g, int bn) {
 
 using namespace tofu;
 
+extern "C" int64_t tofu_sk_workspace_bytes(void) {
+  if (encode_fn_init() != 0) return 0;
+  return (int64_t)g_num_sms * (SK_SLOT_FLOATS * 4 + 4 * SK_FLAGS);
+}
+
 extern "C" int64_t tofu_gemm_workspace_bytes(const tofu_gemm_args* g) {
   return g->splits > 1 ? (int64_t)g->splits * g->M * g->N * 4 : 0;
 }
@@ -513,7 +580,8 @@ extern "C" int tofu_gemm_plan_tmaps(tofu_gemm_args* g, void* tmaps, int* bn_out)
     return TOFU_ERR_ALIGN;
   int bn = (g->bn == 128 || g->bn == 256) ? g->bn : (g->N <= 128 ? 128 : 256);
   // (measured: 128-wide tiles do not recover the last-wave loss of 196-tile shapes, they run ~25% slower)
-  g->splits = auto_splits(g, bn);
+  const bool stream_k = g->splits == -1;
+  g->splits = stream_k ? 1 : auto_splits(g, bn);
   CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(tmaps);
   const CUtensorMapDataType BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   const auto SW128 = CU_TENSOR_MAP_SWIZZLE_128B, SW64 = CU_TENSOR_MAP_SWIZZLE_64B;
@@ -556,6 +624,7 @@ extern "C" int tofu_gemm_plan_tmaps(tofu_gemm_args* g, void* tmaps, int* bn_out)
                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return TOFU_ERR_CUDA;
   }
+  if (stream_k) g->splits = -1;  // kept as the launch's stream-K request
   *bn_out = bn;
   return TOFU_OK;
 }

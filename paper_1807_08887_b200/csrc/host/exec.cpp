@@ -152,6 +152,7 @@ struct Exec {
   std::vector<Launch> launches;
   tofu_piece* pieces_dev = nullptr;
   void* ws_dev = nullptr;  // split-K workspace shared by this executor's GEMMs (one stream)
+  void* sk_dev = nullptr;  // stream-K workspace (partials + flags, zero-filled), shared likewise
   std::vector<tofu_piece> host_pieces;
   bool finalized = false;
   struct GemmLaunch {
@@ -892,6 +893,12 @@ void finalize(Exec& E) {
     if (cudaMemcpy(E.pieces_dev, host.data(), host.size() * sizeof(tofu_piece), cudaMemcpyHostToDevice) != cudaSuccess)
       throw Error(TOFU_ERR_CUDA, "cudaMemcpy pieces");
   }
+  // stream-K workspace: launches run one at a time on the executor's stream, each leaves the flags zeroed
+  if (!E.sk_dev) {
+    const int64_t skb = tofu_sk_workspace_bytes();
+    if (skb <= 0 || cudaMalloc(&E.sk_dev, skb) != cudaSuccess || cudaMemset(E.sk_dev, 0, skb) != cudaSuccess)
+      throw Error(TOFU_ERR_CUDA, "cudaMalloc stream-K workspace");
+  }
   // GEMM descriptors (pass 0 sizes the shared split-K workspace with a placeholder address, pass 1 encodes
   // the real descriptors)
   for (int pass = 0; pass < 2; ++pass) {
@@ -951,6 +958,7 @@ void finalize(Exec& E) {
       }
       G.a.splits = 0;
       G.a.ws = pass == 0 ? reinterpret_cast<void*>(uintptr_t(1) << 20) : E.ws_dev;
+      G.a.sk_ws = E.sk_dev;
       int rc = tofu_gemm_plan_tmaps(&G.a, G.tm, &G.bn);
       if (rc) throw Error(rc, "gemm tensor map for op " + g.ops[o].name + " (pitch/alignment)");
       ws_need = std::max<int64_t>(ws_need, tofu_gemm_workspace_bytes(&G.a));
@@ -968,6 +976,7 @@ void finalize(Exec& E) {
         if (conv1x1_gemm(E, (int)o, li, G)) {
           G.a.splits = 0;
           G.a.ws = pass == 0 ? reinterpret_cast<void*>(uintptr_t(1) << 20) : E.ws_dev;
+          G.a.sk_ws = E.sk_dev;
           if (tofu_gemm_plan_tmaps(&G.a, G.tm, &G.bn) == TOFU_OK) {  // else: the convolution kernel below
             ws_need = std::max<int64_t>(ws_need, tofu_gemm_workspace_bytes(&G.a));
             if (pass == 1) E.gemms[{(int)o, li}] = G;
@@ -999,6 +1008,7 @@ void finalize(Exec& E) {
         }
         C.a.splits = 0;
         C.a.ws = pass == 0 ? reinterpret_cast<void*>(uintptr_t(1) << 20) : E.ws_dev;
+        C.a.sk_ws = E.sk_dev;
         const int rc = tofu_conv_plan(&C.a, C.tm);
         if (rc) throw Error(rc, "conv descriptors for op " + g.ops[o].name + " (geometry/alignment)");
         ws_need = std::max<int64_t>(ws_need, tofu_conv_workspace_bytes(&C.a));
@@ -1458,6 +1468,7 @@ extern "C" void tofu_exec_destroy(tofu_exec* h) {
   if (h->e.pieces_dev) cudaFree(h->e.pieces_dev);
   if (h->e.flags_dev) cudaFree(h->e.flags_dev);
   if (h->e.ws_dev) cudaFree(h->e.ws_dev);
+  if (h->e.sk_dev) cudaFree(h->e.sk_dev);
   delete h;
 }
 

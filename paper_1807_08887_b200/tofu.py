@@ -27,7 +27,7 @@ class GemmArgs(C.Structure):
                 ("C", C.c_void_p), ("ldc", C.c_int), ("c_mode", C.c_int),
                 ("bn", C.c_int), ("max_ctas", C.c_int), ("D", C.c_void_p), ("ldd", C.c_int),
                 ("s0", C.c_float), ("s1", C.c_float), ("splits", C.c_int), ("ws", C.c_void_p),
-                ("aux_add", C.c_void_p), ("aux_mask", C.c_void_p), ("ep", C.c_int)]
+                ("aux_add", C.c_void_p), ("aux_mask", C.c_void_p), ("ep", C.c_int), ("sk_ws", C.c_void_p)]
 
 
 MAX_TAPS = 64
@@ -48,7 +48,8 @@ class ConvArgs(C.Structure):
                 ("c_ys", C.c_int), ("c_y0", C.c_int), ("c_xs", C.c_int), ("c_x0", C.c_int),
                 ("ldc", C.c_int64), ("c_mode", C.c_int), ("D", C.c_void_p), ("ldd", C.c_int64),
                 ("s0", C.c_float), ("s1", C.c_float), ("splits", C.c_int), ("ws", C.c_void_p),
-                ("aux_add", C.c_void_p), ("aux_mask", C.c_void_p), ("ep", C.c_int), ("direct", C.c_int)]
+                ("aux_add", C.c_void_p), ("aux_mask", C.c_void_p), ("ep", C.c_int), ("sk_ws", C.c_void_p),
+                ("direct", C.c_int)]
 
 
 class Piece(C.Structure):
@@ -106,6 +107,9 @@ def lib():
                 continue
             f.argtypes = args
             f.restype = None if name.endswith("_destroy") else C.c_int
+        if hasattr(L, "tofu_sk_workspace_bytes"):   # (absent from experimental builds of older sources)
+            L.tofu_sk_workspace_bytes.argtypes = []
+            L.tofu_sk_workspace_bytes.restype = C.c_int64
         _lib = L
     return _lib
 
@@ -124,12 +128,19 @@ def _stream(stream):
 
 # ----------------------------------------------------------------------------- kernels
 def gemm(A, B, Cout, M, N, K, lda, a_mn, ldb, b_mn, ldc, c_mode, bn=0, max_ctas=0, stream=None, D=None, ldd=0,
-         s0=0.0, s1=0.0, splits=0, aux_add=None, aux_mask=None, ep=0):
+         s0=0.0, s1=0.0, splits=0, aux_add=None, aux_mask=None, ep=0, sk_ws=None):
+    """tofu_gemm_bf16 (include/tofu.h).  sk_ws: a zero-filled uint8 device tensor of tofu_sk_workspace_bytes()
+    bytes enables stream-K (left zeroed by the launch)."""
     a = GemmArgs(M, N, K, A.data_ptr(), lda, a_mn, B.data_ptr(), ldb, b_mn, Cout.data_ptr(), ldc, c_mode, bn, max_ctas,
                  D.data_ptr() if D is not None else None, ldd, s0, s1, splits, None,
                  aux_add.data_ptr() if aux_add is not None else None,
-                 aux_mask.data_ptr() if aux_mask is not None else None, ep)
+                 aux_mask.data_ptr() if aux_mask is not None else None, ep,
+                 sk_ws.data_ptr() if sk_ws is not None else None)
     check(lib().tofu_gemm_bf16(C.byref(a), _stream(stream)), "tofu_gemm_bf16")
+
+
+def sk_workspace_bytes() -> int:
+    return int(lib().tofu_sk_workspace_bytes())
 
 
 def conv(args: ConvArgs, stream=None):

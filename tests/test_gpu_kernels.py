@@ -127,6 +127,58 @@ def test_gemm_split_k(defname, M, N, K, splits, c_mode):
     assert nrm(outs[0], ref) <= (5e-3 if c_mode == 0 else 1e-5)
 
 
+@pytest.mark.parametrize("M,N,K", [(1000, 2048, 1024),      # 64 tiles < 148 SMs: every tile stream-K (splits=-1)
+                                   (6272, 1024, 4096),      # 196 tiles (WResNet stage-2 1x1): all stream-K
+                                   (2600, 2304, 520),       # 189 tiles, ragged M/N/K tails
+                                   (3840, 3072, 512)])      # 360 tiles: 148 data-parallel + 212 stream-K
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 5])
+def test_gemm_stream_k(M, N, K, mode):
+    """Stream-K (common.cuh WorkList): tiles whose k-loop is cut across CTAs are finished by adding the other
+    CTAs' fp32 partials in CTA order.  Same tolerances as the data-parallel GEMM, bitwise deterministic, the
+    workspace flags left zeroed; mode 5 = bf16 output with the fused add+relu+mask epilogue (ep = 7)."""
+    t = _tofu()
+    rng = np.random.default_rng(M + N + K + mode)
+    A, B = q(rng, (M, K), 2 ** -7), q(rng, (N, K), 2 ** -9)   # mm_nt: both K-major
+    acc = A @ B.T
+    c_mode = 0 if mode == 5 else mode
+    ws = torch.zeros(t.sk_workspace_bytes(), dtype=torch.uint8, device="cuda")
+    C0 = q(rng, (M, N), 2 ** -5) if mode in (2, 3) else np.zeros((M, N))
+    W0 = q(rng, (M, N), 2 ** -7)
+    X0, K0 = q(rng, (M, N), 2 ** -6), q(rng, (M, N), 2 ** -6)
+    outs = []
+    for rep in range(2):
+        kw = {}
+        if mode in (1, 2, 3):
+            Cd = torch.from_numpy(C0).float().cuda()
+        else:
+            Cd = torch.zeros((M, N), dtype=torch.bfloat16, device="cuda")
+        if mode == 3:
+            kw = dict(D=cuda_bf16(W0), ldd=N, s0=0.875, s1=0.0078125)
+        if mode == 5:
+            kw = dict(aux_add=cuda_bf16(X0), aux_mask=cuda_bf16(K0), ep=7)
+        t.gemm(cuda_bf16(A), cuda_bf16(B), Cd, M, N, K, K, 0, K, 0, N, c_mode, sk_ws=ws, splits=-1, **kw)
+        torch.cuda.synchronize()
+        outs.append((Cd.double().cpu().numpy(), kw["D"].double().cpu().numpy() if mode == 3 else None))
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    assert int(ws[-sms * 32:].count_nonzero()) == 0   # flags lowered again by the finishers
+    assert np.array_equal(outs[0][0], outs[1][0])
+    got = outs[0][0]
+    if mode == 0:
+        assert nrm(got, acc) <= 5e-3
+        assert np.mean(got == round_bf16(acc)) > 0.97
+    elif mode == 1:
+        assert nrm(got, acc) <= 1e-5
+    elif mode == 2:
+        assert nrm(got, C0 + acc) <= 1e-5
+    elif mode == 3:
+        mref = C0 * 0.875 + acc
+        assert nrm(got, mref) <= 1e-5
+        assert nrm(outs[0][1], round_bf16(W0 - got * 0.0078125)) <= 5e-3
+    else:
+        ref = np.where(K0 > 0, np.maximum(acc + X0, 0.0), 0.0)
+        assert nrm(got, ref) <= 5e-3
+
+
 def test_gemm_strided_output_and_bn():
     t = _tofu()
     rng = np.random.default_rng(9)

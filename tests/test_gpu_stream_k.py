@@ -1,0 +1,136 @@
+"""GPU parity of the stream-K work split (common.cuh WorkList) in the implicit-GEMM convolution kernel: a
+WResNet-like 3x3 convolution (16 x 14 x 14 pixels, 768 channels) whose output tiles cannot fill 148 SMs
+evenly (75 tiles for the forward / data gradient, 162 for the weight gradient; all compute-bound), so tiles' k-loops are cut across CTAs
+and finished from the fp32 partials of the others.  Forward (with the fused add+relu+mask
+epilogue), data gradient (MN-major weights, flipped taps) and weight gradient (store and fused momentum-SGD)
+against an fp64 CPU convolution (torch.nn.functional, float64) of the same bf16-exact inputs, and against
+the same launch without a stream-K workspace.  Tolerances as the north star: bf16 outputs normwise <= 5e-3,
+fp32 <= 1e-5."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+B, H, C = 16, 14, 768
+
+
+def _tofu():
+    from paper_1807_08887_b200 import tofu
+    tofu.lib()
+    return tofu
+
+
+def nrm(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def q(rng, shape, scale):
+    return rng.integers(-128, 129, size=shape).astype(np.float64) * scale
+
+
+def conv_args(t, kind, S, out, Bmat=None, mn=0, flip=False, Y=None):
+    a = t.ConvArgs()
+    a.kind = kind
+    a.nb, a.ngy, a.ngx = B, H, H
+    a.ay = a.ax = 1
+    a.cy = a.cx = 1 if flip else -1
+    a.ntaps = 9
+    for k in range(9):
+        ky, kx = divmod(k, 3)
+        a.tap_dy[k], a.tap_dx[k] = (-ky, -kx) if flip else (ky, kx)
+        a.tap_w[k] = k
+    a.nch = C
+    a.S = S.data_ptr()
+    a.s_sb, a.s_sy, a.s_sx = H * H * C, H * C, C
+    a.sH = a.sW = H
+    if kind == 0:
+        a.n_out = C
+        a.Bp = Bmat.data_ptr()
+        a.ldb = 9 * C
+        a.b_mn_major = mn
+        a.b_tap = C
+        a.b_rows, a.b_cols = C, 9 * C
+        a.C = out.data_ptr()
+        a.c_sb, a.c_sy, a.c_sx = H * H * C, H * C, C
+        a.c_ys = a.c_xs = 1
+    else:
+        a.m_out = C
+        a.Ap = Y.data_ptr()
+        a.lda = C
+        a.C = out.data_ptr()
+        a.ldc = 9 * C
+        a.c_mode = 1
+    return a
+
+
+@pytest.fixture(scope="module")
+def data():
+    rng = np.random.default_rng(31)
+    X = q(rng, (B, H, H, C), 2 ** -7)
+    W = q(rng, (C, 3, 3, C), 2 ** -11)        # [co][ky][kx][ci]
+    D = q(rng, (B, H, H, C), 2 ** -7)         # an output gradient
+    Xt = torch.from_numpy(X).permute(0, 3, 1, 2)
+    Wt = torch.from_numpy(W).permute(0, 3, 1, 2)
+    Dt = torch.from_numpy(D).permute(0, 3, 1, 2)
+    F = torch.nn.functional
+    ref = {
+        "fwd": F.conv2d(Xt, Wt, padding=1).permute(0, 2, 3, 1).numpy(),
+        "dgrad": F.conv_transpose2d(Dt, Wt, padding=1).permute(0, 2, 3, 1).numpy(),
+        "wgrad": torch.nn.grad.conv2d_weight(Xt, Wt.shape, Dt, padding=1).permute(0, 2, 3, 1).numpy(),
+    }
+    return rng, X, W, D, ref
+
+
+def cuda_bf16(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16).cuda()
+
+
+@pytest.mark.parametrize("which", ["fwd", "fwd_ep", "dgrad", "wgrad", "wgrad_opt"])
+def test_conv_stream_k(data, which):
+    t = _tofu()
+    rng, X, W, D, ref = data
+    ws = torch.zeros(t.sk_workspace_bytes(), dtype=torch.uint8, device="cuda")
+    Xd, Wd, Dd = cuda_bf16(X), cuda_bf16(W), cuda_bf16(D)
+    add, mask = q(rng, (B, H, H, C), 2 ** -6), q(rng, (B, H, H, C), 2 ** -6)
+    M0, W0 = q(rng, (C, 3, 3, C), 2 ** -12), q(rng, (C, 3, 3, C), 2 ** -7)
+    mu, lr = 0.875, 0.0078125
+    outs = []
+    for sk in (ws, None, ws):
+        keep = []
+        if which.startswith("fwd") or which == "dgrad":
+            out = torch.zeros((B, H, H, C), dtype=torch.bfloat16, device="cuda")
+            a = (conv_args(t, 0, Xd, out, Wd, 0) if which != "dgrad"
+                 else conv_args(t, 0, Dd, out, Wd, 1, flip=True))
+            if which == "fwd_ep":
+                keep = [cuda_bf16(add), cuda_bf16(mask)]
+                a.ep, a.aux_add, a.aux_mask = 7, keep[0].data_ptr(), keep[1].data_ptr()
+        else:
+            out = (torch.from_numpy(M0).float().cuda() if which == "wgrad_opt"
+                   else torch.zeros((C, 3, 3, C), dtype=torch.float32, device="cuda"))
+            a = conv_args(t, 1, Xd, out, Y=Dd)
+            if which == "wgrad_opt":
+                keep = [cuda_bf16(W0)]
+                a.c_mode, a.D, a.ldd, a.s0, a.s1 = 3, keep[0].data_ptr(), 9 * C, mu, lr
+            a.splits = 1   # stream-K (with ws) vs one data-parallel pass (without)
+        a.sk_ws = sk.data_ptr() if sk is not None else None
+        t.conv(a)
+        torch.cuda.synchronize()
+        outs.append((out.double().cpu().numpy(), keep[0].double().cpu().numpy() if which == "wgrad_opt" else None))
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    assert int(ws[-sms * 32:].count_nonzero()) == 0          # flags lowered by the finishers
+    assert np.array_equal(outs[0][0], outs[2][0])            # deterministic
+    got, plain = outs[0][0], outs[1][0]
+    if which in ("fwd", "dgrad"):
+        assert nrm(got, ref[which]) <= 5e-3
+        assert nrm(got, plain) <= 5e-3
+    elif which == "fwd_ep":
+        r = np.where(mask > 0, np.maximum(ref["fwd"] + add, 0.0), 0.0)
+        assert nrm(got, r) <= 5e-3
+    elif which == "wgrad":
+        assert nrm(got, ref["wgrad"]) <= 1e-5
+        assert nrm(got, plain) <= 1e-5
+    else:
+        mref = M0 * mu + ref["wgrad"]
+        assert nrm(got, mref) <= 1e-5
+        assert nrm(outs[0][1], np.asarray(torch.from_numpy(W0 - got * lr).to(torch.bfloat16).double())) <= 5e-3

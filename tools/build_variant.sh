@@ -16,6 +16,6 @@ for f in $P/csrc/host/*.cpp; do
   nvcc -O3 -std=c++17 -Xcompiler -fPIC -I include -I $P/csrc -x c++ -c $f -o $o &
   objs+=($o)
 done
-wait
+for p in $(jobs -p); do wait $p || { echo "compile failed"; exit 1; }; done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o $OUT "${objs[@]}" -ldl -lpthread -lrt
 echo built $OUT
