@@ -133,6 +133,24 @@ int tofu_exec_time_launch(tofu_exec* e, int index, void* ev_start, void* ev_stop
  *   ldc/ldd in elements.  Requirements: lda, ldb, ldd multiples of 8, ldc*elem a multiple of 16 B;
  *   A, B, C, D 16-byte aligned.  bn: 0 = auto, 128 or 256.  max_ctas: 0 = #SMs (persistent grid).
  */
+/* An operand assembled from up to TOFU_MAX_PIECES 2-D strided views (the fused MultiFetch of a partitioned
+ * sub-op, §6: the remote regions an operand needs are read by the GEMM's TMA producer straight
+ * from their owners' shards — peer HBM over NVLink, or the rank's own shard — instead of being copied into
+ * staging first).  The pieces tile the operand along one GEMM dimension: dim 0 = M (operand A) / N (B),
+ * dim 1 = K.  Piece i covers [start[i], start[i+1]) (the last up to the operand's extent) of that
+ * dimension and the whole operand in the other; its element (0, 0) is at ptr[i] with row pitch ld[i]
+ * elements, in the operand's majorness.  Starts must be multiples of the tile (M 128, N the launch's BN,
+ * K 64); start[0] = 0; pointers 16-byte aligned, pitches multiples of 8.  The memory must stay valid and
+ * unchanged until the launch completes (the executor brackets such launches with device barriers). */
+#define TOFU_MAX_PIECES 8
+typedef struct {
+  int n;    /* number of pieces, 1..TOFU_MAX_PIECES */
+  int dim;  /* 0: M (A) / N (B); 1: K */
+  int start[TOFU_MAX_PIECES];
+  const void* ptr[TOFU_MAX_PIECES];
+  int64_t ld[TOFU_MAX_PIECES];
+} tofu_operand_pieces;
+
 typedef struct {
   int M, N, K;
   const void* A;
@@ -161,11 +179,16 @@ typedef struct {
    * wave split the k-loop of some tiles across CTAs and sum the fp32 partials in fixed CTA order before the
    * epilogue (common.cuh WorkList). */
   void* sk_ws;
+  /* optional piecewise operands (NULL = A / B as given above): see tofu_operand_pieces */
+  const tofu_operand_pieces* a_pieces;
+  const tofu_operand_pieces* b_pieces;
 } tofu_gemm_args;
 int tofu_gemm_bf16(const tofu_gemm_args* args, void* stream);
-/* Split form used by the executor: encode the TMA descriptors (A, B, C, D, workspace, mask) once into `tmaps`
- * (6 x 128 bytes, 64-byte aligned; args->splits/ws are updated), then launch with them.  Split-K results
+/* Split form used by the executor: encode the TMA descriptors (A, B, C, D, workspace, mask, then the
+ * TOFU_MAX_PIECES piece maps of A and of B) once into `tmaps` (TOFU_GEMM_TMAPS x 128 bytes, 64-byte aligned;
+ * args->splits/ws are updated), then launch with them.  Split-K results
  * are reduced in fixed split order (deterministic). */
+#define TOFU_GEMM_TMAPS (6 + 2 * TOFU_MAX_PIECES)
 int tofu_gemm_plan_tmaps(tofu_gemm_args* args, void* tmaps, int* bn_out);
 int tofu_gemm_launch_planned(const tofu_gemm_args* args, const void* tmaps, int bn, void* stream);
 int64_t tofu_gemm_workspace_bytes(const tofu_gemm_args* args);

@@ -24,7 +24,9 @@
 #include <cudaTypedefs.h>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 #include "../tofu_kernels.h"
@@ -69,9 +71,30 @@ struct GemmCfg {
   static_assert(SMEM <= SMEM_MAX, "smem");
 };
 
-template <int BN, bool A_MN, bool B_MN, int MODE_>
+// Piecewise operands (tofu_operand_pieces, the MultiFetch fused into the TMA producer): one map per piece and
+// the pieces' starts along the split dimension (0 = M / N, 1 = K).  Passed by value as a __grid_constant__
+// kernel parameter (TMA reads maps from parameter space) only by the PC instantiations.
+struct PieceMaps {
+  CUtensorMap a_map[TOFU_MAX_PIECES];
+  CUtensorMap b_map[TOFU_MAX_PIECES];
+  int na, a_dim, nb, b_dim;
+  int a_start[TOFU_MAX_PIECES], b_start[TOFU_MAX_PIECES];
+};
+struct NoPieces {};
+
+// the map and the map-local coordinate of a tile coordinate (along the pieces' dimension)
+__device__ __forceinline__ const CUtensorMap* piece_of(const CUtensorMap* maps, const int* start, int n, int c,
+                                                       int& local) {
+  int i = 0;
+  while (i + 1 < n && c >= start[i + 1]) ++i;
+  local = c - start[i];
+  return maps + i;
+}
+
+template <int BN, bool A_MN, bool B_MN, int MODE_, bool PC>
 __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
-    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+    gemm_bf16_kernel(const __grid_constant__ std::conditional_t<PC, PieceMaps, NoPieces> pm,
+                     const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD,
                      const __grid_constant__ CUtensorMap tmE, int M, int N, int K, float s0, float s1, int splits,
                      int ep, int sk_tiles, void* sk_ws) {
@@ -143,17 +166,26 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
           uint8_t* a = sA + s * Cfg::A_BYTES;
           uint8_t* b = sB + s * Cfg::B_BYTES;
           const int k0 = kb * BK;
+          const CUtensorMap* ma = &tmA;
+          const CUtensorMap* mb = &tmB;
+          int am = m0, ak = k0, bnn = n0, bk = k0;
+          if constexpr (PC) {  // operand regions read in place from their owners' shards (peer or own HBM)
+            if (pm.na) ma = pm.a_dim ? piece_of(pm.a_map, pm.a_start, pm.na, k0, ak)
+                                     : piece_of(pm.a_map, pm.a_start, pm.na, m0, am);
+            if (pm.nb) mb = pm.b_dim ? piece_of(pm.b_map, pm.b_start, pm.nb, k0, bk)
+                                     : piece_of(pm.b_map, pm.b_start, pm.nb, n0, bnn);
+          }
           if (!A_MN) {
-            tma_load_2d(a, &tmA, &full[s], k0, m0);
+            tma_load_2d(a, ma, &full[s], ak, am);
           } else {
 #pragma unroll
-            for (int c = 0; c < BM / 64; ++c) tma_load_2d(a + c * 8192, &tmA, &full[s], m0 + 64 * c, k0);
+            for (int c = 0; c < BM / 64; ++c) tma_load_2d(a + c * 8192, ma, &full[s], am + 64 * c, ak);
           }
           if (!B_MN) {
-            tma_load_2d(b, &tmB, &full[s], k0, n0);
+            tma_load_2d(b, mb, &full[s], bk, bnn);
           } else {
 #pragma unroll
-            for (int c = 0; c < BN / 64; ++c) tma_load_2d(b + c * 8192, &tmB, &full[s], n0 + 64 * c, k0);
+            for (int c = 0; c < BN / 64; ++c) tma_load_2d(b + c * 8192, mb, &full[s], bnn + 64 * c, bk);
           }
         }
       }
@@ -423,11 +455,11 @@ static int ew8_override() {  // TOFU_EW8=0 / 1 forces the 4- / 8-warp epilogue (
   return v;
 }
 
-template <int BN, bool A_MN, bool B_MN, int MODE_>
-static int launch_t(const tofu_gemm_args* g, const CUtensorMap* tm, cudaStream_t st, double ai) {
+template <int BN, bool A_MN, bool B_MN, int MODE_, bool PC>
+static int launch_t(const tofu_gemm_args* g, const CUtensorMap* tm, const PieceMaps* pm, cudaStream_t st, double ai) {
   using Cfg = GemmCfg<BN, MODE_>;
   constexpr int MODE = Cfg::MODE;
-  auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, MODE_>;
+  auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, MODE_, PC>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
@@ -440,21 +472,24 @@ static int launch_t(const tofu_gemm_args* g, const CUtensorMap* tm, cudaStream_t
   int grid = units < g_num_sms ? units : g_num_sms;
   if (g->max_ctas > 0 && grid > g->max_ctas) grid = g->max_ctas;
   int sk = 0;
-  // stream-K only on request (splits = -1): measured on one B200 it does not pay for TMA-fed GEMMs, whose
-  // power-capped clock rises when the last partial wave leaves SMs idle (tools/sk_bench.py, e.g. 196 tiles
-  // K = 9216: 111 us data-parallel vs 118 us stream-K); the gathered convolutions use it by default
+  // stream-K only on request (splits = -1): measured on one B200 it does not pay for TMA-fed GEMMs
+  // (tools/sk_bench.py, e.g. 196 tiles K = 9216: 111 us data-parallel vs 118 us stream-K; DESIGN.md has our
+  // reading); the gathered convolutions use it by default
   if (g->splits == -1 && g->max_ctas == 0 && sk_enabled()) {
     (void)ai;
     sk = sk_tiles_for(tiles, (g->K + BK - 1) / BK, g_num_sms, g->sk_ws, false, 1e30);
     if (sk) grid = g_num_sms;
   }
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(tm[0], tm[1], tm[2], tm[3], tm[5], g->M, g->N, g->K, g->s0, g->s1, splits,
-                                         g->ep, sk, g->sk_ws);
+  std::conditional_t<PC, PieceMaps, NoPieces> pp{};
+  if constexpr (PC) pp = *pm;
+  (void)pm;
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(pp, tm[0], tm[1], tm[2], tm[3], tm[5], g->M, g->N, g->K, g->s0, g->s1,
+                                             splits, g->ep, sk, g->sk_ws);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }
 
 template <int BN>
-static int dispatch_bn(const tofu_gemm_args* g, const CUtensorMap* tm, cudaStream_t st) {
+static int dispatch_bn(const tofu_gemm_args* g, const CUtensorMap* tm, const PieceMaps* pm, cudaStream_t st) {
   const int mode = g->c_mode == 0 && g->ep ? 5 : g->c_mode;
   const double ai = gemm_intensity(g, mode);
   const int ov = ew8_override();
@@ -465,14 +500,17 @@ static int dispatch_bn(const tofu_gemm_args* g, const CUtensorMap* tm, cudaStrea
   // weight gradients), bf16 outputs keep 3 (vs 4) and lose at 2K/e >= 1000.
   const double e = mode == 3 ? 12 : 2 + 2 * (((g->ep >> 1) & 1) + ((g->ep >> 2) & 1));
   const double lim = mode == 3 ? 200.0 : 600.0;
-  const bool w8 = (mode == 0 || mode == 3 || mode == 5) && (ov >= 0 ? ov == 1 : 2.0 * g->K / e < lim);
-  const int key = (g->a_mn_major ? 1 : 0) | (g->b_mn_major ? 2 : 0) | ((mode | (w8 ? 8 : 0)) << 2);
+  const bool pc = pm != nullptr;  // piecewise operands: 4-warp epilogue instantiations only
+  const bool w8 = !pc && (mode == 0 || mode == 3 || mode == 5) && (ov >= 0 ? ov == 1 : 2.0 * g->K / e < lim);
+  const int key = (g->a_mn_major ? 1 : 0) | (g->b_mn_major ? 2 : 0) | ((mode | (w8 ? 8 : 0)) << 2) | (pc ? 64 : 0);
   switch (key) {
-#define TOFU_CASE(AM, BMJ, O) \
-  case ((AM) | ((BMJ) << 1) | ((O) << 2)): return launch_t<BN, (bool)(AM), (bool)(BMJ), O>(g, tm, st, ai);
-#define TOFU_CASES(O) TOFU_CASE(0, 0, O) TOFU_CASE(0, 1, O) TOFU_CASE(1, 0, O) TOFU_CASE(1, 1, O)
-    TOFU_CASES(0) TOFU_CASES(1) TOFU_CASES(2) TOFU_CASES(3) TOFU_CASES(4) TOFU_CASES(5)
-    TOFU_CASES(8) TOFU_CASES(11) TOFU_CASES(13)
+#define TOFU_CASE(AM, BMJ, O, P) \
+  case ((AM) | ((BMJ) << 1) | ((O) << 2) | ((P) << 6)): \
+    return launch_t<BN, (bool)(AM), (bool)(BMJ), O, (bool)(P)>(g, tm, pm, st, ai);
+#define TOFU_CASES(O, P) TOFU_CASE(0, 0, O, P) TOFU_CASE(0, 1, O, P) TOFU_CASE(1, 0, O, P) TOFU_CASE(1, 1, O, P)
+    TOFU_CASES(0, 0) TOFU_CASES(1, 0) TOFU_CASES(2, 0) TOFU_CASES(3, 0) TOFU_CASES(4, 0) TOFU_CASES(5, 0)
+    TOFU_CASES(8, 0) TOFU_CASES(11, 0) TOFU_CASES(13, 0)
+    TOFU_CASES(0, 1) TOFU_CASES(1, 1) TOFU_CASES(2, 1) TOFU_CASES(3, 1) TOFU_CASES(4, 1) TOFU_CASES(5, 1)
 #undef TOFU_CASES
 #undef TOFU_CASE
     default: return TOFU_ERR_ARG;
@@ -624,6 +662,28 @@ extern "C" int tofu_gemm_plan_tmaps(tofu_gemm_args* g, void* tmaps, int* bn_out)
                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return TOFU_ERR_CUDA;
   }
+  // piecewise operands: one map per piece (tm[6 + i] for A, tm[6 + TOFU_MAX_PIECES + i] for B)
+  for (int op = 0; op < 2; ++op) {
+    const tofu_operand_pieces* pc = op == 0 ? g->a_pieces : g->b_pieces;
+    if (!pc) continue;
+    const bool mn = op == 0 ? g->a_mn_major : g->b_mn_major;
+    const int mdim = op == 0 ? g->M : g->N;  // the operand's M / N extent
+    const int ext = pc->dim == 0 ? mdim : g->K;
+    const int gran = pc->dim == 1 ? BK : (op == 0 ? BM : bn);
+    if (pc->n < 1 || pc->n > TOFU_MAX_PIECES || pc->dim < 0 || pc->dim > 1 || pc->start[0] != 0) return TOFU_ERR_ARG;
+    for (int i = 0; i < pc->n; ++i) {
+      const int lo = pc->start[i], hi = i + 1 < pc->n ? pc->start[i + 1] : ext;
+      if (hi <= lo || lo % gran || (reinterpret_cast<uintptr_t>(pc->ptr[i]) & 15) || pc->ld[i] % 8 || pc->ld[i] <= 0)
+        return TOFU_ERR_ALIGN;
+      const uint64_t len = hi - lo;
+      // (inner, outer) extents of the piece: K-major = (K, M|N), MN-major = (M|N, K)
+      const uint64_t kx = pc->dim == 1 ? len : (uint64_t)g->K, mx = pc->dim == 0 ? len : (uint64_t)mdim;
+      CUtensorMap* t = &tm[6 + op * TOFU_MAX_PIECES + i];
+      const int rr = !mn ? make_tmap(t, pc->ptr[i], BF, 2, kx, mx, pc->ld[i], 64, op == 0 ? BM : bn, SW128)
+                         : make_tmap(t, pc->ptr[i], BF, 2, mx, kx, pc->ld[i], 64, 64, SW128);
+      if (rr) return TOFU_ERR_CUDA;
+    }
+  }
   if (stream_k) g->splits = -1;  // kept as the launch's stream-K request
   *bn_out = bn;
   return TOFU_OK;
@@ -641,12 +701,34 @@ extern "C" int tofu_gemm_launch_planned(const tofu_gemm_args* g, const void* tma
                : TOFU_ERR_CUDA;
   }
   const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(tmaps);
+  PieceMaps pmv;
+  const PieceMaps* pm = nullptr;
+  if (g->a_pieces || g->b_pieces) {
+    std::memset(&pmv, 0, sizeof pmv);
+    if (const tofu_operand_pieces* pc = g->a_pieces) {
+      pmv.na = pc->n;
+      pmv.a_dim = pc->dim;
+      for (int i = 0; i < pc->n; ++i) {
+        pmv.a_map[i] = tm[6 + i];
+        pmv.a_start[i] = pc->start[i];
+      }
+    }
+    if (const tofu_operand_pieces* pc = g->b_pieces) {
+      pmv.nb = pc->n;
+      pmv.b_dim = pc->dim;
+      for (int i = 0; i < pc->n; ++i) {
+        pmv.b_map[i] = tm[6 + TOFU_MAX_PIECES + i];
+        pmv.b_start[i] = pc->start[i];
+      }
+    }
+    pm = &pmv;
+  }
   if (g->splits > 1) {
     // partial products into the workspace planes, then one ordered reduction into C
     const CUtensorMap tw[6] = {tm[0], tm[1], tm[4], tm[4], tm[4], tm[4]};
     tofu_gemm_args p = *g;
     p.c_mode = 4;
-    int rc = bn == 256 ? dispatch_bn<256>(&p, tw, st) : dispatch_bn<128>(&p, tw, st);
+    int rc = bn == 256 ? dispatch_bn<256>(&p, tw, pm, st) : dispatch_bn<128>(&p, tw, pm, st);
     if (rc) return rc;
     const int64_t n = (int64_t)g->M * g->N / 4 + 1;
     int blocks = (int)((n + 255) / 256);
@@ -656,11 +738,11 @@ extern "C" int tofu_gemm_launch_planned(const tofu_gemm_args* g, const void* tma
                                                  g->s0, g->s1);
     return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
   }
-  return bn == 256 ? dispatch_bn<256>(g, tm, st) : dispatch_bn<128>(g, tm, st);
+  return bn == 256 ? dispatch_bn<256>(g, tm, pm, st) : dispatch_bn<128>(g, tm, pm, st);
 }
 
 extern "C" int tofu_gemm_bf16(const tofu_gemm_args* g, void* stream) {
-  alignas(64) CUtensorMap tm[6];
+  alignas(64) CUtensorMap tm[TOFU_GEMM_TMAPS];
   tofu_gemm_args a = *g;
   int bn = 0;
   int r = tofu_gemm_plan_tmaps(&a, tm, &bn);

@@ -81,6 +81,14 @@ struct Layout {  // one rank's arena
 };
 
 struct Buf {  // an operand buffer of one (op, rank)
+  struct RPiece {
+    int src;        // owner rank
+    int64_t off;    // bytes into the owner's arena of the piece's element (0, 0)
+    int64_t ld;     // row pitch (elements) of the piece's 2-D view
+    int start;      // first index along the cut GEMM dimension
+  };
+  std::vector<RPiece> rp;  // fused fetch: a GEMM operand read in place from its owners' shards (else empty)
+  int rp_dim = 0;          // 0: M / N, 1: K (tofu_operand_pieces.dim)
   bool direct = false;
   int64_t off = 0;            // bytes into the rank's arena
   std::vector<Rng> buf_box;   // the box the buffer holds (dense row-major)
@@ -101,6 +109,7 @@ struct LOp {
   Buf epi_add, epi_mask;      // its bf16 operands (the output's layout)
   std::vector<tofu_piece> fetch, reduce;
   std::vector<int> fetch_src, reduce_nremote;  // for the ledger
+  bool remote_direct = false;  // the compute reads peer memory in place (fused fetch)
 };
 
 Layout layout_rank(const Graph& g, const PlanSeq& p, int rank, std::vector<std::vector<LOp>>* lops_all = nullptr) {
@@ -157,8 +166,9 @@ struct Exec {
   bool finalized = false;
   struct GemmLaunch {
     tofu_gemm_args a;
-    alignas(64) CUtensorMap tm[6];
+    alignas(64) CUtensorMap tm[TOFU_GEMM_TMAPS];
     int bn;
+    tofu_operand_pieces pa, pb;  // piecewise operands (fused fetch), referenced by a.a_pieces / a.b_pieces
   };
   std::map<std::pair<int, int>, GemmLaunch> gemms;  // (op, li)
   struct ConvLaunch {
@@ -171,7 +181,9 @@ struct Exec {
   bool skip_comm = false;
   bool multi_process = false;
   bool fuse = true;
+  bool fuse_fetch = true;  // GEMM operands read in place from their owners' shards (TOFU_PFETCH=0: staged)
   std::vector<char> remote_fetch, remote_reduce;  // per op, over all ranks
+  std::vector<char> remote_direct;                 // per op: a compute launch reads peer memory (fused fetch)
   int timed_launch = -1;
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
 };
@@ -349,6 +361,12 @@ bool conv_operand_ok(const ConvGeom& cg, int pi, const std::vector<Rng>& buf, co
   return true;
 }
 
+// lowering options from the environment (TOFU_FUSE=0: no fusion; TOFU_PFETCH=0: staged MultiFetch only)
+void read_env_options(Exec& E) {
+  if (const char* f = std::getenv("TOFU_FUSE")) E.fuse = std::string(f) != "0";
+  if (const char* f = std::getenv("TOFU_PFETCH")) E.fuse_fetch = std::string(f) != "0";
+}
+
 void lower(Exec& E) {
   const Graph& g = *E.g;
   const PlanSeq& p = E.plan;
@@ -358,6 +376,70 @@ void lower(Exec& E) {
   std::vector<std::vector<LOp>> all(k, std::vector<LOp>(g.ops.size()));
   for (int r = 0; r < k; ++r) E.lay[r] = layout_rank(g, p, r);
   std::vector<int64_t> stage_need(k, 0);
+  // Fused fetch (P:L862-877 MultiFetch, B200 form): a GEMM operand whose required region is not a view of
+  // the rank's own shard is read in place by the GEMM's TMA producer from the shards of its owners (peer
+  // HBM over NVLink), when the owners' pieces tile the region along ONE GEMM dimension in whole tiles and
+  // each piece is a 2-D strided view of its owner's shard.  No staging copy, and the transfer overlaps the
+  // tensor-core work tile by tile.  Otherwise the region is staged by a MultiFetch launch as before.
+  // (an op whose output shares storage with the input is never read in place: a peer could overwrite it
+  // before this rank's read completes)
+  auto root_of = [&](int t) {
+    std::map<int, int> al(g.alias.begin(), g.alias.end());
+    while (al.count(t)) t = al[t];
+    return t;
+  };
+  auto aliases = [&](int t, int u) { return root_of(t) == root_of(u); };
+  auto try_pieces = [&](int t, bool is_a, const GemmForm& gf, Buf& b) -> bool {
+    const int split = is_a ? gf.a_split : gf.b_split;
+    const bool mn = is_a ? gf.a_mn : gf.b_mn;
+    const int nd = (int)b.box.size();
+    std::vector<std::pair<int, std::vector<Rng>>> parts;
+    for (int s = 0; s < k; ++s) {
+      if (E.lay[s].shard_off[t] < 0) continue;
+      std::vector<Rng> x;
+      if (nd == 0 || !inter(b.box, E.lay[s].shard_box[t], x)) continue;
+      parts.push_back({s, x});
+    }
+    if (parts.empty() || (int)parts.size() > TOFU_MAX_PIECES) return false;
+    int d = -1;  // the single dimension along which the pieces differ from the region
+    for (auto& pr : parts)
+      for (int e = 0; e < nd; ++e)
+        if (pr.second[e].lo != b.box[e].lo || pr.second[e].hi != b.box[e].hi) {
+          if (d >= 0 && d != e) return false;
+          d = e;
+        }
+    if (d < 0) d = 0;  // one owner holds the whole region
+    const int g0 = d < split ? 0 : split, g1 = d < split ? split : nd;
+    for (int e = g0; e < d; ++e)
+      if (b.box[e].len() != 1) return false;  // pieces must be contiguous ranges of the 2-D view
+    int64_t inner = 1;
+    for (int e = d + 1; e < g1; ++e) inner *= b.box[e].len();
+    std::sort(parts.begin(), parts.end(),
+              [d](const std::pair<int, std::vector<Rng>>& x, const std::pair<int, std::vector<Rng>>& y) {
+                return x.second[d].lo < y.second[d].lo;
+              });
+    int64_t at = b.box[d].lo;
+    for (auto& pr : parts) {
+      if (pr.second[d].lo != at) return false;
+      at = pr.second[d].hi + 1;
+    }
+    if (at != b.box[d].hi + 1) return false;
+    // GEMM dimension of the cut: K-major operands are [M|N][K], MN-major [K][M|N]
+    const bool kdim = (d < split) == mn;
+    const int gran = kdim ? 64 : (is_a ? 128 : 256);
+    std::vector<Buf::RPiece> rp;
+    for (auto& pr : parts) {
+      const int s = pr.first;
+      int64_t r_, c_, ld_, off_;
+      if (!flat2(E.lay[s].shard_box[t], pr.second, split, r_, c_, ld_, off_)) return false;
+      const int64_t start = (pr.second[d].lo - b.box[d].lo) * inner;
+      if (start % gran || ld_ % 8 || (off_ * g.itemsize(t)) % 16) return false;
+      rp.push_back({s, E.lay[s].shard_off[t] + off_ * g.itemsize(t), ld_, (int)start});
+    }
+    b.rp = std::move(rp);
+    b.rp_dim = kdim ? 1 : 0;
+    return true;
+  };
   for (int r = 0; r < k; ++r) {
     auto dig = worker_digits(r, p.factors);
     for (size_t o = 0; o < g.ops.size(); ++o) {
@@ -392,6 +474,11 @@ void lower(Exec& E) {
           b.direct = true;
           b.off = E.lay[r].shard_off[t];
           b.buf_box = own;
+        } else if (kind == "gemm" && E.fuse_fetch && gf.ok && !aliases(t, oi.output) &&
+                   try_pieces(t, (int)pi == gf.a_param, gf, b)) {
+          b.direct = false;  // read in place from the owners (b.rp); no staging
+          b.off = -1;
+          b.buf_box = b.box;
         } else {
           b.direct = false;
           b.off = soff;  // relative to staging, fixed up below
@@ -436,7 +523,7 @@ void lower(Exec& E) {
     E.lay[r].total = E.lay[r].staging_off + stage_need[r];
     for (auto& L : all[r]) {
       for (auto& b : L.in)
-        if (!b.direct) b.off += E.lay[r].staging_off;
+        if (!b.direct && b.rp.empty()) b.off += E.lay[r].staging_off;
       if (!L.out.direct) L.out.off += E.lay[r].staging_off;
     }
   }
@@ -462,6 +549,19 @@ void lower(Exec& E) {
         Buf& b = L.in[pi];
         if (b.direct) continue;
         const int t = oi.inputs[pi];
+        if (!b.rp.empty()) {  // fused fetch: the GEMM reads the pieces in place; the ledger counts them
+          for (auto& q : b.rp) {
+            L.fetch_src.push_back(q.src);
+            if (q.src != r) {
+              std::vector<Rng> x;
+              inter(b.box, E.lay[q.src].shard_box[t], x);
+              E.ledger_el += vol(x);
+              E.ledger_bytes += vol(x) * g.itemsize(t);
+              L.remote_direct = true;
+            }
+          }
+          continue;
+        }
         for (int s = 0; s < k; ++s) {
           if (E.lay[s].shard_off[t] < 0) continue;
           std::vector<Rng> x;
@@ -748,9 +848,11 @@ void lower(Exec& E) {
   }
   E.remote_fetch.assign(g.ops.size(), 0);
   E.remote_reduce.assign(g.ops.size(), 0);
+  E.remote_direct.assign(g.ops.size(), 0);
   for (int r = 0; r < k; ++r)
     for (size_t o = 0; o < g.ops.size(); ++o) {
       for (int s : all[r][o].fetch_src) E.remote_fetch[o] |= s != r;
+      E.remote_direct[o] |= all[r][o].remote_direct;
       for (int n : all[r][o].reduce_nremote) E.remote_reduce[o] |= n > 0;
     }
   E.lops.clear();
@@ -771,6 +873,8 @@ void build_launches(Exec& E) {
     bool any_fetch = false;
     for (int li = 0; li < nl; ++li) any_fetch |= !E.lops[li][o].fetch.empty();
     const bool bar_f = E.multi_process && E.remote_fetch[o];
+    // fused fetch: the compute launches read peer shards in place, so the WAR barrier follows them
+    const bool bar_c = E.multi_process && E.remote_direct[o];
     if (bar_f) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
     if (any_fetch) {
       Exec::Launch L{0, (int)o, -1, (int64_t)host.size(), 0, 0};
@@ -782,12 +886,13 @@ void build_launches(Exec& E) {
       L.npieces = (int64_t)host.size() - L.piece_off;
       E.launches.push_back(L);
     }
-    if (bar_f) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
+    if (bar_f && any_fetch) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
     for (int li = 0; li < nl; ++li) {
       if (E.lops[li][o].skip) continue;
       if (g.defs[g.ops[o].def].name == "sumsq") E.launches.push_back({4, (int)o, li, 0, 0, 0});
       E.launches.push_back({1, (int)o, li, 0, 0, 0});
     }
+    if (bar_c) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
     bool any_red = false;
     for (int li = 0; li < nl; ++li) any_red |= !E.lops[li][o].reduce.empty();
     const bool bar_r = E.multi_process && E.remote_reduce[o];
@@ -928,6 +1033,27 @@ void finalize(Exec& E) {
       G.a.B = E.arena[r] + B.off + boff * 2;
       G.a.ldb = (int)ldb;
       G.a.b_mn_major = gf.b_mn ? 1 : 0;
+      // fused fetch: operands read in place from their owners' shards (piece 0 doubles as the shape reference)
+      auto set_pieces = [&](const Buf& X, tofu_operand_pieces& P, const void*& ptr, int& ld) {
+        std::memset(&P, 0, sizeof P);
+        P.n = (int)X.rp.size();
+        P.dim = X.rp_dim;
+        for (int i = 0; i < P.n; ++i) {
+          P.start[i] = X.rp[i].start;
+          P.ptr[i] = E.arena[X.rp[i].src] + X.rp[i].off;
+          P.ld[i] = X.rp[i].ld;
+        }
+        ptr = P.ptr[0];
+        ld = (int)P.ld[0];
+      };
+      if (!A.rp.empty()) {
+        set_pieces(A, G.pa, G.a.A, G.a.lda);
+        G.a.a_pieces = &G.pa;
+      }
+      if (!B.rp.empty()) {
+        set_pieces(B, G.pb, G.a.B, G.a.ldb);
+        G.a.b_pieces = &G.pb;
+      }
       const int64_t ec = L.out.dtype == TOFU_BF16 ? 2 : 4;
       G.a.C = E.arena[r] + L.out.off + coff * ec;
       G.a.ldc = (int)ldc;
@@ -962,7 +1088,12 @@ void finalize(Exec& E) {
       int rc = tofu_gemm_plan_tmaps(&G.a, G.tm, &G.bn);
       if (rc) throw Error(rc, "gemm tensor map for op " + g.ops[o].name + " (pitch/alignment)");
       ws_need = std::max<int64_t>(ws_need, tofu_gemm_workspace_bytes(&G.a));
-      if (pass == 1) E.gemms[{(int)o, li}] = G;
+      if (pass == 1) {
+        Exec::GemmLaunch& S = E.gemms[{(int)o, li}];
+        S = G;  // (the piece tables move with it: re-point the args at the stored copies)
+        if (S.a.a_pieces) S.a.a_pieces = &S.pa;
+        if (S.a.b_pieces) S.a.b_pieces = &S.pb;
+      }
     }
   }
   for (int li = 0; li < nl; ++li)
@@ -1398,6 +1529,7 @@ extern "C" int tofu_exec_arena_bytes(const tofu_graph* g, const tofu_plan* p, in
     E.k = tofu::plan_of(p).k;
     if (rank < 0 || rank >= E.k) throw tofu::Error(TOFU_ERR_ARG, "rank out of range");
     E.local = {rank};
+    tofu::read_env_options(E);  // the same lowering options as tofu_exec_create (staging sizes depend on them)
     tofu::lower(E);
     *bytes = E.lay[rank].total;
     return TOFU_OK;
@@ -1445,7 +1577,7 @@ extern "C" int tofu_exec_create(const tofu_graph* g, const tofu_plan* p, int n_l
         E.arena.push_back(static_cast<char*>(arena_dev[r]));
       }
       E.multi_process = n_local < E.k;
-      if (const char* f = std::getenv("TOFU_FUSE")) E.fuse = std::string(f) != "0";
+      tofu::read_env_options(E);
       if (E.multi_process) {
         if (!flags_dev) throw tofu::Error(TOFU_ERR_ARG, "flags_dev required when not all ranks are local");
         for (int r = 0; r < E.k; ++r) E.flags.push_back(flags_dev[r]);
@@ -1570,6 +1702,11 @@ std::string launch_desc(const Exec& E, int i) {
   if (L.kind == 1 && E.lops[L.li][L.op].fused_opt >= 0) o += ",\"fused\":\"gemm+mom+sgd\"";
   if (L.kind == 1 && E.lops[L.li][L.op].fused_next) o += ",\"fused\":\"lstm-cell-pair\"";
   if (L.kind == 1 && E.lops[L.li][L.op].wt_off >= 0) o += ",\"weights\":\"transposed\"";
+  if (L.kind == 1) {
+    int np = 0;
+    for (auto& b : E.lops[L.li][L.op].in) np += !b.rp.empty();
+    if (np) o += ",\"inplace_remote_operands\":" + std::to_string(np);
+  }
   if (L.kind == 1 && E.lops[L.li][L.op].ep) {
     const int ep = E.lops[L.li][L.op].ep;
     o += std::string(",\"fused\":\"epilogue") + (ep & 2 ? "+add" : "") + (ep & 1 ? "+relu" : "") + (ep & 4 ? "+mask" : "") + "\"";

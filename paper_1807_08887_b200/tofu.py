@@ -27,7 +27,16 @@ class GemmArgs(C.Structure):
                 ("C", C.c_void_p), ("ldc", C.c_int), ("c_mode", C.c_int),
                 ("bn", C.c_int), ("max_ctas", C.c_int), ("D", C.c_void_p), ("ldd", C.c_int),
                 ("s0", C.c_float), ("s1", C.c_float), ("splits", C.c_int), ("ws", C.c_void_p),
-                ("aux_add", C.c_void_p), ("aux_mask", C.c_void_p), ("ep", C.c_int), ("sk_ws", C.c_void_p)]
+                ("aux_add", C.c_void_p), ("aux_mask", C.c_void_p), ("ep", C.c_int), ("sk_ws", C.c_void_p),
+                ("a_pieces", C.c_void_p), ("b_pieces", C.c_void_p)]
+
+
+MAX_PIECES = 8
+
+
+class OperandPieces(C.Structure):
+    _fields_ = [("n", C.c_int), ("dim", C.c_int), ("start", C.c_int * MAX_PIECES),
+                ("ptr", C.c_void_p * MAX_PIECES), ("ld", C.c_int64 * MAX_PIECES)]
 
 
 MAX_TAPS = 64
@@ -128,14 +137,26 @@ def _stream(stream):
 
 # ----------------------------------------------------------------------------- kernels
 def gemm(A, B, Cout, M, N, K, lda, a_mn, ldb, b_mn, ldc, c_mode, bn=0, max_ctas=0, stream=None, D=None, ldd=0,
-         s0=0.0, s1=0.0, splits=0, aux_add=None, aux_mask=None, ep=0, sk_ws=None):
+         s0=0.0, s1=0.0, splits=0, aux_add=None, aux_mask=None, ep=0, sk_ws=None, a_pieces=None, b_pieces=None):
     """tofu_gemm_bf16 (include/tofu.h).  sk_ws: a zero-filled uint8 device tensor of tofu_sk_workspace_bytes()
-    bytes enables stream-K (left zeroed by the launch)."""
+    bytes enables stream-K (left zeroed by the launch).  a_pieces / b_pieces: (dim, [(start, tensor, ld), ...])
+    piecewise operands (tofu_operand_pieces; A / B are then only shape references)."""
+    def pieces(p):
+        if p is None:
+            return None
+        dim, lst = p
+        op = OperandPieces()
+        op.n, op.dim = len(lst), dim
+        for i, (st, t, ld) in enumerate(lst):
+            op.start[i], op.ptr[i], op.ld[i] = st, t.data_ptr(), ld
+        return op
+    pa, pb = pieces(a_pieces), pieces(b_pieces)
     a = GemmArgs(M, N, K, A.data_ptr(), lda, a_mn, B.data_ptr(), ldb, b_mn, Cout.data_ptr(), ldc, c_mode, bn, max_ctas,
                  D.data_ptr() if D is not None else None, ldd, s0, s1, splits, None,
                  aux_add.data_ptr() if aux_add is not None else None,
                  aux_mask.data_ptr() if aux_mask is not None else None, ep,
-                 sk_ws.data_ptr() if sk_ws is not None else None)
+                 sk_ws.data_ptr() if sk_ws is not None else None,
+                 C.addressof(pa) if pa is not None else None, C.addressof(pb) if pb is not None else None)
     check(lib().tofu_gemm_bf16(C.byref(a), _stream(stream)), "tofu_gemm_bf16")
 
 

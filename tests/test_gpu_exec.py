@@ -191,3 +191,35 @@ def test_pipelined_train_loop_equals_manual_steps():
     assert np.allclose(la, [float(x) for x in lb], rtol=1e-6, atol=0)
     for t in ("W1", "W2", "M1"):
         assert torch.equal(A.gather(t), B.gather(t))
+
+
+@pytest.mark.parametrize("cfg,k", [(1, 2), (1, 4), (1, 8), (2, 4)])
+def test_fused_fetch_equals_staged_fetch(cfg, k, monkeypatch):
+    """Fused MultiFetch (the GEMM's TMA producer reads the required region in place from its owners'
+    shards, include/tofu.h tofu_operand_pieces) vs the staged MultiFetch launch (TOFU_PFETCH=0): the
+    same operand values reach the same tiles, so the results are bitwise equal; the byte ledger still
+    equals the plan, and the fused executor issues fewer fetch launches."""
+    from paper_1807_08887_b200.runner import TofuRunner
+    if cfg == 2:   # a 2-layer, 6-step LSTM of hidden 512 (configs[2] structure, small)
+        from tofu_inputs.graphs import lstm
+        spec = lstm(2, 512, 6, 64)
+    else:
+        spec = config(cfg)
+    vals = make_values(spec, seed=41)
+    outs, fetches, inplace = {}, {}, {}
+    for pf in ("0", "1"):
+        monkeypatch.setenv("TOFU_PFETCH", pf)
+        R = TofuRunner(spec, k)
+        R.load(vals)
+        R.step()
+        torch.cuda.synchronize()
+        descs = [R.exec.launch_desc(i) for i in range(R.exec.num_launches())]
+        fetches[pf] = sum(d["kind"] == "fetch" for d in descs)
+        inplace[pf] = sum(d.get("inplace_remote_operands", 0) for d in descs)
+        assert R.ledger() == R.plan.cost()
+        outs[pf] = {t: R.gather(t).float().cpu().numpy() for t in spec["tensors"]}
+        del R
+    assert inplace["0"] == 0 and inplace["1"] > 0
+    assert fetches["1"] < fetches["0"]
+    for t in spec["tensors"]:
+        assert np.array_equal(outs["0"][t], outs["1"][t]), t
