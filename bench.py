@@ -225,6 +225,9 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if os.environ.get("BENCH_TRACE_AFTER"):   # debugging aid: dump the Python stacks of a stuck run
+        import faulthandler
+        faulthandler.dump_traceback_later(int(os.environ["BENCH_TRACE_AFTER"]), exit=True)
     if args.impl == "reference":
         return reference_arm(args, world, rank)
 
@@ -233,11 +236,26 @@ def main():
     from paper_1807_08887_b200.runner import TofuRunner
 
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local_rank)
+    # one GPU per rank over NCCL; with fewer GPUs than ranks (a functional check of the multi-process path on
+    # one GPU) the ranks share devices and the host collectives go over gloo (flagged in config.shared_gpu)
+    shared = world > torch.cuda.device_count()
+    dev = local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         group = dist.group.WORLD
+
+    def all_reduce(t, op):
+        if shared:
+            c = t.cpu()
+            dist.all_reduce(c, op=op)
+            t.copy_(c)
+        else:
+            dist.all_reduce(t, op=op)
 
     spec = config(args.config)
     k = world
@@ -323,8 +341,16 @@ def main():
         dom_samples.append(dom_a.elapsed_time(dom_b))   # last step of the timed region
         # keep the same step loop running (untimed) until nvidia-smi has >= 5 samples, so the clock
         # record covers this workload under load even when the timed region is only milliseconds
+        # (every step holds device barriers across ranks: all ranks agree on each extra round, or they hang)
         deadline = time.time() + 3.0
-        while (len(clk.rows) < 5 or time.time() < soak_start + 0.6) and time.time() < deadline:
+        while True:
+            more = (len(clk.rows) < 5 or time.time() < soak_start + 0.6) and time.time() < deadline
+            if world > 1:
+                flag = torch.tensor([1.0 if more else 0.0], device="cuda")
+                all_reduce(flag, dist.ReduceOp.MAX)
+                more = float(flag.item()) > 0
+            if not more:
+                break
             for _ in range(20):
                 R.step()
             torch.cuda.synchronize()
@@ -335,7 +361,7 @@ def main():
     dom_ms = statistics.median(dom_samples)
     if world > 1:
         tt = torch.tensor([ms], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        all_reduce(tt, dist.ReduceOp.MAX)
         ms = float(tt.item())
 
     batch = spec.get("meta", {}).get("samples_per_step", spec["tensors"]["X"]["shape"][0])
@@ -366,9 +392,11 @@ def main():
     e2e_ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
         tt = torch.tensor([e2e_ms, h2d], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt[:1], op=dist.ReduceOp.MAX)
+        t0_ = tt[:1].clone()
+        all_reduce(t0_, dist.ReduceOp.MAX)
+        tt[:1] = t0_
         hh = tt[1:].clone()
-        dist.all_reduce(hh, op=dist.ReduceOp.SUM)
+        all_reduce(hh, dist.ReduceOp.SUM)
         e2e_ms, h2d = float(tt[0]), int(hh[0])
 
     pk = peaks()
@@ -414,6 +442,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, bf16-exact values)",
         "config": {"workload": CONFIG_NAME[args.config], "global_batch": batch, "parallelism": f"tofu-k{k}",
+                   **({"shared_gpu": True} if world > 1 and shared else {}),
                    "plan_factors": R.plan_json["factors"], "l2": "inputs larger than L2 (W+M+dW 640 MiB)"},
         "roofline": roof,
         "step_roofline": {"compute_ms": t_comp * 1e3, "comm_ms": t_comm * 1e3, "hbm_ms": t_hbm * 1e3,
