@@ -109,6 +109,7 @@ def lib():
             "tofu_exec_launch_desc": [vp, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
             "tofu_execute_range": [vp, C.c_int, C.c_int, vp],
             "tofu_exec_time_launch": [vp, C.c_int, vp, vp],
+            "tofu_transpose_taps": [vp, vp, C.c_int, C.c_int, C.c_int, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name, None)
@@ -158,6 +159,12 @@ def gemm(A, B, Cout, M, N, K, lda, a_mn, ldb, b_mn, ldc, c_mode, bn=0, max_ctas=
                  sk_ws.data_ptr() if sk_ws is not None else None,
                  C.addressof(pa) if pa is not None else None, C.addressof(pb) if pb is not None else None)
     check(lib().tofu_gemm_bf16(C.byref(a), _stream(stream)), "tofu_gemm_bf16")
+
+
+def transpose_taps(W, WT, co, taps, ci, stream=None):
+    """tofu_transpose_taps: WT[ci][taps][co] = W[co][taps][ci] (bf16 device tensors)."""
+    check(lib().tofu_transpose_taps(C.c_void_p(W.data_ptr()), C.c_void_p(WT.data_ptr()), co, taps, ci,
+                                    _stream(stream)), "tofu_transpose_taps")
 
 
 def sk_workspace_bytes() -> int:

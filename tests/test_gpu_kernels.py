@@ -239,3 +239,15 @@ def test_elementwise(kind, n):
         mref = a * 2 ** -6 * s0 + b
         assert nrm(m.double().cpu().numpy(), mref) <= 1e-6
         assert nrm(w.double().cpu().numpy(), round_bf16(w0 - mref * s1)) <= 5e-3
+
+
+@pytest.mark.parametrize("co,taps,ci", [(1024, 9, 1024), (256, 49, 8), (72, 9, 200), (13, 9, 7)])
+def test_transpose_taps(co, taps, ci):
+    """The data gradients' K-major weight copy WT[ci][t][co] = W[co][t][ci]: a pure permutation, bit-exact
+    (16-byte vector path when co and ci are multiples of 8, scalar path otherwise, ragged 64-tiles)."""
+    t = _tofu()
+    W = torch.randn(co, taps, ci, device="cuda").bfloat16()
+    WT = torch.zeros(ci, taps, co, device="cuda", dtype=torch.bfloat16)
+    t.transpose_taps(W, WT, co, taps, ci)
+    torch.cuda.synchronize()
+    assert torch.equal(WT.cpu(), W.permute(2, 1, 0).contiguous().cpu())
