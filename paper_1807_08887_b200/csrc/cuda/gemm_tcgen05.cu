@@ -618,6 +618,22 @@ extern "C" int tofu_gemm_plan_tmaps(tofu_gemm_args* g, void* tmaps, int* bn_out)
     return TOFU_ERR_ALIGN;
   int bn = (g->bn == 128 || g->bn == 256) ? g->bn : (g->N <= 128 ? 128 : 256);
   // (measured: 128-wide tiles do not recover the last-wave loss of 196-tile shapes, they run ~25% slower)
+  // Few-tile outputs (256-wide tiles fill at most half the SMs) that 128-wide tiles fill more than half of,
+  // e.g. the LSTM's per-timestep [128 x 16384] gate GEMMs, which stream their 134 MB weight from HBM: 128-wide
+  // tiles instead of split-K.  Measured on configs[2]: forward gate GEMMs 6.78 -> 5.62 ms, recurrent backward
+  // 6.54 -> 6.30 ms per step (stream-K instead: 7.48 / 8.19 ms); outputs with fewer tiles (WResNet stage-0
+  // weight gradients, K = 100352 pixels; FC sub-GEMMs at k = 8) keep split-K, which measured faster there.
+  // TOFU_GEMM_FEW=0 keeps 256-wide tiles + split-K everywhere, 2 = stream-K.
+  static const int few = [] {
+    const char* e = getenv("TOFU_GEMM_FEW");
+    return e ? atoi(e) : 1;
+  }();
+  if (few && g->bn == 0 && g->splits == 0 && !g->ep && bn == 256 &&
+      2 * ((g->M + BM - 1) / BM) * ((g->N + 255) / 256) <= g_num_sms &&
+      (few != 1 || 2 * ((g->M + BM - 1) / BM) * ((g->N + 127) / 128) > g_num_sms)) {
+    if (few == 1) bn = 128;
+    if (few == 2 && g->sk_ws) g->splits = -1;
+  }
   const bool stream_k = g->splits == -1;
   g->splits = stream_k ? 1 : auto_splits(g, bn);
   CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(tmaps);
