@@ -256,8 +256,13 @@ typedef struct {
    * of fewer than 8 channels, unaligned pitches, e.g. an 8-way split of the 8-channel image); the same math
    * then runs on CUDA cores (fp32 accumulation, same epilogues).  Never chosen for aligned shapes. */
   int direct;
+  /* set by tofu_conv_plan: 1 = the gathered operand is loaded by TMA in im2col mode (stride-1 grid; nch a
+   * multiple of 64 (kind 0) / of the N tile (kind 1)), 0 = by the gather warps (cp.async); i2c_dy0/dx0: the
+   * smallest tap offsets.
+   * On entry, im2col = -1 keeps the gather warps (used by the parity tests). */
+  int im2col, i2c_dy0, i2c_dx0;
 } tofu_conv_args;
-/* Encode TMA descriptors once (tmaps: 4 x 128 B, 64-byte aligned; args->splits updated), then launch. */
+/* Encode TMA descriptors once (tmaps: 5 x 128 B, 64-byte aligned; args->splits / direct / im2col updated), then launch. */
 int tofu_conv_plan(tofu_conv_args* args, void* tmaps);
 int tofu_conv_launch_planned(const tofu_conv_args* args, const void* tmaps, void* stream);
 int tofu_conv_bf16(const tofu_conv_args* args, void* stream);

@@ -22,6 +22,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -41,6 +42,7 @@ struct Params {
   tofu_conv_args a;
   int M, N, K, splits;
   int sk_tiles;  // stream-K tiles (common.cuh WorkList); 0 = data-parallel only
+  int dy0, dx0;  // im2col: smallest tap offsets (the map's im2col offsets are tap - min >= 0)
 };
 
 struct RowInfo {
@@ -93,10 +95,14 @@ __device__ __forceinline__ RowInfo no_pixel() {
   return ri;
 }
 
-template <int KIND, int BN, bool B_MN, int MODE>
+// I2C (kind 0): the activation operand is loaded by TMA in im2col mode (tmI) instead of the gather warps:
+// one 128-pixel x 64-channel box per k-block, zero outside the tensor (= padding), straight into the
+// 128B-swizzled layout of the gathered tile.  Used for stride-1 grids whose channel blocks are whole taps.
+template <int KIND, int BN, bool B_MN, int MODE, bool I2C = false>
 __global__ void __launch_bounds__(NTHREADS, 1)
     conv_kernel(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap tmDense,
-                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD) {
+                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD,
+                const __grid_constant__ CUtensorMap tmI) {
   using C_ = Cfg<KIND, BN, MODE>;
   constexpr int STAGES = C_::STAGES;
   constexpr int NBUF = C_::NBUF;
@@ -128,7 +134,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1 + NGATHER);
+      mbar_init(&full[s], I2C ? 1 : 1 + NGATHER);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -140,6 +146,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tma_prefetch_desc(&tmDense);
     if (KIND == 1) tma_prefetch_desc(&tmC);
     if (MODE == 3) tma_prefetch_desc(&tmD);
+    if (I2C) tma_prefetch_desc(&tmI);
   }
   if (warp == 1) tmem_alloc(tmem_slot, C_::TMEM_COLS);
   tc_fence_before();
@@ -157,12 +164,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         wl.seg(i, tile, kb0, kb1, sp, part);
         const int m0 = (tile / tiles_n) * BM;
         const int n0 = (tile % tiles_n) * BN;
+        int iw = 0, ih = 0, in_ = 0;  // im2col: traversal start of the tile's first pixel
+        if constexpr (I2C) {
+          const int gb = m0 / ngyx, rem = m0 - gb * ngyx;
+          const int gy = rem / a.ngx, gx = rem - gy * a.ngx;
+          ih = gy + a.cy + P.dy0;
+          iw = gx + a.cx + P.dx0;
+          in_ = gb + a.sb0;
+        }
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           const int k0 = kb * BK;
           if constexpr (KIND == 0) {
-            mbar_arrive_expect_tx(&full[s], C_::B_BYTES);
+            mbar_arrive_expect_tx(&full[s], C_::B_BYTES + (I2C ? C_::A_BYTES : 0));
+            if constexpr (I2C) {
+              const int t = k0 / a.nch, c = k0 - t * a.nch;
+              tma_load_im2col_4d(sA + s * C_::A_BYTES, &tmI, &full[s], a.sc0 + c, iw, ih, in_,
+                                 (uint16_t)(a.tap_dx[t] - P.dx0), (uint16_t)(a.tap_dy[t] - P.dy0));
+            }
             uint8_t* b = sB + s * C_::B_BYTES;
             if (!B_MN) {  // W[n][taps][c]: columns tap_w[t]*b_tap + c
               const int col = (a.nch % BK == 0) ? a.tap_w[k0 / a.nch] * a.b_tap + k0 % a.nch : k0;
@@ -181,10 +201,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               }
             }
           } else {
-            mbar_arrive_expect_tx(&full[s], C_::A_BYTES);
+            mbar_arrive_expect_tx(&full[s], C_::A_BYTES + (I2C ? C_::B_BYTES : 0));
             uint8_t* aa = sA + s * C_::A_BYTES;
 #pragma unroll
             for (int q = 0; q < BM / 64; ++q) tma_load_2d(aa + q * 8192, &tmDense, &full[s], m0 + 64 * q, k0);
+            if constexpr (I2C) {  // B rows = the k-block's 64 pixels, BN columns = channels of the tile's tap
+              const int gb = k0 / ngyx, rem = k0 - gb * ngyx;
+              const int gy = rem / a.ngx, gx = rem - gy * a.ngx;
+              const int t = n0 / a.nch, c = n0 - t * a.nch;
+              const uint16_t ow = (uint16_t)(a.tap_dx[t] - P.dx0), oh = (uint16_t)(a.tap_dy[t] - P.dy0);
+#pragma unroll
+              for (int q = 0; q < BN / 64; ++q)
+                tma_load_im2col_4d(sB + s * C_::B_BYTES + q * 8192, &tmI, &full[s], a.sc0 + c + 64 * q,
+                                   gx + a.cx + P.dx0, gy + a.cy + P.dy0, gb + a.sb0, ow, oh);
+            }
           }
         }
       }
@@ -224,7 +254,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         umma_commit(&acc_full[buf]);
       }
     }
-  } else if (warp >= 6) {
+  } else if (warp >= 6 && !I2C) {
     // ------------------------------------------------------------ gather producers (warps 6..9)
     // Per stage a thread issues a fixed set of 16-byte copies whose shared-memory slots are compile-time
     // offsets (the 128B swizzle phase of its rows is constant); per copy: one row-info load, two bounds
@@ -302,7 +332,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
       }
     }
-  } else {
+  } else if (warp < 6) {
     // ------------------------------------------------------------ epilogue (warps 2..5)
     const int q = warp & 3;
     constexpr int NCH = BN / 32;
@@ -663,6 +693,7 @@ __global__ void __launch_bounds__(256) conv_direct(Params P) {
 
 // ------------------------------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static PFN_cuTensorMapEncodeIm2col_v12000 g_encode_i2c = nullptr;
 static std::once_flag g_once;
 static int g_sms = 148;
 
@@ -673,6 +704,9 @@ static int init() {
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode_i2c = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(fn);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
@@ -743,10 +777,10 @@ static int auto_splits(const tofu_conv_args* a, int M, int N, int K, int bn) {
   return sp < 2 ? 1 : sp;
 }
 
-template <int KIND, int BN, bool B_MN, int MODE>
+template <int KIND, int BN, bool B_MN, int MODE, bool I2C = false>
 static int launch_t(const Params& P, const CUtensorMap* tm, cudaStream_t st) {
   using C_ = Cfg<KIND, BN, MODE>;
-  auto kern = conv_kernel<KIND, BN, B_MN, MODE>;
+  auto kern = conv_kernel<KIND, BN, B_MN, MODE, I2C>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM) != cudaSuccess)
@@ -765,7 +799,7 @@ static int launch_t(const Params& P, const CUtensorMap* tm, cudaStream_t st) {
                    ? sk_tiles_for(tiles, (P.K + BK - 1) / BK, g_sms, P.a.sk_ws, KIND == 1, 2 * M * N * K / bytes)
                    : 0;
   if (Q.sk_tiles) grid = g_sms;
-  kern<<<grid, NTHREADS, C_::SMEM, st>>>(Q, tm[0], tm[1], tm[2]);
+  kern<<<grid, NTHREADS, C_::SMEM, st>>>(Q, tm[0], tm[1], tm[2], tm[4]);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }
 
@@ -773,8 +807,16 @@ static int dispatch(const Params& P, const CUtensorMap* tm, int mode, cudaStream
   const tofu_conv_args& a = P.a;
   const int bn = bn_of(&a, P.N);
   if (a.kind == 0) {
-    const int key = (bn == 256 ? 1 : 0) | (a.b_mn_major ? 2 : 0) | (mode << 2);
+    const int key = (bn == 256 ? 1 : 0) | (a.b_mn_major ? 2 : 0) | (mode << 2) | (a.im2col ? 8 : 0);
     switch (key) {
+      case 8: return launch_t<0, 128, false, 0, true>(P, tm, st);
+      case 9: return launch_t<0, 256, false, 0, true>(P, tm, st);
+      case 10: return launch_t<0, 128, true, 0, true>(P, tm, st);
+      case 11: return launch_t<0, 256, true, 0, true>(P, tm, st);
+      case 12: return launch_t<0, 128, false, 1, true>(P, tm, st);
+      case 13: return launch_t<0, 256, false, 1, true>(P, tm, st);
+      case 14: return launch_t<0, 128, true, 1, true>(P, tm, st);
+      case 15: return launch_t<0, 256, true, 1, true>(P, tm, st);
       case 0: return launch_t<0, 128, false, 0>(P, tm, st);
       case 1: return launch_t<0, 256, false, 0>(P, tm, st);
       case 2: return launch_t<0, 128, true, 0>(P, tm, st);
@@ -786,18 +828,15 @@ static int dispatch(const Params& P, const CUtensorMap* tm, int mode, cudaStream
       default: return TOFU_ERR_ARG;
     }
   }
-  if (bn == 256) switch (mode) {
-      case 1: return launch_t<1, 256, true, 1>(P, tm, st);
-      case 2: return launch_t<1, 256, true, 2>(P, tm, st);
-      case 3: return launch_t<1, 256, true, 3>(P, tm, st);
-      case 4: return launch_t<1, 256, true, 4>(P, tm, st);
-      default: return TOFU_ERR_ARG;
-    }
-  switch (mode) {
-    case 1: return launch_t<1, 128, true, 1>(P, tm, st);
-    case 2: return launch_t<1, 128, true, 2>(P, tm, st);
-    case 3: return launch_t<1, 128, true, 3>(P, tm, st);
-    case 4: return launch_t<1, 128, true, 4>(P, tm, st);
+  const int key = mode | (bn == 256 ? 8 : 0) | (a.im2col ? 16 : 0);
+  switch (key) {
+#define TOFU_K1(MO, BNV, I) \
+  case (MO) | ((BNV) == 256 ? 8 : 0) | ((I) ? 16 : 0): return launch_t<1, BNV, true, MO, (bool)(I)>(P, tm, st);
+    TOFU_K1(1, 256, 0) TOFU_K1(2, 256, 0) TOFU_K1(3, 256, 0) TOFU_K1(4, 256, 0)
+    TOFU_K1(1, 128, 0) TOFU_K1(2, 128, 0) TOFU_K1(3, 128, 0) TOFU_K1(4, 128, 0)
+    TOFU_K1(1, 256, 1) TOFU_K1(2, 256, 1) TOFU_K1(3, 256, 1) TOFU_K1(4, 256, 1)
+    TOFU_K1(1, 128, 1) TOFU_K1(2, 128, 1) TOFU_K1(3, 128, 1) TOFU_K1(4, 128, 1)
+#undef TOFU_K1
     default: return TOFU_ERR_ARG;
   }
 }
@@ -818,6 +857,46 @@ static bool natural_taps(const tofu_conv_args* a) {
   for (int t = 0; t < a->ntaps; ++t)
     if (a->tap_w[t] != t) return false;
   return true;
+}
+
+// im2col TMA for the gathered activations (tmaps[4]): stride-1 grids, whole 64-channel blocks (kind 0: per
+// tap; kind 1: the N tile of `gran` columns within one tap), corners and tap offsets within the encodable
+// ranges.  pixels = the box's pixel count (kind 0: BM output pixels; kind 1: BK pixels of a k-block).
+// TOFU_I2C=0 (or im2col = -1 on entry) keeps the gather warps.
+static void try_im2col(tofu_conv_args* a, CUtensorMap* tm, int pixels, int gran) {
+  static const bool i2c_on = [] {
+    const char* e = getenv("TOFU_I2C");
+    return !(e && e[0] == '0');
+  }();
+  const bool no_i2c = a->im2col == -1;
+  a->im2col = 0;
+  a->i2c_dy0 = a->i2c_dx0 = 0;
+  if (!i2c_on || no_i2c || !g_encode_i2c || a->ntaps <= 0 || a->ay != 1 || a->ax != 1 || a->nch % gran ||
+      a->s_sx < a->sc0 + a->nch)
+    return;
+  int dy0 = a->tap_dy[0], dx0 = a->tap_dx[0], dy1 = dy0, dx1 = dx0;
+  for (int t = 1; t < a->ntaps; ++t) {
+    dy0 = std::min<int>(dy0, a->tap_dy[t]);
+    dy1 = std::max<int>(dy1, a->tap_dy[t]);
+    dx0 = std::min<int>(dx0, a->tap_dx[t]);
+    dx1 = std::max<int>(dx1, a->tap_dx[t]);
+  }
+  // traversal box (absolute buffer coordinates of the grid's first tap): W [lw, sW-1+uw], H [lh, sH-1+uh]
+  const int lw = a->cx + dx0, lh = a->cy + dy0;
+  const int uw = lw + a->ngx - a->sW, uh = lh + a->ngy - a->sH;
+  auto in8 = [](int v) { return v >= -128 && v <= 127; };
+  if (!in8(lw) || !in8(lh) || !in8(uw) || !in8(uh) || dx1 - dx0 >= 65536 || dy1 - dy0 >= 65536) return;
+  cuuint64_t dims[4] = {(cuuint64_t)a->s_sx, (cuuint64_t)a->sW, (cuuint64_t)a->sH, (cuuint64_t)(a->sb0 + a->nb)};
+  cuuint64_t strides[3] = {(cuuint64_t)a->s_sx * 2, (cuuint64_t)a->s_sy * 2, (cuuint64_t)a->s_sb * 2};
+  int lo[2] = {lw, lh}, hi[2] = {uw, uh};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  if (g_encode_i2c(&tm[4], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(a->S), dims, strides, lo, hi, BK,
+                   (cuuint32_t)pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return;
+  a->im2col = 1;
+  a->i2c_dy0 = dy0;
+  a->i2c_dx0 = dx0;
 }
 
 extern "C" int tofu_conv_plan(tofu_conv_args* a, void* tmaps) {
@@ -862,14 +941,17 @@ extern "C" int tofu_conv_plan(tofu_conv_args* a, void* tmaps) {
                                    : tmap2(&tm[0], a->Bp, BF, 2, a->b_cols, a->b_rows, a->ldb, 64, bk, SW128);
       if (r) return TOFU_ERR_CUDA;
     }
-    tm[1] = tm[2] = tm[0];
+    tm[1] = tm[2] = tm[3] = tm[4] = tm[0];
     a->splits = 1;
+    try_im2col(a, tm, BM, BK);
     return TOFU_OK;
   }
   // kind 1: A = output gradient [K pixels][M channels] MN-major; C f32 [M][N]
   if (a->c_mode < 1 || a->c_mode > 3 || (a->lda % 8) || (a->ldc % 4)) return TOFU_ERR_ALIGN;
   if (a->c_mode == 3 && (!a->D || a->ldd % 8)) return TOFU_ERR_ARG;
   a->splits = auto_splits(a, M, N, K, bn);
+  tm[4] = tm[0];
+  try_im2col(a, tm, BK, bn);  // the N tile (bn columns) must lie within one tap
   if (tmap2(&tm[0], a->Ap, BF, 2, M, K, a->lda, 64, 64, SW128)) return TOFU_ERR_CUDA;
   if (tmap2(&tm[1], a->C, F32, 4, N, M, a->ldc, 32, 32, SW128)) return TOFU_ERR_CUDA;
   if (a->c_mode == 3) {
@@ -902,6 +984,8 @@ extern "C" int tofu_conv_launch_planned(const tofu_conv_args* a, const void* tma
   P.K = K;
   P.splits = a->splits > 1 ? a->splits : 1;
   P.sk_tiles = 0;
+  P.dy0 = a->i2c_dy0;
+  P.dx0 = a->i2c_dx0;
   const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(tmaps);
   if (a->direct) {
     int blocks = (int)(((int64_t)M * N + 255) / 256);
@@ -922,7 +1006,7 @@ extern "C" int tofu_conv_launch_planned(const tofu_conv_args* a, const void* tma
   }
   if (a->kind == 0) return dispatch(P, tm, a->c_mode, st);
   if (P.splits > 1) {
-    const CUtensorMap tw[3] = {tm[0], tm[3], tm[3]};
+    const CUtensorMap tw[5] = {tm[0], tm[3], tm[3], tm[3], tm[4]};
     int rc = dispatch(P, tw, 4, st);
     if (rc) return rc;
     int blocks = (int)(((int64_t)M * N + 255) / 256);
@@ -936,7 +1020,7 @@ extern "C" int tofu_conv_launch_planned(const tofu_conv_args* a, const void* tma
 }
 
 extern "C" int tofu_conv_bf16(const tofu_conv_args* args, void* stream) {
-  alignas(64) CUtensorMap tm[4];
+  alignas(64) CUtensorMap tm[5];
   tofu_conv_args a = *args;
   void* own_ws = nullptr;
   int r = tofu_conv_plan(&a, tm);

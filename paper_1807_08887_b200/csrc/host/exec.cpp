@@ -173,7 +173,7 @@ struct Exec {
   std::map<std::pair<int, int>, GemmLaunch> gemms;  // (op, li)
   struct ConvLaunch {
     tofu_conv_args a;
-    alignas(64) CUtensorMap tm[4];
+    alignas(64) CUtensorMap tm[5];
   };
   std::map<std::pair<int, int>, std::vector<ConvLaunch>> convs;  // (op, li) -> launches (4 phases: stride-2 dgrad)
   int64_t ledger_el = 0, ledger_bytes = 0;

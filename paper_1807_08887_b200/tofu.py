@@ -58,7 +58,7 @@ class ConvArgs(C.Structure):
                 ("ldc", C.c_int64), ("c_mode", C.c_int), ("D", C.c_void_p), ("ldd", C.c_int64),
                 ("s0", C.c_float), ("s1", C.c_float), ("splits", C.c_int), ("ws", C.c_void_p),
                 ("aux_add", C.c_void_p), ("aux_mask", C.c_void_p), ("ep", C.c_int), ("sk_ws", C.c_void_p),
-                ("direct", C.c_int)]
+                ("direct", C.c_int), ("im2col", C.c_int), ("i2c_dy0", C.c_int), ("i2c_dx0", C.c_int)]
 
 
 class Piece(C.Structure):
@@ -110,6 +110,7 @@ def lib():
             "tofu_execute_range": [vp, C.c_int, C.c_int, vp],
             "tofu_exec_time_launch": [vp, C.c_int, vp, vp],
             "tofu_transpose_taps": [vp, vp, C.c_int, C.c_int, C.c_int, vp],
+            "tofu_conv_plan": [C.POINTER(ConvArgs), vp],
         }
         for name, args in sig.items():
             f = getattr(L, name, None)
@@ -169,6 +170,15 @@ def transpose_taps(W, WT, co, taps, ci, stream=None):
 
 def sk_workspace_bytes() -> int:
     return int(lib().tofu_sk_workspace_bytes())
+
+
+def conv_plan(args: ConvArgs) -> ConvArgs:
+    """tofu_conv_plan on a copy of args (the descriptors are discarded): reports splits / direct / im2col."""
+    c = ConvArgs.from_buffer_copy(args)
+    buf = C.create_string_buffer(5 * 128 + 64)
+    ptr = (C.addressof(buf) + 63) // 64 * 64
+    check(lib().tofu_conv_plan(C.byref(c), C.c_void_p(ptr)), "tofu_conv_plan")
+    return c
 
 
 def conv(args: ConvArgs, stream=None):

@@ -134,3 +134,45 @@ def test_conv_stream_k(data, which):
         mref = M0 * mu + ref["wgrad"]
         assert nrm(got, mref) <= 1e-5
         assert nrm(outs[0][1], np.asarray(torch.from_numpy(W0 - got * lr).to(torch.bfloat16).double())) <= 5e-3
+
+
+@pytest.mark.parametrize("which", ["fwd", "fwd_ep", "dgrad", "wgrad", "wgrad_opt"])
+def test_conv_im2col_equals_gather(data, which):
+    """The activation operand loaded by TMA in im2col mode (tofu_conv_args.im2col; the A operand of the forward
+    / data gradient, the B operand of the weight gradient) vs the cp.async gather warps: the same operand tiles
+    reach the tensor cores, so the outputs are bitwise equal; both within tolerance of the fp64 convolution."""
+    t = _tofu()
+    rng, X, W, D, ref = data
+    Xd, Wd, Dd = cuda_bf16(X), cuda_bf16(W), cuda_bf16(D)
+    add, mask = q(rng, (B, H, H, C), 2 ** -6), q(rng, (B, H, H, C), 2 ** -6)
+    keep = [cuda_bf16(add), cuda_bf16(mask)]
+    outs, modes = [], []
+    M0, W0 = q(rng, (C, 3, 3, C), 2 ** -12), q(rng, (C, 3, 3, C), 2 ** -7)
+    for i2c in (-1, 0):
+        if which.startswith("wgrad"):   # kind 1: the gathered activations are the B operand
+            out = (torch.from_numpy(M0).float().cuda() if which == "wgrad_opt"
+                   else torch.zeros((C, 3, 3, C), dtype=torch.float32, device="cuda"))
+            a = conv_args(t, 1, Xd, out, Y=Dd)
+            if which == "wgrad_opt":
+                keep = [cuda_bf16(W0)]
+                a.c_mode, a.D, a.ldd, a.s0, a.s1 = 3, keep[0].data_ptr(), 9 * C, 0.875, 0.0078125
+        else:
+            out = torch.zeros((B, H, H, C), dtype=torch.bfloat16, device="cuda")
+            a = (conv_args(t, 0, Xd, out, Wd, 0) if which != "dgrad" else conv_args(t, 0, Dd, out, Wd, 1, flip=True))
+            if which == "fwd_ep":
+                a.ep, a.aux_add, a.aux_mask = 7, keep[0].data_ptr(), keep[1].data_ptr()
+        a.im2col = i2c
+        modes.append(t.conv_plan(a).im2col)
+        t.conv(a)
+        torch.cuda.synchronize()
+        outs.append(out.double().cpu().numpy())
+    assert modes == [0, 1]
+    assert np.array_equal(outs[0], outs[1])
+    if which.startswith("wgrad"):
+        r = ref["wgrad"] + (M0 * 0.875 if which == "wgrad_opt" else 0.0)
+        assert nrm(outs[1], r) <= 1e-5
+        return
+    r = ref["dgrad" if which == "dgrad" else "fwd"]
+    if which == "fwd_ep":
+        r = np.where(mask > 0, np.maximum(r + add, 0.0), 0.0)
+    assert nrm(outs[1], r) <= 5e-3
