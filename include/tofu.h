@@ -332,7 +332,10 @@ int tofu_pieces_run(const tofu_piece* pieces_dev, int n, int64_t max_elems, void
  *   TOFU_EW_SGD       y = x0 - x1 * s0                    (bf16, f32 -> bf16)
  *   TOFU_EW_SGD_MOM   fused: m' = m*s0 + g; w' = w - m'*s1; x0 = m (f32, in/out), x1 = g (f32),
  *                     x2 = w (bf16, in/out); y unused
- *   TOFU_EW_SUMSQ     y[0] (f32, accumulated with atomicAdd) += Σ (x0 - x1)^2 * s0  (bf16, bf16)
+ *   TOFU_EW_SUMSQ     y[0] (f32) += Σ (x0 - x1)^2 * s0  (bf16, bf16; per-block partials summed in block order
+ *                     by the last block: deterministic; one such launch at a time per device)
+ *   TOFU_EW_SUMSQ_MSE_GRAD  the loss and its gradient in one pass (P:L674-678 coalesced element-wise ops,
+ *                     DESIGN R8): y[0] += Σ (x0 - x1)^2 * s0 as TOFU_EW_SUMSQ, and x2 (bf16) = (x0 - x1) * s1
  *   TOFU_EW_ADD       y = x0 + x1                         (bf16, bf16 -> bf16; gradient sums)
  *   TOFU_EW_ADDRELU   y = max(x0 + x1, 0)                 (bf16, bf16 -> bf16; residual join)
  */
@@ -345,6 +348,7 @@ int tofu_pieces_run(const tofu_piece* pieces_dev, int n, int64_t max_elems, void
 #define TOFU_EW_SUMSQ 6
 #define TOFU_EW_ADD 7
 #define TOFU_EW_ADDRELU 8
+#define TOFU_EW_SUMSQ_MSE_GRAD 9
 int tofu_elementwise(int kind, int64_t n, void* y_dev, const void* x0_dev, const void* x1_dev, void* x2_dev,
                      float s0, float s1, void* stream);
 

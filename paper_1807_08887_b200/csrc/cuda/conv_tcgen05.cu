@@ -168,8 +168,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if constexpr (I2C) {
           const int gb = m0 / ngyx, rem = m0 - gb * ngyx;
           const int gy = rem / a.ngx, gx = rem - gy * a.ngx;
-          ih = gy + a.cy + P.dy0;
-          iw = gx + a.cx + P.dx0;
+          ih = a.ay * gy + a.cy + P.dy0;
+          iw = a.ax * gx + a.cx + P.dx0;
           in_ = gb + a.sb0;
         }
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
               for (int q = 0; q < BN / 64; ++q)
                 tma_load_im2col_4d(sB + s * C_::B_BYTES + q * 8192, &tmI, &full[s], a.sc0 + c + 64 * q,
-                                   gx + a.cx + P.dx0, gy + a.cy + P.dy0, gb + a.sb0, ow, oh);
+                                   a.ax * gx + a.cx + P.dx0, a.ay * gy + a.cy + P.dy0, gb + a.sb0, ow, oh);
             }
           }
         }
@@ -859,7 +859,7 @@ static bool natural_taps(const tofu_conv_args* a) {
   return true;
 }
 
-// im2col TMA for the gathered activations (tmaps[4]): stride-1 grids, whole 64-channel blocks (kind 0: per
+// im2col TMA for the gathered activations (tmaps[4]): grids of stride <= 8, whole 64-channel blocks (kind 0: per
 // tap; kind 1: the N tile of `gran` columns within one tap), corners and tap offsets within the encodable
 // ranges.  pixels = the box's pixel count (kind 0: BM output pixels; kind 1: BK pixels of a k-block).
 // TOFU_I2C=0 (or im2col = -1 on entry) keeps the gather warps.
@@ -871,8 +871,9 @@ static void try_im2col(tofu_conv_args* a, CUtensorMap* tm, int pixels, int gran)
   const bool no_i2c = a->im2col == -1;
   a->im2col = 0;
   a->i2c_dy0 = a->i2c_dx0 = 0;
-  if (!i2c_on || no_i2c || !g_encode_i2c || a->ntaps <= 0 || a->ay != 1 || a->ax != 1 || a->nch % gran ||
-      a->s_sx < a->sc0 + a->nch)
+  // grid strides (stride-2 forward / weight gradient) become the map's traversal strides (elementStrides)
+  if (!i2c_on || no_i2c || !g_encode_i2c || a->ntaps <= 0 || a->ay < 1 || a->ay > 8 || a->ax < 1 || a->ax > 8 ||
+      a->nch % gran || a->s_sx < a->sc0 + a->nch)
     return;
   int dy0 = a->tap_dy[0], dx0 = a->tap_dx[0], dy1 = dy0, dx1 = dx0;
   for (int t = 1; t < a->ntaps; ++t) {
@@ -881,15 +882,16 @@ static void try_im2col(tofu_conv_args* a, CUtensorMap* tm, int pixels, int gran)
     dx0 = std::min<int>(dx0, a->tap_dx[t]);
     dx1 = std::max<int>(dx1, a->tap_dx[t]);
   }
-  // traversal box (absolute buffer coordinates of the grid's first tap): W [lw, sW-1+uw], H [lh, sH-1+uh]
+  // traversal box (absolute buffer coordinates of the grid's first tap): W [lw, sW-1+uw], H [lh, sH-1+uh],
+  // walked with steps ax / ay from the grid's first to its last pixel
   const int lw = a->cx + dx0, lh = a->cy + dy0;
-  const int uw = lw + a->ngx - a->sW, uh = lh + a->ngy - a->sH;
+  const int uw = lw + a->ax * (a->ngx - 1) - (a->sW - 1), uh = lh + a->ay * (a->ngy - 1) - (a->sH - 1);
   auto in8 = [](int v) { return v >= -128 && v <= 127; };
   if (!in8(lw) || !in8(lh) || !in8(uw) || !in8(uh) || dx1 - dx0 >= 65536 || dy1 - dy0 >= 65536) return;
   cuuint64_t dims[4] = {(cuuint64_t)a->s_sx, (cuuint64_t)a->sW, (cuuint64_t)a->sH, (cuuint64_t)(a->sb0 + a->nb)};
   cuuint64_t strides[3] = {(cuuint64_t)a->s_sx * 2, (cuuint64_t)a->s_sy * 2, (cuuint64_t)a->s_sb * 2};
   int lo[2] = {lw, lh}, hi[2] = {uw, uh};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
+  cuuint32_t estr[4] = {1, (cuuint32_t)a->ax, (cuuint32_t)a->ay, 1};
   if (g_encode_i2c(&tm[4], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(a->S), dims, strides, lo, hi, BK,
                    (cuuint32_t)pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)

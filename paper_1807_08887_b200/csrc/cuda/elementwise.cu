@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(256) ew_kernel(int64_t n, void* __restrict__ y
     const int64_t i = v * 8;
     float a[8], b[8], o[8];
     if (KIND == TOFU_EW_RELU || KIND == TOFU_EW_RELU_GRAD || KIND == TOFU_EW_MSE_GRAD || KIND == TOFU_EW_SUMSQ ||
-        KIND == TOFU_EW_ADD || KIND == TOFU_EW_ADDRELU) {
+        KIND == TOFU_EW_ADD || KIND == TOFU_EW_ADDRELU || KIND == TOFU_EW_SUMSQ_MSE_GRAD) {
       unpack8(reinterpret_cast<const uint4*>(x0)[v], a);
       if (KIND != TOFU_EW_RELU) unpack8(reinterpret_cast<const uint4*>(x1)[v], b);
 #pragma unroll
@@ -51,11 +51,13 @@ __global__ void __launch_bounds__(256) ew_kernel(int64_t n, void* __restrict__ y
         if (KIND == TOFU_EW_RELU) o[j] = fmaxf(a[j], 0.f);
         if (KIND == TOFU_EW_RELU_GRAD) o[j] = a[j] > 0.f ? b[j] : 0.f;
         if (KIND == TOFU_EW_MSE_GRAD) o[j] = (a[j] - b[j]) * s0;
-        if (KIND == TOFU_EW_SUMSQ) { const float d = a[j] - b[j]; local += d * d * s0; }
+        if (KIND == TOFU_EW_SUMSQ || KIND == TOFU_EW_SUMSQ_MSE_GRAD) { const float d = a[j] - b[j]; local += d * d * s0; }
+        if (KIND == TOFU_EW_SUMSQ_MSE_GRAD) o[j] = (a[j] - b[j]) * s1;
         if (KIND == TOFU_EW_ADD) o[j] = a[j] + b[j];
         if (KIND == TOFU_EW_ADDRELU) o[j] = fmaxf(a[j] + b[j], 0.f);
       }
-      if (KIND != TOFU_EW_SUMSQ) reinterpret_cast<uint4*>(y)[v] = pack8(o);
+      if (KIND == TOFU_EW_SUMSQ_MSE_GRAD) reinterpret_cast<uint4*>(x2)[v] = pack8(o);
+      else if (KIND != TOFU_EW_SUMSQ) reinterpret_cast<uint4*>(y)[v] = pack8(o);
     } else if (KIND == TOFU_EW_MOM) {
       const float4* m = reinterpret_cast<const float4*>(x0) + 2 * v;
       const float4* g = reinterpret_cast<const float4*>(x1) + 2 * v;
@@ -100,7 +102,11 @@ __global__ void __launch_bounds__(256) ew_kernel(int64_t n, void* __restrict__ y
         reinterpret_cast<__nv_bfloat16*>(y)[i] = __bfloat162float(xb0[i]) > 0.f ? xb1[i] : __float2bfloat16_rn(0.f);
       if (KIND == TOFU_EW_MSE_GRAD)
         reinterpret_cast<__nv_bfloat16*>(y)[i] = __float2bfloat16_rn((__bfloat162float(xb0[i]) - __bfloat162float(xb1[i])) * s0);
-      if (KIND == TOFU_EW_SUMSQ) { const float d = __bfloat162float(xb0[i]) - __bfloat162float(xb1[i]); local += d * d * s0; }
+      if (KIND == TOFU_EW_SUMSQ || KIND == TOFU_EW_SUMSQ_MSE_GRAD) {
+        const float d = __bfloat162float(xb0[i]) - __bfloat162float(xb1[i]);
+        local += d * d * s0;
+        if (KIND == TOFU_EW_SUMSQ_MSE_GRAD) reinterpret_cast<__nv_bfloat16*>(x2)[i] = __float2bfloat16_rn(d * s1);
+      }
       if (KIND == TOFU_EW_ADD)
         reinterpret_cast<__nv_bfloat16*>(y)[i] = __float2bfloat16_rn(__bfloat162float(xb0[i]) + __bfloat162float(xb1[i]));
       if (KIND == TOFU_EW_ADDRELU)
@@ -119,7 +125,7 @@ __global__ void __launch_bounds__(256) ew_kernel(int64_t n, void* __restrict__ y
       }
     }
   }
-  if (KIND == TOFU_EW_SUMSQ) {
+  if (KIND == TOFU_EW_SUMSQ || KIND == TOFU_EW_SUMSQ_MSE_GRAD) {
     // deterministic: per-block partials, summed in block order by the last block to finish (no float atomics,
     // so a loss is bitwise reproducible run to run and across executors)
     __shared__ float red[8];
@@ -175,7 +181,7 @@ extern "C" int tofu_elementwise(int kind, int64_t n, void* y, const void* x0, co
   switch (kind) {
 #define K(X) case X: tofu::ew_kernel<X><<<(unsigned)grid, 256, 0, st>>>(n, y, x0, x1, x2, s0, s1); break;
     K(TOFU_EW_RELU) K(TOFU_EW_RELU_GRAD) K(TOFU_EW_MSE_GRAD) K(TOFU_EW_MOM) K(TOFU_EW_SGD) K(TOFU_EW_SGD_MOM)
-    K(TOFU_EW_SUMSQ) K(TOFU_EW_ADD) K(TOFU_EW_ADDRELU)
+    K(TOFU_EW_SUMSQ) K(TOFU_EW_ADD) K(TOFU_EW_ADDRELU) K(TOFU_EW_SUMSQ_MSE_GRAD)
 #undef K
     default: return TOFU_ERR_ARG;
   }

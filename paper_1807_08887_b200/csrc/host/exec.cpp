@@ -105,6 +105,7 @@ struct LOp {
   int fused_opt = -1;         // GEMM epilogue absorbs mom (this index) + sgd (index + 1)
   int64_t wt_off = -1;        // conv data gradient: arena offset of the transposed weight shard (K-major B)
   bool fused_next = false;    // LSTM cell: this launch also computes the next op (c+h, bwd_a+bwd_c)
+  bool fused_loss_grad = false;  // sumsq: this launch also computes the next op, mse_grad of the same inputs
   int ep = 0;                 // element-wise epilogue of the output's consumers: 1 relu, 2 add, 4 mask
   Buf epi_add, epi_mask;      // its bf16 operands (the output's layout)
   std::vector<tofu_piece> fetch, reduce;
@@ -728,6 +729,23 @@ void lower(Exec& E) {
           for (int q = 0; q < 4; ++q) ok &= same_buf(La.in[3 + q], Lb.in[2 + q]);  // C, DU, DR, DN
         if (!ok) continue;
         La.fused_next = true;
+        Lb.skip = true;
+      }
+  // The loss and its gradient read the same (Y, T) shards: one pass computes both (sumsq + mse_grad, R8)
+  if (E.fuse)
+    for (int r = 0; r < k; ++r)
+      for (size_t o = 0; o + 1 < g.ops.size(); ++o) {
+        if (g.defs[g.ops[o].def].name != "sumsq" || g.defs[g.ops[o + 1].def].name != "mse_grad") continue;
+        if (g.ops[o].inputs != g.ops[o + 1].inputs) continue;
+        LOp &La = all[r][o], &Lb = all[r][o + 1];
+        if (La.skip || Lb.skip || !Lb.out.direct || !Lb.fetch.empty() || !Lb.reduce.empty() || !La.fetch.empty())
+          continue;
+        auto same_buf = [](const Buf& x, const Buf& y) {
+          return x.direct && y.direct && x.off == y.off && same(x.box, y.box) && same(x.buf_box, y.buf_box);
+        };
+        if (!same_buf(La.in[0], Lb.in[0]) || !same_buf(La.in[1], Lb.in[1]) || !same(Lb.out.box, Lb.in[0].box))
+          continue;
+        La.fused_loss_grad = true;
         Lb.skip = true;
       }
   // Element-wise consumers folded into their producer's epilogue (R8/R13): a GEMM / convolution whose bf16
@@ -1496,6 +1514,12 @@ int run_compute(Exec& E, int o, int li, cudaStream_t st) {
   if (dn == "mse_grad") return tofu_elementwise(TOFU_EW_MSE_GRAD, n, y, x0, x1, nullptr, attr("scale", 1), 0, st);
   if (dn == "sumsq") {
     const int64_t m = vol(L.in[0].box);
+    if (L.fused_loss_grad) {  // + the next op (mse_grad of the same inputs) in the same pass
+      const LOp& Ln = E.lops[li][o + 1];
+      auto it = g.ops[o + 1].attrs.find("scale");
+      const float s1 = (float)(it == g.ops[o + 1].attrs.end() ? 1.0 : it->second);
+      return tofu_elementwise(TOFU_EW_SUMSQ_MSE_GRAD, m, y, x0, x1, base + Ln.out.off, attr("scale", 1), s1, st);
+    }
     return tofu_elementwise(TOFU_EW_SUMSQ, m, y, x0, x1, nullptr, attr("scale", 1), 0, st);
   }
   if (is_mom(dn)) {
@@ -1694,6 +1718,7 @@ std::string launch_desc(const Exec& E, int i) {
       if (lo.fused_sgd) bytes += n * (4 + 2);  // m and w written back
       else if (dn != "sumsq") bytes += n * (lo.out.dtype == TOFU_BF16 ? 2 : 4);
       if (lo.fused_sgd) bytes += n * 2;       // w read
+      if (lo.fused_loss_grad) bytes += n * 2;  // the loss gradient written (bf16)
     }
     bytes += (double)vol(lo.out.box) * 2 * (((lo.ep >> 1) & 1) + ((lo.ep >> 2) & 1));  // epilogue operands
   }
@@ -1701,6 +1726,7 @@ std::string launch_desc(const Exec& E, int i) {
   if (L.kind == 1 && lo_fused(E, L)) o += ",\"fused\":\"mom+sgd\"";
   if (L.kind == 1 && E.lops[L.li][L.op].fused_opt >= 0) o += ",\"fused\":\"gemm+mom+sgd\"";
   if (L.kind == 1 && E.lops[L.li][L.op].fused_next) o += ",\"fused\":\"lstm-cell-pair\"";
+  if (L.kind == 1 && E.lops[L.li][L.op].fused_loss_grad) o += ",\"fused\":\"loss+loss_grad\"";
   if (L.kind == 1 && E.lops[L.li][L.op].wt_off >= 0) o += ",\"weights\":\"transposed\"";
   if (L.kind == 1) {
     int np = 0;

@@ -176,3 +176,73 @@ def test_conv_im2col_equals_gather(data, which):
     if which == "fwd_ep":
         r = np.where(mask > 0, np.maximum(r + add, 0.0), 0.0)
     assert nrm(outs[1], r) <= 5e-3
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_conv_im2col_stride2(kind):
+    """Stride-2 3x3 convolution (pad 1, the stage transitions of WResNet): the im2col map walks the input with
+    traversal stride 2 (elementStrides) — forward (kind 0) and weight gradient (kind 1), bitwise equal to the
+    gather path and within tolerance of the fp64 convolution."""
+    t = _tofu()
+    Bs, Hs, Cs = 8, 28, 256
+    Ho = Hs // 2
+    rng = np.random.default_rng(57)
+    X = q(rng, (Bs, Hs, Hs, Cs), 2 ** -7)
+    W = q(rng, (Cs, 3, 3, Cs), 2 ** -10)
+    D = q(rng, (Bs, Ho, Ho, Cs), 2 ** -7)
+    F = torch.nn.functional
+    Xt, Wt, Dt = (torch.from_numpy(v) for v in (X, W, D))
+    Xd, Wd, Dd = cuda_bf16(X), cuda_bf16(W), cuda_bf16(D)
+
+    def args(out):
+        a = t.ConvArgs()
+        a.kind = kind
+        a.nb, a.ngy, a.ngx = Bs, Ho, Ho
+        a.ay = a.ax = 2
+        a.cy = a.cx = -1
+        a.ntaps = 9
+        for k in range(9):
+            a.tap_dy[k], a.tap_dx[k] = divmod(k, 3)
+            a.tap_w[k] = k
+        a.nch = Cs
+        a.S = Xd.data_ptr()
+        a.s_sb, a.s_sy, a.s_sx = Hs * Hs * Cs, Hs * Cs, Cs
+        a.sH = a.sW = Hs
+        if kind == 0:
+            a.n_out = Cs
+            a.Bp = Wd.data_ptr()
+            a.ldb = 9 * Cs
+            a.b_tap = Cs
+            a.b_rows, a.b_cols = Cs, 9 * Cs
+            a.C = out.data_ptr()
+            a.c_sb, a.c_sy, a.c_sx = Ho * Ho * Cs, Ho * Cs, Cs
+            a.c_ys = a.c_xs = 1
+        else:
+            a.m_out = Cs
+            a.Ap = Dd.data_ptr()
+            a.lda = Cs
+            a.C = out.data_ptr()
+            a.ldc = 9 * Cs
+            a.c_mode = 1
+            a.splits = 1
+        return a
+
+    outs, modes = [], []
+    for i2c in (-1, 0):
+        out = (torch.zeros((Bs, Ho, Ho, Cs), dtype=torch.bfloat16, device="cuda") if kind == 0
+               else torch.zeros((Cs, 3, 3, Cs), dtype=torch.float32, device="cuda"))
+        a = args(out)
+        a.im2col = i2c
+        modes.append(t.conv_plan(a).im2col)
+        t.conv(a)
+        torch.cuda.synchronize()
+        outs.append(out.double().cpu().numpy())
+    assert modes == [0, 1]
+    assert np.array_equal(outs[0], outs[1])
+    if kind == 0:
+        ref = F.conv2d(Xt.permute(0, 3, 1, 2), Wt.permute(0, 3, 1, 2), stride=2, padding=1).permute(0, 2, 3, 1).numpy()
+        assert nrm(outs[1], ref) <= 5e-3
+    else:
+        ref = torch.nn.grad.conv2d_weight(Xt.permute(0, 3, 1, 2), (Cs, Cs, 3, 3), Dt.permute(0, 3, 1, 2), stride=2,
+                                          padding=1).permute(0, 2, 3, 1).numpy()
+        assert nrm(outs[1], ref) <= 1e-5

@@ -22,4 +22,12 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm
   -o $O/full_c3_gemm python tools/breakdown.py units 2 4 32 224 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:conv_kernel -s 3 -c 4 \
   -o $O/full_c3_conv python tools/breakdown.py units 0,0,3 4 32 112 > /dev/null 2>&1
+# export the judged metrics as CSV + markdown summaries and drop the large reports (gpurun copies back <= 64 MiB)
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active,sm__throughput.avg.pct_of_peak_sustained_elapsed,launch__grid_size,launch__block_size,launch__registers_per_thread,launch__shared_mem_per_block_dynamic,l1tex__throughput.avg.pct_of_peak_sustained_active,lts__t_bytes.sum
+for f in full_c1 full_c3_gemm full_c3_conv; do
+  ncu -i $O/$f.ncu-rep --page raw --csv --metrics $M > $O/ncu_$f.csv 2>/dev/null
+  python tools/ncu_summary.py $O/$f.ncu-rep > $O/ncu_$f.md 2>&1
+done
+rm -f $O/full_c3_gemm.ncu-rep $O/full_c3_conv.ncu-rep
 ls -la $O
+du -sh $O
