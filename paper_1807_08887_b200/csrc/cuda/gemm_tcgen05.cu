@@ -522,6 +522,30 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
                                                             void* C, int ldc, int mode, __nv_bfloat16* D, int ldd,
                                                             float s0, float s1) {
   const int64_t plane = (int64_t)M * N;
+  if (mode == 3 && N % 4 == 0 && ldc % 4 == 0 && ldd % 4 == 0 && !(reinterpret_cast<uintptr_t>(C) & 15) &&
+      !(reinterpret_cast<uintptr_t>(D) & 7)) {  // vectorised: 4 elements (float4 momentum, 4 bf16 weights)
+    const int64_t n4 = plane / 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+      float4 acc = reinterpret_cast<const float4*>(ws)[i];
+      for (int s = 1; s < splits; ++s) {
+        const float4 v = reinterpret_cast<const float4*>(ws + s * plane)[i];
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+      const int64_t m = (i * 4) / N, n = (i * 4) % N;
+      float4* c = reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + m * ldc + n);
+      const float4 o = *c;
+      const float4 mm = make_float4(o.x * s0 + acc.x, o.y * s0 + acc.y, o.z * s0 + acc.z, o.w * s0 + acc.w);
+      *c = mm;
+      uint2* w = reinterpret_cast<uint2*>(D + m * ldd + n);
+      uint2 wv = *w;
+      __nv_bfloat162* wh = reinterpret_cast<__nv_bfloat162*>(&wv);
+      const float2 w0 = __bfloat1622float2(wh[0]), w1 = __bfloat1622float2(wh[1]);
+      wh[0] = __floats2bfloat162_rn(w0.x - mm.x * s1, w0.y - mm.y * s1);
+      wh[1] = __floats2bfloat162_rn(w1.x - mm.z * s1, w1.y - mm.w * s1);
+      *w = wv;
+    }
+    return;
+  }
   if (mode == 3) {  // fused momentum-SGD on the reduced weight gradient (c_mode 3 with split-K)
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < plane; i += (int64_t)gridDim.x * blockDim.x) {
       float acc = ws[i];

@@ -1427,6 +1427,29 @@ int run_window(Exec& E, int o, int li, cudaStream_t st) {
   return tofu_gap_grad(&a, st);
 }
 
+// CUDA kernels one compute launch issues (split-K reductions, weight transposes and convolution phases included)
+int64_t kernels_of(const Exec& E, int o, int li) {
+  const std::string kind = kernel_kind(E.g->def_of(o));
+  auto gemm_k = [](const tofu_gemm_args& a) -> int64_t {
+    return a.M == 0 || a.N == 0 || a.K == 0 ? 0 : 1 + (a.splits > 1 ? 1 : 0);
+  };
+  if (kind == "gemm") return gemm_k(E.gemms.at({o, li}).a);
+  if (kind == "conv") {
+    auto git = E.gemms.find({o, li});
+    if (git != E.gemms.end()) return gemm_k(git->second.a);
+    int64_t n = E.lops[li][o].wt_off >= 0 ? 1 : 0;
+    for (auto& C : E.convs.at({o, li})) {
+      const auto& a = C.a;
+      const int64_t pix = (int64_t)a.nb * a.ngy * a.ngx;
+      const int64_t M = a.kind == 0 ? pix : a.m_out, N = a.kind == 0 ? a.n_out : (int64_t)a.ntaps * a.nch;
+      if (M == 0 || N == 0) continue;
+      n += 1 + (a.kind == 1 && a.splits > 1 && !a.direct ? 1 : 0);
+    }
+    return n;
+  }
+  return 1;
+}
+
 int run_compute(Exec& E, int o, int li, cudaStream_t st) {
   const Graph& g = *E.g;
   const int r = E.local[li];
@@ -1789,14 +1812,18 @@ extern "C" int tofu_exec_ledger(const tofu_exec* h, int64_t* elements, int64_t* 
 
 extern "C" int tofu_exec_launch_count(const tofu_exec* h, int64_t* launches) {
   if (!h || !launches) return tofu::fail(TOFU_ERR_ARG, "null argument");
-  int64_t n = 0;
-  for (auto& L : h->e.launches) {
-    if (L.kind == 4) continue;
-    if (h->e.skip_comm && (L.kind == 0 || L.kind == 2 || L.kind == 3)) continue;
-    ++n;
-  }
-  *launches = n;
-  return TOFU_OK;
+  return tofu::guard([&]() {
+    tofu::Exec& E = const_cast<tofu_exec*>(h)->e;
+    tofu::finalize(E);  // (descriptors decide the kernels per compute launch)
+    int64_t n = 0;
+    for (auto& L : E.launches) {
+      if (L.kind == 4) continue;  // cudaMemsetAsync, not a kernel of ours
+      if (E.skip_comm && (L.kind == 0 || L.kind == 2 || L.kind == 3)) continue;
+      n += L.kind == 1 ? tofu::kernels_of(E, L.op, L.li) : 1;
+    }
+    *launches = n;
+    return TOFU_OK;
+  });
 }
 
 extern "C" int tofu_exec_set_skip_comm(tofu_exec* h, int skip) {

@@ -72,9 +72,11 @@ def test_gemm_parity(defname, M, N, K, c_mode):
 
 
 @pytest.mark.parametrize("defname", ["mm_tn", "mm_nn"])
-@pytest.mark.parametrize("M,N,K", [(256, 512, 128), (200, 328, 72), (1024, 2048, 512)])
-def test_gemm_fused_momentum_sgd(defname, M, N, K):
-    """c_mode 3: M = M*mu + A.B (fp32, 1e-5), W = bf16(W - lr*M) (5e-3)."""
+@pytest.mark.parametrize("M,N,K,splits", [(256, 512, 128, 0), (200, 328, 72, 0), (1024, 2048, 512, 0),
+                                          (256, 512, 2048, 4), (200, 328, 1000, 3)])
+def test_gemm_fused_momentum_sgd(defname, M, N, K, splits):
+    """c_mode 3: M = M*mu + A.B (fp32, 1e-5), W = bf16(W - lr*M) (5e-3); with split-K the optimizer is
+    applied by the ordered reduction (vectorised when N is a multiple of 4, scalar otherwise)."""
     t = _tofu()
     am, bm = DEF_MAJOR[defname]
     rng = np.random.default_rng(M + N + K)
@@ -88,7 +90,8 @@ def test_gemm_fused_momentum_sgd(defname, M, N, K):
     Md = torch.from_numpy(M0).float().cuda()
     Wd = cuda_bf16(W0)
     mu, lr = 0.875, 0.0078125
-    t.gemm(cuda_bf16(A), cuda_bf16(B), Md, M, N, K, a_shape[1], am, b_shape[1], bm, N, 3, D=Wd, ldd=N, s0=mu, s1=lr)
+    t.gemm(cuda_bf16(A), cuda_bf16(B), Md, M, N, K, a_shape[1], am, b_shape[1], bm, N, 3, D=Wd, ldd=N, s0=mu, s1=lr,
+           splits=splits)
     torch.cuda.synchronize()
     mref = M0 * mu + acc
     got_m = Md.double().cpu().numpy()
