@@ -44,3 +44,22 @@ def test_two_process_step_equals_virtual(tmp_path):
         for t, (box, arr) in res[r]["shards"].items():
             ref = R.view(r, t).float().cpu().numpy()
             assert np.array_equal(arr, ref), (r, t)
+
+
+def test_bench_two_ranks_shared_gpu(tmp_path):
+    """bench.py at N = 2 under torchrun (one process per rank; on a 1-GPU box both ranks share the device
+    and the host collectives go over gloo, config.shared_gpu): the whole multi-process bench path runs to
+    its JSON line with the byte ledger equal to the plan.  Regression test for a hang: every step holds
+    device barriers across ranks, so all ranks must run the same number of steps (the clock-soak loop)."""
+    import json
+    root = os.path.dirname(HERE)
+    port = str(29700 + os.getpid() % 200)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", port, os.path.join(root, "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "3"]
+    p = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=400)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = json.loads([l for l in p.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["bytes_vs_plan"]["equal"]
+    assert line["config"]["parallelism"] == "tofu-k2"
+    assert line["value"] > 0 and line["gpu_launches"] > 0
