@@ -182,6 +182,10 @@ typedef struct {
   /* optional piecewise operands (NULL = A / B as given above): see tofu_operand_pieces */
   const tofu_operand_pieces* a_pieces;
   const tofu_operand_pieces* b_pieces;
+  /* set by tofu_gemm_plan_tmaps: 1 = launched as clusters of 2 CTAs on vertically adjacent tiles that
+   * share (TMA-multicast) the B tile; on entry -1 forbids it, 2 requests it where eligible (parity tests),
+   * 0 = automatic */
+  int cl2;
 } tofu_gemm_args;
 int tofu_gemm_bf16(const tofu_gemm_args* args, void* stream);
 /* Split form used by the executor: encode the TMA descriptors (A, B, C, D, workspace, mask, then the

@@ -140,6 +140,43 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+// commit arriving on the barrier at this smem offset in every CTA of ctaMask (cluster multicast)
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+// ---------------------------------------------------------------- clusters
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t nclusters_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 2-D TMA load multicast to every CTA of ctaMask (same smem offset, each CTA's barrier at `bar`'s offset)
+__device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const void* tmap, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+
 // 32 lanes x 32 columns of 32-bit: thread t of the warp gets lane (base+t), columns [c, c+32)
 __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -191,6 +228,22 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N, int a_mn_ma
 struct WorkList {
   int nk, splits, grid, cta, sk_tile0, n_dp, n_sk, t0;
   int64_t sk_iters, lo, hi;
+  // cluster pairs (gemm_tcgen05.cu CL2): the two CTAs of a cluster take vertically adjacent tiles (m tiles 2p,
+  // 2p+1) of the same n tile, so they share (multicast) the B tile; pair units round-robin over the clusters
+  int pairs = 0, tiles_n = 1, rank = 0;
+  __device__ __forceinline__ void init_pairs(int tiles_m, int tiles_n_, int nk_, int rank_, int cid, int ncl) {
+    nk = nk_;
+    splits = 1;
+    pairs = 1;
+    tiles_n = tiles_n_;
+    rank = rank_;
+    grid = ncl;
+    cta = cid;
+    const int units = ((tiles_m + 1) / 2) * tiles_n;
+    n_dp = cid < units ? (units - cid + ncl - 1) / ncl : 0;
+    n_sk = 0;
+    sk_tile0 = 0;
+  }
   __device__ __forceinline__ void init(int ntiles, int nk_, int splits_, int sk_tiles) {
     nk = nk_;
     splits = splits_;
@@ -210,6 +263,14 @@ struct WorkList {
   // segment i: tile, k-blocks [kb0, kb1), split plane; partial = a leading piece of a cut tile (writes its
   // fp32 partial to the workspace instead of the epilogue's store)
   __device__ __forceinline__ void seg(int i, int& tile, int& kb0, int& kb1, int& split, bool& partial) const {
+    if (pairs) {
+      const int u = cta + i * grid, mp = u / tiles_n;
+      tile = (2 * mp + rank) * tiles_n + (u - mp * tiles_n);
+      split = kb0 = 0;
+      kb1 = nk;
+      partial = false;
+      return;
+    }
     if (i < n_dp) {
       const int u = cta + i * grid;
       partial = false;
@@ -236,6 +297,7 @@ struct WorkList {
   }
   // finisher of stream-K tile `tile` (the segment holding k-block 0): contributors are CTAs cta+1 .. last-1
   __device__ __forceinline__ int contrib_end(int tile) const {
+    if (pairs) return 0;  // (no stream-K pieces; callers loop from blockIdx.x + 1)
     if (tile < sk_tile0) return cta + 1;
     const int64_t te = (int64_t)(tile - sk_tile0 + 1) * nk;
     int c = cta + 1;

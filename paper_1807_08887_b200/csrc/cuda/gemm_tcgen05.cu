@@ -91,7 +91,10 @@ __device__ __forceinline__ const CUtensorMap* piece_of(const CUtensorMap* maps, 
   return maps + i;
 }
 
-template <int BN, bool A_MN, bool B_MN, int MODE_, bool PC>
+// CL2: cluster of 2 CTAs on vertically adjacent tiles (m tiles 2p, 2p+1) of the same n tile; each CTA
+// TMA-loads half of the shared B tile and multicasts it to both (halving B's L2 -> SM traffic per flop), and
+// frees a stage only when both CTAs' MMAs have consumed it (the MMA commit arrives on both CTAs' barriers).
+template <int BN, bool A_MN, bool B_MN, int MODE_, bool PC, bool CL2 = false>
 __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ std::conditional_t<PC, PieceMaps, NoPieces> pm,
                      const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -122,13 +125,19 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
   const int nk = (K + BK - 1) / BK;
   // segments = (output tile, k-block range): data-parallel units (tile, K split) then stream-K pieces
   WorkList wl;
-  wl.init(ntiles, nk, splits, sk_tiles);
+  uint32_t crank = 0;
+  if constexpr (CL2) {
+    crank = cluster_rank();
+    wl.init_pairs(tiles_m, tiles_n, nk, (int)crank, (int)cluster_id_x(), (int)nclusters_x());
+  } else {
+    wl.init(ntiles, nk, splits, sk_tiles);
+  }
   const int nseg = wl.count();
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL2 ? 2 : 1);  // CL2: both CTAs' MMAs must have read the stage
     }
     for (int b = 0; b < Cfg::ACC_BUFS; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -144,7 +153,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
   }
   if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CL2) cluster_sync_all();  // the peer's barriers are initialised before any multicast
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -181,7 +191,17 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
 #pragma unroll
             for (int c = 0; c < BM / 64; ++c) tma_load_2d(a + c * 8192, ma, &full[s], am + 64 * c, ak);
           }
-          if (!B_MN) {
+          if constexpr (CL2) {  // this CTA's half of B, multicast into both CTAs' stage
+            if (!B_MN) {
+              tma_load_2d_mc(b + crank * (Cfg::B_BYTES / 2), mb, &full[s], bk, bnn + (int)crank * (BN / 2), 0x3);
+            } else {
+#pragma unroll
+              for (int c = 0; c < BN / 128; ++c) {
+                const int cc = (int)crank * (BN / 128) + c;
+                tma_load_2d_mc(b + cc * 8192, mb, &full[s], bnn + 64 * cc, bk, 0x3);
+              }
+            }
+          } else if (!B_MN) {
             tma_load_2d(b, mb, &full[s], bk, bnn);
           } else {
 #pragma unroll
@@ -219,7 +239,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
                                      : umma_sdesc_sw128(b0 + kk * 32, 16, 1024);
             umma_bf16(tmem_d, ad, bd, idesc, (kb > kb0 || kk) ? 1u : 0u);
           }
-          umma_commit(&empty[s]);  // frees the smem stage when these MMAs complete
+          if constexpr (CL2) umma_commit_mc(&empty[s], 0x3);  // both CTAs' stage s: this CTA has read it
+          else umma_commit(&empty[s]);  // frees the smem stage when these MMAs complete
         }
         umma_commit(&acc_full[buf]);  // accumulator ready for the epilogue
       }
@@ -395,7 +416,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
     if (lane == 0) bulk_wait<0>();
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CL2) cluster_sync_all();  // no multicast / remote commit may target an exited CTA
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
@@ -455,11 +477,11 @@ static int ew8_override() {  // TOFU_EW8=0 / 1 forces the 4- / 8-warp epilogue (
   return v;
 }
 
-template <int BN, bool A_MN, bool B_MN, int MODE_, bool PC>
+template <int BN, bool A_MN, bool B_MN, int MODE_, bool PC, bool CL2 = false>
 static int launch_t(const tofu_gemm_args* g, const CUtensorMap* tm, const PieceMaps* pm, cudaStream_t st, double ai) {
   using Cfg = GemmCfg<BN, MODE_>;
   constexpr int MODE = Cfg::MODE;
-  auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, MODE_, PC>;
+  auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, MODE_, PC, CL2>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
@@ -483,6 +505,25 @@ static int launch_t(const tofu_gemm_args* g, const CUtensorMap* tm, const PieceM
   std::conditional_t<PC, PieceMaps, NoPieces> pp{};
   if constexpr (PC) pp = *pm;
   (void)pm;
+  if constexpr (CL2) {  // clusters of 2 over pair units (m tiles 2p, 2p+1 of one n tile)
+    const int pair_units = ((g->M + 2 * BM - 1) / (2 * BM)) * ((g->N + BN - 1) / BN);
+    const int ncl = pair_units < g_num_sms / 2 ? pair_units : g_num_sms / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * ncl, 1, 1);
+    cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, pp, tm[0], tm[1], tm[2], tm[3], tm[5], g->M, g->N, g->K,
+                                             g->s0, g->s1, 1, g->ep, 0, g->sk_ws);
+    return e == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
+  }
   kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(pp, tm[0], tm[1], tm[2], tm[3], tm[5], g->M, g->N, g->K, g->s0, g->s1,
                                              splits, g->ep, sk, g->sk_ws);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
@@ -502,11 +543,21 @@ static int dispatch_bn(const tofu_gemm_args* g, const CUtensorMap* tm, const Pie
   const double lim = mode == 3 ? 200.0 : 600.0;
   const bool pc = pm != nullptr;  // piecewise operands: 4-warp epilogue instantiations only
   const bool w8 = !pc && (mode == 0 || mode == 3 || mode == 5) && (ov >= 0 ? ov == 1 : 2.0 * g->K / e < lim);
-  const int key = (g->a_mn_major ? 1 : 0) | (g->b_mn_major ? 2 : 0) | ((mode | (w8 ? 8 : 0)) << 2) | (pc ? 64 : 0);
+  const bool cl2 = BN == 256 && g->cl2 == 1 && !pc && mode != 4;
+  const int key = (g->a_mn_major ? 1 : 0) | (g->b_mn_major ? 2 : 0) | ((mode | (w8 ? 8 : 0)) << 2) | (pc ? 64 : 0) |
+                  (cl2 ? 128 : 0);
   switch (key) {
 #define TOFU_CASE(AM, BMJ, O, P) \
   case ((AM) | ((BMJ) << 1) | ((O) << 2) | ((P) << 6)): \
     return launch_t<BN, (bool)(AM), (bool)(BMJ), O, (bool)(P)>(g, tm, pm, st, ai);
+#define TOFU_CASE2(AM, BMJ, O) \
+  case ((AM) | ((BMJ) << 1) | ((O) << 2) | 128): \
+    return launch_t<BN, (bool)(AM), (bool)(BMJ), O, false, BN == 256>(g, tm, pm, st, ai);
+#define TOFU_CASES2(O) TOFU_CASE2(0, 0, O) TOFU_CASE2(0, 1, O) TOFU_CASE2(1, 0, O) TOFU_CASE2(1, 1, O)
+    TOFU_CASES2(0) TOFU_CASES2(1) TOFU_CASES2(2) TOFU_CASES2(3) TOFU_CASES2(5) TOFU_CASES2(8) TOFU_CASES2(11)
+    TOFU_CASES2(13)
+#undef TOFU_CASES2
+#undef TOFU_CASE2
 #define TOFU_CASES(O, P) TOFU_CASE(0, 0, O, P) TOFU_CASE(0, 1, O, P) TOFU_CASE(1, 0, O, P) TOFU_CASE(1, 1, O, P)
     TOFU_CASES(0, 0) TOFU_CASES(1, 0) TOFU_CASES(2, 0) TOFU_CASES(3, 0) TOFU_CASES(4, 0) TOFU_CASES(5, 0)
     TOFU_CASES(8, 0) TOFU_CASES(11, 0) TOFU_CASES(13, 0)
@@ -600,6 +651,11 @@ static void* g_ws = nullptr;
 static size_t g_ws_bytes = 0;
 static std::mutex g_ws_mu;
 
+// Measured (tools/gemm_major_bench.py, tools/sk_bench.py): pairs pay when both operands are MN-major (the
+// weight-gradient GEMMs; 8192^3 1070 -> 1227 TF/s, 6272x4096x1024 1143 -> 1206) and lose 3-7% on several
+// K-major shapes and on the memory-leaning fused-optimizer epilogue (configs[1], K = 512).
+static bool cl2_auto(const tofu_gemm_args* g) { return g->a_mn_major && g->b_mn_major && g->K >= 2048; }
+
 static int auto_splits(const tofu_gemm_args* g, int bn) {
   if (g->splits == 1 || g->ep) return 1;
   const int nk = (g->K + BK - 1) / BK;
@@ -660,6 +716,17 @@ extern "C" int tofu_gemm_plan_tmaps(tofu_gemm_args* g, void* tmaps, int* bn_out)
   }
   const bool stream_k = g->splits == -1;
   g->splits = stream_k ? 1 : auto_splits(g, bn);
+  // cluster pairs sharing B (see the kernel's CL2): data-parallel launches of 256-wide tiles with at least
+  // two m tiles; TOFU_CL2=0 turns them off, 1 forces them wherever possible (A/B measurements)
+  {
+    static const int env = [] {
+      const char* e = getenv("TOFU_CL2");
+      return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
+    }();
+    const bool ok = g->cl2 != -1 && env != 0 && bn == 256 && g->splits == 1 && !stream_k && !g->a_pieces &&
+                    !g->b_pieces && g->max_ctas == 0 && g->M > BM;
+    g->cl2 = ok && (env == 1 || g->cl2 == 2 || cl2_auto(g)) ? 1 : 0;
+  }
   CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(tmaps);
   const CUtensorMapDataType BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   const auto SW128 = CU_TENSOR_MAP_SWIZZLE_128B, SW64 = CU_TENSOR_MAP_SWIZZLE_64B;
@@ -667,7 +734,7 @@ extern "C" int tofu_gemm_plan_tmaps(tofu_gemm_args* g, void* tmaps, int* bn_out)
   if (!g->a_mn_major) r = make_tmap(&tm[0], g->A, BF, 2, g->K, g->M, g->lda, 64, BM, SW128);
   else r = make_tmap(&tm[0], g->A, BF, 2, g->M, g->K, g->lda, 64, 64, SW128);
   if (r) return TOFU_ERR_CUDA;
-  if (!g->b_mn_major) r = make_tmap(&tm[1], g->B, BF, 2, g->K, g->N, g->ldb, 64, bn, SW128);
+  if (!g->b_mn_major) r = make_tmap(&tm[1], g->B, BF, 2, g->K, g->N, g->ldb, 64, g->cl2 ? bn / 2 : bn, SW128);
   else r = make_tmap(&tm[1], g->B, BF, 2, g->N, g->K, g->ldb, 64, 64, SW128);
   if (r) return TOFU_ERR_CUDA;
   if (g->c_mode == 0) r = make_tmap(&tm[2], g->C, BF, 2, g->N, g->M, g->ldc, 32, 32, SW64);

@@ -1814,12 +1814,22 @@ extern "C" int tofu_exec_launch_count(const tofu_exec* h, int64_t* launches) {
   if (!h || !launches) return tofu::fail(TOFU_ERR_ARG, "null argument");
   return tofu::guard([&]() {
     tofu::Exec& E = const_cast<tofu_exec*>(h)->e;
-    tofu::finalize(E);  // (descriptors decide the kernels per compute launch)
+    // the descriptors decide the kernels per compute launch (split-K reductions, ...); without a device
+    // (host-only lowering checks) every compute launch counts as one kernel
+    bool ready = E.finalized;
+    if (!ready) {
+      try {
+        tofu::finalize(E);
+        ready = true;
+      } catch (const tofu::Error&) {
+        cudaGetLastError();
+      }
+    }
     int64_t n = 0;
     for (auto& L : E.launches) {
       if (L.kind == 4) continue;  // cudaMemsetAsync, not a kernel of ours
       if (E.skip_comm && (L.kind == 0 || L.kind == 2 || L.kind == 3)) continue;
-      n += L.kind == 1 ? tofu::kernels_of(E, L.op, L.li) : 1;
+      n += L.kind == 1 && ready ? tofu::kernels_of(E, L.op, L.li) : 1;
     }
     *launches = n;
     return TOFU_OK;

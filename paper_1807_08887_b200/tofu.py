@@ -28,7 +28,7 @@ class GemmArgs(C.Structure):
                 ("bn", C.c_int), ("max_ctas", C.c_int), ("D", C.c_void_p), ("ldd", C.c_int),
                 ("s0", C.c_float), ("s1", C.c_float), ("splits", C.c_int), ("ws", C.c_void_p),
                 ("aux_add", C.c_void_p), ("aux_mask", C.c_void_p), ("ep", C.c_int), ("sk_ws", C.c_void_p),
-                ("a_pieces", C.c_void_p), ("b_pieces", C.c_void_p)]
+                ("a_pieces", C.c_void_p), ("b_pieces", C.c_void_p), ("cl2", C.c_int)]
 
 
 MAX_PIECES = 8
@@ -139,7 +139,8 @@ def _stream(stream):
 
 # ----------------------------------------------------------------------------- kernels
 def gemm(A, B, Cout, M, N, K, lda, a_mn, ldb, b_mn, ldc, c_mode, bn=0, max_ctas=0, stream=None, D=None, ldd=0,
-         s0=0.0, s1=0.0, splits=0, aux_add=None, aux_mask=None, ep=0, sk_ws=None, a_pieces=None, b_pieces=None):
+         s0=0.0, s1=0.0, splits=0, aux_add=None, aux_mask=None, ep=0, sk_ws=None, a_pieces=None, b_pieces=None,
+         cl2=0):
     """tofu_gemm_bf16 (include/tofu.h).  sk_ws: a zero-filled uint8 device tensor of tofu_sk_workspace_bytes()
     bytes enables stream-K (left zeroed by the launch).  a_pieces / b_pieces: (dim, [(start, tensor, ld), ...])
     piecewise operands (tofu_operand_pieces; A / B are then only shape references)."""
@@ -158,7 +159,7 @@ def gemm(A, B, Cout, M, N, K, lda, a_mn, ldb, b_mn, ldc, c_mode, bn=0, max_ctas=
                  aux_add.data_ptr() if aux_add is not None else None,
                  aux_mask.data_ptr() if aux_mask is not None else None, ep,
                  sk_ws.data_ptr() if sk_ws is not None else None,
-                 C.addressof(pa) if pa is not None else None, C.addressof(pb) if pb is not None else None)
+                 C.addressof(pa) if pa is not None else None, C.addressof(pb) if pb is not None else None, cl2)
     check(lib().tofu_gemm_bf16(C.byref(a), _stream(stream)), "tofu_gemm_bf16")
 
 
