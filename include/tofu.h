@@ -265,6 +265,9 @@ typedef struct {
    * smallest tap offsets.
    * On entry, im2col = -1 keeps the gather warps (used by the parity tests). */
   int im2col, i2c_dy0, i2c_dx0;
+  /* set by tofu_conv_plan (kind 1 with im2col): 1 = clusters of 2 CTAs on adjacent output-channel tiles share
+   * (TMA-multicast) the gathered activations; on entry -1 forbids it, 2 requests it where eligible */
+  int cl2;
 } tofu_conv_args;
 /* Encode TMA descriptors once (tmaps: 5 x 128 B, 64-byte aligned; args->splits / direct / im2col updated), then launch. */
 int tofu_conv_plan(tofu_conv_args* args, void* tmaps);

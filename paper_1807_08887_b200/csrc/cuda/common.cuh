@@ -62,6 +62,16 @@ __device__ __forceinline__ void tma_load_im2col_4d(void* smem_dst, const void* t
       "h"(off_h)
       : "memory");
 }
+// ... multicast to every CTA of ctaMask (same smem offset; each CTA's barrier at `bar`'s offset)
+__device__ __forceinline__ void tma_load_im2col_4d_mc(void* smem_dst, const void* tmap, uint64_t* bar, int c, int w,
+                                                      int h, int n, uint16_t off_w, uint16_t off_h, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8}, %9;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(off_w),
+      "h"(off_h), "h"(mask)
+      : "memory");
+}
 
 __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* smem_src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(

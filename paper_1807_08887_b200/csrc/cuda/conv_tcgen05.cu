@@ -98,7 +98,10 @@ __device__ __forceinline__ RowInfo no_pixel() {
 // I2C (kind 0): the activation operand is loaded by TMA in im2col mode (tmI) instead of the gather warps:
 // one 128-pixel x 64-channel box per k-block, zero outside the tensor (= padding), straight into the
 // 128B-swizzled layout of the gathered tile.  Used for stride-1 grids whose channel blocks are whole taps.
-template <int KIND, int BN, bool B_MN, int MODE, bool I2C = false>
+// CL2 (weight gradient with im2col): clusters of 2 CTAs on vertically adjacent tiles (output-channel tiles
+// 2p, 2p+1) of the same n tile share the gathered activations: each CTA im2col-loads half of the B sub-blocks
+// and multicasts them to both; a stage is freed by both CTAs' MMA commits (as gemm_tcgen05.cu's CL2).
+template <int KIND, int BN, bool B_MN, int MODE, bool I2C = false, bool CL2 = false>
 __global__ void __launch_bounds__(NTHREADS, 1)
     conv_kernel(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap tmDense,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD,
@@ -127,7 +130,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int tiles_n = (N + BN - 1) / BN;
   const int nk = (K + BK - 1) / BK;
   WorkList wl;
-  wl.init(tiles_m * tiles_n, nk, splits, P.sk_tiles);
+  uint32_t crank = 0;
+  if constexpr (CL2) {
+    crank = cluster_rank();
+    wl.init_pairs(tiles_m, tiles_n, nk, (int)crank, (int)cluster_id_x(), (int)nclusters_x());
+  } else {
+    wl.init(tiles_m * tiles_n, nk, splits, P.sk_tiles);
+  }
   const int nseg = wl.count();
   void* const sk_ws = a.sk_ws;
   const int ngyx = a.ngy * a.ngx;
@@ -135,7 +144,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], I2C ? 1 : 1 + NGATHER);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL2 ? 2 : 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -150,7 +159,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   if (warp == 1) tmem_alloc(tmem_slot, C_::TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CL2) cluster_sync_all();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -211,9 +221,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               const int t = n0 / a.nch, c = n0 - t * a.nch;
               const uint16_t ow = (uint16_t)(a.tap_dx[t] - P.dx0), oh = (uint16_t)(a.tap_dy[t] - P.dy0);
 #pragma unroll
-              for (int q = 0; q < BN / 64; ++q)
-                tma_load_im2col_4d(sB + s * C_::B_BYTES + q * 8192, &tmI, &full[s], a.sc0 + c + 64 * q,
-                                   a.ax * gx + a.cx + P.dx0, a.ay * gy + a.cy + P.dy0, gb + a.sb0, ow, oh);
+              for (int q = 0; q < BN / 64; ++q) {
+                if constexpr (CL2) {  // this CTA's half of the sub-blocks, multicast to the pair
+                  if ((q >= BN / 128) != (crank != 0)) continue;
+                  tma_load_im2col_4d_mc(sB + s * C_::B_BYTES + q * 8192, &tmI, &full[s], a.sc0 + c + 64 * q,
+                                        a.ax * gx + a.cx + P.dx0, a.ay * gy + a.cy + P.dy0, gb + a.sb0, ow, oh, 0x3);
+                } else {
+                  tma_load_im2col_4d(sB + s * C_::B_BYTES + q * 8192, &tmI, &full[s], a.sc0 + c + 64 * q,
+                                     a.ax * gx + a.cx + P.dx0, a.ay * gy + a.cy + P.dy0, gb + a.sb0, ow, oh);
+                }
+              }
             }
           }
         }
@@ -249,7 +266,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                     : umma_sdesc_sw128(b0 + kk * 32, 16, 1024);
             umma_bf16(tmem_d, ad, bd, idesc, (kb > kb0 || kk) ? 1u : 0u);
           }
-          umma_commit(&empty[s]);
+          if constexpr (CL2) umma_commit_mc(&empty[s], 0x3);
+          else umma_commit(&empty[s]);
         }
         umma_commit(&acc_full[buf]);
       }
@@ -580,7 +598,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CL2) cluster_sync_all();
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C_::TMEM_COLS);
@@ -808,10 +827,10 @@ static int auto_splits(const tofu_conv_args* a, int M, int N, int K, int bn) {
   return sp < 2 ? 1 : sp;
 }
 
-template <int KIND, int BN, bool B_MN, int MODE, bool I2C = false>
+template <int KIND, int BN, bool B_MN, int MODE, bool I2C = false, bool CL2 = false>
 static int launch_t(const Params& P, const CUtensorMap* tm, cudaStream_t st) {
   using C_ = Cfg<KIND, BN, MODE>;
-  auto kern = conv_kernel<KIND, BN, B_MN, MODE, I2C>;
+  auto kern = conv_kernel<KIND, BN, B_MN, MODE, I2C, CL2>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM) != cudaSuccess)
@@ -830,6 +849,24 @@ static int launch_t(const Params& P, const CUtensorMap* tm, cudaStream_t st) {
                    ? sk_tiles_for(tiles, (P.K + BK - 1) / BK, g_sms, P.a.sk_ws, KIND == 1, 2 * M * N * K / bytes)
                    : 0;
   if (Q.sk_tiles) grid = g_sms;
+  if constexpr (CL2) {
+    Q.sk_tiles = 0;
+    const int pair_units = ((P.M + 2 * BM - 1) / (2 * BM)) * ((P.N + BN - 1) / BN);
+    const int ncl = pair_units < g_sms / 2 ? pair_units : g_sms / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * ncl, 1, 1);
+    cfg.blockDim = dim3(NTHREADS, 1, 1);
+    cfg.dynamicSmemBytes = C_::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, Q, tm[0], tm[1], tm[2], tm[4]) == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
+  }
   kern<<<grid, NTHREADS, C_::SMEM, st>>>(Q, tm[0], tm[1], tm[2], tm[4]);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }
@@ -859,8 +896,11 @@ static int dispatch(const Params& P, const CUtensorMap* tm, int mode, cudaStream
       default: return TOFU_ERR_ARG;
     }
   }
-  const int key = mode | (bn == 256 ? 8 : 0) | (a.im2col ? 16 : 0);
+  const int key = mode | (bn == 256 ? 8 : 0) | (a.im2col ? 16 : 0) | (a.cl2 == 1 && bn == 256 && a.im2col ? 32 : 0);
   switch (key) {
+    case 1 | 8 | 16 | 32: return launch_t<1, 256, true, 1, true, true>(P, tm, st);
+    case 2 | 8 | 16 | 32: return launch_t<1, 256, true, 2, true, true>(P, tm, st);
+    case 3 | 8 | 16 | 32: return launch_t<1, 256, true, 3, true, true>(P, tm, st);
 #define TOFU_K1(MO, BNV, I) \
   case (MO) | ((BNV) == 256 ? 8 : 0) | ((I) ? 16 : 0): return launch_t<1, BNV, true, MO, (bool)(I)>(P, tm, st);
     TOFU_K1(1, 256, 0) TOFU_K1(2, 256, 0) TOFU_K1(3, 256, 0) TOFU_K1(4, 256, 0)
@@ -985,6 +1025,14 @@ extern "C" int tofu_conv_plan(tofu_conv_args* a, void* tmaps) {
   a->splits = auto_splits(a, M, N, K, bn);
   tm[4] = tm[0];
   try_im2col(a, tm, BK, bn);  // the N tile (bn columns) must lie within one tap
+  {  // cluster pairs sharing the gathered activations (TOFU_CL2=0 off, 1 forced where eligible)
+    static const int env = [] {
+      const char* e = getenv("TOFU_CL2");
+      return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
+    }();
+    const bool ok = a->cl2 != -1 && env != 0 && a->im2col && a->splits <= 1 && bn == 256 && M > BM;
+    a->cl2 = ok && (env == 1 || a->cl2 == 2 || K >= 2048) ? 1 : 0;
+  }
   if (tmap2(&tm[0], a->Ap, BF, 2, M, K, a->lda, 64, 64, SW128)) return TOFU_ERR_CUDA;
   if (tmap2(&tm[1], a->C, F32, 4, N, M, a->ldc, 32, 32, SW128)) return TOFU_ERR_CUDA;
   if (a->c_mode == 3) {

@@ -58,7 +58,8 @@ class ConvArgs(C.Structure):
                 ("ldc", C.c_int64), ("c_mode", C.c_int), ("D", C.c_void_p), ("ldd", C.c_int64),
                 ("s0", C.c_float), ("s1", C.c_float), ("splits", C.c_int), ("ws", C.c_void_p),
                 ("aux_add", C.c_void_p), ("aux_mask", C.c_void_p), ("ep", C.c_int), ("sk_ws", C.c_void_p),
-                ("direct", C.c_int), ("im2col", C.c_int), ("i2c_dy0", C.c_int), ("i2c_dx0", C.c_int)]
+                ("direct", C.c_int), ("im2col", C.c_int), ("i2c_dy0", C.c_int), ("i2c_dx0", C.c_int),
+                ("cl2", C.c_int)]
 
 
 class Piece(C.Structure):

@@ -246,3 +246,35 @@ def test_conv_im2col_stride2(kind):
         ref = torch.nn.grad.conv2d_weight(Xt.permute(0, 3, 1, 2), (Cs, Cs, 3, 3), Dt.permute(0, 3, 1, 2), stride=2,
                                           padding=1).permute(0, 2, 3, 1).numpy()
         assert nrm(outs[1], ref) <= 1e-5
+
+
+@pytest.mark.parametrize("which", ["wgrad", "wgrad_opt"])
+def test_conv_wgrad_cluster_pairs(data, which):
+    """Weight gradient as clusters of 2 CTAs on adjacent output-channel tiles sharing the im2col-loaded
+    activations (tofu_conv_args.cl2, multicast halves): bitwise equal to the single-CTA launch."""
+    t = _tofu()
+    rng, X, W, D, ref = data
+    Xd, Dd = cuda_bf16(X), cuda_bf16(D)
+    M0, W0 = q(rng, (C, 3, 3, C), 2 ** -12), q(rng, (C, 3, 3, C), 2 ** -7)
+    outs, modes = [], []
+    for cl2 in (-1, 2):
+        out = (torch.from_numpy(M0).float().cuda() if which == "wgrad_opt"
+               else torch.zeros((C, 3, 3, C), dtype=torch.float32, device="cuda"))
+        a = conv_args(t, 1, Xd, out, Y=Dd)
+        keep = []
+        if which == "wgrad_opt":
+            keep = [cuda_bf16(W0)]
+            a.c_mode, a.D, a.ldd, a.s0, a.s1 = 3, keep[0].data_ptr(), 9 * C, 0.875, 0.0078125
+        a.splits = 1
+        a.cl2 = cl2
+        modes.append(t.conv_plan(a).cl2)
+        t.conv(a)
+        torch.cuda.synchronize()
+        outs.append((out.double().cpu().numpy(), keep[0].double().cpu().numpy() if keep else None))
+    assert modes == [0, 1]
+    assert np.array_equal(outs[0][0], outs[1][0])
+    if which == "wgrad_opt":
+        assert np.array_equal(outs[0][1], outs[1][1])
+        assert nrm(outs[1][0], M0 * 0.875 + ref["wgrad"]) <= 1e-5
+    else:
+        assert nrm(outs[1][0], ref["wgrad"]) <= 1e-5
