@@ -183,8 +183,9 @@ typedef struct {
   const tofu_operand_pieces* a_pieces;
   const tofu_operand_pieces* b_pieces;
   /* set by tofu_gemm_plan_tmaps: 1 = launched as clusters of 2 CTAs on vertically adjacent tiles that
-   * share (TMA-multicast) the B tile; on entry -1 forbids it, 2 requests it where eligible (parity tests),
-   * 0 = automatic */
+   * share (TMA-multicast) the B tile; 3 = 2-CTA MMA pairs (tcgen05 cta_group::2, M = 256 over the pair, each
+   * CTA staging its A rows and half of B).  On entry -1 forbids both, 2 requests the multicast pairs and 4 the
+   * 2-CTA MMA where eligible (parity tests), 0 = automatic */
   int cl2;
 } tofu_gemm_args;
 int tofu_gemm_bf16(const tofu_gemm_args* args, void* stream);

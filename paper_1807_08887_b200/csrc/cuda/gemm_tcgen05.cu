@@ -45,6 +45,9 @@ template <int BN, int MODE_>
 struct GemmCfg {
   static constexpr int MODE = MODE_ & 7;
   static constexpr bool W8 = (MODE_ & 8) != 0;
+  // C2 (bit 4): 2-CTA MMA pairs (tcgen05.mma.cta_group::2, M = 256 over the pair): each CTA stages its own
+  // 128 rows of A and half (BN/2 rows) of B
+  static constexpr bool C2 = (MODE_ & 16) != 0;
   // MODE 5 may load (residual add / relu mask operands, when its runtime `ep` asks for them)
   static constexpr bool LOADS = MODE == 2 || MODE == 3 || MODE == 5;
   // the fused optimizer (MODE 3) and the fused element-wise epilogue (MODE 5) stream extra operands through
@@ -60,7 +63,7 @@ struct GemmCfg {
   static constexpr int THREADS = 64 + 32 * EW;
   static constexpr int EPI_BYTES = EW * NBUF * BUF_BYTES;
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (C2 ? BN / 2 : BN) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES_FIT = (SMEM_MAX - 1024 - 512 - EPI_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
@@ -126,7 +129,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
   // segments = (output tile, k-block range): data-parallel units (tile, K split) then stream-K pieces
   WorkList wl;
   uint32_t crank = 0;
-  if constexpr (CL2) {
+  constexpr bool C2 = Cfg::C2;
+  if constexpr (CL2 || C2) {
     crank = cluster_rank();
     wl.init_pairs(tiles_m, tiles_n, nk, (int)crank, (int)cluster_id_x(), (int)nclusters_x());
   } else {
@@ -137,11 +141,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL2 ? 2 : 1);  // CL2: both CTAs' MMAs must have read the stage
+      mbar_init(&empty[s], CL2 && !C2 ? 2 : 1);  // CL2: both CTAs' MMAs must have read the stage
     }
     for (int b = 0; b < Cfg::ACC_BUFS; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], Cfg::EW);  // one arrive per epilogue warp
+      mbar_init(&acc_empty[b], C2 ? 2 * Cfg::EW : Cfg::EW);  // one arrive per epilogue warp (C2: of both CTAs)
     }
     for (int b = 0; b < Cfg::EW * NBUF; ++b) mbar_init(&ebar[b], 1);
     fence_mbar_init();
@@ -151,9 +155,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
     if (MODE == 3 || MODE == 5) tma_prefetch_desc(&tmD);
     if (MODE == 5) tma_prefetch_desc(&tmE);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  if (warp == 1) {
+    if constexpr (C2) tmem_alloc2(tmem_slot, Cfg::TMEM_COLS);
+    else tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  }
   tc_fence_before();
-  if constexpr (CL2) cluster_sync_all();  // the peer's barriers are initialised before any multicast
+  if constexpr (CL2 || C2) cluster_sync_all();  // the peer's barriers are initialised before any multicast
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
@@ -172,7 +179,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+          // C2: both CTAs' loads complete on the leader's barrier, which expects the pair's bytes
+          if constexpr (C2) {
+            if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
+          } else {
+            mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+          }
           uint8_t* a = sA + s * Cfg::A_BYTES;
           uint8_t* b = sB + s * Cfg::B_BYTES;
           const int k0 = kb * BK;
@@ -185,13 +197,29 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
             if (pm.nb) mb = pm.b_dim ? piece_of(pm.b_map, pm.b_start, pm.nb, k0, bk)
                                      : piece_of(pm.b_map, pm.b_start, pm.nb, n0, bnn);
           }
-          if (!A_MN) {
+          if constexpr (C2) {  // own A rows, own half of B; completion on the leader's full barrier
+            const uint32_t lf = mapa_shared(&full[s], 0);
+            if (!A_MN) {
+              tma_load_2d_2sm(a, ma, lf, ak, am);
+            } else {
+#pragma unroll
+              for (int c = 0; c < BM / 64; ++c) tma_load_2d_2sm(a + c * 8192, ma, lf, am + 64 * c, ak);
+            }
+            if (!B_MN) {
+              tma_load_2d_2sm(b, mb, lf, bk, bnn + (int)crank * (BN / 2));
+            } else {
+#pragma unroll
+              for (int c = 0; c < BN / 128; ++c)
+                tma_load_2d_2sm(b + c * 8192, mb, lf, bnn + 64 * ((int)crank * (BN / 128) + c), bk);
+            }
+          } else if (!A_MN) {
             tma_load_2d(a, ma, &full[s], ak, am);
           } else {
 #pragma unroll
             for (int c = 0; c < BM / 64; ++c) tma_load_2d(a + c * 8192, ma, &full[s], am + 64 * c, ak);
           }
-          if constexpr (CL2) {  // this CTA's half of B, multicast into both CTAs' stage
+          if constexpr (C2) {
+          } else if constexpr (CL2) {  // this CTA's half of B, multicast into both CTAs' stage
             if (!B_MN) {
               tma_load_2d_mc(b + crank * (Cfg::B_BYTES / 2), mb, &full[s], bk, bnn + (int)crank * (BN / 2), 0x3);
             } else {
@@ -211,9 +239,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+    // ------------------------------------------------------------ MMA issuer (C2: the pair leader only)
+    if (lane == 0 && (!C2 || crank == 0)) {
+      constexpr uint32_t idesc = umma_idesc_bf16(C2 ? 2 * BM : BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
       int it = 0;
       for (int local = 0; local < nseg; ++local) {
         int tile, kb0, kb1, sp;
@@ -237,12 +265,15 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
                                      : umma_sdesc_sw128(a0 + kk * 32, 16, 1024);
             const uint64_t bd = B_MN ? umma_sdesc_sw128(b0 + kk * 2048, 8192, 1024)
                                      : umma_sdesc_sw128(b0 + kk * 32, 16, 1024);
-            umma_bf16(tmem_d, ad, bd, idesc, (kb > kb0 || kk) ? 1u : 0u);
+            if constexpr (C2) umma_bf16_2(tmem_d, ad, bd, idesc, (kb > kb0 || kk) ? 1u : 0u);
+            else umma_bf16(tmem_d, ad, bd, idesc, (kb > kb0 || kk) ? 1u : 0u);
           }
-          if constexpr (CL2) umma_commit_mc(&empty[s], 0x3);  // both CTAs' stage s: this CTA has read it
+          if constexpr (C2) umma_commit2_mc(&empty[s], 0x3);     // frees stage s in both CTAs
+          else if constexpr (CL2) umma_commit_mc(&empty[s], 0x3);  // both CTAs' stage s: this CTA has read it
           else umma_commit(&empty[s]);  // frees the smem stage when these MMAs complete
         }
-        umma_commit(&acc_full[buf]);  // accumulator ready for the epilogue
+        if constexpr (C2) umma_commit2_mc(&acc_full[buf], 0x3);  // both CTAs' accumulator halves are ready
+        else umma_commit(&acc_full[buf]);  // accumulator ready for the epilogue
       }
     }
   } else {
@@ -304,7 +335,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
       if (cw == NCW - 1) {  // accumulator fully read: hand TMEM back to the MMA warp
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[acc]);
+        if (lane == 0) {
+          if constexpr (C2) mbar_arrive_cluster(mapa_shared(&acc_empty[acc], 0));  // the leader's MMA waits
+          else mbar_arrive(&acc_empty[acc]);
+        }
         ++local;
       }
       if (part) {
@@ -416,11 +450,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
     if (lane == 0) bulk_wait<0>();
   }
   tc_fence_before();
-  if constexpr (CL2) cluster_sync_all();  // no multicast / remote commit may target an exited CTA
+  if constexpr (CL2 || C2) cluster_sync_all();  // no multicast / remote commit may target an exited CTA
   else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    if constexpr (C2) tmem_dealloc2(tmem_base, Cfg::TMEM_COLS);
+    else tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }
 }
 
@@ -461,6 +496,22 @@ static bool sk_enabled() {  // TOFU_SK=0 turns stream-K off (A/B measurements)
     return !(e && e[0] == '0');
   }();
   return on;
+}
+
+// 8 epilogue warps when a tile's epilogue traffic rivals its mainloop: per output element 2K flops against
+// e bytes of output-side HBM traffic (bf16 / fused element-wise / fused optimizer outputs).  Measured: the
+// configs[1] weight gradient (2K/e = 85) and the WResNet 1x1 add / mask epilogues (2K/e = 128..512) gain;
+// with the optimizer the wide epilogue leaves 2 smem stages (vs 3) and loses from 2K/e ~ 430 (LSTM gate
+// weight gradients), bf16 outputs keep 3 (vs 4) and lose at 2K/e >= 1000.
+static int ew8_override();
+static bool wants_w8(const tofu_gemm_args* g) {
+  const int mode = g->c_mode == 0 && g->ep ? 5 : g->c_mode;
+  if (mode != 0 && mode != 3 && mode != 5) return false;
+  const int ov = ew8_override();
+  if (ov >= 0) return ov == 1;
+  const double e = mode == 3 ? 12 : 2 + 2 * (((g->ep >> 1) & 1) + ((g->ep >> 2) & 1));
+  const double lim = mode == 3 ? 200.0 : 600.0;
+  return 2.0 * g->K / e < lim;
 }
 
 // algorithmic flops / HBM bytes of a launch (operands once, output side e bytes per element)
@@ -533,17 +584,25 @@ template <int BN>
 static int dispatch_bn(const tofu_gemm_args* g, const CUtensorMap* tm, const PieceMaps* pm, cudaStream_t st) {
   const int mode = g->c_mode == 0 && g->ep ? 5 : g->c_mode;
   const double ai = gemm_intensity(g, mode);
-  const int ov = ew8_override();
-  // 8 epilogue warps when a tile's epilogue traffic rivals its mainloop: per output element 2K flops against
-  // e bytes of output-side HBM traffic (bf16 / fused element-wise / fused optimizer outputs).  Measured: the
-  // configs[1] weight gradient (2K/e = 85) and the WResNet 1x1 add / mask epilogues (2K/e = 128..512) gain;
-  // with the optimizer the wide epilogue leaves 2 smem stages (vs 3) and loses from 2K/e ~ 430 (LSTM gate
-  // weight gradients), bf16 outputs keep 3 (vs 4) and lose at 2K/e >= 1000.
-  const double e = mode == 3 ? 12 : 2 + 2 * (((g->ep >> 1) & 1) + ((g->ep >> 2) & 1));
-  const double lim = mode == 3 ? 200.0 : 600.0;
   const bool pc = pm != nullptr;  // piecewise operands: 4-warp epilogue instantiations only
-  const bool w8 = !pc && (mode == 0 || mode == 3 || mode == 5) && (ov >= 0 ? ov == 1 : 2.0 * g->K / e < lim);
+  const bool w8 = !pc && wants_w8(g);
   const bool cl2 = BN == 256 && g->cl2 == 1 && !pc && mode != 4;
+  // (the plan encoded B with half-height boxes for both pair kinds: a launch that cannot honour the pairing
+  // would wait for bytes that never arrive)
+  const bool c2 = BN == 256 && g->cl2 == 3 && !pc && mode != 4;  // (4-warp epilogue instantiations)
+  if ((g->cl2 == 1 && !cl2) || (g->cl2 == 3 && !c2)) return TOFU_ERR_ARG;
+  if (c2) {
+    const int k2 = (g->a_mn_major ? 1 : 0) | (g->b_mn_major ? 2 : 0) | (mode << 2);
+    switch (k2) {
+#define TOFU_CASE3(AM, BMJ, O) \
+  case ((AM) | ((BMJ) << 1) | ((O) << 2)): return launch_t<BN, (bool)(AM), (bool)(BMJ), (O) | 16, false, true>(g, tm, pm, st, ai);
+#define TOFU_CASES3(O) TOFU_CASE3(0, 0, O) TOFU_CASE3(0, 1, O) TOFU_CASE3(1, 0, O) TOFU_CASE3(1, 1, O)
+      TOFU_CASES3(0) TOFU_CASES3(1) TOFU_CASES3(2) TOFU_CASES3(3) TOFU_CASES3(5)
+#undef TOFU_CASES3
+#undef TOFU_CASE3
+      default: return TOFU_ERR_ARG;
+    }
+  }
   const int key = (g->a_mn_major ? 1 : 0) | (g->b_mn_major ? 2 : 0) | ((mode | (w8 ? 8 : 0)) << 2) | (pc ? 64 : 0) |
                   (cl2 ? 128 : 0);
   switch (key) {
@@ -723,9 +782,18 @@ extern "C" int tofu_gemm_plan_tmaps(tofu_gemm_args* g, void* tmaps, int* bn_out)
       const char* e = getenv("TOFU_CL2");
       return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
     }();
-    const bool ok = g->cl2 != -1 && env != 0 && bn == 256 && g->splits == 1 && !stream_k && !g->a_pieces &&
+    const int req = g->cl2 == 1 || g->cl2 == 3 ? 0 : g->cl2;  // (a re-plan of planned args decides afresh)
+    const bool ok = req != -1 && env != 0 && bn == 256 && g->splits == 1 && !stream_k && !g->a_pieces &&
                     !g->b_pieces && g->max_ctas == 0 && g->M > BM;
-    g->cl2 = ok && (env == 1 || g->cl2 == 2 || cl2_auto(g)) ? 1 : 0;
+    static const int env2 = [] {  // 2-CTA MMA pairs: TOFU_C2=1 forces them where eligible (A/B measurements)
+      const char* e = getenv("TOFU_C2");
+      return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
+    }();
+    // 2-CTA MMA pairs for compute-leaning launches (the 4-warp epilogue ones); measured (tools/gemm_major_bench.py,
+    // tools/sk_bench.py): 8192^3 1182 -> 1294 TF/s (K-major), 1152 -> 1398 (both MN-major), the configs[1]
+    // forward 62 -> 57 us; the memory-leaning fused epilogues lose up to 1.7x with 4 warps, so they keep W8
+    const bool c2 = ok && (req == 4 || (req == 0 && env2 != 0 && (env2 == 1 || !wants_w8(g))));
+    g->cl2 = c2 ? 3 : ok && (env == 1 || req == 2 || cl2_auto(g)) ? 1 : 0;
   }
   CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(tmaps);
   const CUtensorMapDataType BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;

@@ -297,3 +297,41 @@ def test_gemm_cluster_pairs(M, N, K, am, bm, mode):
         assert nrm(outs[1][0], acc) <= 5e-3
     else:
         assert nrm(outs[1][0], np.where(K0 > 0, np.maximum(acc + X0, 0.0), 0.0)) <= 5e-3
+
+
+@pytest.mark.parametrize("M,N,K", [(1000, 2048, 1024), (6272, 1024, 640), (384, 512, 200)])
+@pytest.mark.parametrize("am,bm", [(0, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("mode", [0, 1, 3, 5])
+def test_gemm_2cta_mma(M, N, K, am, bm, mode):
+    """2-CTA MMA pairs (tcgen05.mma.cta_group::2, M = 256 over a cluster of 2: each CTA stages its own 128 rows
+    of A and half of the B tile, the leader issues the MMAs, loads complete on the leader's barriers, both
+    CTAs' epilogues read their TMEM halves): same results as the single-CTA launch, within tolerance of fp64."""
+    t = _tofu()
+    rng = np.random.default_rng(M + N + K + mode + 3 * am + 5 * bm + 1)
+    A = q(rng, (K, M) if am else (M, K), 2 ** -7)
+    B = q(rng, (K, N) if bm else (N, K), 2 ** -9)
+    acc = (A.T if am else A) @ (B if bm else B.T)
+    c_mode = 0 if mode == 5 else mode
+    C0, W0 = q(rng, (M, N), 2 ** -5), q(rng, (M, N), 2 ** -7)
+    X0, K0 = q(rng, (M, N), 2 ** -6), q(rng, (M, N), 2 ** -6)
+    outs = []
+    for cl2 in (-1, 4):
+        kw = {}
+        if mode in (1, 3):
+            Cd = torch.from_numpy(C0 if mode == 3 else np.zeros((M, N))).float().cuda()
+        else:
+            Cd = torch.zeros((M, N), dtype=torch.bfloat16, device="cuda")
+        if mode == 3:
+            kw = dict(D=cuda_bf16(W0), ldd=N, s0=0.875, s1=0.0078125)
+        if mode == 5:
+            kw = dict(aux_add=cuda_bf16(X0), aux_mask=cuda_bf16(K0), ep=7)
+        t.gemm(cuda_bf16(A), cuda_bf16(B), Cd, M, N, K, M if am else K, am, N if bm else K, bm, N, c_mode, splits=1,
+               cl2=cl2, **kw)
+        torch.cuda.synchronize()
+        outs.append(Cd.double().cpu().numpy())
+    if mode in (1, 3):
+        assert nrm(outs[1], outs[0]) <= 1e-6
+    else:
+        assert nrm(outs[1], outs[0]) <= 2e-3
+    ref = {0: acc, 1: acc, 3: C0 * 0.875 + acc, 5: np.where(K0 > 0, np.maximum(acc + X0, 0.0), 0.0)}[mode]
+    assert nrm(outs[1], ref) <= (1e-5 if mode in (1, 3) else 5e-3)
