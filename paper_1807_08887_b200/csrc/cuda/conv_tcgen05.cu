@@ -50,10 +50,10 @@ struct RowInfo {
   int y, x;       // buffer coordinates before the tap offset
 };
 
-template <int KIND, int BN, int MODE>
+template <int KIND, int BN, int MODE, bool C2 = false>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (C2 ? BN / 2 : BN) * BK * 2;  // C2: this CTA's half of the B tile
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr bool LOADS = MODE == 2 || MODE == 3;
   static constexpr int NBUF = KIND == 1 ? 2 : 0;
@@ -101,12 +101,15 @@ __device__ __forceinline__ RowInfo no_pixel() {
 // CL2 (weight gradient with im2col): clusters of 2 CTAs on vertically adjacent tiles (output-channel tiles
 // 2p, 2p+1) of the same n tile share the gathered activations: each CTA im2col-loads half of the B sub-blocks
 // and multicasts them to both; a stage is freed by both CTAs' MMA commits (as gemm_tcgen05.cu's CL2).
-template <int KIND, int BN, bool B_MN, int MODE, bool I2C = false, bool CL2 = false>
+// C2 (with im2col): 2-CTA MMA pairs (tcgen05.mma.cta_group::2, M = 256 over a cluster of 2) on vertically
+// adjacent tiles: each CTA stages its own A rows and half of the B tile, loads complete on the leader's
+// barriers, the leader issues the MMAs, both CTAs' epilogues read their TMEM halves (gemm_tcgen05.cu's C2).
+template <int KIND, int BN, bool B_MN, int MODE, bool I2C = false, bool CL2 = false, bool C2 = false>
 __global__ void __launch_bounds__(NTHREADS, 1)
     conv_kernel(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap tmDense,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD,
                 const __grid_constant__ CUtensorMap tmI) {
-  using C_ = Cfg<KIND, BN, MODE>;
+  using C_ = Cfg<KIND, BN, MODE, C2>;
   constexpr int STAGES = C_::STAGES;
   constexpr int NBUF = C_::NBUF;
   const tofu_conv_args& a = P.a;
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int nk = (K + BK - 1) / BK;
   WorkList wl;
   uint32_t crank = 0;
-  if constexpr (CL2) {
+  if constexpr (CL2 || C2) {
     crank = cluster_rank();
     wl.init_pairs(tiles_m, tiles_n, nk, (int)crank, (int)cluster_id_x(), (int)nclusters_x());
   } else {
@@ -148,7 +151,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 4);
+      mbar_init(&acc_empty[b], C2 ? 8 : 4);  // C2: both CTAs' epilogue warps arrive on the leader's
     }
     for (int b = 0; b < 4 * NBUF; ++b) mbar_init(&ebar[b], 1);
     fence_mbar_init();
@@ -157,9 +160,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (MODE == 3) tma_prefetch_desc(&tmD);
     if (I2C) tma_prefetch_desc(&tmI);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, C_::TMEM_COLS);
+  if (warp == 1) {
+    if constexpr (C2) tmem_alloc2(tmem_slot, C_::TMEM_COLS);
+    else tmem_alloc(tmem_slot, C_::TMEM_COLS);
+  }
   tc_fence_before();
-  if constexpr (CL2) cluster_sync_all();
+  if constexpr (CL2 || C2) cluster_sync_all();
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
@@ -187,16 +193,26 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           const int k0 = kb * BK;
           if constexpr (KIND == 0) {
-            mbar_arrive_expect_tx(&full[s], C_::B_BYTES + (I2C ? C_::A_BYTES : 0));
+            const uint32_t lf = C2 ? mapa_shared(&full[s], 0) : 0u;
+            if constexpr (C2) {
+              if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * (C_::A_BYTES + C_::B_BYTES));
+            } else {
+              mbar_arrive_expect_tx(&full[s], C_::B_BYTES + (I2C ? C_::A_BYTES : 0));
+            }
             if constexpr (I2C) {
               const int t = k0 / a.nch, c = k0 - t * a.nch;
-              tma_load_im2col_4d(sA + s * C_::A_BYTES, &tmI, &full[s], a.sc0 + c, iw, ih, in_,
-                                 (uint16_t)(a.tap_dx[t] - P.dx0), (uint16_t)(a.tap_dy[t] - P.dy0));
+              if constexpr (C2)
+                tma_load_im2col_4d_2sm(sA + s * C_::A_BYTES, &tmI, lf, a.sc0 + c, iw, ih, in_,
+                                       (uint16_t)(a.tap_dx[t] - P.dx0), (uint16_t)(a.tap_dy[t] - P.dy0));
+              else
+                tma_load_im2col_4d(sA + s * C_::A_BYTES, &tmI, &full[s], a.sc0 + c, iw, ih, in_,
+                                   (uint16_t)(a.tap_dx[t] - P.dx0), (uint16_t)(a.tap_dy[t] - P.dy0));
             }
             uint8_t* b = sB + s * C_::B_BYTES;
             if (!B_MN) {  // W[n][taps][c]: columns tap_w[t]*b_tap + c
               const int col = (a.nch % BK == 0) ? a.tap_w[k0 / a.nch] * a.b_tap + k0 % a.nch : k0;
-              tma_load_2d(b, &tmDense, &full[s], col, n0);
+              if constexpr (C2) tma_load_2d_2sm(b, &tmDense, lf, col, n0 + (int)crank * (BN / 2));
+              else tma_load_2d(b, &tmDense, &full[s], col, n0);
             } else {      // W[c][taps][n]: rows = the K channels of one tap, columns tap_w[t]*b_tap + n
               // nch >= 64: one tap per k-block; nch in {8,16,32}: 64/nch taps, one box of nch rows each
               const int bk = a.nch < BK ? a.nch : BK;
@@ -211,10 +227,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               }
             }
           } else {
-            mbar_arrive_expect_tx(&full[s], C_::A_BYTES + (I2C ? C_::B_BYTES : 0));
+            const uint32_t lf = C2 ? mapa_shared(&full[s], 0) : 0u;
+            if constexpr (C2) {
+              if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * (C_::A_BYTES + C_::B_BYTES));
+            } else {
+              mbar_arrive_expect_tx(&full[s], C_::A_BYTES + (I2C ? C_::B_BYTES : 0));
+            }
             uint8_t* aa = sA + s * C_::A_BYTES;
 #pragma unroll
-            for (int q = 0; q < BM / 64; ++q) tma_load_2d(aa + q * 8192, &tmDense, &full[s], m0 + 64 * q, k0);
+            for (int q = 0; q < BM / 64; ++q) {
+              if constexpr (C2) tma_load_2d_2sm(aa + q * 8192, &tmDense, lf, m0 + 64 * q, k0);
+              else tma_load_2d(aa + q * 8192, &tmDense, &full[s], m0 + 64 * q, k0);
+            }
             if constexpr (I2C) {  // B rows = the k-block's 64 pixels, BN columns = channels of the tile's tap
               const int gb = k0 / ngyx, rem = k0 - gb * ngyx;
               const int gy = rem / a.ngx, gx = rem - gy * a.ngx;
@@ -222,7 +246,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               const uint16_t ow = (uint16_t)(a.tap_dx[t] - P.dx0), oh = (uint16_t)(a.tap_dy[t] - P.dy0);
 #pragma unroll
               for (int q = 0; q < BN / 64; ++q) {
-                if constexpr (CL2) {  // this CTA's half of the sub-blocks, multicast to the pair
+                if constexpr (C2) {  // this CTA's half of the sub-blocks, into its own (half-size) stage
+                  if (q >= BN / 128) continue;
+                  const int cc = (int)crank * (BN / 128) + q;
+                  tma_load_im2col_4d_2sm(sB + s * C_::B_BYTES + q * 8192, &tmI, lf, a.sc0 + c + 64 * cc,
+                                         a.ax * gx + a.cx + P.dx0, a.ay * gy + a.cy + P.dy0, gb + a.sb0, ow, oh);
+                } else if constexpr (CL2) {  // this CTA's half of the sub-blocks, multicast to the pair
                   if ((q >= BN / 128) != (crank != 0)) continue;
                   tma_load_im2col_4d_mc(sB + s * C_::B_BYTES + q * 8192, &tmI, &full[s], a.sc0 + c + 64 * q,
                                         a.ax * gx + a.cx + P.dx0, a.ay * gy + a.cy + P.dy0, gb + a.sb0, ow, oh, 0x3);
@@ -237,11 +266,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (C2: the pair leader only)
+    if (lane == 0 && (!C2 || crank == 0)) {
       constexpr bool A_MN = KIND == 1;
       constexpr bool BMN = KIND == 1 ? true : B_MN;
-      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN ? 1 : 0, BMN ? 1 : 0);
+      constexpr uint32_t idesc = umma_idesc_bf16(C2 ? 2 * BM : BM, BN, A_MN ? 1 : 0, BMN ? 1 : 0);
       int it = 0;
       for (int local = 0; local < nseg; ++local) {
         int tile, kb0, kb1, sp;
@@ -264,12 +293,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                      : umma_sdesc_sw128(a0 + kk * 32, 16, 1024);
             const uint64_t bd = BMN ? umma_sdesc_sw128(b0 + kk * 2048, 8192, 1024)
                                     : umma_sdesc_sw128(b0 + kk * 32, 16, 1024);
-            umma_bf16(tmem_d, ad, bd, idesc, (kb > kb0 || kk) ? 1u : 0u);
+            if constexpr (C2) umma_bf16_2(tmem_d, ad, bd, idesc, (kb > kb0 || kk) ? 1u : 0u);
+            else umma_bf16(tmem_d, ad, bd, idesc, (kb > kb0 || kk) ? 1u : 0u);
           }
-          if constexpr (CL2) umma_commit_mc(&empty[s], 0x3);
+          if constexpr (C2) umma_commit2_mc(&empty[s], 0x3);
+          else if constexpr (CL2) umma_commit_mc(&empty[s], 0x3);
           else umma_commit(&empty[s]);
         }
-        umma_commit(&acc_full[buf]);
+        if constexpr (C2) umma_commit2_mc(&acc_full[buf], 0x3);
+        else umma_commit(&acc_full[buf]);
       }
     }
   } else if (warp >= 6 && !I2C) {
@@ -400,7 +432,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (c == NCH - 1) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[acc]);
+            if (lane == 0) {
+            if constexpr (C2) mbar_arrive_cluster(mapa_shared(&acc_empty[acc], 0));
+            else mbar_arrive(&acc_empty[acc]);
+          }
           }
           if (part) {  // stream-K leading piece: fp32 partial to this CTA's workspace slot
             sk_write_chunk(sk_slot(sk_ws, blockIdx.x), q, NCH, c, lane, r);
@@ -535,7 +570,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (c == NCH - 1) {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&acc_empty[acc]);
+          if (lane == 0) {
+            if constexpr (C2) mbar_arrive_cluster(mapa_shared(&acc_empty[acc], 0));
+            else mbar_arrive(&acc_empty[acc]);
+          }
           ++local;
         }
         if (part) {
@@ -598,11 +636,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   }
   tc_fence_before();
-  if constexpr (CL2) cluster_sync_all();
+  if constexpr (CL2 || C2) cluster_sync_all();
   else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, C_::TMEM_COLS);
+    if constexpr (C2) tmem_dealloc2(tmem_base, C_::TMEM_COLS);
+    else tmem_dealloc(tmem_base, C_::TMEM_COLS);
   }
 }
 
@@ -827,10 +866,10 @@ static int auto_splits(const tofu_conv_args* a, int M, int N, int K, int bn) {
   return sp < 2 ? 1 : sp;
 }
 
-template <int KIND, int BN, bool B_MN, int MODE, bool I2C = false, bool CL2 = false>
+template <int KIND, int BN, bool B_MN, int MODE, bool I2C = false, bool CL2 = false, bool C2 = false>
 static int launch_t(const Params& P, const CUtensorMap* tm, cudaStream_t st) {
-  using C_ = Cfg<KIND, BN, MODE>;
-  auto kern = conv_kernel<KIND, BN, B_MN, MODE, I2C, CL2>;
+  using C_ = Cfg<KIND, BN, MODE, C2>;
+  auto kern = conv_kernel<KIND, BN, B_MN, MODE, I2C, CL2, C2>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM) != cudaSuccess)
@@ -849,7 +888,7 @@ static int launch_t(const Params& P, const CUtensorMap* tm, cudaStream_t st) {
                    ? sk_tiles_for(tiles, (P.K + BK - 1) / BK, g_sms, P.a.sk_ws, KIND == 1, 2 * M * N * K / bytes)
                    : 0;
   if (Q.sk_tiles) grid = g_sms;
-  if constexpr (CL2) {
+  if constexpr (CL2 || C2) {
     Q.sk_tiles = 0;
     const int pair_units = ((P.M + 2 * BM - 1) / (2 * BM)) * ((P.N + BN - 1) / BN);
     const int ncl = pair_units < g_sms / 2 ? pair_units : g_sms / 2;
@@ -875,8 +914,12 @@ static int dispatch(const Params& P, const CUtensorMap* tm, int mode, cudaStream
   const tofu_conv_args& a = P.a;
   const int bn = bn_of(&a, P.N);
   if (a.kind == 0) {
-    const int key = (bn == 256 ? 1 : 0) | (a.b_mn_major ? 2 : 0) | (mode << 2) | (a.im2col ? 8 : 0);
+    const int key = (bn == 256 ? 1 : 0) | (a.b_mn_major ? 2 : 0) | (mode << 2) | (a.im2col ? 8 : 0) |
+                    (a.cl2 == 3 ? 16 : 0);
+    if (a.cl2 == 3 && (bn != 256 || a.b_mn_major || !a.im2col)) return TOFU_ERR_ARG;  // (plan mismatch)
     switch (key) {
+      case 1 | 8 | 16: return launch_t<0, 256, false, 0, true, false, true>(P, tm, st);
+      case 1 | 4 | 8 | 16: return launch_t<0, 256, false, 1, true, false, true>(P, tm, st);
       case 8: return launch_t<0, 128, false, 0, true>(P, tm, st);
       case 9: return launch_t<0, 256, false, 0, true>(P, tm, st);
       case 10: return launch_t<0, 128, true, 0, true>(P, tm, st);
@@ -896,8 +939,13 @@ static int dispatch(const Params& P, const CUtensorMap* tm, int mode, cudaStream
       default: return TOFU_ERR_ARG;
     }
   }
-  const int key = mode | (bn == 256 ? 8 : 0) | (a.im2col ? 16 : 0) | (a.cl2 == 1 && bn == 256 && a.im2col ? 32 : 0);
+  const int key = mode | (bn == 256 ? 8 : 0) | (a.im2col ? 16 : 0) | (a.cl2 == 1 && bn == 256 && a.im2col ? 32 : 0) |
+                  (a.cl2 == 3 && bn == 256 && a.im2col ? 64 : 0);
+  if ((a.cl2 == 1 || a.cl2 == 3) && !(bn == 256 && a.im2col)) return TOFU_ERR_ARG;  // (plan mismatch)
   switch (key) {
+    case 1 | 8 | 16 | 64: return launch_t<1, 256, true, 1, true, false, true>(P, tm, st);
+    case 2 | 8 | 16 | 64: return launch_t<1, 256, true, 2, true, false, true>(P, tm, st);
+    case 3 | 8 | 16 | 64: return launch_t<1, 256, true, 3, true, false, true>(P, tm, st);
     case 1 | 8 | 16 | 32: return launch_t<1, 256, true, 1, true, true>(P, tm, st);
     case 2 | 8 | 16 | 32: return launch_t<1, 256, true, 2, true, true>(P, tm, st);
     case 3 | 8 | 16 | 32: return launch_t<1, 256, true, 3, true, true>(P, tm, st);
@@ -928,6 +976,14 @@ static bool natural_taps(const tofu_conv_args* a) {
   for (int t = 0; t < a->ntaps; ++t)
     if (a->tap_w[t] != t) return false;
   return true;
+}
+
+static int c2_env() {  // TOFU_C2=0 / 1: 2-CTA MMA pairs off / forced (A/B measurements); -1 = automatic
+  static const int v = [] {
+    const char* e = getenv("TOFU_C2");
+    return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
+  }();
+  return v;
 }
 
 // im2col TMA for the gathered activations (tmaps[4]): grids of stride <= 8, whole 64-channel blocks (kind 0: per
@@ -1016,7 +1072,23 @@ extern "C" int tofu_conv_plan(tofu_conv_args* a, void* tmaps) {
     }
     tm[1] = tm[2] = tm[3] = tm[4] = tm[0];
     a->splits = 1;
+    const int req = a->cl2 == 1 || a->cl2 == 3 ? 0 : a->cl2;  // (a re-plan decides afresh)
     try_im2col(a, tm, BM, BK);
+    // 2-CTA MMA pairs over vertically adjacent pixel tiles (each CTA stages half of the weight tile) for the
+    // im2col forward / data gradient with K-major weights.  They give up stream-K; measured on WResNet-152-4
+    // (bench.py --config 3, CUDA-graph replay, 2 runs each): 39.67 / 39.10 ms per step without, 39.00 / 38.41
+    // with (the SM clock under the power cap rose 1674 -> 1714 MHz), although the isolated per-launch times
+    // of the 3x3 forward rose (4.66 -> 5.03 ms per step, tools/breakdown.py).  TOFU_CONV_C2=0 turns them off.
+    static const bool fwd_c2 = [] {
+      const char* e = getenv("TOFU_CONV_C2");
+      return !(e && e[0] == '0');
+    }();
+    a->cl2 = 0;
+    if (req != -1 && c2_env() != 0 && a->im2col && !a->b_mn_major && bn == 256 && M > BM &&
+        (req == 4 || c2_env() == 1 || fwd_c2)) {
+      if (tmap2(&tm[0], a->Bp, BF, 2, a->b_cols, a->b_rows, a->ldb, 64, bn / 2, SW128)) return TOFU_ERR_CUDA;
+      a->cl2 = 3;
+    }
     return TOFU_OK;
   }
   // kind 1: A = output gradient [K pixels][M channels] MN-major; C f32 [M][N]
@@ -1025,13 +1097,16 @@ extern "C" int tofu_conv_plan(tofu_conv_args* a, void* tmaps) {
   a->splits = auto_splits(a, M, N, K, bn);
   tm[4] = tm[0];
   try_im2col(a, tm, BK, bn);  // the N tile (bn columns) must lie within one tap
-  {  // cluster pairs sharing the gathered activations (TOFU_CL2=0 off, 1 forced where eligible)
+  {  // cluster pairs sharing the gathered activations: 2-CTA MMA pairs (3) by default, multicast pairs (1) when
+     // TOFU_C2=0; TOFU_CL2=0 turns both off; on entry -1 forbids, 2 requests the multicast pairs, 4 the 2-CTA MMA
     static const int env = [] {
       const char* e = getenv("TOFU_CL2");
       return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
     }();
-    const bool ok = a->cl2 != -1 && env != 0 && a->im2col && a->splits <= 1 && bn == 256 && M > BM;
-    a->cl2 = ok && (env == 1 || a->cl2 == 2 || K >= 2048) ? 1 : 0;
+    const int req = a->cl2 == 1 || a->cl2 == 3 ? 0 : a->cl2;
+    const bool ok = req != -1 && env != 0 && a->im2col && a->splits <= 1 && bn == 256 && M > BM;
+    const bool pair = ok && (env == 1 || req == 2 || req == 4 || K >= 2048);
+    a->cl2 = !pair ? 0 : req == 2 ? 1 : req == 4 ? 3 : c2_env() != 0 ? 3 : 1;
   }
   if (tmap2(&tm[0], a->Ap, BF, 2, M, K, a->lda, 64, 64, SW128)) return TOFU_ERR_CUDA;
   if (tmap2(&tm[1], a->C, F32, 4, N, M, a->ldc, 32, 32, SW128)) return TOFU_ERR_CUDA;

@@ -251,13 +251,14 @@ def test_conv_im2col_stride2(kind):
 @pytest.mark.parametrize("which", ["wgrad", "wgrad_opt"])
 def test_conv_wgrad_cluster_pairs(data, which):
     """Weight gradient as clusters of 2 CTAs on adjacent output-channel tiles sharing the im2col-loaded
-    activations (tofu_conv_args.cl2, multicast halves): bitwise equal to the single-CTA launch."""
+    activations (tofu_conv_args.cl2): multicast halves (bitwise equal to the single-CTA launch) and 2-CTA MMA
+    pairs (cta_group::2, each CTA staging half of the activation tile; equal within fp32 rounding)."""
     t = _tofu()
     rng, X, W, D, ref = data
     Xd, Dd = cuda_bf16(X), cuda_bf16(D)
     M0, W0 = q(rng, (C, 3, 3, C), 2 ** -12), q(rng, (C, 3, 3, C), 2 ** -7)
     outs, modes = [], []
-    for cl2 in (-1, 2):
+    for cl2 in (-1, 2, 4):
         out = (torch.from_numpy(M0).float().cuda() if which == "wgrad_opt"
                else torch.zeros((C, 3, 3, C), dtype=torch.float32, device="cuda"))
         a = conv_args(t, 1, Xd, out, Y=Dd)
@@ -271,10 +272,48 @@ def test_conv_wgrad_cluster_pairs(data, which):
         t.conv(a)
         torch.cuda.synchronize()
         outs.append((out.double().cpu().numpy(), keep[0].double().cpu().numpy() if keep else None))
-    assert modes == [0, 1]
+    assert modes == [0, 1, 3]   # single CTA, multicast pairs, 2-CTA MMA pairs
     assert np.array_equal(outs[0][0], outs[1][0])
+    assert nrm(outs[2][0], outs[0][0]) <= 1e-6
     if which == "wgrad_opt":
         assert np.array_equal(outs[0][1], outs[1][1])
+        assert nrm(outs[2][1], outs[0][1]) <= 2e-3
         assert nrm(outs[1][0], M0 * 0.875 + ref["wgrad"]) <= 1e-5
     else:
         assert nrm(outs[1][0], ref["wgrad"]) <= 1e-5
+
+
+@pytest.mark.parametrize("which", ["fwd", "fwd_ep", "dgrad_kmajor"])
+def test_conv_fwd_2cta_mma(data, which):
+    """Forward / data gradient (K-major weights) with 2-CTA MMA pairs over adjacent pixel tiles
+    (tofu_conv_args.cl2 = 3: each CTA im2col-loads its 128 pixels and half of the weight tile, the leader
+    issues M = 256 MMAs): equal to the single-CTA launch and within tolerance of the fp64 convolution."""
+    t = _tofu()
+    rng, X, W, D, ref = data
+    Xd, Dd = cuda_bf16(X), cuda_bf16(D)
+    Wd = cuda_bf16(W)
+    WT = cuda_bf16(np.ascontiguousarray(W.transpose(3, 1, 2, 0)))   # [ci][ky][kx][co]: K-major for the dgrad
+    add, mask = q(rng, (B, H, H, C), 2 ** -6), q(rng, (B, H, H, C), 2 ** -6)
+    keep = [cuda_bf16(add), cuda_bf16(mask)]
+    outs, modes = [], []
+    for cl2 in (-1, 4):
+        out = torch.zeros((B, H, H, C), dtype=torch.bfloat16, device="cuda")
+        if which == "dgrad_kmajor":
+            # tap k = (ky, kx) reads D at (y + 1 - ky, x + 1 - kx) and the weight column block (ky, kx) of
+            # WT[ci][ky][kx][co] (K-major: rows = ci)
+            a = conv_args(t, 0, Dd, out, WT, 0, flip=True)
+        else:
+            a = conv_args(t, 0, Xd, out, Wd, 0)
+        if which == "fwd_ep":
+            a.ep, a.aux_add, a.aux_mask = 7, keep[0].data_ptr(), keep[1].data_ptr()
+        a.cl2 = cl2
+        modes.append(t.conv_plan(a).cl2)
+        t.conv(a)
+        torch.cuda.synchronize()
+        outs.append(out.double().cpu().numpy())
+    assert modes == [0, 3]
+    assert nrm(outs[1], outs[0]) <= 2e-3
+    r = ref["dgrad" if which == "dgrad_kmajor" else "fwd"]
+    if which == "fwd_ep":
+        r = np.where(mask > 0, np.maximum(r + add, 0.0), 0.0)
+    assert nrm(outs[1], r) <= 5e-3
