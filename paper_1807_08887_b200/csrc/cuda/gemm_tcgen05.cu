@@ -589,15 +589,16 @@ static int dispatch_bn(const tofu_gemm_args* g, const CUtensorMap* tm, const Pie
   const bool cl2 = BN == 256 && g->cl2 == 1 && !pc && mode != 4;
   // (the plan encoded B with half-height boxes for both pair kinds: a launch that cannot honour the pairing
   // would wait for bytes that never arrive)
-  const bool c2 = BN == 256 && g->cl2 == 3 && !pc && mode != 4;  // (4-warp epilogue instantiations)
+  const bool c2 = BN == 256 && g->cl2 == 3 && !pc && mode != 4;
   if ((g->cl2 == 1 && !cl2) || (g->cl2 == 3 && !c2)) return TOFU_ERR_ARG;
   if (c2) {
-    const int k2 = (g->a_mn_major ? 1 : 0) | (g->b_mn_major ? 2 : 0) | (mode << 2);
+    const int k2 = (g->a_mn_major ? 1 : 0) | (g->b_mn_major ? 2 : 0) | ((mode | (w8 ? 8 : 0)) << 2);
     switch (k2) {
 #define TOFU_CASE3(AM, BMJ, O) \
   case ((AM) | ((BMJ) << 1) | ((O) << 2)): return launch_t<BN, (bool)(AM), (bool)(BMJ), (O) | 16, false, true>(g, tm, pm, st, ai);
 #define TOFU_CASES3(O) TOFU_CASE3(0, 0, O) TOFU_CASE3(0, 1, O) TOFU_CASE3(1, 0, O) TOFU_CASE3(1, 1, O)
       TOFU_CASES3(0) TOFU_CASES3(1) TOFU_CASES3(2) TOFU_CASES3(3) TOFU_CASES3(5)
+      TOFU_CASES3(8) TOFU_CASES3(11) TOFU_CASES3(13)
 #undef TOFU_CASES3
 #undef TOFU_CASE3
       default: return TOFU_ERR_ARG;
@@ -792,7 +793,11 @@ extern "C" int tofu_gemm_plan_tmaps(tofu_gemm_args* g, void* tmaps, int* bn_out)
     // 2-CTA MMA pairs for compute-leaning launches (the 4-warp epilogue ones); measured (tools/gemm_major_bench.py,
     // tools/sk_bench.py): 8192^3 1182 -> 1294 TF/s (K-major), 1152 -> 1398 (both MN-major), the configs[1]
     // forward 62 -> 57 us; the memory-leaning fused epilogues lose up to 1.7x with 4 warps, so they keep W8
-    const bool c2 = ok && (req == 4 || (req == 0 && env2 != 0 && (env2 == 1 || !wants_w8(g))));
+    static const bool c2w8 = [] {  // TOFU_C2W8=1: 2-CTA pairs also with the 8-warp epilogue (A/B switch)
+      const char* e = getenv("TOFU_C2W8");
+      return e && e[0] == '1';
+    }();
+    const bool c2 = ok && (req == 4 || (req == 0 && env2 != 0 && (env2 == 1 || c2w8 || !wants_w8(g))));
     g->cl2 = c2 ? 3 : ok && (env == 1 || req == 2 || cl2_auto(g)) ? 1 : 0;
   }
   CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(tmaps);
