@@ -3,6 +3,7 @@
     python tools/breakdown.py <config>            # e.g. 3 (WResNet-152-4, batch 32)
     python tools/breakdown.py wresnet L W B IMG   # another WResNet
     python tools/breakdown.py units 1,1 W B IMG   # a WResNet with the given units per stage
+    python tools/breakdown.py lstm L H T B        # an LSTM (layers, hidden, steps, batch)
 Prints per-def totals (count, ms, share, TFLOP/s, GB/s) and the slowest individual launches."""
 import collections
 import os
@@ -15,7 +16,10 @@ from paper_1807_08887_b200.runner import TofuRunner  # noqa: E402
 from tofu_inputs.graphs import config, wresnet_depth  # noqa: E402
 from tofu_inputs.tensors import make_values  # noqa: E402
 
-if sys.argv[1] == "wresnet":
+if sys.argv[1] == "lstm":     # layers hidden steps batch
+    from tofu_inputs.graphs import lstm
+    spec = lstm(*map(int, sys.argv[2:6]))
+elif sys.argv[1] == "wresnet":
     spec = wresnet_depth(*map(int, sys.argv[2:6]))
 elif sys.argv[1] == "units":   # units "1,1" width batch image
     from tofu_inputs.graphs import wresnet
