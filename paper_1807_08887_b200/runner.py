@@ -13,7 +13,10 @@ shards at the offsets libtofu reports, and runs steps through tofu_execute.
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
+
 import torch
 
 from . import tofu
@@ -138,17 +141,19 @@ class TofuRunner:
     def train(self, host_batches, steps: int, result: str = "loss", start_event=None):
         """End-to-end training loop through the public API: every step copies that step's inputs from
         pinned host memory into the ranks' shards and reads the step's `result` back to the host.
-        The host->device copy of step s+1 runs on a copy stream while step s computes (double-buffered
+        The host->device copy of step s+1 runs on two copy streams while step s computes (double-buffered
         device staging); the result is read back asynchronously into pinned memory.
 
         host_batches: callable s -> {name: pinned host tensor (full shape)}.  Returns the pinned host
         tensor of per-step results (valid after the caller synchronises)."""
         comp = torch.cuda.current_stream()
-        copy = torch.cuda.Stream()
+        # two copy streams: one host->device stream reached ~27 GB/s on the B200 boxes, two ~51 GB/s
+        # (tools/h2d_bench.py); every input is split in row halves across them
+        copies = [torch.cuda.Stream() for _ in range(int(os.environ.get("TOFU_COPY_STREAMS", "2")))]
         names = list(host_batches(0).keys())
         slots = [(r, n) for r in self.local for n in names if self.view(r, n) is not None]
         bufs = [{s: torch.empty_like(self.view(*s)) for s in slots} for _ in range(2)]
-        ready = [torch.cuda.Event() for _ in range(2)]
+        ready = [[torch.cuda.Event() for _ in copies] for _ in range(2)]
         free = [torch.cuda.Event() for _ in range(2)]
         used = [False, False]
         res_view = None
@@ -156,22 +161,32 @@ class TofuRunner:
             res_view = self.view(r, result) if res_view is None else res_view
         out = torch.empty([steps] + (list(res_view.shape) if res_view is not None else []),
                           dtype=res_view.dtype if res_view is not None else torch.float32).pin_memory()
-        if start_event is not None:
-            copy.wait_event(start_event)
-        else:
-            copy.wait_stream(comp)
+        for c in copies:
+            if start_event is not None:
+                c.wait_event(start_event)
+            else:
+                c.wait_stream(comp)
 
         def issue(s):
             b = s % 2
             hb = host_batches(s)
-            with torch.cuda.stream(copy):
-                if used[b]:
-                    copy.wait_event(free[b])
-                for (r, n) in slots:
-                    _, box = self.shards[r][n]
-                    sl = tuple(slice(lo, hi + 1) for lo, hi in box)
-                    bufs[b][(r, n)].copy_(hb[n][sl], non_blocking=True)
-                ready[b].record(copy)
+            for ci, c in enumerate(copies):
+                with torch.cuda.stream(c):
+                    if used[b]:
+                        c.wait_event(free[b])
+                    for (r, n) in slots:
+                        _, box = self.shards[r][n]
+                        sl = tuple(slice(lo, hi + 1) for lo, hi in box)
+                        src, dst = hb[n][sl], bufs[b][(r, n)]
+                        if dst.dim() == 0:
+                            if ci == 0:
+                                dst.copy_(src, non_blocking=True)
+                            continue
+                        nc = len(copies)   # row blocks, one per copy stream
+                        h = (dst.shape[0] + nc - 1) // nc
+                        part = slice(min(ci * h, dst.shape[0]), min((ci + 1) * h, dst.shape[0]))
+                        dst[part].copy_(src[part], non_blocking=True)
+                    ready[b][ci].record(c)
             used[b] = True
 
         issue(0)
@@ -179,7 +194,8 @@ class TofuRunner:
             b = s % 2
             if s + 1 < steps:
                 issue(s + 1)
-            comp.wait_event(ready[b])
+            for ev in ready[b]:
+                comp.wait_event(ev)
             for sl in slots:
                 self.view(*sl).copy_(bufs[b][sl], non_blocking=True)
             free[b].record(comp)
