@@ -14,6 +14,8 @@
 // operand allows it, else V = 1).
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "../tofu_kernels.h"
 
@@ -55,6 +57,16 @@ __device__ __forceinline__ void ldv(const LOpnd& o, int64_t i, float (&v)[V]) {
       const float4 b = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(o.p) + i + 4);
       v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
     }
+  } else if (V == 4) {
+    if (o.dt == TOFU_BF16) {
+      const uint2 u = *reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(o.p) + i);
+      const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+      const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+      v[0] = f0.x; v[1] = f0.y; v[2 % V] = f1.x; v[3 % V] = f1.y;
+    } else {
+      const float4 a = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(o.p) + i);
+      v[0] = a.x; v[1 % V] = a.y; v[2 % V] = a.z; v[3 % V] = a.w;
+    }
   } else {
     v[0] = o.dt == TOFU_BF16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(o.p)[i])
                              : reinterpret_cast<const float*>(o.p)[i];
@@ -74,6 +86,15 @@ __device__ __forceinline__ void stv(void* p, int dt, int64_t i, const float (&v)
       float* f = reinterpret_cast<float*>(p) + i;
       *reinterpret_cast<float4*>(f) = make_float4(v[0], v[1], v[2], v[3]);
       *reinterpret_cast<float4*>(f + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    }
+  } else if (V == 4) {
+    if (dt == TOFU_BF16) {
+      uint2 u;
+      *reinterpret_cast<__nv_bfloat162*>(&u.x) = __floats2bfloat162_rn(v[0], v[1 % V]);
+      *reinterpret_cast<__nv_bfloat162*>(&u.y) = __floats2bfloat162_rn(v[2 % V], v[3 % V]);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p) + i) = u;
+    } else {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(p) + i) = make_float4(v[0], v[1 % V], v[2 % V], v[3 % V]);
     }
   } else {
     if (dt == TOFU_BF16) reinterpret_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(v[0]);
@@ -200,13 +221,22 @@ extern "C" int tofu_lstm_cell(int kind, int64_t nb, int64_t nh, int g0, int ng, 
   a.out2 = out2;
   a.out2_ld = out2_ld;
   a.out2_dt = out2_dt;
+  // 4 elements per thread when the operands allow 16-byte vectors: twice the threads of 8 per thread (the
+  // [128 x 4096] cells launched 65536 threads, 0.86 waves at 25% occupancy: latency-bound at 1.5 TB/s);
+  // TOFU_LSTM_V=8 keeps 8 (A/B switch)
+  static const int vpref = [] {
+    const char* e = getenv("TOFU_LSTM_V");
+    return e && e[0] == '8' ? 8 : 4;
+  }();
   const bool v8 = tofu::vec8_ok(a);
-  const int64_t n = nb * (v8 ? nh / 8 : nh);
+  const int vw = v8 ? vpref : 1;
+  const int64_t n = nb * (nh / vw);
   if (n == 0) return TOFU_OK;
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (v8) tofu::lstm_kernel<8><<<(unsigned)blocks, 256, 0, st>>>(a);
+  if (vw == 8) tofu::lstm_kernel<8><<<(unsigned)blocks, 256, 0, st>>>(a);
+  else if (vw == 4) tofu::lstm_kernel<4><<<(unsigned)blocks, 256, 0, st>>>(a);
   else tofu::lstm_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(a);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }
