@@ -904,7 +904,8 @@ void build_launches(Exec& E) {
       L.npieces = (int64_t)host.size() - L.piece_off;
       E.launches.push_back(L);
     }
-    if (bar_f && any_fetch) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
+    // (decided from all ranks, like bar_f: a rank without fetch pieces of its own still issues it)
+    if (bar_f) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
     for (int li = 0; li < nl; ++li) {
       if (E.lops[li][o].skip) continue;
       if (g.defs[g.ops[o].def].name == "sumsq") E.launches.push_back({4, (int)o, li, 0, 0, 0});

@@ -65,3 +65,35 @@ def test_ranks_agree(world, cfg):
         assert o["ledger"] == out[0]["ledger"]
     assert out[0]["ledger"] == out[0]["cost"]
     assert len(out[0]["bseq"]) >= 1 and out[0]["bseq"][-1] is None   # closing barrier
+
+
+def _barrier_seqs(spec, k):
+    """Each rank lowered alone (as its own process would): the op sequence of its device barriers."""
+    from paper_1807_08887_b200 import tofu
+    g = tofu.Graph(spec)
+    plan = tofu.Plan(g, k)
+    fake = [0x100000000 * (r + 1) for r in range(k)]
+    flags = [0x7f0000000000 + 64 * r for r in range(k)]
+    seqs = []
+    for r in range(k):
+        ex = tofu.Exec(g, plan, [r], fake, flags)
+        seqs.append([d["op"] for d in (ex.launch_desc(i) for i in range(ex.num_launches()))
+                     if d["kind"] == "barrier"])
+    return seqs
+
+
+@pytest.mark.parametrize("name,k", [("mlp", 4), ("mlp", 8), ("lstm", 4), ("lstm", 8), ("wres", 4), ("wres", 8)])
+def test_barrier_sequences_identical_across_ranks(name, k):
+    """every process must issue the same device-barrier sequence, including ranks with no
+    fetch pieces of their own for an op (one-sided halos of spatially split convolutions / pools).  The
+    small WResNet at k = 8 used to give odd ranks one barrier more than even ranks (at its pool op)."""
+    from paper_1807_08887_b200 import build
+    from tofu_inputs.graphs import lstm, mlp, wresnet
+    build.build(verbose=False)
+    spec = {"mlp": lambda: mlp(64, [256, 512, 512]),
+            "lstm": lambda: lstm(2, 64, 3, 16),
+            "wres": lambda: wresnet([2, 1, 1], 1, 4, 64, base=16, classes=24)}[name]()
+    seqs = _barrier_seqs(spec, k)
+    for r in range(1, k):
+        assert seqs[r] == seqs[0], (r, len(seqs[r]), len(seqs[0]))
+    assert seqs[0] and seqs[0][-1] is None
