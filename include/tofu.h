@@ -66,20 +66,25 @@ void tofu_graph_destroy(tofu_graph* g);
  * tofu_plan_create — per-tensor partition plan for k workers minimising communicated elements
  * (§5), by the recursive 2-way (kᵢ-way) DP over the coarsened graph.
  * Cost model: DESIGN.md §R3 (direct transfer).  k = Πkᵢ, kᵢ non-increasing primes.
- *   opts may be NULL (defaults: frontier_cap 64, solution_cap 256, search = recursive).
+ *   opts may be NULL (defaults: frontier_cap 64, solution_cap 256, search = 2 auto).
+ *   search = 2 (auto, reading R4 of DESIGN.md): the recursion, then — when the exact joint ("flat")
+ *   search is small (Σ over op classes of its factor-table cells <= 2^20) — the flat search, whose plan
+ *   replaces the recursion's only when strictly cheaper.  Under the direct-transfer cost model (R3) the
+ *   recursion misses the optimum on a few small graphs (tests/test_oracle_optimality.py); auto returns the
+ *   exhaustive optimum on every graph small enough to check it.
  * Errors: TOFU_ERR_PLAN when some tensor/op has no divisible axis at a step.
  */
 typedef struct {
   int frontier_cap;  /* co-optimal prefixes kept per step (>=1) */
   int solution_cap;  /* co-optimal step plans enumerated per prefix (>=1) */
-  int search;        /* 0 = recursive (paper), 1 = flat exact (all steps jointly; small graphs) */
+  int search;        /* 0 = recursive (paper), 1 = flat exact (all steps jointly; small graphs), 2 = auto */
 } tofu_plan_options;
 
 typedef struct tofu_plan tofu_plan;
 int tofu_plan_create(const tofu_graph* g, int k, const tofu_plan_options* opts, tofu_plan** out);
 void tofu_plan_destroy(tofu_plan* p);
 /* {"k","factors":[..],"tdims":{t:[d|null..]},"osplit":{op:[var..]},"cost":elements,"bytes":B,
- *  "deltas":[..],"frontier_truncated":bool,"search_ms":ms} */
+ *  "deltas":[..],"frontier_truncated":bool,"search":"recursive"|"flat","search_ms":ms} */
 int tofu_plan_json(const tofu_plan* p, char* out, size_t cap, size_t* len);
 int tofu_plan_cost(const tofu_plan* p, int64_t* elements, int64_t* bytes);
 

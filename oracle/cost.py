@@ -107,6 +107,16 @@ def _inter(a, b):
 def op_cost_box(g, op, tdims, osplit, factors):
     """(elements, bytes, fetch_elems, out_elems) of one op under a plan
     prefix.  tdims[t] / osplit[op] are sequences of len(factors)."""
+    sl = op_cost_slots(g, op, tdims, osplit, factors)
+    fetch = sum(e for kind, _, e, _ in sl if kind == "in")
+    out = sum(e for kind, _, e, _ in sl if kind == "out")
+    return fetch + out, sum(b for _, _, _, b in sl), fetch, out
+
+
+def op_cost_slots(g, op, tdims, osplit, factors):
+    """The terms of op_cost_box, one per operand slot: [("in", param, elements, bytes) for each input
+    param that is read, then ("out", output, elements, bytes)].  The cost above is the sum of these
+    slots, and a slot's term reads only its own tensor's dim sequence (and the op's split sequence)."""
     d = g.opdef(op)
     R = g.ranges[op["name"]]
     var_order = d.all_vars()
@@ -115,8 +125,9 @@ def op_cost_box(g, op, tdims, osplit, factors):
     for k in factors:
         nw *= k
     partial = any(v in d.red_vars for v in seq)
-    fetch = out = 0
-    fetch_b = out_b = 0
+    slots = {p_: [0, 0] for p_, _ in d.params}
+    read = set()
+    o_el = o_by = 0
     param_t = {p: t for (p, _), t in zip(d.params, op["inputs"])}
     param_off = {p: off for (p, _), off in zip(d.params, op["offsets"])}
     o_t = op["output"]
@@ -136,19 +147,20 @@ def op_cost_box(g, op, tdims, osplit, factors):
                 req = r if req is None else [(min(a[0], b[0]), max(a[1], b[1])) for a, b in zip(req, r)]
             if req is None:
                 continue
+            read.add(p_)
             req = clip(req, shape)
             own = owned_box(shape, tdims[t], factors, dig)
             n_req = _vol(req)
             n_loc = 0 if own is None else _vol(_inter(req, own))
-            fetch += n_req - n_loc
-            fetch_b += (n_req - n_loc) * ITEMSIZE[g.tensors[t]["dtype"]]
+            slots[p_][0] += n_req - n_loc
+            slots[p_][1] += (n_req - n_loc) * ITEMSIZE[g.tensors[t]["dtype"]]
         prod = [(ib[v][0] + off, ib[v][1] + off) for v, off in zip(d.out_vars, op["out_offset"])]
         own = owned_box(g.shape(o_t), tdims[o_t], factors, dig)
         n_p = _vol(prod)
         n_loc = 0 if own is None else _vol(_inter(prod, own))
-        out += n_p - n_loc
-        out_b += (n_p - n_loc) * (4 if partial else ITEMSIZE[g.tensors[o_t]["dtype"]])
-    return fetch + out, fetch_b + out_b, fetch, out
+        o_el += n_p - n_loc
+        o_by += (n_p - n_loc) * (4 if partial else ITEMSIZE[g.tensors[o_t]["dtype"]])
+    return [("in", p_, slots[p_][0], slots[p_][1]) for p_, _ in d.params if p_ in read] + [("out", o_t, o_el, o_by)]
 
 
 def _owner_of(idx, shape, dims_seq, factors):

@@ -13,10 +13,15 @@
   prefix (cost.py); the set of co-optimal prefixes is carried forward
   (reading §R4: ties are kept because under the direct-transfer model the
   paper's commutativity argument, does not hold exactly).
-* ``brute_force`` — exhaustive over all sequences of per-tensor dims and
-  per-op strategies (tiny graphs) — the optimum the recursion must match.
+* ``brute_force`` — exhaustive over all sequences of per-CLASS dims and
+  per-op-class strategies (tiny graphs).
+* ``brute_force_per_tensor`` — exhaustive over all per-TENSOR assignments
+  (no coarsening): the optimum that pins both the coarsening
+  and the searches.
 * ``flat_search`` — the same variable elimination over *sequence-valued*
   variables (all m steps at once): exact global optimum for small graphs.
+* ``auto_search`` — the recursion, plus the flat search when it is cheap,
+  keeping the strictly cheaper plan (reading R4).
 """
 from __future__ import annotations
 
@@ -24,7 +29,7 @@ import itertools
 
 import numpy as np
 
-from .cost import op_cost_box, plan_cost
+from .cost import op_cost_box, op_cost_slots, plan_cost
 
 
 def factorize(k: int):
@@ -345,6 +350,8 @@ def flat_search(g, k, cap=1):
     tclass, classes, oclass, op_classes = g.coarsen()
     tdom = [_seq_domain_tensor(g, ms, factors) for ms in classes]
     odom = [_seq_domain_op(g, ms, factors) for ms in op_classes]
+    if any(not d for d in tdom + odom):
+        raise SearchError("flat search: a class has no divisible split sequence")
     nT = len(classes)
     domains = tdom + odom
     fs = []
@@ -353,15 +360,30 @@ def flat_search(g, k, cap=1):
                       for t in list(g.op(name)["inputs"]) + [g.op(name)["output"]]})
         scope = tcs + [nT + oc]
         shape = [len(domains[x]) for x in scope]
+        # the op cost is a sum of per-slot terms, each reading one tensor's sequence (cost.op_cost_slots):
+        # table[tensor classes..., op] = Σ_members Σ_slots term(slot's class sequence, op sequence)
         table = np.zeros(shape, dtype=np.int64)
-        for idx in itertools.product(*[range(s) for s in shape]):
-            choice = {x: domains[x][i] for x, i in zip(scope, idx)}
-            val = 0
-            for name in members:
-                op = g.op(name)
-                td = {t: list(choice[tclass[t]]) for t in list(op["inputs"]) + [op["output"]]}
-                val += op_cost_box(g, op, td, {name: list(choice[nT + oc])}, factors)[0]
-            table[idx] = val
+        for name in members:
+            op = g.op(name)
+            ts = list(op["inputs"]) + [op["output"]]
+            base = {t: list(domains[tclass[t]][0]) for t in ts}
+            slot_t = [t for (p_, _), t in zip(g.opdef(op).params, op["inputs"])] + [op["output"]]
+            slot_p = [p_ for p_, _ in g.opdef(op).params] + [op["output"]]
+            for si, (t, pname) in enumerate(zip(slot_t, slot_p)):
+                c = tclass[t]
+                ax = scope.index(c)
+                term = np.zeros((len(domains[c]), len(odom[oc])), dtype=np.int64)
+                for qi, q in enumerate(domains[c]):
+                    td = dict(base)
+                    td[t] = list(q)
+                    for oi, oseq in enumerate(odom[oc]):
+                        kind = "out" if si == len(slot_t) - 1 else "in"
+                        term[qi, oi] = sum(e for k_, p2, e, _ in op_cost_slots(g, op, td, {name: list(oseq)}, factors)
+                                           if k_ == kind and p2 == pname)
+                bshape = [1] * len(scope)
+                bshape[ax] = len(domains[c])
+                bshape[-1] = len(odom[oc])
+                table = table + term.reshape(bshape)
         fs.append((scope, table))
     total, sols = _VE(domains, fs).run(cap)
     s = sols[0]
@@ -369,3 +391,127 @@ def flat_search(g, k, cap=1):
             "tdims": {t: list(tdom[tclass[t]][s[tclass[t]]]) for t in g.tensors},
             "osplit": {o["name"]: list(odom[oclass[o["name"]]][s[nT + oclass[o["name"]]]]) for o in g.ops}}
     return total, plan
+
+
+# --------------------------------------------------------------------------- per-tensor brute force
+def _seq_domain_single_tensor(shape, factors):
+    """All split-dim sequences of ONE tensor (no class): dims whose extent stays divisible."""
+    if len(shape) == 0:
+        return [tuple([None] * len(factors))]
+    out = []
+    for seq in itertools.product(range(len(shape)), repeat=len(factors)):
+        n = list(shape)
+        ok = True
+        for i, d in enumerate(seq):
+            if n[d] % factors[i]:
+                ok = False
+                break
+            n[d] //= factors[i]
+        if ok:
+            out.append(seq)
+    return out
+
+
+def _seq_domain_single_op(g, op, factors):
+    out = []
+    for seq in itertools.product(g.split_vars(op), repeat=len(factors)):
+        n = dict(g.ranges[op["name"]])
+        ok = True
+        for i, v in enumerate(seq):
+            if n[v] % factors[i]:
+                ok = False
+                break
+            n[v] //= factors[i]
+        if ok:
+            out.append(seq)
+    return out
+
+
+def brute_force_per_tensor(g, k, limit=1 << 24):
+    """Exhaustive minimum over ALL per-tensor partition assignments — every tensor and every op chooses
+    its own split sequence, with no coarsening (no element-wise / timestep / alias classes) — the
+    north star's "brute-force enumeration of all per-tensor partition assignments".
+
+    Enumeration: a dense array over the joint assignment of every tensor (one axis per tensor, one entry
+    per divisible sequence, so Π|domain| cells: every assignment is visited); each op adds, broadcast
+    over its own tensors' axes, the cost of its best strategy sequence for that assignment of its tensors
+    (given the tensors, the ops' terms are independent, so minimising each separately is exhaustive).
+    No variable elimination: independent of ``flat_search``'s engine.  Returns (cost, plan)."""
+    factors = factorize(k)
+    names = sorted(g.tensors)
+    tdom = [_seq_domain_single_tensor(g.shape(t), factors) for t in names]
+    if any(not d for d in tdom):
+        raise SearchError("a tensor has no divisible split sequence")
+    axis = {t: i for i, t in enumerate(names)}
+    cells = 1
+    for d in tdom:
+        cells *= len(d)
+    if cells > limit:
+        raise SearchError(f"brute force too large ({cells} assignments)")
+    total = np.zeros([len(d) for d in tdom], dtype=np.int64)
+    best_op = []
+    for op in g.ops:
+        odom = _seq_domain_single_op(g, op, factors)
+        if not odom:
+            raise SearchError(f"op {op['name']} has no divisible split sequence")
+        ts = sorted({axis[t] for t in list(op["inputs"]) + [op["output"]]})
+        shape = [len(tdom[a]) for a in ts]
+        tab = np.zeros(shape, dtype=np.int64)
+        arg = np.zeros(shape, dtype=np.int64)
+        for idx in itertools.product(*[range(s) for s in shape]):
+            td = {names[a]: list(tdom[a][i]) for a, i in zip(ts, idx)}
+            vals = [op_cost_box(g, op, td, {op["name"]: list(s)}, factors)[0] for s in odom]
+            j = int(np.argmin(vals))
+            tab[idx] = vals[j]
+            arg[idx] = j
+        bshape = [len(tdom[a]) if a in ts else 1 for a in range(len(names))]
+        total += tab.reshape(bshape)
+        best_op.append((op, ts, arg, odom))
+    flat_i = int(np.argmin(total))
+    cost = int(total.reshape(-1)[flat_i])
+    where = np.unravel_index(flat_i, total.shape)
+    tdims = {t: list(tdom[axis[t]][where[axis[t]]]) for t in names}
+    osplit = {}
+    for op, ts, arg, odom in best_op:
+        osplit[op["name"]] = list(odom[int(arg[tuple(where[a] for a in ts)])])
+    return cost, {"factors": factors, "tdims": tdims, "osplit": osplit}
+
+
+# --------------------------------------------------------------------------- auto (recursion + exact check)
+FLAT_AUTO_CELLS = 1 << 20
+
+
+def flat_cells(g, k):
+    """Σ over op classes of the flat search's factor-table cells (Π of its scope's sequence-domain sizes):
+    the size test of the ``auto`` search.  Domains are enumerated exactly as ``flat_search`` does."""
+    factors = factorize(k)
+    tclass, classes, oclass, op_classes = g.coarsen()
+    tn = [len(_seq_domain_tensor(g, ms, factors)) for ms in classes]
+    on = [len(_seq_domain_op(g, ms, factors)) for ms in op_classes]
+    tot = 0
+    for oc, members in enumerate(op_classes):
+        tcs = sorted({tclass[t] for name in members for t in list(g.op(name)["inputs"]) + [g.op(name)["output"]]})
+        n = on[oc]
+        for c in tcs:
+            n *= tn[c]
+        tot += n
+    return tot
+
+
+def auto_search(g, k, cap=256, frontier_cap=64):
+    """The paper's recursion, then — when the graph is small enough that the exact joint
+    search is cheap (``flat_cells`` <= FLAT_AUTO_CELLS) — the flat exact search, keeping the flat plan
+    only if it is strictly cheaper.  Reading R4: under the direct-transfer cost model the recursion is not
+    always optimal (named cases in tests/test_oracle_optimality.py), so small graphs get the exact
+    optimum.  Returns the plan dict of ``recursive_search`` plus 'search': 'recursive' | 'flat'."""
+    rec = recursive_search(g, k, cap, frontier_cap)
+    rec["search"] = "recursive"
+    if k == 1 or flat_cells(g, k) > FLAT_AUTO_CELLS:
+        return rec
+    c, fp = flat_search(g, k)
+    if c < rec["cost"]:
+        from .cost import step_costs
+        el, by = plan_cost(g, fp)
+        return dict(fp, cost=el, bytes=by, deltas=step_costs(g, fp), frontier_truncated=rec["frontier_truncated"],
+                    search="flat")
+    return rec

@@ -363,7 +363,7 @@ StepResult step_search(const Graph& g, const PlanSeq& pre, int k, int cap, CostM
 
 }  // namespace
 
-PlanResult make_plan(const Graph& g, int k, int frontier_cap, int solution_cap, int search) {
+static PlanResult make_plan_mode(const Graph& g, int k, int frontier_cap, int solution_cap, int search) {
   auto t0 = std::chrono::steady_clock::now();
   PlanResult r;
   r.k = k;
@@ -504,6 +504,82 @@ PlanResult make_plan(const Graph& g, int k, int frontier_cap, int solution_cap, 
   return r;
 }
 
+// Σ over op classes of the flat search's factor-table cells (product of the sequence-domain sizes of the
+// class's tensor classes and its own): the size test of search = 2 (matches oracle.search.flat_cells).
+static int64_t flat_cells(const Graph& g, const std::vector<int>& factors) {
+  const int nT = (int)g.classes.size(), nO = (int)g.op_classes.size();
+  const int m = (int)factors.size();
+  std::vector<int64_t> dsize(nT + nO, 0);
+  for (int c = 0; c < nT + nO; ++c) {
+    bool is_t = c < nT;
+    int rank = is_t ? (int)g.tensors[g.classes[c][0]].shape.size() : 0;
+    std::vector<int> axes = is_t ? std::vector<int>() : g.def_of(g.op_classes[c - nT][0]).split_vars();
+    if (is_t)
+      for (int d = 0; d < rank; ++d) axes.push_back(d);
+    if (is_t && rank == 0) {
+      dsize[c] = 1;
+      continue;
+    }
+    std::vector<int> seq(m, 0);
+    std::function<void(int)> rec = [&](int i) {
+      if (i == m) {
+        const auto& members = is_t ? g.classes[c] : g.op_classes[c - nT];
+        for (int x : members)
+          for (int a : axes) {
+            int64_t n = is_t ? g.tensors[x].shape[a] : g.ops[x].R[a];
+            for (int st = 0; st < m; ++st)
+              if (seq[st] == a) {
+                if (n % factors[st]) return;
+                n /= factors[st];
+              }
+          }
+        ++dsize[c];
+        return;
+      }
+      for (int a : axes) {
+        seq[i] = a;
+        rec(i + 1);
+      }
+    };
+    rec(0);
+  }
+  int64_t tot = 0;
+  for (int oc = 0; oc < nO; ++oc) {
+    std::set<int> tcs;
+    for (int o : g.op_classes[oc]) {
+      for (int t : g.ops[o].inputs) tcs.insert(g.tclass[t]);
+      tcs.insert(g.tclass[g.ops[o].output]);
+    }
+    int64_t n = dsize[nT + oc];
+    for (int c : tcs) n = std::min<int64_t>(n * dsize[c], INT64_C(1) << 40);
+    tot = std::min<int64_t>(tot + n, INT64_C(1) << 40);
+  }
+  return tot;
+}
+
+PlanResult make_plan(const Graph& g, int k, int frontier_cap, int solution_cap, int search) {
+  if (search != 2) {
+    PlanResult r = make_plan_mode(g, k, frontier_cap, solution_cap, search);
+    r.search = search == 1 ? "flat" : "recursive";
+    return r;
+  }
+  // auto (reading R4): the recursion; on graphs whose exact joint search is cheap, that search too,
+  // keeping its plan only when strictly cheaper (the recursion is not always optimal under R3)
+  auto t0 = std::chrono::steady_clock::now();
+  PlanResult r = make_plan_mode(g, k, frontier_cap, solution_cap, 0);
+  r.search = "recursive";
+  if (k > 1 && flat_cells(g, factorize(k)) <= kFlatAutoCells) {
+    PlanResult f = make_plan_mode(g, k, frontier_cap, solution_cap, 1);
+    if (f.cost < r.cost) {
+      f.truncated = r.truncated;
+      r = f;
+      r.search = "flat";
+    }
+  }
+  r.search_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return r;
+}
+
 std::string plan_json(const Graph& g, const PlanResult& r) {
   std::string o = "{\"k\":" + std::to_string(r.k) + ",\"factors\":[";
   for (size_t i = 0; i < r.seq.factors.size(); ++i) o += (i ? "," : "") + std::to_string(r.seq.factors[i]);
@@ -524,7 +600,7 @@ std::string plan_json(const Graph& g, const PlanResult& r) {
   o += "},\"cost\":" + std::to_string(r.cost) + ",\"bytes\":" + std::to_string(r.bytes) + ",\"deltas\":[";
   for (size_t i = 0; i < r.deltas.size(); ++i) o += (i ? "," : "") + std::to_string(r.deltas[i]);
   o += "],\"frontier_truncated\":" + std::string(r.truncated ? "true" : "false") +
-       ",\"search_ms\":" + json_num(r.search_ms) + "}";
+       ",\"search\":" + json_quote(r.search) + ",\"search_ms\":" + json_num(r.search_ms) + "}";
   return o;
 }
 
@@ -542,7 +618,7 @@ const PlanResult& plan_of(const tofu_plan* p) { return p->r; }
 extern "C" int tofu_plan_create(const tofu_graph* g, int k, const tofu_plan_options* opts, tofu_plan** out) {
   return tofu::guard([&]() {
     if (!g || !out || k < 1) throw tofu::Error(TOFU_ERR_ARG, "bad argument");
-    int fc = 64, sc = 256, search = 0;
+    int fc = 64, sc = 256, search = 2;
     if (opts) {
       if (opts->frontier_cap > 0) fc = opts->frontier_cap;
       if (opts->solution_cap > 0) sc = opts->solution_cap;

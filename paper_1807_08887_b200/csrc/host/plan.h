@@ -17,7 +17,10 @@ struct PlanResult {
   std::vector<int64_t> deltas;
   bool truncated = false;
   double search_ms = 0;
+  std::string search = "recursive";   // the search that produced seq: "recursive" | "flat"
 };
+
+constexpr int64_t kFlatAutoCells = INT64_C(1) << 20;   // search = 2: flat search when flat_cells <= this
 
 PlanResult make_plan(const Graph& g, int k, int frontier_cap, int solution_cap, int search);
 std::string plan_json(const Graph& g, const PlanResult& r);

@@ -221,7 +221,7 @@ class Graph:
 
 
 class Plan:
-    def __init__(self, graph: Graph, k: int, frontier_cap=64, solution_cap=256, search=0):
+    def __init__(self, graph: Graph, k: int, frontier_cap=64, solution_cap=256, search=2):
         self.graph = graph
         self.k = k
         h = C.c_void_p()

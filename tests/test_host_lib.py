@@ -13,7 +13,7 @@ import pytest
 from fixtures import random_chain
 from oracle.cost import owned_box, digits, plan_cost
 from oracle.graph import Graph as OGraph
-from oracle.search import SearchError, flat_search, recursive_search
+from oracle.search import SearchError, auto_search, flat_search, recursive_search
 from oracle.strategy import discover_strategies
 from oracle.tdl import parse_def, parse_program
 from tofu_inputs.graphs import config, mlp
@@ -97,17 +97,43 @@ def test_plan_bit_exact_vs_oracle_random(tofu):
         og = OGraph(spec)
         for k in (2, 4, 8):
             try:
-                o = recursive_search(og, k)
+                o = auto_search(og, k)
             except SearchError:
                 with pytest.raises(tofu.TofuError):
                     tofu.Plan(tofu.Graph(spec), k)
                 continue
             p = tofu.Plan(tofu.Graph(spec), k).json()
-            assert (p["cost"], p["bytes"], p["deltas"]) == (o["cost"], o["bytes"], o["deltas"]), (s, k)
+            assert (p["cost"], p["bytes"], p["deltas"], p["search"]) == \
+                (o["cost"], o["bytes"], o["deltas"], o["search"]), (s, k)
             if not o["frontier_truncated"]:
                 assert p["tdims"] == o["tdims"] and p["osplit"] == o["osplit"], (s, k)
             n += 1
     assert n > 60
+
+
+@pytest.mark.parametrize("args,k", [((1, 8, 3, 4), 2), ((1, 8, 3, 4), 4), ((1, 8, 3, 4), 8), ((2, 8, 2, 4), 4)])
+def test_plan_bit_exact_vs_oracle_lstm(tofu, args, k):
+    """LSTM graphs (timestep merging, views, 3-D gate tensors): the C++ plan equals the oracle's bit for bit
+    (auto search: the recursion here, the flat search at k = 2 confirms it is optimal)."""
+    from tofu_inputs.graphs import lstm
+    spec = lstm(*args)
+    o = auto_search(OGraph(spec), k)
+    p = tofu.Plan(tofu.Graph(spec), k).json()
+    assert (p["cost"], p["bytes"], p["deltas"], p["search"]) == (o["cost"], o["bytes"], o["deltas"], o["search"])
+    assert p["tdims"] == o["tdims"] and p["osplit"] == o["osplit"]
+
+
+def test_auto_plan_reaches_the_optimum_on_known_gaps(tofu):
+    """The named recursion gaps (tests/test_oracle_optimality.py): the library's default (auto) search
+    returns the exact optimum, equal to the oracle's auto search; search = 0 keeps the paper's recursion."""
+    from test_oracle_optimality import KNOWN_RECURSION_GAPS
+    for (s, k), (rec, opt) in sorted(KNOWN_RECURSION_GAPS.items()):
+        spec = random_chain(s)
+        p = tofu.Plan(tofu.Graph(spec), k).json()
+        o = auto_search(OGraph(spec), k)
+        assert p["cost"] == o["cost"] == opt and p["search"] == o["search"] == "flat", (s, k)
+        assert p["deltas"] == o["deltas"] and p["bytes"] == o["bytes"]
+        assert tofu.Plan(tofu.Graph(spec), k, search=0).json()["cost"] == rec
 
 
 def test_flat_search_equals_oracle(tofu):
@@ -172,11 +198,11 @@ def test_wresnet_plan_bit_exact_and_ledger(tofu, k, units):
     executor moves exactly the planned bytes (halo and strided-gradient regions included)."""
     from tofu_inputs.graphs import wresnet
     spec = wresnet(units, 1, 8, 16 if k == 2 else 8, base=4, classes=8)
-    o = recursive_search(OGraph(spec), k)
+    o = auto_search(OGraph(spec), k)   # k = 4: the flat search beats the recursion (5871 vs 5999 elements)
     g = tofu.Graph(spec)
     plan = tofu.Plan(g, k)
     p = plan.json()
-    assert (p["cost"], p["bytes"], p["deltas"]) == (o["cost"], o["bytes"], o["deltas"])
+    assert (p["cost"], p["bytes"], p["deltas"], p["search"]) == (o["cost"], o["bytes"], o["deltas"], o["search"])
     if not o["frontier_truncated"]:
         assert p["tdims"] == o["tdims"] and p["osplit"] == o["osplit"]
     fake = [0x100000000 * (r + 1) for r in range(k)]
