@@ -120,6 +120,11 @@ int tofu_exec_num_launches(const tofu_exec* e, int* n);
 /* JSON {"index","kind":"fetch"|"compute"|"reduce"|"barrier"|"memset","op","def","rank","flops",
  *       "bytes"}: flops = 2·M·N·K for GEMM sub-ops; bytes = algorithmic bytes read + written. */
 int tofu_exec_launch_desc(const tofu_exec* e, int index, char* out, size_t cap, size_t* len);
+/* JSON list of the tensors the step never writes to HBM on some rank: intermediates of fused chains
+ * (R8 / R13 — a weight gradient folded into the optimizer epilogue, a GEMM / convolution output
+ * folded into its element-wise consumer).  Their storage holds no defined value after tofu_execute; parity
+ * tests check them through their consumers.  Errors: TOFU_ERR_ARG (null exec) / TOFU_ERR_CAPACITY. */
+int tofu_exec_unmaterialized(const tofu_exec* e, char* out, size_t cap, size_t* len);
 /* Issue launches [first, last) only (instrumented timing). */
 int tofu_execute_range(tofu_exec* e, int first, int last, void* stream);
 /* Record cudaEvent_t ev_start / ev_stop (on the execute stream) around launch `index` during every

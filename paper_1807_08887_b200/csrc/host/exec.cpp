@@ -154,6 +154,7 @@ struct Exec {
   void* flags_dev = nullptr;        // device array of flag pointers
   std::vector<Layout> lay;          // all ranks
   std::vector<std::vector<LOp>> lops;  // [local index][op]
+  std::set<int> unmat;              // tensors some rank never writes to HBM (fused intermediates, R8/R13)
   struct Launch {
     int kind;  // 0 fetch pieces, 1 compute, 2 reduce pieces, 3 barrier, 4 memset
     int op, li;
@@ -703,6 +704,7 @@ void lower(Exec& E) {
         LOp& La = all[r][o];
         if (clash || !La.out.direct || La.partial || La.out.dtype != TOFU_F32) continue;
         La.fused_opt = reader;
+        E.unmat.insert(a.output);   // the weight gradient stays in TMEM / registers
         all[r][reader].skip = true;
       }
   // LSTM: the two cell ops of one timestep read the same gate rows -> one kernel (one pass over GX / GH)
@@ -834,7 +836,9 @@ void lower(Exec& E) {
         if (e2 >= 0) {
           Lo.epi_mask = mask;
           all[r][e2].skip = true;
+          E.unmat.insert(g.ops[e].output);   // the gradient sum before its mask
         }
+        E.unmat.insert(t);                   // the producer's own (pre-epilogue) output
         Lo.out = out;
         Le.skip = true;
       }
@@ -1793,6 +1797,15 @@ extern "C" int tofu_exec_launch_desc(const tofu_exec* h, int index, char* out, s
   return tofu::guard([&]() {
     if (!h || index < 0 || index >= (int)h->e.launches.size()) throw tofu::Error(TOFU_ERR_ARG, "bad launch index");
     return tofu::write_out(tofu::launch_desc(h->e, index), out, cap, len);
+  });
+}
+
+extern "C" int tofu_exec_unmaterialized(const tofu_exec* h, char* out, size_t cap, size_t* len) {
+  return tofu::guard([&]() {
+    if (!h) throw tofu::Error(TOFU_ERR_ARG, "null exec");
+    std::string o = "[";
+    for (int t : h->e.unmat) o += (o.size() > 1 ? "," : "") + tofu::json_quote(h->e.g->tensors[t].name);
+    return tofu::write_out(o + "]", out, cap, len);
   });
 }
 

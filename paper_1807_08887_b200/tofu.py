@@ -108,6 +108,7 @@ def lib():
             "tofu_exec_set_skip_comm": [vp, C.c_int],
             "tofu_exec_num_launches": [vp, C.POINTER(C.c_int)],
             "tofu_exec_launch_desc": [vp, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
+            "tofu_exec_unmaterialized": [vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
             "tofu_execute_range": [vp, C.c_int, C.c_int, vp],
             "tofu_exec_time_launch": [vp, C.c_int, vp, vp],
             "tofu_transpose_taps": [vp, vp, C.c_int, C.c_int, C.c_int, vp],
@@ -296,6 +297,14 @@ class Exec:
         buf = C.create_string_buffer(1024)
         n = C.c_size_t()
         check(lib().tofu_exec_launch_desc(self.h, i, buf, 1024, C.byref(n)), "tofu_exec_launch_desc")
+        return json.loads(buf.value.decode())
+
+    def unmaterialized(self) -> list:
+        """Tensors the step never writes to HBM (fused intermediates, include/tofu.h)."""
+        cap = 1 << 20
+        buf = C.create_string_buffer(cap)
+        n = C.c_size_t()
+        check(lib().tofu_exec_unmaterialized(self.h, buf, cap, C.byref(n)), "tofu_exec_unmaterialized")
         return json.loads(buf.value.decode())
 
     def run_range(self, first: int, last: int, stream=None):

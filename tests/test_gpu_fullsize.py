@@ -1,0 +1,75 @@
+"""Full-size sampled parity of the headline workloads — LSTM-6-4K (configs[2]) and WResNet-152-4 batch 32
+(configs[3]) — in the launch configuration bench.py times (fusion on: the product path), at k = 1 and on
+8 virtual ranks (the k = 8 plan's MultiFetch / partition-n-reduce kernels on one GPU).
+
+Every op of one training step is checked on sampled output boxes against the oracle, on the GPU's own
+inputs (tests/sampled_parity.py): bf16 outputs within normwise 5e-3, fp32 outputs within 1e-5 (north
+star); intermediates the fused kernels never store are recomputed by the oracle without their rounding
+(R13) and checked through their consumers.  Inputs: full-mantissa random bf16 values (tofu_inputs
+mode="bf16"), so fp32 accumulation is not exact.  The byte ledger equals the plan."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from sampled_parity import SampledChecker, runner_source  # noqa: E402
+from tofu_inputs.graphs import config  # noqa: E402
+from tofu_inputs.tensors import make_values  # noqa: E402
+
+_VALS = {}
+
+
+def _vals(cfg):
+    if cfg not in _VALS:
+        _VALS.clear()
+        _VALS[cfg] = make_values(config(cfg), seed=71, mode="bf16")
+    return _VALS[cfg]
+
+
+def _run(cfg, k):
+    from paper_1807_08887_b200.runner import TofuRunner
+    spec = config(cfg)
+    vals = _vals(cfg)
+    R = TofuRunner(spec, k)
+    R.load(vals)
+    R.step()
+    torch.cuda.synchronize()
+    return spec, vals, R
+
+
+@pytest.mark.parametrize("cfg,k", [(2, 1), (2, 8), (3, 1), (3, 8)])
+def test_headline_full_size_sampled_parity(cfg, k):
+    spec, vals, R = _run(cfg, k)
+    assert R.ledger() == R.plan.cost()
+    unmat = R.exec.unmaterialized()
+    chk = SampledChecker(spec, vals, runner_source(R), unmaterialized=unmat, seed=cfg * 10 + k)
+    res = chk.check_all(boxes=1)
+    # every op whose output the step stores is checked; unmaterialised outputs are checked via consumers
+    stored_ops = [o for o in spec["ops"] if o["output"] not in set(unmat)]
+    assert len(res) == len(stored_ops)
+    worst = max(res.items(), key=lambda kv: kv[1][0] / kv[1][1])
+    w32 = max((kv for kv in res.items() if kv[1][1] == 1e-5), key=lambda kv: kv[1][0], default=None)
+    print(f"cfg {cfg} k {k}: {len(res)} ops checked, {len(unmat)} unmaterialised; worst {worst}; "
+          f"worst fp32 path {w32}")
+    del R
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("which,k", [("mlp", 1), ("mlp", 2), ("mlp", 8), ("lstm", 1), ("lstm", 4),
+                                     ("wresnet", 1), ("wresnet", 4), ("wresnet", 8)])
+def test_product_path_per_op_full_mantissa(which, k):
+    """Small graphs of the three families, product path (fusion on), full-mantissa bf16 inputs: every
+    stored op output within 5e-3 / 1e-5 of the oracle on the GPU's own inputs (4 sampled boxes per op)."""
+    from paper_1807_08887_b200.runner import TofuRunner
+    from tofu_inputs.graphs import lstm, wresnet
+    spec = {"mlp": lambda: config(0), "lstm": lambda: lstm(2, 256, 4, 32),
+            "wresnet": lambda: wresnet([1, 1], 2, 8, 64, base=32, classes=64)}[which]()
+    vals = make_values(spec, seed=5, mode="bf16")
+    R = TofuRunner(spec, k)
+    R.load(vals)
+    R.step()
+    torch.cuda.synchronize()
+    assert R.ledger() == R.plan.cost()
+    chk = SampledChecker(spec, vals, runner_source(R), unmaterialized=R.exec.unmaterialized(), seed=k)
+    chk.check_all(boxes=4)

@@ -10,6 +10,10 @@ operands without any rounding code.  Recipes:
   state  M : q * 2^-17                    (non-zero so momentum is exercised)
   mode="int": all of the above replaced by q ~ U{-3..3} (exact fp64 sums,
               used for partitioned-vs-unpartitioned equality tests)
+  mode="bf16": full-mantissa values — u ~ U(-1, 1) continuous, scaled as above (X: u, T: u/2,
+              W: u * 2^-round(log2(sqrt(fan_in))), M: u * 2^-10), then rounded to the tensor's storage
+              dtype (bf16: round-to-nearest-even on the fp32 bit pattern; f32: cast), so every mantissa
+              bit is live and fp32 accumulation is not exact
   tensors with "init": "zeros" (initial recurrent state, zero gradients) are zero, "ones" are one
   a tensor's "fan_in" overrides shape[0] (convolution weights [co, ky, kx, ci]: ky*kx*ci)
   an input's "live_channels" n zeroes its last dim from n on (an RGB image padded to 8 channels)
@@ -23,6 +27,16 @@ import numpy as np
 
 def _q(rng, shape, lo=-128, hi=128):
     return rng.integers(lo, hi + 1, size=shape).astype(np.float64)
+
+
+def _to_storage(x, dtype):
+    """fp64 -> the storage dtype's value set (an input generator step, not method arithmetic)."""
+    f = np.asarray(x, np.float64).astype(np.float32)
+    if dtype != "bf16":
+        return f.astype(np.float64)
+    u = f.view(np.uint32).astype(np.uint64)
+    u = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return u.view(np.float32).astype(np.float64)
 
 
 def make_values(graph: dict, seed: int = 0, mode: str = "float") -> dict:
@@ -42,6 +56,18 @@ def make_values(graph: dict, seed: int = 0, mode: str = "float") -> dict:
             continue
         if mode == "int":
             out[name] = _q(rng, shape, -3, 3)
+            continue
+        if mode == "bf16":
+            u = rng.uniform(-1.0, 1.0, size=shape)
+            if role == "input":
+                u = u * (1.0 if name != "T" else 0.5)
+                if t.get("live_channels") is not None:
+                    u[..., int(t["live_channels"]):] = 0.0
+            elif role == "weight":
+                u = u * 2.0 ** -round(math.log2(math.sqrt(int(t.get("fan_in") or shape[0]))))
+            else:
+                u = u * 2.0 ** -10
+            out[name] = _to_storage(u, t.get("dtype", "f32"))
             continue
         if role == "input":
             out[name] = _q(rng, shape) * (2.0 ** -7 if name != "T" else 2.0 ** -8)
