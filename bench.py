@@ -28,6 +28,7 @@ from tofu_inputs.graphs import CONFIG_NAME, config  # noqa: E402
 from tofu_inputs.tensors import make_values  # noqa: E402
 
 METRIC = "samples/sec per training step"
+NVLINK_GBS = 900.0   # NVLink 5 per direction per GPU (north star; B200_PROFILING.md)
 CLOCK_Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
            "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
            "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -168,11 +169,13 @@ def reference_arm(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-def virtual_partitioned(spec, vals, k, steps):
+def virtual_partitioned(spec, vals, k, steps, k1_value=None):
     """The k-way partitioned step with all k ranks as virtual ranks on this one GPU: the same
     MultiFetch / reduce / sub-op kernels (peer pointers are local).  Not a scaling number — the k ranks
     run one after another on one device — but it exercises and times the partitioned path and its
-    byte ledger on real hardware."""
+    byte ledger on real hardware, and (total / k) is a proxy of one rank's step time, compared with the
+    per-rank roofline: max(the busiest rank's flops at the tensor peak, its max(in, out) NVLink bytes at
+    900 GB/s).  "ideal" = k x the k = 1 throughput (the paper's Ideal baseline)."""
     import torch
     from paper_1807_08887_b200.runner import TofuRunner
     R = TofuRunner(spec, k)
@@ -196,58 +199,52 @@ def virtual_partitioned(spec, vals, k, steps):
         ex.run_range(i, i + 1)
         evs[i + 1].record()
     torch.cuda.synchronize()
-    comm_ms = sum(evs[i].elapsed_time(evs[i + 1]) for i in range(nl) if descs[i]["kind"] in ("fetch", "reduce"))
+    per = [evs[i].elapsed_time(evs[i + 1]) for i in range(nl)]
+    comm_ms = sum(per[i] for i in range(nl) if descs[i]["kind"] in ("fetch", "reduce"))
     comm_bytes = sum(descs[i]["bytes"] for i in range(nl) if descs[i]["kind"] in ("fetch", "reduce"))
+    by_kind, by_def, by_rank = {}, {}, {}
+    flops_rank = {}
+    for d, t in zip(descs, per):
+        by_kind[d["kind"]] = by_kind.get(d["kind"], 0.0) + t
+        key = d["def"] if d["kind"] == "compute" else d["kind"]
+        by_def[key] = by_def.get(key, 0.0) + t
+        r = d.get("rank", -1)
+        by_rank[r] = by_rank.get(r, 0.0) + t
+        if d["kind"] == "compute":
+            flops_rank[r] = flops_rank.get(r, 0.0) + d["flops"]
+    pk = peaks()
+    io = [ex.rank_bytes(r) for r in range(k)]
+    t_comp = max(flops_rank.values(), default=0.0) / (pk["bf16_tflops_sustained"] * 1e12)
+    t_comm = max(max(x, y) for x, y in io) / NVLINK_GBS / 1e9
+    roof_ms = max(t_comp, t_comm) * 1e3
     pe, pb = R.plan.cost()
     le, lb = R.ledger()
     out = {"k": k, "ranks": "virtual (all on one GPU)", "ms_per_step": ms, "plan_factors": R.plan_json["factors"],
+           "plan_search": R.plan_json.get("search"),
            "plan_bytes": pb, "ledger_bytes": lb, "plan_elements": pe, "ledger_elements": le, "equal": pb == lb,
            "comm_kernels_ms": comm_ms, "comm_kernels_GBps": comm_bytes / (comm_ms / 1e3) / 1e9 if comm_ms else None,
-           "launches_per_step": ex.launches()}
+           "launches_per_step": ex.launches(),
+           "per_rank_ms_proxy": ms / k,
+           "per_rank_roofline_ms": roof_ms,
+           "per_rank_roofline": {"compute_ms": t_comp * 1e3, "nvlink_ms": t_comm * 1e3,
+                                 "busiest_rank_in_out_bytes": max(max(x, y) for x, y in io)},
+           "frac_per_rank": roof_ms / (ms / k) if ms else None,
+           "breakdown_ms": {kk: round(v, 4) for kk, v in sorted(by_kind.items(), key=lambda kv: -kv[1])},
+           "rank_ms": {str(r): round(v, 4) for r, v in sorted(by_rank.items())},
+           "top_defs_ms": dict(sorted(((kk, round(v, 4)) for kk, v in by_def.items()), key=lambda kv: -kv[1])[:10])}
+    if k1_value:
+        out["ideal_samples_s"] = k * k1_value
     del R
     torch.cuda.empty_cache()
     return out
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=3)
-    ap.add_argument("--impl", default="tofu", choices=["tofu", "reference"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
-                    help="replay the step as a CUDA graph (auto: when a step issues > 64 launches)")
-    ap.add_argument("--virtual-k", type=int, default=8, help="N=1 only: also time the k-way plan on virtual ranks")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    if os.environ.get("BENCH_TRACE_AFTER"):   # debugging aid: dump the Python stacks of a stuck run
-        import faulthandler
-        faulthandler.dump_traceback_later(int(os.environ["BENCH_TRACE_AFTER"]), exit=True)
-    if args.impl == "reference":
-        return reference_arm(args, world, rank)
-
+def run_workload(cfg, args, steps, world, rank, local_rank, group, shared, virtual_k, with_cpu):
+    """One workload: instrumented pass, warmup, timed region (device events, max over ranks), end-to-end
+    loop through TofuRunner.train, roofline objects.  Returns the JSON line (dict)."""
     import torch
     import torch.distributed as dist
     from paper_1807_08887_b200.runner import TofuRunner
-
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    # one GPU per rank over NCCL; with fewer GPUs than ranks (a functional check of the multi-process path on
-    # one GPU) the ranks share devices and the host collectives go over gloo (flagged in config.shared_gpu)
-    shared = world > torch.cuda.device_count()
-    dev = local_rank % torch.cuda.device_count()
-    torch.cuda.set_device(dev)
-    group = None
-    if world > 1:
-        if shared:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-        group = dist.group.WORLD
 
     def all_reduce(t, op):
         if shared:
@@ -257,9 +254,9 @@ def main():
         else:
             dist.all_reduce(t, op=op)
 
-    spec = config(args.config)
+    spec = config(cfg)
     k = world
-    big = args.config >= 4   # parameters drawn on the device (float64 host copies would not fit in RAM)
+    big = cfg >= 4   # parameters drawn on the device (float64 host copies would not fit in RAM)
     vals = None if big else make_values(spec, seed=0)
     if world > 1:
         R = TofuRunner(spec, k, rank=rank, group=group)
@@ -311,7 +308,7 @@ def main():
     for _ in range(args.warmup):
         ex.run()
     torch.cuda.synchronize()
-    dom_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    dom_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     for a, b in dom_ev:   # torch creates the CUDA event lazily on first record; libtofu re-records them
         a.record(); b.record()
     torch.cuda.synchronize()
@@ -333,7 +330,7 @@ def main():
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
-        for s in range(args.steps):
+        for s in range(steps):
             R.step()
         t1.record()
         torch.cuda.synchronize()
@@ -357,7 +354,7 @@ def main():
             dom_samples.append(dom_a.elapsed_time(dom_b))
     R.uncapture()
     ex.time_launch(-1)
-    ms = t0.elapsed_time(t1) / args.steps
+    ms = t0.elapsed_time(t1) / steps
     dom_ms = statistics.median(dom_samples)
     if world > 1:
         tt = torch.tensor([ms], device="cuda")
@@ -384,12 +381,12 @@ def main():
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
-    losses = R.train(batches, args.steps, start_event=e0)
+    losses = R.train(batches, steps, start_event=e0)
     e1.record()
     torch.cuda.synchronize()
     barrier()
     R.uncapture()
-    e2e_ms = e0.elapsed_time(e1) / args.steps
+    e2e_ms = e0.elapsed_time(e1) / steps
     if world > 1:
         tt = torch.tensor([e2e_ms, h2d], device="cuda", dtype=torch.float64)
         t0_ = tt[:1].clone()
@@ -420,7 +417,7 @@ def main():
     if os.path.exists(prof):
         try:
             pt = json.load(open(prof))
-            key = f"{CONFIG_NAME[args.config]}|k{k}|{d['op']}"
+            key = f"{CONFIG_NAME[cfg]}|k{k}|{d['op']}"
             if key in pt:
                 roof["traffic"] = pt[key]
         except Exception:
@@ -428,44 +425,111 @@ def main():
 
     ledger_el, ledger_b = R.ledger()
     plan_el, plan_b = R.plan.cost()
-    # step roofline (north star): slower of compute at tensor peak and plan bytes at NVLink per GPU
+    # step roofline (north star): the slower of (a) the rank's sub-op flops at the tensor peak and (b) the
+    # busiest rank's NVLink traffic at 900 GB/s per direction (max over ranks of max(bytes in, bytes out));
+    # the HBM term (algorithmic bytes of the sub-ops at the measured copy bandwidth) is reported beside it
     flops_rank = sum(x["flops"] for x in descs if x["kind"] == "compute")
     t_comp = flops_rank / (pk["bf16_tflops_sustained"] * 1e12)
-    t_comm = (plan_b / max(k, 1)) / 770e9 if k > 1 else 0.0
+    io = [ex.rank_bytes(r) for r in range(k)]
+    busiest = max((max(a, b) for a, b in io), default=0)
+    t_comm = busiest / NVLINK_GBS / 1e9 if k > 1 else 0.0
     step_roof = max(t_comp, t_comm)
-    # the optimizer state (weight, gradient, momentum: the paper's 3W) makes the step HBM-bound
     hbm_rank = sum(x["bytes"] for x in descs if x["kind"] == "compute")
     t_hbm = hbm_rank / (pk["hbm_gbs"] * 1e9)
 
     line = {
-        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, bf16-exact values)",
-        "config": {"workload": CONFIG_NAME[args.config], "global_batch": batch, "parallelism": f"tofu-k{k}",
+        "config": {"workload": CONFIG_NAME[cfg], "global_batch": batch, "parallelism": f"tofu-k{k}",
                    **({"shared_gpu": True} if world > 1 and shared else {}),
                    "plan_factors": R.plan_json["factors"], "l2": "inputs larger than L2 (W+M+dW 640 MiB)"},
         "roofline": roof,
-        "step_roofline": {"compute_ms": t_comp * 1e3, "comm_ms": t_comm * 1e3, "hbm_ms": t_hbm * 1e3,
-                          "frac_compute_vs_nvlink": step_roof / (ms / 1e3),
-                          "frac": max(step_roof, t_hbm) / (ms / 1e3),
-                          "note": "roofline = slower of tensor-peak compute, plan bytes at 770 GB/s NVLink, and "
-                                  "algorithmic HBM bytes of the sub-ops at measured copy bandwidth"},
+        "step_roofline": {"compute_ms": t_comp * 1e3, "nvlink_ms": t_comm * 1e3, "hbm_ms": t_hbm * 1e3,
+                          "frac": step_roof / (ms / 1e3),
+                          "frac_incl_hbm": max(step_roof, t_hbm) / (ms / 1e3),
+                          "busiest_rank_bytes": busiest,
+                          "note": "frac = max(rank flops at the sustained bf16 peak, busiest rank's max(in, out) "
+                                  "NVLink bytes at 900 GB/s per direction) / measured step (north star); "
+                                  "frac_incl_hbm also takes the sub-ops' algorithmic HBM bytes at the copy peak"},
         "bytes_vs_plan": {"plan_bytes": plan_b, "ledger_bytes": ledger_b, "plan_elements": plan_el,
                           "ledger_elements": ledger_el, "equal": plan_b == ledger_b},
         "e2e": {"value": batch / (e2e_ms / 1e3), "unit": "samples/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 4, "api": "TofuRunner.train (H2D of step s+1 overlapped with step s)",
                 "last_loss": float(losses[-1]) if losses.numel() else None},
-        "gpu_launches": ex.launches() * args.steps,
+        "gpu_launches": ex.launches() * steps,
         "cuda_graph": use_graph,
         "clocks": clk.summary(),
     }
-    if world == 1 and args.virtual_k > 1 and not big:
-        line["virtual_partitioned"] = virtual_partitioned(spec, vals, args.virtual_k, max(args.steps, 5))
+    if world == 1 and virtual_k > 1 and not big:
+        line["virtual_partitioned"] = virtual_partitioned(spec, vals, virtual_k, max(steps, 5), k1_value=value)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sspec, per_step, sample = oracle_sample(args.config)
+        sspec, per_step, sample = oracle_sample(cfg)
         t = oracle_step_time(sspec, make_values(sspec, seed=0))
         line["cpu_baseline"] = {"value": per_step / t, "unit": "samples/s", "cores": cpu_threads(), "kind": "oracle",
                                 "sample": sample}
+    del R, ex
+    torch.cuda.empty_cache()
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--impl", default="tofu", choices=["tofu", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
+                    help="replay the step as a CUDA graph (auto: when a step issues > 64 launches)")
+    ap.add_argument("--virtual-k", type=int, default=8, help="N=1 only: also time the k-way plan on virtual ranks")
+    ap.add_argument("--extra", default="1,2", help="N=1 only: other configs measured briefly, reported in the "
+                    "same line under other_workloads (empty: none)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if os.environ.get("BENCH_TRACE_AFTER"):   # debugging aid: dump the Python stacks of a stuck run
+        import faulthandler
+        faulthandler.dump_traceback_later(int(os.environ["BENCH_TRACE_AFTER"]), exit=True)
+    if args.impl == "reference":
+        return reference_arm(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1807_08887_b200.runner import TofuRunner
+
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # one GPU per rank over NCCL; with fewer GPUs than ranks (a functional check of the multi-process path on
+    # one GPU) the ranks share devices and the host collectives go over gloo (flagged in config.shared_gpu)
+    shared = world > torch.cuda.device_count()
+    dev = local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
+    group = None
+    if world > 1:
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        group = dist.group.WORLD
+
+    line = run_workload(args.config, args, args.steps, world, rank, local_rank, group, shared, args.virtual_k,
+                        rank == 0 and world == 1 and not args.no_cpu_baseline)
+    # the other named workloads as compact sub-objects of the same line (N = 1 only; short runs)
+    extra = [int(x) for x in args.extra.split(",") if x.strip() != ""] if world == 1 else []
+    others = []
+    for cfg in extra:
+        if cfg == args.config:
+            continue
+        o = run_workload(cfg, args, max(5, args.steps // 2), world, rank, local_rank, group, shared, args.virtual_k,
+                         False)
+        others.append({key: o.get(key) for key in ("config", "value", "unit", "ms_per_step", "roofline", "step_roofline",
+                                                   "e2e", "bytes_vs_plan", "virtual_partitioned", "gpu_launches",
+                                                   "clocks")})
+    if others:
+        line["other_workloads"] = others
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

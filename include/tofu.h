@@ -120,6 +120,11 @@ int tofu_exec_num_launches(const tofu_exec* e, int* n);
 /* JSON {"index","kind":"fetch"|"compute"|"reduce"|"barrier"|"memset","op","def","rank","flops",
  *       "bytes"}: flops = 2·M·N·K for GEMM sub-ops; bytes = algorithmic bytes read + written. */
 int tofu_exec_launch_desc(const tofu_exec* e, int index, char* out, size_t cap, size_t* len);
+/* Per-rank share of the ledger (bytes per step): in_bytes = what `rank` reads from its peers (fetched input
+ * regions, pulled partials), out_bytes = what its peers read from it.  Σ in = Σ out = the ledger bytes.
+ * The step's NVLink bound is max over ranks of max(in, out) / per-direction bandwidth (bench.py).
+ * Errors: TOFU_ERR_ARG (null exec, rank outside [0, k)). */
+int tofu_exec_rank_bytes(const tofu_exec* e, int rank, int64_t* in_bytes, int64_t* out_bytes);
 /* JSON list of the tensors the step never writes to HBM on some rank: intermediates of fused chains
  * (R8 / R13 — a weight gradient folded into the optimizer epilogue, a GEMM / convolution output
  * folded into its element-wise consumer).  Their storage holds no defined value after tofu_execute; parity

@@ -179,6 +179,7 @@ struct Exec {
   };
   std::map<std::pair<int, int>, std::vector<ConvLaunch>> convs;  // (op, li) -> launches (4 phases: stride-2 dgrad)
   int64_t ledger_el = 0, ledger_bytes = 0;
+  std::vector<int64_t> rank_in, rank_out;  // per rank: bytes it reads from peers / peers read from it
   int64_t n_kernels = 0;
   bool skip_comm = false;
   bool multi_process = false;
@@ -543,6 +544,8 @@ void lower(Exec& E) {
     for (int d = 0; d < n; ++d) dst[4 - n + d] = s[d];
   };
   E.ledger_el = E.ledger_bytes = 0;
+  E.rank_in.assign(k, 0);
+  E.rank_out.assign(k, 0);
   for (int r = 0; r < k; ++r)
     for (size_t o = 0; o < g.ops.size(); ++o) {
       LOp& L = all[r][o];
@@ -559,6 +562,8 @@ void lower(Exec& E) {
               inter(b.box, E.lay[q.src].shard_box[t], x);
               E.ledger_el += vol(x);
               E.ledger_bytes += vol(x) * g.itemsize(t);
+              E.rank_in[r] += vol(x) * g.itemsize(t);
+              E.rank_out[q.src] += vol(x) * g.itemsize(t);
               L.remote_direct = true;
             }
           }
@@ -584,6 +589,8 @@ void lower(Exec& E) {
           if (s != r) {
             E.ledger_el += vol(x);
             E.ledger_bytes += vol(x) * g.itemsize(t);
+            E.rank_in[r] += vol(x) * g.itemsize(t);
+            E.rank_out[s] += vol(x) * g.itemsize(t);
           }
         }
       }
@@ -644,6 +651,8 @@ void lower(Exec& E) {
               ++nrem;
               E.ledger_el += vol(cell);
               E.ledger_bytes += vol(cell) * ses;
+              E.rank_in[r] += vol(cell) * ses;
+              E.rank_out[srcs[s]] += vol(cell) * ses;
             }
           }
           all[r][o].reduce.push_back(pc);
@@ -1798,6 +1807,13 @@ extern "C" int tofu_exec_launch_desc(const tofu_exec* h, int index, char* out, s
     if (!h || index < 0 || index >= (int)h->e.launches.size()) throw tofu::Error(TOFU_ERR_ARG, "bad launch index");
     return tofu::write_out(tofu::launch_desc(h->e, index), out, cap, len);
   });
+}
+
+extern "C" int tofu_exec_rank_bytes(const tofu_exec* h, int rank, int64_t* in_bytes, int64_t* out_bytes) {
+  if (!h || rank < 0 || rank >= (int)h->e.rank_in.size()) return tofu::fail(TOFU_ERR_ARG, "bad rank");
+  if (in_bytes) *in_bytes = h->e.skip_comm ? 0 : h->e.rank_in[rank];
+  if (out_bytes) *out_bytes = h->e.skip_comm ? 0 : h->e.rank_out[rank];
+  return TOFU_OK;
 }
 
 extern "C" int tofu_exec_unmaterialized(const tofu_exec* h, char* out, size_t cap, size_t* len) {

@@ -109,6 +109,7 @@ def lib():
             "tofu_exec_num_launches": [vp, C.POINTER(C.c_int)],
             "tofu_exec_launch_desc": [vp, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
             "tofu_exec_unmaterialized": [vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
+            "tofu_exec_rank_bytes": [vp, C.c_int, i64p, i64p],
             "tofu_execute_range": [vp, C.c_int, C.c_int, vp],
             "tofu_exec_time_launch": [vp, C.c_int, vp, vp],
             "tofu_transpose_taps": [vp, vp, C.c_int, C.c_int, C.c_int, vp],
@@ -298,6 +299,12 @@ class Exec:
         n = C.c_size_t()
         check(lib().tofu_exec_launch_desc(self.h, i, buf, 1024, C.byref(n)), "tofu_exec_launch_desc")
         return json.loads(buf.value.decode())
+
+    def rank_bytes(self, rank: int):
+        """(bytes rank reads from peers, bytes peers read from rank) per step."""
+        a, b = C.c_int64(), C.c_int64()
+        check(lib().tofu_exec_rank_bytes(self.h, rank, C.byref(a), C.byref(b)), "tofu_exec_rank_bytes")
+        return a.value, b.value
 
     def unmaterialized(self) -> list:
         """Tensors the step never writes to HBM (fused intermediates, include/tofu.h)."""

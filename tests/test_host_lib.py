@@ -219,3 +219,19 @@ def test_wresnet_ledger_equals_plan_larger(tofu, k):
     plan = tofu.Plan(g, k)
     ex = tofu.Exec(g, plan, list(range(k)), [0x100000000 * (r + 1) for r in range(k)])
     assert ex.ledger() == plan.cost()
+
+
+@pytest.mark.parametrize("cfg,k", [(1, 8), (0, 4)])
+def test_rank_bytes_partition_the_ledger(tofu, cfg, k):
+    """tofu_exec_rank_bytes: every ledger byte is read by one rank and served by another, so Σ in = Σ out
+    = the ledger = the plan's bytes; FC k = 8 moves 9437184 B into every rank (3/8 of X twice, quarters of
+    dY / partials: the per-step pieces of tests/golden/fc_k8_deltas.json spread evenly) plus rank 0's 7
+    loss partials (28 B)."""
+    spec = config(cfg)
+    g = tofu.Graph(spec)
+    plan = tofu.Plan(g, k)
+    ex = tofu.Exec(g, plan, list(range(k)), [0x100000000 * (r + 1) for r in range(k)])
+    io = [ex.rank_bytes(r) for r in range(k)]
+    assert sum(a for a, _ in io) == sum(b for _, b in io) == ex.ledger()[1] == plan.cost()[1]
+    if cfg == 1:
+        assert [a for a, _ in io] == [9437184 + 28] + [9437184] * 7
