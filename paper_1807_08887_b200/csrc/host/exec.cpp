@@ -314,7 +314,7 @@ ConvGeom conv_geom(const OpDef& d) {
   if (std::sscanf(nm, "conv_k%ds%dp%d", &R, &s, &p) == 3 && d.name.rfind("conv_", 0) == 0) kind = 0;
   else if (std::sscanf(nm, "dconv_k%ds%dp%d", &R, &s, &p) == 3) kind = 1;
   else if (std::sscanf(nm, "wconv_k%ds%dp%d", &R, &s, &p) == 3) kind = 2;
-  if (kind < 0 || R < 1 || s < 1 || s > 2 || p < 0) return g;
+  if (kind < 0 || R < 1 || s < 1 || s > 2 || p < 0 || !d.prod2) return g;   // body: reduce(Sum; ..; A[..] * B[..])
   const OpDef ref = parse_tdl(conv_tdl(kind, R, s, p));
   if (ref.vars != d.vars || ref.n_out != d.n_out || ref.reducer != d.reducer ||
       ref.accesses.size() != d.accesses.size())
@@ -333,10 +333,11 @@ const char* kernel_kind(const OpDef& d) {
                                            "sumsq", "relu4",      "relu_grad4", "mom4", "sgd4", "add4", "addrelu"};
   static const std::set<std::string> lstm = {"cell_c", "cell_h", "cell_bwd_a", "cell_bwd_c"};
   static const std::set<std::string> win = {"maxpool", "maxpool_grad", "gap", "gap_grad"};
+  // element-wise / cell / window kernels are bound by the def's canonical TDL (kernel_match.cpp), not its name
   if (gemm_form(d).ok) return "gemm";
-  if (ew.count(d.name)) return "ew";
-  if (lstm.count(d.name)) return "lstm";
-  if (win.count(d.name)) return "window";
+  if (ew.count(d.kernel)) return "ew";
+  if (lstm.count(d.kernel)) return "lstm";
+  if (win.count(d.kernel)) return "window";
   if (conv_geom(d).kind >= 0) return "conv";
   return nullptr;
 }
@@ -668,7 +669,7 @@ void lower(Exec& E) {
   for (int r = 0; r < k; ++r)
     for (size_t o = 0; o + 1 < g.ops.size(); ++o) {
       const OpInfo &a = g.ops[o], &b = g.ops[o + 1];
-      if (!is_mom(g.defs[a.def].name) || !is_sgd(g.defs[b.def].name) || b.inputs[1] != a.output) continue;
+      if (!is_mom(g.defs[a.def].kernel) || !is_sgd(g.defs[b.def].kernel) || b.inputs[1] != a.output) continue;
       LOp &La = all[r][o], &Lb = all[r][o + 1];
       bool ok = La.out.direct && Lb.out.direct && La.fetch.empty() && Lb.fetch.empty();
       for (auto& x : La.in) ok &= x.direct;
@@ -697,7 +698,7 @@ void lower(Exec& E) {
             }
         if (readers != 1 || reader <= (int)o || reader + 1 >= (int)g.ops.size()) continue;
         const OpInfo &b = g.ops[reader], &c = g.ops[reader + 1];
-        if (!is_mom(g.defs[b.def].name) || !all[r][reader].fused_sgd) continue;
+        if (!is_mom(g.defs[b.def].kernel) || !all[r][reader].fused_sgd) continue;
         // moving mom+sgd up to the GEMM must not reorder any access to M / W
         std::set<int> state = {b.inputs[0], b.output, c.inputs[0], c.output};
         for (auto& pr : g.alias)
@@ -720,7 +721,7 @@ void lower(Exec& E) {
   if (E.fuse)
     for (int r = 0; r < k; ++r)
       for (size_t o = 0; o + 1 < g.ops.size(); ++o) {
-        const std::string &na = g.defs[g.ops[o].def].name, &nb = g.defs[g.ops[o + 1].def].name;
+        const std::string &na = g.defs[g.ops[o].def].kernel, &nb = g.defs[g.ops[o + 1].def].kernel;
         const bool fwd = na == "cell_c" && nb == "cell_h";
         const bool bwd = na == "cell_bwd_a" && nb == "cell_bwd_c";
         if (!fwd && !bwd) continue;
@@ -746,7 +747,7 @@ void lower(Exec& E) {
   if (E.fuse)
     for (int r = 0; r < k; ++r)
       for (size_t o = 0; o + 1 < g.ops.size(); ++o) {
-        if (g.defs[g.ops[o].def].name != "sumsq" || g.defs[g.ops[o + 1].def].name != "mse_grad") continue;
+        if (g.defs[g.ops[o].def].kernel != "sumsq" || g.defs[g.ops[o + 1].def].kernel != "mse_grad") continue;
         if (g.ops[o].inputs != g.ops[o + 1].inputs) continue;
         LOp &La = all[r][o], &Lb = all[r][o + 1];
         if (La.skip || Lb.skip || !Lb.out.direct || !Lb.fetch.empty() || !Lb.reduce.empty() || !La.fetch.empty())
@@ -802,7 +803,7 @@ void lower(Exec& E) {
         const int e = consumer(t);
         if (e < 0) continue;
         LOp& Le = all[r][e];
-        const std::string& en = g.def_of(e).name;
+        const std::string& en = g.def_of(e).kernel;
         auto same_direct = [&](const Buf& b) { return b.direct && same(b.box, Lo.out.box) && same(b.buf_box, b.box); };
         bool ok = Le.fetch.empty() && Le.reduce.empty() && !Le.skip && same_direct(Le.out) && Le.out.dtype == TOFU_BF16;
         for (auto& b : Le.in) ok &= same_direct(b) && b.dtype == TOFU_BF16;
@@ -826,7 +827,7 @@ void lower(Exec& E) {
           const int t2 = g.ops[e].output, c2 = consumer(t2);
           if (c2 >= 0) {
             LOp& L2 = all[r][c2];
-            const std::string& n2 = g.def_of(c2).name;
+            const std::string& n2 = g.def_of(c2).kernel;
             bool ok2 = (n2 == "relu_grad" || n2 == "relu_grad4") && g.ops[c2].inputs[1] == t2 &&
                        g.ops[c2].inputs[0] != t2 && earlier(g.ops[c2].inputs[0], (int)o) && L2.fetch.empty() &&
                        L2.reduce.empty() && !L2.skip && same_direct(L2.out) && L2.out.dtype == TOFU_BF16;
@@ -921,7 +922,7 @@ void build_launches(Exec& E) {
     if (bar_f) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
     for (int li = 0; li < nl; ++li) {
       if (E.lops[li][o].skip) continue;
-      if (g.defs[g.ops[o].def].name == "sumsq") E.launches.push_back({4, (int)o, li, 0, 0, 0});
+      if (g.defs[g.ops[o].def].kernel == "sumsq") E.launches.push_back({4, (int)o, li, 0, 0, 0});
       E.launches.push_back({1, (int)o, li, 0, 0, 0});
     }
     if (bar_c) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
@@ -1000,9 +1001,8 @@ bool conv1x1_gemm(Exec& E, int o, int li, Exec::GemmLaunch& G) {
     if (!flat2(Lm.in[0].buf_box, Lm.in[0].box, 1, mr, mc, ldm, moff) ||
         !flat2(Ls.in[0].buf_box, Ls.in[0].box, 1, wr, wc, ldw, woff) || mr != ro || mc != co)
       return false;
-    auto at = [&](int op, const char* key) {
-      auto it = g.ops[op].attrs.find(key);
-      return (float)(it == g.ops[op].attrs.end() ? 0.0 : it->second);
+    auto at = [&](int op, const char*) {  // the mom / sgd def's constant (its TDL literal)
+      return (float)g.defs[g.ops[op].def].kconst.at(0);
     };
     G.a.c_mode = 3;
     G.a.C = base + Lm.in[0].off + moff * 4;
@@ -1098,9 +1098,8 @@ void finalize(Exec& E) {
       if (L.fused_opt >= 0) {
         const LOp& Lm = E.lops[li][L.fused_opt];      // mom(M, G) -> M_new (in place)
         const LOp& Ls = E.lops[li][L.fused_opt + 1];  // sgd(W, M_new) -> W_new (in place)
-        auto at = [&](int op, const char* key) {
-          auto it = g.ops[op].attrs.find(key);
-          return (float)(it == g.ops[op].attrs.end() ? 0.0 : it->second);
+        auto at = [&](int op, const char*) {  // the mom / sgd def's constant (its TDL literal)
+          return (float)g.defs[g.ops[op].def].kconst.at(0);
         };
         int64_t mr, mc, ldm, moff, wr, wc, ldw, woff;
         if (!flat2(Lm.in[0].buf_box, Lm.in[0].box, gf.nm, mr, mc, ldm, moff) ||
@@ -1162,9 +1161,8 @@ void finalize(Exec& E) {
           C.a.ldc = strides_of(Lm.in[0].buf_box)[0];
           C.a.D = E.arena[r] + Ls.in[0].off + offset_in(Ls.in[0].buf_box, Ls.in[0].box) * 2;
           C.a.ldd = strides_of(Ls.in[0].buf_box)[0];
-          auto at = [&](int op, const char* key) {
-            auto it = g.ops[op].attrs.find(key);
-            return (float)(it == g.ops[op].attrs.end() ? 0.0 : it->second);
+          auto at = [&](int op, const char*) {  // the mom / sgd def's constant (its TDL literal)
+            return (float)g.defs[g.ops[op].def].kconst.at(0);
           };
           C.a.s0 = at(L.fused_opt, "mu");
           C.a.s1 = at(L.fused_opt + 1, "lr");
@@ -1360,7 +1358,7 @@ int run_window(Exec& E, int o, int li, cudaStream_t st) {
   const Graph& g = *E.g;
   const int r = E.local[li];
   const LOp& L = E.lops[li][o];
-  const std::string& dn = g.def_of(o).name;
+  const std::string& dn = g.def_of(o).kernel;
   std::vector<Rng> ib;
   iter_box(g, o, E.plan.osplit[o], E.plan.factors, worker_digits(r, E.plan.factors), ib);
   char* base = E.arena[r];
@@ -1423,8 +1421,7 @@ int run_window(Exec& E, int o, int li, cudaStream_t st) {
     a.X = base + X.off + offset_in(X.buf_box, X.box) * 2;
     a.o_sb = os[0];
     a.out = base + L.out.off + offset_in(L.out.buf_box, L.out.box) * oe;
-    auto it = g.ops[o].attrs.find("scale");
-    a.s = it != g.ops[o].attrs.end() ? (float)it->second : 0.f;
+    a.s = (float)g.def_of(o).kconst.at(0);   // the def's own constant (1/(H*W))
     return tofu_gap(&a, st);
   }
   // gap_grad: vars b, y, x, c ; input D[b, c]
@@ -1436,8 +1433,7 @@ int run_window(Exec& E, int o, int li, cudaStream_t st) {
   a.dY = base + D.off + offset_in(D.buf_box, D.box) * 2;
   a.o_sb = os[0]; a.o_sy = os[1]; a.o_sx = os[2];
   a.out = base + L.out.off + offset_in(L.out.buf_box, L.out.box) * oe;
-  auto it = g.ops[o].attrs.find("scale");
-  a.s = it != g.ops[o].attrs.end() ? (float)it->second : 0.f;
+  a.s = (float)g.def_of(o).kconst.at(0);
   return tofu_gap_grad(&a, st);
 }
 
@@ -1469,7 +1465,7 @@ int run_compute(Exec& E, int o, int li, cudaStream_t st) {
   const int r = E.local[li];
   LOp& L = E.lops[li][o];
   const OpInfo& oi = g.ops[o];
-  const std::string& dn = g.defs[oi.def].name;
+  const std::string& dn = g.defs[oi.def].kernel;
   const OpDef& d = g.defs[oi.def];
   char* base = E.arena[r];
   const std::string kind = kernel_kind(d);
@@ -1540,37 +1536,32 @@ int run_compute(Exec& E, int o, int li, cudaStream_t st) {
   void* y = base + L.out.off;
   const void* x0 = L.in.size() > 0 ? base + L.in[0].off : nullptr;
   const void* x1 = L.in.size() > 1 ? base + L.in[1].off : nullptr;
-  auto attr = [&](const char* key, double dflt) {
-    auto it = oi.attrs.find(key);
-    return (float)(it == oi.attrs.end() ? dflt : it->second);
-  };
+  // the kernel's constant: the real literal of the def's TDL (kernel_match.cpp)
+  auto kc = [&](int op) { return (float)g.defs[g.ops[op].def].kconst.at(0); };
   if (dn == "relu" || dn == "relu4") return tofu_elementwise(TOFU_EW_RELU, n, y, x0, nullptr, nullptr, 0, 0, st);
   if (dn == "relu_grad" || dn == "relu_grad4") return tofu_elementwise(TOFU_EW_RELU_GRAD, n, y, x0, x1, nullptr, 0, 0, st);
   if (dn == "add4") return tofu_elementwise(TOFU_EW_ADD, n, y, x0, x1, nullptr, 0, 0, st);
   if (dn == "addrelu") return tofu_elementwise(TOFU_EW_ADDRELU, n, y, x0, x1, nullptr, 0, 0, st);
-  if (dn == "mse_grad") return tofu_elementwise(TOFU_EW_MSE_GRAD, n, y, x0, x1, nullptr, attr("scale", 1), 0, st);
+  if (dn == "mse_grad") return tofu_elementwise(TOFU_EW_MSE_GRAD, n, y, x0, x1, nullptr, kc(o), 0, st);
   if (dn == "sumsq") {
     const int64_t m = vol(L.in[0].box);
     if (L.fused_loss_grad) {  // + the next op (mse_grad of the same inputs) in the same pass
       const LOp& Ln = E.lops[li][o + 1];
-      auto it = g.ops[o + 1].attrs.find("scale");
-      const float s1 = (float)(it == g.ops[o + 1].attrs.end() ? 1.0 : it->second);
-      return tofu_elementwise(TOFU_EW_SUMSQ_MSE_GRAD, m, y, x0, x1, base + Ln.out.off, attr("scale", 1), s1, st);
+      return tofu_elementwise(TOFU_EW_SUMSQ_MSE_GRAD, m, y, x0, x1, base + Ln.out.off, kc(o), kc(o + 1), st);
     }
-    return tofu_elementwise(TOFU_EW_SUMSQ, m, y, x0, x1, nullptr, attr("scale", 1), 0, st);
+    return tofu_elementwise(TOFU_EW_SUMSQ, m, y, x0, x1, nullptr, kc(o), 0, st);
   }
   if (is_mom(dn)) {
     if (L.fused_sgd) {
       const OpInfo& nx = g.ops[o + 1];
       LOp& Ln = E.lops[li][o + 1];
-      auto it = nx.attrs.find("lr");
-      const float lr = (float)(it == nx.attrs.end() ? 0.0 : it->second);
-      return tofu_elementwise(TOFU_EW_SGD_MOM, n, nullptr, base + L.in[0].off, x1, base + Ln.in[0].off, attr("mu", 0),
-                              lr, st);
+      (void)nx;
+      return tofu_elementwise(TOFU_EW_SGD_MOM, n, nullptr, base + L.in[0].off, x1, base + Ln.in[0].off, kc(o),
+                              kc(o + 1), st);
     }
-    return tofu_elementwise(TOFU_EW_MOM, n, y, x0, x1, nullptr, attr("mu", 0), 0, st);
+    return tofu_elementwise(TOFU_EW_MOM, n, y, x0, x1, nullptr, kc(o), 0, st);
   }
-  if (is_sgd(dn)) return tofu_elementwise(TOFU_EW_SGD, n, y, x0, x1, nullptr, attr("lr", 0), 0, st);
+  if (is_sgd(dn)) return tofu_elementwise(TOFU_EW_SGD, n, y, x0, x1, nullptr, kc(o), 0, st);
   return TOFU_ERR_ARG;
 }
 
@@ -1739,14 +1730,20 @@ std::string launch_desc(const Exec& E, int i) {
       for (int q = 0; q < gf.nk; ++q) K *= (double)ab[gf.a_mn ? q : gf.nm + q].len();
       flops = 2 * M * N * K;
       bytes = 2 * (M * K + K * N) + M * N * (lo.fused_opt >= 0 ? (8 + 4) : (lo.out.dtype == TOFU_BF16 ? 2 : 4));
+      o += ",\"mnk\":[" + json_num(M) + "," + json_num(N) + "," + json_num(K) + "]";
       (void)dn;
     } else if (std::string(kernel_kind(dd)) == "conv") {
       // implicit GEMM: 2·M·N·K over the launches (the stride-2 data gradient's phases skip absent taps);
       // bytes: each operand region once + the output (fused optimizer: momentum and weight read + written)
+      std::string shp;
       for (auto& a : conv_args(const_cast<Exec&>(E), L.op, L.li)) {
         const double pix = (double)a.nb * a.ngy * a.ngx, kn = (double)a.ntaps * a.nch;
         flops += a.kind == 0 ? 2 * pix * a.n_out * kn : 2 * (double)a.m_out * kn * pix;
+        if (shp.empty())
+          shp = a.kind == 0 ? "[" + json_num(pix) + "," + json_num(a.n_out) + "," + json_num(kn) + "]"
+                            : "[" + json_num(a.m_out) + "," + json_num(kn) + "," + json_num(pix) + "]";
       }
+      if (!shp.empty()) o += ",\"mnk\":" + shp;
       for (auto& b : lo.in) bytes += (double)vol(b.box) * (b.dtype == TOFU_BF16 ? 2 : 4);
       bytes += (double)vol(lo.out.box) * (lo.fused_opt >= 0 ? 12 : (lo.out.dtype == TOFU_BF16 ? 2 : 4));
     } else {
@@ -1760,6 +1757,12 @@ std::string launch_desc(const Exec& E, int i) {
     bytes += (double)vol(lo.out.box) * 2 * (((lo.ep >> 1) & 1) + ((lo.ep >> 2) & 1));  // epilogue operands
   }
   o += ",\"flops\":" + json_num(flops) + ",\"bytes\":" + json_num(bytes);
+  if (L.kind == 1 && !g.defs[g.ops[L.op].def].kernel.empty()) {  // the kernel bound by the def's TDL body
+    const OpDef& kd = g.defs[g.ops[L.op].def];
+    o += ",\"kernel\":" + json_quote(kd.kernel) + ",\"kconst\":[";
+    for (size_t q = 0; q < kd.kconst.size(); ++q) o += (q ? "," : "") + json_num(kd.kconst[q]);
+    o += "]";
+  }
   if (L.kind == 1 && lo_fused(E, L)) o += ",\"fused\":\"mom+sgd\"";
   if (L.kind == 1 && E.lops[L.li][L.op].fused_opt >= 0) o += ",\"fused\":\"gemm+mom+sgd\"";
   if (L.kind == 1 && E.lops[L.li][L.op].fused_next) o += ",\"fused\":\"lstm-cell-pair\"";

@@ -21,6 +21,7 @@ Graph graph_from_json(const std::string& text) {
   Graph g;
   for (auto& kv : j.at("defs").obj) {
     OpDef d = parse_tdl(kv.second.as_str());
+    match_kernel(d);
     if (d.name != kv.first) throw Error(TOFU_ERR_PARSE, "def key " + kv.first + " != def name " + d.name);
     g.def_ix[d.name] = (int)g.defs.size();
     g.defs.push_back(std::move(d));

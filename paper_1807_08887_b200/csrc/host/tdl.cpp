@@ -401,7 +401,36 @@ std::vector<int> OpDef::split_vars() const {
 OpDef parse_tdl(const std::string& src) {
   Parser p;
   p.t = lex(src);
-  return p.run();
+  OpDef d = p.run();
+  d.src = src;
+  return d;
+}
+
+// Canonical token text of a def: the def's own name dropped, parameter names -> P<i>, index variables ->
+// V<i> (output vars, then reduce vars), real-valued literals (with a '.') -> '#' with their values appended
+// to `consts` in order of appearance; integer literals (ranks, gate indices, strides, 0 / 1) stay literal.
+// Two defs with the same canonical text compute the same function of their operands up to the constants.
+std::string canonical_def(const OpDef& d, std::vector<double>& consts) {
+  consts.clear();
+  std::map<std::string, int> par, var;
+  for (size_t i = 0; i < d.params.size(); ++i) par[d.params[i]] = (int)i;
+  for (size_t i = 0; i < d.vars.size(); ++i) var[d.vars[i]] = (int)i;
+  std::vector<Tok> t = lex(d.src);
+  std::string o;
+  for (size_t i = 0; i < t.size(); ++i) {
+    const Tok& x = t[i];
+    if (x.kind == 3) break;
+    if (i == 1 && x.kind == 1) continue;  // the def's name
+    std::string w = x.s;
+    if (x.kind == 1 && par.count(x.s)) w = "P" + std::to_string(par[x.s]);
+    else if (x.kind == 1 && var.count(x.s)) w = "V" + std::to_string(var[x.s]);
+    else if (x.kind == 0 && x.s.find('.') != std::string::npos) {
+      consts.push_back(std::stod(x.s));
+      w = "#";
+    }
+    o += (o.empty() ? "" : " ") + w;
+  }
+  return o;
 }
 
 int64_t Lin::eval(const int64_t* env) const {

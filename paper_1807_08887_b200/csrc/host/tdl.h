@@ -61,6 +61,9 @@ struct OpDef {
   std::vector<Access> accesses;
   std::string cls;                // ElementWise | Reduction | OpaqueBatched | General
   bool prod2 = false;             // body is exactly `reduce(Sum; ..; A[..] * B[..])` (a contraction)
+  std::string src;                // the def's TDL text
+  std::string kernel;             // element-wise / cell / window kernel whose canonical TDL this def matches, or ""
+  std::vector<double> kconst;     // that kernel's constants, read from the def's text (in order of appearance)
 
   int n_red() const { return (int)vars.size() - n_out; }
   bool is_red(int v) const { return v >= n_out; }
@@ -69,6 +72,13 @@ struct OpDef {
 
 // Throws Error(TOFU_ERR_PARSE, "<Kind>: message").
 OpDef parse_tdl(const std::string& src);
+
+// Canonical text of a def (names -> positions, real literals -> '#' collected in consts); see tdl.cpp.
+std::string canonical_def(const OpDef& d, std::vector<double>& consts);
+
+// Bind d to the element-wise / cell / window kernel whose canonical TDL it matches (kernel_match.cpp):
+// sets d.kernel ("" when none) and d.kconst.
+void match_kernel(OpDef& d);
 
 // Extent of every var given input and output shapes (reduce vars from the first dim they index alone).
 // `given` (may be empty) holds explicit extents (-1 = infer) for vars no dim determines.

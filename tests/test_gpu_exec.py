@@ -223,3 +223,22 @@ def test_fused_fetch_equals_staged_fetch(cfg, k, monkeypatch):
     assert fetches["1"] < fetches["0"]
     for t in spec["tensors"]:
         assert np.array_equal(outs["0"][t], outs["1"][t]), t
+
+
+@pytest.mark.parametrize("fuse", ["0", "1"])
+def test_constants_come_from_the_tdl_text(fuse, monkeypatch):
+    """Learning rate, momentum and loss scale are read from the defs' TDL literals (kernel_match.cpp), not
+    from op attrs: an MLP whose TDL says lr = 0.25, mu = 0.5 with bogus attrs matches the oracle, which
+    evaluates the TDL."""
+    monkeypatch.setenv("TOFU_FUSE", fuse)
+    spec = mlp(64, [256, 512, 512], lr=0.25, mu=0.5)
+    for o in spec["ops"]:
+        o["attrs"] = {"lr": 0.0, "mu": 0.0, "scale": 0.0}
+    vals = make_values(spec, seed=19)
+    R, out = run_gpu(spec, 2, vals)
+    ref = run_graph(OGraph(spec), vals, emulate_storage=True)
+    for t in ["M1_new", "M2_new", "W1_new", "W2_new", "loss"]:
+        r = ref[t]
+        e = nrm(out[t], r) if np.ndim(r) else abs(out[t] - r) / abs(r)
+        assert e <= 2e-2, (t, e)
+    assert not np.array_equal(out["W1_new"], vals["W1"])   # (attrs lr = 0 would have left W unchanged)

@@ -235,3 +235,57 @@ def test_rank_bytes_partition_the_ledger(tofu, cfg, k):
     assert sum(a for a, _ in io) == sum(b for _, b in io) == ex.ledger()[1] == plan.cost()[1]
     if cfg == 1:
         assert [a for a, _ in io] == [9437184 + 28] + [9437184] * 7
+
+
+def _mlp_with_defs(**edits):
+    spec = config(0)
+    spec = json.loads(json.dumps(spec))
+    for old, (new_name, new_src) in edits.items():
+        src = spec["defs"].pop(old)
+        spec["defs"][new_name] = new_src if new_src else src.replace(f"def {old}(", f"def {new_name}(")
+        for o in spec["ops"]:
+            if o["def"] == old:
+                o["def"] = new_name
+    return spec
+
+
+def _exec(tofu, spec, k=1):
+    g = tofu.Graph(spec)
+    plan = tofu.Plan(g, k)
+    return tofu.Exec(g, plan, list(range(k)), [0x100000000 * (r + 1) for r in range(k)])
+
+
+def test_kernels_are_bound_by_tdl_body_not_name(tofu, monkeypatch):
+    """an operator is its TDL description.  Renamed defs keep their kernels; the constants the
+    kernels use are the TDL literals (not the op attrs)."""
+    monkeypatch.setenv("TOFU_FUSE", "0")      # every op its own launch
+    spec = _mlp_with_defs(relu=("rectify", None), sgd=("update", None))
+    for o in spec["ops"]:
+        o["attrs"] = {"lr": 123.0, "mu": 7.0, "scale": 9.0}    # ignored: the TDL text decides
+    ex = _exec(tofu, spec)
+    descs = [ex.launch_desc(i) for i in range(ex.num_launches())]
+    kern = {d["op"]: (d.get("kernel"), d.get("kconst")) for d in descs if d["kind"] == "compute"}
+    assert kern["relu1"] == ("relu", [])
+    assert kern["loss"][0] == "sumsq" and kern["loss"][1] == [1.0 / (64 * 512)]
+    assert kern["mom1"] == ("mom", [0.875])     # (sgd1 runs inside mom1's launch: "mom+sgd")
+
+
+@pytest.mark.parametrize("name,src", [
+    ("relu", "def relu(X(2)) -> lambda i, j: max(X[i, j], 1)"),                   # another function, same name
+    ("sgd", "def sgd(W(2), M(2)) -> lambda i, j: W[i, j] + M[i, j] * 0.0078125"),  # sign flipped
+    ("mom", "def mom(M(2), G(2)) -> lambda i, j: M[i, j] * 0.875 * G[i, j]"),     # product, not sum
+])
+def test_edited_bodies_are_rejected(tofu, name, src):
+    """A def whose body matches no kernel is refused at tofu_exec_create (TOFU_ERR_ARG), whatever its name."""
+    spec = _mlp_with_defs(**{name: (name, src)})
+    with pytest.raises(tofu.TofuError):
+        _exec(tofu, spec)
+
+
+def test_conv_body_must_be_a_contraction(tofu):
+    from tofu_inputs.graphs import wresnet
+    spec = wresnet([1], 1, 2, 32, base=8, classes=8)
+    n = [d for d in spec["defs"] if d.startswith("conv_k3")][0]
+    spec["defs"][n] = spec["defs"][n].replace("] * W[", "] + W[")
+    with pytest.raises(tofu.TofuError):
+        _exec(tofu, spec)
