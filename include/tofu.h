@@ -128,7 +128,7 @@ int tofu_exec_rank_bytes(const tofu_exec* e, int rank, int64_t* in_bytes, int64_
 /* JSON list of the tensors the step never writes to HBM on some rank: intermediates of fused chains
  * (R8 / R13 — a weight gradient folded into the optimizer epilogue, a GEMM / convolution output
  * folded into its element-wise consumer).  Their storage holds no defined value after tofu_execute; parity
- * tests check them through their consumers.  Errors: TOFU_ERR_ARG (null exec) / TOFU_ERR_CAPACITY. */
+ * tests check them through their consumers.  Errors: TOFU_ERR_ARG (null exec) / TOFU_ERR_SPACE. */
 int tofu_exec_unmaterialized(const tofu_exec* e, char* out, size_t cap, size_t* len);
 /* Issue launches [first, last) only (instrumented timing). */
 int tofu_execute_range(tofu_exec* e, int first, int last, void* stream);
@@ -344,8 +344,23 @@ typedef struct {
   int64_t src_stride[4];
   int src_dtype, pad_;
 } tofu_piece;
-/* pieces_dev: device array of n pieces (caller-owned). */
-int tofu_pieces_run(const tofu_piece* pieces_dev, int n, int64_t max_elems, void* stream);
+/* A task: segments [q0, q0 + nq) of piece `piece` (a row — the normalised innermost dim — is cut into
+ * segments of <= 256 vectors; segment q = row q / nseg, part q % nseg).  pad_ = 1 when the piece is a plain
+ * copy (one source, same dtype, 16-byte vectors). */
+typedef struct {
+  int piece, pad_;
+  int64_t q0, nq;
+} tofu_piece_task;
+/* Host: normalise the n pieces IN PLACE (dims contiguous in dst and src merged, unit dims dropped; pad_ =
+ * the vector width V in {8,4,2,1} elements: V divides the row and keeps every row start and base pointer
+ * V-element aligned) and cut them into tasks of whole segments (~4096 vectors, >= 8 segments).  tasks may be NULL (count only); *ntasks =
+ * the number of tasks.  Errors: TOFU_ERR_ARG (nsrc outside [1, TOFU_MAX_SRC], a strided innermost dim in a
+ * rank-4 piece, > 2^32 rows), TOFU_ERR_SPACE (cap < *ntasks; the first cap tasks are written). */
+int tofu_pieces_tasks(tofu_piece* pieces, int n, tofu_piece_task* tasks, int64_t cap, int64_t* ntasks);
+/* Device: run ntasks tasks over pieces (both device arrays, caller-owned, as tofu_pieces_tasks left them).
+ * all_raw != 0 (every task's pad_ == 1) selects the plain-copy kernel (16-byte moves, high occupancy). */
+int tofu_pieces_run(const tofu_piece* pieces_dev, const tofu_piece_task* tasks_dev, int64_t ntasks, int all_raw,
+                    void* stream);
 
 /* a7 — element-wise kernels on contiguous n-element buffers.
  *   TOFU_EW_RELU      y = max(x0, 0)                      (bf16 -> bf16)

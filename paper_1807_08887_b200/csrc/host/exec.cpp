@@ -159,9 +159,13 @@ struct Exec {
     int kind;  // 0 fetch pieces, 1 compute, 2 reduce pieces, 3 barrier, 4 memset
     int op, li;
     int64_t piece_off, npieces, max_elems;
+    int64_t task_off = 0, ntasks = 0;  // fetch / reduce: tofu_piece_task range (tofu_pieces_tasks)
+    int all_raw = 0;                   // every task a plain copy (the copy kernel)
   };
   std::vector<Launch> launches;
   tofu_piece* pieces_dev = nullptr;
+  tofu_piece_task* tasks_dev = nullptr;
+  std::vector<tofu_piece_task> host_tasks;
   void* ws_dev = nullptr;  // split-K workspace shared by this executor's GEMMs (one stream)
   void* sk_dev = nullptr;  // stream-K workspace (partials + flags, zero-filled), shared likewise
   std::vector<tofu_piece> host_pieces;
@@ -943,6 +947,22 @@ void build_launches(Exec& E) {
     if (bar_r) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
   }
   if (E.multi_process) E.launches.push_back({3, -1, -1, 0, 0, 0});
+  // piece tasks of every fetch / reduce launch (pieces normalised in place; task piece indices are
+  // relative to the launch's first piece)
+  E.host_tasks.clear();
+  for (auto& L : E.launches) {
+    if (L.kind != 0 && L.kind != 2) continue;
+    int64_t nt = 0;
+    int rc = tofu_pieces_tasks(host.data() + L.piece_off, (int)L.npieces, nullptr, 0, &nt);
+    if (rc) throw Error(rc, "tofu_pieces_tasks failed");
+    L.task_off = (int64_t)E.host_tasks.size();
+    L.ntasks = nt;
+    E.host_tasks.resize(L.task_off + nt);
+    rc = tofu_pieces_tasks(host.data() + L.piece_off, (int)L.npieces, E.host_tasks.data() + L.task_off, nt, &nt);
+    if (rc) throw Error(rc, "tofu_pieces_tasks failed");
+    L.all_raw = 1;
+    for (int64_t q = 0; q < nt; ++q) L.all_raw &= E.host_tasks[L.task_off + q].pad_ == 1;
+  }
   E.host_pieces = std::move(host);
   int64_t n = 0;
   for (auto& L : E.launches)
@@ -1029,6 +1049,12 @@ void finalize(Exec& E) {
       throw Error(TOFU_ERR_CUDA, "cudaMalloc pieces");
     if (cudaMemcpy(E.pieces_dev, host.data(), host.size() * sizeof(tofu_piece), cudaMemcpyHostToDevice) != cudaSuccess)
       throw Error(TOFU_ERR_CUDA, "cudaMemcpy pieces");
+  }
+  if (!E.host_tasks.empty()) {
+    const size_t nb = E.host_tasks.size() * sizeof(tofu_piece_task);
+    if (cudaMalloc(&E.tasks_dev, nb) != cudaSuccess) throw Error(TOFU_ERR_CUDA, "cudaMalloc piece tasks");
+    if (cudaMemcpy(E.tasks_dev, E.host_tasks.data(), nb, cudaMemcpyHostToDevice) != cudaSuccess)
+      throw Error(TOFU_ERR_CUDA, "cudaMemcpy piece tasks");
   }
   // stream-K workspace: launches run one at a time on the executor's stream, each leaves the flags zeroed
   if (!E.sk_dev) {
@@ -1638,6 +1664,7 @@ extern "C" int tofu_exec_create(const tofu_graph* g, const tofu_plan* p, int n_l
       tofu::build_launches(E);
     } catch (...) {
       if (E.pieces_dev) cudaFree(E.pieces_dev);
+      if (E.tasks_dev) cudaFree(E.tasks_dev);
       if (E.flags_dev) cudaFree(E.flags_dev);
       delete h;
       throw;
@@ -1650,6 +1677,7 @@ extern "C" int tofu_exec_create(const tofu_graph* g, const tofu_plan* p, int n_l
 extern "C" void tofu_exec_destroy(tofu_exec* h) {
   if (!h) return;
   if (h->e.pieces_dev) cudaFree(h->e.pieces_dev);
+  if (h->e.tasks_dev) cudaFree(h->e.tasks_dev);
   if (h->e.flags_dev) cudaFree(h->e.flags_dev);
   if (h->e.ws_dev) cudaFree(h->e.ws_dev);
   if (h->e.sk_dev) cudaFree(h->e.sk_dev);
@@ -1663,7 +1691,7 @@ int run_launch(Exec& E, const Exec::Launch& L, cudaStream_t st) {
   switch (L.kind) {
     case 0:
     case 2:
-      if (!E.skip_comm) rc = tofu_pieces_run(E.pieces_dev + L.piece_off, (int)L.npieces, L.max_elems, st);
+      if (!E.skip_comm) rc = tofu_pieces_run(E.pieces_dev + L.piece_off, E.tasks_dev + L.task_off, L.ntasks, L.all_raw, st);
       break;
     case 1:
       rc = run_compute(E, L.op, L.li, st);
@@ -1713,11 +1741,20 @@ std::string launch_desc(const Exec& E, int i) {
   o += ",\"rank\":" + std::to_string(L.li >= 0 ? E.local[L.li] : -1);
   double flops = 0, bytes = 0;
   if (L.kind == 0 || L.kind == 2) {
+    double rows = 0, row_bytes = 0, vec = 0, elems = 0;
     for (int64_t p = L.piece_off; p < L.piece_off + L.npieces; ++p) {
       const auto& pc = E.host_pieces[p];
       const double n = (double)pc.extent[0] * pc.extent[1] * pc.extent[2] * pc.extent[3];
       bytes += n * ((pc.src_dtype == TOFU_BF16 ? 2 : 4) * pc.nsrc + (pc.dst_dtype == TOFU_BF16 ? 2 : 4));
+      rows += (double)pc.extent[0] * pc.extent[1] * pc.extent[2];
+      row_bytes += n * (pc.dst_dtype == TOFU_BF16 ? 2 : 4);
+      vec += n * pc.pad_;
+      elems += n;
     }
+    // pieces, tasks, mean destination row length (bytes) and element-weighted mean vector width
+    o += ",\"pieces\":" + std::to_string(L.npieces) + ",\"tasks\":" + std::to_string(L.ntasks) +
+         ",\"row_bytes\":" + json_num(rows > 0 ? row_bytes / rows : 0) +
+         ",\"vec\":" + json_num(elems > 0 ? vec / elems : 0);
   } else if (L.kind == 1) {
     const LOp& lo = E.lops[L.li][L.op];
     const std::string& dn = g.defs[g.ops[L.op].def].name;

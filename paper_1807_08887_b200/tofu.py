@@ -88,7 +88,8 @@ def lib():
             "tofu_gemm_bf16": [C.POINTER(GemmArgs), vp],
             "tofu_gemm_plan_tmaps": [C.POINTER(GemmArgs), vp, C.POINTER(C.c_int)],
             "tofu_gemm_launch_planned": [C.POINTER(GemmArgs), vp, C.c_int, vp],
-            "tofu_pieces_run": [vp, C.c_int, C.c_int64, vp],
+            "tofu_pieces_run": [vp, vp, C.c_int64, C.c_int, vp],
+            "tofu_pieces_tasks": [vp, C.c_int, vp, C.c_int64, i64p],
             "tofu_conv_bf16": [C.POINTER(ConvArgs), vp],
             "tofu_elementwise": [C.c_int, C.c_int64, vp, vp, vp, vp, C.c_float, C.c_float, vp],
             "tofu_describe_op": [C.c_char_p, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
@@ -196,8 +197,31 @@ def elementwise(kind, n, y=None, x0=None, x1=None, x2=None, s0=0.0, s1=0.0, stre
                                  s0, s1, _stream(stream)), "tofu_elementwise")
 
 
-def pieces_run(pieces_dev_ptr, n, max_elems, stream=None):
-    check(lib().tofu_pieces_run(C.c_void_p(pieces_dev_ptr), n, max_elems, _stream(stream)), "tofu_pieces_run")
+class Piece(C.Structure):
+    """tofu_piece (include/tofu.h)."""
+    _fields_ = [("extent", C.c_int64 * 4), ("dst", C.c_void_p), ("dst_stride", C.c_int64 * 4), ("dst_dtype", C.c_int),
+                ("nsrc", C.c_int), ("src", C.c_void_p * 8), ("src_stride", C.c_int64 * 4), ("src_dtype", C.c_int),
+                ("pad_", C.c_int)]
+
+
+class PieceTask(C.Structure):
+    _fields_ = [("piece", C.c_int), ("pad_", C.c_int), ("q0", C.c_int64), ("nq", C.c_int64)]
+
+
+def pieces_tasks(pieces):
+    """tofu_pieces_tasks on a ctypes array of Piece (normalised in place): returns a PieceTask array."""
+    n = C.c_int64(0)
+    check(lib().tofu_pieces_tasks(C.addressof(pieces), len(pieces), None, 0, C.byref(n)), "tofu_pieces_tasks")
+    tasks = (PieceTask * max(n.value, 1))()
+    check(lib().tofu_pieces_tasks(C.addressof(pieces), len(pieces), C.addressof(tasks), n.value, C.byref(n)),
+          "tofu_pieces_tasks")
+    return tasks, n.value
+
+
+def pieces_run(pieces_dev_ptr, tasks_dev_ptr, ntasks, all_raw=0, stream=None):
+    """tofu_pieces_run over device copies of the pieces and tasks (all_raw: every task's pad_ == 1)."""
+    check(lib().tofu_pieces_run(C.c_void_p(pieces_dev_ptr), C.c_void_p(tasks_dev_ptr), ntasks, all_raw,
+                                _stream(stream)), "tofu_pieces_run")
 
 
 # ----------------------------------------------------------------------------- host API

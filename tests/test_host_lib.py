@@ -289,3 +289,38 @@ def test_conv_body_must_be_a_contraction(tofu):
     spec["defs"][n] = spec["defs"][n].replace("] * W[", "] + W[")
     with pytest.raises(tofu.TofuError):
         _exec(tofu, spec)
+
+
+def test_piece_tasks_normalise_and_cover(tofu):
+    """tofu_pieces_tasks (host): contiguous dims merge (a whole-row box becomes one long row), the vector
+    width follows the alignment, and the tasks cover every segment (<= 256 vectors of a row) of every piece exactly once."""
+    ps = (tofu.Piece * 3)()
+    # [4, 6, 64] bf16 box that is whole rows in dst and src: merges to one row of 1536 elements, V = 8
+    p = ps[0]
+    for d, (e, s) in enumerate(zip([1, 4, 6, 64], [0, 384, 64, 1])):
+        p.extent[d], p.dst_stride[d], p.src_stride[d] = e, s, s
+    p.dst, p.src[0], p.nsrc, p.dst_dtype, p.src_dtype = 4096, 8192, 1, 0, 0
+    # [10, 3] fp32 rows inside a wider buffer, odd base offset: V = 1
+    p = ps[1]
+    for d, (e, ds_, ss_) in enumerate(zip([1, 1, 10, 3], [0, 0, 7, 1], [0, 0, 5, 1])):
+        p.extent[d], p.dst_stride[d], p.src_stride[d] = e, ds_, ss_
+    p.dst, p.src[0], p.src[1], p.nsrc, p.dst_dtype, p.src_dtype = 4100, 8192, 16384, 2, 1, 1
+    # big 2-D piece: 3 x 10000 bf16 in a pitch-10240 buffer: rows stay, V = 8, several tasks
+    p = ps[2]
+    for d, (e, s) in enumerate(zip([1, 1, 3, 10000], [0, 0, 10240, 1])):
+        p.extent[d], p.dst_stride[d], p.src_stride[d] = e, s, s
+    p.dst, p.src[0], p.nsrc, p.dst_dtype, p.src_dtype = 1 << 20, 1 << 24, 1, 0, 0
+    tasks, nt = tofu.pieces_tasks(ps)
+    assert [list(ps[0].extent), ps[0].pad_] == [[1, 1, 1, 1536], 8]
+    assert ps[1].pad_ == 1 and list(ps[1].extent) == [1, 1, 10, 3]
+    assert ps[2].pad_ == 8 and list(ps[2].extent) == [1, 1, 3, 10000]
+    cover = {}
+    for i in range(nt):
+        t = tasks[i]
+        cover.setdefault(t.piece, []).append((t.q0, t.nq))
+    for i, p in enumerate(ps):
+        rv = p.extent[3] // p.pad_
+        nv = p.extent[0] * p.extent[1] * p.extent[2] * ((rv + 255) // 256)
+        segs = sorted(cover[i])
+        assert segs[0][0] == 0 and all(a + n == b for (a, n), (b, _) in zip(segs, segs[1:]))
+        assert segs[-1][0] + segs[-1][1] == nv

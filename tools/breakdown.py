@@ -59,7 +59,8 @@ print("--- slowest launches")
 for i in sorted(range(nl), key=lambda i: -ms[i])[:25]:
     d = descs[i]
     print(f"{ms[i]:7.3f} ms {d['kind']:8s} {d['op']:22s} {d['def']:14s} TF/s={d['flops'] / (ms[i] / 1e3) / 1e12:7.1f} "
-          f"GB/s={d['bytes'] / (ms[i] / 1e3) / 1e9:7.1f} {d.get('fused', '')} {d.get('weights', '')}")
+          f"GB/s={d['bytes'] / (ms[i] / 1e3) / 1e9:7.1f} r{d.get('rank')} {d.get('mnk', '')} {d.get('fused', '')} "
+          f"{d.get('weights', '')}")
 
 if os.environ.get("UNIT"):
     print("--- launches of", os.environ["UNIT"])
