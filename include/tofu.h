@@ -333,8 +333,22 @@ int tofu_transpose_taps(const void* W, void* WT, int co, int taps, int ci, void*
 
 /* a5/a6 — box copy / reduction pieces (rank <= 4, innermost dim last, strides in elements).
  * A piece copies (nsrc == 1) or sums in order (nsrc > 1, fp32 arithmetic) nsrc source boxes of the same
- * extent into one destination box, converting dtype.  Sources may be peer pointers. */
+ * extent into one destination box, converting dtype.  Sources may be peer pointers.
+ * ep: the element-wise consumer of a reduced tensor applied to the sum v before the store (the
+ * partition-n-reduce fused with the next coalesced element-wise op, P:L674-678 / DESIGN R8); aux0 is laid
+ * out like dst (same strides):
+ *   TOFU_PIECE_RELU      dst = max(v, 0)
+ *   TOFU_PIECE_MASK      dst = aux0 (bf16) > 0 ? v : 0                       (relu gradient)
+ *   TOFU_PIECE_MOM_SGD   dst (f32 momentum, in/out): m = dst * s0 + v; dst = m; aux0 (bf16 weight, in/out):
+ *                        aux0 = aux0 - m * s1                                (momentum + SGD on a gradient)
+ *   TOFU_PIECE_ADD       dst = v + aux0 (bf16)          TOFU_PIECE_ADDRELU  dst = max(v + aux0, 0) */
 #define TOFU_MAX_SRC 8
+#define TOFU_PIECE_COPY 0
+#define TOFU_PIECE_RELU 1
+#define TOFU_PIECE_MASK 2
+#define TOFU_PIECE_MOM_SGD 3
+#define TOFU_PIECE_ADD 4
+#define TOFU_PIECE_ADDRELU 5
 typedef struct {
   int64_t extent[4];
   void* dst;
@@ -343,6 +357,10 @@ typedef struct {
   const void* src[TOFU_MAX_SRC];
   int64_t src_stride[4];
   int src_dtype, pad_;
+  int ep;          /* TOFU_PIECE_* */
+  float s0, s1;
+  int pad2_;
+  void* aux0;
 } tofu_piece;
 /* A task: segments [q0, q0 + nq) of piece `piece` (a row — the normalised innermost dim — is cut into
  * segments of <= 256 vectors; segment q = row q / nseg, part q % nseg).  pad_ = 1 when the piece is a plain

@@ -155,7 +155,7 @@ __device__ __forceinline__ void run_task(const tofu_piece& pc, int64_t q0, int64
   const int64_t rv = pc.extent[3] / V;
   const uint32_t nseg = (uint32_t)((rv + kSeg - 1) / kSeg);
   const uint32_t e2 = (uint32_t)pc.extent[2], e1 = (uint32_t)pc.extent[1];
-  const int nsrc = pc.nsrc;
+  const int nsrc = pc.nsrc, ep = pc.ep;
   const int sdt = pc.src_dtype, ddt = pc.dst_dtype;
   for (int64_t qq = warp; qq < nq; qq += nwarps) {
     const uint32_t q = (uint32_t)(q0 + qq);
@@ -183,6 +183,37 @@ __device__ __forceinline__ void run_task(const tofu_piece& pc, int64_t q0, int64
             load_f<V>(pc.src[s], sb + j * V, sdt, x);
 #pragma unroll
             for (int qv = 0; qv < V; ++qv) acc[u][qv] += x[qv];
+          }
+        }
+      }
+      if (ep != TOFU_PIECE_COPY) {  // the reduced tensor's element-wise consumer (aux0 laid out like dst)
+#pragma unroll
+        for (int u = 0; u < kUnrC; ++u) {
+          const int64_t j = j0 + 32 * u;
+          if (j >= je) continue;
+          float a[V];
+          if (ep == TOFU_PIECE_RELU) {
+#pragma unroll
+            for (int q = 0; q < V; ++q) acc[u][q] = fmaxf(acc[u][q], 0.f);
+          } else if (ep == TOFU_PIECE_MOM_SGD) {
+            float m[V];
+            load_f<V>(pc.dst, db + j * V, TOFU_F32, m);
+            load_f<V>(pc.aux0, db + j * V, TOFU_BF16, a);
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+              m[q] = m[q] * pc.s0 + acc[u][q];
+              a[q] = a[q] - m[q] * pc.s1;
+              acc[u][q] = m[q];
+            }
+            store_f<V>(pc.aux0, db + j * V, TOFU_BF16, a);
+          } else {
+            load_f<V>(pc.aux0, db + j * V, TOFU_BF16, a);
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+              if (ep == TOFU_PIECE_MASK) acc[u][q] = a[q] > 0.f ? acc[u][q] : 0.f;
+              else if (ep == TOFU_PIECE_ADD) acc[u][q] = acc[u][q] + a[q];
+              else acc[u][q] = fmaxf(acc[u][q] + a[q], 0.f);
+            }
           }
         }
       }
@@ -257,7 +288,8 @@ extern "C" int tofu_pieces_tasks(tofu_piece* pieces, int n, tofu_piece_task* tas
   int64_t nt = 0;
   for (int p = 0; p < n; ++p) {
     tofu_piece& pc = pieces[p];
-    if (pc.nsrc < 1 || pc.nsrc > TOFU_MAX_SRC) return TOFU_ERR_ARG;
+    if (pc.nsrc < 1 || pc.nsrc > TOFU_MAX_SRC || pc.ep < TOFU_PIECE_COPY || pc.ep > TOFU_PIECE_ADDRELU) return TOFU_ERR_ARG;
+    if (pc.ep == TOFU_PIECE_MOM_SGD && pc.dst_dtype != TOFU_F32) return TOFU_ERR_ARG;
     // merge dims contiguous in dst and src (inner to outer), drop unit dims
     int64_t ex[4], ds[4], ss[4];
     int m = 0;
@@ -293,6 +325,7 @@ extern "C" int tofu_pieces_tasks(tofu_piece* pieces, int n, tofu_piece_task* tas
       for (int d = 0; d < 3 && ok; ++d) ok = pc.dst_stride[d] % V == 0 && pc.src_stride[d] % V == 0;
       ok = ok && reinterpret_cast<uintptr_t>(pc.dst) % (V * de) == 0;
       for (int s = 0; s < pc.nsrc && ok; ++s) ok = reinterpret_cast<uintptr_t>(pc.src[s]) % (V * se) == 0;
+      if (pc.ep != TOFU_PIECE_COPY && pc.ep != TOFU_PIECE_RELU) ok = ok && reinterpret_cast<uintptr_t>(pc.aux0) % (V * 2) == 0;
       if (ok) break;
     }
     if (V == 1 && (pc.dst_stride[3] != 1 || pc.src_stride[3] != 1)) {
@@ -313,7 +346,7 @@ extern "C" int tofu_pieces_tasks(tofu_piece* pieces, int n, tofu_piece_task* tas
     const int64_t nq = rows * nseg;
     if (nq > 0xFFFFFFFFll) return TOFU_ERR_ARG;   // 32-bit segment index in the kernel
     const int64_t per = std::max<int64_t>(8, tofu::kTaskVecs / std::max<int64_t>(seglen, 1));
-    const int raw = pc.nsrc == 1 && pc.src_dtype == pc.dst_dtype && (V * se) % 16 == 0;
+    const int raw = pc.nsrc == 1 && pc.src_dtype == pc.dst_dtype && (V * se) % 16 == 0 && pc.ep == TOFU_PIECE_COPY;
     for (int64_t q0 = 0; q0 < nq; q0 += per) {
       if (nt < cap && tasks) tasks[nt] = tofu_piece_task{p, raw, q0, std::min<int64_t>(per, nq - q0)};
       ++nt;

@@ -107,6 +107,7 @@ struct LOp {
   bool fused_next = false;    // LSTM cell: this launch also computes the next op (c+h, bwd_a+bwd_c)
   bool fused_loss_grad = false;  // sumsq: this launch also computes the next op, mse_grad of the same inputs
   int ep = 0;                 // element-wise epilogue of the output's consumers: 1 relu, 2 add, 4 mask
+  int red_ep = 0;             // the reduce pieces apply the output's consumer (TOFU_PIECE_*)
   Buf epi_add, epi_mask;      // its bf16 operands (the output's layout)
   std::vector<tofu_piece> fetch, reduce;
   std::vector<int> fetch_src, reduce_nremote;  // for the ledger
@@ -856,6 +857,119 @@ void lower(Exec& E) {
         Lo.out = out;
         Le.skip = true;
       }
+  }
+  // Partition-n-reduce fused with the reduced tensor's element-wise consumer (P:L674-678 coalescing, R8): when
+  // op o's output T is summed by reduce pieces (a split reduction) and T's single reader e is a relu,
+  // relu_grad(·, T), add / addrelu or momentum(+SGD) op whose operands are all the rank's own shards of T's
+  // box, the reduce pieces apply e while storing: T itself is never written, e's launch disappears (and, for the
+  // optimizer, the separate fp32 gradient round trip).  Decided for all ranks at once (the launch sequence is
+  // the same in every process).
+  if (E.fuse) {
+    std::vector<int> producer(g.tensors.size(), -1), nprod(g.tensors.size(), 0), nread(g.tensors.size(), 0);
+    for (size_t o = 0; o < g.ops.size(); ++o) {
+      producer[g.ops[o].output] = (int)o;
+      ++nprod[g.ops[o].output];
+      for (int t : g.ops[o].inputs) ++nread[t];
+    }
+    std::set<int> aliased;
+    for (auto& pr : g.alias) {
+      aliased.insert(pr.first);
+      aliased.insert(pr.second);
+    }
+    auto earlier = [&](int t, int o) { return nprod[t] == 0 || (nprod[t] == 1 && producer[t] < o); };
+    for (size_t o = 0; o < g.ops.size(); ++o) {
+      const int t = g.ops[o].output;
+      if (nread[t] != 1 || nprod[t] != 1 || aliased.count(t)) continue;
+      int e = -1;
+      for (size_t x = o + 1; x < g.ops.size() && e < 0; ++x)
+        for (int u : g.ops[x].inputs)
+          if (u == t) e = (int)x;
+      if (e < 0) continue;
+      const std::string& en = g.def_of(e).kernel;
+      const auto& ins = g.ops[e].inputs;
+      int ep = 0, aux_i = -1;
+      if ((en == "relu" || en == "relu4") && ins[0] == t) ep = TOFU_PIECE_RELU;
+      else if ((en == "relu_grad" || en == "relu_grad4") && ins[1] == t && ins[0] != t) {
+        ep = TOFU_PIECE_MASK;
+        aux_i = 0;
+      } else if ((en == "add4" || en == "addrelu") && ins.size() == 2 && (ins[0] == t) != (ins[1] == t)) {
+        ep = en == "add4" ? TOFU_PIECE_ADD : TOFU_PIECE_ADDRELU;
+        aux_i = ins[0] == t ? 1 : 0;
+      } else if (is_mom(en) && ins[1] == t && e + 1 < (int)g.ops.size()) {
+        ep = TOFU_PIECE_MOM_SGD;
+      }
+      if (!ep || (aux_i >= 0 && !earlier(ins[aux_i], (int)o))) continue;
+      if (ep == TOFU_PIECE_MOM_SGD) {  // moving mom + sgd up to o must not reorder any access to M / W
+        const OpInfo &b = g.ops[e], &c = g.ops[e + 1];
+        std::set<int> state = {b.inputs[0], b.output, c.inputs[0], c.output};
+        for (auto& pr : g.alias)
+          if (state.count(pr.first) || state.count(pr.second)) {
+            state.insert(pr.first);
+            state.insert(pr.second);
+          }
+        bool clash = false;
+        for (int x = (int)o + 1; x < e; ++x) {
+          for (int u : g.ops[x].inputs) clash |= state.count(u) > 0;
+          clash |= state.count(g.ops[x].output) > 0;
+        }
+        if (clash) continue;
+      }
+      bool ok = true, any = false;
+      for (int r = 0; r < k && ok; ++r) {
+        LOp &Lo = all[r][o], &Le = all[r][e];
+        if (E.lay[r].shard_off[t] < 0) {
+          ok = Lo.reduce.empty();
+          continue;
+        }
+        const auto& own = E.lay[r].shard_box[t];
+        int64_t cov = 0;
+        for (auto& pc : Lo.reduce) cov += pc.extent[0] * pc.extent[1] * pc.extent[2] * pc.extent[3];
+        if (Lo.reduce.empty() || cov != vol(own)) {
+          ok = false;
+          break;
+        }
+        any = true;
+        auto mine = [&](const Buf& b) { return b.direct && same(b.box, own) && same(b.buf_box, own); };
+        ok = !Le.skip && Le.fetch.empty() && Le.reduce.empty() && mine(Le.out) && Lo.fused_opt < 0;
+        for (auto& b : Le.in) ok = ok && (b.direct ? mine(b) : false) ;
+        if (ep == TOFU_PIECE_MOM_SGD) {
+          const LOp& Ls = all[r][e + 1];
+          ok = ok && Le.fused_sgd && Ls.skip;
+          for (auto& b : Ls.in) ok = ok && mine(b);
+          ok = ok && mine(Ls.out) && Le.out.dtype == TOFU_F32;
+        } else {
+          ok = ok && Le.out.dtype == TOFU_BF16;
+        }
+      }
+      if (!ok || !any) continue;
+      const float s0 = ep == TOFU_PIECE_MOM_SGD ? (float)g.def_of(e).kconst.at(0) : 0.f;
+      const float s1 = ep == TOFU_PIECE_MOM_SGD ? (float)g.def_of(e + 1).kconst.at(0) : 0.f;
+      for (int r = 0; r < k; ++r) {
+        if (E.lay[r].shard_off[t] < 0) continue;
+        LOp &Lo = all[r][o], &Le = all[r][e];
+        const auto& own = E.lay[r].shard_box[t];
+        char* base = E.arena.empty() ? nullptr : E.arena[r];
+        for (auto& pc : Lo.reduce) {
+          // the piece's destination cell inside `own`: recover its element offset from the T destination
+          const int64_t cell_off = base ? ((char*)pc.dst - (base + E.lay[r].shard_off[t])) / g.itemsize(t) : 0;
+          pc.ep = ep;
+          pc.s0 = s0;
+          pc.s1 = s1;
+          const Buf& outb = Le.out;  // relu / mask / add: e's output; mom: M_new = M (in place)
+          pc.dst_dtype = outb.dtype;
+          pc.dst = base ? base + outb.off + cell_off * (outb.dtype == TOFU_BF16 ? 2 : 4) : nullptr;
+          if (aux_i >= 0) pc.aux0 = base ? base + Le.in[aux_i].off + cell_off * 2 : nullptr;
+          if (ep == TOFU_PIECE_MOM_SGD) {
+            const Buf& W = all[r][e + 1].in[0];
+            pc.aux0 = base ? base + W.off + cell_off * 2 : nullptr;
+          }
+        }
+        Lo.red_ep = ep;
+        Le.skip = true;
+        (void)own;
+      }
+      E.unmat.insert(t);
+    }
   }
   // Conv data gradients read their weights K-major from an executor-owned transposed copy of the weight
   // shard (W[co][ky][kx][ci] -> WT[ci][ky][kx][co], refreshed right before the launch): the MN-major weight
@@ -1746,6 +1860,8 @@ std::string launch_desc(const Exec& E, int i) {
       const auto& pc = E.host_pieces[p];
       const double n = (double)pc.extent[0] * pc.extent[1] * pc.extent[2] * pc.extent[3];
       bytes += n * ((pc.src_dtype == TOFU_BF16 ? 2 : 4) * pc.nsrc + (pc.dst_dtype == TOFU_BF16 ? 2 : 4));
+      if (pc.ep == TOFU_PIECE_MASK || pc.ep == TOFU_PIECE_ADD || pc.ep == TOFU_PIECE_ADDRELU) bytes += n * 2;
+      if (pc.ep == TOFU_PIECE_MOM_SGD) bytes += n * (4 + 2 + 2);  // momentum read, weight read + written
       rows += (double)pc.extent[0] * pc.extent[1] * pc.extent[2];
       row_bytes += n * (pc.dst_dtype == TOFU_BF16 ? 2 : 4);
       vec += n * pc.pad_;
@@ -1799,6 +1915,12 @@ std::string launch_desc(const Exec& E, int i) {
     o += ",\"kernel\":" + json_quote(kd.kernel) + ",\"kconst\":[";
     for (size_t q = 0; q < kd.kconst.size(); ++q) o += (q ? "," : "") + json_num(kd.kconst[q]);
     o += "]";
+  }
+  if (L.kind == 2 && L.op >= 0 && !E.lops.empty()) {
+    static const char* red_names[] = {"", "reduce+relu", "reduce+mask", "reduce+mom+sgd", "reduce+add", "reduce+addrelu"};
+    int rep = 0;
+    for (auto& lops : E.lops) rep = std::max(rep, lops[L.op].red_ep);
+    if (rep) o += std::string(",\"fused\":\"") + red_names[rep] + "\"";
   }
   if (L.kind == 1 && lo_fused(E, L)) o += ",\"fused\":\"mom+sgd\"";
   if (L.kind == 1 && E.lops[L.li][L.op].fused_opt >= 0) o += ",\"fused\":\"gemm+mom+sgd\"";

@@ -201,7 +201,8 @@ class Piece(C.Structure):
     """tofu_piece (include/tofu.h)."""
     _fields_ = [("extent", C.c_int64 * 4), ("dst", C.c_void_p), ("dst_stride", C.c_int64 * 4), ("dst_dtype", C.c_int),
                 ("nsrc", C.c_int), ("src", C.c_void_p * 8), ("src_stride", C.c_int64 * 4), ("src_dtype", C.c_int),
-                ("pad_", C.c_int)]
+                ("pad_", C.c_int), ("ep", C.c_int), ("s0", C.c_float), ("s1", C.c_float), ("pad2_", C.c_int),
+                ("aux0", C.c_void_p)]
 
 
 class PieceTask(C.Structure):
