@@ -1,10 +1,57 @@
 // Shared device helpers for the sm_100a kernels (PTX wrappers).
 #pragma once
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
 namespace tofu {
+
+// ---------------------------------------------------------------- programmatic dependent launch (PDL)
+// Every libtofu kernel is launched with programmatic stream serialization (launch_k below) and calls
+// pdl_trigger(); pdl_wait() once its prologue (barrier init, TMEM allocation, tensor-map prefetch) is done and
+// before it touches global memory a predecessor writes or reads: the next kernel's launch and prologue then
+// overlap the current kernel's tail instead of following its completion.  griddepcontrol.wait returns once
+// every prerequisite grid has completed and its memory is visible (a no-op when launched without PDL).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+inline bool pdl_enabled() {  // TOFU_PDL=0 launches every kernel fully serialised (A/B switch)
+  static const bool on = [] {
+    const char* e = std::getenv("TOFU_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// cudaLaunchKernelEx with PDL (and an optional cluster dimension along x).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (cluster > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = cluster;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  if (pdl_enabled()) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -169,6 +169,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  tofu::pdl_trigger();
+  tofu::pdl_wait();  // prologue done: now wait for the predecessor's results (PDL)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (dense operand)
@@ -650,6 +652,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 __global__ void __launch_bounds__(256) splitk_reduce(const float* __restrict__ ws, int splits, int M, int N, float* C,
                                                      int64_t ldc, int mode, __nv_bfloat16* D, int64_t ldd, float s0,
                                                      float s1) {
+  tofu::pdl_trigger();
+  tofu::pdl_wait();
   const int64_t plane = (int64_t)M * N;
   if (N % 4 == 0 && ldc % 4 == 0 && (mode != 3 || ldd % 4 == 0) && !(reinterpret_cast<uintptr_t>(C) & 15) &&
       !(reinterpret_cast<uintptr_t>(D) & 7)) {  // vectorised: 4 elements per thread
@@ -701,6 +705,8 @@ __global__ void __launch_bounds__(256) splitk_reduce(const float* __restrict__ w
 // zero output rows of a kind-0 sub-op with no taps (e.g. the odd phases of a 1x1 stride-2 data gradient):
 // one thread per (row, 8 channels), 16-byte stores (N % 8 == 0 and 16-byte aligned rows, checked by the host)
 __global__ void __launch_bounds__(256) zero_rows(Params P) {
+  tofu::pdl_trigger();
+  tofu::pdl_wait();
   const tofu_conv_args& a = P.a;
   const int ngyx = a.ngy * a.ngx;
   const int n8 = P.N / 8;
@@ -725,6 +731,8 @@ __global__ void __launch_bounds__(256) zero_rows(Params P) {
 __device__ __forceinline__ float bf(const __nv_bfloat16* p, int64_t i) { return __bfloat162float(p[i]); }
 
 __global__ void __launch_bounds__(256) conv_direct(Params P) {
+  tofu::pdl_trigger();
+  tofu::pdl_wait();
   const tofu_conv_args& a = P.a;
   const int ngyx = a.ngy * a.ngx;
   const int64_t total = (int64_t)P.M * P.N;
@@ -892,22 +900,14 @@ static int launch_t(const Params& P, const CUtensorMap* tm, cudaStream_t st) {
     Q.sk_tiles = 0;
     const int pair_units = ((P.M + 2 * BM - 1) / (2 * BM)) * ((P.N + BN - 1) / BN);
     const int ncl = pair_units < g_sms / 2 ? pair_units : g_sms / 2;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * ncl, 1, 1);
-    cfg.blockDim = dim3(NTHREADS, 1, 1);
-    cfg.dynamicSmemBytes = C_::SMEM;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, Q, tm[0], tm[1], tm[2], tm[4]) == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
+    return tofu::launch_k(kern, dim3(2 * ncl), dim3(NTHREADS), C_::SMEM, st, 2, Q, tm[0], tm[1], tm[2], tm[4]) ==
+                   cudaSuccess
+               ? TOFU_OK
+               : TOFU_ERR_CUDA;
   }
-  kern<<<grid, NTHREADS, C_::SMEM, st>>>(Q, tm[0], tm[1], tm[2], tm[4]);
-  return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
+  return tofu::launch_k(kern, dim3(grid), dim3(NTHREADS), C_::SMEM, st, 1, Q, tm[0], tm[1], tm[2], tm[4]) == cudaSuccess
+             ? TOFU_OK
+             : TOFU_ERR_CUDA;
 }
 
 static int dispatch(const Params& P, const CUtensorMap* tm, int mode, cudaStream_t st) {
@@ -1146,7 +1146,7 @@ extern "C" int tofu_conv_launch_planned(const tofu_conv_args* a, const void* tma
   if (a->direct) {
     int blocks = (int)(((int64_t)M * N + 255) / 256);
     if (blocks > g_sms * 16) blocks = g_sms * 16;
-    conv_direct<<<blocks, 256, 0, st>>>(P);
+    tofu::launch_k(conv_direct, dim3(blocks), dim3(256), 0, st, 1, P);
     return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
   }
   if (K == 0) {
@@ -1157,7 +1157,7 @@ extern "C" int tofu_conv_launch_planned(const tofu_conv_args* a, const void* tma
     if (N % 8) return TOFU_ERR_ALIGN;
     int blocks = (int)(((int64_t)M * (N / 8) + 255) / 256);
     if (blocks > g_sms * 8) blocks = g_sms * 8;
-    zero_rows<<<blocks, 256, 0, st>>>(P);
+    tofu::launch_k(zero_rows, dim3(blocks), dim3(256), 0, st, 1, P);
     return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
   }
   if (a->kind == 0) return dispatch(P, tm, a->c_mode, st);
@@ -1167,7 +1167,7 @@ extern "C" int tofu_conv_launch_planned(const tofu_conv_args* a, const void* tma
     if (rc) return rc;
     int blocks = (int)(((int64_t)M * N + 255) / 256);
     if (blocks > g_sms * 8) blocks = g_sms * 8;
-    splitk_reduce<<<blocks, 256, 0, st>>>(reinterpret_cast<const float*>(a->ws), P.splits, M, N,
+    tofu::launch_k(splitk_reduce, dim3(blocks), dim3(256), 0, st, 1, reinterpret_cast<const float*>(a->ws), P.splits, M, N,
                                           reinterpret_cast<float*>(a->C), a->ldc, a->c_mode,
                                           reinterpret_cast<__nv_bfloat16*>(a->D), a->ldd, a->s0, a->s1);
     return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;

@@ -36,6 +36,8 @@ template <int KIND>
 __global__ void __launch_bounds__(256) ew_kernel(int64_t n, void* __restrict__ y, const void* __restrict__ x0,
                                                  const void* __restrict__ x1, void* __restrict__ x2, float s0,
                                                  float s1) {
+  tofu::pdl_trigger();
+  tofu::pdl_wait();
   const int64_t nvec = n / 8;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   float local = 0.f;
@@ -179,7 +181,7 @@ extern "C" int tofu_elementwise(int kind, int64_t n, void* y, const void* x0, co
   if (grid > tofu::SUMSQ_MAX_BLOCKS) grid = tofu::SUMSQ_MAX_BLOCKS;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   switch (kind) {
-#define K(X) case X: tofu::ew_kernel<X><<<(unsigned)grid, 256, 0, st>>>(n, y, x0, x1, x2, s0, s1); break;
+#define K(X) case X: tofu::launch_k(tofu::ew_kernel<X>, dim3((unsigned)grid), dim3(256), 0, st, 1, n, y, x0, x1, x2, s0, s1); break;
     K(TOFU_EW_RELU) K(TOFU_EW_RELU_GRAD) K(TOFU_EW_MSE_GRAD) K(TOFU_EW_MOM) K(TOFU_EW_SGD) K(TOFU_EW_SGD_MOM)
     K(TOFU_EW_SUMSQ) K(TOFU_EW_ADD) K(TOFU_EW_ADDRELU) K(TOFU_EW_SUMSQ_MSE_GRAD)
 #undef K

@@ -52,7 +52,10 @@ struct GemmCfg {
   static constexpr bool LOADS = MODE == 2 || MODE == 3 || MODE == 5;
   // the fused optimizer (MODE 3) and the fused element-wise epilogue (MODE 5) stream extra operands through
   // the epilogue (HBM-bound): deeper prefetch
-  static constexpr int NBUF = LOADS ? (MODE == 3 ? (W8 ? 2 : 3) : MODE == 5 ? 2 : 3) : 2;
+#ifndef TOFU_NBUF5
+#define TOFU_NBUF5 2
+#endif
+  static constexpr int NBUF = LOADS ? (MODE == 3 ? (W8 ? 2 : 3) : MODE == 5 ? TOFU_NBUF5 : 3) : 2;
   static constexpr int C_BYTES = 32 * 32 * (MODE == 0 || MODE == 5 ? 2 : 4);
   // MODE 3: W chunk at D_OFF.  MODE 5: add chunk at 0 (the bf16 result overwrites it in place, each thread
   // its own 16-byte slots), mask chunk at D_OFF = 2048.
@@ -164,6 +167,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // prologue done: now wait for the predecessor's results (PDL)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -559,25 +564,14 @@ static int launch_t(const tofu_gemm_args* g, const CUtensorMap* tm, const PieceM
   if constexpr (CL2) {  // clusters of 2 over pair units (m tiles 2p, 2p+1 of one n tile)
     const int pair_units = ((g->M + 2 * BM - 1) / (2 * BM)) * ((g->N + BN - 1) / BN);
     const int ncl = pair_units < g_num_sms / 2 ? pair_units : g_num_sms / 2;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * ncl, 1, 1);
-    cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
-    cfg.dynamicSmemBytes = Cfg::SMEM;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, pp, tm[0], tm[1], tm[2], tm[3], tm[5], g->M, g->N, g->K,
-                                             g->s0, g->s1, 1, g->ep, 0, g->sk_ws);
+    const cudaError_t e = launch_k(kern, dim3(2 * ncl), dim3(Cfg::THREADS), Cfg::SMEM, st, 2, pp, tm[0], tm[1], tm[2],
+                                   tm[3], tm[5], g->M, g->N, g->K, g->s0, g->s1, 1, g->ep, 0, g->sk_ws);
     return e == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
   }
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(pp, tm[0], tm[1], tm[2], tm[3], tm[5], g->M, g->N, g->K, g->s0, g->s1,
-                                             splits, g->ep, sk, g->sk_ws);
-  return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
+  return launch_k(kern, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, st, 1, pp, tm[0], tm[1], tm[2], tm[3], tm[5], g->M,
+                  g->N, g->K, g->s0, g->s1, splits, g->ep, sk, g->sk_ws) == cudaSuccess
+             ? TOFU_OK
+             : TOFU_ERR_CUDA;
 }
 
 template <int BN>
@@ -632,6 +626,8 @@ static int dispatch_bn(const tofu_gemm_args* g, const CUtensorMap* tm, const Pie
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N,
                                                             void* C, int ldc, int mode, __nv_bfloat16* D, int ldd,
                                                             float s0, float s1) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t plane = (int64_t)M * N;
   if (mode == 3 && N % 4 == 0 && ldc % 4 == 0 && ldd % 4 == 0 && !(reinterpret_cast<uintptr_t>(C) & 15) &&
       !(reinterpret_cast<uintptr_t>(D) & 7)) {  // vectorised: 4 elements (float4 momentum, 4 bf16 weights)
@@ -913,7 +909,7 @@ extern "C" int tofu_gemm_launch_planned(const tofu_gemm_args* g, const void* tma
     const int64_t n = (int64_t)g->M * g->N / 4 + 1;
     int blocks = (int)((n + 255) / 256);
     if (blocks > g_num_sms * 8) blocks = g_num_sms * 8;
-    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float*>(g->ws), g->splits, g->M, g->N, g->C,
+    launch_k(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, st, 1, reinterpret_cast<const float*>(g->ws), g->splits, g->M, g->N, g->C,
                                                  g->ldc, g->c_mode, reinterpret_cast<__nv_bfloat16*>(g->D), g->ldd,
                                                  g->s0, g->s1);
     return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;

@@ -106,6 +106,8 @@ __device__ __forceinline__ float sig(float x) { return 1.f / (1.f + __expf(-x));
 
 template <int V>
 __global__ void __launch_bounds__(256) lstm_kernel(const LstmArgs a) {
+  tofu::pdl_trigger();
+  tofu::pdl_wait();
   const int64_t nhv = a.nh / V;
   const int64_t n = a.nb * nhv;
   const int kind = a.kind;
@@ -235,8 +237,8 @@ extern "C" int tofu_lstm_cell(int kind, int64_t nb, int64_t nh, int g0, int ng, 
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (vw == 8) tofu::lstm_kernel<8><<<(unsigned)blocks, 256, 0, st>>>(a);
-  else if (vw == 4) tofu::lstm_kernel<4><<<(unsigned)blocks, 256, 0, st>>>(a);
-  else tofu::lstm_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(a);
+  if (vw == 8) tofu::launch_k(tofu::lstm_kernel<8>, dim3((unsigned)blocks), dim3(256), 0, st, 1, a);
+  else if (vw == 4) tofu::launch_k(tofu::lstm_kernel<4>, dim3((unsigned)blocks), dim3(256), 0, st, 1, a);
+  else tofu::launch_k(tofu::lstm_kernel<1>, dim3((unsigned)blocks), dim3(256), 0, st, 1, a);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }

@@ -231,6 +231,8 @@ __device__ __forceinline__ void run_task(const tofu_piece& pc, int64_t q0, int64
 // every piece (checked on the host: the task's pad_ is 1).
 __global__ void __launch_bounds__(256) pieces_copy_kernel(const tofu_piece* __restrict__ pieces,
                                                           const tofu_piece_task* __restrict__ tasks, int ntasks) {
+  tofu::pdl_trigger();
+  tofu::pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
     const tofu_piece_task T = tasks[t];
@@ -269,6 +271,8 @@ __global__ void __launch_bounds__(256) pieces_copy_kernel(const tofu_piece* __re
 
 __global__ void __launch_bounds__(256, 2) pieces_kernel(const tofu_piece* __restrict__ pieces,
                                                      const tofu_piece_task* __restrict__ tasks, int ntasks) {
+  tofu::pdl_trigger();
+  tofu::pdl_wait();
   for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
     const tofu_piece_task T = tasks[t];
     const tofu_piece& pc = pieces[T.piece];
@@ -362,10 +366,11 @@ extern "C" int tofu_pieces_run(const tofu_piece* pieces_dev, const tofu_piece_ta
   const int64_t grid = std::min<int64_t>(ntasks, 148 * 8);
   const int n = (int)std::min<int64_t>(ntasks, INT32_MAX);
   if (all_raw)
-    tofu::pieces_copy_kernel<<<(unsigned)grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(pieces_dev,
-                                                                                                tasks_dev, n);
+    tofu::launch_k(tofu::pieces_copy_kernel, dim3((unsigned)grid), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 1,
+                   pieces_dev, tasks_dev, n);
   else
-    tofu::pieces_kernel<<<(unsigned)grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(pieces_dev, tasks_dev, n);
+    tofu::launch_k(tofu::pieces_kernel, dim3((unsigned)grid), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 1,
+                   pieces_dev, tasks_dev, n);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }
 
@@ -374,6 +379,8 @@ extern "C" int tofu_pieces_run(const tofu_piece* pieces_dev, const tofu_piece_ta
 // acquire on the peer mapping).  flags: device array of n pointers (peer-mapped epoch words).
 namespace tofu {
 __global__ void barrier_kernel(unsigned long long* const* flags, int rank, int n) {
+  tofu::pdl_trigger();
+  tofu::pdl_wait();
   __shared__ unsigned long long epoch;
   if (threadIdx.x == 0) {
     unsigned long long old;
@@ -392,7 +399,7 @@ __global__ void barrier_kernel(unsigned long long* const* flags, int rank, int n
 }  // namespace tofu
 
 extern "C" int tofu_barrier_run(void* flags_ptrs_dev, int rank, int n, void* stream) {
-  tofu::barrier_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<unsigned long long* const*>(flags_ptrs_dev), rank, n);
+  tofu::launch_k(tofu::barrier_kernel, dim3(1), dim3(32), 0, reinterpret_cast<cudaStream_t>(stream), 1,
+                 reinterpret_cast<unsigned long long* const*>(flags_ptrs_dev), rank, n);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }

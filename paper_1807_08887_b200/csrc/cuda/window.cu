@@ -36,6 +36,8 @@ __device__ __forceinline__ void st8(void* p, const float (&f)[8], bool f32) {
 __device__ __forceinline__ int64_t fdiv(int64_t a, int64_t d) { return a >= 0 ? a / d : -((-a + d - 1) / d); }
 
 __global__ void __launch_bounds__(256) maxpool_kernel(tofu_window_args a) {
+  tofu::pdl_trigger();
+  tofu::pdl_wait();
   const int c8 = a.C / 8;
   const int64_t total = (int64_t)a.nb * a.Ho * a.Wo * c8;
   const __nv_bfloat16* X = reinterpret_cast<const __nv_bfloat16*>(a.X);
@@ -68,6 +70,8 @@ __global__ void __launch_bounds__(256) maxpool_kernel(tofu_window_args a) {
 }
 
 __global__ void __launch_bounds__(256) maxpool_grad_kernel(tofu_window_args a) {
+  tofu::pdl_trigger();
+  tofu::pdl_wait();
   const int c8 = a.C / 8;
   const int64_t total = (int64_t)a.nb * a.H * a.W * c8;
   const __nv_bfloat16* X = reinterpret_cast<const __nv_bfloat16*>(a.X);
@@ -109,6 +113,8 @@ __global__ void __launch_bounds__(256) maxpool_grad_kernel(tofu_window_args a) {
 
 // out[b, c] = Σ_{y,x} X[b,y,x,c] * s: one warp per (b, 8 channels), lanes stride the pixels
 __global__ void __launch_bounds__(256) gap_kernel(tofu_window_args a) {
+  tofu::pdl_trigger();
+  tofu::pdl_wait();
   const int c8 = a.C / 8;
   const int64_t items = (int64_t)a.nb * c8;
   const int lane = threadIdx.x & 31;
@@ -135,6 +141,8 @@ __global__ void __launch_bounds__(256) gap_kernel(tofu_window_args a) {
 }
 
 __global__ void __launch_bounds__(256) gap_grad_kernel(tofu_window_args a) {
+  tofu::pdl_trigger();
+  tofu::pdl_wait();
   const int c8 = a.C / 8;
   const int64_t total = (int64_t)a.nb * a.H * a.W * c8;
   const __nv_bfloat16* D = reinterpret_cast<const __nv_bfloat16*>(a.dY);
@@ -157,6 +165,8 @@ __global__ void __launch_bounds__(256) gap_grad_kernel(tofu_window_args a) {
 // WT[i][t][o] = W[o][t][i]: 32x32 tiles through shared memory (coalesced reads and writes)
 __global__ void __launch_bounds__(256) transpose_taps_kernel(const __nv_bfloat16* __restrict__ W,
                                                              __nv_bfloat16* __restrict__ WT, int co, int taps, int ci) {
+  tofu::pdl_trigger();
+  tofu::pdl_wait();
   __shared__ __nv_bfloat16 tile[32][34];
   const int t = blockIdx.z;
   const int o0 = blockIdx.y * 32, i0 = blockIdx.x * 32;
@@ -178,6 +188,8 @@ __global__ void __launch_bounds__(256) transpose_taps_kernel(const __nv_bfloat16
 __global__ void __launch_bounds__(256) transpose_taps_v8_kernel(const __nv_bfloat16* __restrict__ W,
                                                                 __nv_bfloat16* __restrict__ WT, int co, int taps,
                                                                 int ci) {
+  tofu::pdl_trigger();
+  tofu::pdl_wait();
   constexpr int P = 66;
   __shared__ __align__(16) __nv_bfloat16 tile[64 * P];
   const int t = blockIdx.z;
@@ -230,28 +242,28 @@ extern "C" int tofu_maxpool(const tofu_window_args* a, void* stream) {
   if (!ok(a)) return TOFU_ERR_ALIGN;
   const int64_t n = (int64_t)a->nb * a->Ho * a->Wo * (a->C / 8);
   if (n == 0) return TOFU_OK;
-  maxpool_kernel<<<grid_for(n), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(*a);
+  tofu::launch_k(maxpool_kernel, dim3(grid_for(n)), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 1, *a);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }
 extern "C" int tofu_maxpool_grad(const tofu_window_args* a, void* stream) {
   if (!ok(a)) return TOFU_ERR_ALIGN;
   const int64_t n = (int64_t)a->nb * a->H * a->W * (a->C / 8);
   if (n == 0) return TOFU_OK;
-  maxpool_grad_kernel<<<grid_for(n), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(*a);
+  tofu::launch_k(maxpool_grad_kernel, dim3(grid_for(n)), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 1, *a);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }
 extern "C" int tofu_gap(const tofu_window_args* a, void* stream) {
   if (!ok(a)) return TOFU_ERR_ALIGN;
   const int64_t n = (int64_t)a->nb * (a->C / 8) * 32;
   if (n == 0) return TOFU_OK;
-  gap_kernel<<<grid_for(n), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(*a);
+  tofu::launch_k(gap_kernel, dim3(grid_for(n)), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 1, *a);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }
 extern "C" int tofu_gap_grad(const tofu_window_args* a, void* stream) {
   if (!ok(a)) return TOFU_ERR_ALIGN;
   const int64_t n = (int64_t)a->nb * a->H * a->W * (a->C / 8);
   if (n == 0) return TOFU_OK;
-  gap_grad_kernel<<<grid_for(n), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(*a);
+  tofu::launch_k(gap_grad_kernel, dim3(grid_for(n)), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 1, *a);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }
 
@@ -262,12 +274,12 @@ extern "C" int tofu_transpose_taps(const void* W, void* WT, int co, int taps, in
                   !(reinterpret_cast<uintptr_t>(WT) & 15);
   if (v8) {
     dim3 grid((ci + 63) / 64, (co + 63) / 64, taps);
-    tofu::win::transpose_taps_v8_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-        reinterpret_cast<const __nv_bfloat16*>(W), reinterpret_cast<__nv_bfloat16*>(WT), co, taps, ci);
+    tofu::launch_k(tofu::win::transpose_taps_v8_kernel, grid, dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 1,
+                   reinterpret_cast<const __nv_bfloat16*>(W), reinterpret_cast<__nv_bfloat16*>(WT), co, taps, ci);
   } else {
     dim3 grid((ci + 31) / 32, (co + 31) / 32, taps);
-    tofu::win::transpose_taps_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-        reinterpret_cast<const __nv_bfloat16*>(W), reinterpret_cast<__nv_bfloat16*>(WT), co, taps, ci);
+    tofu::launch_k(tofu::win::transpose_taps_kernel, grid, dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 1,
+                   reinterpret_cast<const __nv_bfloat16*>(W), reinterpret_cast<__nv_bfloat16*>(WT), co, taps, ci);
   }
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }
