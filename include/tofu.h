@@ -136,6 +136,22 @@ int tofu_execute_range(tofu_exec* e, int first, int last, void* stream);
  * subsequent tofu_execute; index < 0 disables. */
 int tofu_exec_time_launch(tofu_exec* e, int index, void* ev_start, void* ev_stop);
 
+/* ======================================================================================= a8 (multi-process)
+ * CUDA IPC for one process per GPU.  tofu_ipc_export: the 64-byte cudaIpcMemHandle of the
+ * allocation holding dev_ptr (caller-allocated device memory, e.g. a torch tensor) and dev_ptr's byte offset
+ * in it.  tofu_ipc_open: map a peer's exported allocation into THIS process on local_device (made current),
+ * enabling peer access from local_device to peer_device first (peer_device < 0 or == local_device: same GPU,
+ * nothing to enable); *ptr_out = mapped base + offset, an address this process's kernels on local_device
+ * dereference over NVLink.  tofu_ipc_close(ptr, offset) unmaps it.  Errors: TOFU_ERR_ARG, TOFU_ERR_CUDA (no
+ * peer access between the GPUs, an invalid handle). */
+int tofu_ipc_export(const void* dev_ptr, void* handle_out, int64_t* offset_out);
+int tofu_ipc_open(const void* handle, int64_t offset, int local_device, int peer_device, void** ptr_out);
+int tofu_ipc_close(void* mapped_ptr, int64_t offset);
+/* Test aid: a one-thread kernel that spins ns nanoseconds on the stream.  With TOFU_JITTER=<seed> in the
+ * environment at tofu_exec_create, the executor inserts such spins (0-200 us, pseudo-random per rank, launch
+ * and step) before a quarter of its launches, so cross-process synchronisation is exercised under skew. */
+int tofu_spin(int64_t ns, void* stream);
+
 /* ======================================================================================= kernels
  * Device entry points used by tofu_execute, exported for parity tests.
  */

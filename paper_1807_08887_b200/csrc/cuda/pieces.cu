@@ -403,3 +403,26 @@ extern "C" int tofu_barrier_run(void* flags_ptrs_dev, int rank, int n, void* str
                  reinterpret_cast<unsigned long long* const*>(flags_ptrs_dev), rank, n);
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }
+
+// Jitter injection (tests of the cross-process synchronisation): one thread spins for ns
+// nanoseconds of %globaltimer, delaying everything after it on the stream.
+namespace tofu {
+__global__ void spin_kernel(uint64_t ns) {
+  pdl_trigger();
+  pdl_wait();
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+}  // namespace tofu
+
+extern "C" int tofu_spin(int64_t ns, void* stream) {
+  if (ns <= 0) return TOFU_OK;
+  return tofu::launch_k(tofu::spin_kernel, dim3(1), dim3(1), 0, reinterpret_cast<cudaStream_t>(stream), 1,
+                        (uint64_t)ns) == cudaSuccess
+             ? TOFU_OK
+             : TOFU_ERR_CUDA;
+}

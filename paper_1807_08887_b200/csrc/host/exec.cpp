@@ -23,6 +23,7 @@
 #include "plan.h"
 
 extern "C" int tofu_barrier_run(void* flags_ptrs_dev, int rank, int n, void* stream);
+extern "C" int tofu_spin(int64_t ns, void* stream);
 extern "C" int tofu_lstm_cell(int kind, int64_t nb, int64_t nh, int g0, int ng, const void* const* ptrs,
                               const int64_t* lds, const int64_t* gss, const int* dts, void* out, int64_t out_ld,
                               int64_t out_gs, int out_dt, void* out2, int64_t out2_ld, int out2_dt, void* stream);
@@ -187,6 +188,8 @@ struct Exec {
   std::vector<int64_t> rank_in, rank_out;  // per rank: bytes it reads from peers / peers read from it
   int64_t n_kernels = 0;
   bool skip_comm = false;
+  uint64_t jitter = 0;    // TOFU_JITTER: seed + 1 of the injected delays (0 = off)
+  uint64_t jitter_step = 0;
   bool multi_process = false;
   bool fuse = true;
   bool fuse_fetch = true;  // GEMM operands read in place from their owners' shards (TOFU_PFETCH=0: staged)
@@ -372,6 +375,7 @@ bool conv_operand_ok(const ConvGeom& cg, int pi, const std::vector<Rng>& buf, co
 
 // lowering options from the environment (TOFU_FUSE=0: no fusion; TOFU_PFETCH=0: staged MultiFetch only)
 void read_env_options(Exec& E) {
+  if (const char* j = std::getenv("TOFU_JITTER")) E.jitter = std::strtoull(j, nullptr, 10) + 1;
   if (const char* f = std::getenv("TOFU_FUSE")) E.fuse = std::string(f) != "0";
   if (const char* f = std::getenv("TOFU_PFETCH")) E.fuse_fetch = std::string(f) != "0";
 }
@@ -1839,6 +1843,14 @@ void run_range(Exec& E, int first, int last, cudaStream_t st) {
       if (cudaEventRecordWithFlags(E.ev_start, st, evflags) != cudaSuccess)
         throw Error(TOFU_ERR_CUDA, std::string("timing event: ") + cudaGetErrorString(cudaGetLastError()));
     }
+    if (E.jitter && E.launches[i].kind != 3) {  // injected skew (tests): splitmix64 of (seed, rank, step, i)
+      uint64_t z = E.jitter * 0x9E3779B97F4A7C15ull + (uint64_t)E.local[0] * 0xBF58476D1CE4E5B9ull +
+                   E.jitter_step * 0x94D049BB133111EBull + (uint64_t)i;
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      z ^= z >> 31;
+      if ((z & 3) == 0) tofu_spin((int64_t)((z >> 8) % 200000), st);
+    }
     run_launch(E, E.launches[i], st);
     if (timed && cudaEventRecordWithFlags(E.ev_stop, st, evflags) != cudaSuccess)
       throw Error(TOFU_ERR_CUDA, std::string("timing event: ") + cudaGetErrorString(cudaGetLastError()));
@@ -1884,6 +1896,9 @@ std::string launch_desc(const Exec& E, int i) {
       flops = 2 * M * N * K;
       bytes = 2 * (M * K + K * N) + M * N * (lo.fused_opt >= 0 ? (8 + 4) : (lo.out.dtype == TOFU_BF16 ? 2 : 4));
       o += ",\"mnk\":[" + json_num(M) + "," + json_num(N) + "," + json_num(K) + "]";
+      auto git = E.gemms.find({L.op, L.li});
+      if (git != E.gemms.end())
+        o += ",\"splits\":" + std::to_string(git->second.a.splits) + ",\"bn\":" + std::to_string(git->second.bn);
       (void)dn;
     } else if (std::string(kernel_kind(dd)) == "conv") {
       // implicit GEMM: 2·M·N·K over the launches (the stride-2 data gradient's phases skip absent taps);
@@ -1897,6 +1912,11 @@ std::string launch_desc(const Exec& E, int i) {
                             : "[" + json_num(a.m_out) + "," + json_num(kn) + "," + json_num(pix) + "]";
       }
       if (!shp.empty()) o += ",\"mnk\":" + shp;
+      auto cit = E.convs.find({L.op, L.li});
+      if (cit != E.convs.end() && !cit->second.empty()) o += ",\"splits\":" + std::to_string(cit->second[0].a.splits);
+      auto git = E.gemms.find({L.op, L.li});
+      if (git != E.gemms.end())
+        o += ",\"splits\":" + std::to_string(git->second.a.splits) + ",\"bn\":" + std::to_string(git->second.bn);
       for (auto& b : lo.in) bytes += (double)vol(b.box) * (b.dtype == TOFU_BF16 ? 2 : 4);
       bytes += (double)vol(lo.out.box) * (lo.fused_opt >= 0 ? 12 : (lo.out.dtype == TOFU_BF16 ? 2 : 4));
     } else {
@@ -1945,6 +1965,7 @@ extern "C" int tofu_execute(tofu_exec* h, void* stream) {
   return tofu::guard([&]() {
     if (!h) throw tofu::Error(TOFU_ERR_ARG, "null exec");
     tofu::run_range(h->e, 0, (int)h->e.launches.size(), reinterpret_cast<cudaStream_t>(stream));
+    ++h->e.jitter_step;
     return TOFU_OK;
   });
 }

@@ -44,29 +44,43 @@ class TofuRunner:
             self.exec = tofu.Exec(self.graph, self.plan, self.local, ptrs)
         else:
             # one process per GPU: every rank allocates its own arena (+ 4 KiB of barrier words) and
-            # exports it with CUDA IPC; peers map it (cudaIpcOpenMemHandle, lazy peer access over
-            # NVLink) so libtofu's MultiFetch / reduce kernels load peer HBM directly.
+            # exports it with CUDA IPC (tofu_ipc_export); each peer maps it on ITS OWN device with peer access
+            # enabled explicitly (tofu_ipc_open), so libtofu's MultiFetch / reduce kernels load peer HBM
+            # directly over NVLink.
             import torch.distributed as dist
             nbytes = (max(self.plan.arena_bytes(r) for r in range(k)) + 4095) // 4096 * 4096
             buf = torch.zeros(nbytes + 4096, dtype=torch.uint8, device=self.device)
             self.arenas[rank] = buf
             torch.cuda.synchronize()
-            handle = buf.untyped_storage()._share_cuda_()
+            dev = self.device.index if self.device.index is not None else torch.cuda.current_device()
+            handle, off = tofu.ipc_export(buf.data_ptr())
             handles = [None] * k
-            dist.all_gather_object(handles, (rank, handle), group=group)
+            dist.all_gather_object(handles, (rank, dev, handle, off), group=group)
             self._peer = {}
             ptrs = [0] * k
-            for r, h in handles:
+            for r, pdev, h, o in handles:
                 if r == rank:
                     ptrs[r] = buf.data_ptr()
                 else:
-                    st = torch.UntypedStorage._new_shared_cuda(*h)
-                    self._peer[r] = st
-                    ptrs[r] = st.data_ptr()
+                    ptrs[r] = tofu.ipc_open(h, o, dev, pdev)
+                    self._peer[r] = (ptrs[r], o)
             flags = [p + nbytes for p in ptrs]
             dist.barrier(group=group)
             self.exec = tofu.Exec(self.graph, self.plan, self.local, ptrs, flags)
         self.shards = {r: {t: self.plan.shard(r, t) for t in spec["tensors"]} for r in range(k)}
+
+    def __del__(self):
+        peers = getattr(self, "_peer", None)
+        if not peers:
+            return
+        try:
+            torch.cuda.synchronize()
+            self.exec = None
+            for ptr, off in peers.values():
+                tofu.ipc_close(ptr, off)
+        except Exception:
+            pass
+        self._peer = {}
 
     @staticmethod
     def _aligned(t):

@@ -111,6 +111,9 @@ def lib():
             "tofu_exec_launch_desc": [vp, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
             "tofu_exec_unmaterialized": [vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
             "tofu_exec_rank_bytes": [vp, C.c_int, i64p, i64p],
+            "tofu_ipc_export": [vp, vp, i64p],
+            "tofu_ipc_open": [vp, C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_void_p)],
+            "tofu_ipc_close": [vp, C.c_int64],
             "tofu_execute_range": [vp, C.c_int, C.c_int, vp],
             "tofu_exec_time_launch": [vp, C.c_int, vp, vp],
             "tofu_transpose_taps": [vp, vp, C.c_int, C.c_int, C.c_int, vp],
@@ -223,6 +226,26 @@ def pieces_run(pieces_dev_ptr, tasks_dev_ptr, ntasks, all_raw=0, stream=None):
     """tofu_pieces_run over device copies of the pieces and tasks (all_raw: every task's pad_ == 1)."""
     check(lib().tofu_pieces_run(C.c_void_p(pieces_dev_ptr), C.c_void_p(tasks_dev_ptr), ntasks, all_raw,
                                 _stream(stream)), "tofu_pieces_run")
+
+
+def ipc_export(ptr: int):
+    """tofu_ipc_export: (64-byte handle, offset of ptr in its allocation)."""
+    h = (C.c_char * 64)()
+    off = C.c_int64()
+    check(lib().tofu_ipc_export(C.c_void_p(ptr), h, C.byref(off)), "tofu_ipc_export")
+    return bytes(h), off.value
+
+
+def ipc_open(handle: bytes, offset: int, local_device: int, peer_device: int) -> int:
+    """tofu_ipc_open: map a peer's exported allocation on local_device; returns the mapped address."""
+    h = (C.c_char * 64).from_buffer_copy(handle)
+    p = C.c_void_p()
+    check(lib().tofu_ipc_open(h, offset, local_device, peer_device, C.byref(p)), "tofu_ipc_open")
+    return p.value
+
+
+def ipc_close(ptr: int, offset: int):
+    check(lib().tofu_ipc_close(C.c_void_p(ptr), offset), "tofu_ipc_close")
 
 
 # ----------------------------------------------------------------------------- host API

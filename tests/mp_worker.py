@@ -7,6 +7,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def worker_spec(which):
+    from tofu_inputs.graphs import config, wresnet
+    if which == "wres":   # a small WResNet: halo / strided-gradient fetches, partition-n-reduce + fused consumers
+        return wresnet([1, 1], 1, 8, 32, base=16, classes=16)
+    return config(0)
+
+
 def main():
     import numpy as np
     import torch
@@ -16,10 +23,11 @@ def main():
     from tofu_inputs.tensors import make_values
 
     rank, world, out = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
+    which = sys.argv[5] if len(sys.argv) > 5 else "mlp"
     ngpu = torch.cuda.device_count()
     torch.cuda.set_device(rank % ngpu)
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{sys.argv[4]}", rank=rank, world_size=world)
-    spec = config(0)
+    spec = worker_spec(which)
     vals = make_values(spec, seed=31)
     dbg = os.environ.get("TOFU_MP_DEBUG")
     if dbg: print(f"[{rank}] init ok", file=sys.stderr, flush=True)

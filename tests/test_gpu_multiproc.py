@@ -17,29 +17,39 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def test_two_process_step_equals_virtual(tmp_path):
+@pytest.mark.parametrize("world,which,jitter", [(2, "mlp", None), (2, "mlp", "7"), (4, "wres", None),
+                                                (4, "wres", "11")])
+def test_processes_step_equals_virtual(tmp_path, world, which, jitter):
+    """world processes (one rank each, IPC-mapped peer arenas, device barriers) run two steps and match the
+    virtual-rank executor bitwise.  With TOFU_JITTER every process injects pseudo-random 0-200 us delays
+    before a quarter of its launches (different per rank), so a missing or misplaced barrier shows up as a
+    read of stale / not-yet-produced peer data."""
     out = str(tmp_path / "res")
-    port = str(29600 + os.getpid() % 1000)
-    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp_worker.py"), str(r), "2", out, port])
-             for r in range(2)]
+    port = str(29600 + (os.getpid() + world * 7 + (1 if jitter else 0)) % 1000)
+    env = dict(os.environ)
+    if jitter:
+        env["TOFU_JITTER"] = jitter
+    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp_worker.py"), str(r), str(world), out, port,
+                               which], env=env)
+             for r in range(world)]
     try:
-        rcs = [p.wait(timeout=240) for p in procs]
+        rcs = [p.wait(timeout=300) for p in procs]
     finally:
         for p in procs:
             if p.poll() is None:
                 p.kill()
-    assert rcs == [0, 0]
-    res = [pickle.load(open(f"{out}.{r}", "rb")) for r in range(2)]
+    assert rcs == [0] * world
+    res = [pickle.load(open(f"{out}.{r}", "rb")) for r in range(world)]
+    from mp_worker import worker_spec
     from paper_1807_08887_b200.runner import TofuRunner
-    from tofu_inputs.graphs import config
     from tofu_inputs.tensors import make_values
-    spec = config(0)
-    R = TofuRunner(spec, 2)
+    spec = worker_spec(which)
+    R = TofuRunner(spec, world)
     R.load(make_values(spec, seed=31))
     for _ in range(2):
         R.step()
     torch.cuda.synchronize()
-    for r in range(2):
+    for r in range(world):
         assert res[r]["ledger"] == res[r]["plan"]
         for t, (box, arr) in res[r]["shards"].items():
             ref = R.view(r, t).float().cpu().numpy()
