@@ -106,7 +106,14 @@ int tofu_exec_create(const tofu_graph* g, const tofu_plan* p, int n_local, const
                      void* const* arena_dev, void* const* flags_dev, tofu_exec** out);
 void tofu_exec_destroy(tofu_exec* e);
 /* One training step of the partitioned graph: for each op in order and each local rank: MultiFetch of
- * remote input regions (a5), sub-op (a4/a7), spread reduction / scatter of outputs to owners (a6). */
+ * remote input regions (a5), sub-op (a4/a7), spread reduction / scatter of outputs to owners (a6).
+ * Streams: compute launches go to `stream`; in multi-process mode (and with TOFU_STREAMS=2 on virtual ranks)
+ * fetch / reduce / barrier launches go to an executor-owned comm stream, forked from `stream` at the start
+ * and joined back at the end, each launch waiting (CUDA events) only for the launches it depends on (last
+ * writer / readers of the tensors and of the two alternating staging buffers it touches).  Device barriers
+ * (multi-process) are placed only before a launch that would otherwise race with a peer: reading peer memory
+ * some rank wrote since the last barrier, or writing memory some rank read remotely since then; decided from
+ * all ranks' lowering, so every process issues the same sequence.  `stream` may be capturing a CUDA graph. */
 int tofu_execute(tofu_exec* e, void* stream);
 /* Bytes moved between distinct ranks by the last tofu_execute, counted from the lowered pieces:
  * fetched (tensor dtype) and reduced/scattered (fp32 for partials).  elements likewise. */

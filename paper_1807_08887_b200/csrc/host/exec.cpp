@@ -109,6 +109,8 @@ struct LOp {
   bool fused_loss_grad = false;  // sumsq: this launch also computes the next op, mse_grad of the same inputs
   int ep = 0;                 // element-wise epilogue of the output's consumers: 1 relu, 2 add, 4 mask
   int red_ep = 0;             // the reduce pieces apply the output's consumer (TOFU_PIECE_*)
+  std::vector<int> absorbed;      // ops whose work this op's compute launch does (fused; their launches skip)
+  std::vector<int> red_absorbed;  // ops whose work this op's reduce launch does
   Buf epi_add, epi_mask;      // its bf16 operands (the output's layout)
   std::vector<tofu_piece> fetch, reduce;
   std::vector<int> fetch_src, reduce_nremote;  // for the ledger
@@ -161,6 +163,9 @@ struct Exec {
     int kind;  // 0 fetch pieces, 1 compute, 2 reduce pieces, 3 barrier, 4 memset
     int op, li;
     int64_t piece_off, npieces, max_elems;
+    int stream = 0;           // 0: the caller's (compute) stream, 1: the executor's comm stream
+    std::vector<int> waits;   // launches on the other stream this one waits for (their events)
+    bool rec = false;         // record this launch's event (a launch on the other stream waits for it)
     int64_t task_off = 0, ntasks = 0;  // fetch / reduce: tofu_piece_task range (tofu_pieces_tasks)
     int all_raw = 0;                   // every task a plain copy (the copy kernel)
   };
@@ -191,8 +196,20 @@ struct Exec {
   uint64_t jitter = 0;    // TOFU_JITTER: seed + 1 of the injected delays (0 = off)
   uint64_t jitter_step = 0;
   bool multi_process = false;
+  int streams = 1;         // virtual ranks: 1 (default) or 2 (TOFU_STREAMS=2); multi-process always 2
   bool fuse = true;
   bool fuse_fetch = true;  // GEMM operands read in place from their owners' shards (TOFU_PFETCH=0: staged)
+  struct OpAcc {  // objects (tensor alias roots; staging buffers nt, nt + 1) an op's launches touch, all ranks
+    bool any_fetch = false, any_reduce = false, fetch_remote = false;
+    int stage = -1;
+    std::vector<int> f_rreads;                    // fetch: reads (in peers' memory when remote) -> writes stage
+    std::vector<int> c_reads, c_writes, c_rreads;  // compute (+ absorbed ops); c_rreads: read in place remotely
+    std::vector<int> r_reads, r_writes, r_rreads;  // reduce (+ absorbed ops); r_rreads: peers' staging
+  };
+  std::vector<OpAcc> acc;
+  cudaStream_t comm = nullptr;        // the second stream (fetch / reduce / barrier launches)
+  std::vector<cudaEvent_t> events;    // per launch (recorded when a launch on the other stream waits for it)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<char> remote_fetch, remote_reduce;  // per op, over all ranks
   std::vector<char> remote_direct;                 // per op: a compute launch reads peer memory (fused fetch)
   int timed_launch = -1;
@@ -377,6 +394,7 @@ bool conv_operand_ok(const ConvGeom& cg, int pi, const std::vector<Rng>& buf, co
 void read_env_options(Exec& E) {
   if (const char* j = std::getenv("TOFU_JITTER")) E.jitter = std::strtoull(j, nullptr, 10) + 1;
   if (const char* f = std::getenv("TOFU_FUSE")) E.fuse = std::string(f) != "0";
+  if (const char* f = std::getenv("TOFU_STREAMS")) E.streams = std::atoi(f) >= 2 ? 2 : 1;
   if (const char* f = std::getenv("TOFU_PFETCH")) E.fuse_fetch = std::string(f) != "0";
 }
 
@@ -531,13 +549,18 @@ void lower(Exec& E) {
       stage_need[r] = std::max(stage_need[r], soff);
     }
   }
+  // two staging buffers, alternating op by op (parity of the op index): an op's fetch / partial outputs do not
+  // overwrite the previous op's, so the next op's fetch can run (on the comm stream) while this op's compute
+  // and reduce still read theirs (build_launches)
   for (int r = 0; r < k; ++r) {
-    E.lay[r].staging_bytes = stage_need[r];
-    E.lay[r].total = E.lay[r].staging_off + stage_need[r];
-    for (auto& L : all[r]) {
+    E.lay[r].staging_bytes = 2 * stage_need[r];
+    E.lay[r].total = E.lay[r].staging_off + 2 * stage_need[r];
+    for (size_t o = 0; o < all[r].size(); ++o) {
+      LOp& L = all[r][o];
+      const int64_t base = E.lay[r].staging_off + (int64_t)(o % 2) * stage_need[r];
       for (auto& b : L.in)
-        if (!b.direct && b.rp.empty()) b.off += E.lay[r].staging_off;
-      if (!L.out.direct) L.out.off += E.lay[r].staging_off;
+        if (!b.direct && b.rp.empty()) b.off += base;
+      if (!L.out.direct) L.out.off += base;
     }
   }
   // ------------------------------------------------------------------ pieces
@@ -686,6 +709,7 @@ void lower(Exec& E) {
       ok &= La.in[0].off == La.out.off && Lb.in[0].off == Lb.out.off;  // in place (aliased state)
       if (ok) {
         La.fused_sgd = true;
+        La.absorbed.push_back((int)o + 1);
         Lb.skip = true;
       }
     }
@@ -724,6 +748,8 @@ void lower(Exec& E) {
         if (clash || !La.out.direct || La.partial || La.out.dtype != TOFU_F32) continue;
         La.fused_opt = reader;
         E.unmat.insert(a.output);   // the weight gradient stays in TMEM / registers
+        La.absorbed.push_back(reader);
+        La.absorbed.push_back(reader + 1);
         all[r][reader].skip = true;
       }
   // LSTM: the two cell ops of one timestep read the same gate rows -> one kernel (one pass over GX / GH)
@@ -750,6 +776,7 @@ void lower(Exec& E) {
           for (int q = 0; q < 4; ++q) ok &= same_buf(La.in[3 + q], Lb.in[2 + q]);  // C, DU, DR, DN
         if (!ok) continue;
         La.fused_next = true;
+        La.absorbed.push_back((int)o + 1);
         Lb.skip = true;
       }
   // The loss and its gradient read the same (Y, T) shards: one pass computes both (sumsq + mse_grad, R8)
@@ -767,6 +794,7 @@ void lower(Exec& E) {
         if (!same_buf(La.in[0], Lb.in[0]) || !same_buf(La.in[1], Lb.in[1]) || !same(Lb.out.box, Lb.in[0].box))
           continue;
         La.fused_loss_grad = true;
+        La.absorbed.push_back((int)o + 1);
         Lb.skip = true;
       }
   // Element-wise consumers folded into their producer's epilogue (R8/R13): a GEMM / convolution whose bf16
@@ -855,8 +883,10 @@ void lower(Exec& E) {
         if (e2 >= 0) {
           Lo.epi_mask = mask;
           all[r][e2].skip = true;
+          Lo.absorbed.push_back(e2);
           E.unmat.insert(g.ops[e].output);   // the gradient sum before its mask
         }
+        Lo.absorbed.push_back(e);
         E.unmat.insert(t);                   // the producer's own (pre-epilogue) output
         Lo.out = out;
         Le.skip = true;
@@ -969,6 +999,8 @@ void lower(Exec& E) {
           }
         }
         Lo.red_ep = ep;
+        Lo.red_absorbed.push_back(e);
+        if (ep == TOFU_PIECE_MOM_SGD) Lo.red_absorbed.push_back(e + 1);
         Le.skip = true;
         (void)own;
       }
@@ -1009,6 +1041,68 @@ void lower(Exec& E) {
       E.remote_direct[o] |= all[r][o].remote_direct;
       for (int n : all[r][o].reduce_nremote) E.remote_reduce[o] |= n > 0;
     }
+  // Global memory-access summary of every op's launches (union over ALL ranks, so every process derives the
+  // same synchronisation): objects are tensor storages (alias roots) and the two staging buffers (kStage0 +
+  // op parity).  rreads = objects some rank reads in a PEER's memory.
+  {
+    std::map<int, int> al(g.alias.begin(), g.alias.end());
+    auto root = [&](int t) {
+      while (al.count(t)) t = al[t];
+      return t;
+    };
+    const int nt = (int)g.tensors.size();
+    E.acc.assign(g.ops.size(), {});
+    for (size_t o = 0; o < g.ops.size(); ++o) {
+      Exec::OpAcc& A = E.acc[o];
+      const int S = nt + (int)(o % 2);
+      std::set<int> fr, cr, cw, crr, rr, rw;
+      bool rrem = false;
+      for (int r = 0; r < k; ++r) {
+        const LOp& L = all[r][o];
+        A.any_fetch |= !L.fetch.empty();
+        A.any_reduce |= !L.reduce.empty();
+        for (size_t q = 0; q < L.fetch.size(); ++q)
+          if (L.fetch_src[q] != r) A.fetch_remote = true;
+        for (size_t pi = 0; pi < L.in.size(); ++pi) {
+          const Buf& b = L.in[pi];
+          const int t = root(g.ops[o].inputs[pi]);
+          if (b.direct) {
+            cr.insert(t);
+          } else if (!b.rp.empty()) {
+            cr.insert(t);
+            for (auto& q : b.rp)
+              if (q.src != r) crr.insert(t);
+          } else {
+            fr.insert(t);  // the fetch reads the owners' shards, writes staging
+            cr.insert(S);
+          }
+        }
+        cw.insert(L.out.direct ? root(g.ops[o].output) : S);
+        if (!L.out.direct) cw.insert(root(g.ops[o].output));  // (conservative: the scatter / reduce writes it)
+        for (int a : L.absorbed) {
+          for (int t : g.ops[a].inputs) cr.insert(root(t));
+          cw.insert(root(g.ops[a].output));
+        }
+        if (!L.reduce.empty()) {
+          rr.insert(S);
+          rw.insert(root(g.ops[o].output));
+          for (int n : L.reduce_nremote) rrem |= n > 0;
+          for (int a : L.red_absorbed) {
+            for (int t : g.ops[a].inputs) rr.insert(root(t));
+            rw.insert(root(g.ops[a].output));
+          }
+        }
+      }
+      A.f_rreads.assign(fr.begin(), fr.end());
+      A.c_reads.assign(cr.begin(), cr.end());
+      A.c_writes.assign(cw.begin(), cw.end());
+      A.c_rreads.assign(crr.begin(), crr.end());
+      A.r_reads.assign(rr.begin(), rr.end());
+      A.r_writes.assign(rw.begin(), rw.end());
+      if (rrem) A.r_rreads.push_back(S);
+      A.stage = S;
+    }
+  }
   E.lops.clear();
   for (int r : E.local) E.lops.push_back(all[r]);
 }
@@ -1018,53 +1112,141 @@ void build_launches(Exec& E) {
   std::vector<tofu_piece> host;
   E.launches.clear();
   const int nl = (int)E.local.size();
-  // Multi-process synchronisation.  Barrier placement is decided from ALL ranks' lowered pieces (every
-  // process must issue the same barrier sequence).  A phase that reads peer memory (fetch or reduce with a
-  // source on another rank, anywhere) is bracketed by device barriers: the one before makes the peers'
-  // producers visible (RAW); the one after guarantees no rank overwrites a shard or staging buffer a peer
-  // is still reading (WAR; staging is reused op to op).  A final barrier closes the step.
+  const int nobj = (int)g.tensors.size() + 2;
+  // Two streams: compute launches (and the loss memset) on the caller's stream, fetch / reduce / barrier
+  // launches on the executor's comm stream, ordered by the data dependencies between them (the objects of
+  // E.acc: last writer / readers since): a fetch runs as soon as its inputs exist and its staging buffer is
+  // free, overlapping the previous op's compute (communication overlapped with computation).
+  //
+  // Multi-process synchronisation.  A device barrier (all ranks, comm stream) is inserted only where a hazard
+  // between ranks exists, tracked over the same objects from the ALL-rank summaries (every process derives the
+  // same barrier sequence): before a launch that reads an object in a peer's memory which some rank wrote since
+  // the last barrier (RAW), and before a launch that writes an object some rank read remotely since the last
+  // barrier (WAR).  A barrier waits for the local writers / readers of those objects and later launches that
+  // touch them wait for it.  A final barrier closes the step.
+  // pass 1 (all ranks alike): where the barriers go, and the objects each one orders
+  std::map<std::pair<int, int>, std::vector<int>> bar_before;  // (op, phase 0 fetch / 1 compute / 2 reduce)
+  if (E.multi_process) {
+    std::set<int> w_since, rr_since;  // since the last barrier: objects written (any rank), read remotely
+    auto step = [&](int o, int ph, const std::vector<int>& writes, const std::vector<int>& rreads) {
+      bool hazard = false;
+      for (int x : rreads) hazard |= w_since.count(x) > 0;
+      for (int x : writes) hazard |= rr_since.count(x) > 0;
+      if (hazard) {
+        std::set<int> objs(w_since.begin(), w_since.end());
+        objs.insert(rr_since.begin(), rr_since.end());
+        bar_before[{o, ph}].assign(objs.begin(), objs.end());
+        w_since.clear();
+        rr_since.clear();
+      }
+      w_since.insert(writes.begin(), writes.end());
+      rr_since.insert(rreads.begin(), rreads.end());
+    };
+    for (size_t o = 0; o < g.ops.size(); ++o) {
+      const Exec::OpAcc& A = E.acc[o];
+      if (A.any_fetch) step((int)o, 0, {A.stage}, A.fetch_remote ? A.f_rreads : std::vector<int>());
+      step((int)o, 1, A.c_writes, A.c_rreads);
+      if (A.any_reduce) step((int)o, 2, A.r_writes, A.r_rreads);
+    }
+  }
+  // pass 2: this process's launches, each waiting for its data dependencies (last writer / readers since)
+  std::vector<int> last_writer(nobj, -1);
+  std::vector<std::vector<int>> readers(nobj);
+  auto deps_of = [&](const std::vector<int>& reads, const std::vector<int>& writes) {
+    std::set<int> deps;
+    for (int x : reads)
+      if (last_writer[x] >= 0) deps.insert(last_writer[x]);
+    for (int x : writes) {
+      if (last_writer[x] >= 0) deps.insert(last_writer[x]);
+      for (int y : readers[x]) deps.insert(y);
+    }
+    return std::vector<int>(deps.begin(), deps.end());
+  };
+  int last_compute = -1;
+  auto add = [&](Exec::Launch L, const std::vector<int>& reads, const std::vector<int>& writes) {
+    const int li = (int)E.launches.size();
+    L.waits = deps_of(reads, writes);
+    // virtual ranks (no barriers, one GPU): one stream unless TOFU_STREAMS=2 — measured, the second stream
+    // does not pay there (WResNet-152-4 k = 8: 100.3 ms one stream, 102.9-104.8 ms two: the copy kernels
+    // compete with the convolutions for the same SMs / HBM, and a cross-stream event wait breaks the
+    // programmatic-launch chain); with TOFU_STREAMS=2, a fetch / reduce that needs the compute launch just
+    // before it stays on the compute stream
+    if (!E.multi_process && L.stream == 1 &&
+        (E.streams < 2 || (!L.waits.empty() && L.waits.back() == last_compute && last_compute == li - 1)))
+      L.stream = 0;
+    if (L.kind == 1 || L.kind == 4) last_compute = li;
+    E.launches.push_back(L);
+    for (int x : reads) readers[x].push_back(li);
+    for (int x : writes) {
+      last_writer[x] = li;
+      readers[x].clear();
+    }
+  };
+  // a barrier: after the local writers / readers of every object it orders, before any later launch
+  // touching them (it reads and writes them all)
+  auto barrier = [&](int o, const std::vector<int>& objs) {
+    Exec::Launch B{3, o, -1, 0, 0, 0};
+    B.stream = 1;
+    add(B, objs, objs);
+  };
+  auto maybe_barrier = [&](int o, int ph) {
+    auto it = bar_before.find({(int)o, ph});
+    if (it != bar_before.end()) barrier(o, it->second);
+  };
   for (size_t o = 0; o < g.ops.size(); ++o) {
+    const Exec::OpAcc& A = E.acc[o];
     bool any_fetch = false;
     for (int li = 0; li < nl; ++li) any_fetch |= !E.lops[li][o].fetch.empty();
-    const bool bar_f = E.multi_process && E.remote_fetch[o];
-    // fused fetch: the compute launches read peer shards in place, so the WAR barrier follows them
-    const bool bar_c = E.multi_process && E.remote_direct[o];
-    if (bar_f) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
+    maybe_barrier((int)o, 0);
     if (any_fetch) {
       Exec::Launch L{0, (int)o, -1, (int64_t)host.size(), 0, 0};
+      L.stream = 1;
       for (int li = 0; li < nl; ++li)
         for (auto& pc : E.lops[li][o].fetch) {
           host.push_back(pc);
           L.max_elems = std::max(L.max_elems, pc.extent[0] * pc.extent[1] * pc.extent[2] * pc.extent[3]);
         }
       L.npieces = (int64_t)host.size() - L.piece_off;
-      E.launches.push_back(L);
+      add(L, A.f_rreads, {A.stage});
     }
-    // (decided from all ranks, like bar_f: a rank without fetch pieces of its own still issues it)
-    if (bar_f) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
+    maybe_barrier((int)o, 1);
     for (int li = 0; li < nl; ++li) {
       if (E.lops[li][o].skip) continue;
-      if (g.defs[g.ops[o].def].kernel == "sumsq") E.launches.push_back({4, (int)o, li, 0, 0, 0});
-      E.launches.push_back({1, (int)o, li, 0, 0, 0});
+      if (g.defs[g.ops[o].def].kernel == "sumsq") add({4, (int)o, li, 0, 0, 0}, {}, A.c_writes);
+      add({1, (int)o, li, 0, 0, 0}, A.c_reads, A.c_writes);
     }
-    if (bar_c) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
     bool any_red = false;
     for (int li = 0; li < nl; ++li) any_red |= !E.lops[li][o].reduce.empty();
-    const bool bar_r = E.multi_process && E.remote_reduce[o];
-    if (bar_r) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
+    maybe_barrier((int)o, 2);
     if (any_red) {
       Exec::Launch L{2, (int)o, -1, (int64_t)host.size(), 0, 0};
+      L.stream = 1;
       for (int li = 0; li < nl; ++li)
         for (auto& pc : E.lops[li][o].reduce) {
           host.push_back(pc);
           L.max_elems = std::max(L.max_elems, pc.extent[0] * pc.extent[1] * pc.extent[2] * pc.extent[3]);
         }
       L.npieces = (int64_t)host.size() - L.piece_off;
-      E.launches.push_back(L);
+      add(L, A.r_reads, A.r_writes);
     }
-    if (bar_r) E.launches.push_back({3, (int)o, -1, 0, 0, 0});
   }
-  if (E.multi_process) E.launches.push_back({3, -1, -1, 0, 0, 0});
+  if (E.multi_process) {  // closes the step: orders every object
+    std::vector<int> all_objs(nobj);
+    for (int x = 0; x < nobj; ++x) all_objs[x] = x;
+    barrier(-1, all_objs);
+  }
+  // keep only cross-stream waits (same-stream order is implicit), the latest one per stream suffices
+  for (size_t i = 0; i < E.launches.size(); ++i) {
+    auto& L = E.launches[i];
+    int latest = -1;
+    for (int j : L.waits)
+      if (E.launches[j].stream != L.stream) latest = std::max(latest, j);
+    L.waits.clear();
+    if (latest >= 0) {
+      L.waits.push_back(latest);
+      E.launches[latest].rec = true;
+    }
+  }
   // piece tasks of every fetch / reduce launch (pieces normalised in place; task piece indices are
   // relative to the launch's first piece)
   E.host_tasks.clear();
@@ -1796,6 +1978,11 @@ extern "C" void tofu_exec_destroy(tofu_exec* h) {
   if (!h) return;
   if (h->e.pieces_dev) cudaFree(h->e.pieces_dev);
   if (h->e.tasks_dev) cudaFree(h->e.tasks_dev);
+  for (auto ev : h->e.events)
+    if (ev) cudaEventDestroy(ev);
+  if (h->e.ev_fork) cudaEventDestroy(h->e.ev_fork);
+  if (h->e.ev_join) cudaEventDestroy(h->e.ev_join);
+  if (h->e.comm) cudaStreamDestroy(h->e.comm);
   if (h->e.flags_dev) cudaFree(h->e.flags_dev);
   if (h->e.ws_dev) cudaFree(h->e.ws_dev);
   if (h->e.sk_dev) cudaFree(h->e.sk_dev);
@@ -1829,31 +2016,60 @@ int run_launch(Exec& E, const Exec::Launch& L, cudaStream_t st) {
   return rc;
 }
 
+// Launches [first, last): compute launches on st, comm launches on the executor's comm stream, forked from st
+// at the start and joined back at the end (so st orders the whole range with the caller's work, and the
+// pattern captures into a CUDA graph as a fork / join with the cross-stream waits as graph edges).
 void run_range(Exec& E, int first, int last, cudaStream_t st) {
   finalize(E);
+  if (!E.comm) {
+    if (cudaStreamCreateWithFlags(&E.comm, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&E.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&E.ev_join, cudaEventDisableTiming) != cudaSuccess)
+      throw Error(TOFU_ERR_CUDA, "comm stream / events");
+    E.events.assign(E.launches.size(), nullptr);
+    for (size_t i = 0; i < E.launches.size(); ++i)
+      if (E.launches[i].rec && cudaEventCreateWithFlags(&E.events[i], cudaEventDisableTiming) != cudaSuccess)
+        throw Error(TOFU_ERR_CUDA, "launch events");
+  }
+  bool any_comm = false;
+  for (int i = first; i < last && !any_comm; ++i) any_comm = E.launches[i].stream == 1;
+  auto chk = [](cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Error(TOFU_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  };
+  if (any_comm) {
+    chk(cudaEventRecord(E.ev_fork, st), "fork event");
+    chk(cudaStreamWaitEvent(E.comm, E.ev_fork, 0), "fork wait");
+  }
   for (int i = first; i < last; ++i) {
+    const Exec::Launch& L = E.launches[i];
+    cudaStream_t s = L.stream == 1 ? E.comm : st;
+    for (int j : L.waits)
+      if (j >= first) chk(cudaStreamWaitEvent(s, E.events[j], 0), "dependency wait");
     const bool timed = i == E.timed_launch && E.ev_start;
     // external event nodes when captured into a CUDA graph, so every replay re-times the launch
     // (the External flag is only valid while capturing; eager launches record plainly)
     unsigned evflags = cudaEventRecordDefault;
     if (timed) {
       cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-      cudaStreamIsCapturing(st, &cs);
+      cudaStreamIsCapturing(s, &cs);
       if (cs == cudaStreamCaptureStatusActive) evflags = cudaEventRecordExternal;
-      if (cudaEventRecordWithFlags(E.ev_start, st, evflags) != cudaSuccess)
-        throw Error(TOFU_ERR_CUDA, std::string("timing event: ") + cudaGetErrorString(cudaGetLastError()));
+      chk(cudaEventRecordWithFlags(E.ev_start, s, evflags), "timing event");
     }
-    if (E.jitter && E.launches[i].kind != 3) {  // injected skew (tests): splitmix64 of (seed, rank, step, i)
+    if (E.jitter && L.kind != 3) {  // injected skew (tests): splitmix64 of (seed, rank, step, i)
       uint64_t z = E.jitter * 0x9E3779B97F4A7C15ull + (uint64_t)E.local[0] * 0xBF58476D1CE4E5B9ull +
                    E.jitter_step * 0x94D049BB133111EBull + (uint64_t)i;
       z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
       z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
       z ^= z >> 31;
-      if ((z & 3) == 0) tofu_spin((int64_t)((z >> 8) % 200000), st);
+      if ((z & 3) == 0) tofu_spin((int64_t)((z >> 8) % 200000), s);
     }
-    run_launch(E, E.launches[i], st);
-    if (timed && cudaEventRecordWithFlags(E.ev_stop, st, evflags) != cudaSuccess)
-      throw Error(TOFU_ERR_CUDA, std::string("timing event: ") + cudaGetErrorString(cudaGetLastError()));
+    run_launch(E, L, s);
+    if (timed) chk(cudaEventRecordWithFlags(E.ev_stop, s, evflags), "timing event");
+    if (L.rec) chk(cudaEventRecord(E.events[i], s), "launch event");
+  }
+  if (any_comm) {
+    chk(cudaEventRecord(E.ev_join, E.comm), "join event");
+    chk(cudaStreamWaitEvent(st, E.ev_join, 0), "join wait");
   }
 }
 
@@ -1865,6 +2081,8 @@ std::string launch_desc(const Exec& E, int i) {
   o += ",\"op\":" + (L.op >= 0 ? json_quote(g.ops[L.op].name) : std::string("null"));
   o += ",\"def\":" + (L.op >= 0 ? json_quote(g.defs[g.ops[L.op].def].name) : std::string("null"));
   o += ",\"rank\":" + std::to_string(L.li >= 0 ? E.local[L.li] : -1);
+  o += ",\"stream\":" + std::to_string(L.stream);
+  if (!L.waits.empty()) o += ",\"waits\":" + std::to_string(L.waits[0]);
   double flops = 0, bytes = 0;
   if (L.kind == 0 || L.kind == 2) {
     double rows = 0, row_bytes = 0, vec = 0, elems = 0;

@@ -242,3 +242,30 @@ def test_constants_come_from_the_tdl_text(fuse, monkeypatch):
         e = nrm(out[t], r) if np.ndim(r) else abs(out[t] - r) / abs(r)
         assert e <= 2e-2, (t, e)
     assert not np.array_equal(out["W1_new"], vals["W1"])   # (attrs lr = 0 would have left W unchanged)
+
+
+@pytest.mark.parametrize("which,k", [("wresnet", 4), ("lstm", 4), ("fc", 8)])
+def test_two_streams_equal_one_stream(which, k, monkeypatch):
+    """The executor's comm stream (fetch / reduce launches ordered against the compute stream by their data
+    dependencies) gives bitwise the results of the single-stream order (virtual ranks; TOFU_STREAMS=2
+    forces the two-stream schedule that multi-process mode always uses)."""
+    from paper_1807_08887_b200.runner import TofuRunner
+    from tofu_inputs.graphs import lstm, wresnet
+    spec = {"wresnet": lambda: wresnet([1, 1], 2, 8, 64, base=32, classes=64), "lstm": lambda: lstm(2, 256, 4, 32),
+            "fc": lambda: config(1)}[which]()
+    vals = make_values(spec, seed=23)
+    outs, streams = {}, {}
+    for n in ("1", "2"):
+        monkeypatch.setenv("TOFU_STREAMS", n)
+        R = TofuRunner(spec, k)
+        R.load(vals)
+        for _ in range(2):
+            R.step()
+        torch.cuda.synchronize()
+        descs = [R.exec.launch_desc(i) for i in range(R.exec.num_launches())]
+        streams[n] = sum(d.get("stream", 0) == 1 for d in descs)
+        outs[n] = {t: R.gather(t).float().cpu().numpy() for t in spec["tensors"] if t not in R.exec.unmaterialized()}
+        del R
+    assert streams["1"] == 0
+    for t in outs["1"]:
+        assert np.array_equal(outs["1"][t], outs["2"][t]), t
