@@ -344,11 +344,15 @@ struct WorkList {
   // cluster pairs (gemm_tcgen05.cu CL2): the two CTAs of a cluster take vertically adjacent tiles (m tiles 2p,
   // 2p+1) of the same n tile, so they share (multicast) the B tile; pair units round-robin over the clusters
   int pairs = 0, tiles_n = 1, rank = 0;
+  // raster 1: units walk m fastest (column-major over the tile grid), so one wave covers every m tile of a few
+  // n columns — A (M x K) stays resident in L2 while B streams once; used when B is the larger operand (N > M)
+  int raster = 0, tiles_m = 1;
   __device__ __forceinline__ void init_pairs(int tiles_m, int tiles_n_, int nk_, int rank_, int cid, int ncl) {
     nk = nk_;
     splits = 1;
     pairs = 1;
     tiles_n = tiles_n_;
+    this->tiles_m = tiles_m;
     rank = rank_;
     grid = ncl;
     cta = cid;
@@ -377,8 +381,17 @@ struct WorkList {
   // fp32 partial to the workspace instead of the epilogue's store)
   __device__ __forceinline__ void seg(int i, int& tile, int& kb0, int& kb1, int& split, bool& partial) const {
     if (pairs) {
-      const int u = cta + i * grid, mp = u / tiles_n;
-      tile = (2 * mp + rank) * tiles_n + (u - mp * tiles_n);
+      const int u = cta + i * grid;
+      int mp, nn;
+      if (raster) {
+        const int prow = (tiles_m + 1) / 2;
+        nn = u / prow;
+        mp = u - nn * prow;
+      } else {
+        mp = u / tiles_n;
+        nn = u - mp * tiles_n;
+      }
+      tile = (2 * mp + rank) * tiles_n + nn;
       split = kb0 = 0;
       kb1 = nk;
       partial = false;
@@ -387,8 +400,13 @@ struct WorkList {
     if (i < n_dp) {
       const int u = cta + i * grid;
       partial = false;
-      if (splits == 1) {  // the common case: no divisions
-        tile = u;
+      if (splits == 1) {  // the common case: no divisions (raster 1: one)
+        if (raster) {
+          const int nn = u / tiles_m;
+          tile = (u - nn * tiles_m) * tiles_n + nn;
+        } else {
+          tile = u;
+        }
         split = kb0 = 0;
         kb1 = nk;
         return;

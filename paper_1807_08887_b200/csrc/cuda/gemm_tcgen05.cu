@@ -77,6 +77,18 @@ struct GemmCfg {
   static_assert(SMEM <= SMEM_MAX, "smem");
 };
 
+// Tile order: column-major (m fastest) when B is the larger operand (N > M), so each wave of persistent CTAs
+// covers all of M for a few n columns and A stays resident in L2 while B streams through once (the LSTM gate
+// weight gradients, N = 16384 >> M = 4096: measured DRAM reads 1.57 GB -> see DESIGN); TOFU_RASTER=0 keeps
+// row-major everywhere.
+static int raster_of(const tofu_gemm_args* g) {
+  static const int env = [] {
+    const char* e = getenv("TOFU_RASTER");
+    return e ? atoi(e) : 1;
+  }();
+  return env && g->N > g->M ? 1 : 0;
+}
+
 // Piecewise operands (tofu_operand_pieces, the MultiFetch fused into the TMA producer): one map per piece and
 // the pieces' starts along the split dimension (0 = M / N, 1 = K).  Passed by value as a __grid_constant__
 // kernel parameter (TMA reads maps from parameter space) only by the PC instantiations.
@@ -106,7 +118,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
                      const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD,
                      const __grid_constant__ CUtensorMap tmE, int M, int N, int K, float s0, float s1, int splits,
-                     int ep, int sk_tiles, void* sk_ws) {
+                     int ep, int sk_tiles, void* sk_ws, int raster) {
   using Cfg = GemmCfg<BN, MODE_>;
   constexpr int MODE = Cfg::MODE;
   constexpr int STAGES = Cfg::STAGES;
@@ -131,6 +143,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
   const int nk = (K + BK - 1) / BK;
   // segments = (output tile, k-block range): data-parallel units (tile, K split) then stream-K pieces
   WorkList wl;
+  wl.raster = raster;
+  wl.tiles_m = tiles_m;
+  wl.tiles_n = tiles_n;
   uint32_t crank = 0;
   constexpr bool C2 = Cfg::C2;
   if constexpr (CL2 || C2) {
@@ -565,11 +580,13 @@ static int launch_t(const tofu_gemm_args* g, const CUtensorMap* tm, const PieceM
     const int pair_units = ((g->M + 2 * BM - 1) / (2 * BM)) * ((g->N + BN - 1) / BN);
     const int ncl = pair_units < g_num_sms / 2 ? pair_units : g_num_sms / 2;
     const cudaError_t e = launch_k(kern, dim3(2 * ncl), dim3(Cfg::THREADS), Cfg::SMEM, st, 2, pp, tm[0], tm[1], tm[2],
-                                   tm[3], tm[5], g->M, g->N, g->K, g->s0, g->s1, 1, g->ep, 0, g->sk_ws);
+                                   tm[3], tm[5], g->M, g->N, g->K, g->s0, g->s1, 1, g->ep, 0, g->sk_ws,
+                                   raster_of(g));
     return e == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
   }
   return launch_k(kern, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, st, 1, pp, tm[0], tm[1], tm[2], tm[3], tm[5], g->M,
-                  g->N, g->K, g->s0, g->s1, splits, g->ep, sk, g->sk_ws) == cudaSuccess
+                  g->N, g->K, g->s0, g->s1, splits, g->ep, sk, g->sk_ws,
+                  splits == 1 && sk == 0 ? raster_of(g) : 0) == cudaSuccess
              ? TOFU_OK
              : TOFU_ERR_CUDA;
 }
