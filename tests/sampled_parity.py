@@ -41,7 +41,7 @@ def nrm(a, b):
 class SampledChecker:
     def __init__(self, spec, initial, source, unmaterialized=(), seed=0, out_budget=256):
         self.g = Graph(spec)
-        self.initial = initial                 # name -> numpy array (the step's initial values)
+        self.initial = initial                 # name -> numpy array, or callable (name, box) -> region
         self.source = source
         self.unmat = set(unmaterialized)
         self.rng = np.random.default_rng(seed)
@@ -57,6 +57,8 @@ class SampledChecker:
         if t in self.unmat:
             return self._recompute(t, box)
         if t not in self.producers:
+            if callable(self.initial):       # regenerated on demand (the largest configs)
+                return np.asarray(self.initial(t, box), np.float64)
             v = np.asarray(self.initial[t], np.float64)
             return v[tuple(slice(lo, hi + 1) for lo, hi in box)] if v.ndim else v
         return self.source(t, box)

@@ -113,3 +113,36 @@ def make_values_device(graph: dict, seed: int = 0, device="cuda", names=None):
         else:
             q *= 2.0 ** -17
         yield name, q
+
+
+def make_value_device(graph: dict, name: str, seed: int = 0, device="cuda"):
+    """One tensor of the recipes above (float32, on `device`) drawn from its OWN generator, seeded by (seed, the
+    tensor's name) — so any single tensor can be regenerated on demand (the parity tests of the largest
+    configs, whose parameters fit neither host memory as float64 nor a second device copy).  Returns None for
+    tensors that are not inputs / weights / state."""
+    import hashlib
+
+    import torch
+    t = graph["tensors"][name]
+    role = t["role"]
+    shape = tuple(t["shape"])
+    if role not in ("input", "weight", "state") or name in graph.get("alias", {}):
+        return None
+    if t.get("init") == "zeros":
+        return torch.zeros(shape, device=device)
+    if t.get("init") == "ones":
+        return torch.ones(shape, device=device)
+    h = int.from_bytes(hashlib.sha256(f"{seed}:{name}".encode()).digest()[:8], "little") & ((1 << 63) - 1)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(h)
+    q = torch.randint(-128, 129, shape, generator=gen, device=device).float()
+    if role == "input":
+        q *= 2.0 ** -7 if name != "T" else 2.0 ** -8
+        if t.get("live_channels") is not None:
+            q[..., int(t["live_channels"]):] = 0.0
+    elif role == "weight":
+        fan_in = int(t.get("fan_in") or shape[0])
+        q *= 2.0 ** (-7 - round(math.log2(math.sqrt(fan_in))))
+    else:
+        q *= 2.0 ** -17
+    return q
