@@ -179,7 +179,15 @@ def virtual_partitioned(spec, vals, k, steps, k1_value=None):
     import torch
     from paper_1807_08887_b200.runner import TofuRunner
     R = TofuRunner(spec, k)
-    R.load(vals)
+    if vals is None:   # the largest configs: each tensor regenerated on the device (tofu_inputs.make_value_device)
+        from tofu_inputs.tensors import make_value_device
+        for name in sorted(spec["tensors"]):
+            v = make_value_device(spec, name, seed=0)
+            if v is not None:
+                R.load({name: v})
+                del v
+    else:
+        R.load(vals)
     ex = R.exec
     for _ in range(3):
         ex.run()
@@ -257,6 +265,9 @@ def run_workload(cfg, args, steps, world, rank, local_rank, group, shared, virtu
     spec = config(cfg)
     k = world
     big = cfg >= 4   # parameters drawn on the device (float64 host copies would not fit in RAM)
+    vp_big = None
+    if big and world == 1 and virtual_k > 1:   # the k-way plan first: both runners' arenas do not fit at once
+        vp_big = virtual_partitioned(spec, None, virtual_k, max(steps, 5))
     vals = None if big else make_values(spec, seed=0)
     if world > 1:
         R = TofuRunner(spec, k, rank=rank, group=group)
@@ -461,8 +472,12 @@ def run_workload(cfg, args, steps, world, rank, local_rank, group, shared, virtu
         "cuda_graph": use_graph,
         "clocks": clk.summary(),
     }
-    if world == 1 and virtual_k > 1 and not big:
-        line["virtual_partitioned"] = virtual_partitioned(spec, vals, virtual_k, max(steps, 5), k1_value=value)
+    if world == 1 and virtual_k > 1:
+        if big:
+            vp_big["ideal_samples_s"] = virtual_k * value
+            line["virtual_partitioned"] = vp_big
+        else:
+            line["virtual_partitioned"] = virtual_partitioned(spec, vals, virtual_k, max(steps, 5), k1_value=value)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sspec, per_step, sample = oracle_sample(cfg)
         t = oracle_step_time(sspec, make_values(sspec, seed=0))
