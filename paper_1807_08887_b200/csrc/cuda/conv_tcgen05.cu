@@ -1084,8 +1084,16 @@ extern "C" int tofu_conv_plan(tofu_conv_args* a, void* tmaps) {
       return !(e && e[0] == '0');
     }();
     a->cl2 = 0;
+    // (TOFU_CONV_C2_FEW=0: only when the data-parallel tiles fill the SMs, so a few-tile launch — a rank's
+    // sub-op under an 8-way plan, e.g. [3136 x 512] = 50 tiles — keeps stream-K; measured no different on
+    // WResNet-152-4 over 8 virtual ranks, 101.2 vs 101.1 ms, so the pairs stay the default)
+    static const bool c2_few = [] {
+      const char* e = getenv("TOFU_CONV_C2_FEW");
+      return !(e && e[0] == '0');
+    }();
+    const int dp_tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
     if (req != -1 && c2_env() != 0 && a->im2col && !a->b_mn_major && bn == 256 && M > BM &&
-        (req == 4 || c2_env() == 1 || fwd_c2)) {
+        (req == 4 || c2_env() == 1 || (fwd_c2 && (c2_few || dp_tiles >= g_sms)))) {
       if (tmap2(&tm[0], a->Bp, BF, 2, a->b_cols, a->b_rows, a->ldb, 64, bn / 2, SW128)) return TOFU_ERR_CUDA;
       a->cl2 = 3;
     }

@@ -787,6 +787,20 @@ extern "C" int tofu_gemm_plan_tmaps(tofu_gemm_args* g, void* tmaps, int* bn_out)
     if (few == 1) bn = 128;
     if (few == 2 && g->sk_ws) g->splits = -1;
   }
+  // Few-tile launches with a fused element-wise epilogue (split-K cannot carry those epilogues): stream-K would
+  // spread the K loop over all SMs (a rank's sub-op under an 8-way plan, e.g. [1568 x 2048] with K = 1024: 104
+  // tiles).  Measured slower (WResNet-152-4 on 8 virtual ranks 101.2 -> 104.7 ms: the partial round trip and
+  // the finishers' waits cost more than the idle SMs), so off unless TOFU_GEMM_SK_EP=1.
+  {
+    static const bool sk_ep = [] {
+      const char* e = getenv("TOFU_GEMM_SK_EP");
+      return e && e[0] == '1';
+    }();
+    const int tiles_dp = ((g->M + BM - 1) / BM) * ((g->N + bn - 1) / bn);
+    if (sk_ep && g->splits == 0 && g->ep && g->sk_ws && !g->a_pieces && !g->b_pieces && g->max_ctas == 0 &&
+        sk_enabled() && tiles_dp * 4 <= 3 * g_num_sms && (g->K + BK - 1) / BK >= 8)
+      g->splits = -1;
+  }
   const bool stream_k = g->splits == -1;
   g->splits = stream_k ? 1 : auto_splits(g, bn);
   // cluster pairs sharing B (see the kernel's CL2): data-parallel launches of 256-wide tiles with at least
