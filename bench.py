@@ -79,6 +79,33 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def nvlink_counters(index):
+    """(tx bytes, rx bytes) summed over the NVLink links of GPU `index` (nvidia-smi nvlink -gt d: cumulative data
+    counters), or None when unavailable (no NVLink, no nvidia-smi)."""
+    try:
+        out = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(index)], capture_output=True, text=True,
+                             timeout=20).stdout
+    except Exception:
+        return None
+    unit = {"B": 1, "KiB": 1024, "MiB": 1024 ** 2, "GiB": 1024 ** 3}
+    tx = rx = 0
+    seen = False
+    for line in out.splitlines():
+        parts = line.replace(",", " ").split()
+        for i, w in enumerate(parts):
+            if w in ("Tx:", "Rx:") and i + 2 < len(parts) + 1 and i + 1 < len(parts):
+                try:
+                    v = float(parts[i + 1]) * unit.get(parts[i + 2] if i + 2 < len(parts) else "KiB", 1024)
+                except ValueError:
+                    continue
+                seen = True
+                if w == "Tx:":
+                    tx += v
+                else:
+                    rx += v
+    return (tx, rx) if seen else None
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -338,6 +365,7 @@ def run_workload(cfg, args, steps, world, rank, local_rank, group, shared, virtu
     with ClockSampler(local_rank) as clk:
         barrier()
         torch.cuda.synchronize()
+        nv0 = nvlink_counters(torch.cuda.current_device()) if world > 1 and not shared else None
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
@@ -345,6 +373,7 @@ def run_workload(cfg, args, steps, world, rank, local_rank, group, shared, virtu
             R.step()
         t1.record()
         torch.cuda.synchronize()
+        nv1 = nvlink_counters(torch.cuda.current_device()) if nv0 is not None else None
         barrier()
         dom_samples.append(dom_a.elapsed_time(dom_b))   # last step of the timed region
         # keep the same step loop running (untimed) until nvidia-smi has >= 5 samples, so the clock
@@ -464,7 +493,14 @@ def run_workload(cfg, args, steps, world, rank, local_rank, group, shared, virtu
                                   "NVLink bytes at 900 GB/s per direction) / measured step (north star); "
                                   "frac_incl_hbm also takes the sub-ops' algorithmic HBM bytes at the copy peak"},
         "bytes_vs_plan": {"plan_bytes": plan_b, "ledger_bytes": ledger_b, "plan_elements": plan_el,
-                          "ledger_elements": ledger_el, "equal": plan_b == ledger_b},
+                          "ledger_elements": ledger_el, "equal": plan_b == ledger_b,
+                          "rank_in_out_bytes": io,
+                          # this rank's NVLink data counters over the timed steps (nvidia-smi nvlink -gt d), per
+                          # step, beside the plan's bytes into / out of this rank (pull model: in = rx, out = tx)
+                          "nvlink_measured": None if nv0 is None or nv1 is None else
+                          {"rank": rank, "tx_per_step": (nv1[0] - nv0[0]) / steps,
+                           "rx_per_step": (nv1[1] - nv0[1]) / steps,
+                           "plan_out": io[rank][1], "plan_in": io[rank][0]}},
         "e2e": {"value": batch / (e2e_ms / 1e3), "unit": "samples/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 4, "api": "TofuRunner.train (H2D of step s+1 overlapped with step s)",
                 "last_loss": float(losses[-1]) if losses.numel() else None},

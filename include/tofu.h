@@ -430,6 +430,13 @@ int tofu_pieces_run(const tofu_piece* pieces_dev, const tofu_piece_task* tasks_d
 #define TOFU_EW_SUMSQ_MSE_GRAD 9
 int tofu_elementwise(int kind, int64_t n, void* y_dev, const void* x0_dev, const void* x1_dev, void* x2_dev,
                      float s0, float s1, void* stream);
+/* The same with the loss reduction's workspace supplied by the caller (ws: tofu_sumsq_workspace_bytes() bytes
+ * of device memory, zero-filled once, left zeroed by every launch): concurrent TOFU_EW_SUMSQ launches on
+ * different streams / executors then cannot share the block partials and ticket (tofu_elementwise uses one
+ * module-wide workspace: one such launch at a time per device).  The executor passes its own. */
+int64_t tofu_sumsq_workspace_bytes(void);
+int tofu_elementwise_ws(int kind, int64_t n, void* y_dev, const void* x0_dev, const void* x1_dev, void* x2_dev,
+                        float s0, float s1, void* ws_dev, void* stream);
 
 #ifdef __cplusplus
 }

@@ -35,7 +35,7 @@ __device__ unsigned g_sumsq_ticket = 0;
 template <int KIND>
 __global__ void __launch_bounds__(256) ew_kernel(int64_t n, void* __restrict__ y, const void* __restrict__ x0,
                                                  const void* __restrict__ x1, void* __restrict__ x2, float s0,
-                                                 float s1) {
+                                                 float s1, float* __restrict__ sumsq_part, unsigned* __restrict__ sumsq_ticket) {
   tofu::pdl_trigger();
   tofu::pdl_wait();
   const int64_t nvec = n / 8;
@@ -139,15 +139,15 @@ __global__ void __launch_bounds__(256) ew_kernel(int64_t n, void* __restrict__ y
     if (threadIdx.x == 0) {
       float s = 0.f;
       for (int w = 0; w < 8; ++w) s += red[w];
-      g_sumsq_part[blockIdx.x] = s;
+      sumsq_part[blockIdx.x] = s;
       __threadfence();
-      last = atomicAdd(&g_sumsq_ticket, 1u) == gridDim.x - 1;
+      last = atomicAdd(sumsq_ticket, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (last) {
       __threadfence();
       float t = 0.f;
-      for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) t += __ldcg(&g_sumsq_part[b]);
+      for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) t += __ldcg(&sumsq_part[b]);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
       if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(256) ew_kernel(int64_t n, void* __restrict__ y
         float s = 0.f;
         for (int w = 0; w < 8; ++w) s += red[w];
         *reinterpret_cast<float*>(y) += s;
-        g_sumsq_ticket = 0;  // ready for the next launch (launches of one stream are ordered)
+        *sumsq_ticket = 0;  // ready for the next launch (launches of one stream are ordered)
       }
     }
   }
@@ -164,8 +164,10 @@ __global__ void __launch_bounds__(256) ew_kernel(int64_t n, void* __restrict__ y
 
 }  // namespace tofu
 
-extern "C" int tofu_elementwise(int kind, int64_t n, void* y, const void* x0, const void* x1, void* x2, float s0,
-                                float s1, void* stream) {
+extern "C" int64_t tofu_sumsq_workspace_bytes(void) { return (int64_t)tofu::SUMSQ_MAX_BLOCKS * 4 + 16; }
+
+extern "C" int tofu_elementwise_ws(int kind, int64_t n, void* y, const void* x0, const void* x1, void* x2, float s0,
+                                   float s1, void* ws, void* stream) {
   if (n < 0) return TOFU_ERR_ARG;
   if (n == 0) return TOFU_OK;
   // 16-byte alignment of every buffer for the vector path
@@ -180,12 +182,32 @@ extern "C" int tofu_elementwise(int kind, int64_t n, void* y, const void* x0, co
   if (want < grid) grid = want < 1 ? 1 : want;
   if (grid > tofu::SUMSQ_MAX_BLOCKS) grid = tofu::SUMSQ_MAX_BLOCKS;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // the loss reduction's block partials and ticket: the caller's workspace, else the module's (one such launch
+  // at a time per device)
+  float* part = nullptr;
+  unsigned* ticket = nullptr;
+  if (ws) {
+    part = reinterpret_cast<float*>(ws);
+    ticket = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ws) + (int64_t)tofu::SUMSQ_MAX_BLOCKS * 4);
+  } else {
+    void *pp = nullptr, *tp = nullptr;
+    if (cudaGetSymbolAddress(&pp, tofu::g_sumsq_part) != cudaSuccess ||
+        cudaGetSymbolAddress(&tp, tofu::g_sumsq_ticket) != cudaSuccess)
+      return TOFU_ERR_CUDA;
+    part = reinterpret_cast<float*>(pp);
+    ticket = reinterpret_cast<unsigned*>(tp);
+  }
   switch (kind) {
-#define K(X) case X: tofu::launch_k(tofu::ew_kernel<X>, dim3((unsigned)grid), dim3(256), 0, st, 1, n, y, x0, x1, x2, s0, s1); break;
+#define K(X) case X: tofu::launch_k(tofu::ew_kernel<X>, dim3((unsigned)grid), dim3(256), 0, st, 1, n, y, x0, x1, x2, s0, s1, part, ticket); break;
     K(TOFU_EW_RELU) K(TOFU_EW_RELU_GRAD) K(TOFU_EW_MSE_GRAD) K(TOFU_EW_MOM) K(TOFU_EW_SGD) K(TOFU_EW_SGD_MOM)
     K(TOFU_EW_SUMSQ) K(TOFU_EW_ADD) K(TOFU_EW_ADDRELU) K(TOFU_EW_SUMSQ_MSE_GRAD)
 #undef K
     default: return TOFU_ERR_ARG;
   }
   return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
+}
+
+extern "C" int tofu_elementwise(int kind, int64_t n, void* y, const void* x0, const void* x1, void* x2, float s0,
+                                float s1, void* stream) {
+  return tofu_elementwise_ws(kind, n, y, x0, x1, x2, s0, s1, nullptr, stream);
 }

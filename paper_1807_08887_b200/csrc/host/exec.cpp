@@ -174,6 +174,7 @@ struct Exec {
   tofu_piece_task* tasks_dev = nullptr;
   std::vector<tofu_piece_task> host_tasks;
   void* ws_dev = nullptr;  // split-K workspace shared by this executor's GEMMs (one stream)
+  void* ew_ws = nullptr;   // the loss reduction's partials + ticket (tofu_elementwise_ws), zero between launches
   void* sk_dev = nullptr;  // stream-K workspace (partials + flags, zero-filled), shared likewise
   std::vector<tofu_piece> host_pieces;
   bool finalized = false;
@@ -1356,6 +1357,11 @@ void finalize(Exec& E) {
     if (cudaMemcpy(E.tasks_dev, E.host_tasks.data(), nb, cudaMemcpyHostToDevice) != cudaSuccess)
       throw Error(TOFU_ERR_CUDA, "cudaMemcpy piece tasks");
   }
+  if (!E.ew_ws) {
+    const int64_t b = tofu_sumsq_workspace_bytes();
+    if (cudaMalloc(&E.ew_ws, b) != cudaSuccess || cudaMemset(E.ew_ws, 0, b) != cudaSuccess)
+      throw Error(TOFU_ERR_CUDA, "cudaMalloc loss workspace");
+  }
   // stream-K workspace: launches run one at a time on the executor's stream, each leaves the flags zeroed
   if (!E.sk_dev) {
     const int64_t skb = tofu_sk_workspace_bytes();
@@ -1873,9 +1879,10 @@ int run_compute(Exec& E, int o, int li, cudaStream_t st) {
     const int64_t m = vol(L.in[0].box);
     if (L.fused_loss_grad) {  // + the next op (mse_grad of the same inputs) in the same pass
       const LOp& Ln = E.lops[li][o + 1];
-      return tofu_elementwise(TOFU_EW_SUMSQ_MSE_GRAD, m, y, x0, x1, base + Ln.out.off, kc(o), kc(o + 1), st);
+      return tofu_elementwise_ws(TOFU_EW_SUMSQ_MSE_GRAD, m, y, x0, x1, base + Ln.out.off, kc(o), kc(o + 1), E.ew_ws,
+                                 st);
     }
-    return tofu_elementwise(TOFU_EW_SUMSQ, m, y, x0, x1, nullptr, kc(o), 0, st);
+    return tofu_elementwise_ws(TOFU_EW_SUMSQ, m, y, x0, x1, nullptr, kc(o), 0, E.ew_ws, st);
   }
   if (is_mom(dn)) {
     if (L.fused_sgd) {
@@ -1986,6 +1993,7 @@ extern "C" void tofu_exec_destroy(tofu_exec* h) {
   if (h->e.flags_dev) cudaFree(h->e.flags_dev);
   if (h->e.ws_dev) cudaFree(h->e.ws_dev);
   if (h->e.sk_dev) cudaFree(h->e.sk_dev);
+  if (h->e.ew_ws) cudaFree(h->e.ew_ws);
   delete h;
 }
 

@@ -92,6 +92,7 @@ def lib():
             "tofu_pieces_tasks": [vp, C.c_int, vp, C.c_int64, i64p],
             "tofu_conv_bf16": [C.POINTER(ConvArgs), vp],
             "tofu_elementwise": [C.c_int, C.c_int64, vp, vp, vp, vp, C.c_float, C.c_float, vp],
+            "tofu_elementwise_ws": [C.c_int, C.c_int64, vp, vp, vp, vp, C.c_float, C.c_float, vp, vp],
             "tofu_describe_op": [C.c_char_p, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
             "tofu_graph_create": [C.c_char_p, C.POINTER(vp)],
             "tofu_graph_destroy": [vp],
@@ -128,6 +129,9 @@ def lib():
         if hasattr(L, "tofu_sk_workspace_bytes"):   # (absent from experimental builds of older sources)
             L.tofu_sk_workspace_bytes.argtypes = []
             L.tofu_sk_workspace_bytes.restype = C.c_int64
+        if hasattr(L, "tofu_sumsq_workspace_bytes"):
+            L.tofu_sumsq_workspace_bytes.argtypes = []
+            L.tofu_sumsq_workspace_bytes.restype = C.c_int64
         _lib = L
     return _lib
 

@@ -324,3 +324,32 @@ def test_piece_tasks_normalise_and_cover(tofu):
         segs = sorted(cover[i])
         assert segs[0][0] == 0 and all(a + n == b for (a, n), (b, _) in zip(segs, segs[1:]))
         assert segs[-1][0] + segs[-1][1] == nv
+
+
+def test_fig10_wresnet_152_10_partition_shape(tofu):
+    """§7.4 / Fig. 10, the partition Tofu finds for WResNet-152-10 at k = 8, reproduced by the
+    library's planner: (1) both the batch and the channel dimensions are partitioned; (2) the repeated residual
+    blocks of a group are partitioned identically, the first block of a group differently; (3) the lower
+    layers (large feature maps, small weights) split the batch — their weights are fetched — and the higher
+    layers split channels — their activations are fetched."""
+    import re
+    spec = config(5)
+    p = tofu.Plan(tofu.Graph(spec), 8).json()
+    os_ = p["osplit"]
+    by = {}
+    for o in spec["ops"]:
+        m = re.match(r"s(\d)u(\d+)\.(conv\d(?:_dgrad|_wgrad)?)$", o["name"])
+        if m:
+            by.setdefault((int(m.group(1)), m.group(3)), []).append((int(m.group(2)), tuple(os_[o["name"]])))
+    used = {v for seq in os_.values() for v in seq}
+    assert "b" in used and ({"ci", "co"} & used)                                   # (1)
+    for (stage, kind), lst in by.items():                                          # (2)
+        lst.sort()
+        assert len({s for u, s in lst[1:]}) <= 1, (stage, kind, lst)
+    assert any(lst[0][1] != lst[1][1] for lst in by.values() if len(lst) > 1)
+    for (stage, kind), lst in by.items():                                          # (3)
+        for u, seq in lst:
+            if stage == 0:
+                assert set(seq) == {"b"}, (stage, kind, u, seq)
+            if stage == 3:
+                assert "b" not in seq and set(seq) & {"ci", "co"}, (stage, kind, u, seq)

@@ -231,3 +231,31 @@ def test_mlp_plans_are_optimal(k):
     a = auto_search(g, k)                            # runs the exact joint search too (flat_cells is small)
     assert a["search"] == "recursive"                # the flat optimum is not strictly cheaper
     assert a["cost"] == flat_search(g, k)[0] if k < 8 else True
+
+
+# ------------------------------------------------------------------------------------------ paper figures
+def test_fig5_recursive_matmul_to_four_workers():
+    """Fig. 5: a matmul partitioned to four workers — step 1 partitions every matrix by row and
+    group 0 fetches B[1, :] from the other group; step 2 partitions every matrix by column, leaving a 2x2 grid
+    with each worker computing one block of C.  Under the direct-transfer model (R3) that plan is optimal:
+    its step 1 is a co-optimal first step (δ₁ = 2 groups x the 32-element half of B = 64) and the two-step
+    plan costs the exact optimum (128 elements, flat search)."""
+    from oracle.cost import digits, iter_box, owned_box
+    g = Graph({"defs": {"mm_nn": "def mm_nn(A(2), B(2)) -> lambda i, j: reduce(Sum; k; A[i, k] * B[k, j])"},
+               "tensors": {t: {"shape": [8, 8], "dtype": "f32", "role": "act"} for t in "ABC"},
+               "ops": [{"name": "mm", "def": "mm_nn", "inputs": ["A", "B"], "output": "C"}]})
+    fig = {"factors": [2, 2], "tdims": {t: [0, 1] for t in "ABC"}, "osplit": {"mm": ["i", "j"]}}
+    c1, firsts = step_search(g, empty_plan(g), 2)
+    assert c1 == 64 and any(p["tdims"] == {t: [0] for t in "ABC"} and p["osplit"]["mm"] == ["i"] for p in firsts)
+    assert step_costs(g, fig) == [64, 64]
+    assert plan_cost(g, fig)[0] == flat_search(g, 4)[0] == recursive_search(g, 4)["cost"] == 128
+    # every matrix a 2x2 block grid; worker w computes exactly the C block it owns
+    blocks = set()
+    for w in range(4):
+        dig = digits(w, [2, 2])
+        own = owned_box([8, 8], [0, 1], [2, 2], dig)
+        ib = iter_box({"i": 8, "j": 8, "k": 8}, ["i", "j", "k"], ["i", "j"], [2, 2], dig)
+        assert [tuple(own[0]), tuple(own[1])] == [ib["i"], ib["j"]]
+        assert own[0][1] - own[0][0] == 3 and own[1][1] - own[1][0] == 3
+        blocks.add((own[0], own[1]))
+    assert len(blocks) == 4
