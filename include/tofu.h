@@ -120,7 +120,10 @@ int tofu_execute(tofu_exec* e, void* stream);
 int tofu_exec_ledger(const tofu_exec* e, int64_t* elements, int64_t* bytes);
 /* Number of kernel launches issued by one tofu_execute (all local ranks). */
 int tofu_exec_launch_count(const tofu_exec* e, int64_t* launches);
-/* 1 = skip fetch/reduce kernels (compute-only time), 0 = normal. */
+/* 1 = skip the fetch / reduce / barrier launches (compute-only time), 0 = normal.  A GEMM whose
+ * operand is read in place from its owners (fused fetch, tofu_operand_pieces) still performs those reads inside
+ * the compute launch: its time includes that transfer (it is not separable — the point of the fusion), so at
+ * k > 1 the compute-only time is an upper bound for plans with fused operands. */
 int tofu_exec_set_skip_comm(tofu_exec* e, int skip);
 /* Launch list introspection (kernels, barriers and memsets of one step, in issue order). */
 int tofu_exec_num_launches(const tofu_exec* e, int* n);
