@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <functional>
+#include <tuple>
 #include <cstring>
 #include <map>
 #include <set>
@@ -117,6 +119,48 @@ struct LOp {
   bool remote_direct = false;  // the compute reads peer memory in place (fused fetch)
 };
 
+// Memory planner ("leveraging the existing memory planner"; TOFU_MEMPLAN=1): the transient
+// tensors of a step (roles act / grad: activations, gradients, weight gradients) share arena space when their
+// lifetimes are disjoint; inputs, weights, optimizer state and the loss keep their own.  A lifetime runs from
+// the earliest op that may write the tensor — its producer, or an op whose launch absorbs the producer by
+// fusion (R8: a producer of one of the producer's inputs, two levels up) — to its last reader.  Offsets are
+// identical on every rank (shards of a tensor have the same size on every rank that owns one).  Off by
+// default: the per-op parity tests read every tensor after the step.
+bool memplan_enabled() {  // read at every layout (arena size, shard offsets and the executor must agree)
+  const char* e = std::getenv("TOFU_MEMPLAN");
+  return e && e[0] == '1';
+}
+
+bool transient(const Graph& g, int t) {
+  const std::string& r = g.tensors[t].role;
+  return r == "act" || r == "grad";
+}
+
+// [first op that may write t, last op that reads it] (op indices), for the transient tensors
+std::vector<std::pair<int, int>> lifetimes(const Graph& g) {
+  const int nt = (int)g.tensors.size(), no = (int)g.ops.size();
+  std::vector<std::vector<int>> producers(nt);
+  for (int o = 0; o < no; ++o) producers[g.ops[o].output].push_back(o);
+  std::vector<std::pair<int, int>> life(nt, {INT32_MAX, -1});
+  for (int o = 0; o < no; ++o) {
+    const int t = g.ops[o].output;
+    int start = o;
+    for (int x : g.ops[o].inputs)
+      for (int p : producers[x]) {
+        start = std::min(start, p);
+        for (int y : g.ops[p].inputs)
+          for (int q : producers[y]) start = std::min(start, q);
+      }
+    if (o > 0) start = std::min(start, o - 1);  // (fused_next / loss pair: written by the previous op's launch)
+    life[t].first = std::min(life[t].first, start);
+    life[t].second = std::max(life[t].second, o);
+    for (int x : g.ops[o].inputs) life[x].second = std::max(life[x].second, o);
+  }
+  for (auto& l : life)
+    if (l.first == INT32_MAX) l = {0, std::max(l.second, 0)};
+  return life;
+}
+
 Layout layout_rank(const Graph& g, const PlanSeq& p, int rank, std::vector<std::vector<LOp>>* lops_all = nullptr) {
   Layout L;
   const int nt = (int)g.tensors.size();
@@ -125,15 +169,55 @@ Layout layout_rank(const Graph& g, const PlanSeq& p, int rank, std::vector<std::
   L.shard_box.assign(nt, {});
   std::map<int, int> alias_old;
   for (auto& pr : g.alias) alias_old[pr.first] = pr.second;
+  std::set<int> aliased;
+  for (auto& pr : g.alias) {
+    aliased.insert(pr.first);
+    aliased.insert(pr.second);
+  }
+  const bool plan_mem = memplan_enabled();
   int64_t off = 0;
+  std::vector<int> packed;
   for (int t = 0; t < nt; ++t) {
     std::vector<Rng> box;
     bool own = owned_box(g, t, p.tdims[t], p.factors, dig, box);
     L.shard_box[t] = box;
     if (!own) continue;
     if (alias_old.count(t)) continue;  // stored in the old tensor's shard
+    if (plan_mem && transient(g, t) && !aliased.count(t)) {
+      packed.push_back(t);
+      continue;
+    }
     L.shard_off[t] = off;
     off = align_up(off + vol(box) * g.itemsize(t));
+  }
+  if (!packed.empty()) {
+    // interval packing: in order of first write, each tensor at the lowest offset whose range no tensor of an
+    // overlapping lifetime occupies
+    const auto life = lifetimes(g);
+    std::stable_sort(packed.begin(), packed.end(), [&](int a, int b) { return life[a].first < life[b].first; });
+    struct Placed {
+      int64_t lo, hi;
+      int t;
+    };
+    std::vector<Placed> placed;
+    const int64_t base = off;
+    int64_t top = off;
+    for (int t : packed) {
+      const int64_t sz = align_up(vol(L.shard_box[t]) * g.itemsize(t));
+      std::vector<std::pair<int64_t, int64_t>> busy;
+      for (auto& q : placed)
+        if (!(life[q.t].second < life[t].first || life[t].second < life[q.t].first)) busy.push_back({q.lo, q.hi});
+      std::sort(busy.begin(), busy.end());
+      int64_t at = base;
+      for (auto& b : busy) {
+        if (at + sz <= b.first) break;
+        at = std::max(at, b.second);
+      }
+      placed.push_back({at, at + sz, t});
+      L.shard_off[t] = at;
+      top = std::max(top, at + sz);
+    }
+    off = align_up(top);
   }
   for (auto& kv : alias_old) {
     // chains resolve to the root storage
@@ -1047,11 +1131,32 @@ void lower(Exec& E) {
   // op parity).  rreads = objects some rank reads in a PEER's memory.
   {
     std::map<int, int> al(g.alias.begin(), g.alias.end());
-    auto root = [&](int t) {
+    auto aroot = [&](int t) {
       while (al.count(t)) t = al[t];
       return t;
     };
     const int nt = (int)g.tensors.size();
+    // tensors whose storage overlaps on some rank (the memory planner packs transient tensors of disjoint
+    // lifetimes into the same bytes) are ONE object: a write to one waits for the readers of the other
+    std::vector<int> uf(nt);
+    for (int t = 0; t < nt; ++t) uf[t] = t;
+    std::function<int(int)> find = [&](int x) { return uf[x] == x ? x : uf[x] = find(uf[x]); };
+    for (int r = 0; r < k; ++r) {
+      std::vector<std::tuple<int64_t, int64_t, int>> iv;
+      for (int t = 0; t < nt; ++t)
+        if (E.lay[r].shard_off[t] >= 0 && !al.count(t))
+          iv.emplace_back(E.lay[r].shard_off[t], E.lay[r].shard_off[t] + vol(E.lay[r].shard_box[t]) * g.itemsize(t), t);
+      std::sort(iv.begin(), iv.end());
+      int64_t hi = -1;
+      int grp = -1;
+      for (auto& [lo, h, t] : iv) {
+        if (grp >= 0 && lo < hi) uf[find(t)] = find(grp);
+        else grp = t;
+        if (lo >= hi) grp = t;
+        hi = std::max(hi, h);
+      }
+    }
+    auto root = [&](int t) { return find(aroot(t)); };
     E.acc.assign(g.ops.size(), {});
     for (size_t o = 0; o < g.ops.size(); ++o) {
       Exec::OpAcc& A = E.acc[o];

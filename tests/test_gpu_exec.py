@@ -269,3 +269,30 @@ def test_two_streams_equal_one_stream(which, k, monkeypatch):
     assert streams["1"] == 0
     for t in outs["1"]:
         assert np.array_equal(outs["1"][t], outs["2"][t]), t
+
+
+@pytest.mark.parametrize("which,k", [("wresnet", 1), ("wresnet", 4), ("lstm", 4)])
+def test_memory_planner_equals_dedicated_storage(which, k, monkeypatch):
+    """TOFU_MEMPLAN=1 (transient tensors of disjoint lifetimes share arena bytes): two training
+    steps leave the persistent tensors (weights, momentum, loss) bitwise equal to the run with dedicated
+    storage for every tensor, with a smaller arena."""
+    from paper_1807_08887_b200.runner import TofuRunner
+    from tofu_inputs.graphs import lstm, wresnet
+    spec = {"wresnet": lambda: wresnet([1, 2], 2, 8, 64, base=32, classes=64), "lstm": lambda: lstm(2, 256, 4, 32)}[which]()
+    vals = make_values(spec, seed=29)
+    persist = [t for t, i in spec["tensors"].items() if i["role"] in ("weight", "state", "loss")]
+    outs, arena = {}, {}
+    for m in ("0", "1"):
+        monkeypatch.setenv("TOFU_MEMPLAN", m)
+        R = TofuRunner(spec, k)
+        arena[m] = sum(R.plan.arena_bytes(r) for r in range(k))
+        R.load(vals)
+        for _ in range(2):
+            R.step()
+        torch.cuda.synchronize()
+        outs[m] = {t: R.gather(t).float().cpu().numpy() for t in persist}
+        assert R.ledger() == R.plan.cost()
+        del R
+    assert arena["1"] <= arena["0"]
+    for t in persist:
+        assert np.array_equal(outs["0"][t], outs["1"][t]), t

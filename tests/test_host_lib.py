@@ -353,3 +353,70 @@ def test_fig10_wresnet_152_10_partition_shape(tofu):
                 assert set(seq) == {"b"}, (stage, kind, u, seq)
             if stage == 3:
                 assert "b" not in seq and set(seq) & {"ci", "co"}, (stage, kind, u, seq)
+
+
+def _lifetimes_py(spec):
+    """Tensor lifetimes re-derived here (op indices): [earliest op that may write it — its producer or, by
+    fusion, a producer of the producer's inputs two levels up, or the op before — , last reader]."""
+    ops = spec["ops"]
+    prod = {}
+    for i, o in enumerate(ops):
+        prod.setdefault(o["output"], []).append(i)
+    life = {}
+    for i, o in enumerate(ops):
+        start = i
+        for x in o["inputs"]:
+            for p in prod.get(x, []):
+                start = min(start, p)
+                for y in ops[p]["inputs"]:
+                    for q in prod.get(y, []):
+                        start = min(start, q)
+        if i > 0:
+            start = min(start, i - 1)
+        lo, hi = life.get(o["output"], (10 ** 9, -1))
+        life[o["output"]] = (min(lo, start), max(hi, i))
+        for x in o["inputs"]:
+            lo, hi = life.get(x, (10 ** 9, -1))
+            life[x] = (lo, max(hi, i))
+    return life
+
+
+@pytest.mark.parametrize("which", ["mlp", "lstm", "wresnet"])
+def test_memory_planner_layout(tofu, which, monkeypatch):
+    """TOFU_MEMPLAN=1: transient tensors (activations, gradients) share arena bytes only when their
+    lifetimes are disjoint; persistent tensors (inputs, weights, state, loss) keep their own; the arena shrinks;
+    the ledger still equals the plan."""
+    from tofu_inputs.graphs import lstm, wresnet
+    spec = {"mlp": lambda: config(0), "lstm": lambda: lstm(2, 64, 4, 8),
+            "wresnet": lambda: wresnet([1, 2], 2, 4, 64, base=16, classes=16)}[which]()
+    g = tofu.Graph(spec)
+    plan = tofu.Plan(g, 4)
+    monkeypatch.setenv("TOFU_MEMPLAN", "0")
+    before = [plan.arena_bytes(r) for r in range(4)]
+    monkeypatch.setenv("TOFU_MEMPLAN", "1")
+    after = [plan.arena_bytes(r) for r in range(4)]
+    assert all(a <= b for a, b in zip(after, before)), (before, after)
+    if which == "wresnet":
+        assert all(a < b for a, b in zip(after, before)), (before, after)
+    life = _lifetimes_py(spec)
+    isz = {"bf16": 2, "f32": 4}
+    alias = set(spec.get("alias", {})) | set(spec.get("alias", {}).values())
+    for r in range(4):
+        iv = []
+        for t, info in spec["tensors"].items():
+            off, box = plan.shard(r, t)
+            if off < 0 or t in spec.get("alias", {}):
+                continue
+            n = 1
+            for lo, hi in box:
+                n *= hi - lo + 1
+            iv.append((off, off + n * isz[info["dtype"]], t))
+        for i, (a0, a1, ta) in enumerate(iv):
+            for b0, b1, tb in iv[i + 1:]:
+                if a0 < b1 and b0 < a1:   # shared bytes: both transient, lifetimes disjoint
+                    for t in (ta, tb):
+                        assert spec["tensors"][t]["role"] in ("act", "grad") and t not in alias, t
+                    la, lb = life[ta], life[tb]
+                    assert la[1] < lb[0] or lb[1] < la[0], (ta, la, tb, lb)
+    ex = tofu.Exec(g, plan, list(range(4)), [0x100000000 * (r + 1) for r in range(4)])
+    assert ex.ledger() == plan.cost()
