@@ -770,6 +770,13 @@ extern "C" int tofu_gemm_plan_tmaps(tofu_gemm_args* g, void* tmaps, int* bn_out)
       (reinterpret_cast<uintptr_t>(g->D) & 15))
     return TOFU_ERR_ALIGN;
   int bn = (g->bn == 128 || g->bn == 256) ? g->bn : (g->N <= 128 ? 128 : 256);
+  {  // TOFU_EP_BN=128: 128-wide tiles for the fused element-wise epilogues (A/B switch)
+    static const int ep_bn = [] {
+      const char* e = getenv("TOFU_EP_BN");
+      return e ? atoi(e) : 0;
+    }();
+    if (ep_bn == 128 && g->bn == 0 && g->ep) bn = 128;
+  }
   // (measured: 128-wide tiles do not recover the last-wave loss of 196-tile shapes, they run ~25% slower)
   // Few-tile outputs (256-wide tiles fill at most half the SMs) that 128-wide tiles fill more than half of,
   // e.g. the LSTM's per-timestep [128 x 16384] gate GEMMs, which stream their 134 MB weight from HBM: 128-wide
