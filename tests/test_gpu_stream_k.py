@@ -3,8 +3,8 @@ WResNet-like 3x3 convolution (16 x 14 x 14 pixels, 768 channels) whose output ti
 evenly (75 tiles for the forward / data gradient, 162 for the weight gradient; all compute-bound), so tiles' k-loops are cut across CTAs
 and finished from the fp32 partials of the others.  Forward (with the fused add+relu+mask
 epilogue), data gradient (MN-major weights, flipped taps) and weight gradient (store and fused momentum-SGD)
-against an fp64 CPU convolution (torch.nn.functional, float64) of the same bf16-exact inputs, and against
-the same launch without a stream-K workspace.  Tolerances as the north star: bf16 outputs normwise <= 5e-3,
+against the oracle's fp64 evaluation of the convolution TDL defs (cross-checked with torch's fp64 convolution)
+on the same bf16-exact inputs, and against the same launch without a stream-K workspace.  Tolerances as the north star: bf16 outputs normwise <= 5e-3,
 fp32 <= 1e-5."""
 import numpy as np
 import pytest
@@ -73,12 +73,30 @@ def data():
     Xt = torch.from_numpy(X).permute(0, 3, 1, 2)
     Wt = torch.from_numpy(W).permute(0, 3, 1, 2)
     Dt = torch.from_numpy(D).permute(0, 3, 1, 2)
-    F = torch.nn.functional
+    # references: the oracle's evaluation of the convolution TDL defs (oracle.exec_ref.fast_eval, fp64), checked
+    # against torch's fp64 convolution as a second, independent computation
+    from oracle.exec_ref import fast_eval
+    from oracle.tdl import parse_def
+    from tofu_inputs.graphs import conv_defs
+    defs = {n: parse_def(src) for n, src in conv_defs(3, 1, 1).items()}
+    z4 = (0, 0, 0, 0)
+    full = lambda **kw: {v: (0, n - 1) for v, n in kw.items()}
     ref = {
+        "fwd": fast_eval(defs["conv_k3s1p1"], {"X": (X, z4), "W": (W, z4)},
+                         full(b=B, y=H, x=H, co=C, ky=3, kx=3, ci=C)),
+        "dgrad": fast_eval(defs["dconv_k3s1p1"], {"D": (D, z4), "W": (W, z4)},
+                           full(b=B, y=H, x=H, ci=C, ky=3, kx=3, co=C)),
+        "wgrad": fast_eval(defs["wconv_k3s1p1"], {"D": (D, z4), "X": (X, z4)},
+                           full(co=C, ky=3, kx=3, ci=C, b=B, y=H, x=H)),
+    }
+    F = torch.nn.functional
+    tref = {
         "fwd": F.conv2d(Xt, Wt, padding=1).permute(0, 2, 3, 1).numpy(),
         "dgrad": F.conv_transpose2d(Dt, Wt, padding=1).permute(0, 2, 3, 1).numpy(),
         "wgrad": torch.nn.grad.conv2d_weight(Xt, Wt.shape, Dt, padding=1).permute(0, 2, 3, 1).numpy(),
     }
+    for k in ref:
+        assert nrm(np.asarray(ref[k]), tref[k]) < 1e-12, k
     return rng, X, W, D, ref
 
 
@@ -239,12 +257,26 @@ def test_conv_im2col_stride2(kind):
         outs.append(out.double().cpu().numpy())
     assert modes == [0, 1]
     assert np.array_equal(outs[0], outs[1])
+    # reference: the oracle's evaluation of the stride-2 convolution TDL (R11), cross-checked with torch fp64
+    from oracle.exec_ref import fast_eval
+    from oracle.tdl import parse_def
+    from tofu_inputs.graphs import conv_defs
+    defs = {n: parse_def(src) for n, src in conv_defs(3, 2, 1).items()}
+    z4 = (0, 0, 0, 0)
     if kind == 0:
-        ref = F.conv2d(Xt.permute(0, 3, 1, 2), Wt.permute(0, 3, 1, 2), stride=2, padding=1).permute(0, 2, 3, 1).numpy()
+        ref = fast_eval(defs["conv_k3s2p1"], {"X": (X, z4), "W": (W, z4)},
+                        {"b": (0, Bs - 1), "y": (0, Ho - 1), "x": (0, Ho - 1), "co": (0, Cs - 1), "ky": (0, 2),
+                         "kx": (0, 2), "ci": (0, Cs - 1)})
+        tref = F.conv2d(Xt.permute(0, 3, 1, 2), Wt.permute(0, 3, 1, 2), stride=2, padding=1).permute(0, 2, 3, 1).numpy()
+        assert nrm(np.asarray(ref), tref) < 1e-12
         assert nrm(outs[1], ref) <= 5e-3
     else:
-        ref = torch.nn.grad.conv2d_weight(Xt.permute(0, 3, 1, 2), (Cs, Cs, 3, 3), Dt.permute(0, 3, 1, 2), stride=2,
-                                          padding=1).permute(0, 2, 3, 1).numpy()
+        ref = fast_eval(defs["wconv_k3s2p1"], {"D": (D, z4), "X": (X, z4)},
+                        {"co": (0, Cs - 1), "ky": (0, 2), "kx": (0, 2), "ci": (0, Cs - 1), "b": (0, Bs - 1),
+                         "y": (0, Ho - 1), "x": (0, Ho - 1)})
+        tref = torch.nn.grad.conv2d_weight(Xt.permute(0, 3, 1, 2), (Cs, Cs, 3, 3), Dt.permute(0, 3, 1, 2), stride=2,
+                                           padding=1).permute(0, 2, 3, 1).numpy()
+        assert nrm(np.asarray(ref), tref) < 1e-12
         assert nrm(outs[1], ref) <= 1e-5
 
 
