@@ -69,3 +69,17 @@ if os.environ.get("UNIT"):
             print(f"{ms[i]:7.3f} ms {d['kind']:8s} {d['op']:22s} {d['def']:14s} "
                   f"TF/s={d['flops'] / (ms[i] / 1e3) / 1e12:7.1f} GB/s={d['bytes'] / (ms[i] / 1e3) / 1e9:7.1f} "
                   f"{d.get('fused', '')}")
+
+if os.environ.get("BY_SHAPE"):   # rank-0 launches aggregated by (def, shape, work split, fused)
+    print("--- rank 0 by shape")
+    agg2 = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    for i, d in enumerate(descs):
+        if d.get("rank") not in (0, -1):
+            continue
+        key = (d["kind"], d["def"], str(d.get("mnk", "")), d.get("splits", ""), d.get("bn", ""), d.get("fused", ""))
+        a = agg2[key]
+        a[0] += 1
+        a[1] += ms[i]
+        a[2] += d["flops"]
+    for key, a in sorted(agg2.items(), key=lambda x: -x[1][1])[:40]:
+        print(f"{a[1]:8.3f} ms n={a[0]:4d} TF/s={a[2] / (a[1] / 1e3) / 1e12:7.1f} {key}")
