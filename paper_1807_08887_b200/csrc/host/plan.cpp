@@ -12,6 +12,9 @@
 #include <set>
 #include <string>
 #include <unordered_map>
+#include <cstdlib>
+#include <exception>
+#include <thread>
 
 #include "common.h"
 #include "graph.h"
@@ -375,14 +378,37 @@ static PlanResult make_plan_mode(const Graph& g, int k, int frontier_cap, int so
     r.seq = empty;
   } else if (search == 0) {
     std::vector<PlanSeq> frontier = {empty};
-    CostMemo memo;
-    OrderCache ocache;
-    TableCache tcache;
+    // the frontier's prefixes are searched in parallel (host threads, each with its own caches: the caches
+    // never change a value), and their results combined in frontier order — the same plan as sequentially
+    const int nthreads = [] {
+      const char* e = std::getenv("TOFU_PLAN_THREADS");
+      const int hw = (int)std::thread::hardware_concurrency();
+      return std::max(1, e ? std::atoi(e) : std::min(hw > 0 ? hw : 1, 16));
+    }();
+    std::vector<CostMemo> memo(nthreads);
+    std::vector<OrderCache> ocache(nthreads);
+    std::vector<TableCache> tcache(nthreads);
     for (int ki : factors) {
       int64_t best = INT64_MAX;
       std::vector<PlanSeq> cands;
-      for (auto& pre : frontier) {
-        StepResult s = step_search(g, pre, ki, solution_cap, memo, ocache, tcache);
+      std::vector<StepResult> res(frontier.size());
+      std::vector<std::exception_ptr> err(nthreads);
+      auto work = [&](int tid) {
+        try {
+          for (size_t i = tid; i < frontier.size(); i += nthreads)
+            res[i] = step_search(g, frontier[i], ki, solution_cap, memo[tid], ocache[tid], tcache[tid]);
+        } catch (...) {
+          err[tid] = std::current_exception();
+        }
+      };
+      const int nt = std::min<int>(nthreads, (int)frontier.size());
+      std::vector<std::thread> pool;
+      for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+      work(0);
+      for (auto& th : pool) th.join();
+      for (auto& e : err)
+        if (e) std::rethrow_exception(e);
+      for (auto& s : res) {
         r.truncated |= s.truncated;
         if (s.cost < best) {
           best = s.cost;
