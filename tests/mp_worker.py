@@ -11,6 +11,9 @@ def worker_spec(which):
     from tofu_inputs.graphs import config, wresnet
     if which == "wres":   # a small WResNet: halo / strided-gradient fetches, partition-n-reduce + fused consumers
         return wresnet([1, 1], 1, 8, 32, base=16, classes=16)
+    if which == "lstm":   # a small LSTM: stacked-state views, fused cells, fused (in-place) GEMM operand fetches
+        from tofu_inputs.graphs import lstm
+        return lstm(2, 256, 4, 32)
     return config(0)
 
 

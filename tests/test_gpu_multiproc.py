@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 @pytest.mark.parametrize("world,which,jitter", [(2, "mlp", None), (2, "mlp", "7"), (4, "wres", None),
-                                                (4, "wres", "11")])
+                                                (4, "wres", "11"), (4, "lstm", "5")])
 def test_processes_step_equals_virtual(tmp_path, world, which, jitter):
     """world processes (one rank each, IPC-mapped peer arenas, device barriers) run two steps and match the
     virtual-rank executor bitwise.  With TOFU_JITTER every process injects pseudo-random 0-200 us delays
