@@ -58,7 +58,13 @@ __device__ __forceinline__ void st4(void* p, int64_t i, int dt, float4 v) {
 constexpr int kTaskVecs = 4096;
 constexpr int kSeg = 256;   // vectors per segment (one warp's unit of work)
 constexpr int kUnr = 4;    // raw copies: 16-byte moves in flight per lane
-constexpr int kUnrC = 2;   // converting / summing path: vectors in flight per lane (register budget)
+#ifndef TOFU_PIECES_UNRC
+#define TOFU_PIECES_UNRC 1
+#endif
+#ifndef TOFU_PIECES_MINB
+#define TOFU_PIECES_MINB 2
+#endif
+constexpr int kUnrC = TOFU_PIECES_UNRC;   // converting / summing path: vectors in flight per lane (1: 8 x fp32 -> bf16 reduce 2.0 -> 2.9 TB/s)
 
 template <int V, typename ST>
 struct Vec;  // V elements of storage type ST
@@ -269,7 +275,7 @@ __global__ void __launch_bounds__(256) pieces_copy_kernel(const tofu_piece* __re
   }
 }
 
-__global__ void __launch_bounds__(256, 2) pieces_kernel(const tofu_piece* __restrict__ pieces,
+__global__ void __launch_bounds__(256, TOFU_PIECES_MINB) pieces_kernel(const tofu_piece* __restrict__ pieces,
                                                      const tofu_piece_task* __restrict__ tasks, int ntasks) {
   tofu::pdl_trigger();
   tofu::pdl_wait();
