@@ -55,7 +55,13 @@ struct GemmCfg {
 #ifndef TOFU_NBUF5
 #define TOFU_NBUF5 2
 #endif
-  static constexpr int NBUF = LOADS ? (MODE == 3 ? (W8 ? 2 : 3) : MODE == 5 ? TOFU_NBUF5 : 3) : 2;
+#ifndef TOFU_NBUF5_128
+#define TOFU_NBUF5_128 TOFU_NBUF5
+#endif
+#ifndef TOFU_NBUF3
+#define TOFU_NBUF3 2
+#endif
+  static constexpr int NBUF = LOADS ? (MODE == 3 ? (W8 ? TOFU_NBUF3 : 3) : MODE == 5 ? (BN == 256 ? TOFU_NBUF5 : TOFU_NBUF5_128) : 3) : 2;
   static constexpr int C_BYTES = 32 * 32 * (MODE == 0 || MODE == 5 ? 2 : 4);
   // MODE 3: W chunk at D_OFF.  MODE 5: add chunk at 0 (the bf16 result overwrites it in place, each thread
   // its own 16-byte slots), mask chunk at D_OFF = 2048.
@@ -187,7 +193,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
+#ifdef TOFU_EXP_NOMAIN
+    if (false) {
+#else
     if (lane == 0) {
+#endif
       int it = 0;
       for (int i = 0; i < nseg; ++i) {
         int tile, kb0, kb1, sp;
@@ -272,6 +282,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
         mbar_wait(&acc_empty[buf], aph ^ 1);  // epilogue has drained this accumulator
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + buf * BN;
+#ifdef TOFU_EXP_NOMAIN
+        kb1 = kb0;
+#endif
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
@@ -307,18 +320,35 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
     uint64_t* wbar = ebar + e * NBUF;
     int split_of_chunk = 0;
     bool part_of_chunk = false;
-    auto chunk_coords = [&](int s, int& col, int& row) {
-      int tile, kb0, kb1;
-      wl.seg(s / NCW, tile, kb0, kb1, split_of_chunk, part_of_chunk);
-      col = (tile % tiles_n) * BN + (h * NCW + s % NCW) * 32;
-      row = (tile / tiles_n) * BM + q * 32;
+    // chunk coordinates through a cursor that re-derives its segment (integer divisions) only when the chunk
+    // crosses into the next tile: one cursor for the operand loads running ahead, one for the stores
+    struct Cursor {
+      int seg = -1, col0 = 0, row = 0, split = 0;
+      bool part = false;
     };
+    Cursor lcur, scur;
+    auto chunk_coords_c = [&](Cursor& k, int s, int& col, int& row) {
+      const int sg = s / NCW;
+      if (sg != k.seg) {
+        int tile, kb0, kb1;
+        wl.seg(sg, tile, kb0, kb1, k.split, k.part);
+        const int tm = tile / tiles_n;
+        k.seg = sg;
+        k.col0 = (tile - tm * tiles_n) * BN + h * NCW * 32;
+        k.row = tm * BM + q * 32;
+      }
+      split_of_chunk = k.split;
+      part_of_chunk = k.part;
+      col = k.col0 + (s - sg * NCW) * 32;
+      row = k.row;
+    };
+    auto chunk_coords = [&](int s, int& col, int& row) { chunk_coords_c(scur, s, col, row); };
     // MODE 5 loads only the operands its runtime `ep` names (2 KB each: a 32x32 bf16 chunk, SWIZZLE_64B)
     const bool loads = MODE == 5 ? (ep & 6) != 0 : Cfg::LOADS;
     const uint32_t load_bytes = MODE == 3 ? 6144 : MODE == 5 ? 2048u * (((ep >> 1) & 1) + ((ep >> 2) & 1)) : 4096;
     auto issue_load = [&](int s) {  // lane 0 only
       int col, row;
-      chunk_coords(s, col, row);
+      chunk_coords_c(lcur, s, col, row);
       uint8_t* b = wbuf + (s % NBUF) * Cfg::BUF_BYTES;
       if (part_of_chunk) {  // a stream-K partial: no epilogue operands needed
         mbar_arrive_expect_tx(&wbar[s % NBUF], 0);
@@ -350,8 +380,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
         tc_fence_after();
       }
       uint32_t r[32];
+#ifdef TOFU_EXP_NOTMEM
+      for (int i = 0; i < 32; ++i) r[i] = 0;
+#else
       tmem_ld_32x32b_x32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, r);
       tmem_ld_wait();
+#endif
       if (cw == NCW - 1) {  // accumulator fully read: hand TMEM back to the MMA warp
         tc_fence_before();
         __syncwarp();
@@ -370,9 +404,22 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
           for (int cc = blockIdx.x + 1; cc < cend; ++cc) *sk_flag(sk_ws, gridDim.x, cc, e) = 0;
       }
       uint8_t* b = wbuf + (s % NBUF) * Cfg::BUF_BYTES;
-      if (loads) {
+      // Refill of the buffer chunk s-1 used (operand chunk s+NBUF-1), issued once chunk s is done: the store of
+      // chunk s-1 has had a whole chunk's time to read that buffer, so the wait rarely blocks (waiting instead for
+      // the store issued just before serialised every chunk behind a TMA store's smem read).
+      auto refill = [&](bool stored) {
         if (lane == 0 && s + NBUF - 1 < S) {
-          bulk_wait_read<0>();  // the store that last used that buffer has read its smem
+          if (stored) bulk_wait_read<1>();  // all but the newest store (chunk s, another buffer) have read smem
+          else bulk_wait_read<0>();
+          issue_load(s + NBUF - 1);
+        }
+      };
+      // (with two buffers the refill of chunk s+1 cannot wait for chunk s to finish: issued first, after the
+      // store of chunk s-1 has read its buffer)
+      constexpr bool LATE = NBUF >= 3;
+      if (loads) {
+        if (!LATE && lane == 0 && s + NBUF - 1 < S) {
+          bulk_wait_read<0>();
           issue_load(s + NBUF - 1);
         }
         __syncwarp();
@@ -381,7 +428,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
         if (lane == 0) bulk_wait_read<NBUF - 1>();
         __syncwarp();
       }
-      if (part) continue;
+      if (part) {
+        if (LATE && loads) refill(false);
+        continue;
+      }
       if (MODE == 5) {
         // fused element-wise ops of the output's consumers (DESIGN R8/R13): v = acc (+ add), relu, mask
 #pragma unroll
@@ -390,33 +440,35 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
           float v[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[8 * j + e]);
-          if (ep & 2) {
+          if (ep & 2) {  // + residual: bf16 pairs widened by shift / mask, added as fp32 pairs (FADD2)
             const uint4 u = *reinterpret_cast<const uint4*>(b + off);
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+            const uint32_t uw[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(h[e]);
-              v[2 * e] += f.x;
-              v[2 * e + 1] += f.y;
+              const uint64_t a2 = (uint64_t)r[8 * j + 2 * e] | ((uint64_t)r[8 * j + 2 * e + 1] << 32);
+              const uint64_t b2 = (uint64_t)(uw[e] << 16) | ((uint64_t)(uw[e] & 0xffff0000u) << 32);
+              uint64_t s2;
+              asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s2) : "l"(a2), "l"(b2));
+              v[2 * e] = __uint_as_float((uint32_t)s2);
+              v[2 * e + 1] = __uint_as_float((uint32_t)(s2 >> 32));
             }
           }
           if (ep & 1)
 #pragma unroll
             for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
-          if (ep & 4) {
-            const uint4 u = *reinterpret_cast<const uint4*>(b + Cfg::D_OFF + off);
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(h[e]);
-              if (!(f.x > 0.f)) v[2 * e] = 0.f;
-              if (!(f.y > 0.f)) v[2 * e + 1] = 0.f;
-            }
-          }
           uint4 w;
           __nv_bfloat162* wh = reinterpret_cast<__nv_bfloat162*>(&w);
 #pragma unroll
           for (int e = 0; e < 4; ++e) wh[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+          if (ep & 4) {  // relu-gradient mask, on the packed result: keep where mask > 0 (NaN, +-0: zero)
+            const uint4 u = *reinterpret_cast<const uint4*>(b + Cfg::D_OFF + off);
+            const __nv_bfloat162* mh = reinterpret_cast<const __nv_bfloat162*>(&u);
+            const __nv_bfloat162 z = __float2bfloat162_rn(0.f);
+            w.x &= __hgt2_mask(mh[0], z);
+            w.y &= __hgt2_mask(mh[1], z);
+            w.z &= __hgt2_mask(mh[2], z);
+            w.w &= __hgt2_mask(mh[3], z);
+          }
           *reinterpret_cast<uint4*>(b + off) = w;
         }
       } else if (MODE == 0) {
@@ -466,6 +518,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
         if (MODE == 3) tma_store_2d(&tmD, b + Cfg::D_OFF, col, row);
         bulk_commit();
       }
+      if (LATE && loads) refill(true);
     }
     if (lane == 0) bulk_wait<0>();
   }
