@@ -114,7 +114,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   constexpr int NBUF = C_::NBUF;
   const tofu_conv_args& a = P.a;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned by an offset from the __shared__ array (an integer round trip through uintptr_t would lose
+  // the address space: every epilogue smem access became a generic LD.E / ST.E)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C_::A_BYTES;
   uint8_t* sE = smem + STAGES * C_::STAGE_BYTES;
