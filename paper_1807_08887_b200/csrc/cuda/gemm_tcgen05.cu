@@ -48,6 +48,12 @@ struct GemmCfg {
   // C2 (bit 4): 2-CTA MMA pairs (tcgen05.mma.cta_group::2, M = 256 over the pair): each CTA stages its own
   // 128 rows of A and half (BN/2 rows) of B
   static constexpr bool C2 = (MODE_ & 16) != 0;
+  // WIDE (bit 5, MODE 5 only): the epilogue moves 32 x 64 chunks (two 32 x 32 boxes per operand behind one
+  // barrier wait, one proxy fence, one store issue), halving the per-chunk fixed instructions of the
+  // issue-bound fused epilogues; double-size buffers, so only for short-K launches that need few stages
+  static constexpr bool WIDE = (MODE_ & 32) != 0;
+  static constexpr int CWD = WIDE ? 2 : 1;
+  static_assert(!WIDE || (MODE_ & 7) == 5, "wide chunks: fused element-wise epilogue only");
   // MODE 5 may load (residual add / relu mask operands, when its runtime `ep` asks for them)
   static constexpr bool LOADS = MODE == 2 || MODE == 3 || MODE == 5;
   // the fused optimizer (MODE 3) and the fused element-wise epilogue (MODE 5) stream extra operands through
@@ -65,8 +71,8 @@ struct GemmCfg {
   static constexpr int C_BYTES = 32 * 32 * (MODE == 0 || MODE == 5 ? 2 : 4);
   // MODE 3: W chunk at D_OFF.  MODE 5: add chunk at 0 (the bf16 result overwrites it in place, each thread
   // its own 16-byte slots), mask chunk at D_OFF = 2048.
-  static constexpr int D_OFF = MODE == 5 ? 2048 : 4096;
-  static constexpr int BUF_BYTES = MODE == 3 ? 6144 : MODE == 5 ? 4096 : (C_BYTES < 1024 ? 1024 : C_BYTES);
+  static constexpr int D_OFF = MODE == 5 ? 2048 * CWD : 4096;
+  static constexpr int BUF_BYTES = MODE == 3 ? 6144 : MODE == 5 ? 4096 * CWD : (C_BYTES < 1024 ? 1024 : C_BYTES);
   // epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter, each half of the tile's columns)
   static constexpr int EW = W8 ? 8 : 4;
   static constexpr int THREADS = 64 + 32 * EW;
@@ -314,8 +320,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
   } else {
     // ------------------------------------------------------------ epilogue (warps 2..5)
     const int q = warp & 3;  // TMEM lane quarter = tile rows 32q..32q+31
-    constexpr int NCH = BN / 32;              // 32-column chunks of a tile row quarter
-    constexpr int NCW = NCH / (Cfg::EW / 4);  // of which this warp handles [h*NCW, (h+1)*NCW)
+    constexpr int CWD = Cfg::CWD;                // 32-column sub-chunks per chunk
+    constexpr int NCH = BN / (32 * CWD);         // chunks of a tile row quarter
+    constexpr int NCW = NCH / (Cfg::EW / 4);     // of which this warp handles [h*NCW, (h+1)*NCW)
     const int e = warp - 2, h = e / 4;
     const int S = nseg * NCW;
     uint8_t* wbuf = sE + e * NBUF * Cfg::BUF_BYTES;
@@ -336,18 +343,19 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
         wl.seg(sg, tile, kb0, kb1, k.split, k.part);
         const int tm = tile / tiles_n;
         k.seg = sg;
-        k.col0 = (tile - tm * tiles_n) * BN + h * NCW * 32;
+        k.col0 = (tile - tm * tiles_n) * BN + h * NCW * 32 * CWD;
         k.row = tm * BM + q * 32;
       }
       split_of_chunk = k.split;
       part_of_chunk = k.part;
-      col = k.col0 + (s - sg * NCW) * 32;
+      col = k.col0 + (s - sg * NCW) * 32 * CWD;
       row = k.row;
     };
     auto chunk_coords = [&](int s, int& col, int& row) { chunk_coords_c(scur, s, col, row); };
     // MODE 5 loads only the operands its runtime `ep` names (2 KB each: a 32x32 bf16 chunk, SWIZZLE_64B)
     const bool loads = MODE == 5 ? (ep & 6) != 0 : Cfg::LOADS;
-    const uint32_t load_bytes = MODE == 3 ? 6144 : MODE == 5 ? 2048u * (((ep >> 1) & 1) + ((ep >> 2) & 1)) : 4096;
+    const uint32_t load_bytes =
+        MODE == 3 ? 6144 : MODE == 5 ? 2048u * CWD * (((ep >> 1) & 1) + ((ep >> 2) & 1)) : 4096;
     auto issue_load = [&](int s) {  // lane 0 only
       int col, row;
       chunk_coords_c(lcur, s, col, row);
@@ -358,8 +366,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
       }
       mbar_arrive_expect_tx(&wbar[s % NBUF], load_bytes);
       if (MODE == 5) {
-        if (ep & 2) tma_load_2d(b, &tmD, &wbar[s % NBUF], col, row);
-        if (ep & 4) tma_load_2d(b + Cfg::D_OFF, &tmE, &wbar[s % NBUF], col, row);
+#pragma unroll
+        for (int d = 0; d < CWD; ++d) {
+          if (ep & 2) tma_load_2d(b + d * 2048, &tmD, &wbar[s % NBUF], col + 32 * d, row);
+          if (ep & 4) tma_load_2d(b + Cfg::D_OFF + d * 2048, &tmE, &wbar[s % NBUF], col + 32 * d, row);
+        }
       } else {
         tma_load_2d(b, &tmC, &wbar[s % NBUF], col, row);
         if (MODE == 3) tma_load_2d(b + Cfg::D_OFF, &tmD, &wbar[s % NBUF], col, row);
@@ -381,11 +392,14 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
         mbar_wait(&acc_full[acc], (local >> 1) & 1);
         tc_fence_after();
       }
-      uint32_t r[32];
+      uint32_t rr[CWD][32];
+      uint32_t(&r)[32] = rr[0];
 #ifdef TOFU_EXP_NOTMEM
       for (int i = 0; i < 32; ++i) r[i] = 0;
 #else
-      tmem_ld_32x32b_x32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, r);
+#pragma unroll
+      for (int d = 0; d < CWD; ++d)
+        tmem_ld_32x32b_x32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + (c * CWD + d) * 32, rr[d]);
       tmem_ld_wait();
 #endif
       if (cw == NCW - 1) {  // accumulator fully read: hand TMEM back to the MMA warp
@@ -397,7 +411,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
         }
         ++local;
       }
-      if (part) {
+      if (Cfg::WIDE) {  // (the dispatcher never pairs wide chunks with stream-K)
+      } else if (part) {
         sk_write_chunk(sk_slot(sk_ws, blockIdx.x), q, NCH, c, lane, r);
         if (cw == NCW - 1) sk_signal(sk_flag(sk_ws, gridDim.x, blockIdx.x, e));
       } else {
@@ -437,8 +452,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
       if (MODE == 5) {
         // fused element-wise ops of the output's consumers (DESIGN R8/R13): v = acc (+ add), relu, mask
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int off = lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
+        for (int dj = 0; dj < 4 * CWD; ++dj) {
+          const int d = dj >> 2, j = dj & 3;
+          const uint32_t(&r)[32] = rr[d];
+          const int off = d * 2048 + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
           float v[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[8 * j + e]);
@@ -516,7 +533,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
         int col, row;
         chunk_coords(s, col, row);
         if (MODE == 4) tma_store_3d(&tmC, b, col, row, split_of_chunk);  // fp32 partial plane of this split
-        else tma_store_2d(&tmC, b, col, row);
+        else
+#pragma unroll
+          for (int d = 0; d < CWD; ++d) tma_store_2d(&tmC, b + d * 2048, col + 32 * d, row);
         if (MODE == 3) tma_store_2d(&tmD, b + Cfg::D_OFF, col, row);
         bulk_commit();
       }
@@ -595,6 +614,18 @@ static double gemm_intensity(const tofu_gemm_args* g, int mode) {
   const double e = mode == 3 ? 12 : mode == 2 ? 8 : mode == 1 ? 4 : 2 + 2 * (((g->ep >> 1) & 1) + ((g->ep >> 2) & 1));
   return 2 * M * N * K / (2 * M * K + 2 * N * K + e * M * N);
 }
+// Wide (32 x 64) epilogue chunks for the 8-warp fused element-wise epilogues of short-K launches: half the
+// per-chunk fixed instructions, but the double-size buffers leave 256-wide tiles 2 smem stages instead of 3,
+// which the K loop of long-K launches feels.  TOFU_EP_WIDE_K = largest K that takes them (0: never).  Measured
+// (tools/ep_stream_bench.py): K = 256 add+mask 119 -> 112 us (0.91 of the copy peak), add+relu 100 -> 95 us;
+// K = 512 add+mask 74 -> 87 us and K = 1024 mask 66 -> 82 us (slower: the lost stage).
+static bool ep_wide(const tofu_gemm_args* g) {
+  static const int kmax = [] {
+    const char* e = getenv("TOFU_EP_WIDE_K");
+    return e ? atoi(e) : 256;
+  }();
+  return g->K <= kmax;
+}
 static int ew8_override() {  // TOFU_EW8=0 / 1 forces the 4- / 8-warp epilogue (A/B measurements); else auto
   static const int v = [] {
     const char* e = getenv("TOFU_EW8");
@@ -668,6 +699,14 @@ static int dispatch_bn(const tofu_gemm_args* g, const CUtensorMap* tm, const Pie
 #undef TOFU_CASES3
 #undef TOFU_CASE3
       default: return TOFU_ERR_ARG;
+    }
+  }
+  if (mode == 5 && w8 && !pc && !cl2 && g->splits != -1 && ep_wide(g)) {  // 32 x 64 epilogue chunks
+    switch ((g->a_mn_major ? 1 : 0) | (g->b_mn_major ? 2 : 0)) {
+      case 0: return launch_t<BN, false, false, 13 | 32, false>(g, tm, pm, st, ai);
+      case 1: return launch_t<BN, true, false, 13 | 32, false>(g, tm, pm, st, ai);
+      case 2: return launch_t<BN, false, true, 13 | 32, false>(g, tm, pm, st, ai);
+      default: return launch_t<BN, true, true, 13 | 32, false>(g, tm, pm, st, ai);
     }
   }
   const int key = (g->a_mn_major ? 1 : 0) | (g->b_mn_major ? 2 : 0) | ((mode | (w8 ? 8 : 0)) << 2) | (pc ? 64 : 0) |
