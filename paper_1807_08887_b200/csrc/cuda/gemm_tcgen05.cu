@@ -186,6 +186,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
     tma_prefetch_desc(&tmC);
     if (MODE == 3 || MODE == 5) tma_prefetch_desc(&tmD);
     if (MODE == 5) tma_prefetch_desc(&tmE);
+    if constexpr (PC) {  // the piece maps (fused fetch) live in parameter space like the others
+      for (int i = 0; i < pm.na; ++i) tma_prefetch_desc(&pm.a_map[i]);
+      for (int i = 0; i < pm.nb; ++i) tma_prefetch_desc(&pm.b_map[i]);
+    }
   }
   if (warp == 1) {
     if constexpr (C2) tmem_alloc2(tmem_slot, Cfg::TMEM_COLS);
@@ -681,8 +685,8 @@ template <int BN>
 static int dispatch_bn(const tofu_gemm_args* g, const CUtensorMap* tm, const PieceMaps* pm, cudaStream_t st) {
   const int mode = g->c_mode == 0 && g->ep ? 5 : g->c_mode;
   const double ai = gemm_intensity(g, mode);
-  const bool pc = pm != nullptr;  // piecewise operands: 4-warp epilogue instantiations only
-  const bool w8 = !pc && wants_w8(g);
+  const bool pc = pm != nullptr;  // piecewise operands (fused fetch)
+  const bool w8 = wants_w8(g);
   const bool cl2 = BN == 256 && g->cl2 == 1 && !pc && mode != 4;
   // (the plan encoded B with half-height boxes for both pair kinds: a launch that cannot honour the pairing
   // would wait for bytes that never arrive)
@@ -701,12 +705,16 @@ static int dispatch_bn(const tofu_gemm_args* g, const CUtensorMap* tm, const Pie
       default: return TOFU_ERR_ARG;
     }
   }
-  if (mode == 5 && w8 && !pc && !cl2 && g->splits != -1 && ep_wide(g)) {  // 32 x 64 epilogue chunks
-    switch ((g->a_mn_major ? 1 : 0) | (g->b_mn_major ? 2 : 0)) {
+  if (mode == 5 && w8 && !cl2 && g->splits != -1 && ep_wide(g)) {  // 32 x 64 epilogue chunks
+    switch ((g->a_mn_major ? 1 : 0) | (g->b_mn_major ? 2 : 0) | (pc ? 4 : 0)) {
       case 0: return launch_t<BN, false, false, 13 | 32, false>(g, tm, pm, st, ai);
       case 1: return launch_t<BN, true, false, 13 | 32, false>(g, tm, pm, st, ai);
       case 2: return launch_t<BN, false, true, 13 | 32, false>(g, tm, pm, st, ai);
-      default: return launch_t<BN, true, true, 13 | 32, false>(g, tm, pm, st, ai);
+      case 3: return launch_t<BN, true, true, 13 | 32, false>(g, tm, pm, st, ai);
+      case 4: return launch_t<BN, false, false, 13 | 32, true>(g, tm, pm, st, ai);
+      case 5: return launch_t<BN, true, false, 13 | 32, true>(g, tm, pm, st, ai);
+      case 6: return launch_t<BN, false, true, 13 | 32, true>(g, tm, pm, st, ai);
+      default: return launch_t<BN, true, true, 13 | 32, true>(g, tm, pm, st, ai);
     }
   }
   const int key = (g->a_mn_major ? 1 : 0) | (g->b_mn_major ? 2 : 0) | ((mode | (w8 ? 8 : 0)) << 2) | (pc ? 64 : 0) |
@@ -727,6 +735,7 @@ static int dispatch_bn(const tofu_gemm_args* g, const CUtensorMap* tm, const Pie
     TOFU_CASES(0, 0) TOFU_CASES(1, 0) TOFU_CASES(2, 0) TOFU_CASES(3, 0) TOFU_CASES(4, 0) TOFU_CASES(5, 0)
     TOFU_CASES(8, 0) TOFU_CASES(11, 0) TOFU_CASES(13, 0)
     TOFU_CASES(0, 1) TOFU_CASES(1, 1) TOFU_CASES(2, 1) TOFU_CASES(3, 1) TOFU_CASES(4, 1) TOFU_CASES(5, 1)
+    TOFU_CASES(8, 1) TOFU_CASES(11, 1) TOFU_CASES(13, 1)
 #undef TOFU_CASES
 #undef TOFU_CASE
     default: return TOFU_ERR_ARG;

@@ -284,6 +284,10 @@ struct Exec {
   int streams = 1;         // virtual ranks: 1 (default) or 2 (TOFU_STREAMS=2); multi-process always 2
   bool fuse = true;
   bool fuse_fetch = true;  // GEMM operands read in place from their owners' shards (TOFU_PFETCH=0: staged)
+  // ... also 1x1 stride-1 convolutions' operands (TOFU_PFETCH_CONV=1).  Off by default: measured on 8 virtual
+  // ranks of one B200 (WResNet-152-4, tools/kineto_step.py) 94.7 -> 97.5 ms per step although 171 of 425
+  // staged fetch launches disappear: the fused-fetch fp32-partial GEMMs run 28 -> 41 us each
+  bool fuse_fetch_conv = false;
   struct OpAcc {  // objects (tensor alias roots; staging buffers nt, nt + 1) an op's launches touch, all ranks
     bool any_fetch = false, any_reduce = false, fetch_remote = false;
     int stage = -1;
@@ -438,6 +442,23 @@ ConvGeom conv_geom(const OpDef& d) {
   return g;
 }
 
+// A 1x1 stride-1 convolution's operands as the GEMM it runs on (conv1x1_gemm): A = param 0, the pixel-row
+// operand [b, y, x][c] (MN-major for the weight gradient); B = param 1, the weight [co][1][1][ci] (MN-major for
+// the data gradient) or, for the weight gradient, the activations [b, y, x][ci] (MN-major).  Lets the lowering
+// read those operands in place from their owners' shards (fused fetch), as for GEMM defs.
+GemmForm conv1x1_form(const ConvGeom& cg) {
+  GemmForm f;
+  if (cg.kind < 0 || cg.R != 1 || cg.s != 1 || cg.p != 0) return f;
+  f.ok = true;
+  f.a_param = 0;
+  f.b_param = 1;
+  f.a_split = 3;
+  f.a_mn = cg.kind == 2;
+  f.b_split = cg.kind == 2 ? 3 : 1;
+  f.b_mn = cg.kind != 0;
+  return f;
+}
+
 const char* kernel_kind(const OpDef& d) {
   static const std::set<std::string> ew = {"relu",  "relu_grad",  "mse_grad", "mom",  "sgd",     "mom3", "sgd3",
                                            "sumsq", "relu4",      "relu_grad4", "mom4", "sgd4", "add4", "addrelu"};
@@ -481,6 +502,7 @@ void read_env_options(Exec& E) {
   if (const char* f = std::getenv("TOFU_FUSE")) E.fuse = std::string(f) != "0";
   if (const char* f = std::getenv("TOFU_STREAMS")) E.streams = std::atoi(f) >= 2 ? 2 : 1;
   if (const char* f = std::getenv("TOFU_PFETCH")) E.fuse_fetch = std::string(f) != "0";
+  if (const char* f = std::getenv("TOFU_PFETCH_CONV")) E.fuse_fetch_conv = std::string(f) == "1";
 }
 
 void lower(Exec& E) {
@@ -590,8 +612,10 @@ void lower(Exec& E) {
           b.direct = true;
           b.off = E.lay[r].shard_off[t];
           b.buf_box = own;
-        } else if (kind == "gemm" && E.fuse_fetch && gf.ok && !aliases(t, oi.output) &&
-                   try_pieces(t, (int)pi == gf.a_param, gf, b)) {
+        } else if (E.fuse_fetch && !aliases(t, oi.output) &&
+                   ((kind == "gemm" && gf.ok && try_pieces(t, (int)pi == gf.a_param, gf, b)) ||
+                    (kind == "conv" && E.fuse_fetch_conv && pi < 2 && conv1x1_form(conv_geom(d)).ok &&
+                     try_pieces(t, pi == 0, conv1x1_form(conv_geom(d)), b)))) {
           b.direct = false;  // read in place from the owners (b.rp); no staging
           b.off = -1;
           b.buf_box = b.box;
@@ -1378,6 +1402,20 @@ void build_launches(Exec& E) {
 
 std::vector<tofu_conv_args> conv_args(Exec& E, int o, int li);
 
+// fused fetch: a GEMM operand read in place from its owners' shards (piece 0 doubles as the shape reference)
+void set_operand_pieces(const Exec& E, const Buf& X, tofu_operand_pieces& P, const void*& ptr, int& ld) {
+  std::memset(&P, 0, sizeof P);
+  P.n = (int)X.rp.size();
+  P.dim = X.rp_dim;
+  for (int i = 0; i < P.n; ++i) {
+    P.start[i] = X.rp[i].start;
+    P.ptr[i] = E.arena[X.rp[i].src] + X.rp[i].off;
+    P.ld[i] = X.rp[i].ld;
+  }
+  ptr = P.ptr[0];
+  ld = (int)P.ld[0];
+}
+
 // 1x1 stride-1 convolution as tofu_gemm_args (forward: pixels x ci . (co x ci)^T; data gradient:
 // pixels x co . (co x ci); weight gradient: (pixels x co)^T . (pixels x ci)), optimizer fused as for GEMMs.
 bool conv1x1_gemm(Exec& E, int o, int li, Exec::GemmLaunch& G) {
@@ -1410,6 +1448,14 @@ bool conv1x1_gemm(Exec& E, int o, int li, Exec::GemmLaunch& G) {
     G.a.K = (int)r0;
     G.a.a_mn_major = 1;
     G.a.b_mn_major = 1;
+  }
+  if (!P0.rp.empty()) {  // operands read in place from their owners' shards (fused fetch, conv1x1_form)
+    set_operand_pieces(E, P0, G.pa, G.a.A, G.a.lda);
+    G.a.a_pieces = &G.pa;
+  }
+  if (!P1.rp.empty()) {
+    set_operand_pieces(E, P1, G.pb, G.a.B, G.a.ldb);
+    G.a.b_pieces = &G.pb;
   }
   const int64_t ec = O.dtype == TOFU_BF16 ? 2 : 4;
   G.a.C = base + O.off + offo * ec;
@@ -1502,18 +1548,8 @@ void finalize(Exec& E) {
       G.a.B = E.arena[r] + B.off + boff * 2;
       G.a.ldb = (int)ldb;
       G.a.b_mn_major = gf.b_mn ? 1 : 0;
-      // fused fetch: operands read in place from their owners' shards (piece 0 doubles as the shape reference)
       auto set_pieces = [&](const Buf& X, tofu_operand_pieces& P, const void*& ptr, int& ld) {
-        std::memset(&P, 0, sizeof P);
-        P.n = (int)X.rp.size();
-        P.dim = X.rp_dim;
-        for (int i = 0; i < P.n; ++i) {
-          P.start[i] = X.rp[i].start;
-          P.ptr[i] = E.arena[X.rp[i].src] + X.rp[i].off;
-          P.ld[i] = X.rp[i].ld;
-        }
-        ptr = P.ptr[0];
-        ld = (int)P.ld[0];
+        set_operand_pieces(E, X, P, ptr, ld);
       };
       if (!A.rp.empty()) {
         set_pieces(A, G.pa, G.a.A, G.a.lda);
@@ -1572,16 +1608,24 @@ void finalize(Exec& E) {
       {  // a 1x1 stride-1 convolution is a plain GEMM over pixel rows: the TMA-fed tcgen05 GEMM when every
          // operand is a row block of its buffer (else the gather kernel)
         Exec::GemmLaunch G;
+        const bool fused = !L.in[0].rp.empty() || (L.in.size() > 1 && !L.in[1].rp.empty());
         if (conv1x1_gemm(E, (int)o, li, G)) {
           G.a.splits = 0;
           G.a.ws = pass == 0 ? reinterpret_cast<void*>(uintptr_t(1) << 20) : E.ws_dev;
           G.a.sk_ws = E.sk_dev;
           if (tofu_gemm_plan_tmaps(&G.a, G.tm, &G.bn) == TOFU_OK) {  // else: the convolution kernel below
             ws_need = std::max<int64_t>(ws_need, tofu_gemm_workspace_bytes(&G.a));
-            if (pass == 1) E.gemms[{(int)o, li}] = G;
+            if (pass == 1) {
+              Exec::GemmLaunch& S = E.gemms[{(int)o, li}];
+              S = G;  // (re-point the piece tables at the stored copies)
+              if (S.a.a_pieces) S.a.a_pieces = &S.pa;
+              if (S.a.b_pieces) S.a.b_pieces = &S.pb;
+            }
             continue;
           }
         }
+        // (the convolution kernel reads staged or owned operands only)
+        if (fused) throw Error(TOFU_ERR_ARG, "fused-fetch 1x1 convolution " + g.ops[o].name + " has no GEMM form");
       }
       std::vector<Exec::ConvLaunch> cls;
       for (auto& a : conv_args(E, (int)o, li)) {

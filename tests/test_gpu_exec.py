@@ -225,6 +225,35 @@ def test_fused_fetch_equals_staged_fetch(cfg, k, monkeypatch):
         assert np.array_equal(outs["0"][t], outs["1"][t]), t
 
 
+@pytest.mark.parametrize("k", [4])
+def test_fused_fetch_of_1x1_convolutions_equals_staged(k, monkeypatch):
+    """The fused MultiFetch for 1x1 stride-1 convolutions (TOFU_PFETCH_CONV=1: their pixel-row / weight
+    operands read in place from the owners' shards by the GEMM they run on, exec.cpp conv1x1_form) vs the
+    staged MultiFetch: bitwise equal results on a small WResNet, ledger == plan, fewer fetch launches, and
+    convolution launches that read peer shards in place."""
+    from paper_1807_08887_b200.runner import TofuRunner
+    from tofu_inputs.graphs import wresnet
+    spec = wresnet([2, 1], 2, 8, 64, base=16, classes=24)
+    vals = make_values(spec, seed=43, mode="bf16")
+    outs, fetches, inplace = {}, {}, {}
+    for pf in ("0", "1"):
+        monkeypatch.setenv("TOFU_PFETCH_CONV", pf)
+        R = TofuRunner(spec, k)
+        R.load(vals)
+        R.step()
+        torch.cuda.synchronize()
+        descs = [R.exec.launch_desc(i) for i in range(R.exec.num_launches())]
+        fetches[pf] = sum(d["kind"] == "fetch" for d in descs)
+        inplace[pf] = sum(d.get("inplace_remote_operands", 0) for d in descs if "conv" in (d["def"] or ""))
+        assert R.ledger() == R.plan.cost()
+        outs[pf] = {t: R.gather(t).float().cpu().numpy() for t in spec["tensors"]}
+        del R
+    assert inplace["0"] == 0 and inplace["1"] > 0
+    assert fetches["1"] < fetches["0"]
+    for t in spec["tensors"]:
+        assert np.array_equal(outs["0"][t], outs["1"][t]), t
+
+
 @pytest.mark.parametrize("fuse", ["0", "1"])
 def test_constants_come_from_the_tdl_text(fuse, monkeypatch):
     """Learning rate, momentum and loss scale are read from the defs' TDL literals (kernel_match.cpp), not
