@@ -405,11 +405,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int m = m0 + q * 32 + lane;
         char* rowp = nullptr;
         int64_t erow = 0;
+        // split-K (few-tile launches): this K range's fp32 partial goes to plane sp of the workspace, dense
+        // [M][N]; splitk_reduce_rows sums the planes in split order and applies the epilogue
+        float* prow = nullptr;
         if (m < M) {
-          const int gb = m / ngyx, rem = m - gb * ngyx;
-          const int gy = rem / a.ngx, gx = rem - gy * a.ngx;
-          erow = (int64_t)gb * a.c_sb + (int64_t)(a.c_ys * gy + a.c_y0) * a.c_sy + (int64_t)(a.c_xs * gx + a.c_x0) * a.c_sx;
-          rowp = reinterpret_cast<char*>(a.C) + erow * (MODE == 0 ? 2 : 4);
+          if (KIND == 0 && splits > 1) {
+            prow = reinterpret_cast<float*>(a.ws) + ((int64_t)sp * M + m) * N;
+          } else {
+            const int gb = m / ngyx, rem = m - gb * ngyx;
+            const int gy = rem / a.ngx, gx = rem - gy * a.ngx;
+            erow = (int64_t)gb * a.c_sb + (int64_t)(a.c_ys * gy + a.c_y0) * a.c_sy + (int64_t)(a.c_xs * gx + a.c_x0) * a.c_sx;
+            rowp = reinterpret_cast<char*>(a.C) + erow * (MODE == 0 ? 2 : 4);
+          }
         }
         // fused element-wise operands of this row's chunk, prefetched one chunk ahead (64 B each)
         uint4 xa[4], xm[4];
@@ -450,6 +457,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (c == NCH - 1 && lane == 0)
             for (int cc = blockIdx.x + 1; cc < cend; ++cc) *sk_flag(sk_ws, gridDim.x, cc, q) = 0;
           const int n = n0 + c * 32;
+          if (KIND == 0 && prow) {  // split-K partial (N % 8 == 0, checked by the host)
+            if (n < N) {
+              float* o = prow + n;
+              if (n + 32 <= N) {
+#pragma unroll
+                for (int v = 0; v < 8; ++v)
+                  reinterpret_cast<float4*>(o)[v] = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                                                __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+              } else {
+#pragma unroll
+                for (int e = 0; e < 32; ++e)
+                  if (e < N - n) o[e] = __uint_as_float(r[e]);
+              }
+            }
+            continue;
+          }
           if (!rowp || n >= N) continue;
           if (MODE == 0 && a.ep && n + 32 <= N) {
             // fused element-wise consumers (DESIGN R8/R13): v = acc (+ add), relu, zero where mask <= 0
@@ -704,6 +727,70 @@ __global__ void __launch_bounds__(256) splitk_reduce(const float* __restrict__ w
   }
 }
 
+// Split-K reduction of a few-tile forward / data-gradient launch: out(m, n) = epilogue(Σ_s WS[s][m][n]) in split
+// order, written through the output's row layout (c_sb / c_sy / c_sx, stride-2 phase offsets) with the fused
+// element-wise consumers of c_mode 0 (add, relu, mask; bf16) or the fp32 store of c_mode 1.  One thread per
+// (row, 8 channels).
+__global__ void __launch_bounds__(256) splitk_reduce_rows(Params P) {
+  tofu::pdl_trigger();
+  tofu::pdl_wait();
+  const tofu_conv_args& a = P.a;
+  const int ngyx = a.ngy * a.ngx;
+  const int M = P.M, N = P.N, n8 = N / 8;
+  const int64_t plane = (int64_t)M * N, total = (int64_t)M * n8;
+  const float* ws = reinterpret_cast<const float*>(a.ws);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i / n8), n = (int)(i - (int64_t)m * n8) * 8;
+    const float* w0 = ws + (int64_t)m * N + n;
+    float4 lo = reinterpret_cast<const float4*>(w0)[0], hi = reinterpret_cast<const float4*>(w0)[1];
+    for (int sp = 1; sp < P.splits; ++sp) {
+      const float4 l2 = reinterpret_cast<const float4*>(w0 + sp * plane)[0];
+      const float4 h2 = reinterpret_cast<const float4*>(w0 + sp * plane)[1];
+      lo.x += l2.x; lo.y += l2.y; lo.z += l2.z; lo.w += l2.w;
+      hi.x += h2.x; hi.y += h2.y; hi.z += h2.z; hi.w += h2.w;
+    }
+    float f[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    const int gb = m / ngyx, rem = m - gb * ngyx;
+    const int gy = rem / a.ngx, gx = rem - gy * a.ngx;
+    const int64_t erow =
+        (int64_t)gb * a.c_sb + (int64_t)(a.c_ys * gy + a.c_y0) * a.c_sy + (int64_t)(a.c_xs * gx + a.c_x0) * a.c_sx;
+    if (a.c_mode == 1) {
+      float* o = reinterpret_cast<float*>(a.C) + erow + n;
+      reinterpret_cast<float4*>(o)[0] = make_float4(f[0], f[1], f[2], f[3]);
+      reinterpret_cast<float4*>(o)[1] = make_float4(f[4], f[5], f[6], f[7]);
+      continue;
+    }
+    if (a.ep & 2) {
+      const uint4 u = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.aux_add) + erow + n);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 x = __bfloat1622float2(h[e]);
+        f[2 * e] += x.x;
+        f[2 * e + 1] += x.y;
+      }
+    }
+    if (a.ep & 1)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) f[e] = fmaxf(f[e], 0.f);
+    if (a.ep & 4) {
+      const uint4 u = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.aux_mask) + erow + n);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 x = __bfloat1622float2(h[e]);
+        if (!(x.x > 0.f)) f[2 * e] = 0.f;
+        if (!(x.y > 0.f)) f[2 * e + 1] = 0.f;
+      }
+    }
+    uint4 w;
+    __nv_bfloat162* wh = reinterpret_cast<__nv_bfloat162*>(&w);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) wh[e] = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.C) + erow + n) = w;
+  }
+}
+
 // zero output rows of a kind-0 sub-op with no taps (e.g. the odd phases of a 1x1 stride-2 data gradient):
 // one thread per (row, 8 channels), 16-byte stores (N % 8 == 0 and 16-byte aligned rows, checked by the host)
 __global__ void __launch_bounds__(256) zero_rows(Params P) {
@@ -864,6 +951,23 @@ static bool sk_enabled() {  // TOFU_SK=0 turns stream-K off (A/B measurements)
   return on;
 }
 
+// Split-K for few-tile forward / data-gradient launches (a rank's sub-op under a k-way plan, e.g. the 3x3
+// convolutions of WResNet-152-4 at k = 8: [3136 x 512] = 50 tiles of 256 with K = 4608): each split writes an
+// fp32 partial plane, splitk_reduce_rows sums them and applies the epilogue.  Only with a caller workspace
+// (the executor's; one-shot calls keep one pass).  Measured: see DESIGN.md.  TOFU_CONV_SPLIT0=0 turns it off.
+static int auto_splits0(const tofu_conv_args* a, int tiles, int K) {
+  static const bool on = [] {
+    const char* e = getenv("TOFU_CONV_SPLIT0");
+    return !(e && e[0] == '0');
+  }();
+  const int nk = (K + BK - 1) / BK;
+  if (!on || !a->ws || a->direct || a->n_out % 8 || a->c_mode > 1 || tiles * 2 > g_sms || nk < 16) return 1;
+  int sp = g_sms / tiles;
+  if (sp > nk / 8) sp = nk / 8;
+  if (sp > 8) sp = 8;
+  return sp < 2 ? 1 : sp;
+}
+
 static int auto_splits(const tofu_conv_args* a, int M, int N, int K, int bn) {
   if (a->kind != 1 || a->splits == 1) return 1;
   const int nk = (K + BK - 1) / BK;
@@ -970,7 +1074,7 @@ using namespace tofu::conv;
 extern "C" int64_t tofu_conv_workspace_bytes(const tofu_conv_args* a) {
   int M, N, K;
   dims_of(a, M, N, K);
-  return a->kind == 1 && a->splits > 1 ? (int64_t)a->splits * M * N * 4 : 0;
+  return a->splits > 1 ? (int64_t)a->splits * M * N * 4 : 0;
 }
 
 // tmaps: 4 x CUtensorMap (dense operand, C, D, split-K workspace)
@@ -1094,7 +1198,8 @@ extern "C" int tofu_conv_plan(tofu_conv_args* a, void* tmaps) {
       return !(e && e[0] == '0');
     }();
     const int dp_tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
-    if (req != -1 && c2_env() != 0 && a->im2col && !a->b_mn_major && bn == 256 && M > BM &&
+    a->splits = auto_splits0(a, dp_tiles, K);
+    if (a->splits <= 1 && req != -1 && c2_env() != 0 && a->im2col && !a->b_mn_major && bn == 256 && M > BM &&
         (req == 4 || c2_env() == 1 || (fwd_c2 && (c2_few || dp_tiles >= g_sms)))) {
       if (tmap2(&tm[0], a->Bp, BF, 2, a->b_cols, a->b_rows, a->ldb, 64, bn / 2, SW128)) return TOFU_ERR_CUDA;
       a->cl2 = 3;
@@ -1170,7 +1275,14 @@ extern "C" int tofu_conv_launch_planned(const tofu_conv_args* a, const void* tma
     tofu::launch_k(zero_rows, dim3(blocks), dim3(256), 0, st, 1, P);
     return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
   }
-  if (a->kind == 0) return dispatch(P, tm, a->c_mode, st);
+  if (a->kind == 0) {
+    const int rc = dispatch(P, tm, a->c_mode, st);
+    if (rc || P.splits <= 1) return rc;
+    int blocks = (int)(((int64_t)M * (N / 8) + 255) / 256);
+    if (blocks > g_sms * 8) blocks = g_sms * 8;
+    tofu::launch_k(splitk_reduce_rows, dim3(blocks), dim3(256), 0, st, 1, P);
+    return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
+  }
   if (P.splits > 1) {
     const CUtensorMap tw[5] = {tm[0], tm[3], tm[3], tm[3], tm[4]};
     int rc = dispatch(P, tw, 4, st);

@@ -1934,7 +1934,7 @@ int64_t kernels_of(const Exec& E, int o, int li) {
       const int64_t pix = (int64_t)a.nb * a.ngy * a.ngx;
       const int64_t M = a.kind == 0 ? pix : a.m_out, N = a.kind == 0 ? a.n_out : (int64_t)a.ntaps * a.nch;
       if (M == 0 || N == 0) continue;
-      n += 1 + (a.kind == 1 && a.splits > 1 && !a.direct ? 1 : 0);
+      n += 1 + (a.splits > 1 && !a.direct ? 1 : 0);
     }
     return n;
   }

@@ -53,10 +53,28 @@ def args(kind, S, out, Bmat=None, mn=0, flip=False):
     return a
 
 
+SKWS = torch.zeros(tofu.sk_workspace_bytes(), dtype=torch.uint8, device=dev) if os.environ.get("SK") == "1" else None
+
+
 def timeit(a, n=20):
+    if SKWS is not None:  # stream-K workspace (as the executor passes): few-tile launches may spread their K loop
+        a.sk_ws = SKWS.data_ptr()
     for _ in range(3):
         tofu.conv(a)
     torch.cuda.synchronize()
+    if os.environ.get("GRAPH") == "1":  # device time without the per-call host planning (tensor maps)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(n):
+                tofu.conv(a, stream=torch.cuda.current_stream())
+        g.replay()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        g.replay()
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / n
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for _ in range(n):
@@ -77,6 +95,6 @@ for name, a in [("fwd  (B K-major)", args(0, X, Y, W, 0)),
                 ("dgrad(B MN-major)", args(0, X, Y, W, 1, flip=True)),
                 ("dgrad(B K-major, W^T)", args(0, X, Y, WT, 0, flip=True)),
                 ("dgrad(W^T) + mask epilogue", dm),
-                ("wgrad", args(1, X, dW))]:
+                ] + ([] if os.environ.get("GRAPH") == "1" else [("wgrad", args(1, X, dW))]):
     ms = timeit(a)
     print(f"{name:24s} {ms * 1e3:8.1f} us  {flops / ms / 1e9:7.1f} TF/s")
