@@ -402,7 +402,9 @@ typedef struct {
  * rank-4 piece, > 2^32 rows), TOFU_ERR_SPACE (cap < *ntasks; the first cap tasks are written). */
 int tofu_pieces_tasks(tofu_piece* pieces, int n, tofu_piece_task* tasks, int64_t cap, int64_t* ntasks);
 /* Device: run ntasks tasks over pieces (both device arrays, caller-owned, as tofu_pieces_tasks left them).
- * all_raw != 0 (every task's pad_ == 1) selects the plain-copy kernel (16-byte moves, high occupancy). */
+ * all_raw == 1 (every task's pad_ == 1) selects the plain-copy kernel (16-byte moves, high occupancy);
+ * all_raw == 2 the many-source kernel (every source's vector in flight at once, one CTA per SM: for
+ * reductions of >= 4 sources); 0 the general kernel.  Every kernel sums the sources in index order. */
 int tofu_pieces_run(const tofu_piece* pieces_dev, const tofu_piece_task* tasks_dev, int64_t ntasks, int all_raw,
                     void* stream);
 

@@ -155,7 +155,7 @@ __device__ __forceinline__ void store_f(void* p, int64_t i, int dt, const float 
 // <= kSeg vectors; segment q is (row q / nseg, vectors [(q % nseg) * kSeg, ...)).  Warp w of the CTA takes
 // segments q0 + w, q0 + w + nwarps, ...: the row's (c0, c1, c2) is decoded once per segment, then the lanes
 // stride over its vectors, kUnr vectors per lane in flight (loads of every source issued before the stores).
-template <int V>
+template <int V, bool WIDE>
 __device__ __forceinline__ void run_task(const tofu_piece& pc, int64_t q0, int64_t nq) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int64_t rv = pc.extent[3] / V;
@@ -173,6 +173,53 @@ __device__ __forceinline__ void run_task(const tofu_piece& pc, int64_t q0, int64
     const uint32_t c0 = row / e1;
     const int64_t sb = c0 * pc.src_stride[0] + c1 * pc.src_stride[1] + c2 * pc.src_stride[2];
     const int64_t db = c0 * pc.dst_stride[0] + c1 * pc.dst_stride[1] + c2 * pc.dst_stride[2];
+    if constexpr (WIDE) {
+      // every source's vector (and the consumer's operands) in flight at once: one DRAM / NVLink round trip
+      // per vector instead of one per source; the sum still runs in rank order (bitwise as the other path).
+      // ~210 registers: one 256-thread CTA per SM (pieces_kernel_wide), used for launches of >= 4 sources
+      for (int64_t j = jb + lane; j < je; j += 32) {
+        float xs[TOFU_MAX_SRC][V];
+#pragma unroll
+        for (int k = 0; k < TOFU_MAX_SRC; ++k)
+          if (k < nsrc) load_f<V>(pc.src[k], sb + j * V, sdt, xs[k]);
+        float a[V], m[V];
+        if (ep == TOFU_PIECE_MOM_SGD) {
+          load_f<V>(pc.dst, db + j * V, TOFU_F32, m);
+          load_f<V>(pc.aux0, db + j * V, TOFU_BF16, a);
+        } else if (ep != TOFU_PIECE_COPY && ep != TOFU_PIECE_RELU) {
+          load_f<V>(pc.aux0, db + j * V, TOFU_BF16, a);
+        }
+        float acc[V];
+#pragma unroll
+        for (int q = 0; q < V; ++q) acc[q] = xs[0][q];
+#pragma unroll
+        for (int k = 1; k < TOFU_MAX_SRC; ++k)
+          if (k < nsrc)
+#pragma unroll
+            for (int q = 0; q < V; ++q) acc[q] += xs[k][q];
+        if (ep == TOFU_PIECE_RELU) {
+#pragma unroll
+          for (int q = 0; q < V; ++q) acc[q] = fmaxf(acc[q], 0.f);
+        } else if (ep == TOFU_PIECE_MOM_SGD) {
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            m[q] = m[q] * pc.s0 + acc[q];
+            a[q] = a[q] - m[q] * pc.s1;
+            acc[q] = m[q];
+          }
+          store_f<V>(pc.aux0, db + j * V, TOFU_BF16, a);
+        } else if (ep != TOFU_PIECE_COPY) {
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            if (ep == TOFU_PIECE_MASK) acc[q] = a[q] > 0.f ? acc[q] : 0.f;
+            else if (ep == TOFU_PIECE_ADD) acc[q] = acc[q] + a[q];
+            else acc[q] = fmaxf(acc[q] + a[q], 0.f);
+          }
+        }
+        store_f<V>(pc.dst, db + j * V, ddt, acc);
+      }
+      continue;
+    }
     for (int64_t j0 = jb + lane; j0 < je; j0 += 32 * kUnrC) {
       float acc[kUnrC][V];
 #pragma unroll
@@ -275,20 +322,31 @@ __global__ void __launch_bounds__(256) pieces_copy_kernel(const tofu_piece* __re
   }
 }
 
-__global__ void __launch_bounds__(256, TOFU_PIECES_MINB) pieces_kernel(const tofu_piece* __restrict__ pieces,
-                                                     const tofu_piece_task* __restrict__ tasks, int ntasks) {
+template <bool WIDE>
+__device__ __forceinline__ void pieces_body(const tofu_piece* __restrict__ pieces,
+                                            const tofu_piece_task* __restrict__ tasks, int ntasks) {
   tofu::pdl_trigger();
   tofu::pdl_wait();
   for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
     const tofu_piece_task T = tasks[t];
     const tofu_piece& pc = pieces[T.piece];
     switch (pc.pad_) {
-      case 8: run_task<8>(pc, T.q0, T.nq); break;
-      case 4: run_task<4>(pc, T.q0, T.nq); break;
-      case 2: run_task<2>(pc, T.q0, T.nq); break;
-      default: run_task<1>(pc, T.q0, T.nq); break;
+      case 8: run_task<8, WIDE>(pc, T.q0, T.nq); break;
+      case 4: run_task<4, WIDE>(pc, T.q0, T.nq); break;
+      case 2: run_task<2, WIDE>(pc, T.q0, T.nq); break;
+      default: run_task<1, WIDE>(pc, T.q0, T.nq); break;
     }
   }
+}
+__global__ void __launch_bounds__(256, TOFU_PIECES_MINB) pieces_kernel(const tofu_piece* __restrict__ pieces,
+                                                     const tofu_piece_task* __restrict__ tasks, int ntasks) {
+  pieces_body<false>(pieces, tasks, ntasks);
+}
+// Measured (tools/pieces_bench.py, graph replay): 8 x fp32 -> bf16 [1024 x 4096] 47.0 -> 29.2 us (3.0 -> 4.9 TB/s),
+// 4 x fp32 -> bf16 [12544 x 1024] 68.9 -> 59.7 us; 2 sources slower (19.0 -> 32.2 us): launches of >= 4 sources only
+__global__ void __launch_bounds__(256, 1) pieces_kernel_wide(const tofu_piece* __restrict__ pieces,
+                                                          const tofu_piece_task* __restrict__ tasks, int ntasks) {
+  pieces_body<true>(pieces, tasks, ntasks);
 }
 
 }  // namespace tofu
@@ -371,9 +429,12 @@ extern "C" int tofu_pieces_run(const tofu_piece* pieces_dev, const tofu_piece_ta
   if (ntasks <= 0) return TOFU_OK;
   const int64_t grid = std::min<int64_t>(ntasks, 148 * 8);
   const int n = (int)std::min<int64_t>(ntasks, INT32_MAX);
-  if (all_raw)
+  if (all_raw == 1)
     tofu::launch_k(tofu::pieces_copy_kernel, dim3((unsigned)grid), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 1,
                    pieces_dev, tasks_dev, n);
+  else if (all_raw == 2)
+    tofu::launch_k(tofu::pieces_kernel_wide, dim3((unsigned)std::min<int64_t>(ntasks, 148)), dim3(256), 0,
+                   reinterpret_cast<cudaStream_t>(stream), 1, pieces_dev, tasks_dev, n);
   else
     tofu::launch_k(tofu::pieces_kernel, dim3((unsigned)grid), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 1,
                    pieces_dev, tasks_dev, n);

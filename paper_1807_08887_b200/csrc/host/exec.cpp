@@ -251,7 +251,7 @@ struct Exec {
     std::vector<int> waits;   // launches on the other stream this one waits for (their events)
     bool rec = false;         // record this launch's event (a launch on the other stream waits for it)
     int64_t task_off = 0, ntasks = 0;  // fetch / reduce: tofu_piece_task range (tofu_pieces_tasks)
-    int all_raw = 0;                   // every task a plain copy (the copy kernel)
+    int all_raw = 0;                   // 1: every task a plain copy (the copy kernel); 2: >= 4 sources
   };
   std::vector<Launch> launches;
   tofu_piece* pieces_dev = nullptr;
@@ -1392,6 +1392,9 @@ void build_launches(Exec& E) {
     if (rc) throw Error(rc, "tofu_pieces_tasks failed");
     L.all_raw = 1;
     for (int64_t q = 0; q < nt; ++q) L.all_raw &= E.host_tasks[L.task_off + q].pad_ == 1;
+    int maxsrc = 0;
+    for (int64_t pq = L.piece_off; pq < L.piece_off + L.npieces; ++pq) maxsrc = std::max(maxsrc, host[pq].nsrc);
+    if (!L.all_raw && maxsrc >= 4) L.all_raw = 2;  // many-source reduce kernel (tofu_pieces_run)
   }
   E.host_pieces = std::move(host);
   int64_t n = 0;

@@ -59,8 +59,11 @@ def _case(rng, n_pieces):
     return pieces, refs, keep
 
 
+@pytest.mark.parametrize("wide", [False, True])
 @pytest.mark.parametrize("seed", range(6))
-def test_pieces_copy_and_ordered_sum(seed):
+def test_pieces_copy_and_ordered_sum(seed, wide):
+    """wide: the many-source kernel (tofu_pieces_run all_raw = 2: every source's vector in flight at once) on
+    the same pieces, bitwise equal to the ordered sum as the general kernel."""
     rng = random.Random(seed)
     pieces, refs, keep = _case(rng, rng.randint(1, 12))
     tasks, nt = tofu.pieces_tasks(pieces)
@@ -68,7 +71,8 @@ def test_pieces_copy_and_ordered_sum(seed):
     td = torch.empty(max(C.sizeof(tasks), 1), dtype=torch.uint8, device="cuda")
     pd.copy_(torch.frombuffer(bytearray(bytes(pieces)), dtype=torch.uint8))
     td.copy_(torch.frombuffer(bytearray(bytes(tasks)), dtype=torch.uint8)[:td.numel()])
-    tofu.pieces_run(pd.data_ptr(), td.data_ptr(), nt, int(all(tasks[i].pad_ == 1 for i in range(nt))))
+    raw = int(all(tasks[i].pad_ == 1 for i in range(nt)))
+    tofu.pieces_run(pd.data_ptr(), td.data_ptr(), nt, 2 if wide and not raw else raw)
     torch.cuda.synchronize()
     for dbig, dsl, ref in refs:
         exp = torch.zeros_like(dbig)

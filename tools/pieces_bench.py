@@ -32,12 +32,20 @@ def run(name, shape, box, nsrc=1, sdt=0, ddt=0, reps=20):
     tasks, nt = tofu.pieces_tasks(ps)
     pd = torch.frombuffer(bytearray(bytes(ps)), dtype=torch.uint8).cuda()
     td = torch.frombuffer(bytearray(bytes(tasks)), dtype=torch.uint8).cuda()
+    raw = int(all(tasks[i].pad_ == 1 for i in range(nt)))  # (host work kept out of the timed loop)
+    if not raw and nsrc >= 4:
+        raw = 2  # the many-source kernel (as the executor picks it)
     for _ in range(3):
-        tofu.pieces_run(pd.data_ptr(), td.data_ptr(), nt, int(all(tasks[i].pad_ == 1 for i in range(nt))))
+        tofu.pieces_run(pd.data_ptr(), td.data_ptr(), nt, raw)
+    g = torch.cuda.CUDAGraph()  # graph replay: device time only, no per-call host cost
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            tofu.pieces_run(pd.data_ptr(), td.data_ptr(), nt, raw, stream=torch.cuda.current_stream())
+    g.replay()
+    torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for _ in range(reps):
-        tofu.pieces_run(pd.data_ptr(), td.data_ptr(), nt, int(all(tasks[i].pad_ == 1 for i in range(nt))))
+    g.replay()
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / reps
@@ -54,3 +62,5 @@ run("channel slice [32,56,56,64 of 256]", [32, 56, 56, 256], [(0, 32), (0, 56), 
 run("halo rows [32,28+2 of 56,56,256]", [32, 56, 56, 256], [(0, 32), (27, 57 - 1), (0, 56), (0, 256)])
 run("reduce 8 x fp32 -> bf16 [1024,4096]", [1024, 4096], [(0, 1024), (0, 4096)], nsrc=8, sdt=1, ddt=0)
 run("reduce 2 x fp32 -> fp32 [2048,2048]", [4096, 4096], [(0, 4096), (1024, 3072)], nsrc=2, sdt=1, ddt=1)
+run("reduce 8 x fp32 -> bf16 [3136,512]", [3136, 512], [(0, 3136), (0, 512)], nsrc=8, sdt=1, ddt=0)
+run("reduce 4 x fp32 -> bf16 [12544,1024]", [12544, 1024], [(0, 12544), (0, 1024)], nsrc=4, sdt=1, ddt=0)
