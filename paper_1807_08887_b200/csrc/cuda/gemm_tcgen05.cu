@@ -934,7 +934,10 @@ extern "C" int tofu_gemm_plan_tmaps(tofu_gemm_args* g, void* tmaps, int* bn_out)
       const char* e = getenv("TOFU_C2W8");
       return e && e[0] == '1';
     }();
-    const bool c2 = ok && (req == 4 || (req == 0 && env2 != 0 && (env2 == 1 || c2w8 || !wants_w8(g))));
+    // (8-warp epilogues pair too from K = 1024: measured with the issue-lean epilogue, tools/ep_stream_bench.py,
+    // [100352 x 256 x 1024] + mask 66.2 -> 60.7 us, [6272 x 4096 x 1024] + add + mask 60.8 -> 54.8 us; shorter K
+    // loses: K = 512 74.4 -> 78.7 us, K = 256 112 -> 137 us)
+    const bool c2 = ok && (req == 4 || (req == 0 && env2 != 0 && (env2 == 1 || c2w8 || !wants_w8(g) || g->K >= 1024)));
     g->cl2 = c2 ? 3 : ok && (env == 1 || req == 2 || cl2_auto(g)) ? 1 : 0;
   }
   CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(tmaps);
