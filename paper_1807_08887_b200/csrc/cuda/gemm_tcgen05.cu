@@ -839,7 +839,8 @@ static int auto_splits(const tofu_gemm_args* g, int bn) {
   const int tiles = ((g->M + BM - 1) / BM) * ((g->N + bn - 1) / bn);
   if (tiles * 2 > g_num_sms || nk < 8) return 1;
   int sp = g_num_sms / tiles;
-  if (sp > nk / 4) sp = nk / 4;
+  const bool skinny = g->M <= 256 && g->K <= 8192;  // (see tofu_gemm_plan_tmaps: >= 8 k-blocks per split)
+  if (sp > nk / (skinny ? 8 : 4)) sp = nk / (skinny ? 8 : 4);
   if (sp > 16) sp = 16;
   return sp < 2 ? 1 : sp;
 }
@@ -891,9 +892,14 @@ extern "C" int tofu_gemm_plan_tmaps(tofu_gemm_args* g, void* tmaps, int* bn_out)
     const char* e = getenv("TOFU_GEMM_FEW");
     return e ? atoi(e) : 1;
   }();
+  // Skinny (M <= 256) few-tile launches with K <= 8192 — a rank's per-timestep recurrent GEMMs under an
+  // 8-way plan, [128 x 2048 x 4096] / [128 x 4096 x 2048] — take 128-wide tiles AND split-K with >= 8 k-blocks
+  // per split (auto_splits): device time incl. the reduction (graph replay, tools/small_gemm_sweep.py)
+  // 13.0 -> 9.9 us and 11.1 -> 9.4 us against 256-wide tiles with 16 / 8 splits.
+  const bool skinny = g->M <= 256 && g->K <= 8192;
   if (few && g->bn == 0 && g->splits == 0 && !g->ep && bn == 256 &&
       2 * ((g->M + BM - 1) / BM) * ((g->N + 255) / 256) <= g_num_sms &&
-      (few != 1 || 2 * ((g->M + BM - 1) / BM) * ((g->N + 127) / 128) > g_num_sms)) {
+      (few != 1 || skinny || 2 * ((g->M + BM - 1) / BM) * ((g->N + 127) / 128) > g_num_sms)) {
     if (few == 1) bn = 128;
     if (few == 2 && g->sk_ws) g->splits = -1;
   }

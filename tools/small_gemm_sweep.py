@@ -11,13 +11,20 @@ from paper_1807_08887_b200 import tofu  # noqa: E402
 
 
 def bench(fn, reps=50):
+    """device time per call: a CUDA graph of reps calls (the per-call host work, tensor-map encoding and ctypes,
+    outlasts these kernels and would otherwise be what is timed)"""
     for _ in range(5):
         fn()
     torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
     s, e = torch.cuda.Event(True), torch.cuda.Event(True)
     s.record()
-    for _ in range(reps):
-        fn()
+    g.replay()
     e.record()
     torch.cuda.synchronize()
     return s.elapsed_time(e) / reps * 1e3
@@ -30,7 +37,8 @@ for name, (M, N, K, am, bm) in {"gate": (128, 2048, 4096, 0, 1), "mm_rec": (128,
     for bn in (128, 256):
         for sp in (1, 2, 4, 8, 16, 32):
             try:
-                t = bench(lambda: tofu.gemm(a, b, c, M, N, K, a.shape[1], am, b.shape[1], bm, N, 0, bn=bn, splits=sp))
+                t = bench(lambda: tofu.gemm(a, b, c, M, N, K, a.shape[1], am, b.shape[1], bm, N, 0, bn=bn, splits=sp,
+                                            stream=torch.cuda.current_stream()))
             except Exception as ex:  # noqa: BLE001
                 print(name, bn, sp, "error", ex)
                 continue
