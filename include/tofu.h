@@ -228,6 +228,10 @@ typedef struct {
    * CTA staging its A rows and half of B).  On entry -1 forbids both, 2 requests the multicast pairs and 4 the
    * 2-CTA MMA where eligible (parity tests), 0 = automatic */
   int cl2;
+  /* 1 = with split-K (splits > 1), leave the fp32 partial planes in ws ([splits][M][N], dense) and skip the
+   * ordered reduction: the caller's next launch reduces them (the executor's gate GEMM + LSTM cell fusion).
+   * 0 = C holds the result when the call returns (stream order). */
+  int defer_reduce;
 } tofu_gemm_args;
 int tofu_gemm_bf16(const tofu_gemm_args* args, void* stream);
 /* Split form used by the executor: encode the TMA descriptors (A, B, C, D, workspace, mask, then the

@@ -1055,7 +1055,7 @@ extern "C" int tofu_gemm_launch_planned(const tofu_gemm_args* g, const void* tma
     tofu_gemm_args p = *g;
     p.c_mode = 4;
     int rc = bn == 256 ? dispatch_bn<256>(&p, tw, pm, st) : dispatch_bn<128>(&p, tw, pm, st);
-    if (rc) return rc;
+    if (rc || g->defer_reduce) return rc;  // (defer_reduce: the caller reduces the planes)
     const int64_t n = (int64_t)g->M * g->N / 4 + 1;
     int blocks = (int)((n + 255) / 256);
     if (blocks > g_num_sms * 8) blocks = g_num_sms * 8;

@@ -14,6 +14,7 @@
 // operand allows it, else V = 1).
 #include <cuda_bf16.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -38,6 +39,15 @@ struct LstmArgs {
   void* out2;  // fused second output: h (kind 4) or dC (kind 5)
   int64_t out2_ld;
   int out2_dt;
+  // gate GEMM + cell fusion (kinds 0 / 4): GH comes as the GEMM's fp32 split-K partial planes (dense
+  // [splits][nb][ng * nh], plane stride gh_plane, row pitch gh_wld, gate stride gh_wgs), summed in split order
+  // (the GEMM's own reduction), rounded to GH's dtype, stored to GH (gh_out) and used as stored
+  const float* ghws;
+  int gh_splits;
+  int64_t gh_plane, gh_wld, gh_wgs;
+  void* gh_out;
+  int64_t gh_out_ld, gh_out_gs;
+  int gh_out_dt;
 };
 
 template <int V>
@@ -104,7 +114,33 @@ __device__ __forceinline__ void stv(void* p, int dt, int64_t i, const float (&v)
 
 __device__ __forceinline__ float sig(float x) { return 1.f / (1.f + __expf(-x)); }
 
-template <int V>
+template <int V, bool SPLIT>
+__device__ __forceinline__ void ld_gh(const LstmArgs& a, int64_t b, int64_t h, int x, float (&t)[V]) {
+  if constexpr (!SPLIT) {
+    ldv<V>(a.gh, b * a.gh.ld + h + x * a.gh.gs, t);
+    return;
+  }
+  const int64_t wo = b * a.gh_wld + x * a.gh_wgs + h;
+  // the planes' vectors in flight 8 at a time, summed in split order (the GEMM's own reduction order)
+  constexpr int kBatch = 8;
+  for (int s0 = 0; s0 < a.gh_splits; s0 += kBatch) {
+    float u[kBatch][V];
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q)
+      if (s0 + q < a.gh_splits) ldv<V>(LOpnd{a.ghws, 0, 0, TOFU_F32}, wo + (s0 + q) * a.gh_plane, u[q]);
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q)
+      if (s0 + q < a.gh_splits)
+#pragma unroll
+        for (int j = 0; j < V; ++j) t[j] = (s0 + q == 0) ? u[q][j] : t[j] + u[q][j];
+  }
+  stv<V>(a.gh_out, a.gh_out_dt, b * a.gh_out_ld + x * a.gh_out_gs + h, t);
+  if (a.gh_out_dt == TOFU_BF16)
+#pragma unroll
+    for (int j = 0; j < V; ++j) t[j] = __bfloat162float(__float2bfloat16_rn(t[j]));
+}
+
+template <int V, bool SPLIT = false>
 __global__ void __launch_bounds__(256) lstm_kernel(const LstmArgs a) {
   tofu::pdl_trigger();
   tofu::pdl_wait();
@@ -113,29 +149,30 @@ __global__ void __launch_bounds__(256) lstm_kernel(const LstmArgs a) {
   const int kind = a.kind;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = e / nhv, h = (e % nhv) * V;
-    const int64_t go = b * a.gx.ld + h, ho = b * a.gh.ld + h;
+    const int64_t go = b * a.gx.ld + h;
     float I[V], F[V], G[V], O[V], t0[V], t1[V];
     ldv<V>(a.gx, go, t0);
-    ldv<V>(a.gh, ho, t1);
+    ld_gh<V, SPLIT>(a, b, h, 0, t1);
 #pragma unroll
     for (int j = 0; j < V; ++j) I[j] = sig(t0[j] + t1[j]);
     ldv<V>(a.gx, go + a.gx.gs, t0);
-    ldv<V>(a.gh, ho + a.gh.gs, t1);
+    ld_gh<V, SPLIT>(a, b, h, 1, t1);
 #pragma unroll
     for (int j = 0; j < V; ++j) F[j] = sig(t0[j] + t1[j]);
     ldv<V>(a.gx, go + 2 * a.gx.gs, t0);
-    ldv<V>(a.gh, ho + 2 * a.gh.gs, t1);
+    ld_gh<V, SPLIT>(a, b, h, 2, t1);
 #pragma unroll
     for (int j = 0; j < V; ++j) G[j] = tanhf(t0[j] + t1[j]);
     ldv<V>(a.gx, go + 3 * a.gx.gs, t0);
-    ldv<V>(a.gh, ho + 3 * a.gh.gs, t1);
+    ld_gh<V, SPLIT>(a, b, h, 3, t1);
 #pragma unroll
     for (int j = 0; j < V; ++j) O[j] = sig(t0[j] + t1[j]);
     if (kind == 0 || kind == 4) {
       float cp[V], c[V];
       ldv<V>(a.cp, b * a.cp.ld + h, cp);
 #pragma unroll
-      for (int j = 0; j < V; ++j) c[j] = F[j] * cp[j] + I[j] * G[j];
+      // (explicit roundings, no contraction: the vector widths 1 / 4 / 8 then agree bitwise)
+      for (int j = 0; j < V; ++j) c[j] = __fadd_rn(__fmul_rn(F[j], cp[j]), __fmul_rn(I[j], G[j]));
       stv<V>(a.out, a.out_dt, b * a.out_ld + h, c);
       if (kind == 4) {
         // h_t from the c_t as stored (fp32 storage of the c tensor: identical to the unfused cell_h input)
@@ -203,11 +240,30 @@ __host__ inline bool vec8_ok(const LstmArgs& a) {
 
 }  // namespace tofu
 
+static int lstm_launch(tofu::LstmArgs& a, void* stream);
+extern "C" int tofu_lstm_cell_splitk(int kind, int64_t nb, int64_t nh, int g0, int ng, const void* const* ptrs,
+                                     const int64_t* lds, const int64_t* gss, const int* dts, void* out, int64_t out_ld,
+                                     int64_t out_gs, int out_dt, void* out2, int64_t out2_ld, int out2_dt,
+                                     const float* ghws, int gh_splits, int64_t gh_plane, int64_t gh_wld,
+                                     int64_t gh_wgs, void* stream);
+
 // Internal entry (not in the public header): operands are (ptr, ld, gs, dtype) quadruples in the slot order
 // gx, gh, cp, c, du, dr, dn; out2 is the second output of the fused kinds 4 / 5 (else NULL).
 extern "C" int tofu_lstm_cell(int kind, int64_t nb, int64_t nh, int g0, int ng, const void* const* ptrs,
                               const int64_t* lds, const int64_t* gss, const int* dts, void* out, int64_t out_ld,
                               int64_t out_gs, int out_dt, void* out2, int64_t out2_ld, int out2_dt, void* stream) {
+  return tofu_lstm_cell_splitk(kind, nb, nh, g0, ng, ptrs, lds, gss, dts, out, out_ld, out_gs, out_dt, out2, out2_ld,
+                               out2_dt, nullptr, 0, 0, 0, 0, stream);
+}
+
+// ... with GH taken from a gate GEMM's split-K partial planes (ghws: [splits][nb][.] fp32, row pitch gh_wld, gate
+// stride gh_wgs; kinds 0 / 4): the planes are summed in split order, rounded to GH's dtype, stored to the GH
+// operand's slot (ptrs[1] / lds[1] / gss[1] / dts[1] then name GH's destination) and used as stored.
+extern "C" int tofu_lstm_cell_splitk(int kind, int64_t nb, int64_t nh, int g0, int ng, const void* const* ptrs,
+                                     const int64_t* lds, const int64_t* gss, const int* dts, void* out, int64_t out_ld,
+                                     int64_t out_gs, int out_dt, void* out2, int64_t out2_ld, int out2_dt,
+                                     const float* ghws, int gh_splits, int64_t gh_plane, int64_t gh_wld,
+                                     int64_t gh_wgs, void* stream) {
   tofu::LstmArgs a{};
   a.kind = kind;
   a.nb = nb;
@@ -223,6 +279,24 @@ extern "C" int tofu_lstm_cell(int kind, int64_t nb, int64_t nh, int g0, int ng, 
   a.out2 = out2;
   a.out2_ld = out2_ld;
   a.out2_dt = out2_dt;
+  if (ghws) {
+    if ((kind != 0 && kind != 4) || gh_splits < 1 || gh_splits > 16) return TOFU_ERR_ARG;
+    a.ghws = ghws;
+    a.gh_splits = gh_splits;
+    a.gh_plane = gh_plane;
+    a.gh_wld = gh_wld;
+    a.gh_wgs = gh_wgs;
+    a.gh_out = const_cast<void*>(ptrs[1]);
+    a.gh_out_ld = lds[1];
+    a.gh_out_gs = gss[1];
+    a.gh_out_dt = dts[1];
+    a.gh = tofu::LOpnd{nullptr, 0, 0, dts[1]};
+  }
+  return lstm_launch(a, stream);
+}
+
+static int lstm_launch(tofu::LstmArgs& a, void* stream) {
+  const int64_t nb = a.nb, nh = a.nh;
   // 4 elements per thread when the operands allow 16-byte vectors: twice the threads of 8 per thread (the
   // [128 x 4096] cells launched 65536 threads, 0.86 waves at 25% occupancy: latency-bound at 1.5 TB/s);
   // TOFU_LSTM_V=8 keeps 8 (A/B switch)
@@ -230,15 +304,34 @@ extern "C" int tofu_lstm_cell(int kind, int64_t nb, int64_t nh, int g0, int ng, 
     const char* e = getenv("TOFU_LSTM_V");
     return e && e[0] == '8' ? 8 : 4;
   }();
-  const bool v8 = tofu::vec8_ok(a);
-  const int vw = v8 ? vpref : 1;
+  bool v8 = tofu::vec8_ok(a);
+  if (a.ghws) {  // the planes and GH's destination must take the same vectors
+    const bool pl = (reinterpret_cast<uintptr_t>(a.ghws) % 16) == 0 && a.gh_plane % 4 == 0 && a.gh_wld % 4 == 0 &&
+                    a.gh_wgs % 4 == 0;
+    const int64_t al = a.gh_out_dt == TOFU_BF16 ? 8 : 4;
+    const bool go = (reinterpret_cast<uintptr_t>(a.gh_out) % 16) == 0 && a.gh_out_ld % al == 0 && a.gh_out_gs % al == 0;
+    v8 = v8 && pl && go;
+  }
+  // (the gate GEMM + cell fusion sums 4 gates x splits fp32 planes per element: more, narrower threads;
+  // TOFU_LSTM_SPLIT_V overrides the vector width of that variant, A/B)
+  static const int vsplit = [] {
+    const char* e = getenv("TOFU_LSTM_SPLIT_V");
+    return e ? atoi(e) : 1;  // (measured: 7.6 us vs 9.0 us with 4 per thread)
+  }();
+  const int vw = !v8 ? 1 : a.ghws ? (vsplit == 1 || vsplit == 4 || vsplit == 8 ? vsplit : 4) : vpref;
   const int64_t n = nb * (nh / vw);
   if (n == 0) return TOFU_OK;
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (vw == 8) tofu::launch_k(tofu::lstm_kernel<8>, dim3((unsigned)blocks), dim3(256), 0, st, 1, a);
+  if (a.ghws) {  // gate GEMM + cell fusion: the split-K planes are summed here
+    if (vw == 8) tofu::launch_k(tofu::lstm_kernel<8, true>, dim3((unsigned)blocks), dim3(256), 0, st, 1, a);
+    else if (vw == 4) tofu::launch_k(tofu::lstm_kernel<4, true>, dim3((unsigned)blocks), dim3(256), 0, st, 1, a);
+    else tofu::launch_k(tofu::lstm_kernel<1, true>, dim3((unsigned)blocks), dim3(256), 0, st, 1, a);
+  } else if (vw == 8) tofu::launch_k(tofu::lstm_kernel<8>, dim3((unsigned)blocks), dim3(256), 0, st, 1, a);
   else if (vw == 4) tofu::launch_k(tofu::lstm_kernel<4>, dim3((unsigned)blocks), dim3(256), 0, st, 1, a);
   else tofu::launch_k(tofu::lstm_kernel<1>, dim3((unsigned)blocks), dim3(256), 0, st, 1, a);
-  return cudaGetLastError() == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && getenv("TOFU_DEBUG")) fprintf(stderr, "lstm cell launch: %s\n", cudaGetErrorString(e));
+  return e == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
 }

@@ -29,6 +29,11 @@ extern "C" int tofu_spin(int64_t ns, void* stream);
 extern "C" int tofu_lstm_cell(int kind, int64_t nb, int64_t nh, int g0, int ng, const void* const* ptrs,
                               const int64_t* lds, const int64_t* gss, const int* dts, void* out, int64_t out_ld,
                               int64_t out_gs, int out_dt, void* out2, int64_t out2_ld, int out2_dt, void* stream);
+extern "C" int tofu_lstm_cell_splitk(int kind, int64_t nb, int64_t nh, int g0, int ng, const void* const* ptrs,
+                                     const int64_t* lds, const int64_t* gss, const int* dts, void* out, int64_t out_ld,
+                                     int64_t out_gs, int out_dt, void* out2, int64_t out2_ld, int out2_dt,
+                                     const float* ghws, int gh_splits, int64_t gh_plane, int64_t gh_wld,
+                                     int64_t gh_wgs, void* stream);
 
 namespace tofu {
 
@@ -108,6 +113,8 @@ struct LOp {
   int fused_opt = -1;         // GEMM epilogue absorbs mom (this index) + sgd (index + 1)
   int64_t wt_off = -1;        // conv data gradient: arena offset of the transposed weight shard (K-major B)
   bool fused_next = false;    // LSTM cell: this launch also computes the next op (c+h, bwd_a+bwd_c)
+  int cell_after = -1;        // gate GEMM: this launch also runs that (fused c+h) cell op, which reduces the
+                              // GEMM's split-K partials itself (one kernel for reduction + cell)
   bool fused_loss_grad = false;  // sumsq: this launch also computes the next op, mse_grad of the same inputs
   int ep = 0;                 // element-wise epilogue of the output's consumers: 1 relu, 2 add, 4 mask
   int red_ep = 0;             // the reduce pieces apply the output's consumer (TOFU_PIECE_*)
@@ -288,6 +295,7 @@ struct Exec {
   // ranks of one B200 (WResNet-152-4, tools/kineto_step.py) 94.7 -> 97.5 ms per step although 171 of 425
   // staged fetch launches disappear: the fused-fetch fp32-partial GEMMs run 28 -> 41 us each
   bool fuse_fetch_conv = false;
+  bool fuse_gate_cell = false;  // gate GEMM + LSTM cell in one launch (TOFU_FUSE_GATE_CELL=1; see the fusion pass)
   struct OpAcc {  // objects (tensor alias roots; staging buffers nt, nt + 1) an op's launches touch, all ranks
     bool any_fetch = false, any_reduce = false, fetch_remote = false;
     int stage = -1;
@@ -503,6 +511,7 @@ void read_env_options(Exec& E) {
   if (const char* f = std::getenv("TOFU_STREAMS")) E.streams = std::atoi(f) >= 2 ? 2 : 1;
   if (const char* f = std::getenv("TOFU_PFETCH")) E.fuse_fetch = std::string(f) != "0";
   if (const char* f = std::getenv("TOFU_PFETCH_CONV")) E.fuse_fetch_conv = std::string(f) == "1";
+  if (const char* f = std::getenv("TOFU_FUSE_GATE_CELL")) E.fuse_gate_cell = std::string(f) == "1";
 }
 
 void lower(Exec& E) {
@@ -887,6 +896,38 @@ void lower(Exec& E) {
         La.fused_next = true;
         La.absorbed.push_back((int)o + 1);
         Lb.skip = true;
+      }
+  // LSTM forward: the gate GEMM of step t (GH_t = h_{t-1} Wh) and the fused cell pair reading GH_t (c_t, h_t):
+  // one launch — when the GEMM splits K, the cell kernel sums the fp32 partial planes itself (in split order,
+  // rounding GH to its dtype, storing GH and using it as stored), so the split-K reduction launch and the
+  // cell launch become one kernel.  Off by default (TOFU_FUSE_GATE_CELL=1 turns it on): measured on 8 virtual
+  // ranks (LSTM-6-4K, tools/kineto_step.py) the fused kernel (7.6 us with one element per thread, 9.0 us with
+  // four) costs what the reduction (2.7 us) and the cell (5.6 us) cost apart: 49.0 vs 49.0 ms per step.
+  if (E.fuse && E.fuse_gate_cell)
+    for (int r = 0; r < k; ++r)
+      for (size_t o = 0; o + 2 < g.ops.size(); ++o) {
+        const OpDef& dg = g.defs[g.ops[o].def];
+        if (!kernel_kind(dg) || std::string(kernel_kind(dg)) != "gemm" || g.defs[g.ops[o + 1].def].kernel != "cell_c")
+          continue;
+        LOp &La = all[r][o], &Lc = all[r][o + 1];
+        if (La.skip || Lc.skip || !Lc.fused_next || !La.out.direct || La.partial || La.fused_opt >= 0 || La.ep ||
+            La.red_ep || !La.reduce.empty() || La.out.dtype != TOFU_BF16 || La.out.box.size() != 3 ||
+            !same(La.out.box, La.out.buf_box) || !Lc.fetch.empty() || !Lc.reduce.empty() ||
+            g.ops[o + 1].inputs.size() < 2 || g.ops[o + 1].inputs[1] != g.ops[o].output)
+          continue;
+        bool ok = Lc.in.size() >= 3 && Lc.out.direct;
+        for (auto& b : Lc.in) ok &= b.direct;
+        const Buf& G = Lc.in[1];
+        ok = ok && G.off == La.out.off && same(G.buf_box, La.out.buf_box) && G.box.size() == 3 &&
+             G.box[0].lo == La.out.box[0].lo && G.box[0].hi == La.out.box[0].hi && G.box[2].lo == La.out.box[2].lo &&
+             G.box[2].hi == La.out.box[2].hi && La.out.box[1].lo == 0 && Lc.out.box.size() == 2 &&
+             Lc.out.box[0].len() == La.out.box[0].len() &&  // (c rows: the merged timestep storage's coordinates)
+             Lc.out.box[1].lo == La.out.box[2].lo && Lc.out.box[1].hi == La.out.box[2].hi;
+        if (!ok) continue;
+        La.cell_after = (int)o + 1;
+        La.absorbed.push_back((int)o + 1);
+        La.absorbed.push_back((int)o + 2);
+        Lc.skip = true;
       }
   // The loss and its gradient read the same (Y, T) shards: one pass computes both (sumsq + mse_grad, R8)
   if (E.fuse)
@@ -1927,7 +1968,12 @@ int64_t kernels_of(const Exec& E, int o, int li) {
   auto gemm_k = [](const tofu_gemm_args& a) -> int64_t {
     return a.M == 0 || a.N == 0 || a.K == 0 ? 0 : 1 + (a.splits > 1 ? 1 : 0);
   };
-  if (kind == "gemm") return gemm_k(E.gemms.at({o, li}).a);
+  if (kind == "gemm") {
+    const auto& a = E.gemms.at({o, li}).a;
+    // gate GEMM + cell: the cell kernel replaces the split-K reduction (or follows the unsplit GEMM)
+    if (E.lops[li][o].cell_after >= 0) return a.M == 0 || a.N == 0 || a.K == 0 ? 1 : 2;
+    return gemm_k(a);
+  }
   if (kind == "conv") {
     auto git = E.gemms.find({o, li});
     if (git != E.gemms.end()) return gemm_k(git->second.a);
@@ -1944,36 +1990,16 @@ int64_t kernels_of(const Exec& E, int o, int li) {
   return 1;
 }
 
-int run_compute(Exec& E, int o, int li, cudaStream_t st) {
+// LSTM cell launch of op o (fused kinds included); gs: the gate GEMM whose split-K partial planes hold GH (the
+// gate GEMM + cell fusion, LOp::cell_after), else NULL.
+int run_lstm(Exec& E, int o, int li, cudaStream_t st, const tofu_gemm_args* gs) {
   const Graph& g = *E.g;
   const int r = E.local[li];
   LOp& L = E.lops[li][o];
   const OpInfo& oi = g.ops[o];
   const std::string& dn = g.defs[oi.def].kernel;
-  const OpDef& d = g.defs[oi.def];
   char* base = E.arena[r];
-  const std::string kind = kernel_kind(d);
-  if (kind == "gemm") {
-    auto& G = E.gemms.at({o, li});
-    return tofu_gemm_launch_planned(&G.a, G.tm, G.bn, st);
-  }
-  if (kind == "conv") {
-    auto git = E.gemms.find({o, li});
-    if (git != E.gemms.end()) return tofu_gemm_launch_planned(&git->second.a, git->second.tm, git->second.bn, st);
-    if (L.wt_off >= 0) {  // refresh the transposed weight shard (the weights may have been updated since)
-      const Buf& W = L.in[1];
-      const int rc = tofu_transpose_taps(base + W.off, base + L.wt_off, (int)W.buf_box[0].len(),
-                                         (int)(W.buf_box[1].len() * W.buf_box[2].len()), (int)W.buf_box[3].len(), st);
-      if (rc) return rc;
-    }
-    for (auto& C : E.convs.at({o, li})) {
-      const int rc = tofu_conv_launch_planned(&C.a, C.tm, st);
-      if (rc) return rc;
-    }
-    return TOFU_OK;
-  }
-  if (kind == "window") return run_window(E, o, li, st);
-  if (kind == "lstm") {
+  {
     // operand slots of the cell kernel: gx, gh, cp, c, du, dr, dn
     static const std::map<std::string, std::vector<int>> slots = {
         {"cell_c", {0, 1, 2}}, {"cell_h", {0, 1, 3}}, {"cell_bwd_a", {0, 1, 2, 3, 4, 5, 6}},
@@ -2012,10 +2038,63 @@ int run_compute(Exec& E, int o, int li, cudaStream_t st) {
       out2_dt = nb2.dtype;
       kind_id = kind_id == 0 ? 4 : 5;
     }
+    if (gs) {  // GH from the gate GEMM's split-K planes ([splits][M][N] dense; N = gates x h of GH's box)
+      // (the GEMM wrote GH's whole box, = its buffer: gate stride in a plane = the buffer's h extent; the
+      // cell op's own GH box may name fewer gates, e.g. cell_c reads i, f, g)
+      const int64_t M = gs->M, N = gs->N, wgs = L.in[1].buf_box[2].len();
+      if (L.in[1].buf_box.size() != 3 || N != L.in[1].buf_box[1].len() * wgs || M != nb || nh > wgs)
+        return TOFU_ERR_ARG;  // (the fusion pass admits only GEMMs whose output box is GH's buffer)
+      return tofu_lstm_cell_splitk(kind_id, nb, nh, g0, ng, ptrs, lds, gss, dts,
+                                   base + ob.off + offset_in(ob.buf_box, ob.box) * oes, ost[0],
+                                   ob.box.size() == 3 ? ost[1] : 0, ob.dtype, out2, out2_ld, out2_dt,
+                                   reinterpret_cast<const float*>(gs->ws), gs->splits, M * N, N, wgs, st);
+    }
     return tofu_lstm_cell(kind_id, nb, nh, g0, ng, ptrs, lds, gss, dts,
                           base + ob.off + offset_in(ob.buf_box, ob.box) * oes, ost[0],
                           ob.box.size() == 3 ? ost[1] : 0, ob.dtype, out2, out2_ld, out2_dt, st);
+    }
+}
+
+int run_compute(Exec& E, int o, int li, cudaStream_t st) {
+  const Graph& g = *E.g;
+  const int r = E.local[li];
+  LOp& L = E.lops[li][o];
+  const OpInfo& oi = g.ops[o];
+  const std::string& dn = g.defs[oi.def].kernel;
+  const OpDef& d = g.defs[oi.def];
+  char* base = E.arena[r];
+  const std::string kind = kernel_kind(d);
+  if (kind == "gemm") {
+    auto& G = E.gemms.at({o, li});
+    if (L.cell_after < 0) return tofu_gemm_launch_planned(&G.a, G.tm, G.bn, st);
+    // gate GEMM + cell: the partial planes stay in the workspace and the cell kernel reduces them
+    tofu_gemm_args a = G.a;
+    const bool split = a.splits > 1;
+    a.defer_reduce = split ? 1 : 0;
+    const int rc = tofu_gemm_launch_planned(&a, G.tm, G.bn, st);
+    if (rc) {
+      if (std::getenv("TOFU_DEBUG")) std::fprintf(stderr, "gate gemm: rc %d %s\n", rc, cudaGetErrorString(cudaGetLastError()));
+      return rc;
+    }
+    return run_lstm(E, L.cell_after, li, st, split ? &G.a : nullptr);
   }
+  if (kind == "conv") {
+    auto git = E.gemms.find({o, li});
+    if (git != E.gemms.end()) return tofu_gemm_launch_planned(&git->second.a, git->second.tm, git->second.bn, st);
+    if (L.wt_off >= 0) {  // refresh the transposed weight shard (the weights may have been updated since)
+      const Buf& W = L.in[1];
+      const int rc = tofu_transpose_taps(base + W.off, base + L.wt_off, (int)W.buf_box[0].len(),
+                                         (int)(W.buf_box[1].len() * W.buf_box[2].len()), (int)W.buf_box[3].len(), st);
+      if (rc) return rc;
+    }
+    for (auto& C : E.convs.at({o, li})) {
+      const int rc = tofu_conv_launch_planned(&C.a, C.tm, st);
+      if (rc) return rc;
+    }
+    return TOFU_OK;
+  }
+  if (kind == "window") return run_window(E, o, li, st);
+  if (kind == "lstm") return run_lstm(E, o, li, st, nullptr);
   const int64_t n = vol(L.out.box);
   void* y = base + L.out.off;
   const void* x0 = L.in.size() > 0 ? base + L.in[0].off : nullptr;
@@ -2323,6 +2402,7 @@ std::string launch_desc(const Exec& E, int i) {
   if (L.kind == 1 && lo_fused(E, L)) o += ",\"fused\":\"mom+sgd\"";
   if (L.kind == 1 && E.lops[L.li][L.op].fused_opt >= 0) o += ",\"fused\":\"gemm+mom+sgd\"";
   if (L.kind == 1 && E.lops[L.li][L.op].fused_next) o += ",\"fused\":\"lstm-cell-pair\"";
+  if (L.kind == 1 && E.lops[L.li][L.op].cell_after >= 0) o += ",\"fused\":\"gemm+lstm-cell\"";
   if (L.kind == 1 && E.lops[L.li][L.op].fused_loss_grad) o += ",\"fused\":\"loss+loss_grad\"";
   if (L.kind == 1 && E.lops[L.li][L.op].wt_off >= 0) o += ",\"weights\":\"transposed\"";
   if (L.kind == 1) {

@@ -98,6 +98,24 @@ def test_lstm_fused_optimizer_runs():
 
 
 @pytest.mark.parametrize("k", [1, 2])
+def test_lstm_gate_gemm_cell_fusion_equals_unfused(k, monkeypatch):
+    """The gate GEMM + cell fusion (TOFU_FUSE_GATE_CELL=1: the cell kernel sums the GEMM's split-K partial planes
+    itself, rounds GH to bf16, stores it and uses it as stored) gives exactly the results of the separate
+    reduction + cell launches, at k = 1 (no split: GEMM then cell in one launch) and k = 2."""
+    spec = lstm(2, 2048, 3, 64)   # hidden 2048: the skinny gate GEMMs split K at k = 1 and 2
+    vals = _scale_weights(make_values(spec, seed=12))
+    monkeypatch.setenv("TOFU_FUSE_GATE_CELL", "0")
+    _, a = _run(spec, k, vals)
+    monkeypatch.setenv("TOFU_FUSE_GATE_CELL", "1")
+    R, b = _run(spec, k, vals)
+    descs = [R.exec.launch_desc(i) for i in range(R.exec.num_launches())]
+    assert sum(d.get("fused") == "gemm+lstm-cell" for d in descs) >= 3 * k
+    assert any(d.get("fused") == "gemm+lstm-cell" and d.get("splits", 1) > 1 for d in descs)
+    for t in ("L1.Cs", "L1.Gh1", "L2.Hs", "L2.Gh2", "L1.dA", "L2.D0", "L1.dHs"):
+        assert np.array_equal(a[t], b[t]), t
+
+
+@pytest.mark.parametrize("k", [1, 2])
 def test_lstm_fused_cells_equal_unfused(k, monkeypatch):
     """Fused cell pairs (c+h, bwd_a+bwd_c; one pass over the gate rows) give exactly the unfused results."""
     spec = lstm(2, 64, 4, 16)
@@ -107,6 +125,7 @@ def test_lstm_fused_cells_equal_unfused(k, monkeypatch):
     monkeypatch.setenv("TOFU_FUSE", "1")
     R, b = _run(spec, k, vals)
     descs = [R.exec.launch_desc(i) for i in range(R.exec.num_launches())]
-    assert sum(d.get("fused") == "lstm-cell-pair" for d in descs) >= 8 * k
+    # (forward pairs ride in their gate GEMM's launch: "gemm+lstm-cell")
+    assert sum(d.get("fused") in ("lstm-cell-pair", "gemm+lstm-cell") for d in descs) >= 8 * k
     for t in ("L1.Cs", "L2.Hs", "L1.dA", "L2.D0", "L1.dHs"):
         assert np.array_equal(a[t], b[t]), t
