@@ -1161,10 +1161,15 @@ void lower(Exec& E) {
   // shard (W[co][ky][kx][ci] -> WT[ci][ky][kx][co], refreshed right before the launch): the MN-major weight
   // operand runs ~30% slower on the tensor cores (profiles/r01b_summary.md).  Appended after the staging
   // region (persistent, one per op).  TOFU_WT=0 disables.
+  // A weight fetched into staging (a batch-split layer's whole weight under a k-way plan) is transposed from the
+  // staging copy into one scratch region per rank shared by all such launches (each transposes right before
+  // its own convolution, on the compute stream): the 8-way WResNet data gradients otherwise ran MN-major.
   {
     const char* ev = std::getenv("TOFU_WT");
     const bool use_wt = !(ev && ev[0] == '0');
-    for (int r = 0; r < k && use_wt; ++r)
+    for (int r = 0; r < k && use_wt; ++r) {
+      std::vector<int> staged;
+      int64_t scratch = 0;
       for (size_t o = 0; o < g.ops.size(); ++o) {
         const OpDef& d = g.def_of((int)o);
         const char* kk = kernel_kind(d);
@@ -1173,14 +1178,26 @@ void lower(Exec& E) {
         LOp& L = all[r][o];
         if (cg.kind != 1 || L.skip || (cg.R == 1 && cg.s == 1)) continue;  // 1x1 stride-1: the GEMM path
         const Buf& W = L.in[1];
-        if (!W.direct || W.buf_box.size() != 4 || W.box[1].lo != W.buf_box[1].lo || W.box[1].hi != W.buf_box[1].hi ||
-            W.box[2].lo != W.buf_box[2].lo || W.box[2].hi != W.buf_box[2].hi)
+        const bool stg = !W.direct && W.rp.empty() && same(W.box, W.buf_box);
+        if ((!W.direct && !stg) || W.buf_box.size() != 4 || W.box[1].lo != W.buf_box[1].lo ||
+            W.box[1].hi != W.buf_box[1].hi || W.box[2].lo != W.buf_box[2].lo || W.box[2].hi != W.buf_box[2].hi)
           continue;
         const int64_t nch = W.box[0].len(), co_sh = W.buf_box[0].len();
         if (nch % 64 || co_sh % 8 || W.buf_box[3].len() % 8) continue;  // whole 64-channel K blocks per tap
+        if (stg) {
+          staged.push_back((int)o);
+          scratch = std::max<int64_t>(scratch, vol(W.buf_box) * 2);
+          continue;
+        }
         L.wt_off = E.lay[r].total;
         E.lay[r].total = align_up(E.lay[r].total + vol(W.buf_box) * 2);
       }
+      if (!staged.empty()) {
+        const int64_t off = E.lay[r].total;
+        E.lay[r].total = align_up(off + scratch);
+        for (int o : staged) all[r][o].wt_off = off;
+      }
+    }
   }
   E.remote_fetch.assign(g.ops.size(), 0);
   E.remote_reduce.assign(g.ops.size(), 0);

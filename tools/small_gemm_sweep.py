@@ -30,7 +30,10 @@ def bench(fn, reps=50):
     return s.elapsed_time(e) / reps * 1e3
 
 
-for name, (M, N, K, am, bm) in {"gate": (128, 2048, 4096, 0, 1), "mm_rec": (128, 4096, 2048, 0, 0)}.items():
+SHAPES = {"gate": (128, 2048, 4096, 0, 1), "mm_rec": (128, 4096, 2048, 0, 0)}
+if len(sys.argv) > 1 and sys.argv[1] == "k1":  # configs[2] at k = 1: the full recurrent GEMMs (weights 134 MB)
+    SHAPES = {"gate": (128, 16384, 4096, 0, 1), "mm_rec": (128, 4096, 16384, 0, 0)}
+for name, (M, N, K, am, bm) in SHAPES.items():
     a = torch.randn((K, M) if am else (M, K), device="cuda").bfloat16()
     b = torch.randn((K, N) if bm else (N, K), device="cuda").bfloat16()
     c = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
