@@ -349,3 +349,42 @@ def test_conv_fwd_2cta_mma(data, which):
     if which == "fwd_ep":
         r = np.where(mask > 0, np.maximum(r + add, 0.0), 0.0)
     assert nrm(outs[1], r) <= 5e-3
+
+
+@pytest.mark.parametrize("which", ["fwd", "fwd_ep", "fwd_f32", "dgrad"])
+def test_conv_fwd_dgrad_split_k(data, which):
+    """Split-K for a few-tile forward / data-gradient launch (a rank's sub-op under a k-way plan; chosen when the
+    caller passes a workspace): the fp32 partial planes summed in split order by splitk_reduce_rows, which also
+    applies the fused add / relu / mask epilogue or stores fp32 (c_mode 1).  4 of the 16 images (21 tiles): checked
+    against the oracle's fp64 evaluation of the TDL defs and the one-pass launch; deterministic."""
+    t = _tofu()
+    rng, X, W, D, ref = data
+    nb = 4
+    Xd, Wd, Dd = cuda_bf16(X[:nb]), cuda_bf16(W), cuda_bf16(D[:nb])
+    add, mask = q(rng, (nb, H, H, C), 2 ** -6), q(rng, (nb, H, H, C), 2 ** -6)
+    keep = [cuda_bf16(add), cuda_bf16(mask)]
+    ws = torch.zeros(16 * nb * H * H * C, dtype=torch.float32, device="cuda")
+    outs = []
+    for use_ws in (True, False, True):
+        f32 = which == "fwd_f32"
+        out = torch.zeros((nb, H, H, C), dtype=torch.float32 if f32 else torch.bfloat16, device="cuda")
+        a = (conv_args(t, 0, Dd, out, Wd, 1, flip=True) if which == "dgrad" else conv_args(t, 0, Xd, out, Wd, 0))
+        a.nb = nb
+        if f32:
+            a.c_mode = 1
+        if which == "fwd_ep":
+            a.ep, a.aux_add, a.aux_mask = 7, keep[0].data_ptr(), keep[1].data_ptr()
+        a.ws = ws.data_ptr() if use_ws else None
+        planned = t.conv_plan(a)
+        assert (planned.splits > 1) == use_ws, planned.splits
+        t.conv(a)
+        torch.cuda.synchronize()
+        outs.append(out.double().cpu().numpy())
+    assert np.array_equal(outs[0], outs[2])  # deterministic (split order)
+    got, plain = outs[0], outs[1]
+    r = ref["dgrad" if which == "dgrad" else "fwd"][:nb]
+    if which == "fwd_ep":
+        r = np.where(mask > 0, np.maximum(r + add, 0.0), 0.0)
+    tol = 1e-5 if which == "fwd_f32" else 5e-3
+    assert nrm(got, r) <= tol
+    assert nrm(got, plain) <= tol
