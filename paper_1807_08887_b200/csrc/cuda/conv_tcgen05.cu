@@ -1199,8 +1199,20 @@ extern "C" int tofu_conv_plan(tofu_conv_args* a, void* tmaps) {
     }();
     const int dp_tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
     a->splits = auto_splits0(a, dp_tiles, K);
+    // (pairs give up stream-K: when their last wave leaves many clusters idle, the single-CTA launch with
+    // stream-K wins in isolation — WResNet-152-4 stage-3 3x3 [6272 x 1024 x 9216], 100 pair units on 74 clusters
+    // (wave efficiency 0.68): 95.4 us paired vs 89.0 us stream-K, GRAPH=1 tools/conv_bench.py — but not in the
+    // step: 36.2 / 36.3 ms with the pairs vs 37.1 / 36.6 ms (same box, tools/kineto_step.py 3), so the rule is
+    // off unless TOFU_CONV_C2_WAVE=1)
+    const int pair_units = ((M + 2 * BM - 1) / (2 * BM)) * ((N + bn - 1) / bn), ncl = g_sms / 2;
+    const double pair_wave_eff = (double)pair_units / ((double)((pair_units + ncl - 1) / ncl) * ncl);
+    static const bool wave_rule = [] {  // TOFU_CONV_C2_WAVE=1: stream-K instead of poorly-filled pairs (A/B)
+      const char* e = getenv("TOFU_CONV_C2_WAVE");
+      return e && e[0] == '1';
+    }();
+    const bool sk_better = wave_rule && a->sk_ws && sk_enabled() && pair_wave_eff < 0.8;
     if (a->splits <= 1 && req != -1 && c2_env() != 0 && a->im2col && !a->b_mn_major && bn == 256 && M > BM &&
-        (req == 4 || c2_env() == 1 || (fwd_c2 && (c2_few || dp_tiles >= g_sms)))) {
+        (req == 4 || c2_env() == 1 || (fwd_c2 && !sk_better && (c2_few || dp_tiles >= g_sms)))) {
       if (tmap2(&tm[0], a->Bp, BF, 2, a->b_cols, a->b_rows, a->ldb, 64, bn / 2, SW128)) return TOFU_ERR_CUDA;
       a->cl2 = 3;
     }

@@ -54,11 +54,17 @@ def args(kind, S, out, Bmat=None, mn=0, flip=False):
 
 
 SKWS = torch.zeros(tofu.sk_workspace_bytes(), dtype=torch.uint8, device=dev) if os.environ.get("SK") == "1" else None
+# WS=1: a caller split-K workspace (as the executor passes; the one-shot path otherwise allocates one per call)
+WS = torch.empty(16 * 9 * C * C, dtype=torch.float32, device=dev) if os.environ.get("WS") == "1" else None
 
 
 def timeit(a, n=20):
     if SKWS is not None:  # stream-K workspace (as the executor passes): few-tile launches may spread their K loop
         a.sk_ws = SKWS.data_ptr()
+    if WS is not None:
+        a.ws = WS.data_ptr()
+    if a.kind == 1 and os.environ.get("SPLITS"):  # weight gradient: force the split count (A/B)
+        a.splits = int(os.environ["SPLITS"])
     for _ in range(3):
         tofu.conv(a)
     torch.cuda.synchronize()
@@ -95,6 +101,6 @@ for name, a in [("fwd  (B K-major)", args(0, X, Y, W, 0)),
                 ("dgrad(B MN-major)", args(0, X, Y, W, 1, flip=True)),
                 ("dgrad(B K-major, W^T)", args(0, X, Y, WT, 0, flip=True)),
                 ("dgrad(W^T) + mask epilogue", dm),
-                ] + ([] if os.environ.get("GRAPH") == "1" else [("wgrad", args(1, X, dW))]):
+                ] + ([] if os.environ.get("GRAPH") == "1" and SKWS is None and WS is None else [("wgrad", args(1, X, dW))]):
     ms = timeit(a)
     print(f"{name:24s} {ms * 1e3:8.1f} us  {flops / ms / 1e9:7.1f} TF/s")
