@@ -943,7 +943,12 @@ extern "C" int tofu_gemm_plan_tmaps(tofu_gemm_args* g, void* tmaps, int* bn_out)
     // (8-warp epilogues pair too from K = 1024: measured with the issue-lean epilogue, tools/ep_stream_bench.py,
     // [100352 x 256 x 1024] + mask 66.2 -> 60.7 us, [6272 x 4096 x 1024] + add + mask 60.8 -> 54.8 us; shorter K
     // loses: K = 512 74.4 -> 78.7 us, K = 256 112 -> 137 us)
-    const bool c2 = ok && (req == 4 || (req == 0 && env2 != 0 && (env2 == 1 || c2w8 || !wants_w8(g) || g->K >= 1024)));
+    static const int c2w8_k = [] {  // TOFU_C2W8_K: smallest K at which 8-warp epilogues pair (A/B)
+      const char* e = getenv("TOFU_C2W8_K");
+      return e ? atoi(e) : 1024;
+    }();
+    const bool c2 =
+        ok && (req == 4 || (req == 0 && env2 != 0 && (env2 == 1 || c2w8 || !wants_w8(g) || g->K >= c2w8_k)));
     g->cl2 = c2 ? 3 : ok && (env == 1 || req == 2 || cl2_auto(g)) ? 1 : 0;
   }
   CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(tmaps);
