@@ -71,10 +71,23 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// TOFU_MBAR_HINT (compile time, ns): suspend-time hint of the potentially-blocking try_wait (0 = none)
+#ifndef TOFU_MBAR_HINT
+#define TOFU_MBAR_HINT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   uint32_t done = 0;
   const uint32_t a = smem_u32(bar);
   do {
+#if TOFU_MBAR_HINT > 0
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(phase), "n"(TOFU_MBAR_HINT)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -82,6 +95,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         : "=r"(done)
         : "r"(a), "r"(phase)
         : "memory");
+#endif
   } while (!done);
 }
 

@@ -50,6 +50,21 @@ for ev in kern:
     agg[name][1] += d
     iv.append((ev.time_range.start, ev.time_range.end))
 iv.sort()
+# per-step spans and the idle gaps between consecutive steps (kernels in launch order; a step = its share)
+per = len(iv) // steps if steps else 0
+if per:
+    starts = [iv[i * per][0] for i in range(steps)]
+    ends = [max(b for _, b in iv[i * per:(i + 1) * per]) for i in range(steps)]
+    gaps = [(starts[i + 1] - ends[i]) for i in range(steps - 1)]
+    print("per-step spans (ms):", [round((ends[i] - starts[i]) / 1e3, 3) for i in range(steps)],
+          "gaps between steps (us):", [round(g, 1) for g in gaps])
+s2, e2 = torch.cuda.Event(True), torch.cuda.Event(True)
+s2.record()
+for _ in range(steps):
+    R.step()
+e2.record()
+torch.cuda.synchronize()
+print(f"events after profiling: {s2.elapsed_time(e2) / steps:.3f} ms/step")
 busy, cur_s, cur_e = 0.0, None, None
 for a, b in iv:
     if cur_e is None or a > cur_e:
