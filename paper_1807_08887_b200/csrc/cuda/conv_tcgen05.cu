@@ -1200,7 +1200,7 @@ extern "C" int tofu_conv_plan(tofu_conv_args* a, void* tmaps) {
     const int dp_tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
     a->splits = auto_splits0(a, dp_tiles, K);
     // (pairs give up stream-K: when their last wave leaves many clusters idle, the single-CTA launch with
-    // stream-K wins in isolation — WResNet-152-4 stage-3 3x3 [6272 x 1024 x 9216], 100 pair units on 74 clusters
+    // stream-K wins in isolation — WResNet-152-4 stage-2 (14 x 14) 3x3 [6272 x 1024 x 9216], 100 pair units on 74 clusters
     // (wave efficiency 0.68): 95.4 us paired vs 89.0 us stream-K, GRAPH=1 tools/conv_bench.py — but not in the
     // step: 36.2 / 36.3 ms with the pairs vs 37.1 / 36.6 ms (same box, tools/kineto_step.py 3), so the rule is
     // off unless TOFU_CONV_C2_WAVE=1)
