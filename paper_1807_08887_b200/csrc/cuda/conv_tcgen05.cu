@@ -494,20 +494,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               if (a.ep & 1)
 #pragma unroll
                 for (int e = 0; e < 8; ++e) f[e] = fmaxf(f[e], 0.f);
-              if (a.ep & 4) {
-                const uint4 u = xm[v];
-                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const float2 x = __bfloat1622float2(h[e]);
-                  if (!(x.x > 0.f)) f[2 * e] = 0.f;
-                  if (!(x.y > 0.f)) f[2 * e + 1] = 0.f;
-                }
-              }
               uint4 w;
               __nv_bfloat162* wh = reinterpret_cast<__nv_bfloat162*>(&w);
 #pragma unroll
               for (int e = 0; e < 4; ++e) wh[e] = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+              if (a.ep & 4) {  // relu-gradient mask on the packed result (as the GEMM epilogue): keep where mask > 0
+                const __nv_bfloat162* mh = reinterpret_cast<const __nv_bfloat162*>(&xm[v]);
+                const __nv_bfloat162 z = __float2bfloat162_rn(0.f);
+                w.x &= __hgt2_mask(mh[0], z);
+                w.y &= __hgt2_mask(mh[1], z);
+                w.z &= __hgt2_mask(mh[2], z);
+                w.w &= __hgt2_mask(mh[3], z);
+              }
               reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(rowp) + n)[v] = w;
             }
 #pragma unroll
