@@ -288,7 +288,9 @@ struct Exec {
   uint64_t jitter = 0;    // TOFU_JITTER: seed + 1 of the injected delays (0 = off)
   uint64_t jitter_step = 0;
   bool multi_process = false;
-  int streams = 1;         // virtual ranks: 1 (default) or 2 (TOFU_STREAMS=2); multi-process always 2
+  // virtual ranks: 2 (default; same-box A/B, programmatic launch on: WResNet-152-4 k = 8 87.67 -> 86.89 ms, LSTM
+  // and FC even) or 1 (TOFU_STREAMS=1); multi-process always 2
+  int streams = 2;
   bool fuse = true;
   bool fuse_fetch = true;  // GEMM operands read in place from their owners' shards (TOFU_PFETCH=0: staged)
   // ... also 1x1 stride-1 convolutions' operands (TOFU_PFETCH_CONV=1).  Off by default: measured on 8 virtual

@@ -39,7 +39,27 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(steps):
         R.step()
     torch.cuda.synchronize()
+if os.environ.get("TRACE"):  # chrome trace of the profiled steps (streams as rows)
+    prof.export_chrome_trace(os.environ["TRACE"])
 evs = [ev for ev in prof.events() if ev.device_type == torch.autograd.DeviceType.CUDA and ev.name != ""]
+# comm kernels (MultiFetch / partition-n-reduce / barrier) running while a compute kernel runs: the overlap the
+# executor's second stream buys (TOFU_STREAMS=2 on virtual ranks; always two in multi-process mode)
+comm_names = ("pieces_kernel", "pieces_copy_kernel", "pieces_kernel_wide", "barrier_kernel")
+ci = sorted((e.time_range.start, e.time_range.end) for e in evs if any(c in e.name for c in comm_names))
+ki = sorted((e.time_range.start, e.time_range.end) for e in evs
+            if not any(c in e.name for c in comm_names) and "Memcpy" not in e.name and "Memset" not in e.name)
+ov, j = 0.0, 0
+for a, b in ci:
+    while j < len(ki) and ki[j][1] <= a:
+        j += 1
+    t = j
+    while t < len(ki) and ki[t][0] < b:
+        ov += max(0.0, min(b, ki[t][1]) - max(a, ki[t][0]))
+        t += 1
+ctot = sum(b - a for a, b in ci)
+if ctot:
+    print(f"comm kernels {ctot / steps / 1e3:.3f} ms/step, of which under compute kernels {ov / steps / 1e3:.3f} ms "
+          f"({100 * ov / ctot:.0f}%)")
 kern = [ev for ev in evs if "Memcpy" not in ev.name and "Memset" not in ev.name]
 agg = collections.defaultdict(lambda: [0, 0.0])
 iv = []
