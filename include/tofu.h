@@ -107,8 +107,8 @@ int tofu_exec_create(const tofu_graph* g, const tofu_plan* p, int n_local, const
 void tofu_exec_destroy(tofu_exec* e);
 /* One training step of the partitioned graph: for each op in order and each local rank: MultiFetch of
  * remote input regions (a5), sub-op (a4/a7), spread reduction / scatter of outputs to owners (a6).
- * Streams: compute launches go to `stream`; in multi-process mode (and with TOFU_STREAMS=2 on virtual ranks)
- * fetch / reduce / barrier launches go to an executor-owned comm stream, forked from `stream` at the start
+ * Streams: compute launches go to `stream`; fetch / reduce / barrier launches go to an executor-owned comm
+ * stream (always in multi-process mode; on virtual ranks by default, TOFU_STREAMS=1 keeps one stream), forked from `stream` at the start
  * and joined back at the end, each launch waiting (CUDA events) only for the launches it depends on (last
  * writer / readers of the tensors and of the two alternating staging buffers it touches).  Device barriers
  * (multi-process) are placed only before a launch that would otherwise race with a peer: reading peer memory
