@@ -2359,6 +2359,10 @@ std::string launch_desc(const Exec& E, int i) {
     o += ",\"pieces\":" + std::to_string(L.npieces) + ",\"tasks\":" + std::to_string(L.ntasks) +
          ",\"row_bytes\":" + json_num(rows > 0 ? row_bytes / rows : 0) +
          ",\"vec\":" + json_num(elems > 0 ? vec / elems : 0);
+    int maxsrc = 0;
+    for (int64_t p = L.piece_off; p < L.piece_off + L.npieces; ++p) maxsrc = std::max(maxsrc, E.host_pieces[p].nsrc);
+    o += ",\"max_src\":" + std::to_string(maxsrc) + ",\"piece_kernel\":\"" +
+         (L.all_raw == 1 ? "copy" : L.all_raw == 2 ? "many_source" : "general") + "\"";
   } else if (L.kind == 1) {
     const LOp& lo = E.lops[L.li][L.op];
     const std::string& dn = g.defs[g.ops[L.op].def].name;
@@ -2423,7 +2427,10 @@ std::string launch_desc(const Exec& E, int i) {
   if (L.kind == 1 && E.lops[L.li][L.op].fused_next) o += ",\"fused\":\"lstm-cell-pair\"";
   if (L.kind == 1 && E.lops[L.li][L.op].cell_after >= 0) o += ",\"fused\":\"gemm+lstm-cell\"";
   if (L.kind == 1 && E.lops[L.li][L.op].fused_loss_grad) o += ",\"fused\":\"loss+loss_grad\"";
-  if (L.kind == 1 && E.lops[L.li][L.op].wt_off >= 0) o += ",\"weights\":\"transposed\"";
+  if (L.kind == 1 && E.lops[L.li][L.op].wt_off >= 0) {
+    o += ",\"weights\":\"transposed\"";
+    if (!E.lops[L.li][L.op].in[1].direct) o += ",\"weights_from\":\"staging\"";  // (fetched; shared scratch)
+  }
   if (L.kind == 1) {
     int np = 0;
     for (auto& b : E.lops[L.li][L.op].in) np += !b.rp.empty();

@@ -420,3 +420,62 @@ def test_memory_planner_layout(tofu, which, monkeypatch):
                     assert la[1] < lb[0] or lb[1] < la[0], (ta, la, tb, lb)
     ex = tofu.Exec(g, plan, list(range(4)), [0x100000000 * (r + 1) for r in range(4)])
     assert ex.ledger() == plan.cost()
+
+
+def test_many_source_reduce_kernel_is_chosen_from_four_sources(tofu):
+    """Partition-n-reduce launches with >= 4 sources run the many-source piece kernel (every source's vector in
+    flight at once, tofu_pieces_run all_raw = 2), fewer sources the general one, plain copies the copy kernel."""
+    ex = _exec(tofu, config(1), k=8)
+    seen = set()
+    for i in range(ex.num_launches()):
+        d = ex.launch_desc(i)
+        if d["kind"] not in ("fetch", "reduce"):
+            continue
+        want = "many_source" if d["max_src"] >= 4 else None
+        if want:
+            assert d["piece_kernel"] == want, d
+        else:
+            assert d["piece_kernel"] in ("copy", "general"), d
+        seen.add(d["piece_kernel"])
+    assert "many_source" in seen
+
+
+def test_staged_conv_weights_are_transposed_for_the_data_gradient(tofu, monkeypatch):
+    """Every 3x3 convolution data gradient reads its weight K-major: owned weights from a per-op transposed
+    copy, weights fetched into staging (batch-split layers under a k-way plan) from one per-rank scratch the
+    launch transposes into (exec.cpp; the arena grows by the scratch only).  TOFU_WT=0: none transposed."""
+    from tofu_inputs.graphs import wresnet
+    spec = wresnet([2, 1], 2, 8, 64, base=32, classes=24)
+    counts = {}
+    for wt in ("1", "0"):
+        monkeypatch.setenv("TOFU_WT", wt)
+        ex = _exec(tofu, spec, k=8)
+        descs = [ex.launch_desc(i) for i in range(ex.num_launches())]
+        dg = [d for d in descs if d["kind"] == "compute" and d["def"].startswith("dconv_k3")]
+        counts[wt] = (len(dg), sum(d.get("weights") == "transposed" for d in dg),
+                      sum(d.get("weights_from") == "staging" for d in dg))
+        assert ex.ledger() == tuple(tofu.Plan(tofu.Graph(spec), 8).cost())
+    assert counts["1"][0] > 0 and counts["1"][1] == counts["1"][0]
+    assert counts["1"][2] > 0                                # some of them from staging
+    assert counts["0"][1] == 0
+
+
+def test_gate_gemm_cell_fusion_lowering(tofu, monkeypatch):
+    """TOFU_FUSE_GATE_CELL=1: every forward gate GEMM whose output GH_t feeds the fused cell pair of step t
+    carries the pair in its launch (desc "gemm+lstm-cell"; the cell ops launch nothing), the ledger still equals
+    the plan; off by default."""
+    from tofu_inputs.graphs import lstm
+    spec = lstm(2, 512, 3, 64)
+    got = {}
+    for v in ("0", "1"):
+        monkeypatch.setenv("TOFU_FUSE_GATE_CELL", v)
+        for k in (1, 2):
+            ex = _exec(tofu, spec, k=k)
+            descs = [ex.launch_desc(i) for i in range(ex.num_launches())]
+            got[(v, k)] = (sum(d.get("fused") == "gemm+lstm-cell" for d in descs),
+                           sum(d["kind"] == "compute" and d["def"] == "cell_c" for d in descs))
+            assert ex.ledger() == tuple(tofu.Plan(tofu.Graph(spec), k).cost())
+    for k in (1, 2):
+        assert got[("0", k)][0] == 0
+        assert got[("1", k)][0] == 2 * 3 * k                 # layers x steps x ranks
+        assert got[("1", k)][1] == got[("0", k)][1] - 2 * 3 * k  # those cell launches are gone
