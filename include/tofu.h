@@ -232,6 +232,10 @@ typedef struct {
    * ordered reduction: the caller's next launch reduces them (the executor's gate GEMM + LSTM cell fusion).
    * 0 = C holds the result when the call returns (stream order). */
   int defer_reduce;
+  /* 1 = every CTA walks its k-blocks from the last to the first (the same sums in reverse order): the executor
+   * alternates it launch by launch over the same weight so that a pass starts on the rows the previous pass
+   * read last, still in L2.  0 = ascending. */
+  int k_reverse;
 } tofu_gemm_args;
 int tofu_gemm_bf16(const tofu_gemm_args* args, void* stream);
 /* Split form used by the executor: encode the TMA descriptors (A, B, C, D, workspace, mask, then the

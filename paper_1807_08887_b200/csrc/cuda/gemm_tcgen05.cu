@@ -157,7 +157,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
   const int nk = (K + BK - 1) / BK;
   // segments = (output tile, k-block range): data-parallel units (tile, K split) then stream-K pieces
   WorkList wl;
-  wl.raster = raster;
+  wl.raster = raster & 1;
+  // bit 1: walk each segment's k-blocks from the last to the first (alternated launch by launch over the same
+  // weight by the executor: the tail of the previous pass is still in L2 when the next pass starts)
+  const bool krev = (raster & 2) != 0;
   wl.tiles_m = tiles_m;
   wl.tiles_n = tiles_n;
   uint32_t crank = 0;
@@ -217,7 +220,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
         wl.seg(i, tile, kb0, kb1, sp, part);
         const int m0 = (tile / tiles_n) * BM;
         const int n0 = (tile % tiles_n) * BN;
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        for (int ki = 0; ki < kb1 - kb0; ++ki, ++it) {
+          const int kb = krev ? kb1 - 1 - ki : kb0 + ki;
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
@@ -297,7 +301,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
 #ifdef TOFU_EXP_NOMAIN
         kb1 = kb0;
 #endif
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        for (int ki = 0; ki < kb1 - kb0; ++ki, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&full[s], ph);
@@ -310,8 +314,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, MODE_>::THREADS, 1)
                                      : umma_sdesc_sw128(a0 + kk * 32, 16, 1024);
             const uint64_t bd = B_MN ? umma_sdesc_sw128(b0 + kk * 2048, 8192, 1024)
                                      : umma_sdesc_sw128(b0 + kk * 32, 16, 1024);
-            if constexpr (C2) umma_bf16_2(tmem_d, ad, bd, idesc, (kb > kb0 || kk) ? 1u : 0u);
-            else umma_bf16(tmem_d, ad, bd, idesc, (kb > kb0 || kk) ? 1u : 0u);
+            if constexpr (C2) umma_bf16_2(tmem_d, ad, bd, idesc, (ki > 0 || kk) ? 1u : 0u);
+            else umma_bf16(tmem_d, ad, bd, idesc, (ki > 0 || kk) ? 1u : 0u);
           }
           if constexpr (C2) umma_commit2_mc(&empty[s], 0x3);     // frees stage s in both CTAs
           else if constexpr (CL2) umma_commit_mc(&empty[s], 0x3);  // both CTAs' stage s: this CTA has read it
@@ -671,12 +675,12 @@ static int launch_t(const tofu_gemm_args* g, const CUtensorMap* tm, const PieceM
     const int ncl = pair_units < g_num_sms / 2 ? pair_units : g_num_sms / 2;
     const cudaError_t e = launch_k(kern, dim3(2 * ncl), dim3(Cfg::THREADS), Cfg::SMEM, st, 2, pp, tm[0], tm[1], tm[2],
                                    tm[3], tm[5], g->M, g->N, g->K, g->s0, g->s1, 1, g->ep, 0, g->sk_ws,
-                                   raster_of(g));
+                                   raster_of(g) | (g->k_reverse ? 2 : 0));
     return e == cudaSuccess ? TOFU_OK : TOFU_ERR_CUDA;
   }
   return launch_k(kern, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, st, 1, pp, tm[0], tm[1], tm[2], tm[3], tm[5], g->M,
                   g->N, g->K, g->s0, g->s1, splits, g->ep, sk, g->sk_ws,
-                  splits == 1 && sk == 0 ? raster_of(g) : 0) == cudaSuccess
+                  (splits == 1 && sk == 0 ? raster_of(g) : 0) | (g->k_reverse ? 2 : 0)) == cudaSuccess
              ? TOFU_OK
              : TOFU_ERR_CUDA;
 }

@@ -1584,8 +1584,30 @@ void finalize(Exec& E) {
   }
   // GEMM descriptors (pass 0 sizes the shared split-K workspace with a placeholder address, pass 1 encodes
   // the real descriptors)
+  // k-block order alternated launch by launch over the same weight tensor (per rank, op order): a pass then
+  // starts on the rows the previous pass read last, still in L2 — the LSTM's per-timestep recurrent GEMMs each
+  // stream their whole Wh (134 MB at configs[2], L2 126 MB).  Keyed by the B operand's tensor (alias root), so
+  // fused / staged fetch and one / two streams take the same orders (bitwise-equal tests).  TOFU_KREV=0: off.
+  static const bool krev_on = [] {
+    const char* e = std::getenv("TOFU_KREV");
+    return !(e && e[0] == '0');
+  }();
+  std::map<int, int> alias_up(g.alias.begin(), g.alias.end());
+  auto troot = [&](int t) {
+    while (alias_up.count(t)) t = alias_up[t];
+    return t;
+  };
   for (int pass = 0; pass < 2; ++pass) {
   int64_t ws_need = 0;
+  std::map<std::pair<int, int>, int> kdir;  // (local rank, B tensor root) -> the last launch's order
+  auto next_dir = [&](int li, int t) {
+    if (!krev_on) return 0;
+    const auto key = std::make_pair(li, troot(t));
+    const auto it = kdir.find(key);
+    const int d = it == kdir.end() ? 0 : 1 - it->second;
+    kdir[key] = d;
+    return d;
+  };
   for (int li = 0; li < nl; ++li) {
     const int r = E.local[li];
     for (size_t o = 0; o < g.ops.size(); ++o) {
@@ -1652,6 +1674,7 @@ void finalize(Exec& E) {
       G.a.splits = 0;
       G.a.ws = pass == 0 ? reinterpret_cast<void*>(uintptr_t(1) << 20) : E.ws_dev;
       G.a.sk_ws = E.sk_dev;
+      G.a.k_reverse = next_dir(li, g.ops[o].inputs[gf.b_param]);
       int rc = tofu_gemm_plan_tmaps(&G.a, G.tm, &G.bn);
       if (rc) throw Error(rc, "gemm tensor map for op " + g.ops[o].name + " (pitch/alignment)");
       ws_need = std::max<int64_t>(ws_need, tofu_gemm_workspace_bytes(&G.a));

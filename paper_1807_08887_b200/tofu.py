@@ -28,7 +28,8 @@ class GemmArgs(C.Structure):
                 ("bn", C.c_int), ("max_ctas", C.c_int), ("D", C.c_void_p), ("ldd", C.c_int),
                 ("s0", C.c_float), ("s1", C.c_float), ("splits", C.c_int), ("ws", C.c_void_p),
                 ("aux_add", C.c_void_p), ("aux_mask", C.c_void_p), ("ep", C.c_int), ("sk_ws", C.c_void_p),
-                ("a_pieces", C.c_void_p), ("b_pieces", C.c_void_p), ("cl2", C.c_int), ("defer_reduce", C.c_int)]
+                ("a_pieces", C.c_void_p), ("b_pieces", C.c_void_p), ("cl2", C.c_int), ("defer_reduce", C.c_int),
+                ("k_reverse", C.c_int)]
 
 
 MAX_PIECES = 8
